@@ -1,0 +1,230 @@
+"""Generate the golden fixtures in tests/golden/ from the REAL reference.
+
+Run in the build container (the only place /root/reference exists):
+
+    PYTHONPATH=/root/reference/pkg/src:/root/repo python tests/golden/make_golden.py
+
+Every fixture is produced by calling the reference package `xsvd`
+(/root/reference/pkg/src/xsvd) through its own public functions:
+gaussian_band / uniform_bits (rng.py), block_multiply / thin_qr /
+svd_small (kernels.py), randomized_svd (pipeline.py), and the
+"xsvd-reorth" composition of those primitives. Inputs are
+regenerated from the seeds stored beside them, so the fixtures stay small.
+The oracle (oracle/) is pinned against these files by
+tests/test_oracle_golden.py; the GPU parity tests use them too.
+"""
+
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+
+import xsvd  # noqa: E402
+from xsvd import (  # noqa: E402
+    BlockPartition, BlockPool, Density, DenseBlock, MatrixDescriptor, Precision,
+    RsvdConfig, SparseBlock, StoredMatrix, block_multiply, randomized_svd, svd_small, thin_qr,
+)
+from xsvd.pool import matrix_from_coo, matrix_from_dense  # noqa: E402
+from xsvd.rng import gaussian_band, uniform_bits  # noqa: E402
+
+from paper_1907_06470_b200.workloads import CONFIGS, dense_lowrank_np  # noqa: E402
+
+PREC = {"double": Precision.DOUBLE, "single": Precision.SINGLE}
+
+
+def save(name, **arrays):
+    path = os.path.join(HERE, name + ".npz")
+    np.savez_compressed(path, **arrays)
+    print(f"wrote {path} ({os.path.getsize(path)} B)")
+
+
+def dense(pool, mid, arr, precision=Precision.DOUBLE):
+    return matrix_from_dense(pool, mid, arr, precision=precision)
+
+
+def gen_rng():
+    out = {}
+    cases = [(0, 0, 16, 30), (7, 0, 33, 25), (3, 5, 21, 120), (11, 2**32 - 3, 2**32 + 4, 9),
+             (2, 0, 8, 550), (123456789, 1000, 1010, 1)]
+    for i, (seed, r0, r1, n) in enumerate(cases):
+        out[f"band{i}"] = gaussian_band(seed, r0, r1, n)
+        out[f"case{i}"] = np.array([seed, r0, r1, n], dtype=np.int64)
+    out["bits"] = uniform_bits(42, 3, 1000)
+    out["bits_case"] = np.array([42, 3, 1000], dtype=np.int64)
+    save("rng", **out)
+
+
+def gen_multiply():
+    rng = np.random.default_rng(0)
+    out = {}
+    x = rng.standard_normal((300, 520))
+    y = rng.standard_normal((520, 30))
+    pool = BlockPool()
+    mx, my = dense(pool, "x", x), dense(pool, "y", y)
+    out["x"], out["y"] = x, y
+    out["nn"] = block_multiply(pool, mx, my, "nn")[0].to_array()
+    w = rng.standard_normal((300, 30))
+    out["w"] = w
+    out["tn"] = block_multiply(pool, mx.T, dense(pool, "w", w), "tn")[0].to_array()
+    # single precision: f32 compute, f32 storage
+    pool32 = BlockPool()
+    x32, y32 = x.astype(np.float32), y.astype(np.float32)
+    out["nn32"] = block_multiply(
+        pool32, dense(pool32, "x", x32, Precision.SINGLE), dense(pool32, "y", y32, Precision.SINGLE), "o"
+    )[0].to_array()
+    # sparse x dense, sparse^T x dense, dense x sparse
+    m, n = 400, 270
+    nnz = 3000
+    r = rng.integers(0, m, nnz)
+    c = rng.integers(0, n, nnz)
+    v = rng.standard_normal(nnz)
+    sp = matrix_from_coo(pool, "sp", m, n, r, c, v, precision=Precision.DOUBLE)
+    blk = pool.get("sp", 0, 0)
+    out["sp_rows"], out["sp_cols"], out["sp_vals"] = (
+        blk.rows.astype(np.int64), blk.cols.astype(np.int64), blk.values)
+    out["sp_shape"] = np.array([m, n])
+    z = rng.standard_normal((n, 12))
+    out["z"] = z
+    out["spmm"] = block_multiply(pool, sp, dense(pool, "z", z), "spmm")[0].to_array()
+    q = rng.standard_normal((m, 12))
+    out["q"] = q
+    out["spmm_t"] = block_multiply(pool, sp.T, dense(pool, "q", q), "spmmt")[0].to_array()
+    out["dense_sp"] = block_multiply(pool, dense(pool, "q2", q).T, sp, "dsp")[0].to_array()
+    save("multiply", **out)
+
+
+def gen_qr():
+    rng = np.random.default_rng(1)
+    out = {}
+    cases = {
+        "tall": rng.standard_normal((600, 30)),
+        "c345": np.array([[3.0], [4.0]]),
+        "eye": np.eye(4),
+        "zero": np.zeros((10, 3)),
+    }
+    dep = rng.standard_normal((30, 6))
+    dep[:, 3] = 2.0 * dep[:, 1] - dep[:, 0]
+    cases["deficient"] = dep
+    cases["tall32"] = rng.standard_normal((520, 17)).astype(np.float32)
+    for name, a in cases.items():
+        pool = BlockPool()
+        prec = Precision.SINGLE if a.dtype == np.float32 else Precision.DOUBLE
+        res = thin_qr(pool, dense(pool, "a", a, prec), "q")
+        out[f"{name}_a"] = a
+        out[f"{name}_q"] = res.q.to_array()
+        out[f"{name}_r"] = res.r
+        out[f"{name}_def"] = np.array(res.deficient_columns, dtype=np.int64)
+    save("qr", **out)
+
+
+def gen_svd():
+    rng = np.random.default_rng(2)
+    out = {}
+    cases = {
+        "wide": rng.standard_normal((20, 60)),
+        "diag": np.diag([3.0, 2.0, 1.0]),
+        "perm": np.array([[0.0, 1.0], [1.0, 0.0]]),
+        "r30": rng.standard_normal((30, 700)),
+        "deficient": np.vstack([np.array([[1.0, 0, 0, 0, 0]]), np.zeros((2, 5))]),
+    }
+    for name, b in cases.items():
+        res = svd_small(b)
+        out[f"{name}_b"] = b
+        out[f"{name}_u"], out[f"{name}_s"], out[f"{name}_v"] = res.u, res.s, res.v
+    save("svd", **out)
+
+
+def rsvd_reorth_ref(pool, a, k, p, q, seed, precision):
+    """xsvd-reorth with the REFERENCE primitives."""
+    from xsvd.pipeline import gaussian_matrix
+
+    n = a.shape[1]
+    o = gaussian_matrix(pool, "O", n, k + p, seed, precision=precision)
+    y, _ = block_multiply(pool, a, o, "Y", out_precision=precision)
+    res = thin_qr(pool, y, "Q0")
+    qm = res.q
+    for i in range(q):
+        z, _ = block_multiply(pool, a.T, qm, f"Z{i}", out_precision=precision)
+        qz = thin_qr(pool, z, f"QZ{i}").q
+        y, _ = block_multiply(pool, a, qz, f"Y{i}", out_precision=precision)
+        res = thin_qr(pool, y, f"Q{i + 1}")
+        qm = res.q
+    b, _ = block_multiply(pool, qm.T, a, "B", out_precision=precision)
+    sv = svd_small(b.to_array().astype(np.float64))
+    ub = matrix_from_dense(pool, "UB", sv.u[:, :k], precision=Precision.DOUBLE)
+    u, _ = block_multiply(pool, qm, ub, "U", out_precision=precision)
+    return u.to_array(), sv.s[:k], sv.v[:, :k].astype(precision.storage_dtype), res.deficient_columns
+
+
+def gen_rsvd():
+    out = {}
+    rng = np.random.default_rng(3)
+    cases = []
+    # name, kind, m, n, k, p, q, seed, precision
+    cases.append(("d_small", "dense", 300, 200, 10, 5, 2, 4, "double"))
+    cases.append(("d_q0", "dense", 120, 90, 6, 3, 0, 1, "double"))
+    cases.append(("d_wide", "dense", 90, 260, 8, 4, 1, 9, "double"))
+    cases.append(("s_small", "dense", 300, 200, 10, 5, 2, 4, "single"))
+    cases.append(("sp_small", "sparse", 500, 300, 10, 5, 1, 2, "double"))
+    for name, kind, m, n, k, p, q, seed, prec in cases:
+        precision = PREC[prec]
+        if kind == "dense":
+            a = dense_lowrank_np(m, n, "pow-1.5", 1e-8, 500 + len(out), 600 + len(out))
+            a = a.astype(precision.storage_dtype)
+            out[f"{name}_a"] = a
+        else:
+            nnz = 4 * m
+            r = rng.integers(0, m, nnz)
+            c = rng.integers(0, n, nnz)
+            v = rng.standard_normal(nnz)
+        for variant in ("shipped", "reorth"):
+            pool = BlockPool()
+            if kind == "dense":
+                ma = dense(pool, "A", a, precision)
+            else:
+                ma = matrix_from_coo(pool, "A", m, n, r, c, v, precision=precision)
+                blk = pool.get("A", 0, 0)
+                out[f"{name}_rows"] = blk.rows.astype(np.int64)
+                out[f"{name}_cols"] = blk.cols.astype(np.int64)
+                out[f"{name}_vals"] = blk.values
+                out[f"{name}_shape"] = np.array([m, n])
+            if variant == "shipped":
+                res = randomized_svd(pool, ma, RsvdConfig(rank=k, oversample=p, power=q, seed=seed,
+                                                          precision=precision))
+                u, s, vv, d = res.u.to_array(), res.s, res.v.to_array(), res.deficient_columns
+            else:
+                u, s, vv, d = rsvd_reorth_ref(pool, ma, k, p, q, seed, precision)
+            out[f"{name}_{variant}_u"] = u
+            out[f"{name}_{variant}_s"] = s
+            out[f"{name}_{variant}_v"] = vv
+            out[f"{name}_{variant}_def"] = np.array(d, dtype=np.int64)
+        out[f"{name}_cfg"] = np.array([m, n, k, p, q, seed, 1 if prec == "double" else 0])
+    save("rsvd", **out)
+
+
+def gen_cfg1():
+    """Config 1 at full size: the shipped reference driver (its own parity
+    oracle) and xsvd-reorth; A regenerated from its seeds."""
+    w = CONFIGS[1]
+    a = dense_lowrank_np(w.m, w.n, w.spectrum, w.noise, 1000 + w.cfg, 2000 + w.cfg)
+    out = {"checksum": np.array([float(np.sum(a)), float(np.sum(a * a))])}
+    pool = BlockPool()
+    ma = dense(pool, "A", a)
+    res = randomized_svd(pool, ma, RsvdConfig(rank=w.k, oversample=w.p, power=w.q, seed=w.cfg))
+    out["shipped_u"], out["shipped_s"], out["shipped_v"] = res.u.to_array(), res.s, res.v.to_array()
+    pool = BlockPool()
+    ma = dense(pool, "A", a)
+    u, s, v, _ = rsvd_reorth_ref(pool, ma, w.k, w.p, w.q, w.cfg, Precision.DOUBLE)
+    out["reorth_u"], out["reorth_s"], out["reorth_v"] = u, s, v
+    save("cfg1", **out)
+
+
+if __name__ == "__main__":
+    assert xsvd.__file__.startswith("/root/reference"), xsvd.__file__
+    which = sys.argv[1:] or ["rng", "multiply", "qr", "svd", "rsvd", "cfg1"]
+    for w in which:
+        globals()[f"gen_{w}"]()
