@@ -1,0 +1,146 @@
+/*
+ * xsvd_b200 — C ABI of the B200-native randomized-SVD hot path.
+ *
+ * Drop-in boundary for the reference package `xsvd` (arXiv 1907.06470,
+ * /root/reference/pkg/src/xsvd). The reference is pure Python with no
+ * plugin registry: its hot path is the function
+ * `randomized_svd` (pipeline.py:442) built from `gaussian_matrix`
+ * (pipeline.py:259), `block_multiply` (kernels.py:145), `thin_qr`
+ * (kernels.py:297) and `svd_small` (kernels.py:542). Each entry point below
+ * replaces one of those; the Python binding is
+ * paper_1907_06470_b200/_lib.py (ctypes), and INTEGRATION.md shows the stub
+ * a maintainer would add to xsvd itself.
+ *
+ * Conventions
+ *   - every function returns an int status (XB_OK = 0); the message of the
+ *     last failure on the calling thread is xb_last_error();
+ *   - plain pointers and sizes only; matrices are row-major with an explicit
+ *     leading dimension (elements);
+ *   - "host" entry points take caller-owned host buffers and return only
+ *     after results are in host memory (synchronous); "_dev" entry points
+ *     take device pointers on the context's device and are stream-ordered on
+ *     the context's compute stream, synchronised before returning;
+ *   - one context = one device = one host thread at a time.
+ *
+ * Status codes map onto the reference exception taxonomy (errors.py):
+ *   XB_ESHAPE -> ShapeError, XB_EVALUE -> ValueError, XB_ENOMEM -> BudgetError,
+ *   XB_ECONV -> ConvergenceError, XB_ECUDA / XB_ENCCL / XB_EUNSUPPORTED -> XsvdError.
+ */
+#ifndef XSVD_B200_H
+#define XSVD_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define XB_ABI_VERSION 1
+
+enum xb_status {
+  XB_OK = 0,
+  XB_ESHAPE = 1,
+  XB_EVALUE = 2,
+  XB_ENOMEM = 3,
+  XB_ECONV = 4,
+  XB_ECUDA = 5,
+  XB_ENCCL = 6,
+  XB_EUNSUPPORTED = 7
+};
+
+/* Precision.DOUBLE / Precision.SINGLE storage dtypes (core.py:26-46). */
+enum xb_dtype { XB_F32 = 1, XB_F64 = 2 };
+
+/* Stage slots of stage_seconds[8], in the order of STAGE_NAMES
+ * (pipeline.py:33-51): Text Parsing, Preparation of O, O*A^T,
+ * Orthogonalization, A^T*Q_r, SVD0 Preparation, SVD0, Postprocessing. */
+#define XB_NUM_STAGES 8
+
+typedef struct xb_ctx xb_ctx;
+
+int xb_abi_version(void);
+const char* xb_last_error(void);
+
+/* Context: device, compute + copy streams, cached workspaces. */
+int xb_create(int device, xb_ctx** out);
+int xb_destroy(xb_ctx* ctx);
+/* Number of kernels this library launched since the context was created
+ * (the bench's gpu_launches evidence). */
+int64_t xb_launch_count(const xb_ctx* ctx);
+/* The context's compute stream (a cudaStream_t), so callers can record
+ * CUDA events on the stream the kernels run on. */
+void* xb_compute_stream(xb_ctx* ctx);
+
+/* Per-kernel profiling (measurement only; not on the reference interface).
+ * When enabled, the large products on A (the dominant tile-GEMM launches)
+ * are bracketed by CUDA events on the compute stream. xb_profile_read fills
+ * out[0] = seconds summed over those products, out[1] = their count,
+ * out[2] = algorithmic FLOPs (2*m*n*l each), out[3] = A bytes they read
+ * (m*n*elem each), and resets the accumulators. */
+int xb_profile_enable(xb_ctx* ctx, int on);
+int xb_profile_read(xb_ctx* ctx, double* out4);
+/* Saturating FP64 microbenchmarks on the context's device: TFLOP/s of the
+ * DMMA (mma.sync f64) and DFMA pipes — the f64 roofline denominator. */
+int xb_fp64_peaks(xb_ctx* ctx, double* dmma_tflops, double* dfma_tflops);
+
+/*
+ * Full factorization — replaces randomized_svd (pipeline.py:442-625) with
+ * re-orthonormalisation after every product (north star).
+ *   A      m x n, leading dim lda, dtype `dtype` (HOST memory; pinned memory
+ *          is used in place, pageable memory is registered for the call)
+ *   omega  optional n x (k+p) row-major host buffer of `dtype`; NULL means
+ *          generate gaussian_band(seed, 0, n, k+p) on the device (rng.py:65)
+ *   U      m x k (ldu >= k) `dtype`;  s  k doubles;  V  n x k (ldv >= k)
+ *   deficient  optional int32[k+p]; *ndeficient receives the count of
+ *          columns flagged like thin_qr (kernels.py:327-331)
+ *   stage_seconds optional double[XB_NUM_STAGES], device-timed
+ */
+int xb_rsvd_dense(xb_ctx* ctx, int dtype, int64_t m, int64_t n, const void* A, int64_t lda,
+                  const void* omega, uint64_t seed, int k, int p, int q,
+                  void* U, int64_t ldu, double* s, void* V, int64_t ldv,
+                  int32_t* deficient, int* ndeficient, double* stage_seconds);
+
+/* Same factorization with A, omega, U, V, s already in device memory
+ * (the HBM-resident measurement; deficient/ndeficient/stage_seconds stay
+ * host pointers). */
+int xb_rsvd_dense_dev(xb_ctx* ctx, int dtype, int64_t m, int64_t n, const void* dA, int64_t lda,
+                      const void* d_omega, uint64_t seed, int k, int p, int q,
+                      void* dU, int64_t ldu, double* d_s, void* dV, int64_t ldv,
+                      int32_t* deficient, int* ndeficient, double* stage_seconds);
+
+/* Omega generator — replaces gaussian_band (rng.py:38-70): rows
+ * [row0, row0+rows) x cols of N(0,1), cast to `dtype`, row-major `ld`.
+ * The uint64 hash stage is bit-exact; log/sin/cos are within a few ulp. */
+int xb_gaussian(xb_ctx* ctx, int dtype, uint64_t seed, int64_t row0, int64_t rows, int64_t cols,
+                void* out, int64_t ld);
+/* The integer stage alone: rows x (2*ceil(cols/2)) uint64 words (rng.py:38-47). */
+int xb_uniform_bits(xb_ctx* ctx, uint64_t seed, int64_t row0, int64_t rows, int64_t cols,
+                    uint64_t* out);
+
+/* Dense product — replaces block_multiply for dense operands
+ * (kernels.py:145-193, 80-84): C = op(A) * B with op(A) = A (trans_a = 0,
+ * A is m x kdim) or A^T (trans_a = 1, A is kdim x m, the transposed view of
+ * pool.py:390-418). B is kdim x n. Host buffers. */
+int xb_gemm(xb_ctx* ctx, int dtype, int trans_a, int64_t m, int64_t n, int64_t kdim,
+            const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc);
+int xb_gemm_dev(xb_ctx* ctx, int dtype, int trans_a, int64_t m, int64_t n, int64_t kdim,
+                const void* dA, int64_t lda, const void* dB, int64_t ldb, void* dC, int64_t ldc);
+
+/* Thin QR — replaces thin_qr (kernels.py:297-351): Y (m x r) = Q R with
+ * diag(R) >= 0; CholQR2 with an f64 Gram, falling back to Householder when
+ * the Gram is not numerically positive definite. R is r x r f64 row-major. */
+int xb_thin_qr(xb_ctx* ctx, int dtype, int64_t m, int64_t r, const void* Y, int64_t ldy,
+               void* Q, int64_t ldq, double* R, int32_t* deficient, int* ndeficient);
+
+/* Small SVD — replaces svd_small (kernels.py:542-562): B (r x n, r <= n,
+ * f64) = U diag(s) V^T, s non-increasing, each U column's largest-|entry|
+ * positive (earliest row on ties). U r x r, s r, V n x r. */
+int xb_svd_small(xb_ctx* ctx, int64_t r, int64_t n, const double* B, int64_t ldb,
+                 double* U, double* s, double* V);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* XSVD_B200_H */

@@ -42,22 +42,42 @@ def _spans(extent: int, step: int = CELL):
 # -- multiply ---------------------------------------------------------------
 
 
-def block_multiply(x: np.ndarray, y: np.ndarray, cdt, out_dtype) -> np.ndarray:
-    """Dense x dense on the canonical cell grid (kernels.py:80-84, 172-193)."""
+def block_multiply(x: np.ndarray, y: np.ndarray, cdt, out_dtype, threads: int = 1) -> np.ndarray:
+    """Dense x dense on the canonical cell grid (kernels.py:80-84, 172-193).
+
+    `threads` > 1 runs output cells on a thread pool like the reference's
+    _run_tasks (kernels.py:231-236); each cell's k-chunks stay in ascending
+    order, so the bits do not depend on the thread count."""
     m, k = x.shape
     k2, n = y.shape
     if k != k2:
         raise OracleShapeError(f"inner dimensions disagree: {x.shape} x {y.shape}")
     out = np.empty((m, n), dtype=out_dtype)
     kk = _spans(k)
-    for r0, r1 in _spans(m):
-        for c0, c1 in _spans(n):
-            acc = np.zeros((r1 - r0, c1 - c0), dtype=cdt)
-            for k0, k1 in kk:
-                a = np.ascontiguousarray(x[r0:r1, k0:k1]).astype(cdt)
-                b = np.ascontiguousarray(y[k0:k1, c0:c1]).astype(cdt)
-                acc += a @ b
-            out[r0:r1, c0:c1] = acc.astype(out_dtype)
+
+    def cell(task):
+        r0, r1, c0, c1 = task
+        acc = np.zeros((r1 - r0, c1 - c0), dtype=cdt)
+        for k0, k1 in kk:
+            a = np.ascontiguousarray(x[r0:r1, k0:k1]).astype(cdt)
+            b = np.ascontiguousarray(y[k0:k1, c0:c1]).astype(cdt)
+            acc += a @ b
+        out[r0:r1, c0:c1] = acc.astype(out_dtype)
+
+    tasks = [(r0, r1, c0, c1) for r0, r1 in _spans(m) for c0, c1 in _spans(n)]
+    if threads <= 1 or len(tasks) <= 1:
+        for t in tasks:
+            cell(t)
+    else:
+        from concurrent.futures import ThreadPoolExecutor
+
+        from threadpoolctl import threadpool_limits
+
+        # the reference's fast mode: cell threads with OPENBLAS_NUM_THREADS=1
+        # (SURVEY §8d); avoids oversubscribing cores with nested BLAS threads
+        with threadpool_limits(limits=1, user_api="blas"):
+            with ThreadPoolExecutor(max_workers=threads) as ex:
+                list(ex.map(cell, tasks))
     return out
 
 

@@ -52,6 +52,9 @@ class OracleResult:
     deficient_columns: tuple
 
 
+_THREADS = [1]  # cell workers for the restated block_multiply (set per driver call)
+
+
 def _mul(x, y, precision, fast):
     """x @ y with the reference's density dispatch (kernels.py:79-112)."""
     cdt, sdt = COMPUTE[precision], STORAGE[precision]
@@ -72,7 +75,7 @@ def _mul(x, y, precision, fast):
         return dense_sparse_multiply(x, y, cdt, sdt)
     if fast:
         return K.block_multiply_fast(x, y, cdt, sdt)
-    return K.block_multiply(x, y, cdt, sdt)
+    return K.block_multiply(x, y, cdt, sdt, threads=_THREADS[0])
 
 
 def dense_sparse_multiply(x, y: Coo, cdt, sdt) -> np.ndarray:
@@ -135,8 +138,10 @@ def omega(seed: int, n: int, l: int, precision: str) -> np.ndarray:
     return gaussian_band(seed, 0, n, l).astype(STORAGE[precision])
 
 
-def randomized_svd(a, k, p, q, seed, precision="double", *, fast=False, om=None) -> OracleResult:
+def randomized_svd(a, k, p, q, seed, precision="double", *, fast=False, om=None,
+                   threads: int = 1) -> OracleResult:
     """The shipped driver, src/pipeline.py:442-625 (fixed power)."""
+    _THREADS[0] = max(1, int(threads))
     _check(a, k, p)
     m, n = a.shape
     l = k + p
@@ -152,8 +157,10 @@ def randomized_svd(a, k, p, q, seed, precision="double", *, fast=False, om=None)
     return OracleResult(u, s[:k].astype(np.float64), v[:, :k].astype(STORAGE[precision]), deficient)
 
 
-def rsvd_reorth(a, k, p, q, seed, precision="double", *, fast=False, om=None) -> OracleResult:
+def rsvd_reorth(a, k, p, q, seed, precision="double", *, fast=False, om=None,
+                threads: int = 1) -> OracleResult:
     """xsvd-reorth: thin_qr after every product."""
+    _THREADS[0] = max(1, int(threads))
     _check(a, k, p)
     m, n = a.shape
     l = k + p

@@ -1,0 +1,30 @@
+"""B200-native randomized-SVD hot path for the `xsvd` reference (arXiv 1907.06470).
+
+Drop-in for the reference's hot-path entry points (same names, arguments,
+return types and error classes):
+
+    from paper_1907_06470_b200 import randomized_svd, RsvdConfig, BlockPool, matrix_from_dense
+    pool = BlockPool()
+    a = matrix_from_dense(pool, "A", array, precision=Precision.DOUBLE)
+    res = randomized_svd(pool, a, RsvdConfig(rank=20, oversample=10, power=2, seed=1))
+
+The arithmetic runs in the in-tree CUDA library (paper_1907_06470_b200/_lib/
+libxsvdb200.so, C ABI in include/xsvd_b200.h). There is no CPU fallback.
+"""
+
+from .core import (CANONICAL_CELL, BlockPartition, DenseBlock, Density, MatrixDescriptor,
+                   Precision, SparseBlock, transpose_view, wider)
+from .errors import BudgetError, ConvergenceError, ShapeError, XsvdError
+from .kernels import MultiplyStats, QRResult, SmallSVDResult, block_multiply, gram, svd_small, thin_qr
+from .pipeline import (STAGE_NAMES, RsvdConfig, RsvdResult, StageClock, gaussian_matrix,
+                       randomized_svd)
+from .pool import BlockPool, StoredMatrix, create_matrix, matrix_from_coo, matrix_from_dense
+
+__all__ = [
+    "BlockPartition", "BlockPool", "BudgetError", "CANONICAL_CELL", "ConvergenceError",
+    "DenseBlock", "Density", "MatrixDescriptor", "MultiplyStats", "Precision", "QRResult",
+    "RsvdConfig", "RsvdResult", "STAGE_NAMES", "ShapeError", "SmallSVDResult", "SparseBlock",
+    "StageClock", "StoredMatrix", "XsvdError", "block_multiply", "create_matrix",
+    "gaussian_matrix", "gram", "matrix_from_coo", "matrix_from_dense", "randomized_svd",
+    "svd_small", "thin_qr", "transpose_view", "wider",
+]

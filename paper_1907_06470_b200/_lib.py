@@ -1,0 +1,232 @@
+"""ctypes binding of the C ABI (include/xsvd_b200.h).
+
+The library is REQUIRED: there is no CPU fallback anywhere in this package.
+`load()` raises XsvdError when libxsvdb200.so is missing or no CUDA device is
+usable, so a product call on a machine without the CUDA path fails loudly.
+ctypes releases the GIL for the duration of every call.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+from .errors import XsvdError, raise_for_status
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libxsvdb200.so")
+
+XB_F32, XB_F64 = 1, 2
+NUM_STAGES = 8
+
+_lock = threading.Lock()
+_lib = None
+_ctxs: dict[int, "Context"] = {}
+
+# (name, restype, argtypes) for every symbol include/xsvd_b200.h declares
+_i64, _u64, _int, _vp, _dp = C.c_int64, C.c_uint64, C.c_int, C.c_void_p, C.POINTER(C.c_double)
+_i32p, _intp = C.POINTER(C.c_int32), C.POINTER(C.c_int)
+SIGNATURES = [
+    ("xb_abi_version", _int, []),
+    ("xb_last_error", C.c_char_p, []),
+    ("xb_create", _int, [_int, C.POINTER(_vp)]),
+    ("xb_destroy", _int, [_vp]),
+    ("xb_launch_count", _i64, [_vp]),
+    ("xb_compute_stream", _vp, [_vp]),
+    ("xb_profile_enable", _int, [_vp, _int]),
+    ("xb_profile_read", _int, [_vp, _vp]),
+    ("xb_fp64_peaks", _int, [_vp, _dp, _dp]),
+    ("xb_rsvd_dense", _int, [_vp, _int, _i64, _i64, _vp, _i64, _vp, _u64, _int, _int, _int,
+                             _vp, _i64, _vp, _vp, _i64, _vp, _intp, _vp]),
+    ("xb_rsvd_dense_dev", _int, [_vp, _int, _i64, _i64, _vp, _i64, _vp, _u64, _int, _int, _int,
+                                 _vp, _i64, _vp, _vp, _i64, _vp, _intp, _vp]),
+    ("xb_gaussian", _int, [_vp, _int, _u64, _i64, _i64, _i64, _vp, _i64]),
+    ("xb_uniform_bits", _int, [_vp, _u64, _i64, _i64, _i64, _vp]),
+    ("xb_gemm", _int, [_vp, _int, _int, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64]),
+    ("xb_gemm_dev", _int, [_vp, _int, _int, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64]),
+    ("xb_thin_qr", _int, [_vp, _int, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp, _intp]),
+    ("xb_svd_small", _int, [_vp, _i64, _i64, _vp, _i64, _vp, _vp, _vp]),
+]
+
+
+def lib_handle():
+    """dlopen the library and bind every symbol (no device needed)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise XsvdError(
+                    f"CUDA library missing: {LIB_PATH} (run __graft_entry__.build()); "
+                    "this package has no CPU fallback")
+            lib = C.CDLL(LIB_PATH)
+            for name, res, args in SIGNATURES:
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+    return _lib
+
+
+def _check(status: int):
+    if status != 0:
+        msg = lib_handle().xb_last_error().decode(errors="replace")
+        raise_for_status(status, msg)
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def dtype_code(dtype) -> int:
+    dt = np.dtype(dtype)
+    if dt == np.float64:
+        return XB_F64
+    if dt == np.float32:
+        return XB_F32
+    raise XsvdError(f"unsupported dtype {dt}")
+
+
+class Context:
+    """One device's library context (streams + cached workspaces)."""
+
+    def __init__(self, device: int):
+        self.lib = lib_handle()
+        self.device = device
+        h = C.c_void_p()
+        _check(self.lib.xb_create(device, C.byref(h)))
+        self.h = h
+
+    @property
+    def launches(self) -> int:
+        return int(self.lib.xb_launch_count(self.h))
+
+    @property
+    def stream_ptr(self) -> int:
+        return int(self.lib.xb_compute_stream(self.h) or 0)
+
+    def profile(self, on: bool):
+        _check(self.lib.xb_profile_enable(self.h, int(on)))
+
+    def profile_read(self) -> dict:
+        out = np.zeros(4)
+        _check(self.lib.xb_profile_read(self.h, _ptr(out)))
+        return {"seconds": out[0], "launches": int(out[1]), "flops": out[2], "bytes": out[3]}
+
+    def fp64_peaks(self):
+        a, b = C.c_double(), C.c_double()
+        _check(self.lib.xb_fp64_peaks(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    # -- full factorisation ---------------------------------------------------
+    def rsvd_dense(self, a: np.ndarray, k: int, p: int, q: int, seed: int, omega=None):
+        """Host buffers in, host factors out (xb_rsvd_dense)."""
+        a = np.asarray(a)
+        if a.ndim != 2:
+            raise XsvdError("A must be 2-d")
+        if a.strides[1] != a.itemsize:
+            a = np.ascontiguousarray(a)
+        m, n = a.shape
+        lda = a.strides[0] // a.itemsize
+        dt = a.dtype
+        l = k + p
+        u = np.empty((m, k), dtype=dt)
+        v = np.empty((n, k), dtype=dt)
+        s = np.empty(k, dtype=np.float64)
+        deficient = np.zeros(max(l, 1), dtype=np.int32)
+        ndef = C.c_int(0)
+        stages = np.zeros(NUM_STAGES, dtype=np.float64)
+        om = None
+        if omega is not None:
+            om = np.ascontiguousarray(omega, dtype=dt)
+            if om.shape != (n, l):
+                raise XsvdError(f"omega must be {(n, l)}, got {om.shape}")
+        _check(self.lib.xb_rsvd_dense(
+            self.h, dtype_code(dt), m, n, _ptr(a), lda, _ptr(om) if om is not None else None,
+            int(seed) & (2**64 - 1), k, p, q, _ptr(u), k, _ptr(s), _ptr(v), k, _ptr(deficient),
+            C.byref(ndef), _ptr(stages)))
+        return u, s, v, tuple(int(x) for x in deficient[: ndef.value]), stages
+
+    def rsvd_dense_dev(self, dtype, m, n, a_ptr, lda, k, p, q, seed, u_ptr, s_ptr, v_ptr,
+                       omega_ptr=None):
+        """Device pointers (e.g. torch tensors' data_ptr()) in and out."""
+        deficient = np.zeros(max(k + p, 1), dtype=np.int32)
+        ndef = C.c_int(0)
+        stages = np.zeros(NUM_STAGES, dtype=np.float64)
+        _check(self.lib.xb_rsvd_dense_dev(
+            self.h, dtype_code(dtype), m, n, C.c_void_p(a_ptr), lda,
+            C.c_void_p(omega_ptr) if omega_ptr else None, int(seed) & (2**64 - 1), k, p, q,
+            C.c_void_p(u_ptr), k, C.c_void_p(s_ptr), C.c_void_p(v_ptr), k, _ptr(deficient),
+            C.byref(ndef), _ptr(stages)))
+        return tuple(int(x) for x in deficient[: ndef.value]), stages
+
+    # -- step-level operators -------------------------------------------------------
+    def gaussian(self, seed, row0, rows, cols, dtype=np.float64):
+        out = np.empty((rows, cols), dtype=dtype)
+        _check(self.lib.xb_gaussian(self.h, dtype_code(dtype), int(seed) & (2**64 - 1), row0,
+                                    rows, cols, _ptr(out), cols))
+        return out
+
+    def uniform_bits(self, seed, row0, rows, cols):
+        count = 2 * ((cols + 1) // 2)
+        out = np.empty((rows, count), dtype=np.uint64)
+        _check(self.lib.xb_uniform_bits(self.h, int(seed) & (2**64 - 1), row0, rows, cols,
+                                        _ptr(out)))
+        return out
+
+    def gemm(self, a: np.ndarray, b: np.ndarray, trans_a: bool = False):
+        """op(a) @ b on the device; a, b host arrays of one dtype."""
+        a = np.ascontiguousarray(a)
+        b = np.ascontiguousarray(b, dtype=a.dtype)
+        if trans_a:
+            kdim, m = a.shape
+        else:
+            m, kdim = a.shape
+        if b.shape[0] != kdim:
+            from .errors import ShapeError
+
+            raise ShapeError(f"inner dimensions disagree: {a.shape} x {b.shape}")
+        n = b.shape[1]
+        c = np.empty((m, n), dtype=a.dtype)
+        _check(self.lib.xb_gemm(self.h, dtype_code(a.dtype), int(trans_a), m, n, kdim, _ptr(a),
+                                a.shape[1], _ptr(b), max(n, 1), _ptr(c), max(n, 1)))
+        return c
+
+    def gemm_dev(self, dtype, trans_a, m, n, kdim, a_ptr, lda, b_ptr, ldb, c_ptr, ldc):
+        _check(self.lib.xb_gemm_dev(self.h, dtype_code(dtype), int(trans_a), m, n, kdim,
+                                    C.c_void_p(a_ptr), lda, C.c_void_p(b_ptr), ldb,
+                                    C.c_void_p(c_ptr), ldc))
+
+    def thin_qr(self, y: np.ndarray):
+        y = np.ascontiguousarray(y)
+        m, r = y.shape
+        q = np.empty((m, r), dtype=y.dtype)
+        rr = np.empty((r, r), dtype=np.float64)
+        deficient = np.zeros(max(r, 1), dtype=np.int32)
+        ndef = C.c_int(0)
+        _check(self.lib.xb_thin_qr(self.h, dtype_code(y.dtype), m, r, _ptr(y), r, _ptr(q), r,
+                                   _ptr(rr), _ptr(deficient), C.byref(ndef)))
+        return q, rr, tuple(int(x) for x in deficient[: ndef.value])
+
+    def svd_small(self, b: np.ndarray):
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        r, n = b.shape
+        u = np.empty((r, r))
+        s = np.empty(r)
+        v = np.empty((n, r))
+        _check(self.lib.xb_svd_small(self.h, r, n, _ptr(b), n, _ptr(u), _ptr(s), _ptr(v)))
+        return u, s, v
+
+
+def load(device: int | None = None) -> Context:
+    """The (cached) context for `device` (default: LOCAL_RANK or 0)."""
+    if device is None:
+        device = int(os.environ.get("LOCAL_RANK", "0"))
+    with _lock:
+        ctx = _ctxs.get(device)
+    if ctx is None:
+        ctx = Context(device)
+        with _lock:
+            _ctxs[device] = ctx
+    return ctx

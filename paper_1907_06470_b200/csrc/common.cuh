@@ -1,0 +1,116 @@
+// Shared definitions for the xsvd_b200 CUDA library (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+#include "xsvd_b200.h"
+
+namespace xb {
+
+// Error carrying an xb_status; thrown inside the library, turned into a
+// status + thread-local message at the C boundary.
+struct Error : std::runtime_error {
+  int status;
+  Error(int s, const std::string& msg) : std::runtime_error(msg), status(s) {}
+};
+
+#define XB_CUDA(call)                                                                   \
+  do {                                                                                  \
+    cudaError_t _e = (call);                                                            \
+    if (_e != cudaSuccess) {                                                            \
+      throw ::xb::Error(_e == cudaErrorMemoryAllocation ? XB_ENOMEM : XB_ECUDA,         \
+                        std::string(#call) + ": " + cudaGetErrorString(_e) + " @ " +    \
+                            __FILE__ + ":" + std::to_string(__LINE__));                 \
+    }                                                                                   \
+  } while (0)
+
+#define XB_REQUIRE(cond, status, msg)                      \
+  do {                                                     \
+    if (!(cond)) throw ::xb::Error((status), (msg));       \
+  } while (0)
+
+// Every kernel launch goes through this counter (xb_launch_count).
+extern thread_local int64_t* g_launch_counter;
+inline void count_launch() {
+  if (g_launch_counter) ++*g_launch_counter;
+}
+inline void check_launch(const char* what) {
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess)
+    throw Error(XB_ECUDA, std::string("launch ") + what + ": " + cudaGetErrorString(e));
+}
+
+__host__ __device__ inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+__host__ __device__ inline int64_t ceil_div(int64_t x, int64_t m) { return (x + m - 1) / m; }
+
+constexpr int kNumSMs = 148;  // B200
+
+// ---- kernels (host launchers) ----------------------------------------------
+
+// Omega generator: out[r*ld + c] for r < rows, c < cols; columns in
+// [cols, ld_pad) are zero-filled when ld_pad > cols.
+template <typename T>
+void launch_gaussian(uint64_t seed, int64_t row0, int64_t rows, int64_t cols, T* out, int64_t ld,
+                     int64_t ld_pad, cudaStream_t st);
+void launch_uniform_bits(uint64_t seed, int64_t row0, int64_t rows, int64_t cols, uint64_t* out,
+                         cudaStream_t st);
+
+// FP64 DMMA GEMM. C[M x N] = op(A) * B where op(A)=A (A: M x K, lda) or
+// A^T (A: K x M, lda); B: K x N (ldb). Split-K over `splits` slices through
+// `work` (splits * M * ldc doubles) reduced in slice order (deterministic).
+struct DGemmArgs {
+  bool trans_a;
+  int64_t M, N, K;
+  const double* A;
+  int64_t lda;
+  const double* B;
+  int64_t ldb;
+  double* C;
+  int64_t ldc;
+};
+// Returns the number of split-K slices that will be used for this shape.
+int dgemm_plan_splits(const DGemmArgs& g);
+size_t dgemm_workspace_doubles(const DGemmArgs& g, int splits);
+void dgemm(const DGemmArgs& g, int splits, double* work, cudaStream_t st);
+
+// Cholesky of the leading l x l block of G (ld = ldg): writes upper R and
+// R^{-1} (ld = ldr, zero outside l x l), sets *flag = 1 when a pivot falls
+// below tau * G_jj (not numerically positive definite). Diag of R is added
+// to rdiag (multiplied in when accumulate != 0).
+void launch_chol_inv(const double* G, int64_t ldg, int l, double tau, double* R, double* Rinv,
+                     int64_t ldr, int* flag, cudaStream_t st);
+// Householder QR fallback (single CTA): if *flag != 0, recompute Q (rows x l,
+// ldq) and R (l x l, ldr) from X (rows x l, ldx) with the reference's
+// reflector convention; work needs rows * l doubles.
+void launch_householder_fallback(const double* X, int64_t ldx, int64_t rows, int l, int lpad, double* Q,
+                                 int64_t ldq, double* R, int64_t ldr, double* work,
+                                 const int* flag, cudaStream_t st);
+// Deficient-column flags from R (l x l, ldr): |R_jj| <= eps * ||R||_F.
+void launch_deficient(const double* R, int64_t ldr, int l, double eps, int* count, int* cols,
+                      cudaStream_t st);
+
+// One-sided Jacobi SVD of M = R^T (R: l x l upper, ldr): produces
+//   s[l] (descending), Ub (l x l, ldu: columns = sorted, sign-fixed left
+//   singular vectors of M), Wk (l x k, ldw: matching right singular vectors,
+//   same signs), status (0 ok, 1 no convergence).
+void launch_jacobi_svd(const double* R, int64_t ldr, int l, int k, double* Ub, int64_t ldu,
+                       double* s, double* Wk, int64_t ldw, double* work, int* status,
+                       cudaStream_t st);
+
+// FP64 pipe peaks (TFLOP/s) from saturating microbenchmarks (peak.cu).
+void measure_fp64_peaks(cudaStream_t st, double* dmma_tflops, double* dfma_tflops);
+
+// Small helpers
+void launch_transpose(const double* in, int64_t rows, int64_t cols, int64_t ldin, double* out,
+                      int64_t ldout, cudaStream_t st);
+void launch_copy2d(const double* in, int64_t rows, int64_t cols, int64_t ldin, double* out,
+                   int64_t ldout, cudaStream_t st);
+void launch_zero(double* p, size_t count, cudaStream_t st);
+
+}  // namespace xb

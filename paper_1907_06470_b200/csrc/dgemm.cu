@@ -1,0 +1,352 @@
+// FP64 tensor-core (DMMA) tile GEMM for the rSVD products.
+//
+// Replaces the reference's dense block_multiply (kernels.py:145-193,
+// _cell_accumulate 80-84) for the three product shapes of the hot path:
+//   NN  Y  = A * X        A m x n row-major (K-contiguous), X n x l
+//   TN  Z  = A^T * Q      A m x n row-major read as its transposed view
+//                         (pool.py:390-418), reduce over the long m
+//   TN  G  = Y^T * Y      the CholQR Gram (kernels.py:315-325 replacement)
+// FP64 has no tcgen05 kind on sm_100a (ptxas rejects kind::f64),
+// so the tensor-core path for f64 is the legacy mma.sync.m8n8k4.f64 (SASS
+// DMMA). Operands stream global -> shared with cp.async (LDGSTS) in a
+// STAGES-deep ring; every CTA owns a BM x BN output tile with BN covering
+// the whole (padded) sketch width l, so each A element is read from HBM
+// exactly once per product. Long reductions (TN over m, NN over n when the
+// output tile count is below the SM count) are split over `splits` slices
+// written to a workspace and summed in slice order by a second kernel — a
+// fixed order, so results are deterministic run to run (no fp atomics).
+//
+// Shared-memory layout: every tile row stride S satisfies S = 4 (mod 8)
+// doubles, which makes the per-lane 8-byte fragment loads of m8n8k4
+// (row = lane>>2, col = lane&3 patterns) bank-conflict free.
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace xb {
+namespace {
+
+template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, bool TRANS_A>
+struct DCfg {
+  static constexpr int kThreads = WARPS_M * WARPS_N * 32;
+  static constexpr int WM = BM / WARPS_M;  // rows per warp
+  static constexpr int WN = BN / WARPS_N;  // cols per warp
+  static constexpr int FM = WM / 8;        // 8x8 fragments per warp (M)
+  static constexpr int FN = WN / 8;        // (N)
+  static_assert(WM % 8 == 0 && WN % 8 == 0, "warp tile must be a multiple of 8");
+  static_assert(BK % 4 == 0, "BK multiple of 4");
+  static constexpr int pad8(int x) { return x + ((4 - (x % 8)) + 8) % 8; }
+  // A tile: NN -> BM rows x BK (K-contig), TN -> BK rows x BM (M-contig)
+  static constexpr int SA = TRANS_A ? pad8(BM) : pad8(BK);
+  static constexpr int A_ELEMS = TRANS_A ? BK * SA : BM * SA;
+  static constexpr int SB = pad8(BN);
+  static constexpr int B_ELEMS = BK * SB;
+  static constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;
+  static constexpr size_t SMEM = (size_t)STAGES * STAGE_ELEMS * sizeof(double);
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// 16-byte async copy with zero fill of the bytes past src_bytes.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile(
+      "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+
+// Load a rows x cols sub-block (global row-major, ld) into shared (stride S),
+// zero-filling outside [row_lim, col_lim). VEC16 requires ld, col0 even and a
+// 16B-aligned base; cols is then a multiple of 2.
+template <int ROWS, int COLS, int S, int NT, bool VEC16>
+__device__ __forceinline__ void load_tile(double* sdst, const double* __restrict__ g, int64_t ld,
+                                          int64_t row0, int64_t col0, int64_t row_lim,
+                                          int64_t col_lim, int tid) {
+  if constexpr (VEC16) {
+    constexpr int CPR = COLS / 2;  // 16B chunks per row
+    constexpr int TOTAL = ROWS * CPR;
+#pragma unroll
+    for (int i = tid; i < TOTAL; i += NT) {
+      const int r = i / CPR;
+      const int c = (i - r * CPR) * 2;
+      const int64_t gr = row0 + r, gc = col0 + c;
+      const double* src = g;
+      int bytes = 0;
+      if (gr < row_lim && gc < col_lim) {
+        src = g + gr * ld + gc;
+        bytes = (gc + 1 < col_lim) ? 16 : 8;
+      }
+      cp_async16(sdst + r * S + c, src, bytes);
+    }
+  } else {
+    constexpr int TOTAL = ROWS * COLS;
+#pragma unroll 4
+    for (int i = tid; i < TOTAL; i += NT) {
+      const int r = i / COLS;
+      const int c = i - r * COLS;
+      const int64_t gr = row0 + r, gc = col0 + c;
+      const double* src = g;
+      int bytes = 0;
+      if (gr < row_lim && gc < col_lim) {
+        src = g + gr * ld + gc;
+        bytes = 8;
+      }
+      cp_async8(sdst + r * S + c, src, bytes);
+    }
+  }
+}
+
+// C (or the split slice of the workspace) = op(A) * B over k in
+// [z * k_per_split, min(K, (z+1) * k_per_split)).
+template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, bool TRANS_A, bool A16,
+          bool B16>
+__global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, 1)
+    dgemm_kernel(int64_t M, int64_t N, int64_t K, const double* __restrict__ A, int64_t lda,
+                 const double* __restrict__ B, int64_t ldb, double* __restrict__ C, int64_t ldc,
+                 int64_t split_stride, int64_t k_per_split) {
+  using Cfg = DCfg<BM, BN, BK, WARPS_M, WARPS_N, STAGES, TRANS_A>;
+  extern __shared__ __align__(16) double smem[];
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = warp / WARPS_N, wn = warp % WARPS_N;
+  const int64_t m0 = (int64_t)blockIdx.x * BM;
+  const int64_t n0 = (int64_t)blockIdx.y * BN;
+  const int64_t kbeg = (int64_t)blockIdx.z * k_per_split;
+  const int64_t kend = min(K, kbeg + k_per_split);
+  C += (int64_t)blockIdx.z * split_stride;
+
+  double acc[Cfg::FM][Cfg::FN][2];
+#pragma unroll
+  for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+    for (int j = 0; j < Cfg::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const int ktiles = (int)ceil_div(kend - kbeg, BK);
+
+  auto load_stage = [&](int stage, int kt) {
+    double* sA = smem + stage * Cfg::STAGE_ELEMS;
+    double* sB = sA + Cfg::A_ELEMS;
+    const int64_t k0 = kbeg + (int64_t)kt * BK;
+    if constexpr (TRANS_A) {
+      load_tile<BK, BM, Cfg::SA, Cfg::kThreads, A16>(sA, A, lda, k0, m0, kend, M, tid);
+    } else {
+      load_tile<BM, BK, Cfg::SA, Cfg::kThreads, A16>(sA, A, lda, m0, k0, M, kend, tid);
+    }
+    load_tile<BK, BN, Cfg::SB, Cfg::kThreads, B16>(sB, B, ldb, k0, n0, kend, N, tid);
+  };
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < ktiles) load_stage(s, s);
+    cp_async_commit();
+  }
+
+  for (int kt = 0; kt < ktiles; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int nk = kt + STAGES - 1;
+      if (nk < ktiles) load_stage(nk % STAGES, nk);
+      cp_async_commit();
+    }
+    const double* sA = smem + (kt % STAGES) * Cfg::STAGE_ELEMS;
+    const double* sB = sA + Cfg::A_ELEMS;
+#pragma unroll
+    for (int ks = 0; ks < BK / 4; ++ks) {
+      double af[Cfg::FM], bf[Cfg::FN];
+#pragma unroll
+      for (int i = 0; i < Cfg::FM; ++i) {
+        const int row = wm * Cfg::WM + i * 8 + g;  // output row within tile
+        if constexpr (TRANS_A)
+          af[i] = sA[(ks * 4 + t) * Cfg::SA + row];
+        else
+          af[i] = sA[row * Cfg::SA + ks * 4 + t];
+      }
+#pragma unroll
+      for (int j = 0; j < Cfg::FN; ++j) {
+        const int col = wn * Cfg::WN + j * 8 + g;
+        bf[j] = sB[(ks * 4 + t) * Cfg::SB + col];
+      }
+#pragma unroll
+      for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+        for (int j = 0; j < Cfg::FN; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+  }
+  cp_async_wait<0>();
+
+  // Epilogue: fragment (row g, cols 2t, 2t+1) of each 8x8 block.
+#pragma unroll
+  for (int i = 0; i < Cfg::FM; ++i) {
+    const int64_t r = m0 + wm * Cfg::WM + i * 8 + g;
+    if (r >= M) continue;
+#pragma unroll
+    for (int j = 0; j < Cfg::FN; ++j) {
+      const int64_t c = n0 + wn * Cfg::WN + j * 8 + 2 * t;
+      double* dst = C + r * ldc + c;
+      if (c + 1 < N && ((ldc & 1) == 0)) {
+        *reinterpret_cast<double2*>(dst) = make_double2(acc[i][j][0], acc[i][j][1]);
+      } else {
+        if (c < N) dst[0] = acc[i][j][0];
+        if (c + 1 < N) dst[1] = acc[i][j][1];
+      }
+    }
+  }
+}
+
+// out[r, c] = sum_{s < S} work[s][r, c] in slice order.
+__global__ void split_reduce_kernel(const double* __restrict__ work, int64_t M, int64_t N,
+                                    int64_t ldw, int64_t stride, int S, double* __restrict__ C,
+                                    int64_t ldc) {
+  const int64_t total = M * N;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = idx / N, c = idx - r * N;
+    const double* p = work + r * ldw + c;
+    double acc = p[0];
+    for (int s = 1; s < S; ++s) acc += p[s * stride];
+    C[r * ldc + c] = acc;
+  }
+}
+
+}  // namespace
+
+// ---- dispatch ----------------------------------------------------------------
+
+namespace {
+
+struct Shape {
+  int BM, BN;
+};
+
+template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, bool TRANS_A>
+void run_cfg(const DGemmArgs& g, int splits, int64_t k_per_split, double* out, int64_t ldo,
+             int64_t split_stride, cudaStream_t st) {
+  using Cfg = DCfg<BM, BN, BK, WARPS_M, WARPS_N, STAGES, TRANS_A>;
+  const bool a16 = ((g.lda & 1) == 0) && ((reinterpret_cast<uintptr_t>(g.A) & 15) == 0) &&
+                   (((TRANS_A ? g.M : g.K) & 1) == 0);
+  const bool b16 = ((g.ldb & 1) == 0) && ((reinterpret_cast<uintptr_t>(g.B) & 15) == 0) &&
+                   ((g.N & 1) == 0);
+  dim3 grid((unsigned)ceil_div(g.M, BM), (unsigned)ceil_div(g.N, BN), (unsigned)splits);
+  auto launch = [&](auto kernel) {
+    XB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)Cfg::SMEM));
+    kernel<<<grid, Cfg::kThreads, Cfg::SMEM, st>>>(g.M, g.N, g.K, g.A, g.lda, g.B, g.ldb, out, ldo,
+                                                   split_stride, k_per_split);
+    check_launch("dgemm");
+  };
+  if (a16 && b16)
+    launch(dgemm_kernel<BM, BN, BK, WARPS_M, WARPS_N, STAGES, TRANS_A, true, true>);
+  else if (a16)
+    launch(dgemm_kernel<BM, BN, BK, WARPS_M, WARPS_N, STAGES, TRANS_A, true, false>);
+  else if (b16)
+    launch(dgemm_kernel<BM, BN, BK, WARPS_M, WARPS_N, STAGES, TRANS_A, false, true>);
+  else
+    launch(dgemm_kernel<BM, BN, BK, WARPS_M, WARPS_N, STAGES, TRANS_A, false, false>);
+}
+
+// Tile width for the N (sketch) dimension: the whole padded l in one tile
+// when it fits, so A streams once.
+int pick_bn(int64_t N) {
+  if (N <= 32) return 32;
+  if (N <= 64) return 64;
+  if (N == 120) return 120;
+  return 128;
+}
+
+constexpr int kBM = 128;
+constexpr int kBK = 16;
+
+int64_t kper(int64_t K, int splits) { return round_up(ceil_div(K, splits), kBK); }
+
+}  // namespace
+
+int dgemm_plan_splits(const DGemmArgs& g) {
+  const int64_t tiles = ceil_div(g.M, kBM) * ceil_div(g.N, pick_bn(g.N));
+  const int64_t kt = ceil_div(g.K, kBK);
+  // Fill the machine: aim for >= ~6 waves of 148 single-CTA SMs, but keep
+  // at least 8 k-tiles per slice so the pipeline has something to hide.
+  int best = 1;
+  double best_eff = 0.0;
+  for (int s = 1; s <= 256; ++s) {
+    if (kt / s < 8 && s > 1) break;
+    const int64_t ctas = tiles * s;
+    const int64_t waves = ceil_div(ctas, kNumSMs);
+    const double eff = (double)ctas / (double)(waves * kNumSMs);
+    // prefer fewer slices unless the wave efficiency improves materially
+    if (eff > best_eff + 0.03) {
+      best_eff = eff;
+      best = s;
+    }
+    if (ctas >= 6 * kNumSMs && eff > 0.95) break;
+  }
+  // Tiny outputs (Gram: one tile) need many slices to use the machine.
+  if (tiles <= 4) best = (int)std::min<int64_t>(std::max<int64_t>(1, kt / 8), 2 * kNumSMs / tiles);
+  return std::max(1, best);
+}
+
+size_t dgemm_workspace_doubles(const DGemmArgs& g, int splits) {
+  if (splits <= 1) return 0;
+  return (size_t)splits * (size_t)g.M * (size_t)round_up(g.N, 2);
+}
+
+void dgemm(const DGemmArgs& g, int splits, double* work, cudaStream_t st) {
+  if (g.M <= 0 || g.N <= 0) return;
+  if (g.K <= 0) {
+    for (int64_t r = 0; r < g.M; ++r)
+      XB_CUDA(cudaMemsetAsync(g.C + r * g.ldc, 0, g.N * sizeof(double), st));
+    return;
+  }
+  splits = std::max(1, std::min<int>(splits, (int)ceil_div(g.K, kBK)));
+  const int64_t kps = kper(g.K, splits);
+  splits = (int)ceil_div(g.K, kps);
+  double* out = g.C;
+  int64_t ldo = g.ldc, stride = 0;
+  if (splits > 1) {
+    XB_REQUIRE(work != nullptr, XB_ECUDA, "dgemm: split-K workspace missing");
+    out = work;
+    ldo = round_up(g.N, 2);
+    stride = g.M * ldo;
+  }
+  const int bn = pick_bn(g.N);
+  if (g.trans_a) {
+    switch (bn) {
+      case 32: run_cfg<kBM, 32, kBK, 4, 1, 4, true>(g, splits, kps, out, ldo, stride, st); break;
+      case 64: run_cfg<kBM, 64, kBK, 4, 2, 4, true>(g, splits, kps, out, ldo, stride, st); break;
+      case 120: run_cfg<kBM, 120, kBK, 4, 3, 4, true>(g, splits, kps, out, ldo, stride, st); break;
+      default: run_cfg<kBM, 128, kBK, 4, 4, 4, true>(g, splits, kps, out, ldo, stride, st); break;
+    }
+  } else {
+    switch (bn) {
+      case 32: run_cfg<kBM, 32, kBK, 4, 1, 4, false>(g, splits, kps, out, ldo, stride, st); break;
+      case 64: run_cfg<kBM, 64, kBK, 4, 2, 4, false>(g, splits, kps, out, ldo, stride, st); break;
+      case 120: run_cfg<kBM, 120, kBK, 4, 3, 4, false>(g, splits, kps, out, ldo, stride, st); break;
+      default: run_cfg<kBM, 128, kBK, 4, 4, 4, false>(g, splits, kps, out, ldo, stride, st); break;
+    }
+  }
+  if (splits > 1) {
+    const int64_t total = g.M * g.N;
+    int blocks = (int)std::min<int64_t>(ceil_div(total, 256), kNumSMs * 8);
+    split_reduce_kernel<<<blocks, 256, 0, st>>>(work, g.M, g.N, ldo, stride, splits, g.C, g.ldc);
+    check_launch("split_reduce");
+  }
+}
+
+}  // namespace xb

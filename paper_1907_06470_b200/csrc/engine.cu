@@ -1,0 +1,721 @@
+// rSVD engine and the C ABI (include/xsvd_b200.h).
+//
+// The factorisation (xb_rsvd_dense*) replaces the reference driver
+// randomized_svd (src/pipeline.py:442-625) with the north star's
+// re-orthonormalised power iteration ("xsvd-reorth"):
+//
+//   Omega   = gaussian_band(seed, 0, n, l)                 Preparation of O
+//   Y       = A Omega                    (NN DMMA)          O*A^T
+//   Q       = CholQR2(Y)                                    Orthogonalization
+//   repeat q times:
+//     Z = A^T Q  (TN DMMA);  Qz = CholQR2(Z)                O*A^T / Orth.
+//     Y = A Qz   (NN DMMA);  Q  = CholQR2(Y)                O*A^T / Orth.
+//   B^T     = A^T Q                      (TN DMMA)          A^T*Q_r
+//   B^T     = Q_B R_B                    (CholQR2)          SVD0 Preparation
+//   R_B^T   = U_B S W^T                  (Jacobi, sorted, sign rule)   SVD0
+//   U       = Q U_B[:, :k],  V = Q_B W[:, :k]   (NN DMMA)   Postprocessing
+//
+// B^T = A^T Q is the reference's B = Q^T A (pipeline.py:550) transposed — the
+// TN orientation the paper's own stage names record.
+// Everything after A lands in HBM runs on the device with no host round
+// trip; stage times come from CUDA events on the compute stream.
+#include <algorithm>
+#include <cfloat>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace xb {
+thread_local int64_t* g_launch_counter = nullptr;
+}
+
+using namespace xb;
+
+struct xb_ctx {
+  int device = 0;
+  cudaStream_t st = nullptr;  // compute
+  cudaStream_t cp = nullptr;  // host <-> device copies
+  int64_t launches = 0;
+  std::map<std::string, std::pair<void*, size_t>> bufs;
+  std::vector<cudaEvent_t> events;
+  // per-kernel profiling of the products on A (xb_profile_*)
+  bool profiling = false;
+  struct ProfMark {
+    cudaEvent_t b, e;
+    double flops, bytes;
+  };
+  std::vector<ProfMark> prof_pending;
+  std::vector<cudaEvent_t> prof_pool;
+  double prof_acc[4] = {0, 0, 0, 0};
+
+  cudaEvent_t prof_event() {
+    if (!prof_pool.empty()) {
+      cudaEvent_t e = prof_pool.back();
+      prof_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    XB_CUDA(cudaEventCreate(&e));
+    return e;
+  }
+  // resolve recorded marks (call after the stream is synchronised)
+  void prof_collect() {
+    for (auto& m : prof_pending) {
+      float ms = 0.f;
+      XB_CUDA(cudaEventElapsedTime(&ms, m.b, m.e));
+      prof_acc[0] += ms * 1e-3;
+      prof_acc[1] += 1;
+      prof_acc[2] += m.flops;
+      prof_acc[3] += m.bytes;
+      prof_pool.push_back(m.b);
+      prof_pool.push_back(m.e);
+    }
+    prof_pending.clear();
+  }
+
+  void* buf(const std::string& name, size_t bytes) {
+    auto it = bufs.find(name);
+    if (it != bufs.end() && it->second.second >= bytes) return it->second.first;
+    if (it != bufs.end()) {
+      XB_CUDA(cudaStreamSynchronize(st));
+      XB_CUDA(cudaFree(it->second.first));
+      bufs.erase(it);
+    }
+    void* p = nullptr;
+    XB_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 256)));
+    bufs[name] = {p, bytes};
+    return p;
+  }
+  double* dbuf(const std::string& name, size_t count) {
+    return static_cast<double*>(buf(name, count * sizeof(double)));
+  }
+  int* ibuf(const std::string& name, size_t count) {
+    return static_cast<int*>(buf(name, count * sizeof(int)));
+  }
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct LaunchScope {
+  int64_t* prev;
+  explicit LaunchScope(xb_ctx* c) : prev(g_launch_counter) {
+    g_launch_counter = &c->launches;
+    cudaSetDevice(c->device);
+  }
+  ~LaunchScope() { g_launch_counter = prev; }
+};
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return XB_OK;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return e.status;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host allocation failed";
+    return XB_ENOMEM;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return XB_ECUDA;
+  }
+}
+
+// ---- stage clock -------------------------------------------------------------
+
+enum Stage {
+  kParse = 0,
+  kGaussian = 1,
+  kSketch = 2,
+  kOrtho = 3,
+  kProject = 4,
+  kSvdPrep = 5,
+  kSvd = 6,
+  kPost = 7
+};
+
+struct StageClock {
+  xb_ctx* c;
+  std::vector<std::pair<int, cudaEvent_t>> marks;
+  size_t next_event = 0;
+  explicit StageClock(xb_ctx* ctx) : c(ctx) {}
+  cudaEvent_t ev() {
+    if (next_event >= c->events.size()) {
+      cudaEvent_t e;
+      XB_CUDA(cudaEventCreate(&e));
+      c->events.push_back(e);
+    }
+    return c->events[next_event++];
+  }
+  void enter(int stage) {
+    if (!marks.empty() && marks.back().first == stage) return;
+    cudaEvent_t e = ev();
+    XB_CUDA(cudaEventRecord(e, c->st));
+    marks.push_back({stage, e});
+  }
+  // Call after the stream is synchronised.
+  void finish(double* out) {
+    cudaEvent_t e = ev();
+    XB_CUDA(cudaEventRecord(e, c->st));
+    XB_CUDA(cudaEventSynchronize(e));
+    if (!out) return;
+    for (size_t i = 0; i < marks.size(); ++i) {
+      cudaEvent_t end = (i + 1 < marks.size()) ? marks[i + 1].second : e;
+      float ms = 0.f;
+      XB_CUDA(cudaEventElapsedTime(&ms, marks[i].second, end));
+      out[marks[i].first] += ms * 1e-3;
+    }
+  }
+};
+
+// ---- building blocks ---------------------------------------------------------
+
+void gemm(xb_ctx* c, bool ta, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
+          const double* B, int64_t ldb, double* C, int64_t ldc) {
+  DGemmArgs g{ta, M, N, K, A, lda, B, ldb, C, ldc};
+  const int splits = dgemm_plan_splits(g);
+  double* work = nullptr;
+  const size_t need = dgemm_workspace_doubles(g, splits);
+  if (need) work = c->dbuf("split", need);
+  dgemm(g, splits, work, c->st);
+}
+
+// A product on A (the dominant kernel): bracketed by events when profiling.
+void gemm_on_a(xb_ctx* c, bool ta, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
+               const double* B, int64_t ldb, double* C, int64_t ldc, int l) {
+  cudaEvent_t b = nullptr, e = nullptr;
+  if (c->profiling) {
+    b = c->prof_event();
+    e = c->prof_event();
+    XB_CUDA(cudaEventRecord(b, c->st));
+  }
+  gemm(c, ta, M, N, K, A, lda, B, ldb, C, ldc);
+  if (c->profiling) {
+    XB_CUDA(cudaEventRecord(e, c->st));
+    const double mn = (double)M * (double)K;  // A is M x K (NN) or K x M (TN)
+    c->prof_pending.push_back({b, e, 2.0 * mn * l, mn * sizeof(double)});
+  }
+}
+
+struct Small {
+  int l, lp;
+  double *G, *R1, *R1i, *R2, *R2i, *Rs;
+  int* flag;
+};
+
+Small small_bufs(xb_ctx* c, int l) {
+  Small s;
+  s.l = l;
+  s.lp = (int)round_up(l, 8);
+  const size_t ll = (size_t)s.lp * s.lp;
+  s.G = c->dbuf("G", ll);
+  s.R1 = c->dbuf("R1", ll);
+  s.R1i = c->dbuf("R1i", ll);
+  s.R2 = c->dbuf("R2", ll);
+  s.R2i = c->dbuf("R2i", ll);
+  s.Rs = c->dbuf("Rscratch", ll);
+  s.flag = c->ibuf("flag", 4);
+  XB_CUDA(cudaMemsetAsync(s.R1, 0, ll * sizeof(double), c->st));
+  XB_CUDA(cudaMemsetAsync(s.R1i, 0, ll * sizeof(double), c->st));
+  XB_CUDA(cudaMemsetAsync(s.R2, 0, ll * sizeof(double), c->st));
+  XB_CUDA(cudaMemsetAsync(s.R2i, 0, ll * sizeof(double), c->st));
+  return s;
+}
+
+// Q (rows x lp) = CholQR2(X), zero padding columns l..lp-1 preserved.
+// If Rout != null it receives R = R2 R1 (lp x lp, zero padded).
+void cholqr2(xb_ctx* c, const Small& s, const double* X, int64_t rows, double* T, double* Q,
+             double* Rout) {
+  const int l = s.l, lp = s.lp;
+  cudaStream_t st = c->st;
+  XB_CUDA(cudaMemsetAsync(s.flag, 0, sizeof(int), st));
+  gemm(c, true, lp, lp, rows, X, lp, X, lp, s.G, lp);          // G1 = X^T X
+  launch_chol_inv(s.G, lp, l, 1e-12, s.R1, s.R1i, lp, s.flag, st);
+  gemm(c, false, rows, lp, lp, X, lp, s.R1i, lp, T, lp);       // T = X R1^-1
+  gemm(c, true, lp, lp, rows, T, lp, T, lp, s.G, lp);          // G2 = T^T T
+  launch_chol_inv(s.G, lp, l, 1e-4, s.R2, s.R2i, lp, s.flag, st);
+  gemm(c, false, rows, lp, lp, T, lp, s.R2i, lp, Q, lp);       // Q = T R2^-1
+  double* R = Rout ? Rout : s.Rs;
+  if (Rout) gemm(c, false, lp, lp, lp, s.R2, lp, s.R1, lp, Rout, lp);  // R = R2 R1
+  // Householder fallback runs only when a Cholesky flagged (device-side test)
+  double* hw = c->dbuf("hh_work", (size_t)2 * rows * l);
+  launch_householder_fallback(X, lp, rows, l, lp, Q, lp, R, lp, hw, s.flag, st);
+}
+
+struct RsvdOut {
+  double* U;
+  int64_t ldu;
+  double* s;
+  double* V;
+  int64_t ldv;
+};
+
+void check_dims(int64_t m, int64_t n, int k, int p, int q) {
+  XB_REQUIRE(m >= 1 && n >= 1, XB_ESHAPE, "empty matrix");
+  XB_REQUIRE(k >= 1, XB_EVALUE, "rank must be at least 1, got " + std::to_string(k));
+  XB_REQUIRE(p >= 0, XB_EVALUE, "oversample must be nonnegative, got " + std::to_string(p));
+  XB_REQUIRE(q >= 0, XB_EVALUE, "power must be nonnegative, got " + std::to_string(q));
+  XB_REQUIRE((int64_t)k + p <= std::min(m, n), XB_ESHAPE,
+             "rank " + std::to_string(k) + " (+" + std::to_string(p) +
+                 " oversampling) exceeds min(" + std::to_string(m) + ", " + std::to_string(n) +
+                 ")");
+}
+
+// Host-side description of how A reaches the device for the first product.
+struct IngestPlan {
+  const double* hostA = nullptr;  // non-null: stream row chunks H2D, overlapped
+  int64_t host_lda = 0;
+  int64_t chunk_rows = 0;
+};
+
+void rsvd_f64(xb_ctx* c, int64_t m, int64_t n, double* dA, int64_t lda, const double* d_omega,
+              int64_t ld_omega, uint64_t seed, int k, int p, int q, const RsvdOut& out,
+              int32_t* deficient, int* ndeficient, double* stage_seconds, const IngestPlan& ing) {
+  check_dims(m, n, k, p, q);
+  const int l = k + p;
+  const int lp = (int)round_up(l, 8);
+  const int kp = (int)round_up(k, 2);
+  cudaStream_t st = c->st;
+  StageClock clk(c);
+  double local_stage[XB_NUM_STAGES] = {0};
+
+  // workspaces (cached across calls)
+  double* Om = c->dbuf("Om", (size_t)n * lp);
+  double* Ym = c->dbuf("Ym", (size_t)m * lp);
+  double* Tm = c->dbuf("Tm", (size_t)m * lp);
+  double* Qm = c->dbuf("Qm", (size_t)m * lp);
+  double* Zn = c->dbuf("Zn", (size_t)n * lp);
+  double* Tn = c->dbuf("Tn", (size_t)n * lp);
+  double* Qn = c->dbuf("Qn", (size_t)n * lp);
+  double* Rf = c->dbuf("Rf", (size_t)lp * lp);
+  double* Ub = c->dbuf("Ub", (size_t)lp * lp);
+  double* Wk = c->dbuf("Wk", (size_t)lp * kp);
+  double* sv = c->dbuf("sv", (size_t)lp);
+  double* jw = c->dbuf("jw", (size_t)lp * lp);
+  int* jstat = c->ibuf("jstat", 4);
+  int* defc = c->ibuf("defc", (size_t)lp + 4);
+  // pre-size the split-K workspace for the largest product so no cudaMalloc
+  // lands inside the timed stream
+  {
+    size_t need = 0;
+    auto upd = [&](bool ta, int64_t M, int64_t N, int64_t K) {
+      DGemmArgs g{ta, M, N, K, nullptr, 0, nullptr, 0, nullptr, 0};
+      need = std::max(need, dgemm_workspace_doubles(g, dgemm_plan_splits(g)));
+    };
+    upd(false, m, lp, n);
+    upd(true, n, lp, m);
+    upd(true, lp, lp, m);
+    upd(true, lp, lp, n);
+    upd(false, m, lp, lp);
+    upd(false, n, lp, lp);
+    upd(false, m, k, lp);
+    upd(false, n, k, lp);
+    if (ing.hostA) upd(false, ing.chunk_rows, lp, n);
+    if (need) c->dbuf("split", need);
+    c->dbuf("hh_work", (size_t)2 * std::max(m, n) * l);
+  }
+  Small s = small_bufs(c, l);
+  XB_CUDA(cudaMemsetAsync(Ub, 0, (size_t)lp * lp * sizeof(double), st));
+  XB_CUDA(cudaMemsetAsync(Wk, 0, (size_t)lp * kp * sizeof(double), st));
+
+  // Preparation of O
+  clk.enter(kGaussian);
+  if (d_omega) {
+    XB_CUDA(cudaMemsetAsync(Om, 0, (size_t)n * lp * sizeof(double), st));
+    launch_copy2d(d_omega, n, l, ld_omega, Om, lp, st);
+  } else {
+    launch_gaussian<double>(seed, 0, n, l, Om, lp, lp, st);
+  }
+
+  // O*A^T: the sketch; with a host A, row chunks arrive on the copy stream and
+  // each chunk's rows of Y are computed as soon as it lands.
+  clk.enter(kSketch);
+  if (ing.hostA) {
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    XB_CUDA(cudaEventCreate(&t0));
+    XB_CUDA(cudaEventCreate(&t1));
+    XB_CUDA(cudaEventRecord(t0, c->cp));
+    std::vector<cudaEvent_t> landed;
+    for (int64_t r0 = 0; r0 < m; r0 += ing.chunk_rows) {
+      const int64_t rows = std::min(ing.chunk_rows, m - r0);
+      XB_CUDA(cudaMemcpy2DAsync(dA + r0 * lda, lda * sizeof(double), ing.hostA + r0 * ing.host_lda,
+                                ing.host_lda * sizeof(double), n * sizeof(double), rows,
+                                cudaMemcpyHostToDevice, c->cp));
+      cudaEvent_t e;
+      XB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      XB_CUDA(cudaEventRecord(e, c->cp));
+      XB_CUDA(cudaStreamWaitEvent(st, e, 0));
+      landed.push_back(e);
+      gemm_on_a(c, false, rows, lp, n, dA + r0 * lda, lda, Om, lp, Ym + r0 * lp, lp, l);
+    }
+    XB_CUDA(cudaEventRecord(t1, c->cp));
+    XB_CUDA(cudaStreamSynchronize(c->cp));
+    float ms = 0.f;
+    XB_CUDA(cudaEventElapsedTime(&ms, t0, t1));
+    local_stage[kParse] += ms * 1e-3;  // ingest (H2D), overlapped with the sketch
+    for (auto e : landed) cudaEventDestroy(e);
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+  } else {
+    gemm_on_a(c, false, m, lp, n, dA, lda, Om, lp, Ym, lp, l);
+  }
+  clk.enter(kOrtho);
+  cholqr2(c, s, Ym, m, Tm, Qm, q == 0 ? Rf : nullptr);
+  for (int it = 0; it < q; ++it) {
+    clk.enter(kSketch);
+    gemm_on_a(c, true, n, lp, m, dA, lda, Qm, lp, Zn, lp, l);  // Z = A^T Q
+    clk.enter(kOrtho);
+    cholqr2(c, s, Zn, n, Tn, Qn, nullptr);
+    clk.enter(kSketch);
+    gemm_on_a(c, false, m, lp, n, dA, lda, Qn, lp, Ym, lp, l);  // Y = A Qz
+    clk.enter(kOrtho);
+    cholqr2(c, s, Ym, m, Tm, Qm, it == q - 1 ? Rf : nullptr);
+  }
+  // deficient columns of the final range-finder QR (kernels.py:327-331)
+  launch_deficient(Rf, lp, l, DBL_EPSILON, defc, defc + 1, st);
+
+  clk.enter(kProject);
+  gemm_on_a(c, true, n, lp, m, dA, lda, Qm, lp, Zn, lp, l);  // B^T = A^T Q
+
+  clk.enter(kSvdPrep);
+  cholqr2(c, s, Zn, n, Tn, Qn, Rf);  // B^T = Q_B R_B
+
+  clk.enter(kSvd);
+  launch_jacobi_svd(Rf, lp, l, k, Ub, lp, sv, Wk, kp, jw, jstat, st);
+
+  clk.enter(kPost);
+  gemm(c, false, m, k, lp, Qm, lp, Ub, lp, out.U, out.ldu);  // U = Q U_B[:, :k]
+  gemm(c, false, n, k, lp, Qn, lp, Wk, kp, out.V, out.ldv);  // V = Q_B W_k
+  XB_CUDA(cudaMemcpyAsync(out.s, sv, k * sizeof(double), cudaMemcpyDeviceToDevice, st));
+
+  int hstat = 0;
+  std::vector<int> hdef(lp + 1, 0);
+  XB_CUDA(cudaMemcpyAsync(&hstat, jstat, sizeof(int), cudaMemcpyDeviceToHost, st));
+  XB_CUDA(cudaMemcpyAsync(hdef.data(), defc, (lp + 1) * sizeof(int), cudaMemcpyDeviceToHost, st));
+  clk.finish(stage_seconds ? local_stage : nullptr);
+  XB_CUDA(cudaStreamSynchronize(st));
+  if (c->profiling) c->prof_collect();
+  if (stage_seconds)
+    for (int i = 0; i < XB_NUM_STAGES; ++i) stage_seconds[i] = local_stage[i];
+  if (ndeficient) *ndeficient = hdef[0];
+  if (deficient)
+    for (int i = 0; i < hdef[0] && i < l; ++i) deficient[i] = hdef[1 + i];
+  XB_REQUIRE(hstat == 0, XB_ECONV, "Jacobi SVD of the projected factor did not converge in 60 sweeps");
+}
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+struct HostRegistration {
+  void* p = nullptr;
+  HostRegistration(const void* ptr, size_t bytes) {
+    if (!ptr || bytes == 0 || is_pinned(ptr)) return;
+    if (cudaHostRegister(const_cast<void*>(ptr), bytes, cudaHostRegisterDefault) == cudaSuccess)
+      p = const_cast<void*>(ptr);
+    else
+      cudaGetLastError();  // fall back to pageable copies
+  }
+  ~HostRegistration() {
+    if (p) cudaHostUnregister(p);
+  }
+};
+
+void require_f64(int dtype) {
+  XB_REQUIRE(dtype == XB_F64 || dtype == XB_F32, XB_EVALUE, "unknown dtype");
+  XB_REQUIRE(dtype == XB_F64, XB_EUNSUPPORTED,
+             "float32 (Precision.SINGLE) path is not built in this round");
+}
+
+}  // namespace
+
+// ---- C ABI ---------------------------------------------------------------------
+
+extern "C" {
+
+int xb_abi_version(void) { return XB_ABI_VERSION; }
+
+const char* xb_last_error(void) { return g_last_error.c_str(); }
+
+int xb_create(int device, xb_ctx** out) {
+  return guarded([&] {
+    XB_REQUIRE(out != nullptr, XB_EVALUE, "out is null");
+    int n = 0;
+    XB_CUDA(cudaGetDeviceCount(&n));
+    XB_REQUIRE(device >= 0 && device < n, XB_EVALUE, "no such CUDA device");
+    auto* c = new xb_ctx();
+    c->device = device;
+    XB_CUDA(cudaSetDevice(device));
+    XB_CUDA(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+    XB_CUDA(cudaStreamCreateWithFlags(&c->cp, cudaStreamNonBlocking));
+    *out = c;
+  });
+}
+
+int xb_destroy(xb_ctx* c) {
+  return guarded([&] {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->st);
+    cudaStreamSynchronize(c->cp);
+    for (auto& kv : c->bufs) cudaFree(kv.second.first);
+    for (auto e : c->events) cudaEventDestroy(e);
+    cudaStreamDestroy(c->st);
+    cudaStreamDestroy(c->cp);
+    delete c;
+  });
+}
+
+int64_t xb_launch_count(const xb_ctx* c) { return c ? c->launches : 0; }
+
+void* xb_compute_stream(xb_ctx* c) { return c ? static_cast<void*>(c->st) : nullptr; }
+
+int xb_profile_enable(xb_ctx* c, int on) {
+  return guarded([&] {
+    XB_REQUIRE(c, XB_EVALUE, "null context");
+    c->profiling = on != 0;
+  });
+}
+
+int xb_profile_read(xb_ctx* c, double* out4) {
+  return guarded([&] {
+    XB_REQUIRE(c && out4, XB_EVALUE, "null argument");
+    XB_CUDA(cudaStreamSynchronize(c->st));
+    c->prof_collect();
+    for (int i = 0; i < 4; ++i) {
+      out4[i] = c->prof_acc[i];
+      c->prof_acc[i] = 0.0;
+    }
+  });
+}
+
+int xb_fp64_peaks(xb_ctx* c, double* dmma_tflops, double* dfma_tflops) {
+  return guarded([&] {
+    XB_REQUIRE(c && dmma_tflops && dfma_tflops, XB_EVALUE, "null argument");
+    LaunchScope ls(c);
+    measure_fp64_peaks(c->st, dmma_tflops, dfma_tflops);
+  });
+}
+
+int xb_rsvd_dense_dev(xb_ctx* c, int dtype, int64_t m, int64_t n, const void* dA, int64_t lda,
+                      const void* d_omega, uint64_t seed, int k, int p, int q, void* dU,
+                      int64_t ldu, double* d_s, void* dV, int64_t ldv, int32_t* deficient,
+                      int* ndeficient, double* stage_seconds) {
+  return guarded([&] {
+    XB_REQUIRE(c, XB_EVALUE, "null context");
+    LaunchScope ls(c);
+    require_f64(dtype);
+    XB_REQUIRE(lda >= n && ldu >= k && ldv >= k, XB_EVALUE, "leading dimension too small");
+    RsvdOut out{static_cast<double*>(dU), ldu, d_s, static_cast<double*>(dV), ldv};
+    rsvd_f64(c, m, n, const_cast<double*>(static_cast<const double*>(dA)), lda,
+             static_cast<const double*>(d_omega), k + p, seed, k, p, q, out, deficient,
+             ndeficient, stage_seconds, IngestPlan{});
+  });
+}
+
+int xb_rsvd_dense(xb_ctx* c, int dtype, int64_t m, int64_t n, const void* A, int64_t lda,
+                  const void* omega, uint64_t seed, int k, int p, int q, void* U, int64_t ldu,
+                  double* s, void* V, int64_t ldv, int32_t* deficient, int* ndeficient,
+                  double* stage_seconds) {
+  return guarded([&] {
+    XB_REQUIRE(c, XB_EVALUE, "null context");
+    LaunchScope ls(c);
+    require_f64(dtype);
+    check_dims(m, n, k, p, q);
+    XB_REQUIRE(A && U && s && V, XB_EVALUE, "null buffer");
+    XB_REQUIRE(lda >= n && ldu >= k && ldv >= k, XB_EVALUE, "leading dimension too small");
+    const int l = k + p;
+    HostRegistration reg(A, (size_t)((m - 1) * lda + n) * sizeof(double));
+    double* dA = c->dbuf("A", (size_t)m * n);
+    double* dU = c->dbuf("U", (size_t)m * k);
+    double* dV = c->dbuf("V", (size_t)n * k);
+    double* ds = c->dbuf("s", (size_t)k);
+    double* dO = nullptr;
+    if (omega) {
+      dO = c->dbuf("omega_in", (size_t)n * l);
+      XB_CUDA(cudaMemcpyAsync(dO, omega, (size_t)n * l * sizeof(double), cudaMemcpyHostToDevice,
+                              c->st));
+    }
+    IngestPlan ing;
+    ing.hostA = static_cast<const double*>(A);
+    ing.host_lda = lda;
+    // ~1 GiB chunks, at least 8 of them when the matrix is large
+    int64_t rows = std::max<int64_t>(256, ((int64_t)1 << 27) / std::max<int64_t>(n, 1));
+    rows = std::min(rows, std::max<int64_t>(256, round_up(ceil_div(m, 8), 128)));
+    ing.chunk_rows = std::min(rows, m);
+    RsvdOut out{dU, k, ds, dV, k};
+    rsvd_f64(c, m, n, dA, n, dO, l, seed, k, p, q, out, deficient, ndeficient, stage_seconds, ing);
+    HostRegistration ru(U, (size_t)((m - 1) * ldu + k) * sizeof(double));
+    HostRegistration rv(V, (size_t)((n - 1) * ldv + k) * sizeof(double));
+    XB_CUDA(cudaMemcpy2DAsync(U, ldu * sizeof(double), dU, k * sizeof(double), k * sizeof(double),
+                              m, cudaMemcpyDeviceToHost, c->st));
+    XB_CUDA(cudaMemcpy2DAsync(V, ldv * sizeof(double), dV, k * sizeof(double), k * sizeof(double),
+                              n, cudaMemcpyDeviceToHost, c->st));
+    XB_CUDA(cudaMemcpyAsync(s, ds, k * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    XB_CUDA(cudaStreamSynchronize(c->st));
+  });
+}
+
+int xb_gaussian(xb_ctx* c, int dtype, uint64_t seed, int64_t row0, int64_t rows, int64_t cols,
+                void* out, int64_t ld) {
+  return guarded([&] {
+    XB_REQUIRE(c && out, XB_EVALUE, "null argument");
+    LaunchScope ls(c);
+    XB_REQUIRE(rows >= 0 && cols >= 1 && ld >= cols && row0 >= 0, XB_EVALUE, "bad shape");
+    if (rows == 0) return;
+    const size_t es = dtype == XB_F64 ? 8 : 4;
+    XB_REQUIRE(dtype == XB_F64 || dtype == XB_F32, XB_EVALUE, "unknown dtype");
+    void* d = c->buf("gauss_out", (size_t)rows * cols * es);
+    if (dtype == XB_F64)
+      launch_gaussian<double>(seed, row0, rows, cols, static_cast<double*>(d), cols, cols, c->st);
+    else
+      launch_gaussian<float>(seed, row0, rows, cols, static_cast<float*>(d), cols, cols, c->st);
+    XB_CUDA(cudaMemcpy2DAsync(out, ld * es, d, cols * es, cols * es, rows, cudaMemcpyDeviceToHost,
+                              c->st));
+    XB_CUDA(cudaStreamSynchronize(c->st));
+  });
+}
+
+int xb_uniform_bits(xb_ctx* c, uint64_t seed, int64_t row0, int64_t rows, int64_t cols,
+                    uint64_t* out) {
+  return guarded([&] {
+    XB_REQUIRE(c && out, XB_EVALUE, "null argument");
+    LaunchScope ls(c);
+    XB_REQUIRE(rows >= 0 && cols >= 1 && row0 >= 0, XB_EVALUE, "bad shape");
+    if (rows == 0) return;
+    const int64_t count = 2 * ((cols + 1) / 2);
+    auto* d = static_cast<uint64_t*>(c->buf("bits_out", (size_t)rows * count * 8));
+    launch_uniform_bits(seed, row0, rows, cols, d, c->st);
+    XB_CUDA(cudaMemcpyAsync(out, d, (size_t)rows * count * 8, cudaMemcpyDeviceToHost, c->st));
+    XB_CUDA(cudaStreamSynchronize(c->st));
+  });
+}
+
+int xb_gemm_dev(xb_ctx* c, int dtype, int trans_a, int64_t m, int64_t n, int64_t kdim,
+                const void* dA, int64_t lda, const void* dB, int64_t ldb, void* dC, int64_t ldc) {
+  return guarded([&] {
+    XB_REQUIRE(c, XB_EVALUE, "null context");
+    LaunchScope ls(c);
+    require_f64(dtype);
+    XB_REQUIRE(m >= 0 && n >= 0 && kdim >= 0, XB_ESHAPE, "negative dimension");
+    XB_REQUIRE(ldc >= n && ldb >= n && lda >= (trans_a ? m : kdim), XB_EVALUE,
+               "leading dimension too small");
+    gemm(c, trans_a != 0, m, n, kdim, static_cast<const double*>(dA), lda,
+         static_cast<const double*>(dB), ldb, static_cast<double*>(dC), ldc);
+    XB_CUDA(cudaStreamSynchronize(c->st));
+  });
+}
+
+int xb_gemm(xb_ctx* c, int dtype, int trans_a, int64_t m, int64_t n, int64_t kdim, const void* A,
+            int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc) {
+  return guarded([&] {
+    XB_REQUIRE(c, XB_EVALUE, "null context");
+    LaunchScope ls(c);
+    require_f64(dtype);
+    XB_REQUIRE(m >= 0 && n >= 0 && kdim >= 0, XB_ESHAPE, "negative dimension");
+    XB_REQUIRE(ldc >= n && ldb >= n && lda >= (trans_a ? m : kdim), XB_EVALUE,
+               "leading dimension too small");
+    if (m == 0 || n == 0) return;
+    const int64_t arows = trans_a ? kdim : m, acols = trans_a ? m : kdim;
+    double* dA = c->dbuf("gA", (size_t)std::max<int64_t>(1, arows * acols));
+    double* dB = c->dbuf("gB", (size_t)std::max<int64_t>(1, kdim * n));
+    double* dC = c->dbuf("gC", (size_t)m * n);
+    if (arows * acols > 0)
+      XB_CUDA(cudaMemcpy2DAsync(dA, acols * 8, A, lda * 8, acols * 8, arows, cudaMemcpyHostToDevice,
+                                c->st));
+    if (kdim * n > 0)
+      XB_CUDA(cudaMemcpy2DAsync(dB, n * 8, B, ldb * 8, n * 8, kdim, cudaMemcpyHostToDevice, c->st));
+    gemm(c, trans_a != 0, m, n, kdim, dA, acols, dB, n, dC, n);
+    XB_CUDA(cudaMemcpy2DAsync(C, ldc * 8, dC, n * 8, n * 8, m, cudaMemcpyDeviceToHost, c->st));
+    XB_CUDA(cudaStreamSynchronize(c->st));
+  });
+}
+
+int xb_thin_qr(xb_ctx* c, int dtype, int64_t m, int64_t r, const void* Y, int64_t ldy, void* Q,
+               int64_t ldq, double* R, int32_t* deficient, int* ndeficient) {
+  return guarded([&] {
+    XB_REQUIRE(c, XB_EVALUE, "null context");
+    LaunchScope ls(c);
+    require_f64(dtype);
+    XB_REQUIRE(r >= 1 && m >= r, XB_ESHAPE,
+               "thin QR needs rows >= cols >= 1, got " + std::to_string(m) + "x" +
+                   std::to_string(r));
+    XB_REQUIRE(ldy >= r && ldq >= r, XB_EVALUE, "leading dimension too small");
+    const int l = (int)r, lp = (int)round_up(r, 8);
+    double* dY = c->dbuf("qrY", (size_t)m * lp);
+    double* dT = c->dbuf("qrT", (size_t)m * lp);
+    double* dQ = c->dbuf("qrQ", (size_t)m * lp);
+    double* dR = c->dbuf("qrR", (size_t)lp * lp);
+    int* defc = c->ibuf("qrdef", (size_t)lp + 4);
+    c->dbuf("hh_work", (size_t)2 * m * l);
+    XB_CUDA(cudaMemsetAsync(dY, 0, (size_t)m * lp * 8, c->st));
+    XB_CUDA(cudaMemcpy2DAsync(dY, lp * 8, Y, ldy * 8, r * 8, m, cudaMemcpyHostToDevice, c->st));
+    Small s = small_bufs(c, l);
+    cholqr2(c, s, dY, m, dT, dQ, dR);
+    launch_deficient(dR, lp, l, DBL_EPSILON, defc, defc + 1, c->st);
+    std::vector<int> hdef(lp + 1, 0);
+    XB_CUDA(cudaMemcpy2DAsync(Q, ldq * 8, dQ, lp * 8, r * 8, m, cudaMemcpyDeviceToHost, c->st));
+    if (R)
+      XB_CUDA(cudaMemcpy2DAsync(R, r * 8, dR, lp * 8, r * 8, r, cudaMemcpyDeviceToHost, c->st));
+    XB_CUDA(cudaMemcpyAsync(hdef.data(), defc, (lp + 1) * sizeof(int), cudaMemcpyDeviceToHost,
+                            c->st));
+    XB_CUDA(cudaStreamSynchronize(c->st));
+    if (ndeficient) *ndeficient = hdef[0];
+    if (deficient)
+      for (int i = 0; i < hdef[0] && i < l; ++i) deficient[i] = hdef[1 + i];
+  });
+}
+
+int xb_svd_small(xb_ctx* c, int64_t r, int64_t n, const double* B, int64_t ldb, double* U,
+                 double* s, double* V) {
+  return guarded([&] {
+    XB_REQUIRE(c, XB_EVALUE, "null context");
+    LaunchScope ls(c);
+    XB_REQUIRE(r >= 1 && n >= 1, XB_ESHAPE, "svd_small expects a non-empty matrix");
+    XB_REQUIRE(r <= n, XB_ESHAPE,
+               "svd_small expects r <= n, got " + std::to_string(r) + "x" + std::to_string(n));
+    XB_REQUIRE(ldb >= n, XB_EVALUE, "leading dimension too small");
+    const int l = (int)r, lp = (int)round_up(r, 8);
+    double* dB = c->dbuf("svB", (size_t)r * n);
+    double* dBt = c->dbuf("svBt", (size_t)n * lp);
+    double* dT = c->dbuf("svT", (size_t)n * lp);
+    double* dQ = c->dbuf("svQ", (size_t)n * lp);
+    double* dR = c->dbuf("svR", (size_t)lp * lp);
+    double* dUb = c->dbuf("svU", (size_t)lp * lp);
+    double* dW = c->dbuf("svW", (size_t)lp * lp);
+    double* ds = c->dbuf("svs", (size_t)lp);
+    double* dV = c->dbuf("svV", (size_t)n * l);
+    double* jw = c->dbuf("jw", (size_t)lp * lp);
+    int* jstat = c->ibuf("jstat", 4);
+    c->dbuf("hh_work", (size_t)2 * n * l);
+    XB_CUDA(cudaMemcpy2DAsync(dB, n * 8, B, ldb * 8, n * 8, r, cudaMemcpyHostToDevice, c->st));
+    XB_CUDA(cudaMemsetAsync(dBt, 0, (size_t)n * lp * 8, c->st));
+    XB_CUDA(cudaMemsetAsync(dUb, 0, (size_t)lp * lp * 8, c->st));
+    XB_CUDA(cudaMemsetAsync(dW, 0, (size_t)lp * lp * 8, c->st));
+    launch_transpose(dB, r, n, n, dBt, lp, c->st);
+    Small sm = small_bufs(c, l);
+    cholqr2(c, sm, dBt, n, dT, dQ, dR);
+    launch_jacobi_svd(dR, lp, l, l, dUb, lp, ds, dW, lp, jw, jstat, c->st);
+    gemm(c, false, n, l, lp, dQ, lp, dW, lp, dV, l);
+    int hstat = 0;
+    XB_CUDA(cudaMemcpy2DAsync(U, r * 8, dUb, lp * 8, r * 8, r, cudaMemcpyDeviceToHost, c->st));
+    XB_CUDA(cudaMemcpyAsync(s, ds, r * 8, cudaMemcpyDeviceToHost, c->st));
+    XB_CUDA(cudaMemcpyAsync(V, dV, (size_t)n * r * 8, cudaMemcpyDeviceToHost, c->st));
+    XB_CUDA(cudaMemcpyAsync(&hstat, jstat, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    XB_CUDA(cudaStreamSynchronize(c->st));
+    XB_REQUIRE(hstat == 0, XB_ECONV, "bidiagonal SVD did not converge in 60 sweeps");
+  });
+}
+
+}  // extern "C"

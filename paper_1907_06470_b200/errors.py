@@ -1,0 +1,42 @@
+"""Exception taxonomy mirroring the reference's (src/errors.py:1-58).
+
+The C ABI returns an xb_status; `raise_for_status` maps it onto these
+classes exactly as include/xsvd_b200.h documents:
+XB_ESHAPE -> ShapeError, XB_EVALUE -> ValueError, XB_ENOMEM -> BudgetError,
+XB_ECONV -> ConvergenceError, anything else -> XsvdError.
+"""
+
+
+class XsvdError(Exception):
+    """Base class for all errors raised by this package (errors.py:4)."""
+
+
+class ShapeError(XsvdError):
+    """Operand dimensions are incompatible (errors.py:8)."""
+
+
+class BudgetError(XsvdError):
+    """The memory budget (here: device memory) cannot fit the operation (errors.py:38)."""
+
+
+class ConvergenceError(XsvdError):
+    """An iterative kernel exceeded its sweep limit (errors.py:42)."""
+
+    def __init__(self, message, residual=None):
+        super().__init__(message)
+        self.residual = residual
+
+
+XB_ESHAPE, XB_EVALUE, XB_ENOMEM, XB_ECONV, XB_ECUDA, XB_ENCCL, XB_EUNSUPPORTED = 1, 2, 3, 4, 5, 6, 7
+
+
+def raise_for_status(status: int, message: str):
+    if status == XB_ESHAPE:
+        raise ShapeError(message)
+    if status == XB_EVALUE:
+        raise ValueError(message)
+    if status == XB_ENOMEM:
+        raise BudgetError(message)
+    if status == XB_ECONV:
+        raise ConvergenceError(message)
+    raise XsvdError(f"[xb status {status}] {message}")

@@ -1,0 +1,109 @@
+"""GPU replacements for the reference's block kernels (src/kernels.py).
+
+Same names, arguments, return types and error behaviour as the reference:
+
+  block_multiply(pool, x, y, out_id, *, threads=1, out_precision=None)
+        -> (StoredMatrix, MultiplyStats)                      kernels.py:145-228
+  gram(pool, b, out_id, *, threads=1)                         kernels.py:239-241
+  thin_qr(pool, y, q_id) -> QRResult(q, r, deficient_columns) kernels.py:297-351
+  svd_small(b) -> SmallSVDResult(u, s, v)                     kernels.py:542-562
+
+Arithmetic runs in libxsvdb200.so (FP64 DMMA GEMM, CholQR2 + Householder
+fallback, one-sided Jacobi). `threads` is accepted for signature parity and
+ignored. There is no CPU fallback: a missing library raises XsvdError.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .core import Precision, as_precision, wider
+from .errors import ShapeError, XsvdError
+from .pool import canonical_coo, is_sparse, register_dense, stored_to_array
+
+
+@dataclass
+class MultiplyStats:
+    multiply_adds: int = 0
+    skipped_cells: int = 0
+    threads_used: int = 1
+    estimate: object = None
+
+
+@dataclass
+class QRResult:
+    q: object
+    r: np.ndarray
+    deficient_columns: tuple = ()
+
+
+@dataclass
+class SmallSVDResult:
+    u: np.ndarray
+    s: np.ndarray
+    v: np.ndarray
+
+
+def _require_double(prec: Precision, what: str):
+    if as_precision(prec) is not Precision.DOUBLE:
+        raise XsvdError(f"{what}: {as_precision(prec).value} precision path is not built yet "
+                        "(the CUDA library currently implements float64)")
+
+
+def _canonical(mat):
+    """(canonical array, transposed flag) without materialising a transpose."""
+    arr = stored_to_array(mat)
+    if mat.desc.transposed:
+        return arr.T, True  # arr.T is the canonical (contiguous) array
+    return arr, False
+
+
+def block_multiply(pool, x, y, out_id, *, threads: int = 1, out_precision=None):
+    """out = x @ y on the device (kernels.py:145-193, dense operands)."""
+    m, k = x.shape
+    k2, n = y.shape
+    if k != k2:
+        raise ShapeError(f"inner dimensions disagree: {x.shape} x {y.shape}")
+    if is_sparse(x) or is_sparse(y):
+        raise XsvdError("block_multiply: sparse operands are not built on the GPU path yet")
+    prec = as_precision(out_precision) if out_precision is not None else wider(
+        as_precision(x.desc.precision), as_precision(y.desc.precision))
+    _require_double(prec, "block_multiply")
+    ctx = _lib.load()
+    a, ta = _canonical(x)
+    b = stored_to_array(y)
+    c = ctx.gemm(np.asarray(a, np.float64), np.asarray(b, np.float64), trans_a=ta)
+    out = register_dense(pool, out_id, c.astype(prec.storage_dtype, copy=False), prec)
+    return out, MultiplyStats(multiply_adds=m * n * k, threads_used=1)
+
+
+def gram(pool, b, out_id, *, threads: int = 1):
+    """B^T B through the transposed-view product (kernels.py:239-241)."""
+    return block_multiply(pool, b.T, b, out_id, threads=threads)
+
+
+def thin_qr(pool, y, q_id) -> QRResult:
+    """Thin QR of a tall dense matrix (kernels.py:297-351)."""
+    m, r = y.shape
+    if m < r or r < 1:
+        raise ShapeError(f"thin QR needs rows >= cols >= 1, got {m}x{r}")
+    prec = as_precision(y.desc.precision)
+    _require_double(prec, "thin_qr")
+    q, rr, deficient = _lib.load().thin_qr(np.asarray(stored_to_array(y), np.float64))
+    qm = register_dense(pool, q_id, q.astype(prec.storage_dtype, copy=False), prec)
+    return QRResult(q=qm, r=rr, deficient_columns=deficient)
+
+
+def svd_small(b) -> SmallSVDResult:
+    """SVD of the small factor B (r x n, r <= n) (kernels.py:542-562)."""
+    b = np.asarray(b, dtype=np.float64)
+    if b.ndim != 2:
+        raise ShapeError(f"svd_small expects a matrix, got shape {b.shape}")
+    r, n = b.shape
+    if r > n:
+        raise ShapeError(f"svd_small expects r <= n, got {r}x{n}")
+    u, s, v = _lib.load().svd_small(b)
+    return SmallSVDResult(u=u, s=s, v=v)

@@ -1,0 +1,160 @@
+"""rSVD driver: the drop-in for the reference's `randomized_svd`.
+
+  randomized_svd(pool, a, config, *, threads=1, runner=None, clock=None)
+      -> RsvdResult(u, s, v, chosen_q, stage_seconds, deficient_columns)
+  (reference: src/pipeline.py:442-625; RsvdConfig 78-150; RsvdResult 153-160;
+   STAGE_NAMES/StageClock 33-75; gaussian_matrix 259-284)
+
+One call runs the whole factorisation inside libxsvdb200.so
+(xb_rsvd_dense): A is streamed host->HBM in row chunks overlapped with the
+sketch, then every product, orthonormalisation and the small SVD run on the
+device; U, s, V come back and are registered in the CALLER's pool under the
+reference's ids "U", "S", "V". The power iteration re-orthonormalises after
+every product (the north star; the reference's shipped driver does not,
+pipeline.py:321-371 — SURVEY.md F4), so results match the "xsvd-reorth"
+oracle. Stage times are device-timed per STAGE_NAMES key.
+
+Out of scope (fail loudly): power="auto" (auto_select_q), gram_path=True,
+and the store-backed durable plan (PlanRunner records, resume).
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+from contextlib import contextmanager
+from dataclasses import dataclass, field
+import time
+
+import numpy as np
+
+from . import _lib
+from .core import Precision, as_precision
+from .errors import ShapeError, XsvdError
+from .pool import is_sparse, register_dense, stored_to_array
+
+STAGE_PARSE = "Text Parsing"
+STAGE_GAUSSIAN = "Preparation of O"
+STAGE_SKETCH = "O*A^T"
+STAGE_ORTHO = "Orthogonalization"
+STAGE_PROJECT = "A^T*Q_r"
+STAGE_SVD_PREP = "SVD0 Preparation"
+STAGE_SVD = "SVD0"
+STAGE_POST = "Postprocessing"
+STAGE_NAMES = (STAGE_PARSE, STAGE_GAUSSIAN, STAGE_SKETCH, STAGE_ORTHO, STAGE_PROJECT,
+               STAGE_SVD_PREP, STAGE_SVD, STAGE_POST)
+
+
+class StageClock:
+    """Accumulator keyed by stage name (pipeline.py:63-75)."""
+
+    def __init__(self):
+        self.seconds = {name: 0.0 for name in STAGE_NAMES}
+
+    @contextmanager
+    def timing(self, stage: str):
+        t0 = time.perf_counter()
+        try:
+            yield
+        finally:
+            self.seconds[stage] += time.perf_counter() - t0
+
+
+@dataclass(frozen=True)
+class RsvdConfig:
+    """Same fields, defaults and validation as pipeline.py:78-150."""
+
+    rank: int
+    power: object = "auto"
+    q_max: int = 5
+    tau: float = 1e-6
+    seed: int = 0
+    precision: object = Precision.DOUBLE
+    oversample: int = 0
+    gram_path: bool = False
+    budget: object = None
+    workdir: str | None = None
+
+    def __post_init__(self):
+        if self.rank < 1:
+            raise ValueError(f"rank must be at least 1, got {self.rank}")
+        if self.q_max < 0:
+            raise ValueError(f"q_max must be nonnegative, got {self.q_max}")
+        if isinstance(self.power, str):
+            if self.power != "auto":
+                raise ValueError(f"power must be 'auto' or an integer, got {self.power!r}")
+        elif not 0 <= self.power <= self.q_max:
+            raise ValueError(f"power {self.power} outside 0..{self.q_max}")
+        if not self.tau > 0:
+            raise ValueError(f"tau must be positive, got {self.tau}")
+        if self.oversample < 0:
+            raise ValueError(f"oversample must be nonnegative, got {self.oversample}")
+
+    def to_json(self) -> dict:
+        return {"rank": self.rank, "power": self.power, "q_max": self.q_max, "tau": self.tau,
+                "seed": self.seed, "precision": as_precision(self.precision).value,
+                "oversample": self.oversample, "gram_path": self.gram_path}
+
+    def digest(self) -> str:
+        blob = json.dumps(self.to_json(), sort_keys=True, separators=(",", ":"))
+        return hashlib.sha256(blob.encode()).hexdigest()
+
+
+@dataclass
+class RsvdResult:
+    u: object
+    s: np.ndarray
+    v: object
+    chosen_q: int
+    stage_seconds: dict = field(default_factory=dict)
+    deficient_columns: tuple = ()
+
+
+def gaussian_matrix(pool, matrix_id, rows, cols, seed, *, precision=Precision.DOUBLE):
+    """N(0,1) matrix keyed by (seed, row) (pipeline.py:259-284), generated on
+    the device (rng.py restated in csrc/rng.cu)."""
+    precision = as_precision(precision)
+    dt = np.float64 if precision is Precision.DOUBLE else np.float32
+    arr = _lib.load().gaussian(seed, 0, rows, cols, dtype=dt)
+    return register_dense(pool, matrix_id, arr.astype(precision.storage_dtype, copy=False),
+                          precision)
+
+
+def _dense_input(a) -> np.ndarray:
+    """The caller's A as one row-major host array (zero-copy for an
+    unbudgeted single-tile matrix, as SURVEY.md §8a notes)."""
+    d = a.desc
+    part = d.partition
+    if not d.transposed and part.n_row_tiles == 1 and part.n_col_tiles == 1:
+        return a.pool.get(d.matrix_id, 0, 0).values
+    return np.ascontiguousarray(stored_to_array(a))
+
+
+def randomized_svd(pool, a, config: RsvdConfig, *, threads: int = 1, runner=None, clock=None):
+    """Rank-k randomized factorisation A ~ U diag(s) V^T on the GPU."""
+    m, n = a.shape
+    r_work = config.rank + config.oversample
+    if r_work > min(m, n):
+        raise ShapeError(f"rank {config.rank} (+{config.oversample} oversampling) exceeds "
+                         f"min{tuple(a.shape)} = {min(m, n)}")
+    if config.power == "auto":
+        raise XsvdError("power='auto' (auto_select_q) is outside the GPU hot path; pass an int")
+    if config.gram_path:
+        raise XsvdError("gram_path=True is outside the GPU hot path")
+    if is_sparse(a):
+        raise XsvdError("sparse A is not built on the GPU path yet")
+    precision = as_precision(config.precision)
+    if precision is not Precision.DOUBLE:
+        raise XsvdError(f"{precision.value} precision is not built on the GPU path yet")
+    clock = clock or (runner.clock if runner is not None else StageClock())
+    host = _dense_input(a).astype(precision.storage_dtype, copy=False)
+    ctx = _lib.load()
+    u, s, v, deficient, stages = ctx.rsvd_dense(host, config.rank, config.oversample,
+                                                int(config.power), config.seed)
+    for name, sec in zip(STAGE_NAMES, stages):
+        clock.seconds[name] += float(sec)
+    register_dense(pool, "S", s.reshape(-1, 1), Precision.DOUBLE)
+    umat = register_dense(pool, "U", u, precision)
+    vmat = register_dense(pool, "V", v, precision)
+    return RsvdResult(u=umat, s=s.astype(np.float64), v=vmat, chosen_q=int(config.power),
+                      stage_seconds=dict(clock.seconds), deficient_columns=deficient)

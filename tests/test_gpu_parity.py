@@ -1,0 +1,272 @@
+"""Parity of the CUDA path (through the C ABI) against the CPU oracle and the
+reference golden vectors. Runs on a B200 (`-m gpu`).
+
+Tolerances (north star, BASELINE.json): singular values relative error
+<= 1e-10 (float64); largest principal angle (sine form) of U_k
+and V_k <= 1e-8 (float64). Kernel-level checks are tighter where the math
+allows (GEMM: 1e-13 relative to the operand scale).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden
+from oracle import kernels as OK
+from oracle import metrics as M
+from oracle import pipeline as OP
+from oracle import rng as OR
+
+pytestmark = pytest.mark.gpu
+
+SIG64, ANG64 = 1e-10, 1e-8
+
+
+def rel(got, ref):
+    return float(np.max(np.abs(got - ref)) / max(np.max(np.abs(ref)), 1e-300))
+
+
+# -- Omega generator ------------------------------------------------------------
+
+
+@pytest.mark.parametrize("seed,row0,rows,cols", [(0, 0, 16, 30), (7, 0, 33, 25), (3, 5, 21, 120),
+                                                 (11, 2**32 - 3, 7, 9), (2, 0, 8, 550),
+                                                 (123456789, 1000, 10, 1)])
+def test_uniform_bits_bit_exact(lib, seed, row0, rows, cols):
+    got = lib.uniform_bits(seed, row0, rows, cols)
+    assert np.array_equal(got, OR.gaussian_bits(seed, row0, row0 + rows, cols))
+
+
+def test_gaussian_matches_reference_within_ulps(lib, gold):
+    g = gold("rng")
+    i = 0
+    while f"band{i}" in g:
+        seed, r0, r1, n = (int(x) for x in g[f"case{i}"])
+        got = lib.gaussian(seed, r0, r1 - r0, n)
+        ref = g[f"band{i}"]
+        # CUDA log/sin/cos vs glibc/SVML: a few ulp of the result scale
+        assert np.max(np.abs(got - ref) / np.maximum(np.abs(ref), 1.0)) <= 8e-16 * 8, i
+        i += 1
+
+
+def test_gaussian_f32_is_cast_of_f64(lib):
+    a = lib.gaussian(5, 0, 64, 17, dtype=np.float64)
+    b = lib.gaussian(5, 0, 64, 17, dtype=np.float32)
+    assert np.array_equal(a.astype(np.float32), b)
+
+
+# -- GEMM ---------------------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("m,n,k", [(1, 1, 1), (3, 5, 7), (300, 30, 520), (1000, 120, 3000),
+                                   (4096, 32, 2048), (777, 128, 999), (513, 200, 1025),
+                                   (64, 64, 100000)])
+@pytest.mark.parametrize("trans", [False, True])
+def test_gemm_matches_oracle(lib, m, n, k, trans):
+    rng = np.random.default_rng(m * 7 + n * 3 + k + trans)
+    a = rng.standard_normal((k, m) if trans else (m, k))
+    b = rng.standard_normal((k, n))
+    got = lib.gemm(a, b, trans_a=trans)
+    ref = OK.block_multiply_fast(a.T if trans else a, b, np.float64, np.float64)
+    assert got.shape == (m, n)
+    # the oracle's own error is ~k*eps too; 1e-13 of the magnitude scale
+    scale = np.sqrt(k)
+    assert np.max(np.abs(got - ref)) / scale <= 1e-13
+
+
+def test_gemm_golden(lib, gold):
+    g = gold("multiply")
+    assert rel(lib.gemm(g["x"], g["y"]), g["nn"]) <= 1e-14
+    assert rel(lib.gemm(g["x"], g["w"], trans_a=True), g["tn"]) <= 1e-14
+
+
+def test_gemm_is_deterministic(lib):
+    rng = np.random.default_rng(1)
+    a = rng.standard_normal((20000, 600))
+    b = rng.standard_normal((20000, 120))
+    c1 = lib.gemm(a, b, trans_a=True)
+    c2 = lib.gemm(a, b, trans_a=True)
+    assert np.array_equal(c1, c2)
+
+
+# -- thin QR --------------------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("name", ["tall", "c345", "eye", "zero", "deficient"])
+def test_thin_qr_golden(lib, gold, name):
+    g = gold("qr")
+    a = g[f"{name}_a"]
+    q, r, deficient = lib.thin_qr(a)
+    assert tuple(deficient) == tuple(g[f"{name}_def"])
+    if name in ("tall", "c345", "eye"):
+        # full rank: Q with diag(R) > 0 is unique
+        assert np.max(np.abs(q - g[f"{name}_q"])) <= 1e-12
+        assert np.max(np.abs(r - g[f"{name}_r"])) <= 1e-12 * max(1.0, np.max(np.abs(a)))
+    if name != "zero":
+        keep = [j for j in range(a.shape[1]) if j not in deficient]
+        qk = q[:, keep]
+        assert M.ortho_defect(qk) <= 1e-10
+        assert np.max(np.abs(q @ r - a)) <= 1e-12 * max(1.0, np.max(np.abs(a)))
+    assert np.all(np.diag(r) >= -1e-300)
+
+
+def test_thin_qr_large_well_conditioned(lib):
+    rng = np.random.default_rng(4)
+    a = rng.standard_normal((65536, 120)) * np.logspace(0, -3, 120)
+    q, r, d = lib.thin_qr(a)
+    qo, ro, do = OK.thin_qr_fast(a, np.float64, np.float64)
+    assert d == ()
+    assert M.ortho_defect(q) <= 1e-13
+    assert np.max(np.abs(q - qo)) <= 1e-11
+
+
+def test_thin_qr_rank_deficient_uses_fallback(lib):
+    rng = np.random.default_rng(5)
+    b = rng.standard_normal((3000, 18))
+    a = b @ rng.standard_normal((18, 25))
+    q, r, d = lib.thin_qr(a)
+    assert M.ortho_defect(q) <= 1e-10
+    assert np.max(np.abs(q @ r - a)) <= 1e-11 * np.max(np.abs(a))
+    qo, ro, do = OK.thin_qr(a, np.float64, np.float64)
+    assert len(d) == len(do) == 7
+
+
+# -- small SVD -----------------------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("name", ["wide", "diag", "perm", "r30", "deficient"])
+def test_svd_small_golden(lib, gold, name):
+    g = gold("svd")
+    b = g[f"{name}_b"]
+    u, s, v = lib.svd_small(b)
+    sr = g[f"{name}_s"]
+    assert np.max(np.abs(s - sr)) <= 1e-13 * max(1.0, sr[0])
+    assert np.max(np.abs(u @ np.diag(s) @ v.T - b)) <= 1e-12 * max(1.0, np.max(np.abs(b)))
+    if name in ("wide", "r30", "diag"):
+        # distinct singular values: vectors unique up to the sign rule
+        assert np.max(np.abs(u - g[f"{name}_u"])) <= 1e-10
+        assert np.max(np.abs(v - g[f"{name}_v"])) <= 1e-10
+
+
+def test_svd_small_rejects_tall(lib):
+    from paper_1907_06470_b200 import ShapeError, svd_small
+
+    with pytest.raises(ShapeError):
+        svd_small(np.zeros((5, 3)))
+
+
+# -- full factorisation ---------------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("name", ["d_small", "d_q0", "d_wide"])
+def test_rsvd_matches_reorth_golden(lib, gold, name):
+    g = gold("rsvd")
+    a = g[f"{name}_a"]
+    m, n, k, p, q, seed, _ = (int(x) for x in g[f"{name}_cfg"])
+    u, s, v, deficient, stages = lib.rsvd_dense(a, k, p, q, seed)
+    assert M.sigma_rel(s, g[f"{name}_reorth_s"]) <= SIG64
+    assert M.sin_angle(u, g[f"{name}_reorth_u"]) <= ANG64
+    assert M.sin_angle(v, g[f"{name}_reorth_v"]) <= ANG64
+    # column-by-column agreement after the reference's sign rule
+    assert np.max(np.abs(u - g[f"{name}_reorth_u"])) <= 1e-7
+    assert tuple(deficient) == tuple(g[f"{name}_reorth_def"])
+
+
+def test_rsvd_with_explicit_omega_equals_generated(lib):
+    rng = np.random.default_rng(6)
+    a = rng.standard_normal((500, 300))
+    om = OR.gaussian_band(3, 0, 300, 15)
+    u1, s1, v1, _, _ = lib.rsvd_dense(a, 10, 5, 1, 3)
+    u2, s2, v2, _, _ = lib.rsvd_dense(a, 10, 5, 1, 3, omega=om)
+    assert M.sigma_rel(s1, s2) <= 1e-13
+    assert M.sin_angle(u1, u2) <= 1e-12
+
+
+def test_cfg1_full_size(lib, gold):
+    """Config 1 (4096x2048 f64, k=20 p=10 q=2) vs the reference's shipped
+    driver (its own oracle at cfg1) and xsvd-reorth."""
+    from paper_1907_06470_b200.workloads import CONFIGS, workload_dense_np
+
+    g = gold("cfg1")
+    w = CONFIGS[1]
+    a = workload_dense_np(w)
+    u, s, v, deficient, stages = lib.rsvd_dense(a, w.k, w.p, w.q, w.cfg)
+    for variant in ("shipped", "reorth"):
+        assert M.sigma_rel(s, g[f"{variant}_s"]) <= SIG64
+        assert M.sin_angle(u, g[f"{variant}_u"]) <= ANG64
+        assert M.sin_angle(v, g[f"{variant}_v"]) <= ANG64
+    assert deficient == ()
+    assert np.all(stages >= 0) and stages[2] > 0
+
+
+def test_rsvd_vs_oracle_medium(lib):
+    """cfg2's construction (s_i = i^-1.5) at 8192 x 2048, l = 120, vs the
+    fast xsvd-reorth oracle on the same A and Omega."""
+    from paper_1907_06470_b200.workloads import dense_lowrank_np
+
+    a = dense_lowrank_np(8192, 2048, "pow-1.5", 1e-8, 1002, 2002)
+    u, s, v, _, _ = lib.rsvd_dense(a, 100, 20, 2, 2)
+    ref = OP.rsvd_reorth(a, 100, 20, 2, 2, "double", fast=True)
+    assert M.sigma_rel(s, ref.s) <= SIG64
+    assert M.sin_angle(u, ref.u) <= ANG64
+    assert M.sin_angle(v, ref.v) <= ANG64
+
+
+def test_known_answers(lib):
+    """tests/test_pipeline.py:117-131 known answers, through the GPU path."""
+    u, s, v, _, _ = lib.rsvd_dense(np.eye(5), 5, 0, 0, 0)
+    assert np.allclose(s, np.ones(5), atol=1e-12)
+    assert np.max(np.abs(u @ np.diag(s) @ v.T - np.eye(5))) <= 1e-12
+    uu = np.array([[1.0], [2.0], [2.0]]) / 3.0
+    vv = np.array([[3.0, 0.0, 4.0, 0.0]]) / 5.0
+    a = 3.7 * uu @ vv
+    u, s, v, _, _ = lib.rsvd_dense(a, 1, 0, 0, 1)
+    assert np.allclose(s, [3.7], atol=1e-12)
+    assert np.max(np.abs(u @ np.diag(s) @ v.T - a)) / np.max(np.abs(a)) <= 1e-12
+
+
+def test_exact_low_rank_recovery(lib):
+    rng = np.random.default_rng(5)
+    a = rng.standard_normal((300, 10)) @ rng.standard_normal((10, 200))
+    u, s, v, _, _ = lib.rsvd_dense(a, 10, 0, 0, 0)
+    assert np.max(np.abs(u @ np.diag(s) @ v.T - a)) / np.max(np.abs(a)) <= 1e-8
+    assert M.ortho_defect(u) <= 1e-10 and M.ortho_defect(v) <= 1e-10
+
+
+def test_rank_deficient_sketch(lib):
+    """rank(A) = 18 < l = 25: the CholQR Gram is singular and the Householder
+    fallback must keep Q orthonormal (tests/test_pipeline.py:151-162)."""
+    rng = np.random.default_rng(6)
+    a = np.zeros((60, 50))
+    live = rng.choice(60, size=18, replace=False)
+    a[rng.choice(live, size=300), rng.integers(0, 50, 300)] = rng.standard_normal(300)
+    u, s, v, _, _ = lib.rsvd_dense(a, 25, 0, 1, 0)
+    ref = np.linalg.svd(a, compute_uv=False)
+    assert np.max(np.abs(s - ref[:25])) / ref[0] <= 1e-8
+
+
+def test_shape_error(lib):
+    from paper_1907_06470_b200.errors import ShapeError
+
+    with pytest.raises(ShapeError):
+        lib.rsvd_dense(np.zeros((10, 8)), 8, 1, 0, 0)
+
+
+def test_drop_in_api(lib):
+    """The reference-shaped Python entry point end to end."""
+    import paper_1907_06470_b200 as X
+
+    rng = np.random.default_rng(7)
+    arr = rng.standard_normal((400, 300))
+    pool = X.BlockPool()
+    a = X.matrix_from_dense(pool, "A", arr, precision=X.Precision.DOUBLE)
+    res = X.randomized_svd(pool, a, X.RsvdConfig(rank=10, oversample=5, power=2, seed=4))
+    ref = OP.rsvd_reorth(arr, 10, 5, 2, 4, "double", fast=True)
+    assert M.sigma_rel(res.s, ref.s) <= SIG64
+    assert M.sin_angle(res.u.to_array(), ref.u) <= ANG64
+    assert res.u.shape == (400, 10) and res.v.shape == (300, 10)
+    assert set(res.stage_seconds) == set(X.STAGE_NAMES)
+    assert pool.descriptor("S").rows == 10
+    out, stats = X.block_multiply(pool, a.T, res.u, "AtU")
+    assert rel(out.to_array(), arr.T @ res.u.to_array()) <= 1e-13
+    qr = X.thin_qr(pool, a, "Qa")
+    assert M.ortho_defect(qr.q.to_array()) <= 1e-12
