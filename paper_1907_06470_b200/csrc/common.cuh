@@ -103,6 +103,11 @@ void launch_jacobi_svd(const double* R, int64_t ldr, int l, int k, double* Ub, i
                        double* s, double* Wk, int64_t ldw, double* work, int* status,
                        cudaStream_t st);
 
+// Opt-in dynamic shared memory per block on the current device.
+size_t max_dyn_smem();
+// Global scratch (doubles) launch_jacobi_svd needs in `work` for l.
+size_t jacobi_work_doubles(int l);
+
 // FP64 pipe peaks (TFLOP/s) from saturating microbenchmarks (peak.cu).
 void measure_fp64_peaks(cudaStream_t st, double* dmma_tflops, double* dfma_tflops);
 

@@ -20,6 +20,7 @@
 // doubles, which makes the per-lane 8-byte fragment loads of m8n8k4
 // (row = lane>>2, col = lane&3 patterns) bank-conflict free.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -226,15 +227,39 @@ __global__ void split_reduce_kernel(const double* __restrict__ work, int64_t M, 
   }
 }
 
+// Many slices, few outputs (the CholQR Gram: l x l outputs, ~300 slices):
+// a block owns 32 consecutive outputs, its 8 warps stride the slices, and
+// warp partials are combined in warp order — a fixed order, deterministic.
+__global__ void __launch_bounds__(256) split_reduce_wide_kernel(
+    const double* __restrict__ work, int64_t M, int64_t N, int64_t ldw, int64_t stride, int S,
+    double* __restrict__ C, int64_t ldc) {
+  __shared__ double part[8][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t idx = (int64_t)blockIdx.x * 32 + lane;
+  const int64_t total = M * N;
+  double acc = 0.0;
+  int64_t r = 0, c = 0;
+  if (idx < total) {
+    r = idx / N;
+    c = idx - r * N;
+    const double* p = work + r * ldw + c;
+    for (int s = warp; s < S; s += 8) acc += p[(int64_t)s * stride];
+  }
+  part[warp][lane] = acc;
+  __syncthreads();
+  if (warp == 0 && idx < total) {
+    double sum = part[0][lane];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) sum += part[w][lane];
+    C[r * ldc + c] = sum;
+  }
+}
+
 }  // namespace
 
 // ---- dispatch ----------------------------------------------------------------
 
 namespace {
-
-struct Shape {
-  int BM, BN;
-};
 
 template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, bool TRANS_A>
 void run_cfg(const DGemmArgs& g, int splits, int64_t k_per_split, double* out, int64_t ldo,
@@ -271,31 +296,55 @@ int pick_bn(int64_t N) {
   return 128;
 }
 
-constexpr int kBM = 128;
-constexpr int kBK = 16;
+// Tile variants. The l = 120 products over A (cfg2's hot shape) have
+// alternatives selectable with XB_DGEMM_VARIANT for tuning runs; everything
+// else uses variant 0.
+struct Variant {
+  int id, BM, BK, ctas_per_sm;
+};
 
-int64_t kper(int64_t K, int splits) { return round_up(ceil_div(K, splits), kBK); }
+Variant pick_variant(const DGemmArgs& g) {
+  const int bn = pick_bn(g.N);
+  int v = 0;
+  if (bn == 120 && g.K >= 4096) {
+    static const int env = [] {
+      const char* e = getenv("XB_DGEMM_VARIANT");
+      return e ? atoi(e) : -1;
+    }();
+    v = env >= 0 ? env : 0;
+  }
+  switch (v) {
+    case 1: return {1, 128, 32, 1};
+    case 2: return {2, 64, 16, 2};
+    case 3: return {3, 128, 16, 1};
+    default: return {0, 128, 16, 1};
+  }
+}
+
+int64_t kper(int64_t K, int splits, int bk) { return round_up(ceil_div(K, splits), bk); }
 
 }  // namespace
 
 int dgemm_plan_splits(const DGemmArgs& g) {
-  const int64_t tiles = ceil_div(g.M, kBM) * ceil_div(g.N, pick_bn(g.N));
-  const int64_t kt = ceil_div(g.K, kBK);
-  // Fill the machine: aim for >= ~6 waves of 148 single-CTA SMs, but keep
-  // at least 8 k-tiles per slice so the pipeline has something to hide.
+  const Variant var = pick_variant(g);
+  const int64_t tiles = ceil_div(g.M, var.BM) * ceil_div(g.N, pick_bn(g.N));
+  const int64_t kt = ceil_div(g.K, var.BK);
+  const int64_t slots = (int64_t)kNumSMs * var.ctas_per_sm;
+  // Fill the machine: aim for >= ~6 waves, but keep at least 8 k-tiles per
+  // slice so the pipeline has something to hide.
   int best = 1;
   double best_eff = 0.0;
   for (int s = 1; s <= 256; ++s) {
     if (kt / s < 8 && s > 1) break;
     const int64_t ctas = tiles * s;
-    const int64_t waves = ceil_div(ctas, kNumSMs);
-    const double eff = (double)ctas / (double)(waves * kNumSMs);
+    const int64_t waves = ceil_div(ctas, slots);
+    const double eff = (double)ctas / (double)(waves * slots);
     // prefer fewer slices unless the wave efficiency improves materially
     if (eff > best_eff + 0.03) {
       best_eff = eff;
       best = s;
     }
-    if (ctas >= 6 * kNumSMs && eff > 0.95) break;
+    if (ctas >= 6 * slots && eff > 0.95) break;
   }
   // Tiny outputs (Gram: one tile) need many slices to use the machine.
   if (tiles <= 4) best = (int)std::min<int64_t>(std::max<int64_t>(1, kt / 8), 2 * kNumSMs / tiles);
@@ -314,8 +363,9 @@ void dgemm(const DGemmArgs& g, int splits, double* work, cudaStream_t st) {
       XB_CUDA(cudaMemsetAsync(g.C + r * g.ldc, 0, g.N * sizeof(double), st));
     return;
   }
-  splits = std::max(1, std::min<int>(splits, (int)ceil_div(g.K, kBK)));
-  const int64_t kps = kper(g.K, splits);
+  const Variant var = pick_variant(g);
+  splits = std::max(1, std::min<int>(splits, (int)ceil_div(g.K, var.BK)));
+  const int64_t kps = kper(g.K, splits, var.BK);
   splits = (int)ceil_div(g.K, kps);
   double* out = g.C;
   int64_t ldo = g.ldc, stride = 0;
@@ -327,24 +377,45 @@ void dgemm(const DGemmArgs& g, int splits, double* work, cudaStream_t st) {
   }
   const int bn = pick_bn(g.N);
   if (g.trans_a) {
-    switch (bn) {
-      case 32: run_cfg<kBM, 32, kBK, 4, 1, 4, true>(g, splits, kps, out, ldo, stride, st); break;
-      case 64: run_cfg<kBM, 64, kBK, 4, 2, 4, true>(g, splits, kps, out, ldo, stride, st); break;
-      case 120: run_cfg<kBM, 120, kBK, 4, 3, 4, true>(g, splits, kps, out, ldo, stride, st); break;
-      default: run_cfg<kBM, 128, kBK, 4, 4, 4, true>(g, splits, kps, out, ldo, stride, st); break;
+    if (bn == 120) {
+      switch (var.id) {
+        case 1: run_cfg<128, 120, 32, 4, 3, 3, true>(g, splits, kps, out, ldo, stride, st); break;
+        case 2: run_cfg<64, 120, 16, 2, 3, 4, true>(g, splits, kps, out, ldo, stride, st); break;
+        case 3: run_cfg<128, 120, 16, 2, 3, 4, true>(g, splits, kps, out, ldo, stride, st); break;
+        default: run_cfg<128, 120, 16, 4, 3, 4, true>(g, splits, kps, out, ldo, stride, st); break;
+      }
+    } else {
+      switch (bn) {
+        case 32: run_cfg<128, 32, 16, 4, 1, 4, true>(g, splits, kps, out, ldo, stride, st); break;
+        case 64: run_cfg<128, 64, 16, 4, 2, 4, true>(g, splits, kps, out, ldo, stride, st); break;
+        default: run_cfg<128, 128, 16, 4, 4, 4, true>(g, splits, kps, out, ldo, stride, st); break;
+      }
     }
   } else {
-    switch (bn) {
-      case 32: run_cfg<kBM, 32, kBK, 4, 1, 4, false>(g, splits, kps, out, ldo, stride, st); break;
-      case 64: run_cfg<kBM, 64, kBK, 4, 2, 4, false>(g, splits, kps, out, ldo, stride, st); break;
-      case 120: run_cfg<kBM, 120, kBK, 4, 3, 4, false>(g, splits, kps, out, ldo, stride, st); break;
-      default: run_cfg<kBM, 128, kBK, 4, 4, 4, false>(g, splits, kps, out, ldo, stride, st); break;
+    if (bn == 120) {
+      switch (var.id) {
+        case 1: run_cfg<128, 120, 32, 4, 3, 3, false>(g, splits, kps, out, ldo, stride, st); break;
+        case 2: run_cfg<64, 120, 16, 2, 3, 4, false>(g, splits, kps, out, ldo, stride, st); break;
+        case 3: run_cfg<128, 120, 16, 2, 3, 4, false>(g, splits, kps, out, ldo, stride, st); break;
+        default: run_cfg<128, 120, 16, 4, 3, 4, false>(g, splits, kps, out, ldo, stride, st); break;
+      }
+    } else {
+      switch (bn) {
+        case 32: run_cfg<128, 32, 16, 4, 1, 4, false>(g, splits, kps, out, ldo, stride, st); break;
+        case 64: run_cfg<128, 64, 16, 4, 2, 4, false>(g, splits, kps, out, ldo, stride, st); break;
+        default: run_cfg<128, 128, 16, 4, 4, 4, false>(g, splits, kps, out, ldo, stride, st); break;
+      }
     }
   }
   if (splits > 1) {
     const int64_t total = g.M * g.N;
-    int blocks = (int)std::min<int64_t>(ceil_div(total, 256), kNumSMs * 8);
-    split_reduce_kernel<<<blocks, 256, 0, st>>>(work, g.M, g.N, ldo, stride, splits, g.C, g.ldc);
+    if (splits >= 16) {
+      split_reduce_wide_kernel<<<(unsigned)ceil_div(total, 32), 256, 0, st>>>(
+          work, g.M, g.N, ldo, stride, splits, g.C, g.ldc);
+    } else {
+      int blocks = (int)std::min<int64_t>(ceil_div(total, 256), kNumSMs * 8);
+      split_reduce_kernel<<<blocks, 256, 0, st>>>(work, g.M, g.N, ldo, stride, splits, g.C, g.ldc);
+    }
     check_launch("split_reduce");
   }
 }

@@ -297,7 +297,7 @@ void rsvd_f64(xb_ctx* c, int64_t m, int64_t n, double* dA, int64_t lda, const do
   double* Ub = c->dbuf("Ub", (size_t)lp * lp);
   double* Wk = c->dbuf("Wk", (size_t)lp * kp);
   double* sv = c->dbuf("sv", (size_t)lp);
-  double* jw = c->dbuf("jw", (size_t)lp * lp);
+  double* jw = c->dbuf("jw", jacobi_work_doubles(lp));
   int* jstat = c->ibuf("jstat", 4);
   int* defc = c->ibuf("defc", (size_t)lp + 4);
   // pre-size the split-K workspace for the largest product so no cudaMalloc
@@ -696,7 +696,7 @@ int xb_svd_small(xb_ctx* c, int64_t r, int64_t n, const double* B, int64_t ldb, 
     double* dW = c->dbuf("svW", (size_t)lp * lp);
     double* ds = c->dbuf("svs", (size_t)lp);
     double* dV = c->dbuf("svV", (size_t)n * l);
-    double* jw = c->dbuf("jw", (size_t)lp * lp);
+    double* jw = c->dbuf("jw", jacobi_work_doubles(lp));
     int* jstat = c->ibuf("jstat", 4);
     c->dbuf("hh_work", (size_t)2 * n * l);
     XB_CUDA(cudaMemcpy2DAsync(dB, n * 8, B, ldb * 8, n * 8, r, cudaMemcpyHostToDevice, c->st));

@@ -1,0 +1,282 @@
+// l x l kernels of the hot path (single CTA, latency-bound, l <= ~160 in
+// shared memory, larger l from an L2-resident global scratch).
+//
+//  chol_inv  G = R^T R (upper R, f64) and R^{-1}: the small step of CholQR2,
+//            which replaces the reference's Householder thin_qr
+//            (kernels.py:297-351). Right-looking, unscaled Schur updates with
+//            ONE barrier per column; triangular inverse column by column
+//            (LAPACK dtrti2 order) with warp-level dot products.
+//  jacobi    one-sided Hestenes Jacobi SVD of M = R_B^T, replacing the
+//            Golub-Kahan svd_small (kernels.py:542-562) on the projected
+//            factor. Round-robin (circle) ordering: every round rotates l/2
+//            disjoint column pairs in parallel, one 16-lane group per pair;
+//            M's columns and the accumulated right rotations J both live in
+//            shared memory when they fit. Output sorted descending (stable,
+//            kernels.py:535) with the sign rule of kernels.py:556-561.
+#include <cfloat>
+
+#include "common.cuh"
+
+namespace xb {
+namespace {
+
+constexpr int kThreads = 1024;
+constexpr int kWarps = kThreads / 32;
+
+__device__ __forceinline__ double warp_sum32(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads, 1)
+    chol_inv_kernel(const double* __restrict__ G, int64_t ldg, int l, double tau,
+                    double* __restrict__ R, double* __restrict__ Rinv, int64_t ldr,
+                    int* __restrict__ flag, double* gw, int use_smem) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ double diag0[1024];
+  __shared__ double pivs[1024];
+  __shared__ double tmp[1024];
+  double* W = use_smem ? sm : gw;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // load the upper triangle (row-major, stride l)
+  for (int i = warp; i < l; i += kWarps)
+    for (int c = lane; c < l; c += 32) W[(int64_t)i * l + c] = (c >= i) ? G[(int64_t)i * ldg + c] : 0.0;
+  for (int j = tid; j < l; j += kThreads) diag0[j] = G[(int64_t)j * ldg + j];
+  __syncthreads();
+  // Cholesky: unscaled right-looking elimination, one barrier per column.
+  bool failed = false;
+  for (int j = 0; j < l; ++j) {
+    const double piv = W[(int64_t)j * l + j];
+    const bool ok = (piv > tau * diag0[j]) && (piv > 0.0);
+    const double pe = ok ? piv : fmax(fabs(diag0[j]), DBL_MIN);  // keep going; result discarded
+    failed |= !ok;
+    if (tid == 0) pivs[j] = pe;
+    const double inv = 1.0 / pe;
+    const double* rowj = W + (int64_t)j * l;
+    for (int i = j + 1 + warp; i < l; i += kWarps) {
+      const double f = rowj[i] * inv;
+      double* rowi = W + (int64_t)i * l;
+      for (int c = i + lane; c < l; c += 32) rowi[c] -= f * rowj[c];
+    }
+    __syncthreads();
+  }
+  if (failed && tid == 0) *flag = 1;
+  // scale rows: R[j][c] = W[j][c] / sqrt(piv_j)
+  for (int j = warp; j < l; j += kWarps) {
+    const double rs = 1.0 / sqrt(pivs[j]);
+    for (int c = lane; c < l; c += 32) {
+      const double v = (c >= j) ? W[(int64_t)j * l + c] * rs : 0.0;
+      W[(int64_t)j * l + c] = v;
+      R[(int64_t)j * ldr + c] = v;
+    }
+  }
+  __syncthreads();
+  for (int j = tid; j < l; j += kThreads) pivs[j] = W[(int64_t)j * l + j];  // R's diagonal
+  __syncthreads();
+  // In-place upper-triangular inverse, column by column (dtrti2 order):
+  // X[0:j, j] = -X[0:j, 0:j] R[0:j, j] / R[j][j], X[j][j] = 1 / R[j][j].
+  // Column j reads only X[:, <j] and R[<j, j], so W[j][j] may be replaced
+  // in the same step.
+  for (int j = 0; j < l; ++j) {
+    for (int i = warp; i < j; i += kWarps) {
+      double acc = 0.0;
+      for (int p = i + lane; p < j; p += 32) acc += W[(int64_t)i * l + p] * W[(int64_t)p * l + j];
+      acc = warp_sum32(acc);
+      if (lane == 0) tmp[i] = acc;
+    }
+    __syncthreads();
+    const double ajj = 1.0 / pivs[j];
+    for (int i = tid; i < j; i += kThreads) W[(int64_t)i * l + j] = -tmp[i] * ajj;
+    if (tid == 0) W[(int64_t)j * l + j] = ajj;
+    __syncthreads();
+  }
+  for (int i = warp; i < l; i += kWarps)
+    for (int c = lane; c < l; c += 32) Rinv[(int64_t)i * ldr + c] = (c >= i) ? W[(int64_t)i * l + c] : 0.0;
+}
+
+// ---------------------------------------------------------------------------
+// Jacobi. X (l x l, column-major: X[c*l + r]) = M = R^T, i.e. X[:, c] = R[c, :].
+// J (column-major) in shared memory (j_in_smem) or global `gj`.
+constexpr int kGroup = 16;                    // lanes per column pair
+constexpr int kGroups = kThreads / kGroup;    // 64 pairs in flight per round
+
+__device__ __forceinline__ void group_sum3(double& a, double& b, double& c) {
+#pragma unroll
+  for (int o = kGroup / 2; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+    c += __shfl_xor_sync(0xffffffffu, c, o);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    jacobi_kernel(const double* __restrict__ Rm, int64_t ldr, int l, int k, double* __restrict__ Ub,
+                  int64_t ldu, double* __restrict__ s_out, double* __restrict__ Wk, int64_t ldw,
+                  double* __restrict__ work, int* __restrict__ status, int j_in_smem, double tol,
+                  int max_sweeps) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ int s_rot;
+  const int64_t ll = (int64_t)l * l;
+  double* X = sm;
+  double* J = j_in_smem ? sm + ll : work;
+  // scratch after J in global: norms, perm, sign
+  double* gnorm = work + ll;
+  int* gperm = reinterpret_cast<int*>(gnorm + l);
+  int* gsign = gperm + l;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int grp = tid / kGroup, gl = tid % kGroup;
+  for (int c = warp; c < l; c += kWarps)
+    for (int r = lane; r < l; r += 32) {
+      X[(int64_t)c * l + r] = Rm[(int64_t)c * ldr + r];
+      J[(int64_t)c * l + r] = (r == c) ? 1.0 : 0.0;
+    }
+  __syncthreads();
+  const int L2 = l + (l & 1);
+  const int npairs = L2 / 2;
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    if (tid == 0) s_rot = 0;
+    __syncthreads();
+    for (int round = 0; round < L2 - 1; ++round) {
+      for (int pi = grp; pi < npairs; pi += kGroups) {
+        const int pa = pi, pb = L2 - 1 - pi;  // circle method: position 0 fixed
+        int p = pa == 0 ? 0 : 1 + (pa - 1 + round) % (L2 - 1);
+        int q = 1 + (pb - 1 + round) % (L2 - 1);
+        if (p > q) {
+          const int t = p;
+          p = q;
+          q = t;
+        }
+        if (q >= l) continue;  // dummy player when l is odd
+        double* xp = X + (int64_t)p * l;
+        double* xq = X + (int64_t)q * l;
+        double a = 0.0, b = 0.0, g = 0.0;
+        for (int r = gl; r < l; r += kGroup) {
+          const double u = xp[r], v = xq[r];
+          a = fma(u, u, a);
+          b = fma(v, v, b);
+          g = fma(u, v, g);
+        }
+        group_sum3(a, b, g);
+        if (g != 0.0 && fabs(g) > tol * sqrt(a * b)) {
+          const double zeta = (b - a) / (2.0 * g);
+          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          const double cs = 1.0 / sqrt(1.0 + t * t);
+          const double sn = cs * t;
+          for (int r = gl; r < l; r += kGroup) {
+            const double u = xp[r], v = xq[r];
+            xp[r] = cs * u - sn * v;
+            xq[r] = sn * u + cs * v;
+          }
+          double* jp = J + (int64_t)p * l;
+          double* jq = J + (int64_t)q * l;
+          for (int r = gl; r < l; r += kGroup) {
+            const double u = jp[r], v = jq[r];
+            jp[r] = cs * u - sn * v;
+            jq[r] = sn * u + cs * v;
+          }
+          if (gl == 0) s_rot = 1;
+        }
+      }
+      __syncthreads();
+    }
+    const int rotated = s_rot;
+    __syncthreads();
+    if (!rotated) break;
+  }
+  if (tid == 0) *status = (sweep >= max_sweeps) ? 1 : 0;
+  // singular values = column norms
+  for (int c = warp; c < l; c += kWarps) {
+    double a = 0.0;
+    for (int r = lane; r < l; r += 32) a += X[(int64_t)c * l + r] * X[(int64_t)c * l + r];
+    a = warp_sum32(a);
+    if (lane == 0) gnorm[c] = sqrt(a);
+  }
+  __syncthreads();
+  // stable descending order: rank = #{i: s_i > s_j} + #{i < j: s_i == s_j}
+  for (int j = tid; j < l; j += kThreads) {
+    const double sj = gnorm[j];
+    int rank = 0;
+    for (int i = 0; i < l; ++i) {
+      const double si = gnorm[i];
+      rank += (si > sj) || (si == sj && i < j);
+    }
+    gperm[rank] = j;
+  }
+  __syncthreads();
+  // sign rule on U_B columns: largest |entry| positive, earliest row on ties
+  for (int i = warp; i < l; i += kWarps) {
+    const int c = gperm[i];
+    double best = -1.0;
+    int brow = 0;
+    for (int r = lane; r < l; r += 32) {
+      const double v = fabs(X[(int64_t)c * l + r]);
+      if (v > best) {
+        best = v;
+        brow = r;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int orow = __shfl_xor_sync(0xffffffffu, brow, o);
+      if (ob > best || (ob == best && orow < brow)) {
+        best = ob;
+        brow = orow;
+      }
+    }
+    if (lane == 0) gsign[i] = (X[(int64_t)c * l + brow] < 0.0) ? -1 : 1;
+  }
+  __syncthreads();
+  for (int i = tid; i < l; i += kThreads) s_out[i] = gnorm[gperm[i]];
+  for (int r = warp; r < l; r += kWarps)
+    for (int i = lane; i < l; i += 32) {
+      const int c = gperm[i];
+      const double sc = gnorm[c];
+      const double inv = sc > 0.0 ? 1.0 / sc : 0.0;
+      Ub[(int64_t)r * ldu + i] = gsign[i] * X[(int64_t)c * l + r] * inv;
+    }
+  for (int r = warp; r < l; r += kWarps)
+    for (int i = lane; i < k; i += 32) Wk[(int64_t)r * ldw + i] = gsign[i] * J[(int64_t)gperm[i] * l + r];
+}
+
+}  // namespace
+
+void launch_chol_inv(const double* G, int64_t ldg, int l, double tau, double* R, double* Rinv,
+                     int64_t ldr, int* flag, cudaStream_t st) {
+  XB_REQUIRE(l <= 1024, XB_EUNSUPPORTED, "chol_inv: l > 1024");
+  const size_t bytes = (size_t)l * l * sizeof(double);
+  const int use_smem = bytes + 26 * 1024 <= max_dyn_smem();
+  double* gw = nullptr;
+  if (!use_smem) XB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&gw), bytes, st));
+  const size_t dyn = use_smem ? bytes : 0;
+  XB_CUDA(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)dyn));
+  chol_inv_kernel<<<1, kThreads, dyn, st>>>(G, ldg, l, tau, R, Rinv, ldr, flag, gw, use_smem);
+  check_launch("chol_inv");
+  if (gw) XB_CUDA(cudaFreeAsync(gw, st));
+}
+
+size_t jacobi_work_doubles(int l) { return (size_t)l * l + 2 * (size_t)l + 8; }
+
+void launch_jacobi_svd(const double* R, int64_t ldr, int l, int k, double* Ub, int64_t ldu,
+                       double* s, double* Wk, int64_t ldw, double* work, int* status,
+                       cudaStream_t st) {
+  XB_REQUIRE(l <= 1024, XB_EUNSUPPORTED, "jacobi_svd: l > 1024");
+  const size_t lim = max_dyn_smem() - 512;  // static: s_rot
+  const size_t one = (size_t)l * l * sizeof(double);
+  XB_REQUIRE(one <= lim, XB_EUNSUPPORTED,
+             "jacobi_svd: l x l factor exceeds shared memory (multi-CTA Jacobi not built yet)");
+  const int j_in_smem = 2 * one <= lim;
+  const size_t dyn = j_in_smem ? 2 * one : one;
+  XB_CUDA(cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)dyn));
+  const double tol = fmax(1e-15, (double)l * DBL_EPSILON);
+  jacobi_kernel<<<1, kThreads, dyn, st>>>(R, ldr, l, k, Ub, ldu, s, Wk, ldw, work, status,
+                                          j_in_smem, tol, 60);
+  check_launch("jacobi_svd");
+}
+
+}  // namespace xb
