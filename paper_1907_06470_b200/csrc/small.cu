@@ -102,12 +102,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 constexpr int kGroup = 16;                    // lanes per column pair
 constexpr int kGroups = kThreads / kGroup;    // 64 pairs in flight per round
 
+// Sum over the 16 lanes of this half-warp. The mask names only this half:
+// the other half may be idle (odd l, dummy pair) or on a different pair.
 __device__ __forceinline__ void group_sum3(double& a, double& b, double& c) {
+  const unsigned mask = (threadIdx.x & 16) ? 0xffff0000u : 0x0000ffffu;
 #pragma unroll
   for (int o = kGroup / 2; o > 0; o >>= 1) {
-    a += __shfl_xor_sync(0xffffffffu, a, o);
-    b += __shfl_xor_sync(0xffffffffu, b, o);
-    c += __shfl_xor_sync(0xffffffffu, c, o);
+    a += __shfl_xor_sync(mask, a, o);
+    b += __shfl_xor_sync(mask, b, o);
+    c += __shfl_xor_sync(mask, c, o);
   }
 }
 
