@@ -20,6 +20,8 @@
 // Everything after A lands in HBM runs on the device with no host round
 // trip; stage times come from CUDA events on the compute stream.
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <cfloat>
 #include <cstring>
 #include <map>
@@ -100,6 +102,10 @@ struct xb_ctx {
 namespace {
 
 thread_local std::string g_last_error;
+
+double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
 
 struct LaunchScope {
   int64_t* prev;
@@ -555,15 +561,21 @@ int xb_rsvd_dense(xb_ctx* c, int dtype, int64_t m, int64_t n, const void* A, int
     rows = std::min(rows, std::max<int64_t>(256, round_up(ceil_div(m, 8), 128)));
     ing.chunk_rows = std::min(rows, m);
     RsvdOut out{dU, k, ds, dV, k};
+    const double t0 = now_s();
     rsvd_f64(c, m, n, dA, n, dO, l, seed, k, p, q, out, deficient, ndeficient, stage_seconds, ing);
+    const double t1 = now_s();
     HostRegistration ru(U, (size_t)((m - 1) * ldu + k) * sizeof(double));
     HostRegistration rv(V, (size_t)((n - 1) * ldv + k) * sizeof(double));
+    const double t2 = now_s();
     XB_CUDA(cudaMemcpy2DAsync(U, ldu * sizeof(double), dU, k * sizeof(double), k * sizeof(double),
                               m, cudaMemcpyDeviceToHost, c->st));
     XB_CUDA(cudaMemcpy2DAsync(V, ldv * sizeof(double), dV, k * sizeof(double), k * sizeof(double),
                               n, cudaMemcpyDeviceToHost, c->st));
     XB_CUDA(cudaMemcpyAsync(s, ds, k * sizeof(double), cudaMemcpyDeviceToHost, c->st));
     XB_CUDA(cudaStreamSynchronize(c->st));
+    if (getenv("XB_TRACE"))
+      fprintf(stderr, "[xb] rsvd_dense host: compute+ingest %.1f ms, register outputs %.1f ms, "
+              "d2h %.1f ms\n", (t1 - t0) * 1e3, (t2 - t1) * 1e3, (now_s() - t2) * 1e3);
   });
 }
 
