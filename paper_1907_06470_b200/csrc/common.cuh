@@ -67,12 +67,13 @@ void launch_uniform_bits(uint64_t seed, int64_t row0, int64_t rows, int64_t cols
 struct DGemmArgs {
   bool trans_a;
   int64_t M, N, K;
-  const double* A;
+  const void* A;  // double, or float when a_f32 (widened to f64 in the kernel)
   int64_t lda;
   const double* B;
   int64_t ldb;
   double* C;
   int64_t ldc;
+  bool a_f32 = false;
 };
 // Returns the number of split-K slices that will be used for this shape.
 int dgemm_plan_splits(const DGemmArgs& g);
@@ -116,6 +117,10 @@ void launch_transpose(const double* in, int64_t rows, int64_t cols, int64_t ldin
                       int64_t ldout, cudaStream_t st);
 void launch_copy2d(const double* in, int64_t rows, int64_t cols, int64_t ldin, double* out,
                    int64_t ldout, cudaStream_t st);
+template <typename Tin, typename Tout>
+void launch_copy2d_cast(const Tin* in, int64_t rows, int64_t cols, int64_t ldin, Tout* out,
+                        int64_t ldout, cudaStream_t st);
+void launch_round_f32(double* p, int64_t rows, int64_t cols, int64_t ld, cudaStream_t st);
 void launch_zero(double* p, size_t count, cudaStream_t st);
 
 }  // namespace xb

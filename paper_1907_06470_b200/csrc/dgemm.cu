@@ -1,7 +1,7 @@
 // FP64 tensor-core (DMMA) tile GEMM for the rSVD products.
 //
 // Replaces the reference's dense block_multiply (kernels.py:145-193,
-// _cell_accumulate 80-84) for the three product shapes of the hot path:
+// _cell_accumulate 80-84) for the product shapes of the hot path:
 //   NN  Y  = A * X        A m x n row-major (K-contiguous), X n x l
 //   TN  Z  = A^T * Q      A m x n row-major read as its transposed view
 //                         (pool.py:390-418), reduce over the long m
@@ -16,18 +16,27 @@
 // written to a workspace and summed in slice order by a second kernel — a
 // fixed order, so results are deterministic run to run (no fp atomics).
 //
-// Shared-memory layout: every tile row stride S satisfies S = 4 (mod 8)
-// doubles, which makes the per-lane 8-byte fragment loads of m8n8k4
-// (row = lane>>2, col = lane&3 patterns) bank-conflict free.
+// A may be float64 or float32 (Precision.SINGLE storage): a float32 A tile
+// is widened to f64 in registers at fragment load, so products over f32
+// inputs run with f64 accumulation (more accurate than the reference's f32
+// compute dtype, core.py:43-46).
+//
+// Shared-memory layout: tile row strides are padded so the per-lane
+// fragment loads of m8n8k4 (row = lane>>2, col = lane&3) are bank-conflict
+// free: S = 4 (mod 8) elements for 8-byte tiles and K-contiguous 4-byte
+// tiles, S = 8 (mod 16) for M-contiguous 4-byte tiles.
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 
 namespace xb {
 namespace {
 
-template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, bool TRANS_A>
+constexpr int pad_to(int x, int mod, int rem) { return x + ((rem - (x % mod)) % mod + mod) % mod; }
+
+template <typename TA, int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, bool TRANS_A>
 struct DCfg {
   static constexpr int kThreads = WARPS_M * WARPS_N * 32;
   static constexpr int WM = BM / WARPS_M;  // rows per warp
@@ -36,28 +45,30 @@ struct DCfg {
   static constexpr int FN = WN / 8;        // (N)
   static_assert(WM % 8 == 0 && WN % 8 == 0, "warp tile must be a multiple of 8");
   static_assert(BK % 4 == 0, "BK multiple of 4");
-  static constexpr int pad8(int x) { return x + ((4 - (x % 8)) + 8) % 8; }
+  static constexpr bool kF32 = sizeof(TA) == 4;
   // A tile: NN -> BM rows x BK (K-contig), TN -> BK rows x BM (M-contig)
-  static constexpr int SA = TRANS_A ? pad8(BM) : pad8(BK);
+  static constexpr int SA = TRANS_A ? (kF32 ? pad_to(BM, 16, 8) : pad_to(BM, 8, 4)) : pad_to(BK, 8, 4);
   static constexpr int A_ELEMS = TRANS_A ? BK * SA : BM * SA;
-  static constexpr int SB = pad8(BN);
+  static constexpr size_t A_BYTES = ((size_t)A_ELEMS * sizeof(TA) + 15) / 16 * 16;
+  static constexpr int SB = pad_to(BN, 8, 4);
   static constexpr int B_ELEMS = BK * SB;
-  static constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;
-  static constexpr size_t SMEM = (size_t)STAGES * STAGE_ELEMS * sizeof(double);
+  static constexpr size_t STAGE_BYTES = A_BYTES + (size_t)B_ELEMS * sizeof(double);
+  static constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-// 16-byte async copy with zero fill of the bytes past src_bytes.
+// Async copies with zero fill of the bytes past src_bytes.
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
                "r"(src_bytes));
 }
-__device__ __forceinline__ void cp_async8(void* dst, const void* src, int src_bytes) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
-               "r"(src_bytes));
+template <int BYTES>
+__device__ __forceinline__ void cp_async_small(void* dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(smem_u32(dst)), "l"(src),
+               "n"(BYTES), "r"(src_bytes));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
@@ -72,26 +83,28 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
       : "d"(a), "d"(b));
 }
 
-// Load a rows x cols sub-block (global row-major, ld) into shared (stride S),
-// zero-filling outside [row_lim, col_lim). VEC16 requires ld, col0 even and a
-// 16B-aligned base; cols is then a multiple of 2.
-template <int ROWS, int COLS, int S, int NT, bool VEC16>
-__device__ __forceinline__ void load_tile(double* sdst, const double* __restrict__ g, int64_t ld,
-                                          int64_t row0, int64_t col0, int64_t row_lim,
-                                          int64_t col_lim, int tid) {
+// Load a ROWS x COLS sub-block (global row-major, ld) into shared (stride S),
+// zero-filling outside [row_lim, col_lim). VEC16 requires ld and col0 to be
+// multiples of 16/sizeof(T) and a 16B-aligned base.
+template <typename T, int ROWS, int COLS, int S, int NT, bool VEC16>
+__device__ __forceinline__ void load_tile(T* sdst, const T* __restrict__ g, int64_t ld, int64_t row0,
+                                          int64_t col0, int64_t row_lim, int64_t col_lim, int tid) {
   if constexpr (VEC16) {
-    constexpr int CPR = COLS / 2;  // 16B chunks per row
+    constexpr int E = 16 / sizeof(T);  // elements per 16B chunk
+    constexpr int CPR = COLS / E;
+    static_assert(COLS % E == 0, "tile width must hold whole 16B chunks");
     constexpr int TOTAL = ROWS * CPR;
 #pragma unroll
     for (int i = tid; i < TOTAL; i += NT) {
       const int r = i / CPR;
-      const int c = (i - r * CPR) * 2;
+      const int c = (i - r * CPR) * E;
       const int64_t gr = row0 + r, gc = col0 + c;
-      const double* src = g;
+      const T* src = g;
       int bytes = 0;
       if (gr < row_lim && gc < col_lim) {
         src = g + gr * ld + gc;
-        bytes = (gc + 1 < col_lim) ? 16 : 8;
+        const int64_t left = col_lim - gc;
+        bytes = (int)(left >= E ? 16 : left * (int64_t)sizeof(T));
       }
       cp_async16(sdst + r * S + c, src, bytes);
     }
@@ -102,27 +115,27 @@ __device__ __forceinline__ void load_tile(double* sdst, const double* __restrict
       const int r = i / COLS;
       const int c = i - r * COLS;
       const int64_t gr = row0 + r, gc = col0 + c;
-      const double* src = g;
+      const T* src = g;
       int bytes = 0;
       if (gr < row_lim && gc < col_lim) {
         src = g + gr * ld + gc;
-        bytes = 8;
+        bytes = sizeof(T);
       }
-      cp_async8(sdst + r * S + c, src, bytes);
+      cp_async_small<sizeof(T)>(sdst + r * S + c, src, bytes);
     }
   }
 }
 
 // C (or the split slice of the workspace) = op(A) * B over k in
 // [z * k_per_split, min(K, (z+1) * k_per_split)).
-template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, bool TRANS_A, bool A16,
-          bool B16>
+template <typename TA, int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, bool TRANS_A,
+          bool A16, bool B16>
 __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, 1)
-    dgemm_kernel(int64_t M, int64_t N, int64_t K, const double* __restrict__ A, int64_t lda,
+    dgemm_kernel(int64_t M, int64_t N, int64_t K, const TA* __restrict__ A, int64_t lda,
                  const double* __restrict__ B, int64_t ldb, double* __restrict__ C, int64_t ldc,
                  int64_t split_stride, int64_t k_per_split) {
-  using Cfg = DCfg<BM, BN, BK, WARPS_M, WARPS_N, STAGES, TRANS_A>;
-  extern __shared__ __align__(16) double smem[];
+  using Cfg = DCfg<TA, BM, BN, BK, WARPS_M, WARPS_N, STAGES, TRANS_A>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
@@ -141,16 +154,20 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, 1)
 
   const int ktiles = (int)ceil_div(kend - kbeg, BK);
 
+  auto stage_a = [&](int stage) {
+    return reinterpret_cast<TA*>(smem_raw + (size_t)stage * Cfg::STAGE_BYTES);
+  };
+  auto stage_b = [&](int stage) {
+    return reinterpret_cast<double*>(smem_raw + (size_t)stage * Cfg::STAGE_BYTES + Cfg::A_BYTES);
+  };
   auto load_stage = [&](int stage, int kt) {
-    double* sA = smem + stage * Cfg::STAGE_ELEMS;
-    double* sB = sA + Cfg::A_ELEMS;
     const int64_t k0 = kbeg + (int64_t)kt * BK;
     if constexpr (TRANS_A) {
-      load_tile<BK, BM, Cfg::SA, Cfg::kThreads, A16>(sA, A, lda, k0, m0, kend, M, tid);
+      load_tile<TA, BK, BM, Cfg::SA, Cfg::kThreads, A16>(stage_a(stage), A, lda, k0, m0, kend, M, tid);
     } else {
-      load_tile<BM, BK, Cfg::SA, Cfg::kThreads, A16>(sA, A, lda, m0, k0, M, kend, tid);
+      load_tile<TA, BM, BK, Cfg::SA, Cfg::kThreads, A16>(stage_a(stage), A, lda, m0, k0, M, kend, tid);
     }
-    load_tile<BK, BN, Cfg::SB, Cfg::kThreads, B16>(sB, B, ldb, k0, n0, kend, N, tid);
+    load_tile<double, BK, BN, Cfg::SB, Cfg::kThreads, B16>(stage_b(stage), B, ldb, k0, n0, kend, N, tid);
   };
 
 #pragma unroll
@@ -167,8 +184,8 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, 1)
       if (nk < ktiles) load_stage(nk % STAGES, nk);
       cp_async_commit();
     }
-    const double* sA = smem + (kt % STAGES) * Cfg::STAGE_ELEMS;
-    const double* sB = sA + Cfg::A_ELEMS;
+    const TA* sA = stage_a(kt % STAGES);
+    const double* sB = stage_b(kt % STAGES);
 #pragma unroll
     for (int ks = 0; ks < BK / 4; ++ks) {
       double af[Cfg::FM], bf[Cfg::FN];
@@ -176,9 +193,9 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, 1)
       for (int i = 0; i < Cfg::FM; ++i) {
         const int row = wm * Cfg::WM + i * 8 + g;  // output row within tile
         if constexpr (TRANS_A)
-          af[i] = sA[(ks * 4 + t) * Cfg::SA + row];
+          af[i] = (double)sA[(ks * 4 + t) * Cfg::SA + row];
         else
-          af[i] = sA[row * Cfg::SA + ks * 4 + t];
+          af[i] = (double)sA[row * Cfg::SA + ks * 4 + t];
       }
 #pragma unroll
       for (int j = 0; j < Cfg::FN; ++j) {
@@ -261,30 +278,30 @@ __global__ void __launch_bounds__(256) split_reduce_wide_kernel(
 
 namespace {
 
-template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, bool TRANS_A>
+template <typename TA, int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, bool TRANS_A>
 void run_cfg(const DGemmArgs& g, int splits, int64_t k_per_split, double* out, int64_t ldo,
              int64_t split_stride, cudaStream_t st) {
-  using Cfg = DCfg<BM, BN, BK, WARPS_M, WARPS_N, STAGES, TRANS_A>;
-  const bool a16 = ((g.lda & 1) == 0) && ((reinterpret_cast<uintptr_t>(g.A) & 15) == 0) &&
-                   (((TRANS_A ? g.M : g.K) & 1) == 0);
-  const bool b16 = ((g.ldb & 1) == 0) && ((reinterpret_cast<uintptr_t>(g.B) & 15) == 0) &&
-                   ((g.N & 1) == 0);
+  using Cfg = DCfg<TA, BM, BN, BK, WARPS_M, WARPS_N, STAGES, TRANS_A>;
+  constexpr int64_t E = 16 / sizeof(TA);
+  const TA* A = static_cast<const TA*>(g.A);
+  const bool a16 = (g.lda % E == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
+  const bool b16 = ((g.ldb & 1) == 0) && ((reinterpret_cast<uintptr_t>(g.B) & 15) == 0);
   dim3 grid((unsigned)ceil_div(g.M, BM), (unsigned)ceil_div(g.N, BN), (unsigned)splits);
   auto launch = [&](auto kernel) {
     XB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)Cfg::SMEM));
-    kernel<<<grid, Cfg::kThreads, Cfg::SMEM, st>>>(g.M, g.N, g.K, g.A, g.lda, g.B, g.ldb, out, ldo,
+    kernel<<<grid, Cfg::kThreads, Cfg::SMEM, st>>>(g.M, g.N, g.K, A, g.lda, g.B, g.ldb, out, ldo,
                                                    split_stride, k_per_split);
     check_launch("dgemm");
   };
   if (a16 && b16)
-    launch(dgemm_kernel<BM, BN, BK, WARPS_M, WARPS_N, STAGES, TRANS_A, true, true>);
+    launch(dgemm_kernel<TA, BM, BN, BK, WARPS_M, WARPS_N, STAGES, TRANS_A, true, true>);
   else if (a16)
-    launch(dgemm_kernel<BM, BN, BK, WARPS_M, WARPS_N, STAGES, TRANS_A, true, false>);
+    launch(dgemm_kernel<TA, BM, BN, BK, WARPS_M, WARPS_N, STAGES, TRANS_A, true, false>);
   else if (b16)
-    launch(dgemm_kernel<BM, BN, BK, WARPS_M, WARPS_N, STAGES, TRANS_A, false, true>);
+    launch(dgemm_kernel<TA, BM, BN, BK, WARPS_M, WARPS_N, STAGES, TRANS_A, false, true>);
   else
-    launch(dgemm_kernel<BM, BN, BK, WARPS_M, WARPS_N, STAGES, TRANS_A, false, false>);
+    launch(dgemm_kernel<TA, BM, BN, BK, WARPS_M, WARPS_N, STAGES, TRANS_A, false, false>);
 }
 
 // Tile width for the N (sketch) dimension: the whole padded l in one tile
@@ -297,8 +314,9 @@ int pick_bn(int64_t N) {
 }
 
 // Tile variants. The l = 120 products over A (cfg2's hot shape) have
-// alternatives selectable with XB_DGEMM_VARIANT for tuning runs; everything
-// else uses variant 0.
+// alternatives selectable with XB_DGEMM_VARIANT for tuning runs (measured
+// on B200, tools/tune_gemm.py: BK=32/3 stages is the fastest); everything
+// else uses the BK=16 / 4-stage tile.
 struct Variant {
   int id, BM, BK, ctas_per_sm;
 };
@@ -306,12 +324,12 @@ struct Variant {
 Variant pick_variant(const DGemmArgs& g) {
   const int bn = pick_bn(g.N);
   int v = 0;
-  if (bn == 120 && g.K >= 4096) {
+  if (bn == 120 && g.K >= 4096 && !g.a_f32) {
     static const int env = [] {
       const char* e = getenv("XB_DGEMM_VARIANT");
       return e ? atoi(e) : -1;
     }();
-    v = env >= 0 ? env : 0;
+    v = env >= 0 ? env : 1;
   }
   switch (v) {
     case 1: return {1, 128, 32, 1};
@@ -322,6 +340,27 @@ Variant pick_variant(const DGemmArgs& g) {
 }
 
 int64_t kper(int64_t K, int splits, int bk) { return round_up(ceil_div(K, splits), bk); }
+
+template <typename TA, bool TRANS_A>
+void dispatch(const DGemmArgs& g, const Variant& var, int splits, int64_t kps, double* out,
+              int64_t ldo, int64_t stride, cudaStream_t st) {
+  const int bn = pick_bn(g.N);
+  if constexpr (std::is_same<TA, double>::value) {
+    if (bn == 120) {
+      switch (var.id) {
+        case 1: run_cfg<TA, 128, 120, 32, 4, 3, 3, TRANS_A>(g, splits, kps, out, ldo, stride, st); return;
+        case 2: run_cfg<TA, 64, 120, 16, 2, 3, 4, TRANS_A>(g, splits, kps, out, ldo, stride, st); return;
+        case 3: run_cfg<TA, 128, 120, 16, 2, 3, 4, TRANS_A>(g, splits, kps, out, ldo, stride, st); return;
+        default: run_cfg<TA, 128, 120, 16, 4, 3, 4, TRANS_A>(g, splits, kps, out, ldo, stride, st); return;
+      }
+    }
+  }
+  switch (bn) {
+    case 32: run_cfg<TA, 128, 32, 16, 4, 1, 4, TRANS_A>(g, splits, kps, out, ldo, stride, st); break;
+    case 64: run_cfg<TA, 128, 64, 16, 4, 2, 4, TRANS_A>(g, splits, kps, out, ldo, stride, st); break;
+    default: run_cfg<TA, 128, 128, 16, 4, 4, 4, TRANS_A>(g, splits, kps, out, ldo, stride, st); break;
+  }
+}
 
 }  // namespace
 
@@ -375,37 +414,16 @@ void dgemm(const DGemmArgs& g, int splits, double* work, cudaStream_t st) {
     ldo = round_up(g.N, 2);
     stride = g.M * ldo;
   }
-  const int bn = pick_bn(g.N);
-  if (g.trans_a) {
-    if (bn == 120) {
-      switch (var.id) {
-        case 1: run_cfg<128, 120, 32, 4, 3, 3, true>(g, splits, kps, out, ldo, stride, st); break;
-        case 2: run_cfg<64, 120, 16, 2, 3, 4, true>(g, splits, kps, out, ldo, stride, st); break;
-        case 3: run_cfg<128, 120, 16, 2, 3, 4, true>(g, splits, kps, out, ldo, stride, st); break;
-        default: run_cfg<128, 120, 16, 4, 3, 4, true>(g, splits, kps, out, ldo, stride, st); break;
-      }
-    } else {
-      switch (bn) {
-        case 32: run_cfg<128, 32, 16, 4, 1, 4, true>(g, splits, kps, out, ldo, stride, st); break;
-        case 64: run_cfg<128, 64, 16, 4, 2, 4, true>(g, splits, kps, out, ldo, stride, st); break;
-        default: run_cfg<128, 128, 16, 4, 4, 4, true>(g, splits, kps, out, ldo, stride, st); break;
-      }
-    }
+  if (g.a_f32) {
+    if (g.trans_a)
+      dispatch<float, true>(g, var, splits, kps, out, ldo, stride, st);
+    else
+      dispatch<float, false>(g, var, splits, kps, out, ldo, stride, st);
   } else {
-    if (bn == 120) {
-      switch (var.id) {
-        case 1: run_cfg<128, 120, 32, 4, 3, 3, false>(g, splits, kps, out, ldo, stride, st); break;
-        case 2: run_cfg<64, 120, 16, 2, 3, 4, false>(g, splits, kps, out, ldo, stride, st); break;
-        case 3: run_cfg<128, 120, 16, 2, 3, 4, false>(g, splits, kps, out, ldo, stride, st); break;
-        default: run_cfg<128, 120, 16, 4, 3, 4, false>(g, splits, kps, out, ldo, stride, st); break;
-      }
-    } else {
-      switch (bn) {
-        case 32: run_cfg<128, 32, 16, 4, 1, 4, false>(g, splits, kps, out, ldo, stride, st); break;
-        case 64: run_cfg<128, 64, 16, 4, 2, 4, false>(g, splits, kps, out, ldo, stride, st); break;
-        default: run_cfg<128, 128, 16, 4, 4, 4, false>(g, splits, kps, out, ldo, stride, st); break;
-      }
-    }
+    if (g.trans_a)
+      dispatch<double, true>(g, var, splits, kps, out, ldo, stride, st);
+    else
+      dispatch<double, false>(g, var, splits, kps, out, ldo, stride, st);
   }
   if (splits > 1) {
     const int64_t total = g.M * g.N;

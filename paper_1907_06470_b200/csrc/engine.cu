@@ -192,20 +192,36 @@ void gemm(xb_ctx* c, bool ta, int64_t M, int64_t N, int64_t K, const double* A, 
   dgemm(g, splits, work, c->st);
 }
 
+// The caller's A in device memory: f64, or f32 (Precision.SINGLE storage).
+struct AView {
+  const void* p;
+  int64_t ld;
+  bool f32;
+  size_t esz() const { return f32 ? 4 : 8; }
+  const void* rows_from(int64_t r0) const {
+    return static_cast<const char*>(p) + (size_t)r0 * ld * esz();
+  }
+};
+
 // A product on A (the dominant kernel): bracketed by events when profiling.
-void gemm_on_a(xb_ctx* c, bool ta, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
-               const double* B, int64_t ldb, double* C, int64_t ldc, int l) {
+void gemm_on_a(xb_ctx* c, bool ta, int64_t M, int64_t N, int64_t K, const AView& a,
+               int64_t row0, const double* B, int64_t ldb, double* C, int64_t ldc, int l) {
   cudaEvent_t b = nullptr, e = nullptr;
   if (c->profiling) {
     b = c->prof_event();
     e = c->prof_event();
     XB_CUDA(cudaEventRecord(b, c->st));
   }
-  gemm(c, ta, M, N, K, A, lda, B, ldb, C, ldc);
+  DGemmArgs g{ta, M, N, K, a.rows_from(row0), a.ld, B, ldb, C, ldc, a.f32};
+  const int splits = dgemm_plan_splits(g);
+  double* work = nullptr;
+  const size_t need = dgemm_workspace_doubles(g, splits);
+  if (need) work = c->dbuf("split", need);
+  dgemm(g, splits, work, c->st);
   if (c->profiling) {
     XB_CUDA(cudaEventRecord(e, c->st));
     const double mn = (double)M * (double)K;  // A is M x K (NN) or K x M (TN)
-    c->prof_pending.push_back({b, e, 2.0 * mn * l, mn * sizeof(double)});
+    c->prof_pending.push_back({b, e, 2.0 * mn * l, mn * a.esz()});
   }
 }
 
@@ -275,14 +291,18 @@ void check_dims(int64_t m, int64_t n, int k, int p, int q) {
 
 // Host-side description of how A reaches the device for the first product.
 struct IngestPlan {
-  const double* hostA = nullptr;  // non-null: stream row chunks H2D, overlapped
+  const void* hostA = nullptr;  // non-null: stream row chunks H2D, overlapped
   int64_t host_lda = 0;
   int64_t chunk_rows = 0;
 };
 
-void rsvd_f64(xb_ctx* c, int64_t m, int64_t n, double* dA, int64_t lda, const double* d_omega,
-              int64_t ld_omega, uint64_t seed, int k, int p, int q, const RsvdOut& out,
-              int32_t* deficient, int* ndeficient, double* stage_seconds, const IngestPlan& ing) {
+// One factorisation. A (device, f64 or f32) is only touched by the five or
+// more products over A; everything downstream of a product is f64. With an
+// f32 A, Omega is rounded through float32 first, as the reference stores it
+// at the storage dtype (pipeline.py:281-282).
+void rsvd_impl(xb_ctx* c, const AView& a, int64_t m, int64_t n, const void* d_omega,
+               int64_t ld_omega, uint64_t seed, int k, int p, int q, const RsvdOut& out,
+               int32_t* deficient, int* ndeficient, double* stage_seconds, const IngestPlan& ing) {
   check_dims(m, n, k, p, q);
   const int l = k + p;
   const int lp = (int)round_up(l, 8);
@@ -310,19 +330,19 @@ void rsvd_f64(xb_ctx* c, int64_t m, int64_t n, double* dA, int64_t lda, const do
   // lands inside the timed stream
   {
     size_t need = 0;
-    auto upd = [&](bool ta, int64_t M, int64_t N, int64_t K) {
-      DGemmArgs g{ta, M, N, K, nullptr, 0, nullptr, 0, nullptr, 0};
+    auto upd = [&](bool ta, int64_t M, int64_t N, int64_t K, bool af32) {
+      DGemmArgs g{ta, M, N, K, nullptr, 0, nullptr, 0, nullptr, 0, af32};
       need = std::max(need, dgemm_workspace_doubles(g, dgemm_plan_splits(g)));
     };
-    upd(false, m, lp, n);
-    upd(true, n, lp, m);
-    upd(true, lp, lp, m);
-    upd(true, lp, lp, n);
-    upd(false, m, lp, lp);
-    upd(false, n, lp, lp);
-    upd(false, m, k, lp);
-    upd(false, n, k, lp);
-    if (ing.hostA) upd(false, ing.chunk_rows, lp, n);
+    upd(false, m, lp, n, a.f32);
+    upd(true, n, lp, m, a.f32);
+    upd(true, lp, lp, m, false);
+    upd(true, lp, lp, n, false);
+    upd(false, m, lp, lp, false);
+    upd(false, n, lp, lp, false);
+    upd(false, m, k, lp, false);
+    upd(false, n, k, lp, false);
+    if (ing.hostA) upd(false, ing.chunk_rows, lp, n, a.f32);
     if (need) c->dbuf("split", need);
     c->dbuf("hh_work", (size_t)2 * std::max(m, n) * l);
   }
@@ -334,9 +354,14 @@ void rsvd_f64(xb_ctx* c, int64_t m, int64_t n, double* dA, int64_t lda, const do
   clk.enter(kGaussian);
   if (d_omega) {
     XB_CUDA(cudaMemsetAsync(Om, 0, (size_t)n * lp * sizeof(double), st));
-    launch_copy2d(d_omega, n, l, ld_omega, Om, lp, st);
+    if (a.f32)
+      launch_copy2d_cast<float, double>(static_cast<const float*>(d_omega), n, l, ld_omega, Om, lp,
+                                        st);
+    else
+      launch_copy2d(static_cast<const double*>(d_omega), n, l, ld_omega, Om, lp, st);
   } else {
     launch_gaussian<double>(seed, 0, n, l, Om, lp, lp, st);
+    if (a.f32) launch_round_f32(Om, n, l, lp, st);
   }
 
   // O*A^T: the sketch; with a host A, row chunks arrive on the copy stream and
@@ -350,15 +375,16 @@ void rsvd_f64(xb_ctx* c, int64_t m, int64_t n, double* dA, int64_t lda, const do
     std::vector<cudaEvent_t> landed;
     for (int64_t r0 = 0; r0 < m; r0 += ing.chunk_rows) {
       const int64_t rows = std::min(ing.chunk_rows, m - r0);
-      XB_CUDA(cudaMemcpy2DAsync(dA + r0 * lda, lda * sizeof(double), ing.hostA + r0 * ing.host_lda,
-                                ing.host_lda * sizeof(double), n * sizeof(double), rows,
-                                cudaMemcpyHostToDevice, c->cp));
+      const size_t es = a.esz();
+      XB_CUDA(cudaMemcpy2DAsync(const_cast<void*>(a.rows_from(r0)), a.ld * es,
+                                static_cast<const char*>(ing.hostA) + (size_t)r0 * ing.host_lda * es,
+                                ing.host_lda * es, n * es, rows, cudaMemcpyHostToDevice, c->cp));
       cudaEvent_t e;
       XB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       XB_CUDA(cudaEventRecord(e, c->cp));
       XB_CUDA(cudaStreamWaitEvent(st, e, 0));
       landed.push_back(e);
-      gemm_on_a(c, false, rows, lp, n, dA + r0 * lda, lda, Om, lp, Ym + r0 * lp, lp, l);
+      gemm_on_a(c, false, rows, lp, n, a, r0, Om, lp, Ym + r0 * lp, lp, l);
     }
     XB_CUDA(cudaEventRecord(t1, c->cp));
     XB_CUDA(cudaStreamSynchronize(c->cp));
@@ -369,25 +395,25 @@ void rsvd_f64(xb_ctx* c, int64_t m, int64_t n, double* dA, int64_t lda, const do
     cudaEventDestroy(t0);
     cudaEventDestroy(t1);
   } else {
-    gemm_on_a(c, false, m, lp, n, dA, lda, Om, lp, Ym, lp, l);
+    gemm_on_a(c, false, m, lp, n, a, 0, Om, lp, Ym, lp, l);
   }
   clk.enter(kOrtho);
   cholqr2(c, s, Ym, m, Tm, Qm, q == 0 ? Rf : nullptr);
   for (int it = 0; it < q; ++it) {
     clk.enter(kSketch);
-    gemm_on_a(c, true, n, lp, m, dA, lda, Qm, lp, Zn, lp, l);  // Z = A^T Q
+    gemm_on_a(c, true, n, lp, m, a, 0, Qm, lp, Zn, lp, l);  // Z = A^T Q
     clk.enter(kOrtho);
     cholqr2(c, s, Zn, n, Tn, Qn, nullptr);
     clk.enter(kSketch);
-    gemm_on_a(c, false, m, lp, n, dA, lda, Qn, lp, Ym, lp, l);  // Y = A Qz
+    gemm_on_a(c, false, m, lp, n, a, 0, Qn, lp, Ym, lp, l);  // Y = A Qz
     clk.enter(kOrtho);
     cholqr2(c, s, Ym, m, Tm, Qm, it == q - 1 ? Rf : nullptr);
   }
   // deficient columns of the final range-finder QR (kernels.py:327-331)
-  launch_deficient(Rf, lp, l, DBL_EPSILON, defc, defc + 1, st);
+  launch_deficient(Rf, lp, l, a.f32 ? (double)FLT_EPSILON : DBL_EPSILON, defc, defc + 1, st);
 
   clk.enter(kProject);
-  gemm_on_a(c, true, n, lp, m, dA, lda, Qm, lp, Zn, lp, l);  // B^T = A^T Q
+  gemm_on_a(c, true, n, lp, m, a, 0, Qm, lp, Zn, lp, l);  // B^T = A^T Q
 
   clk.enter(kSvdPrep);
   cholqr2(c, s, Zn, n, Tn, Qn, Rf);  // B^T = Q_B R_B
@@ -438,10 +464,33 @@ struct HostRegistration {
   }
 };
 
-void require_f64(int dtype) {
+// true for float32 (Precision.SINGLE), false for float64
+bool check_dtype(int dtype) {
   XB_REQUIRE(dtype == XB_F64 || dtype == XB_F32, XB_EVALUE, "unknown dtype");
-  XB_REQUIRE(dtype == XB_F64, XB_EUNSUPPORTED,
-             "float32 (Precision.SINGLE) path is not built in this round");
+  return dtype == XB_F32;
+}
+
+// C = op(A) B for device operands of one dtype. float32 follows the
+// reference's storage rule (core.py:43-46: f32 in, f32 out) but accumulates
+// in f64: A is widened in the kernel, B and C go through f64 scratch.
+void gemm_any(xb_ctx* c, bool f32, bool ta, int64_t m, int64_t n, int64_t kdim, const void* dA,
+              int64_t lda, const void* dB, int64_t ldb, void* dC, int64_t ldc) {
+  if (!f32) {
+    gemm(c, ta, m, n, kdim, static_cast<const double*>(dA), lda, static_cast<const double*>(dB),
+         ldb, static_cast<double*>(dC), ldc);
+    return;
+  }
+  const int64_t np = round_up(n, 2);
+  double* B64 = c->dbuf("gB64", (size_t)std::max<int64_t>(1, kdim * np));
+  double* C64 = c->dbuf("gC64", (size_t)m * np);
+  launch_copy2d_cast<float, double>(static_cast<const float*>(dB), kdim, n, ldb, B64, np, c->st);
+  DGemmArgs g{ta, m, n, kdim, dA, lda, B64, np, C64, np, true};
+  const int splits = dgemm_plan_splits(g);
+  double* work = nullptr;
+  const size_t need = dgemm_workspace_doubles(g, splits);
+  if (need) work = c->dbuf("split", need);
+  dgemm(g, splits, work, c->st);
+  launch_copy2d_cast<double, float>(C64, m, n, np, static_cast<float*>(dC), ldc, c->st);
 }
 
 }  // namespace
@@ -521,12 +570,25 @@ int xb_rsvd_dense_dev(xb_ctx* c, int dtype, int64_t m, int64_t n, const void* dA
   return guarded([&] {
     XB_REQUIRE(c, XB_EVALUE, "null context");
     LaunchScope ls(c);
-    require_f64(dtype);
+    const bool f32 = check_dtype(dtype);
     XB_REQUIRE(lda >= n && ldu >= k && ldv >= k, XB_EVALUE, "leading dimension too small");
-    RsvdOut out{static_cast<double*>(dU), ldu, d_s, static_cast<double*>(dV), ldv};
-    rsvd_f64(c, m, n, const_cast<double*>(static_cast<const double*>(dA)), lda,
-             static_cast<const double*>(d_omega), k + p, seed, k, p, q, out, deficient,
-             ndeficient, stage_seconds, IngestPlan{});
+    const AView a{dA, lda, f32};
+    if (!f32) {
+      RsvdOut out{static_cast<double*>(dU), ldu, d_s, static_cast<double*>(dV), ldv};
+      rsvd_impl(c, a, m, n, d_omega, k + p, seed, k, p, q, out, deficient, ndeficient,
+                stage_seconds, IngestPlan{});
+      return;
+    }
+    // float32 outputs: factors are formed in f64, then stored at the storage
+    // dtype like the reference (pipeline.py:589-591, 603-611)
+    double* Ud = c->dbuf("Ud", (size_t)m * k);
+    double* Vd = c->dbuf("Vd", (size_t)n * k);
+    RsvdOut out{Ud, k, d_s, Vd, k};
+    rsvd_impl(c, a, m, n, d_omega, k + p, seed, k, p, q, out, deficient, ndeficient,
+              stage_seconds, IngestPlan{});
+    launch_copy2d_cast<double, float>(Ud, m, k, k, static_cast<float*>(dU), ldu, c->st);
+    launch_copy2d_cast<double, float>(Vd, n, k, k, static_cast<float*>(dV), ldv, c->st);
+    XB_CUDA(cudaStreamSynchronize(c->st));
   });
 }
 
@@ -537,45 +599,50 @@ int xb_rsvd_dense(xb_ctx* c, int dtype, int64_t m, int64_t n, const void* A, int
   return guarded([&] {
     XB_REQUIRE(c, XB_EVALUE, "null context");
     LaunchScope ls(c);
-    require_f64(dtype);
+    const bool f32 = check_dtype(dtype);
+    const size_t es = f32 ? 4 : 8;
     check_dims(m, n, k, p, q);
     XB_REQUIRE(A && U && s && V, XB_EVALUE, "null buffer");
     XB_REQUIRE(lda >= n && ldu >= k && ldv >= k, XB_EVALUE, "leading dimension too small");
     const int l = k + p;
-    HostRegistration reg(A, (size_t)((m - 1) * lda + n) * sizeof(double));
-    double* dA = c->dbuf("A", (size_t)m * n);
+    const double t0 = now_s();
+    HostRegistration reg(A, (size_t)((m - 1) * lda + n) * es);
+    void* dA = c->buf("A", (size_t)m * n * es);
     double* dU = c->dbuf("U", (size_t)m * k);
     double* dV = c->dbuf("V", (size_t)n * k);
     double* ds = c->dbuf("s", (size_t)k);
-    double* dO = nullptr;
+    void* dO = nullptr;
     if (omega) {
-      dO = c->dbuf("omega_in", (size_t)n * l);
-      XB_CUDA(cudaMemcpyAsync(dO, omega, (size_t)n * l * sizeof(double), cudaMemcpyHostToDevice,
-                              c->st));
+      dO = c->buf("omega_in", (size_t)n * l * es);
+      XB_CUDA(cudaMemcpyAsync(dO, omega, (size_t)n * l * es, cudaMemcpyHostToDevice, c->st));
     }
     IngestPlan ing;
-    ing.hostA = static_cast<const double*>(A);
+    ing.hostA = A;
     ing.host_lda = lda;
     // ~1 GiB chunks, at least 8 of them when the matrix is large
-    int64_t rows = std::max<int64_t>(256, ((int64_t)1 << 27) / std::max<int64_t>(n, 1));
+    int64_t rows = std::max<int64_t>(256, ((int64_t)1 << 30) / std::max<int64_t>(n * (int64_t)es, 1));
     rows = std::min(rows, std::max<int64_t>(256, round_up(ceil_div(m, 8), 128)));
     ing.chunk_rows = std::min(rows, m);
     RsvdOut out{dU, k, ds, dV, k};
-    const double t0 = now_s();
-    rsvd_f64(c, m, n, dA, n, dO, l, seed, k, p, q, out, deficient, ndeficient, stage_seconds, ing);
     const double t1 = now_s();
-    HostRegistration ru(U, (size_t)((m - 1) * ldu + k) * sizeof(double));
-    HostRegistration rv(V, (size_t)((n - 1) * ldv + k) * sizeof(double));
+    rsvd_impl(c, AView{dA, n, f32}, m, n, dO, l, seed, k, p, q, out, deficient, ndeficient,
+              stage_seconds, ing);
     const double t2 = now_s();
-    XB_CUDA(cudaMemcpy2DAsync(U, ldu * sizeof(double), dU, k * sizeof(double), k * sizeof(double),
-                              m, cudaMemcpyDeviceToHost, c->st));
-    XB_CUDA(cudaMemcpy2DAsync(V, ldv * sizeof(double), dV, k * sizeof(double), k * sizeof(double),
-                              n, cudaMemcpyDeviceToHost, c->st));
+    void* oU = dU;
+    void* oV = dV;
+    if (f32) {
+      oU = c->buf("U32", (size_t)m * k * 4);
+      oV = c->buf("V32", (size_t)n * k * 4);
+      launch_copy2d_cast<double, float>(dU, m, k, k, static_cast<float*>(oU), k, c->st);
+      launch_copy2d_cast<double, float>(dV, n, k, k, static_cast<float*>(oV), k, c->st);
+    }
+    XB_CUDA(cudaMemcpy2DAsync(U, ldu * es, oU, k * es, k * es, m, cudaMemcpyDeviceToHost, c->st));
+    XB_CUDA(cudaMemcpy2DAsync(V, ldv * es, oV, k * es, k * es, n, cudaMemcpyDeviceToHost, c->st));
     XB_CUDA(cudaMemcpyAsync(s, ds, k * sizeof(double), cudaMemcpyDeviceToHost, c->st));
     XB_CUDA(cudaStreamSynchronize(c->st));
     if (getenv("XB_TRACE"))
-      fprintf(stderr, "[xb] rsvd_dense host: compute+ingest %.1f ms, register outputs %.1f ms, "
-              "d2h %.1f ms\n", (t1 - t0) * 1e3, (t2 - t1) * 1e3, (now_s() - t2) * 1e3);
+      fprintf(stderr, "[xb] rsvd_dense host: setup %.1f ms, ingest+compute %.1f ms, d2h %.1f ms\n",
+              (t1 - t0) * 1e3, (t2 - t1) * 1e3, (now_s() - t2) * 1e3);
   });
 }
 
@@ -619,12 +686,12 @@ int xb_gemm_dev(xb_ctx* c, int dtype, int trans_a, int64_t m, int64_t n, int64_t
   return guarded([&] {
     XB_REQUIRE(c, XB_EVALUE, "null context");
     LaunchScope ls(c);
-    require_f64(dtype);
+    const bool f32 = check_dtype(dtype);
     XB_REQUIRE(m >= 0 && n >= 0 && kdim >= 0, XB_ESHAPE, "negative dimension");
     XB_REQUIRE(ldc >= n && ldb >= n && lda >= (trans_a ? m : kdim), XB_EVALUE,
                "leading dimension too small");
-    gemm(c, trans_a != 0, m, n, kdim, static_cast<const double*>(dA), lda,
-         static_cast<const double*>(dB), ldb, static_cast<double*>(dC), ldc);
+    if (m == 0 || n == 0) return;
+    gemm_any(c, f32, trans_a != 0, m, n, kdim, dA, lda, dB, ldb, dC, ldc);
     XB_CUDA(cudaStreamSynchronize(c->st));
   });
 }
@@ -634,22 +701,24 @@ int xb_gemm(xb_ctx* c, int dtype, int trans_a, int64_t m, int64_t n, int64_t kdi
   return guarded([&] {
     XB_REQUIRE(c, XB_EVALUE, "null context");
     LaunchScope ls(c);
-    require_f64(dtype);
+    const bool f32 = check_dtype(dtype);
+    const size_t es = f32 ? 4 : 8;
     XB_REQUIRE(m >= 0 && n >= 0 && kdim >= 0, XB_ESHAPE, "negative dimension");
     XB_REQUIRE(ldc >= n && ldb >= n && lda >= (trans_a ? m : kdim), XB_EVALUE,
                "leading dimension too small");
     if (m == 0 || n == 0) return;
     const int64_t arows = trans_a ? kdim : m, acols = trans_a ? m : kdim;
-    double* dA = c->dbuf("gA", (size_t)std::max<int64_t>(1, arows * acols));
-    double* dB = c->dbuf("gB", (size_t)std::max<int64_t>(1, kdim * n));
-    double* dC = c->dbuf("gC", (size_t)m * n);
+    void* dA = c->buf("gA", (size_t)std::max<int64_t>(1, arows * acols) * es);
+    void* dB = c->buf("gB", (size_t)std::max<int64_t>(1, kdim * n) * es);
+    void* dC = c->buf("gC", (size_t)m * n * es);
     if (arows * acols > 0)
-      XB_CUDA(cudaMemcpy2DAsync(dA, acols * 8, A, lda * 8, acols * 8, arows, cudaMemcpyHostToDevice,
-                                c->st));
+      XB_CUDA(cudaMemcpy2DAsync(dA, acols * es, A, lda * es, acols * es, arows,
+                                cudaMemcpyHostToDevice, c->st));
     if (kdim * n > 0)
-      XB_CUDA(cudaMemcpy2DAsync(dB, n * 8, B, ldb * 8, n * 8, kdim, cudaMemcpyHostToDevice, c->st));
-    gemm(c, trans_a != 0, m, n, kdim, dA, acols, dB, n, dC, n);
-    XB_CUDA(cudaMemcpy2DAsync(C, ldc * 8, dC, n * 8, n * 8, m, cudaMemcpyDeviceToHost, c->st));
+      XB_CUDA(cudaMemcpy2DAsync(dB, n * es, B, ldb * es, n * es, kdim, cudaMemcpyHostToDevice,
+                                c->st));
+    gemm_any(c, f32, trans_a != 0, m, n, kdim, dA, acols, dB, n, dC, n);
+    XB_CUDA(cudaMemcpy2DAsync(C, ldc * es, dC, n * es, n * es, m, cudaMemcpyDeviceToHost, c->st));
     XB_CUDA(cudaStreamSynchronize(c->st));
   });
 }
@@ -659,7 +728,7 @@ int xb_thin_qr(xb_ctx* c, int dtype, int64_t m, int64_t r, const void* Y, int64_
   return guarded([&] {
     XB_REQUIRE(c, XB_EVALUE, "null context");
     LaunchScope ls(c);
-    require_f64(dtype);
+    const bool f32 = check_dtype(dtype);
     XB_REQUIRE(r >= 1 && m >= r, XB_ESHAPE,
                "thin QR needs rows >= cols >= 1, got " + std::to_string(m) + "x" +
                    std::to_string(r));
@@ -672,12 +741,26 @@ int xb_thin_qr(xb_ctx* c, int dtype, int64_t m, int64_t r, const void* Y, int64_
     int* defc = c->ibuf("qrdef", (size_t)lp + 4);
     c->dbuf("hh_work", (size_t)2 * m * l);
     XB_CUDA(cudaMemsetAsync(dY, 0, (size_t)m * lp * 8, c->st));
-    XB_CUDA(cudaMemcpy2DAsync(dY, lp * 8, Y, ldy * 8, r * 8, m, cudaMemcpyHostToDevice, c->st));
+    // the reference factors in f64 whatever the storage precision (kernels.py:308-316)
+    if (f32) {
+      float* y32 = static_cast<float*>(c->buf("qrY32", (size_t)m * r * 4));
+      XB_CUDA(cudaMemcpy2DAsync(y32, r * 4, Y, ldy * 4, r * 4, m, cudaMemcpyHostToDevice, c->st));
+      launch_copy2d_cast<float, double>(y32, m, r, r, dY, lp, c->st);
+    } else {
+      XB_CUDA(cudaMemcpy2DAsync(dY, lp * 8, Y, ldy * 8, r * 8, m, cudaMemcpyHostToDevice, c->st));
+    }
     Small s = small_bufs(c, l);
     cholqr2(c, s, dY, m, dT, dQ, dR);
-    launch_deficient(dR, lp, l, DBL_EPSILON, defc, defc + 1, c->st);
+    // compute-dtype eps for the deficiency threshold (kernels.py:328)
+    launch_deficient(dR, lp, l, f32 ? (double)FLT_EPSILON : DBL_EPSILON, defc, defc + 1, c->st);
     std::vector<int> hdef(lp + 1, 0);
-    XB_CUDA(cudaMemcpy2DAsync(Q, ldq * 8, dQ, lp * 8, r * 8, m, cudaMemcpyDeviceToHost, c->st));
+    if (f32) {
+      float* q32 = static_cast<float*>(c->buf("qrQ32", (size_t)m * r * 4));
+      launch_copy2d_cast<double, float>(dQ, m, r, lp, q32, r, c->st);
+      XB_CUDA(cudaMemcpy2DAsync(Q, ldq * 4, q32, r * 4, r * 4, m, cudaMemcpyDeviceToHost, c->st));
+    } else {
+      XB_CUDA(cudaMemcpy2DAsync(Q, ldq * 8, dQ, lp * 8, r * 8, m, cudaMemcpyDeviceToHost, c->st));
+    }
     if (R)
       XB_CUDA(cudaMemcpy2DAsync(R, r * 8, dR, lp * 8, r * 8, r, cudaMemcpyDeviceToHost, c->st));
     XB_CUDA(cudaMemcpyAsync(hdef.data(), defc, (lp + 1) * sizeof(int), cudaMemcpyDeviceToHost,

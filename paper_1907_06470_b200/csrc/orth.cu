@@ -188,13 +188,25 @@ __global__ void transpose_kernel(const double* __restrict__ in, int64_t rows, in
   }
 }
 
-__global__ void copy2d_kernel(const double* __restrict__ in, int64_t rows, int64_t cols,
-                              int64_t ldin, double* __restrict__ out, int64_t ldout) {
+template <typename Tin, typename Tout>
+__global__ void copy2d_kernel(const Tin* __restrict__ in, int64_t rows, int64_t cols,
+                              int64_t ldin, Tout* __restrict__ out, int64_t ldout) {
   const int64_t total = rows * cols;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = idx / cols, c = idx - r * cols;
-    out[r * ldout + c] = in[r * ldin + c];
+    out[r * ldout + c] = (Tout)in[r * ldin + c];
+  }
+}
+
+// x <- (double)(float)x: Omega cast to the float32 storage dtype
+// (pipeline.py:281-282) while the sketch buffers stay f64.
+__global__ void round_f32_kernel(double* __restrict__ p, int64_t rows, int64_t cols, int64_t ld) {
+  const int64_t total = rows * cols;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = idx / cols, c = idx - r * cols;
+    p[r * ld + c] = (double)(float)p[r * ld + c];
   }
 }
 
@@ -221,12 +233,31 @@ void launch_transpose(const double* in, int64_t rows, int64_t cols, int64_t ldin
   check_launch("transpose");
 }
 
-void launch_copy2d(const double* in, int64_t rows, int64_t cols, int64_t ldin, double* out,
-                   int64_t ldout, cudaStream_t st) {
+template <typename Tin, typename Tout>
+void launch_copy2d_cast(const Tin* in, int64_t rows, int64_t cols, int64_t ldin, Tout* out,
+                        int64_t ldout, cudaStream_t st) {
   if (rows <= 0 || cols <= 0) return;
   int blocks = (int)std::min<int64_t>(ceil_div(rows * cols, 256), kNumSMs * 8);
-  copy2d_kernel<<<blocks, 256, 0, st>>>(in, rows, cols, ldin, out, ldout);
+  copy2d_kernel<Tin, Tout><<<blocks, 256, 0, st>>>(in, rows, cols, ldin, out, ldout);
   check_launch("copy2d");
+}
+template void launch_copy2d_cast<double, double>(const double*, int64_t, int64_t, int64_t, double*,
+                                                 int64_t, cudaStream_t);
+template void launch_copy2d_cast<float, double>(const float*, int64_t, int64_t, int64_t, double*,
+                                                int64_t, cudaStream_t);
+template void launch_copy2d_cast<double, float>(const double*, int64_t, int64_t, int64_t, float*,
+                                                int64_t, cudaStream_t);
+
+void launch_copy2d(const double* in, int64_t rows, int64_t cols, int64_t ldin, double* out,
+                   int64_t ldout, cudaStream_t st) {
+  launch_copy2d_cast<double, double>(in, rows, cols, ldin, out, ldout, st);
+}
+
+void launch_round_f32(double* p, int64_t rows, int64_t cols, int64_t ld, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return;
+  int blocks = (int)std::min<int64_t>(ceil_div(rows * cols, 256), kNumSMs * 8);
+  round_f32_kernel<<<blocks, 256, 0, st>>>(p, rows, cols, ld);
+  check_launch("round_f32");
 }
 
 void launch_zero(double* p, size_t count, cudaStream_t st) {

@@ -13,7 +13,11 @@
 //            M's columns and the accumulated right rotations J both live in
 //            shared memory when they fit. Output sorted descending (stable,
 //            kernels.py:535) with the sign rule of kernels.py:556-561.
+#include <cooperative_groups.h>
+
 #include <cfloat>
+#include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 
@@ -245,6 +249,146 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = lane; i < k; i += 32) Wk[(int64_t)r * ldw + i] = gsign[i] * J[(int64_t)gperm[i] * l + r];
 }
 
+// ---------------------------------------------------------------------------
+// Cooperative multi-CTA Jacobi for large l (l x l does not fit one SM's
+// shared memory: cfg4 l=220, cfg5 l=550). X and J live in global memory
+// (L2-resident: 2 l^2 doubles), one warp per column pair, a grid-wide
+// barrier between rounds. Same rotation, ordering, sort and sign rule as
+// the single-CTA kernel.
+__global__ void __launch_bounds__(256)
+    jacobi_coop_kernel(const double* __restrict__ Rm, int64_t ldr, int l, int k,
+                       double* __restrict__ Ub, int64_t ldu, double* __restrict__ s_out,
+                       double* __restrict__ Wk, int64_t ldw, double* __restrict__ work,
+                       int* __restrict__ status, double tol, int max_sweeps) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  const int64_t ll = (int64_t)l * l;
+  double* X = work;
+  double* J = work + ll;
+  double* gnorm = work + 2 * ll;
+  int* gperm = reinterpret_cast<int*>(gnorm + l);
+  int* gsign = gperm + l;
+  int* rotflag = gsign + l;  // max_sweeps ints, zeroed here
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t gthreads = (int64_t)gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31;
+  const int gwarp = (int)(gtid >> 5);
+  const int nwarps = (int)(gthreads >> 5);
+  for (int64_t idx = gtid; idx < ll; idx += gthreads) {
+    const int c = (int)(idx / l), r = (int)(idx - (int64_t)c * l);
+    X[idx] = Rm[(int64_t)c * ldr + r];
+    J[idx] = (r == c) ? 1.0 : 0.0;
+  }
+  for (int64_t i = gtid; i < max_sweeps; i += gthreads) rotflag[i] = 0;
+  grid.sync();
+  const int L2 = l + (l & 1);
+  const int npairs = L2 / 2;
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    for (int round = 0; round < L2 - 1; ++round) {
+      for (int pi = gwarp; pi < npairs; pi += nwarps) {
+        const int pa = pi, pb = L2 - 1 - pi;
+        int p = pa == 0 ? 0 : 1 + (pa - 1 + round) % (L2 - 1);
+        int q = 1 + (pb - 1 + round) % (L2 - 1);
+        if (p > q) {
+          const int t = p;
+          p = q;
+          q = t;
+        }
+        if (q >= l) continue;
+        double* xp = X + (int64_t)p * l;
+        double* xq = X + (int64_t)q * l;
+        double a = 0.0, b = 0.0, g = 0.0;
+        // L2-coherent loads (__ldcg): columns move between SMs every round
+        for (int r = lane; r < l; r += 32) {
+          const double u = __ldcg(xp + r), v = __ldcg(xq + r);
+          a = fma(u, u, a);
+          b = fma(v, v, b);
+          g = fma(u, v, g);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          a += __shfl_xor_sync(0xffffffffu, a, o);
+          b += __shfl_xor_sync(0xffffffffu, b, o);
+          g += __shfl_xor_sync(0xffffffffu, g, o);
+        }
+        if (g != 0.0 && fabs(g) > tol * sqrt(a * b)) {
+          const double zeta = (b - a) / (2.0 * g);
+          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          const double cs = 1.0 / sqrt(1.0 + t * t);
+          const double sn = cs * t;
+          double* jp = J + (int64_t)p * l;
+          double* jq = J + (int64_t)q * l;
+          for (int r = lane; r < l; r += 32) {
+            const double u = __ldcg(xp + r), v = __ldcg(xq + r);
+            __stcg(xp + r, cs * u - sn * v);
+            __stcg(xq + r, sn * u + cs * v);
+            const double uj = __ldcg(jp + r), vj = __ldcg(jq + r);
+            __stcg(jp + r, cs * uj - sn * vj);
+            __stcg(jq + r, sn * uj + cs * vj);
+          }
+          if (lane == 0) rotflag[sweep] = 1;
+        }
+      }
+      grid.sync();
+    }
+    if (*(volatile int*)&rotflag[sweep] == 0) break;
+  }
+  if (gtid == 0) *status = (sweep >= max_sweeps) ? 1 : 0;
+  for (int c = gwarp; c < l; c += nwarps) {
+    double a = 0.0;
+    for (int r = lane; r < l; r += 32) a += X[(int64_t)c * l + r] * X[(int64_t)c * l + r];
+    a = warp_sum32(a);
+    if (lane == 0) gnorm[c] = sqrt(a);
+  }
+  grid.sync();
+  for (int64_t j = gtid; j < l; j += gthreads) {
+    const double sj = gnorm[j];
+    int rank = 0;
+    for (int i = 0; i < l; ++i) {
+      const double si = gnorm[i];
+      rank += (si > sj) || (si == sj && i < (int)j);
+    }
+    gperm[rank] = (int)j;
+  }
+  grid.sync();
+  for (int i = gwarp; i < l; i += nwarps) {
+    const int c = gperm[i];
+    double best = -1.0;
+    int brow = 0;
+    for (int r = lane; r < l; r += 32) {
+      const double v = fabs(X[(int64_t)c * l + r]);
+      if (v > best) {
+        best = v;
+        brow = r;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int orow = __shfl_xor_sync(0xffffffffu, brow, o);
+      if (ob > best || (ob == best && orow < brow)) {
+        best = ob;
+        brow = orow;
+      }
+    }
+    if (lane == 0) gsign[i] = (X[(int64_t)c * l + brow] < 0.0) ? -1 : 1;
+  }
+  grid.sync();
+  for (int64_t i = gtid; i < l; i += gthreads) s_out[i] = gnorm[gperm[i]];
+  for (int64_t idx = gtid; idx < ll; idx += gthreads) {
+    const int r = (int)(idx / l), i = (int)(idx - (int64_t)r * l);
+    const int c = gperm[i];
+    const double sc = gnorm[c];
+    const double inv = sc > 0.0 ? 1.0 / sc : 0.0;
+    Ub[(int64_t)r * ldu + i] = gsign[i] * X[(int64_t)c * l + r] * inv;
+  }
+  for (int64_t idx = gtid; idx < (int64_t)l * k; idx += gthreads) {
+    const int r = (int)(idx / k), i = (int)(idx - (int64_t)r * k);
+    Wk[(int64_t)r * ldw + i] = gsign[i] * J[(int64_t)gperm[i] * l + r];
+  }
+}
+
 }  // namespace
 
 void launch_chol_inv(const double* G, int64_t ldg, int l, double tau, double* R, double* Rinv,
@@ -262,23 +406,47 @@ void launch_chol_inv(const double* G, int64_t ldg, int l, double tau, double* R,
   if (gw) XB_CUDA(cudaFreeAsync(gw, st));
 }
 
-size_t jacobi_work_doubles(int l) { return (size_t)l * l + 2 * (size_t)l + 8; }
+constexpr int kMaxSweeps = 60;
+
+size_t jacobi_work_doubles(int l) {
+  return 2 * (size_t)l * l + 3 * (size_t)l + kMaxSweeps + 16;
+}
 
 void launch_jacobi_svd(const double* R, int64_t ldr, int l, int k, double* Ub, int64_t ldu,
                        double* s, double* Wk, int64_t ldw, double* work, int* status,
                        cudaStream_t st) {
-  XB_REQUIRE(l <= 1024, XB_EUNSUPPORTED, "jacobi_svd: l > 1024");
   const size_t lim = max_dyn_smem() - 512;  // static: s_rot
   const size_t one = (size_t)l * l * sizeof(double);
-  XB_REQUIRE(one <= lim, XB_EUNSUPPORTED,
-             "jacobi_svd: l x l factor exceeds shared memory (multi-CTA Jacobi not built yet)");
+  const double tol = fmax(1e-15, (double)l * DBL_EPSILON);
+  // one CTA while M's columns fit in shared memory, else (or on request,
+  // XB_JACOBI=coop) the cooperative grid version
+  static const int mode = [] {
+    const char* e = getenv("XB_JACOBI");
+    return e ? (strcmp(e, "coop") == 0 ? 1 : (strcmp(e, "single") == 0 ? 2 : 0)) : 0;
+  }();
+  const bool coop = mode == 1 || (mode == 0 && one > lim);
+  if (coop) {
+    int dev = 0, per_sm = 0;
+    XB_CUDA(cudaGetDevice(&dev));
+    XB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_coop_kernel, 256, 0));
+    const int npairs = (l + (l & 1)) / 2;
+    int blocks = std::max(1, std::min((npairs + 7) / 8, kNumSMs * std::max(per_sm, 1)));
+    blocks = std::min(blocks, kNumSMs);
+    int max_sweeps = kMaxSweeps;
+    void* args[] = {(void*)&R, (void*)&ldr, (void*)&l, (void*)&k, (void*)&Ub, (void*)&ldu,
+                    (void*)&s, (void*)&Wk, (void*)&ldw, (void*)&work, (void*)&status,
+                    (void*)&tol, (void*)&max_sweeps};
+    XB_CUDA(cudaLaunchCooperativeKernel((void*)jacobi_coop_kernel, dim3(blocks), dim3(256), args, 0,
+                                        st));
+    check_launch("jacobi_coop");
+    return;
+  }
   const int j_in_smem = 2 * one <= lim;
   const size_t dyn = j_in_smem ? 2 * one : one;
   XB_CUDA(cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)dyn));
-  const double tol = fmax(1e-15, (double)l * DBL_EPSILON);
   jacobi_kernel<<<1, kThreads, dyn, st>>>(R, ldr, l, k, Ub, ldu, s, Wk, ldw, work, status,
-                                          j_in_smem, tol, 60);
+                                          j_in_smem, tol, kMaxSweeps);
   check_launch("jacobi_svd");
 }
 

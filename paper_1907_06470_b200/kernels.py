@@ -47,10 +47,13 @@ class SmallSVDResult:
     v: np.ndarray
 
 
-def _require_double(prec: Precision, what: str):
-    if as_precision(prec) is not Precision.DOUBLE:
-        raise XsvdError(f"{what}: {as_precision(prec).value} precision path is not built yet "
-                        "(the CUDA library currently implements float64)")
+def _device_dtype(prec: Precision, what: str):
+    """float64 for DOUBLE, float32 for SINGLE (the compute dtype's storage,
+    core.py:43-46). HALF (storage-only in the reference) is not built."""
+    prec = as_precision(prec)
+    if prec is Precision.HALF:
+        raise XsvdError(f"{what}: half precision is not built on the GPU path")
+    return np.float64 if prec is Precision.DOUBLE else np.float32
 
 
 def _canonical(mat):
@@ -71,11 +74,11 @@ def block_multiply(pool, x, y, out_id, *, threads: int = 1, out_precision=None):
         raise XsvdError("block_multiply: sparse operands are not built on the GPU path yet")
     prec = as_precision(out_precision) if out_precision is not None else wider(
         as_precision(x.desc.precision), as_precision(y.desc.precision))
-    _require_double(prec, "block_multiply")
+    dt = _device_dtype(prec, "block_multiply")
     ctx = _lib.load()
     a, ta = _canonical(x)
     b = stored_to_array(y)
-    c = ctx.gemm(np.asarray(a, np.float64), np.asarray(b, np.float64), trans_a=ta)
+    c = ctx.gemm(np.asarray(a, dt), np.asarray(b, dt), trans_a=ta)
     out = register_dense(pool, out_id, c.astype(prec.storage_dtype, copy=False), prec)
     return out, MultiplyStats(multiply_adds=m * n * k, threads_used=1)
 
@@ -91,8 +94,8 @@ def thin_qr(pool, y, q_id) -> QRResult:
     if m < r or r < 1:
         raise ShapeError(f"thin QR needs rows >= cols >= 1, got {m}x{r}")
     prec = as_precision(y.desc.precision)
-    _require_double(prec, "thin_qr")
-    q, rr, deficient = _lib.load().thin_qr(np.asarray(stored_to_array(y), np.float64))
+    dt = _device_dtype(prec, "thin_qr")
+    q, rr, deficient = _lib.load().thin_qr(np.asarray(stored_to_array(y), dt))
     qm = register_dense(pool, q_id, q.astype(prec.storage_dtype, copy=False), prec)
     return QRResult(q=qm, r=rr, deficient_columns=deficient)
 
