@@ -5,23 +5,29 @@
 
 A "step" is one full factorisation (Omega, 2q+1 products with
 re-orthonormalisation, projection, small SVD, lift) of the workload's A.
-Workload at N=1: config 2 (65536 x 16384 float64, k=100, p=20, q=2), the
-BASELINE.json config quoted for HBM-resident single-GPU runs.
+Workload at N=1 (default): config 2 (65536 x 16384 float64, k=100, p=20,
+q=2), the BASELINE.json config quoted for HBM-resident single-GPU runs.
+--config 1 / 3 / 5 run the other single-GPU configs (3: 1e6 x 2e5 CSR,
+5: 16384 x 1048576 float32); config 4 (256 GiB) does not fit one GPU.
 
-value  = matrix elements factorised per second (m*n / T_step) with A already
-         resident in HBM; T_step from CUDA events on the library's compute
-         stream over exactly K steps (barrier + synchronize on both sides,
-         max over ranks). A (8.6 GB) is far larger than L2 (126 MB), so no
-         L2 flush is needed between steps.
+value  = matrix elements factorised per second (m*n / T_step for dense,
+         nnz / T_step for sparse, SURVEY §8d) with A already resident in HBM;
+         T_step from CUDA events on the library's compute stream over exactly
+         K steps (barrier + synchronize on both sides, max over ranks). Every
+         config's A is larger than L2 (126 MB) except config 1 (64 MB), whose
+         line says so; no L2 flush is done.
 e2e    = the same metric through the reference-facing C ABI call
-         (xb_rsvd_dense) with HOST buffers: pinned A copied H2D inside the
-         timed region (overlapped with the sketch), U/s/V copied back.
-roofline = the dominant kernel (the FP64 DMMA tile GEMM over A: 6 launches
-         per step), achieved = 2*m*n*l flops per launch / its event-timed
-         average duration, peak = the FP64 DMMA pipe peak measured in-process
-         by a saturating microbenchmark (MEASURED_PEAKS.json has no FP64).
+         (xb_rsvd_dense / xb_rsvd_coo) with HOST buffers: pinned A copied
+         H2D inside the timed region (overlapped with the sketch), U/s/V
+         copied back.
+roofline = the dominant kernel: dense -> the FP64 DMMA tile GEMM over A
+         (achieved = 2*m*n*l flops per launch / its event-timed mean duration,
+         peak = the FP64 DMMA pipe rate measured in-process: MEASURED_PEAKS.json
+         has no FP64 figure); sparse -> the CSR SpMM (achieved = algorithmic
+         bytes per launch / duration, peak = MEASURED_PEAKS.json hbm_gbs).
 cpu_baseline = the oracle's restatement of the reference's shipped driver
-         (oracle/, "port") on a bounded row sample, on this host's cores.
+         (oracle/, "port") on two bounded samples of the workload, extrapolated
+         linearly to full size, on this host's cores.
 
 --impl reference prints the reference arm: the same port timed on all host
 threads (the reference is pure Python and cannot travel to the GPU box).
@@ -42,6 +48,8 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+STAGE_NAMES = ["Text Parsing", "Preparation of O", "O*A^T", "Orthogonalization", "A^T*Q_r",
+               "SVD0 Preparation", "SVD0", "Postprocessing"]
 
 
 def parse():
@@ -62,6 +70,14 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+def measured_peaks() -> dict:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
 
 
 # -- clocks during the timed region ----------------------------------------------
@@ -119,59 +135,59 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-# -- workloads ---------------------------------------------------------------------
+# -- CPU baseline (oracle port of the reference's shipped driver) -------------------
 
-def make_device_matrix(w, rows_lo, rows_hi, device):
-    """This rank's rows of the config's A, built on the GPU from the seeds."""
-    import torch
-
-    from paper_1907_06470_b200.workloads import dense_lowrank_torch
-
-    # the full-matrix construction is seeded once; every rank builds the same
-    # A and keeps its row block (construction cost is outside the timed region)
-    a = dense_lowrank_torch(w.m, w.n, w.spectrum, w.noise, w.cfg, w.signal_rank,
-                            dtype=torch.float64, device=device)
-    if rows_lo == 0 and rows_hi == w.m:
-        return a
-    part = a[rows_lo:rows_hi].clone()
-    del a
-    torch.cuda.empty_cache()
-    return part
-
-
-def _time_port(w, rows: int, threads: int) -> float:
+def _time_port(w, size: int, threads: int) -> float:
+    """One shipped-driver run on a sample: `size` rows (tall / sparse) or
+    columns (wide cfg5). Run time does not depend on A's spectrum (SURVEY
+    A.4), so dense samples use a seeded Gaussian A of the config's shape."""
     from oracle import pipeline as OP
 
-    # the reference's run time does not depend on A's spectrum (SURVEY A.4),
-    # so the CPU sample uses a seeded Gaussian A of the config's width
-    a = np.random.default_rng(3000 + w.cfg).standard_normal((rows, w.n))
+    rng = np.random.default_rng(3000 + w.cfg)
+    prec = w.precision
+    if w.density == "sparse":
+        from paper_1907_06470_b200.workloads import sparse_uniform_np
+
+        rowptr, col, val = sparse_uniform_np(size, w.n, 20, 3000 + w.cfg)
+        rows = np.repeat(np.arange(size), np.diff(rowptr))
+        a = OP.Coo(rows, col.astype(np.int64), val, (size, w.n))
+    elif w.m >= w.n:
+        a = rng.standard_normal((size, w.n)).astype(np.float64 if prec == "double" else np.float32)
+    else:
+        a = rng.standard_normal((w.m, size)).astype(np.float64 if prec == "double" else np.float32)
     t0 = time.perf_counter()
-    OP.randomized_svd(a, w.k, w.p, w.q, w.cfg, "double", threads=threads)
+    OP.randomized_svd(a, w.k, w.p, w.q, w.cfg, prec, threads=threads)
     return time.perf_counter() - t0
 
 
 def cpu_baseline(w, budget_s: float, threads: int) -> dict:
-    """Oracle port of the reference's shipped driver on two row samples of A,
-    extrapolated linearly in m to the full config (T = a + b*m, SURVEY §8d:
-    the products and panel QR are linear in m; Omega and svd_small are not)."""
-    r1 = min(w.m, 1024)
+    """Two bounded samples along the long dimension, extrapolated linearly
+    (T = a + b*size: products and panel QR are linear in the long
+    dimension)."""
+    long_dim = w.m if (w.m >= w.n or w.density == "sparse") else w.n
+    base = max(1024, w.l * 4)
+    if w.density == "sparse":
+        base = 20000
+    r1 = min(long_dim, base)
     t1 = _time_port(w, r1, threads)
-    # second sample sized to use the rest of the budget
-    per_row = max(t1 / r1, 1e-9)
-    r2 = int(min(w.m, max(2 * r1, (budget_s - t1) / per_row * 0.6)))
-    r2 = max(r1 + 256, (r2 // 256) * 256)
-    r2 = min(r2, w.m)
+    per = max(t1 / r1, 1e-9)
+    r2 = int(min(long_dim, max(2 * r1, (budget_s - t1) / per * 0.6)))
+    r2 = min(long_dim, max(r1 + 256, (r2 // 256) * 256))
     t2 = _time_port(w, r2, threads) if r2 > r1 else t1
     b = (t2 - t1) / (r2 - r1) if r2 > r1 else t1 / r1
     a0 = max(t1 - b * r1, 0.0)
-    t_full = a0 + b * w.m
-    return {"value": w.m * w.n / t_full, "unit": "elements/s", "cores": threads, "kind": "port",
+    t_full = a0 + b * long_dim
+    units = w.m * w.n if w.density == "dense" else w.m * 20
+    what = "rows" if long_dim == w.m else "columns"
+    shape1 = f"{r1}x{w.n}" if what == "rows" else f"{w.m}x{r1}"
+    shape2 = f"{r2}x{w.n}" if what == "rows" else f"{w.m}x{r2}"
+    return {"value": units / t_full, "unit": "elements/s", "cores": threads, "kind": "port",
             "sample": (f"oracle restatement of xsvd.randomized_svd (shipped driver: 256-cell "
                        f"block_multiply on {threads} threads, Householder thin_qr, Golub-Kahan "
-                       f"svd_small) on seeded Gaussian {r1}x{w.n} ({t1:.2f} s) and {r2}x{w.n} "
-                       f"({t2:.2f} s) samples, k={w.k} p={w.p} q={w.q}; extrapolated linearly in "
-                       f"m to {w.m} rows: {t_full:.1f} s"),
-            "seconds": t_full, "rows": r2, "sample_seconds": t2}
+                       f"svd_small) on seeded {w.density} {w.precision} {shape1} ({t1:.2f} s) and "
+                       f"{shape2} ({t2:.2f} s) samples, k={w.k} p={w.p} q={w.q}; extrapolated "
+                       f"linearly in {what} to the full {w.m}x{w.n}: {t_full:.1f} s"),
+            "seconds": t_full, "size": r2, "sample_seconds": t2, "a0": a0}
 
 
 def run_reference(args):
@@ -183,26 +199,27 @@ def run_reference(args):
     w = CONFIGS[args.config]
     threads = os.cpu_count() or 1
     # calibration (counts as warm-up): fixes the sample size and the
-    # m-independent part a0 of the linear time model
+    # size-independent part a0 of the linear time model
     base = cpu_baseline(w, args.cpu_budget_s, threads)
-    rows = base["rows"]
-    slope = (base["seconds"] - base["sample_seconds"]) / max(w.m - rows, 1)
-    a0 = max(base["sample_seconds"] - slope * rows, 0.0)
+    size, a0 = base["size"], base["a0"]
+    long_dim = w.m if (w.m >= w.n or w.density == "sparse") else w.n
     for _ in range(max(args.warmup - 1, 0)):
-        _time_port(w, rows, threads)
+        _time_port(w, size, threads)
     full = []
     for _ in range(args.steps):
-        t = _time_port(w, rows, threads)
-        full.append(a0 + (t - a0) * (w.m / rows))
+        t = _time_port(w, size, threads)
+        full.append(a0 + (t - a0) * (long_dim / size))
     dt = float(np.mean(full))
-    value = w.m * w.n / dt
+    units = w.m * w.n if w.density == "dense" else w.m * 20
+    value = units / dt
     line = {
         "impl": "reference", "metric": "rank-k rSVD matrix-elements/s", "value": value,
         "unit": "elements/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded cfg construction)",
-        "config": {"workload": w.name, "sample_rows": rows,
-                   "step": f"one {rows}x{w.n} sample run, extrapolated linearly in m"},
+        "vs_baseline": None, "dtype": "f64" if w.precision == "double" else "f32",
+        "data": "synthetic (seeded config construction)",
+        "config": {"workload": w.name, "sample": size,
+                   "step": "one bounded sample run, extrapolated linearly to full size"},
         "cpu_baseline": {"value": value, "unit": "elements/s", "cores": threads, "kind": "port",
                          "sample": base["sample"]},
         "e2e": {"value": value, "unit": "elements/s", "h2d_bytes_per_step": 0,
@@ -210,6 +227,112 @@ def run_reference(args):
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+# -- device workloads -----------------------------------------------------------------
+
+class DenseCase:
+    """Dense A resident on the device (torch tensor) + pinned host copy for e2e."""
+
+    def __init__(self, ctx, w, device):
+        import torch
+
+        from paper_1907_06470_b200.workloads import dense_lowrank_torch
+
+        self.ctx, self.w, self.device = ctx, w, device
+        self.torch_dtype = torch.float64 if w.precision == "double" else torch.float32
+        self.np_dtype = np.float64 if w.precision == "double" else np.float32
+        self.a = dense_lowrank_torch(w.m, w.n, w.spectrum, w.noise, w.cfg, w.signal_rank,
+                                     dtype=self.torch_dtype, device=device)
+        self.u = torch.empty((w.m, w.k), dtype=self.torch_dtype, device=device)
+        self.v = torch.empty((w.n, w.k), dtype=self.torch_dtype, device=device)
+        self.s = torch.empty((w.k,), dtype=torch.float64, device=device)
+        self.units = w.m * w.n
+        self.esz = 8 if w.precision == "double" else 4
+
+    def step(self):
+        w = self.w
+        return self.ctx.rsvd_dense_dev(self.np_dtype, w.m, w.n, self.a.data_ptr(), w.n, w.k, w.p,
+                                       w.q, w.cfg, self.u.data_ptr(), self.s.data_ptr(),
+                                       self.v.data_ptr())[1]
+
+    def prepare_e2e(self):
+        import torch
+
+        self.a_host = torch.empty((self.w.m, self.w.n), dtype=self.torch_dtype, pin_memory=True)
+        self.a_host.copy_(self.a)
+        del self.a
+        torch.cuda.empty_cache()
+        self.a_np = self.a_host.numpy()
+
+    def e2e(self):
+        w = self.w
+        return self.ctx.rsvd_dense(self.a_np, w.k, w.p, w.q, w.cfg)[4]
+
+    def io_bytes(self):
+        w = self.w
+        return w.m * w.n * self.esz, (w.m + w.n) * w.k * self.esz + w.k * 8
+
+    def roofline(self, prof, dmma_peak, dfma_peak, hbm_peak):
+        per_s = prof["seconds"] / max(prof["launches"], 1)
+        achieved = prof["flops"] / max(prof["launches"], 1) / per_s / 1e12
+        return {"bound": "tensor", "achieved": achieved, "peak": dmma_peak, "unit": "TFLOP/s",
+                "frac": achieved / dmma_peak if dmma_peak else None,
+                "kernel": "dgemm_kernel (FP64 DMMA m8n8k4, NN/TN over A"
+                          + (", float32 A widened to f64)" if self.esz == 4 else ")"),
+                "peak_source": f"in-process DMMA microbenchmark ({dmma_peak:.1f} TF/s; DFMA "
+                               f"{dfma_peak:.1f} TF/s); MEASURED_PEAKS.json has no FP64 entry",
+                "hbm_gbs_achieved": prof["bytes"] / prof["seconds"] / 1e9 if prof["seconds"] else None}
+
+
+class SparseCase:
+    """CSR A resident on the device; host COO for e2e."""
+
+    def __init__(self, ctx, w, device):
+        import torch
+
+        from paper_1907_06470_b200.workloads import sparse_uniform_np
+
+        self.ctx, self.w = ctx, w
+        rowptr, col, val = sparse_uniform_np(w.m, w.n, 20, 3000 + w.cfg)
+        self.rows_np = np.repeat(np.arange(w.m, dtype=np.int64), np.diff(rowptr))
+        self.cols_np = col.astype(np.int64)
+        self.vals_np = val
+        self.nnz = len(val)
+        self.rowptr = torch.from_numpy(rowptr).to(device)
+        self.col = torch.from_numpy(col).to(device)
+        self.val = torch.from_numpy(val).to(device)
+        self.u = torch.empty((w.m, w.k), dtype=torch.float64, device=device)
+        self.v = torch.empty((w.n, w.k), dtype=torch.float64, device=device)
+        self.s = torch.empty((w.k,), dtype=torch.float64, device=device)
+        self.units = self.nnz
+
+    def step(self):
+        w = self.w
+        return self.ctx.rsvd_csr_dev(w.m, w.n, self.nnz, self.rowptr.data_ptr(), self.col.data_ptr(),
+                                     self.val.data_ptr(), w.k, w.p, w.q, w.cfg, self.u.data_ptr(),
+                                     self.s.data_ptr(), self.v.data_ptr())[1]
+
+    def prepare_e2e(self):
+        pass
+
+    def e2e(self):
+        w = self.w
+        return self.ctx.rsvd_coo(self.rows_np, self.cols_np, self.vals_np, (w.m, w.n), w.k, w.p,
+                                 w.q, w.cfg)[4]
+
+    def io_bytes(self):
+        w = self.w
+        return self.nnz * 24, (w.m + w.n) * w.k * 8 + w.k * 8
+
+    def roofline(self, prof, dmma_peak, dfma_peak, hbm_peak):
+        per_s = prof["seconds"] / max(prof["launches"], 1)
+        achieved = prof["bytes"] / max(prof["launches"], 1) / per_s / 1e9
+        return {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": achieved / hbm_peak if hbm_peak else None,
+                "kernel": "spmm_kernel (CSR gather SpMM, warp per row; A and A^T CSR)",
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy bandwidth)",
+                "algorithmic_bytes": "12 nnz + 8 (rows+1) + 8 l (cols_in + rows_out) per launch"}
 
 
 def run_ours(args):
@@ -225,25 +348,16 @@ def run_ours(args):
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     w = CONFIGS[args.config]
-    if w.density != "dense" or w.precision != "double":
-        raise SystemExit(f"config {args.config} ({w.density}/{w.precision}) not built yet")
+    if args.config == 4:
+        raise SystemExit("config 4 (256 GiB f32) exceeds one GPU's HBM; see DESIGN.md")
     if world > 1:
         raise SystemExit("multi-GPU row sharding lands with the NCCL reducer (DESIGN.md)")
     ctx = _lib.load(local)
-    m, n, k, p, q = w.m, w.n, w.k, w.p, w.q
-    l = k + p
-    a = make_device_matrix(w, 0, m, device)
-    u = torch.empty((m, k), dtype=torch.float64, device=device)
-    v = torch.empty((n, k), dtype=torch.float64, device=device)
-    s = torch.empty((k,), dtype=torch.float64, device=device)
+    case = SparseCase(ctx, w, device) if w.density == "sparse" else DenseCase(ctx, w, device)
     torch.cuda.synchronize()
 
-    def step():
-        return ctx.rsvd_dense_dev(np.float64, m, n, a.data_ptr(), n, k, p, q, w.cfg,
-                                  u.data_ptr(), s.data_ptr(), v.data_ptr())
-
     for _ in range(args.warmup):
-        step()
+        case.step()
     stream = torch.cuda.ExternalStream(ctx.stream_ptr, device=device)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ctx.profile(True)
@@ -252,12 +366,11 @@ def run_ours(args):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    stage_tot = np.zeros(8)
     with ClockSampler(local) as clocks:
         ev0.record(stream)
-        stage_tot = np.zeros(8)
         for _ in range(args.steps):
-            _, stages = step()
-            stage_tot += stages
+            stage_tot += case.step()
         ev1.record(stream)
         torch.cuda.synchronize()
     launches = ctx.launches - launches0
@@ -268,69 +381,59 @@ def run_ours(args):
         t = torch.tensor([ms], device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    value = m * n / (ms * 1e-3)
+    value = case.units / (ms * 1e-3)
 
-    # roofline of the dominant kernel (FP64 DMMA tile GEMM on A)
     dmma_peak, dfma_peak = ctx.fp64_peaks()
-    per_launch_s = prof["seconds"] / max(prof["launches"], 1)
-    per_launch_flops = prof["flops"] / max(prof["launches"], 1)
-    achieved = per_launch_flops / per_launch_s / 1e12
+    hbm_peak = measured_peaks().get("hbm_gbs", 6650.0)
+    roofline = case.roofline(prof, dmma_peak, dfma_peak, hbm_peak)
+    roofline["launches_per_step"] = prof["launches"] / args.steps
+    roofline["share_of_step"] = prof["seconds"] / (ms * 1e-3 * args.steps)
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
             traffic = json.load(f).get(f"cfg{w.cfg}")
-    roofline = {"bound": "tensor", "achieved": achieved, "peak": dmma_peak, "unit": "TFLOP/s",
-                "frac": achieved / dmma_peak if dmma_peak else None, "traffic": traffic,
-                "kernel": "dgemm_kernel (FP64 DMMA m8n8k4, NN/TN over A)",
-                "launches_per_step": prof["launches"] / args.steps,
-                "share_of_step": prof["seconds"] / (ms * 1e-3 * args.steps),
-                "peak_source": f"in-process DMMA microbenchmark ({dmma_peak:.1f} TF/s; DFMA "
-                               f"{dfma_peak:.1f} TF/s); MEASURED_PEAKS.json has no FP64 entry",
-                "hbm_gbs_achieved": prof["bytes"] / prof["seconds"] / 1e9 if prof["seconds"] else None}
+    roofline["traffic"] = traffic
 
-    # e2e through the host-buffer C ABI call (pinned A, copies inside the timed region)
     e2e = None
     if args.e2e_steps > 0:
-        a_host = torch.empty((m, n), dtype=torch.float64, pin_memory=True)
-        a_host.copy_(a)
-        del a
-        torch.cuda.empty_cache()
-        a_np = a_host.numpy()
-        ctx.rsvd_dense(a_np, k, p, q, w.cfg)  # warm (allocates the host-path buffers)
+        case.prepare_e2e()
+        case.e2e()  # warm (allocates the host-path buffers)
         e2e_t, ingest = [], []
         for _ in range(args.e2e_steps):
             t0 = time.perf_counter()
-            U, S, V, _, st = ctx.rsvd_dense(a_np, k, p, q, w.cfg)
+            st = case.e2e()
             e2e_t.append(time.perf_counter() - t0)
             ingest.append(st[0])
         e2e_s = float(np.median(e2e_t))
-        e2e = {"value": m * n / e2e_s, "unit": "elements/s", "h2d_bytes_per_step": m * n * 8,
-               "d2h_bytes_per_step": (m * k + n * k + k) * 8, "seconds": e2e_s,
-               "h2d_gbs": m * n * 8 / float(np.median(ingest)) / 1e9 if min(ingest) > 0 else None,
+        h2d, d2h = case.io_bytes()
+        e2e = {"value": case.units / e2e_s, "unit": "elements/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "seconds": e2e_s,
+               "ingest_s": float(np.median(ingest)),
                "timer": "host perf_counter around the synchronous C ABI call"}
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         cpu = cpu_baseline(w, args.cpu_budget_s, os.cpu_count() or 1)
-        for key in ("seconds", "rows", "sample_seconds"):
+        for key in ("seconds", "size", "sample_seconds", "a0"):
             cpu.pop(key, None)
 
-    stage_names = ["Text Parsing", "Preparation of O", "O*A^T", "Orthogonalization", "A^T*Q_r",
-                   "SVD0 Preparation", "SVD0", "Postprocessing"]
+    l2 = ("inputs larger than L2, no flush" if case.units * (8 if w.precision == "double" else 4)
+          > 126e6 else "A (64 MB) fits L2; no flush between steps")
     line = {
         "metric": "rank-k rSVD matrix-elements/s", "value": value, "unit": "elements/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic: A = U diag(i^-1.5) V^T + 1e-8 N(0,1), U/V Haar from seed 1002/2002 "
-                "(built on the GPU with torch, outside the timed region)",
-        "config": {"workload": w.name, "m": m, "n": n, "k": k, "p": p, "q": q, "l": l,
-                   "omega": "gaussian_band(seed=2) generated on device each step",
-                   "l2": "inputs larger than L2 (A = 8.6 GB), no flush",
-                   "parallelism": f"rows{world}"},
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64" if w.precision == "double" else "f32",
+        "data": (f"synthetic, seeded: {w.spectrum} spectrum, noise {w.noise}"
+                 if w.density == "dense" else "synthetic, seeded: 20 uniform columns/row, N(0,1)")
+                + " (built on the device/host outside the timed region)",
+        "config": {"workload": w.name, "m": w.m, "n": w.n, "k": w.k, "p": w.p, "q": w.q,
+                   "l": w.l, "omega": f"gaussian_band(seed={w.cfg}) generated on device each step",
+                   "l2": l2, "parallelism": f"rows{world}"},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
         "clocks": clocks.summary(),
-        "stage_ms": {nm: 1e3 * t / args.steps for nm, t in zip(stage_names, stage_tot)},
+        "stage_ms": {nm: 1e3 * t / args.steps for nm, t in zip(STAGE_NAMES, stage_tot)},
     }
     if rank == 0:
         print(json.dumps(line), flush=True)

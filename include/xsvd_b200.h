@@ -109,6 +109,33 @@ int xb_rsvd_dense_dev(xb_ctx* ctx, int dtype, int64_t m, int64_t n, const void* 
                       void* dU, int64_t ldu, double* d_s, void* dV, int64_t ldv,
                       int32_t* deficient, int* ndeficient, double* stage_seconds);
 
+/*
+ * Sparse A — replaces randomized_svd on a SPARSE StoredMatrix, i.e. the
+ * sparse x dense and dense x sparse products of kernels.py:85-112 (Y = A X,
+ * Z = A^T Q via a once-built CSR of A^T, B^T = A^T Q). A arrives as the
+ * reference's SparseBlock COO (core.py:245-284): int64 rows/cols,
+ * (row, col)-sorted without duplicates, float64 values (Precision.DOUBLE).
+ * Host buffers; same outputs as xb_rsvd_dense.
+ */
+int xb_rsvd_coo(xb_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const int64_t* rows,
+                const int64_t* cols, const double* vals, const double* omega, uint64_t seed,
+                int k, int p, int q, double* U, int64_t ldu, double* s, double* V, int64_t ldv,
+                int32_t* deficient, int* ndeficient, double* stage_seconds);
+/* Device-resident CSR variant: rowptr int64[m+1], col int32[nnz] (sorted
+ * within rows), val f64[nnz]; U, s, V device pointers. */
+int xb_rsvd_csr_dev(xb_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const int64_t* d_rowptr,
+                    const int32_t* d_col, const double* d_val, const double* d_omega,
+                    uint64_t seed, int k, int p, int q, double* dU, int64_t ldu, double* d_s,
+                    double* dV, int64_t ldv, int32_t* deficient, int* ndeficient,
+                    double* stage_seconds);
+/* Sparse product step (block_multiply with a sparse left operand,
+ * kernels.py:85-97, or its transposed view, pool.py:420-445): Y = op(A) X
+ * with op(A) = A (trans = 0, X n x l, Y m x l) or A^T (trans = 1, X m x l,
+ * Y n x l). COO as above; host buffers, row-major, f64. */
+int xb_spmm_coo(xb_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const int64_t* rows,
+                const int64_t* cols, const double* vals, int trans, const double* X, int64_t l,
+                double* Y);
+
 /* Omega generator — replaces gaussian_band (rng.py:38-70): rows
  * [row0, row0+rows) x cols of N(0,1), cast to `dtype`, row-major `ld`.
  * The uint64 hash stage is bit-exact; log/sin/cos are within a few ulp. */

@@ -42,6 +42,11 @@ SIGNATURES = [
                              _vp, _i64, _vp, _vp, _i64, _vp, _intp, _vp]),
     ("xb_rsvd_dense_dev", _int, [_vp, _int, _i64, _i64, _vp, _i64, _vp, _u64, _int, _int, _int,
                                  _vp, _i64, _vp, _vp, _i64, _vp, _intp, _vp]),
+    ("xb_rsvd_coo", _int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _u64, _int, _int, _int,
+                           _vp, _i64, _vp, _vp, _i64, _vp, _intp, _vp]),
+    ("xb_rsvd_csr_dev", _int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _u64, _int, _int, _int,
+                               _vp, _i64, _vp, _vp, _i64, _vp, _intp, _vp]),
+    ("xb_spmm_coo", _int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _int, _vp, _i64, _vp]),
     ("xb_gaussian", _int, [_vp, _int, _u64, _i64, _i64, _i64, _vp, _i64]),
     ("xb_uniform_bits", _int, [_vp, _u64, _i64, _i64, _i64, _vp]),
     ("xb_gemm", _int, [_vp, _int, _int, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64]),
@@ -160,6 +165,65 @@ class Context:
             C.c_void_p(u_ptr), k, C.c_void_p(s_ptr), C.c_void_p(v_ptr), k, _ptr(deficient),
             C.byref(ndef), _ptr(stages)))
         return tuple(int(x) for x in deficient[: ndef.value]), stages
+
+    # -- sparse A ----------------------------------------------------------------------
+    @staticmethod
+    def _coo(rows, cols, vals):
+        """int64 (row, col)-sorted COO, the SparseBlock invariant (core.py:245-284)."""
+        r = np.ascontiguousarray(rows, dtype=np.int64)
+        c = np.ascontiguousarray(cols, dtype=np.int64)
+        v = np.ascontiguousarray(vals, dtype=np.float64)
+        if len(r) > 1 and not np.all((r[1:] > r[:-1]) | ((r[1:] == r[:-1]) & (c[1:] > c[:-1]))):
+            order = np.lexsort((c, r))
+            r, c, v = r[order], c[order], v[order]
+        return r, c, v
+
+    def rsvd_coo(self, rows, cols, vals, shape, k, p, q, seed, omega=None):
+        """Sparse A (COO host arrays) in, host factors out (xb_rsvd_coo)."""
+        m, n = shape
+        r, c, v = self._coo(rows, cols, vals)
+        l = k + p
+        u = np.empty((m, k))
+        vv = np.empty((n, k))
+        s = np.empty(k)
+        deficient = np.zeros(max(l, 1), dtype=np.int32)
+        ndef = C.c_int(0)
+        stages = np.zeros(NUM_STAGES)
+        om = None
+        if omega is not None:
+            om = np.ascontiguousarray(omega, dtype=np.float64)
+            if om.shape != (n, l):
+                raise XsvdError(f"omega must be {(n, l)}, got {om.shape}")
+        _check(self.lib.xb_rsvd_coo(
+            self.h, m, n, len(v), _ptr(r), _ptr(c), _ptr(v), _ptr(om) if om is not None else None,
+            int(seed) & (2**64 - 1), k, p, q, _ptr(u), k, _ptr(s), _ptr(vv), k, _ptr(deficient),
+            C.byref(ndef), _ptr(stages)))
+        return u, s, vv, tuple(int(x) for x in deficient[: ndef.value]), stages
+
+    def rsvd_csr_dev(self, m, n, nnz, rowptr_ptr, col_ptr, val_ptr, k, p, q, seed, u_ptr, s_ptr,
+                     v_ptr):
+        deficient = np.zeros(max(k + p, 1), dtype=np.int32)
+        ndef = C.c_int(0)
+        stages = np.zeros(NUM_STAGES)
+        _check(self.lib.xb_rsvd_csr_dev(
+            self.h, m, n, nnz, C.c_void_p(rowptr_ptr), C.c_void_p(col_ptr), C.c_void_p(val_ptr),
+            None, int(seed) & (2**64 - 1), k, p, q, C.c_void_p(u_ptr), k, C.c_void_p(s_ptr),
+            C.c_void_p(v_ptr), k, _ptr(deficient), C.byref(ndef), _ptr(stages)))
+        return tuple(int(x) for x in deficient[: ndef.value]), stages
+
+    def spmm(self, rows, cols, vals, shape, x, trans=False):
+        """op(A) @ x for a COO A on the device (xb_spmm_coo)."""
+        m, n = shape
+        r, c, v = self._coo(rows, cols, vals)
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        if x.ndim != 2 or x.shape[0] != (m if trans else n):
+            from .errors import ShapeError
+
+            raise ShapeError(f"inner dimensions disagree: {'A^T' if trans else 'A'} {shape} x {x.shape}")
+        out = np.empty((n if trans else m, x.shape[1]))
+        _check(self.lib.xb_spmm_coo(self.h, m, n, len(v), _ptr(r), _ptr(c), _ptr(v), int(trans),
+                                    _ptr(x), x.shape[1], _ptr(out)))
+        return out
 
     # -- step-level operators -------------------------------------------------------
     def gaussian(self, seed, row0, rows, cols, dtype=np.float64):

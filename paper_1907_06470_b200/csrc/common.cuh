@@ -80,6 +80,25 @@ int dgemm_plan_splits(const DGemmArgs& g);
 size_t dgemm_workspace_doubles(const DGemmArgs& g, int splits);
 void dgemm(const DGemmArgs& g, int splits, double* work, cudaStream_t st);
 
+// Sparse A in CSR (device pointers): rowptr int64[rows+1], col int32[nnz],
+// val f64[nnz]; columns sorted within each row.
+struct Csr {
+  int64_t rows = 0, cols = 0, nnz = 0;
+  const int64_t* rowptr = nullptr;
+  const int32_t* col = nullptr;
+  const double* val = nullptr;
+};
+// Y (rows x l, ldy) = A X, X (cols x l, ldx). Deterministic gather SpMM.
+void launch_spmm(const Csr& a, const double* X, int64_t ldx, double* Y, int64_t ldy, int l,
+                 cudaStream_t st);
+// COO (rows sorted, int64 indices) -> CSR rowptr + int32 columns.
+void launch_coo_to_csr(const int64_t* rows, const int64_t* cols, int64_t nnz, int64_t m,
+                       int64_t* rowptr, int32_t* col32, cudaStream_t st);
+// CSR of A^T (cols x rows): tptr[cols+1], trow[nnz], tval[nnz]; each segment
+// ordered by row. scratch: cols+1 counters.
+void launch_csr_transpose(const Csr& a, int64_t* tptr, int32_t* trow, double* tval,
+                          unsigned long long* scratch, cudaStream_t st);
+
 // Cholesky of the leading l x l block of G (ld = ldg): writes upper R and
 // R^{-1} (ld = ldr, zero outside l x l), sets *flag = 1 when a pivot falls
 // below tau * G_jj (not numerically positive definite). Diag of R is added

@@ -296,13 +296,57 @@ struct IngestPlan {
   int64_t chunk_rows = 0;
 };
 
-// One factorisation. A (device, f64 or f32) is only touched by the five or
-// more products over A; everything downstream of a product is f64. With an
+// The operator A: dense (f64/f32, DMMA tile GEMM) or sparse (CSR of A and of
+// A^T, gather SpMM). The reference dispatches the same way on density
+// (kernels.py:79-112).
+struct AOp {
+  bool sparse = false;
+  AView dense{nullptr, 0, false};
+  Csr csr, csrt;  // A (m x n) and A^T (n x m)
+};
+
+void spmm_on_a(xb_ctx* c, const Csr& s, const double* X, double* Y, int lp, int l) {
+  cudaEvent_t b = nullptr, e = nullptr;
+  if (c->profiling) {
+    b = c->prof_event();
+    e = c->prof_event();
+    XB_CUDA(cudaEventRecord(b, c->st));
+  }
+  launch_spmm(s, X, lp, Y, lp, lp, c->st);
+  if (c->profiling) {
+    XB_CUDA(cudaEventRecord(e, c->st));
+    // algorithmic bytes: 12 nnz + 8 (rows+1) + 8 l (cols_in + rows_out)
+    const double bytes = 12.0 * s.nnz + 8.0 * (s.rows + 1) + 8.0 * l * (s.cols + s.rows);
+    c->prof_pending.push_back({b, e, 2.0 * s.nnz * l, bytes});
+  }
+}
+
+// Y (m x lp) = A X
+void op_nn(xb_ctx* c, const AOp& op, int64_t m, int64_t n, const double* X, double* Y, int lp,
+           int l) {
+  if (op.sparse)
+    spmm_on_a(c, op.csr, X, Y, lp, l);
+  else
+    gemm_on_a(c, false, m, lp, n, op.dense, 0, X, lp, Y, lp, l);
+}
+
+// Z (n x lp) = A^T Q
+void op_tn(xb_ctx* c, const AOp& op, int64_t m, int64_t n, const double* Q, double* Z, int lp,
+           int l) {
+  if (op.sparse)
+    spmm_on_a(c, op.csrt, Q, Z, lp, l);
+  else
+    gemm_on_a(c, true, n, lp, m, op.dense, 0, Q, lp, Z, lp, l);
+}
+
+// One factorisation. A (device, f64 or f32 dense, or f64 CSR) is only touched
+// by the products over A; everything downstream of a product is f64. With an
 // f32 A, Omega is rounded through float32 first, as the reference stores it
 // at the storage dtype (pipeline.py:281-282).
-void rsvd_impl(xb_ctx* c, const AView& a, int64_t m, int64_t n, const void* d_omega,
+void rsvd_impl(xb_ctx* c, const AOp& op, int64_t m, int64_t n, const void* d_omega,
                int64_t ld_omega, uint64_t seed, int k, int p, int q, const RsvdOut& out,
                int32_t* deficient, int* ndeficient, double* stage_seconds, const IngestPlan& ing) {
+  const AView& a = op.dense;
   check_dims(m, n, k, p, q);
   const int l = k + p;
   const int lp = (int)round_up(l, 8);
@@ -395,17 +439,17 @@ void rsvd_impl(xb_ctx* c, const AView& a, int64_t m, int64_t n, const void* d_om
     cudaEventDestroy(t0);
     cudaEventDestroy(t1);
   } else {
-    gemm_on_a(c, false, m, lp, n, a, 0, Om, lp, Ym, lp, l);
+    op_nn(c, op, m, n, Om, Ym, lp, l);
   }
   clk.enter(kOrtho);
   cholqr2(c, s, Ym, m, Tm, Qm, q == 0 ? Rf : nullptr);
   for (int it = 0; it < q; ++it) {
     clk.enter(kSketch);
-    gemm_on_a(c, true, n, lp, m, a, 0, Qm, lp, Zn, lp, l);  // Z = A^T Q
+    op_tn(c, op, m, n, Qm, Zn, lp, l);  // Z = A^T Q
     clk.enter(kOrtho);
     cholqr2(c, s, Zn, n, Tn, Qn, nullptr);
     clk.enter(kSketch);
-    gemm_on_a(c, false, m, lp, n, a, 0, Qn, lp, Ym, lp, l);  // Y = A Qz
+    op_nn(c, op, m, n, Qn, Ym, lp, l);  // Y = A Qz
     clk.enter(kOrtho);
     cholqr2(c, s, Ym, m, Tm, Qm, it == q - 1 ? Rf : nullptr);
   }
@@ -413,7 +457,7 @@ void rsvd_impl(xb_ctx* c, const AView& a, int64_t m, int64_t n, const void* d_om
   launch_deficient(Rf, lp, l, a.f32 ? (double)FLT_EPSILON : DBL_EPSILON, defc, defc + 1, st);
 
   clk.enter(kProject);
-  gemm_on_a(c, true, n, lp, m, a, 0, Qm, lp, Zn, lp, l);  // B^T = A^T Q
+  op_tn(c, op, m, n, Qm, Zn, lp, l);  // B^T = A^T Q
 
   clk.enter(kSvdPrep);
   cholqr2(c, s, Zn, n, Tn, Qn, Rf);  // B^T = Q_B R_B
@@ -572,7 +616,8 @@ int xb_rsvd_dense_dev(xb_ctx* c, int dtype, int64_t m, int64_t n, const void* dA
     LaunchScope ls(c);
     const bool f32 = check_dtype(dtype);
     XB_REQUIRE(lda >= n && ldu >= k && ldv >= k, XB_EVALUE, "leading dimension too small");
-    const AView a{dA, lda, f32};
+    AOp a;
+    a.dense = AView{dA, lda, f32};
     if (!f32) {
       RsvdOut out{static_cast<double*>(dU), ldu, d_s, static_cast<double*>(dV), ldv};
       rsvd_impl(c, a, m, n, d_omega, k + p, seed, k, p, q, out, deficient, ndeficient,
@@ -625,8 +670,9 @@ int xb_rsvd_dense(xb_ctx* c, int dtype, int64_t m, int64_t n, const void* A, int
     ing.chunk_rows = std::min(rows, m);
     RsvdOut out{dU, k, ds, dV, k};
     const double t1 = now_s();
-    rsvd_impl(c, AView{dA, n, f32}, m, n, dO, l, seed, k, p, q, out, deficient, ndeficient,
-              stage_seconds, ing);
+    AOp op;
+    op.dense = AView{dA, n, f32};
+    rsvd_impl(c, op, m, n, dO, l, seed, k, p, q, out, deficient, ndeficient, stage_seconds, ing);
     const double t2 = now_s();
     void* oU = dU;
     void* oV = dV;
@@ -643,6 +689,125 @@ int xb_rsvd_dense(xb_ctx* c, int dtype, int64_t m, int64_t n, const void* A, int
     if (getenv("XB_TRACE"))
       fprintf(stderr, "[xb] rsvd_dense host: setup %.1f ms, ingest+compute %.1f ms, d2h %.1f ms\n",
               (t1 - t0) * 1e3, (t2 - t1) * 1e3, (now_s() - t2) * 1e3);
+  });
+}
+
+}  // extern "C"
+
+namespace {
+
+// Device CSR of A plus the once-built CSR of A^T (ingest, "Text Parsing").
+AOp sparse_op(xb_ctx* c, int64_t m, int64_t n, int64_t nnz, const int64_t* d_rowptr,
+              const int32_t* d_col, const double* d_val) {
+  AOp op;
+  op.sparse = true;
+  op.csr = Csr{m, n, nnz, d_rowptr, d_col, d_val};
+  auto* tptr = static_cast<int64_t*>(c->buf("t_ptr", (size_t)(n + 1) * 8));
+  auto* trow = static_cast<int32_t*>(c->buf("t_row", (size_t)std::max<int64_t>(nnz, 1) * 4));
+  double* tval = c->dbuf("t_val", (size_t)std::max<int64_t>(nnz, 1));
+  auto* scr = static_cast<unsigned long long*>(c->buf("t_scr", (size_t)(n + 1) * 8));
+  launch_csr_transpose(op.csr, tptr, trow, tval, scr, c->st);
+  op.csrt = Csr{n, m, nnz, tptr, trow, tval};
+  return op;
+}
+
+// Host COO -> device CSR (+ A^T). Returns the operator; timing into stage 0.
+AOp sparse_from_host_coo(xb_ctx* c, int64_t m, int64_t n, int64_t nnz, const int64_t* rows,
+                         const int64_t* cols, const double* vals) {
+  XB_REQUIRE(m >= 1 && n >= 1 && nnz >= 0, XB_ESHAPE, "bad sparse shape");
+  XB_REQUIRE(n < (int64_t)1 << 31 && m < (int64_t)1 << 31, XB_EUNSUPPORTED,
+             "sparse dimensions must fit int32 column indices");
+  const size_t nz = (size_t)std::max<int64_t>(nnz, 1);
+  auto* drows = static_cast<int64_t*>(c->buf("coo_r", nz * 8));
+  auto* dcols = static_cast<int64_t*>(c->buf("coo_c", nz * 8));
+  double* dval = c->dbuf("csr_v", nz);
+  auto* rowptr = static_cast<int64_t*>(c->buf("csr_p", (size_t)(m + 1) * 8));
+  auto* col32 = static_cast<int32_t*>(c->buf("csr_c", nz * 4));
+  if (nnz > 0) {
+    XB_CUDA(cudaMemcpyAsync(drows, rows, nnz * 8, cudaMemcpyHostToDevice, c->st));
+    XB_CUDA(cudaMemcpyAsync(dcols, cols, nnz * 8, cudaMemcpyHostToDevice, c->st));
+    XB_CUDA(cudaMemcpyAsync(dval, vals, nnz * 8, cudaMemcpyHostToDevice, c->st));
+  }
+  launch_coo_to_csr(drows, dcols, nnz, m, rowptr, col32, c->st);
+  return sparse_op(c, m, n, nnz, rowptr, col32, dval);
+}
+
+}  // namespace
+
+extern "C" {
+
+int xb_rsvd_csr_dev(xb_ctx* c, int64_t m, int64_t n, int64_t nnz, const int64_t* d_rowptr,
+                    const int32_t* d_col, const double* d_val, const double* d_omega,
+                    uint64_t seed, int k, int p, int q, double* dU, int64_t ldu, double* d_s,
+                    double* dV, int64_t ldv, int32_t* deficient, int* ndeficient,
+                    double* stage_seconds) {
+  return guarded([&] {
+    XB_REQUIRE(c, XB_EVALUE, "null context");
+    LaunchScope ls(c);
+    check_dims(m, n, k, p, q);
+    XB_REQUIRE(ldu >= k && ldv >= k, XB_EVALUE, "leading dimension too small");
+    AOp op = sparse_op(c, m, n, nnz, d_rowptr, d_col, d_val);
+    RsvdOut out{dU, ldu, d_s, dV, ldv};
+    rsvd_impl(c, op, m, n, d_omega, k + p, seed, k, p, q, out, deficient, ndeficient,
+              stage_seconds, IngestPlan{});
+  });
+}
+
+int xb_rsvd_coo(xb_ctx* c, int64_t m, int64_t n, int64_t nnz, const int64_t* rows,
+                const int64_t* cols, const double* vals, const double* omega, uint64_t seed,
+                int k, int p, int q, double* U, int64_t ldu, double* s, double* V, int64_t ldv,
+                int32_t* deficient, int* ndeficient, double* stage_seconds) {
+  return guarded([&] {
+    XB_REQUIRE(c, XB_EVALUE, "null context");
+    LaunchScope ls(c);
+    check_dims(m, n, k, p, q);
+    XB_REQUIRE(U && s && V && (nnz == 0 || (rows && cols && vals)), XB_EVALUE, "null buffer");
+    XB_REQUIRE(ldu >= k && ldv >= k, XB_EVALUE, "leading dimension too small");
+    const int l = k + p;
+    cudaEvent_t e0, e1;
+    XB_CUDA(cudaEventCreate(&e0));
+    XB_CUDA(cudaEventCreate(&e1));
+    XB_CUDA(cudaEventRecord(e0, c->st));
+    AOp op = sparse_from_host_coo(c, m, n, nnz, rows, cols, vals);
+    XB_CUDA(cudaEventRecord(e1, c->st));
+    double* dU = c->dbuf("U", (size_t)m * k);
+    double* dV = c->dbuf("V", (size_t)n * k);
+    double* ds = c->dbuf("s", (size_t)k);
+    double* dO = nullptr;
+    if (omega) {
+      dO = c->dbuf("omega_in", (size_t)n * l);
+      XB_CUDA(cudaMemcpyAsync(dO, omega, (size_t)n * l * 8, cudaMemcpyHostToDevice, c->st));
+    }
+    RsvdOut out{dU, k, ds, dV, k};
+    rsvd_impl(c, op, m, n, dO, l, seed, k, p, q, out, deficient, ndeficient, stage_seconds,
+              IngestPlan{});
+    XB_CUDA(cudaMemcpy2DAsync(U, ldu * 8, dU, k * 8, k * 8, m, cudaMemcpyDeviceToHost, c->st));
+    XB_CUDA(cudaMemcpy2DAsync(V, ldv * 8, dV, k * 8, k * 8, n, cudaMemcpyDeviceToHost, c->st));
+    XB_CUDA(cudaMemcpyAsync(s, ds, k * 8, cudaMemcpyDeviceToHost, c->st));
+    XB_CUDA(cudaStreamSynchronize(c->st));
+    float ms = 0.f;
+    XB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    if (stage_seconds) stage_seconds[kParse] += ms * 1e-3;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  });
+}
+
+int xb_spmm_coo(xb_ctx* c, int64_t m, int64_t n, int64_t nnz, const int64_t* rows,
+                const int64_t* cols, const double* vals, int trans, const double* X, int64_t l,
+                double* Y) {
+  return guarded([&] {
+    XB_REQUIRE(c, XB_EVALUE, "null context");
+    LaunchScope ls(c);
+    XB_REQUIRE(l >= 1 && l <= 576, XB_EUNSUPPORTED, "spmm: 1 <= l <= 576");
+    AOp op = sparse_from_host_coo(c, m, n, nnz, rows, cols, vals);
+    const Csr& s = trans ? op.csrt : op.csr;
+    double* dX = c->dbuf("spX", (size_t)s.cols * l);
+    double* dY = c->dbuf("spY", (size_t)s.rows * l);
+    XB_CUDA(cudaMemcpyAsync(dX, X, (size_t)s.cols * l * 8, cudaMemcpyHostToDevice, c->st));
+    launch_spmm(s, dX, l, dY, l, (int)l, c->st);
+    XB_CUDA(cudaMemcpyAsync(Y, dY, (size_t)s.rows * l * 8, cudaMemcpyDeviceToHost, c->st));
+    XB_CUDA(cudaStreamSynchronize(c->st));
   });
 }
 

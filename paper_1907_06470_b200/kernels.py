@@ -70,10 +70,10 @@ def block_multiply(pool, x, y, out_id, *, threads: int = 1, out_precision=None):
     k2, n = y.shape
     if k != k2:
         raise ShapeError(f"inner dimensions disagree: {x.shape} x {y.shape}")
-    if is_sparse(x) or is_sparse(y):
-        raise XsvdError("block_multiply: sparse operands are not built on the GPU path yet")
     prec = as_precision(out_precision) if out_precision is not None else wider(
         as_precision(x.desc.precision), as_precision(y.desc.precision))
+    if is_sparse(x) or is_sparse(y):
+        return _sparse_multiply(pool, x, y, out_id, prec, m, n)
     dt = _device_dtype(prec, "block_multiply")
     ctx = _lib.load()
     a, ta = _canonical(x)
@@ -81,6 +81,37 @@ def block_multiply(pool, x, y, out_id, *, threads: int = 1, out_precision=None):
     c = ctx.gemm(np.asarray(a, dt), np.asarray(b, dt), trans_a=ta)
     out = register_dense(pool, out_id, c.astype(prec.storage_dtype, copy=False), prec)
     return out, MultiplyStats(multiply_adds=m * n * k, threads_used=1)
+
+
+def _coo_view(mat):
+    """(rows, cols, vals, shape) of a sparse handle in VIEW coordinates."""
+    r, c, v = canonical_coo(mat)
+    if mat.desc.transposed:
+        r, c = c, r
+    return r, c, v, tuple(mat.shape)
+
+
+def _sparse_multiply(pool, x, y, out_id, prec, m, n):
+    """Sparse x dense (kernels.py:85-97) and dense x sparse (98-112) on the
+    device CSR SpMM; sparse x sparse (113-141) is off the hot path."""
+    if is_sparse(x) and is_sparse(y):
+        raise XsvdError("block_multiply: sparse x sparse is not built on the GPU path")
+    if as_precision(prec) is not Precision.DOUBLE:
+        raise XsvdError("block_multiply: sparse operands are built for float64 only")
+    ctx = _lib.load()
+    if is_sparse(x):
+        r, c, v, shape = _coo_view(x)
+        out = ctx.spmm(r, c, v, shape, np.asarray(stored_to_array(y), np.float64))
+        nnz = len(v)
+        ops = nnz * n
+    else:
+        # x @ y = (y^T x^T)^T with y sparse
+        r, c, v, shape = _coo_view(y)
+        xt = np.ascontiguousarray(np.asarray(stored_to_array(x), np.float64).T)
+        out = ctx.spmm(r, c, v, shape, xt, trans=True).T
+        ops = len(v) * m
+    res = register_dense(pool, out_id, np.ascontiguousarray(out), prec)
+    return res, MultiplyStats(multiply_adds=ops, threads_used=1)
 
 
 def gram(pool, b, out_id, *, threads: int = 1):

@@ -31,7 +31,7 @@ import numpy as np
 from . import _lib
 from .core import Precision, as_precision
 from .errors import ShapeError, XsvdError
-from .pool import is_sparse, register_dense, stored_to_array
+from .pool import canonical_coo, is_sparse, register_dense, stored_to_array
 
 STAGE_PARSE = "Text Parsing"
 STAGE_GAUSSIAN = "Preparation of O"
@@ -141,16 +141,24 @@ def randomized_svd(pool, a, config: RsvdConfig, *, threads: int = 1, runner=None
         raise XsvdError("power='auto' (auto_select_q) is outside the GPU hot path; pass an int")
     if config.gram_path:
         raise XsvdError("gram_path=True is outside the GPU hot path")
-    if is_sparse(a):
-        raise XsvdError("sparse A is not built on the GPU path yet")
     precision = as_precision(config.precision)
     if precision is Precision.HALF:
         raise XsvdError("half precision (storage-only in the reference) is not built on the GPU path")
     clock = clock or (runner.clock if runner is not None else StageClock())
-    host = _dense_input(a).astype(precision.storage_dtype, copy=False)
     ctx = _lib.load()
-    u, s, v, deficient, stages = ctx.rsvd_dense(host, config.rank, config.oversample,
-                                                int(config.power), config.seed)
+    if is_sparse(a):
+        if precision is not Precision.DOUBLE:
+            raise XsvdError("sparse A is built for float64 only")
+        rows, cols, vals = canonical_coo(a)
+        if a.desc.transposed:
+            rows, cols = cols, rows
+        u, s, v, deficient, stages = ctx.rsvd_coo(rows, cols, vals, tuple(a.shape), config.rank,
+                                                  config.oversample, int(config.power),
+                                                  config.seed)
+    else:
+        host = _dense_input(a).astype(precision.storage_dtype, copy=False)
+        u, s, v, deficient, stages = ctx.rsvd_dense(host, config.rank, config.oversample,
+                                                    int(config.power), config.seed)
     for name, sec in zip(STAGE_NAMES, stages):
         clock.seconds[name] += float(sec)
     register_dense(pool, "S", s.reshape(-1, 1), Precision.DOUBLE)

@@ -109,12 +109,22 @@ def dense_lowrank_torch(m: int, n: int, kind: str, noise: float, seed: int,
     u = haar(m, r)
     u.mul_(s)
     v = haar(n, r)
-    a = u @ v.T
+    # fill in row chunks of <= 2 GiB of f64 so wide/large A (cfg5: 16384 x 2^20)
+    # never materialises in f64
+    a = torch.empty((m, n), dtype=dtype, device=device)
+    chunk = max(1, min(m, (1 << 28) // max(n, 1)))
+    gn = torch.Generator(device=device)
+    gn.manual_seed(2000 + seed)
+    for r0 in range(0, m, chunk):
+        r1 = min(m, r0 + chunk)
+        blk = u[r0:r1] @ v.T
+        if noise:
+            blk.add_(torch.randn(r1 - r0, n, generator=gn, device=device, dtype=torch.float64),
+                     alpha=noise)
+        a[r0:r1].copy_(blk)
+        del blk
     del u, v
-    if noise:
-        g.manual_seed(2000 + seed)
-        a.add_(torch.randn(m, n, generator=g, device=device, dtype=torch.float64), alpha=noise)
-    return a.to(dtype)
+    return a
 
 
 def sparse_uniform_np(m: int, n: int, per_row: int, seed: int):
