@@ -167,7 +167,7 @@ def cpu_baseline(w, budget_s: float, threads: int) -> dict:
     long_dim = w.m if (w.m >= w.n or w.density == "sparse") else w.n
     base = max(1024, w.l * 4)
     if w.density == "sparse":
-        base = 20000
+        base = 4096
     r1 = min(long_dim, base)
     t1 = _time_port(w, r1, threads)
     per = max(t1 / r1, 1e-9)
