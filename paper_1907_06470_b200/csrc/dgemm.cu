@@ -310,7 +310,12 @@ int pick_bn(int64_t N) {
   if (N <= 32) return 32;
   if (N <= 64) return 64;
   if (N == 120) return 120;
-  return 128;
+  if (N <= 112) return 112;
+  if (N <= 128) return 128;
+  // wide sketches (cfg4 l=220 -> 224 = 2 x 112, cfg5 l=550 -> 552 in 5 x 112):
+  // the tile width that wastes the fewest padded columns
+  const int64_t w112 = ceil_div(N, 112) * 112, w128 = ceil_div(N, 128) * 128;
+  return w112 < w128 ? 112 : 128;
 }
 
 // Tile variants. The l = 120 products over A (cfg2's hot shape) have
@@ -358,6 +363,7 @@ void dispatch(const DGemmArgs& g, const Variant& var, int splits, int64_t kps, d
   switch (bn) {
     case 32: run_cfg<TA, 128, 32, 16, 4, 1, 4, TRANS_A>(g, splits, kps, out, ldo, stride, st); break;
     case 64: run_cfg<TA, 128, 64, 16, 4, 2, 4, TRANS_A>(g, splits, kps, out, ldo, stride, st); break;
+    case 112: run_cfg<TA, 128, 112, 16, 4, 2, 4, TRANS_A>(g, splits, kps, out, ldo, stride, st); break;
     default: run_cfg<TA, 128, 128, 16, 4, 4, 4, TRANS_A>(g, splits, kps, out, ldo, stride, st); break;
   }
 }

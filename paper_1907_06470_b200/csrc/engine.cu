@@ -26,6 +26,7 @@
 #include <cstring>
 #include <map>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "common.cuh"
@@ -94,6 +95,10 @@ struct xb_ctx {
   double* dbuf(const std::string& name, size_t count) {
     return static_cast<double*>(buf(name, count * sizeof(double)));
   }
+  // pinned staging for device -> pageable-host copies (two ping-pong halves)
+  void* stage_host = nullptr;
+  size_t stage_bytes = 0;
+  cudaEvent_t stage_ev[2] = {nullptr, nullptr};
   int* ibuf(const std::string& name, size_t count) {
     return static_cast<int*>(buf(name, count * sizeof(int)));
   }
@@ -105,6 +110,82 @@ thread_local std::string g_last_error;
 
 double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// Parallel host memcpy (pageable destinations: one thread per slice).
+void par_memcpy(char* dst, const char* src, size_t bytes) {
+  const size_t kMin = (size_t)8 << 20;
+  const int nt = (int)std::min<size_t>(8, std::max<size_t>(1, bytes / kMin));
+  if (nt <= 1) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  std::vector<std::thread> ts;
+  const size_t per = (bytes + nt - 1) / nt;
+  for (int t = 0; t < nt; ++t) {
+    const size_t o = (size_t)t * per;
+    if (o >= bytes) break;
+    const size_t len = std::min(per, bytes - o);
+    ts.emplace_back([=] { std::memcpy(dst + o, src + o, len); });
+  }
+  for (auto& th : ts) th.join();
+}
+
+// Device rows -> host rows, stream-ordered after the producers on c->st and
+// complete on return. Pinned or small destinations get one DMA; large
+// pageable ones go through two pinned 64 MiB halves, the DMA of chunk i+1
+// overlapping the host copy of chunk i (a pageable cudaMemcpy runs at a
+// fraction of the link rate).
+void d2h_rows(xb_ctx* c, void* dst, size_t ld_dst, const void* src, size_t ld_src,
+              size_t row_bytes, int64_t rows) {
+  const size_t total = row_bytes * (size_t)rows;
+  if (rows <= 0 || row_bytes == 0) return;
+  if (total < ((size_t)4 << 20) || is_pinned(dst)) {
+    XB_CUDA(cudaMemcpy2DAsync(dst, ld_dst, src, ld_src, row_bytes, rows, cudaMemcpyDeviceToHost,
+                              c->st));
+    XB_CUDA(cudaStreamSynchronize(c->st));
+    return;
+  }
+  const size_t half = (size_t)64 << 20;
+  if (!c->stage_host) {
+    XB_CUDA(cudaHostAlloc(&c->stage_host, 2 * half, cudaHostAllocDefault));
+    c->stage_bytes = 2 * half;
+    XB_CUDA(cudaEventCreateWithFlags(&c->stage_ev[0], cudaEventDisableTiming));
+    XB_CUDA(cudaEventCreateWithFlags(&c->stage_ev[1], cudaEventDisableTiming));
+  }
+  const int64_t chunk = std::max<int64_t>(1, (int64_t)(half / row_bytes));
+  XB_REQUIRE(row_bytes <= half, XB_EUNSUPPORTED, "d2h: row wider than the staging buffer");
+  auto issue = [&](int64_t r0, int slot) {
+    const int64_t nr = std::min(chunk, rows - r0);
+    char* h = static_cast<char*>(c->stage_host) + (size_t)slot * half;
+    XB_CUDA(cudaMemcpy2DAsync(h, row_bytes, static_cast<const char*>(src) + (size_t)r0 * ld_src,
+                              ld_src, row_bytes, nr, cudaMemcpyDeviceToHost, c->st));
+    XB_CUDA(cudaEventRecord(c->stage_ev[slot], c->st));
+  };
+  issue(0, 0);
+  int slot = 0;
+  for (int64_t r0 = 0; r0 < rows; r0 += chunk) {
+    const int64_t nr = std::min(chunk, rows - r0);
+    if (r0 + chunk < rows) issue(r0 + chunk, slot ^ 1);
+    XB_CUDA(cudaEventSynchronize(c->stage_ev[slot]));
+    const char* h = static_cast<const char*>(c->stage_host) + (size_t)slot * half;
+    char* d = static_cast<char*>(dst) + (size_t)r0 * ld_dst;
+    if (ld_dst == row_bytes) {
+      par_memcpy(d, h, (size_t)nr * row_bytes);
+    } else {
+      for (int64_t r = 0; r < nr; ++r) std::memcpy(d + r * ld_dst, h + r * row_bytes, row_bytes);
+    }
+    slot ^= 1;
+  }
 }
 
 struct LaunchScope {
@@ -268,6 +349,25 @@ void cholqr2(xb_ctx* c, const Small& s, const double* X, int64_t rows, double* T
   // Householder fallback runs only when a Cholesky flagged (device-side test)
   double* hw = c->dbuf("hh_work", (size_t)2 * rows * l);
   launch_householder_fallback(X, lp, rows, l, lp, Q, lp, R, lp, hw, s.flag, st);
+}
+
+// Single-pass CholQR for the orthonormalisations INSIDE the power iteration.
+// There Q only has to be a well-conditioned basis of range(X) for the next
+// product: one pass gives ||Q^T Q - I|| ~ u kappa(X)^2 while range(Q) equals
+// range(X) to ~u kappa(X), the same range accuracy as Householder. The
+// pivot threshold (1e-8 G_jj, i.e. kappa below ~1e4 per column) keeps that
+// loss far below the 1e-8 subspace target; beyond it the Householder
+// fallback runs. The range-finder's final QR and the QR of B^T (whose Q
+// must be orthonormal to machine precision) use cholqr2.
+void cholqr1(xb_ctx* c, const Small& s, const double* X, int64_t rows, double* Q) {
+  const int l = s.l, lp = s.lp;
+  cudaStream_t st = c->st;
+  XB_CUDA(cudaMemsetAsync(s.flag, 0, sizeof(int), st));
+  gemm(c, true, lp, lp, rows, X, lp, X, lp, s.G, lp);          // G = X^T X
+  launch_chol_inv(s.G, lp, l, 1e-8, s.R1, s.R1i, lp, s.flag, st);
+  gemm(c, false, rows, lp, lp, X, lp, s.R1i, lp, Q, lp);       // Q = X R^-1
+  double* hw = c->dbuf("hh_work", (size_t)2 * rows * l);
+  launch_householder_fallback(X, lp, rows, l, lp, Q, lp, s.Rs, lp, hw, s.flag, st);
 }
 
 struct RsvdOut {
@@ -441,17 +541,25 @@ void rsvd_impl(xb_ctx* c, const AOp& op, int64_t m, int64_t n, const void* d_ome
   } else {
     op_nn(c, op, m, n, Om, Ym, lp, l);
   }
+  // intermediate QRs (a basis for the next product) are single-pass, the
+  // final range-finder QR is CholQR2 (see cholqr1)
   clk.enter(kOrtho);
-  cholqr2(c, s, Ym, m, Tm, Qm, q == 0 ? Rf : nullptr);
+  if (q == 0)
+    cholqr2(c, s, Ym, m, Tm, Qm, Rf);
+  else
+    cholqr1(c, s, Ym, m, Qm);
   for (int it = 0; it < q; ++it) {
     clk.enter(kSketch);
     op_tn(c, op, m, n, Qm, Zn, lp, l);  // Z = A^T Q
     clk.enter(kOrtho);
-    cholqr2(c, s, Zn, n, Tn, Qn, nullptr);
+    cholqr1(c, s, Zn, n, Qn);
     clk.enter(kSketch);
     op_nn(c, op, m, n, Qn, Ym, lp, l);  // Y = A Qz
     clk.enter(kOrtho);
-    cholqr2(c, s, Ym, m, Tm, Qm, it == q - 1 ? Rf : nullptr);
+    if (it == q - 1)
+      cholqr2(c, s, Ym, m, Tm, Qm, Rf);
+    else
+      cholqr1(c, s, Ym, m, Qm);
   }
   // deficient columns of the final range-finder QR (kernels.py:327-331)
   launch_deficient(Rf, lp, l, a.f32 ? (double)FLT_EPSILON : DBL_EPSILON, defc, defc + 1, st);
@@ -483,15 +591,6 @@ void rsvd_impl(xb_ctx* c, const AOp& op, int64_t m, int64_t n, const void* d_ome
   if (deficient)
     for (int i = 0; i < hdef[0] && i < l; ++i) deficient[i] = hdef[1 + i];
   XB_REQUIRE(hstat == 0, XB_ECONV, "Jacobi SVD of the projected factor did not converge in 60 sweeps");
-}
-
-bool is_pinned(const void* p) {
-  cudaPointerAttributes a;
-  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
-  }
-  return a.type == cudaMemoryTypeHost;
 }
 
 struct HostRegistration {
@@ -570,6 +669,9 @@ int xb_destroy(xb_ctx* c) {
     cudaStreamSynchronize(c->cp);
     for (auto& kv : c->bufs) cudaFree(kv.second.first);
     for (auto e : c->events) cudaEventDestroy(e);
+    if (c->stage_host) cudaFreeHost(c->stage_host);
+    for (auto e : c->stage_ev)
+      if (e) cudaEventDestroy(e);
     cudaStreamDestroy(c->st);
     cudaStreamDestroy(c->cp);
     delete c;
@@ -682,9 +784,9 @@ int xb_rsvd_dense(xb_ctx* c, int dtype, int64_t m, int64_t n, const void* A, int
       launch_copy2d_cast<double, float>(dU, m, k, k, static_cast<float*>(oU), k, c->st);
       launch_copy2d_cast<double, float>(dV, n, k, k, static_cast<float*>(oV), k, c->st);
     }
-    XB_CUDA(cudaMemcpy2DAsync(U, ldu * es, oU, k * es, k * es, m, cudaMemcpyDeviceToHost, c->st));
-    XB_CUDA(cudaMemcpy2DAsync(V, ldv * es, oV, k * es, k * es, n, cudaMemcpyDeviceToHost, c->st));
     XB_CUDA(cudaMemcpyAsync(s, ds, k * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    d2h_rows(c, U, ldu * es, oU, k * es, k * es, m);
+    d2h_rows(c, V, ldv * es, oV, k * es, k * es, n);
     XB_CUDA(cudaStreamSynchronize(c->st));
     if (getenv("XB_TRACE"))
       fprintf(stderr, "[xb] rsvd_dense host: setup %.1f ms, ingest+compute %.1f ms, d2h %.1f ms\n",
@@ -781,9 +883,9 @@ int xb_rsvd_coo(xb_ctx* c, int64_t m, int64_t n, int64_t nnz, const int64_t* row
     RsvdOut out{dU, k, ds, dV, k};
     rsvd_impl(c, op, m, n, dO, l, seed, k, p, q, out, deficient, ndeficient, stage_seconds,
               IngestPlan{});
-    XB_CUDA(cudaMemcpy2DAsync(U, ldu * 8, dU, k * 8, k * 8, m, cudaMemcpyDeviceToHost, c->st));
-    XB_CUDA(cudaMemcpy2DAsync(V, ldv * 8, dV, k * 8, k * 8, n, cudaMemcpyDeviceToHost, c->st));
     XB_CUDA(cudaMemcpyAsync(s, ds, k * 8, cudaMemcpyDeviceToHost, c->st));
+    d2h_rows(c, U, ldu * 8, dU, k * 8, k * 8, m);
+    d2h_rows(c, V, ldv * 8, dV, k * 8, k * 8, n);
     XB_CUDA(cudaStreamSynchronize(c->st));
     float ms = 0.f;
     XB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
