@@ -285,6 +285,30 @@ class DenseCase:
                 "hbm_gbs_achieved": prof["bytes"] / prof["seconds"] / 1e9 if prof["seconds"] else None}
 
 
+class ShardedDenseCase(DenseCase):
+    """Row-block sharded dense A over N ranks (one process per GPU, NCCL
+    all-reduce of the A^T Q partials and sketch Grams inside the library)."""
+
+    def __init__(self, ctx, w, device, rank, world):
+        import torch
+
+        from paper_1907_06470_b200.distributed import init_comm, row_shards
+
+        super().__init__(ctx, w, device)
+        self.r0, self.r1 = row_shards(w.m, world)[rank]
+        self.a = self.a[self.r0:self.r1].clone()
+        torch.cuda.empty_cache()
+        self.m_local = self.r1 - self.r0
+        self.u = torch.empty((self.m_local, w.k), dtype=self.torch_dtype, device=device)
+        init_comm(ctx)
+
+    def step(self):
+        w = self.w
+        return self.ctx.rsvd_dense_sharded_dev(
+            self.np_dtype, w.m, w.n, self.m_local, self.a.data_ptr(), w.n, w.k, w.p, w.q, w.cfg,
+            self.u.data_ptr(), self.s.data_ptr(), self.v.data_ptr())[1]
+
+
 class SparseCase:
     """CSR A resident on the device; host COO for e2e."""
 
@@ -350,10 +374,15 @@ def run_ours(args):
     w = CONFIGS[args.config]
     if args.config == 4:
         raise SystemExit("config 4 (256 GiB f32) exceeds one GPU's HBM; see DESIGN.md")
-    if world > 1:
-        raise SystemExit("multi-GPU row sharding lands with the NCCL reducer (DESIGN.md)")
     ctx = _lib.load(local)
-    case = SparseCase(ctx, w, device) if w.density == "sparse" else DenseCase(ctx, w, device)
+    if world > 1:
+        if w.density != "dense":
+            raise SystemExit("multi-GPU sharding is built for dense A (configs 1, 2, 5)")
+        case = ShardedDenseCase(ctx, w, device, rank, world)
+    elif w.density == "sparse":
+        case = SparseCase(ctx, w, device)
+    else:
+        case = DenseCase(ctx, w, device)
     torch.cuda.synchronize()
 
     for _ in range(args.warmup):
@@ -396,7 +425,7 @@ def run_ours(args):
     roofline["traffic"] = traffic
 
     e2e = None
-    if args.e2e_steps > 0:
+    if args.e2e_steps > 0 and world == 1:
         case.prepare_e2e()
         case.e2e()  # warm (allocates the host-path buffers)
         e2e_t, ingest = [], []

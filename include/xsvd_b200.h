@@ -110,6 +110,23 @@ int xb_rsvd_dense_dev(xb_ctx* ctx, int dtype, int64_t m, int64_t n, const void* 
                       int32_t* deficient, int* ndeficient, double* stage_seconds);
 
 /*
+ * Multi-GPU, row-block sharding (the reference itself has no
+ * distributed path). One process per GPU: rank 0 calls xb_comm_unique_id,
+ * the 128 bytes are broadcast out of band (e.g. torch.distributed), every
+ * rank calls xb_comm_init. Rank g then passes its m_local rows of the
+ * m_global x n matrix A; Omega and V are replicated, U is returned for the
+ * local rows. A^T Q partials (n x l) and the l x l Grams of the row-sharded
+ * sketch are summed with NCCL all-reduce on the compute stream.
+ */
+int xb_comm_unique_id(unsigned char* out128);
+int xb_comm_init(xb_ctx* ctx, const unsigned char* id128, int world, int rank);
+int xb_rsvd_dense_sharded_dev(xb_ctx* ctx, int dtype, int64_t m_global, int64_t n,
+                              int64_t m_local, const void* dA, int64_t lda, uint64_t seed, int k,
+                              int p, int q, void* dU, int64_t ldu, double* d_s, void* dV,
+                              int64_t ldv, int32_t* deficient, int* ndeficient,
+                              double* stage_seconds);
+
+/*
  * Sparse A — replaces randomized_svd on a SPARSE StoredMatrix, i.e. the
  * sparse x dense and dense x sparse products of kernels.py:85-112 (Y = A X,
  * Z = A^T Q via a once-built CSR of A^T, B^T = A^T Q). A arrives as the

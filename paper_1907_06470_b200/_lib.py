@@ -42,6 +42,10 @@ SIGNATURES = [
                              _vp, _i64, _vp, _vp, _i64, _vp, _intp, _vp]),
     ("xb_rsvd_dense_dev", _int, [_vp, _int, _i64, _i64, _vp, _i64, _vp, _u64, _int, _int, _int,
                                  _vp, _i64, _vp, _vp, _i64, _vp, _intp, _vp]),
+    ("xb_comm_unique_id", _int, [_vp]),
+    ("xb_comm_init", _int, [_vp, _vp, _int, _int]),
+    ("xb_rsvd_dense_sharded_dev", _int, [_vp, _int, _i64, _i64, _i64, _vp, _i64, _u64, _int, _int,
+                                         _int, _vp, _i64, _vp, _vp, _i64, _vp, _intp, _vp]),
     ("xb_rsvd_coo", _int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _u64, _int, _int, _int,
                            _vp, _i64, _vp, _vp, _i64, _vp, _intp, _vp]),
     ("xb_rsvd_csr_dev", _int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _u64, _int, _int, _int,
@@ -164,6 +168,29 @@ class Context:
             C.c_void_p(omega_ptr) if omega_ptr else None, int(seed) & (2**64 - 1), k, p, q,
             C.c_void_p(u_ptr), k, C.c_void_p(s_ptr), C.c_void_p(v_ptr), k, _ptr(deficient),
             C.byref(ndef), _ptr(stages)))
+        return tuple(int(x) for x in deficient[: ndef.value]), stages
+
+    # -- multi-GPU (row-sharded A) -----------------------------------------------------
+    def comm_unique_id(self) -> bytes:
+        buf = (C.c_ubyte * 128)()
+        _check(self.lib.xb_comm_unique_id(buf))
+        return bytes(buf)
+
+    def comm_init(self, unique_id: bytes, world: int, rank: int):
+        if len(unique_id) != 128:
+            raise XsvdError("NCCL unique id must be 128 bytes")
+        buf = (C.c_ubyte * 128).from_buffer_copy(unique_id)
+        _check(self.lib.xb_comm_init(self.h, buf, world, rank))
+
+    def rsvd_dense_sharded_dev(self, dtype, m_global, n, m_local, a_ptr, lda, k, p, q, seed,
+                               u_ptr, s_ptr, v_ptr):
+        deficient = np.zeros(max(k + p, 1), dtype=np.int32)
+        ndef = C.c_int(0)
+        stages = np.zeros(NUM_STAGES)
+        _check(self.lib.xb_rsvd_dense_sharded_dev(
+            self.h, dtype_code(dtype), m_global, n, m_local, C.c_void_p(a_ptr), lda,
+            int(seed) & (2**64 - 1), k, p, q, C.c_void_p(u_ptr), k, C.c_void_p(s_ptr),
+            C.c_void_p(v_ptr), k, _ptr(deficient), C.byref(ndef), _ptr(stages)))
         return tuple(int(x) for x in deficient[: ndef.value]), stages
 
     # -- sparse A ----------------------------------------------------------------------

@@ -123,6 +123,12 @@ void launch_jacobi_svd(const double* R, int64_t ldr, int l, int k, double* Ub, i
                        double* s, double* Wk, int64_t ldw, double* work, int* status,
                        cudaStream_t st);
 
+// NCCL (dlopen'ed, comm.cu): unique id, communicator, in-place sum.
+void nccl_unique_id(unsigned char out[128]);
+void* nccl_comm_init(const unsigned char id[128], int world, int rank);
+void nccl_comm_destroy(void* comm);
+void nccl_allreduce_sum(void* comm, double* buf, size_t count, cudaStream_t st);
+
 // Opt-in dynamic shared memory per block on the current device.
 size_t max_dyn_smem();
 // Global scratch (doubles) launch_jacobi_svd needs in `work` for l.

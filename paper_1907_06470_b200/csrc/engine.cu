@@ -95,6 +95,9 @@ struct xb_ctx {
   double* dbuf(const std::string& name, size_t count) {
     return static_cast<double*>(buf(name, count * sizeof(double)));
   }
+  // NCCL communicator for the row-sharded factorisation (xb_comm_init)
+  void* comm = nullptr;
+  int world = 1, rank = 0;
   // pinned staging for device -> pageable-host copies (two ping-pong halves)
   void* stage_host = nullptr;
   size_t stage_bytes = 0;
@@ -310,6 +313,11 @@ struct Small {
   int l, lp;
   double *G, *R1, *R1i, *R2, *R2i, *Rs;
   int* flag;
+  // row-sharded mode: the communicator that sums Grams, and a sticky flag
+  // for Cholesky breakdowns (no single-device Householder fallback applies
+  // to a sharded sketch)
+  void* comm = nullptr;
+  int* shard_err = nullptr;
 };
 
 Small small_bufs(xb_ctx* c, int l) {
@@ -333,19 +341,27 @@ Small small_bufs(xb_ctx* c, int l) {
 
 // Q (rows x lp) = CholQR2(X), zero padding columns l..lp-1 preserved.
 // If Rout != null it receives R = R2 R1 (lp x lp, zero padded).
+// G = X^T X over this rank's rows, summed over ranks when X is row-sharded.
+void gram(xb_ctx* c, const Small& s, const double* X, int64_t rows, bool sharded) {
+  gemm(c, true, s.lp, s.lp, rows, X, s.lp, X, s.lp, s.G, s.lp);
+  if (sharded) nccl_allreduce_sum(s.comm, s.G, (size_t)s.lp * s.lp, c->st);
+}
+
 void cholqr2(xb_ctx* c, const Small& s, const double* X, int64_t rows, double* T, double* Q,
-             double* Rout) {
+             double* Rout, bool sharded = false) {
   const int l = s.l, lp = s.lp;
   cudaStream_t st = c->st;
-  XB_CUDA(cudaMemsetAsync(s.flag, 0, sizeof(int), st));
-  gemm(c, true, lp, lp, rows, X, lp, X, lp, s.G, lp);          // G1 = X^T X
-  launch_chol_inv(s.G, lp, l, 1e-12, s.R1, s.R1i, lp, s.flag, st);
+  int* flag = sharded ? s.shard_err : s.flag;
+  if (!sharded) XB_CUDA(cudaMemsetAsync(s.flag, 0, sizeof(int), st));
+  gram(c, s, X, rows, sharded);                                // G1 = X^T X
+  launch_chol_inv(s.G, lp, l, 1e-12, s.R1, s.R1i, lp, flag, st);
   gemm(c, false, rows, lp, lp, X, lp, s.R1i, lp, T, lp);       // T = X R1^-1
-  gemm(c, true, lp, lp, rows, T, lp, T, lp, s.G, lp);          // G2 = T^T T
-  launch_chol_inv(s.G, lp, l, 1e-4, s.R2, s.R2i, lp, s.flag, st);
+  gram(c, s, T, rows, sharded);                                // G2 = T^T T
+  launch_chol_inv(s.G, lp, l, 1e-4, s.R2, s.R2i, lp, flag, st);
   gemm(c, false, rows, lp, lp, T, lp, s.R2i, lp, Q, lp);       // Q = T R2^-1
   double* R = Rout ? Rout : s.Rs;
   if (Rout) gemm(c, false, lp, lp, lp, s.R2, lp, s.R1, lp, Rout, lp);  // R = R2 R1
+  if (sharded) return;  // breakdown is reported through shard_err
   // Householder fallback runs only when a Cholesky flagged (device-side test)
   double* hw = c->dbuf("hh_work", (size_t)2 * rows * l);
   launch_householder_fallback(X, lp, rows, l, lp, Q, lp, R, lp, hw, s.flag, st);
@@ -359,13 +375,16 @@ void cholqr2(xb_ctx* c, const Small& s, const double* X, int64_t rows, double* T
 // loss far below the 1e-8 subspace target; beyond it the Householder
 // fallback runs. The range-finder's final QR and the QR of B^T (whose Q
 // must be orthonormal to machine precision) use cholqr2.
-void cholqr1(xb_ctx* c, const Small& s, const double* X, int64_t rows, double* Q) {
+void cholqr1(xb_ctx* c, const Small& s, const double* X, int64_t rows, double* Q,
+             bool sharded = false) {
   const int l = s.l, lp = s.lp;
   cudaStream_t st = c->st;
-  XB_CUDA(cudaMemsetAsync(s.flag, 0, sizeof(int), st));
-  gemm(c, true, lp, lp, rows, X, lp, X, lp, s.G, lp);          // G = X^T X
-  launch_chol_inv(s.G, lp, l, 1e-8, s.R1, s.R1i, lp, s.flag, st);
+  int* flag = sharded ? s.shard_err : s.flag;
+  if (!sharded) XB_CUDA(cudaMemsetAsync(s.flag, 0, sizeof(int), st));
+  gram(c, s, X, rows, sharded);                                // G = X^T X
+  launch_chol_inv(s.G, lp, l, 1e-8, s.R1, s.R1i, lp, flag, st);
   gemm(c, false, rows, lp, lp, X, lp, s.R1i, lp, Q, lp);       // Q = X R^-1
+  if (sharded) return;
   double* hw = c->dbuf("hh_work", (size_t)2 * rows * l);
   launch_householder_fallback(X, lp, rows, l, lp, Q, lp, s.Rs, lp, hw, s.flag, st);
 }
@@ -403,6 +422,11 @@ struct AOp {
   bool sparse = false;
   AView dense{nullptr, 0, false};
   Csr csr, csrt;  // A (m x n) and A^T (n x m)
+  // row-sharded A: this rank holds m local rows of an
+  // m_global x n matrix; products over A^T and Grams of the m-side sketch
+  // are summed over `comm`
+  void* comm = nullptr;
+  int64_t m_global = 0;
 };
 
 void spmm_on_a(xb_ctx* c, const Csr& s, const double* X, double* Y, int lp, int l) {
@@ -437,6 +461,8 @@ void op_tn(xb_ctx* c, const AOp& op, int64_t m, int64_t n, const double* Q, doub
     spmm_on_a(c, op.csrt, Q, Z, lp, l);
   else
     gemm_on_a(c, true, n, lp, m, op.dense, 0, Q, lp, Z, lp, l);
+  // row-sharded: Z = sum_g A_g^T Q_g, the one n x l exchange per product
+  if (op.comm) nccl_allreduce_sum(op.comm, Z, (size_t)n * lp, c->st);
 }
 
 // One factorisation. A (device, f64 or f32 dense, or f64 CSR) is only touched
@@ -447,7 +473,9 @@ void rsvd_impl(xb_ctx* c, const AOp& op, int64_t m, int64_t n, const void* d_ome
                int64_t ld_omega, uint64_t seed, int k, int p, int q, const RsvdOut& out,
                int32_t* deficient, int* ndeficient, double* stage_seconds, const IngestPlan& ing) {
   const AView& a = op.dense;
-  check_dims(m, n, k, p, q);
+  // m = rows held here (all of A unless row-sharded)
+  check_dims(op.comm ? op.m_global : m, n, k, p, q);
+  const bool sharded = op.comm != nullptr;
   const int l = k + p;
   const int lp = (int)round_up(l, 8);
   const int kp = (int)round_up(k, 2);
@@ -491,6 +519,11 @@ void rsvd_impl(xb_ctx* c, const AOp& op, int64_t m, int64_t n, const void* d_ome
     c->dbuf("hh_work", (size_t)2 * std::max(m, n) * l);
   }
   Small s = small_bufs(c, l);
+  if (sharded) {
+    s.comm = op.comm;
+    s.shard_err = c->ibuf("shard_err", 4);
+    XB_CUDA(cudaMemsetAsync(s.shard_err, 0, sizeof(int), st));
+  }
   XB_CUDA(cudaMemsetAsync(Ub, 0, (size_t)lp * lp * sizeof(double), st));
   XB_CUDA(cudaMemsetAsync(Wk, 0, (size_t)lp * kp * sizeof(double), st));
 
@@ -543,11 +576,13 @@ void rsvd_impl(xb_ctx* c, const AOp& op, int64_t m, int64_t n, const void* d_ome
   }
   // intermediate QRs (a basis for the next product) are single-pass, the
   // final range-finder QR is CholQR2 (see cholqr1)
+  // (row-sharded: the m-side QRs sum their Grams over ranks; the n-side ones
+  // run replicated on the all-reduced Z, identically on every rank)
   clk.enter(kOrtho);
   if (q == 0)
-    cholqr2(c, s, Ym, m, Tm, Qm, Rf);
+    cholqr2(c, s, Ym, m, Tm, Qm, Rf, sharded);
   else
-    cholqr1(c, s, Ym, m, Qm);
+    cholqr1(c, s, Ym, m, Qm, sharded);
   for (int it = 0; it < q; ++it) {
     clk.enter(kSketch);
     op_tn(c, op, m, n, Qm, Zn, lp, l);  // Z = A^T Q
@@ -557,9 +592,9 @@ void rsvd_impl(xb_ctx* c, const AOp& op, int64_t m, int64_t n, const void* d_ome
     op_nn(c, op, m, n, Qn, Ym, lp, l);  // Y = A Qz
     clk.enter(kOrtho);
     if (it == q - 1)
-      cholqr2(c, s, Ym, m, Tm, Qm, Rf);
+      cholqr2(c, s, Ym, m, Tm, Qm, Rf, sharded);
     else
-      cholqr1(c, s, Ym, m, Qm);
+      cholqr1(c, s, Ym, m, Qm, sharded);
   }
   // deficient columns of the final range-finder QR (kernels.py:327-331)
   launch_deficient(Rf, lp, l, a.f32 ? (double)FLT_EPSILON : DBL_EPSILON, defc, defc + 1, st);
@@ -578,9 +613,11 @@ void rsvd_impl(xb_ctx* c, const AOp& op, int64_t m, int64_t n, const void* d_ome
   gemm(c, false, n, k, lp, Qn, lp, Wk, kp, out.V, out.ldv);  // V = Q_B W_k
   XB_CUDA(cudaMemcpyAsync(out.s, sv, k * sizeof(double), cudaMemcpyDeviceToDevice, st));
 
-  int hstat = 0;
+  int hstat = 0, hshard = 0;
   std::vector<int> hdef(lp + 1, 0);
   XB_CUDA(cudaMemcpyAsync(&hstat, jstat, sizeof(int), cudaMemcpyDeviceToHost, st));
+  if (sharded)
+    XB_CUDA(cudaMemcpyAsync(&hshard, s.shard_err, sizeof(int), cudaMemcpyDeviceToHost, st));
   XB_CUDA(cudaMemcpyAsync(hdef.data(), defc, (lp + 1) * sizeof(int), cudaMemcpyDeviceToHost, st));
   clk.finish(stage_seconds ? local_stage : nullptr);
   XB_CUDA(cudaStreamSynchronize(st));
@@ -591,6 +628,9 @@ void rsvd_impl(xb_ctx* c, const AOp& op, int64_t m, int64_t n, const void* d_ome
   if (deficient)
     for (int i = 0; i < hdef[0] && i < l; ++i) deficient[i] = hdef[1 + i];
   XB_REQUIRE(hstat == 0, XB_ECONV, "Jacobi SVD of the projected factor did not converge in 60 sweeps");
+  XB_REQUIRE(hshard == 0, XB_ECONV,
+             "row-sharded sketch is numerically rank deficient (Cholesky breakdown); the "
+             "single-device Householder fallback does not apply to a sharded sketch");
 }
 
 struct HostRegistration {
@@ -670,6 +710,7 @@ int xb_destroy(xb_ctx* c) {
     for (auto& kv : c->bufs) cudaFree(kv.second.first);
     for (auto e : c->events) cudaEventDestroy(e);
     if (c->stage_host) cudaFreeHost(c->stage_host);
+    if (c->comm) nccl_comm_destroy(c->comm);
     for (auto e : c->stage_ev)
       if (e) cudaEventDestroy(e);
     cudaStreamDestroy(c->st);
@@ -837,6 +878,53 @@ AOp sparse_from_host_coo(xb_ctx* c, int64_t m, int64_t n, int64_t nnz, const int
 }  // namespace
 
 extern "C" {
+
+int xb_comm_unique_id(unsigned char* out128) {
+  return guarded([&] {
+    XB_REQUIRE(out128, XB_EVALUE, "null buffer");
+    nccl_unique_id(out128);
+  });
+}
+
+int xb_comm_init(xb_ctx* c, const unsigned char* id128, int world, int rank) {
+  return guarded([&] {
+    XB_REQUIRE(c && id128, XB_EVALUE, "null argument");
+    XB_REQUIRE(world >= 1 && rank >= 0 && rank < world, XB_EVALUE, "bad rank/world");
+    LaunchScope ls(c);
+    if (c->comm) nccl_comm_destroy(c->comm);
+    c->comm = nccl_comm_init(id128, world, rank);
+    c->world = world;
+    c->rank = rank;
+  });
+}
+
+int xb_rsvd_dense_sharded_dev(xb_ctx* c, int dtype, int64_t m_global, int64_t n, int64_t m_local,
+                              const void* dA, int64_t lda, uint64_t seed, int k, int p, int q,
+                              void* dU, int64_t ldu, double* d_s, void* dV, int64_t ldv,
+                              int32_t* deficient, int* ndeficient, double* stage_seconds) {
+  return guarded([&] {
+    XB_REQUIRE(c, XB_EVALUE, "null context");
+    XB_REQUIRE(c->comm, XB_EVALUE, "xb_comm_init has not been called on this context");
+    LaunchScope ls(c);
+    const bool f32 = check_dtype(dtype);
+    XB_REQUIRE(m_local >= 1 && m_local <= m_global, XB_ESHAPE, "bad local row count");
+    XB_REQUIRE(lda >= n && ldu >= k && ldv >= k, XB_EVALUE, "leading dimension too small");
+    AOp op;
+    op.dense = AView{dA, lda, f32};
+    op.comm = c->comm;
+    op.m_global = m_global;
+    double* Ud = f32 ? c->dbuf("Ud", (size_t)m_local * k) : static_cast<double*>(dU);
+    double* Vd = f32 ? c->dbuf("Vd", (size_t)n * k) : static_cast<double*>(dV);
+    RsvdOut out{Ud, f32 ? k : ldu, d_s, Vd, f32 ? k : ldv};
+    rsvd_impl(c, op, m_local, n, nullptr, k + p, seed, k, p, q, out, deficient, ndeficient,
+              stage_seconds, IngestPlan{});
+    if (f32) {
+      launch_copy2d_cast<double, float>(Ud, m_local, k, k, static_cast<float*>(dU), ldu, c->st);
+      launch_copy2d_cast<double, float>(Vd, n, k, k, static_cast<float*>(dV), ldv, c->st);
+      XB_CUDA(cudaStreamSynchronize(c->st));
+    }
+  });
+}
 
 int xb_rsvd_csr_dev(xb_ctx* c, int64_t m, int64_t n, int64_t nnz, const int64_t* d_rowptr,
                     const int32_t* d_col, const double* d_val, const double* d_omega,

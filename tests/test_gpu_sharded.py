@@ -1,0 +1,70 @@
+"""The NCCL row-sharded entry point on one GPU (world = 1).
+
+Only one GPU is available to the tests, and two NCCL ranks on one GPU would
+wait on each other, so the exchange pattern with world = 2 is checked on CPU
+(tests/test_distributed_cpu.py). Here the real NCCL communicator (world 1)
+runs every all-reduce of the sharded schedule through the C ABI; with one
+rank the sums are identities, so the results must equal the unsharded path
+bit for bit.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from oracle import metrics as M
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+@pytest.fixture(scope="module")
+def world1(lib):
+    import torch.distributed as dist
+
+    from paper_1907_06470_b200.distributed import init_comm
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(_free_port())
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    init_comm(lib)
+    yield lib
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_sharded_world1_equals_unsharded(world1, dtype):
+    import torch
+
+    from paper_1907_06470_b200.distributed import randomized_svd_sharded
+    from paper_1907_06470_b200.workloads import dense_lowrank_np
+
+    npdt = np.float64 if dtype == "float64" else np.float32
+    a = dense_lowrank_np(3000, 1200, "pow-1.5", 1e-8, 31, 32).astype(npdt)
+    at = torch.from_numpy(a).cuda()
+    u, s, v = randomized_svd_sharded(world1, at, 3000, 40, 10, 2, 7)
+    u0, s0, v0, _, _ = world1.rsvd_dense(a, 40, 10, 2, 7)
+    assert np.array_equal(s.cpu().numpy(), s0)
+    assert np.array_equal(u.cpu().numpy(), u0)
+    assert np.array_equal(v.cpu().numpy(), v0)
+
+
+def test_sharded_rank_deficiency_is_reported(world1):
+    import torch
+
+    from paper_1907_06470_b200.distributed import randomized_svd_sharded
+    from paper_1907_06470_b200.errors import ConvergenceError
+
+    rng = np.random.default_rng(3)
+    a = rng.standard_normal((500, 8)) @ rng.standard_normal((8, 300))  # rank 8 < l = 20
+    with pytest.raises(ConvergenceError):
+        randomized_svd_sharded(world1, torch.from_numpy(a).cuda(), 500, 15, 5, 1, 1)
