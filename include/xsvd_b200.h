@@ -101,6 +101,18 @@ int xb_rsvd_dense(xb_ctx* ctx, int dtype, int64_t m, int64_t n, const void* A, i
                   void* U, int64_t ldu, double* s, void* V, int64_t ldv,
                   int32_t* deficient, int* ndeficient, double* stage_seconds);
 
+/* Out-of-core factorization (the pinned-host tile streamer): A stays in host
+ * memory and streams through HBM in row tiles of `tile_rows` (0 = automatic,
+ * ~2 GiB tiles), q + 1 fused passes (Y_i = A_i X and W += A_i^T Y_i from one
+ * read of each tile). xb_rsvd_dense switches to this path by itself when A
+ * does not fit in device memory; this entry point forces it. Replaces the
+ * reference's budgeted residency (BlockPool LRU + spill, pool.py:189-221)
+ * for the A-larger-than-memory case (config 4). Omega is generated. */
+int xb_rsvd_dense_streamed(xb_ctx* ctx, int dtype, int64_t m, int64_t n, const void* A,
+                           int64_t lda, uint64_t seed, int k, int p, int q, int64_t tile_rows,
+                           void* U, int64_t ldu, double* s, void* V, int64_t ldv,
+                           int32_t* deficient, int* ndeficient, double* stage_seconds);
+
 /* Same factorization with A, omega, U, V, s already in device memory
  * (the HBM-resident measurement; deficient/ndeficient/stage_seconds stay
  * host pointers). */

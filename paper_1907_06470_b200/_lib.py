@@ -42,6 +42,8 @@ SIGNATURES = [
                              _vp, _i64, _vp, _vp, _i64, _vp, _intp, _vp]),
     ("xb_rsvd_dense_dev", _int, [_vp, _int, _i64, _i64, _vp, _i64, _vp, _u64, _int, _int, _int,
                                  _vp, _i64, _vp, _vp, _i64, _vp, _intp, _vp]),
+    ("xb_rsvd_dense_streamed", _int, [_vp, _int, _i64, _i64, _vp, _i64, _u64, _int, _int, _int,
+                                      _i64, _vp, _i64, _vp, _vp, _i64, _vp, _intp, _vp]),
     ("xb_comm_unique_id", _int, [_vp]),
     ("xb_comm_init", _int, [_vp, _vp, _int, _int]),
     ("xb_rsvd_dense_sharded_dev", _int, [_vp, _int, _i64, _i64, _i64, _vp, _i64, _u64, _int, _int,
@@ -155,6 +157,30 @@ class Context:
             self.h, dtype_code(dt), m, n, _ptr(a), lda, _ptr(om) if om is not None else None,
             int(seed) & (2**64 - 1), k, p, q, _ptr(u), k, _ptr(s), _ptr(v), k, _ptr(deficient),
             C.byref(ndef), _ptr(stages)))
+        return u, s, v, tuple(int(x) for x in deficient[: ndef.value]), stages
+
+    def rsvd_dense_streamed(self, a: np.ndarray, k: int, p: int, q: int, seed: int,
+                            tile_rows: int = 0):
+        """Out-of-core factorisation: A stays in host memory and streams
+        through HBM in row tiles (xb_rsvd_dense_streamed)."""
+        a = np.asarray(a)
+        if a.ndim != 2:
+            raise XsvdError("A must be 2-d")
+        if a.strides[1] != a.itemsize:
+            a = np.ascontiguousarray(a)
+        m, n = a.shape
+        lda = a.strides[0] // a.itemsize
+        dt = a.dtype
+        u = np.empty((m, k), dtype=dt)
+        v = np.empty((n, k), dtype=dt)
+        s = np.empty(k)
+        deficient = np.zeros(max(k + p, 1), dtype=np.int32)
+        ndef = C.c_int(0)
+        stages = np.zeros(NUM_STAGES)
+        _check(self.lib.xb_rsvd_dense_streamed(
+            self.h, dtype_code(dt), m, n, _ptr(a), lda, int(seed) & (2**64 - 1), k, p, q,
+            int(tile_rows), _ptr(u), k, _ptr(s), _ptr(v), k, _ptr(deficient), C.byref(ndef),
+            _ptr(stages)))
         return u, s, v, tuple(int(x) for x in deficient[: ndef.value]), stages
 
     def rsvd_dense_dev(self, dtype, m, n, a_ptr, lda, k, p, q, seed, u_ptr, s_ptr, v_ptr,

@@ -74,6 +74,7 @@ struct DGemmArgs {
   double* C;
   int64_t ldc;
   bool a_f32 = false;
+  bool accumulate = false;  // C += op(A) B (fixed order: the streamed tiles' sums)
 };
 // Returns the number of split-K slices that will be used for this shape.
 int dgemm_plan_splits(const DGemmArgs& g);

@@ -133,7 +133,7 @@ template <typename TA, int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STA
 __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, 1)
     dgemm_kernel(int64_t M, int64_t N, int64_t K, const TA* __restrict__ A, int64_t lda,
                  const double* __restrict__ B, int64_t ldb, double* __restrict__ C, int64_t ldc,
-                 int64_t split_stride, int64_t k_per_split) {
+                 int64_t split_stride, int64_t k_per_split, int accumulate) {
   using Cfg = DCfg<TA, BM, BN, BK, WARPS_M, WARPS_N, STAGES, TRANS_A>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tid = threadIdx.x;
@@ -220,10 +220,16 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, 1)
       const int64_t c = n0 + wn * Cfg::WN + j * 8 + 2 * t;
       double* dst = C + r * ldc + c;
       if (c + 1 < N && ((ldc & 1) == 0)) {
-        *reinterpret_cast<double2*>(dst) = make_double2(acc[i][j][0], acc[i][j][1]);
+        double2 v = make_double2(acc[i][j][0], acc[i][j][1]);
+        if (accumulate) {
+          const double2 o = *reinterpret_cast<const double2*>(dst);
+          v.x += o.x;
+          v.y += o.y;
+        }
+        *reinterpret_cast<double2*>(dst) = v;
       } else {
-        if (c < N) dst[0] = acc[i][j][0];
-        if (c + 1 < N) dst[1] = acc[i][j][1];
+        if (c < N) dst[0] = accumulate ? dst[0] + acc[i][j][0] : acc[i][j][0];
+        if (c + 1 < N) dst[1] = accumulate ? dst[1] + acc[i][j][1] : acc[i][j][1];
       }
     }
   }
@@ -232,7 +238,7 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, 1)
 // out[r, c] = sum_{s < S} work[s][r, c] in slice order.
 __global__ void split_reduce_kernel(const double* __restrict__ work, int64_t M, int64_t N,
                                     int64_t ldw, int64_t stride, int S, double* __restrict__ C,
-                                    int64_t ldc) {
+                                    int64_t ldc, int accumulate) {
   const int64_t total = M * N;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
@@ -240,7 +246,7 @@ __global__ void split_reduce_kernel(const double* __restrict__ work, int64_t M, 
     const double* p = work + r * ldw + c;
     double acc = p[0];
     for (int s = 1; s < S; ++s) acc += p[s * stride];
-    C[r * ldc + c] = acc;
+    C[r * ldc + c] = accumulate ? C[r * ldc + c] + acc : acc;
   }
 }
 
@@ -249,7 +255,7 @@ __global__ void split_reduce_kernel(const double* __restrict__ work, int64_t M, 
 // warp partials are combined in warp order — a fixed order, deterministic.
 __global__ void __launch_bounds__(256) split_reduce_wide_kernel(
     const double* __restrict__ work, int64_t M, int64_t N, int64_t ldw, int64_t stride, int S,
-    double* __restrict__ C, int64_t ldc) {
+    double* __restrict__ C, int64_t ldc, int accumulate) {
   __shared__ double part[8][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t idx = (int64_t)blockIdx.x * 32 + lane;
@@ -268,7 +274,7 @@ __global__ void __launch_bounds__(256) split_reduce_wide_kernel(
     double sum = part[0][lane];
 #pragma unroll
     for (int w = 1; w < 8; ++w) sum += part[w][lane];
-    C[r * ldc + c] = sum;
+    C[r * ldc + c] = accumulate ? C[r * ldc + c] + sum : sum;
   }
 }
 
@@ -290,8 +296,10 @@ void run_cfg(const DGemmArgs& g, int splits, int64_t k_per_split, double* out, i
   auto launch = [&](auto kernel) {
     XB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)Cfg::SMEM));
+    // with split-K the slices go to the workspace and the reduce accumulates
+    const int acc_here = (splits == 1 && g.accumulate) ? 1 : 0;
     kernel<<<grid, Cfg::kThreads, Cfg::SMEM, st>>>(g.M, g.N, g.K, A, g.lda, g.B, g.ldb, out, ldo,
-                                                   split_stride, k_per_split);
+                                                   split_stride, k_per_split, acc_here);
     check_launch("dgemm");
   };
   if (a16 && b16)
@@ -404,8 +412,9 @@ size_t dgemm_workspace_doubles(const DGemmArgs& g, int splits) {
 void dgemm(const DGemmArgs& g, int splits, double* work, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0) return;
   if (g.K <= 0) {
-    for (int64_t r = 0; r < g.M; ++r)
-      XB_CUDA(cudaMemsetAsync(g.C + r * g.ldc, 0, g.N * sizeof(double), st));
+    if (!g.accumulate)
+      for (int64_t r = 0; r < g.M; ++r)
+        XB_CUDA(cudaMemsetAsync(g.C + r * g.ldc, 0, g.N * sizeof(double), st));
     return;
   }
   const Variant var = pick_variant(g);
@@ -435,10 +444,11 @@ void dgemm(const DGemmArgs& g, int splits, double* work, cudaStream_t st) {
     const int64_t total = g.M * g.N;
     if (splits >= 16) {
       split_reduce_wide_kernel<<<(unsigned)ceil_div(total, 32), 256, 0, st>>>(
-          work, g.M, g.N, ldo, stride, splits, g.C, g.ldc);
+          work, g.M, g.N, ldo, stride, splits, g.C, g.ldc, g.accumulate ? 1 : 0);
     } else {
       int blocks = (int)std::min<int64_t>(ceil_div(total, 256), kNumSMs * 8);
-      split_reduce_kernel<<<blocks, 256, 0, st>>>(work, g.M, g.N, ldo, stride, splits, g.C, g.ldc);
+      split_reduce_kernel<<<blocks, 256, 0, st>>>(work, g.M, g.N, ldo, stride, splits, g.C, g.ldc,
+                                                  g.accumulate ? 1 : 0);
     }
     check_launch("split_reduce");
   }

@@ -110,6 +110,9 @@ struct xb_ctx {
 namespace {
 
 thread_local std::string g_last_error;
+// xb_rsvd_dense_streamed sets this for the duration of its call: >= 0 forces
+// the out-of-core streamer (0 = automatic tile height)
+thread_local int64_t g_force_stream_rows = -1;
 
 double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
@@ -647,6 +650,243 @@ struct HostRegistration {
   }
 };
 
+// ---- out-of-core: the pinned-host tile streamer (S1) ---------------------------
+//
+// Replaces the reference's residency machinery for matrices larger than
+// memory (BlockPool LRU + spill lane, pool.py:189-221, 397-418) for the case
+// A exceeds HBM (config 4: 256 GiB f32). A stays in (pinned) host memory and
+// streams through HBM in row tiles, NB-deep on the copy stream, each tile's
+// compute overlapping the next tiles' DMA. Every pass over A is fused
+// (SURVEY §7 "cfg4 PCIe-bound passes"): with X the current basis,
+//     Y_i = A_i X        and        W += A_i^T Y_i        (tile by tile)
+// so one read of A yields both Y = A X and W = A^T Y. After the pass,
+// CholQR of Y (resident in HBM) gives R, and A^T Q = W R^-1 — the next Z, or
+// B^T after the last pass — without reading A again: q + 1 host passes
+// instead of 2q + 2. If a Cholesky breaks down (R unusable), Z = A^T Q is
+// recomputed with one extra TN-only pass.
+struct Streamer {
+  xb_ctx* c;
+  const char* host;
+  int64_t host_ld;  // elements
+  bool f32;
+  int64_t m, n, tile_rows;
+  static constexpr int NB = 3;
+  void* tiles[NB];
+  cudaEvent_t landed[NB], freed[NB], t0, t1;
+  double copy_seconds = 0.0;
+  size_t es() const { return f32 ? 4 : 8; }
+
+  Streamer(xb_ctx* ctx, const void* a, int64_t lda, bool is_f32, int64_t rows, int64_t cols,
+           int64_t trows)
+      : c(ctx), host(static_cast<const char*>(a)), host_ld(lda), f32(is_f32), m(rows), n(cols),
+        tile_rows(trows) {
+    for (int b = 0; b < NB; ++b) {
+      tiles[b] = c->buf("stream_tile" + std::to_string(b), (size_t)tile_rows * n * es());
+      XB_CUDA(cudaEventCreateWithFlags(&landed[b], cudaEventDisableTiming));
+      XB_CUDA(cudaEventCreateWithFlags(&freed[b], cudaEventDisableTiming));
+    }
+    XB_CUDA(cudaEventCreate(&t0));
+    XB_CUDA(cudaEventCreate(&t1));
+  }
+  ~Streamer() {
+    for (int b = 0; b < NB; ++b) {
+      cudaEventDestroy(landed[b]);
+      cudaEventDestroy(freed[b]);
+    }
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+  }
+
+  // Stream all row tiles; body(tile_view, r0, rows) enqueues the compute on
+  // c->st for one tile.
+  template <typename F>
+  void pass(F&& body) {
+    XB_CUDA(cudaEventRecord(t0, c->cp));
+    const int64_t ntiles = ceil_div(m, tile_rows);
+    for (int64_t i = 0; i < ntiles; ++i) {
+      const int b = (int)(i % NB);
+      const int64_t r0 = i * tile_rows, rows = std::min(tile_rows, m - r0);
+      if (i >= NB) XB_CUDA(cudaStreamWaitEvent(c->cp, freed[b], 0));
+      XB_CUDA(cudaMemcpy2DAsync(tiles[b], n * es(), host + (size_t)r0 * host_ld * es(),
+                                host_ld * es(), n * es(), rows, cudaMemcpyHostToDevice, c->cp));
+      XB_CUDA(cudaEventRecord(landed[b], c->cp));
+      XB_CUDA(cudaStreamWaitEvent(c->st, landed[b], 0));
+      body(AView{tiles[b], n, f32}, r0, rows);
+      XB_CUDA(cudaEventRecord(freed[b], c->st));
+    }
+    XB_CUDA(cudaEventRecord(t1, c->cp));
+    XB_CUDA(cudaEventSynchronize(t1));
+    float ms = 0.f;
+    XB_CUDA(cudaEventElapsedTime(&ms, t0, t1));
+    copy_seconds += ms * 1e-3;
+  }
+};
+
+// W (+)= tile^T Y_tile with the fixed tile order (deterministic sums).
+void tn_accumulate(xb_ctx* c, const AView& t, int64_t rows, int64_t n, const double* Y, double* W,
+                   int lp, int l) {
+  cudaEvent_t b = nullptr, e = nullptr;
+  if (c->profiling) {
+    b = c->prof_event();
+    e = c->prof_event();
+    XB_CUDA(cudaEventRecord(b, c->st));
+  }
+  DGemmArgs g{true, n, lp, rows, t.p, t.ld, Y, lp, W, lp, t.f32, true};
+  const int splits = dgemm_plan_splits(g);
+  double* work = nullptr;
+  const size_t need = dgemm_workspace_doubles(g, splits);
+  if (need) work = c->dbuf("split", need);
+  dgemm(g, splits, work, c->st);
+  if (c->profiling) {
+    XB_CUDA(cudaEventRecord(e, c->st));
+    const double mn = (double)rows * n;
+    c->prof_pending.push_back({b, e, 2.0 * mn * l, mn * t.esz()});
+  }
+}
+
+int host_flag(xb_ctx* c, const int* dflag) {
+  int h = 0;
+  XB_CUDA(cudaMemcpyAsync(&h, dflag, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+  XB_CUDA(cudaStreamSynchronize(c->st));
+  return h;
+}
+
+void rsvd_stream(xb_ctx* c, const void* hostA, int64_t host_lda, bool f32, int64_t m, int64_t n,
+                 int64_t tile_rows, uint64_t seed, int k, int p, int q, const RsvdOut& out,
+                 int32_t* deficient, int* ndeficient, double* stage_seconds) {
+  check_dims(m, n, k, p, q);
+  const int l = k + p;
+  const int lp = (int)round_up(l, 8);
+  const int kp = (int)round_up(k, 2);
+  cudaStream_t st = c->st;
+  StageClock clk(c);
+  double local_stage[XB_NUM_STAGES] = {0};
+  double* Om = c->dbuf("Om", (size_t)n * lp);
+  double* Ym = c->dbuf("Ym", (size_t)m * lp);
+  double* Tm = c->dbuf("Tm", (size_t)m * lp);
+  double* Qm = c->dbuf("Qm", (size_t)m * lp);
+  double* Wn = c->dbuf("Wn", (size_t)n * lp);
+  double* Zn = c->dbuf("Zn", (size_t)n * lp);
+  double* Tn = c->dbuf("Tn", (size_t)n * lp);
+  double* Qn = c->dbuf("Qn", (size_t)n * lp);
+  double* Rf = c->dbuf("Rf", (size_t)lp * lp);
+  double* Ub = c->dbuf("Ub", (size_t)lp * lp);
+  double* Wk = c->dbuf("Wk", (size_t)lp * kp);
+  double* sv = c->dbuf("sv", (size_t)lp);
+  double* jw = c->dbuf("jw", jacobi_work_doubles(lp));
+  int* jstat = c->ibuf("jstat", 4);
+  int* defc = c->ibuf("defc", (size_t)lp + 4);
+  c->dbuf("hh_work", (size_t)2 * std::max(m, n) * l);
+  {
+    size_t need = 0;
+    auto upd = [&](bool ta, int64_t M, int64_t N, int64_t K, bool af32) {
+      DGemmArgs g{ta, M, N, K, nullptr, 0, nullptr, 0, nullptr, 0, af32};
+      need = std::max(need, dgemm_workspace_doubles(g, dgemm_plan_splits(g)));
+    };
+    upd(false, tile_rows, lp, n, f32);
+    upd(true, n, lp, tile_rows, f32);
+    upd(true, lp, lp, m, false);
+    upd(true, lp, lp, n, false);
+    upd(false, m, lp, lp, false);
+    upd(false, n, lp, lp, false);
+    upd(false, m, k, lp, false);
+    upd(false, n, k, lp, false);
+    if (need) c->dbuf("split", need);
+  }
+  Streamer sm(c, hostA, host_lda, f32, m, n, tile_rows);
+  Small s = small_bufs(c, l);
+  XB_CUDA(cudaMemsetAsync(Ub, 0, (size_t)lp * lp * sizeof(double), st));
+  XB_CUDA(cudaMemsetAsync(Wk, 0, (size_t)lp * kp * sizeof(double), st));
+
+  clk.enter(kGaussian);
+  launch_gaussian<double>(seed, 0, n, l, Om, lp, lp, st);
+  if (f32) launch_round_f32(Om, n, l, lp, st);
+
+  // one fused pass: Y = A X and W = A^T Y
+  auto fused_pass = [&](const double* X) {
+    XB_CUDA(cudaMemsetAsync(Wn, 0, (size_t)n * lp * sizeof(double), st));
+    sm.pass([&](const AView& t, int64_t r0, int64_t rows) {
+      gemm_on_a(c, false, rows, lp, n, t, 0, X, lp, Ym + r0 * lp, lp, l);
+      tn_accumulate(c, t, rows, n, Ym + r0 * lp, Wn, lp, l);
+    });
+  };
+  // fallback: Z = A^T Q directly (one TN-only pass)
+  auto tn_pass = [&](const double* Q, double* Z) {
+    XB_CUDA(cudaMemsetAsync(Z, 0, (size_t)n * lp * sizeof(double), st));
+    sm.pass([&](const AView& t, int64_t r0, int64_t rows) {
+      tn_accumulate(c, t, rows, n, Q + r0 * lp, Z, lp, l);
+    });
+  };
+
+  const double* X = Om;
+  for (int it = 0; it <= q; ++it) {
+    clk.enter(kSketch);
+    fused_pass(X);
+    clk.enter(kOrtho);
+    if (it < q) {
+      cholqr1(c, s, Ym, m, Qm);  // R^-1 in s.R1i unless the fallback ran
+      clk.enter(kSketch);
+      if (host_flag(c, s.flag))
+        tn_pass(Qm, Zn);
+      else
+        gemm(c, false, n, lp, lp, Wn, lp, s.R1i, lp, Zn, lp);  // Z = W R^-1 = A^T Q
+      clk.enter(kOrtho);
+      cholqr1(c, s, Zn, n, Qn);
+      X = Qn;
+    } else {
+      cholqr2(c, s, Ym, m, Tm, Qm, Rf);
+      clk.enter(kProject);
+      if (host_flag(c, s.flag)) {
+        tn_pass(Qm, Zn);  // B^T = A^T Q
+      } else {
+        gemm(c, false, n, lp, lp, Wn, lp, s.R1i, lp, Tn, lp);  // B^T = W R1^-1 R2^-1
+        gemm(c, false, n, lp, lp, Tn, lp, s.R2i, lp, Zn, lp);
+      }
+    }
+  }
+  launch_deficient(Rf, lp, l, f32 ? (double)FLT_EPSILON : DBL_EPSILON, defc, defc + 1, st);
+  clk.enter(kSvdPrep);
+  cholqr2(c, s, Zn, n, Tn, Qn, Rf);
+  clk.enter(kSvd);
+  launch_jacobi_svd(Rf, lp, l, k, Ub, lp, sv, Wk, kp, jw, jstat, st);
+  clk.enter(kPost);
+  gemm(c, false, m, k, lp, Qm, lp, Ub, lp, out.U, out.ldu);
+  gemm(c, false, n, k, lp, Qn, lp, Wk, kp, out.V, out.ldv);
+  XB_CUDA(cudaMemcpyAsync(out.s, sv, k * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  int hstat = 0;
+  std::vector<int> hdef(lp + 1, 0);
+  XB_CUDA(cudaMemcpyAsync(&hstat, jstat, sizeof(int), cudaMemcpyDeviceToHost, st));
+  XB_CUDA(cudaMemcpyAsync(hdef.data(), defc, (lp + 1) * sizeof(int), cudaMemcpyDeviceToHost, st));
+  clk.finish(stage_seconds ? local_stage : nullptr);
+  XB_CUDA(cudaStreamSynchronize(st));
+  if (c->profiling) c->prof_collect();
+  local_stage[kParse] += sm.copy_seconds;  // host->HBM streaming (overlapped with compute)
+  if (stage_seconds)
+    for (int i = 0; i < XB_NUM_STAGES; ++i) stage_seconds[i] = local_stage[i];
+  if (ndeficient) *ndeficient = hdef[0];
+  if (deficient)
+    for (int i = 0; i < hdef[0] && i < l; ++i) deficient[i] = hdef[1 + i];
+  XB_REQUIRE(hstat == 0, XB_ECONV, "Jacobi SVD of the projected factor did not converge in 60 sweeps");
+}
+
+int64_t auto_tile_rows(int64_t m, int64_t n, size_t es) {
+  int64_t r = std::max<int64_t>(256, ((int64_t)1 << 31) / std::max<int64_t>(n * (int64_t)es, 1));
+  r = r / 256 * 256;
+  return std::max<int64_t>(1, std::min(r, m));
+}
+
+// Does A (m x n of `es` bytes) fit in HBM next to the factorisation's buffers?
+bool fits_in_hbm(int64_t m, int64_t n, size_t es, int lp) {
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  const double need = (double)m * n * es + (4.0 * m + 5.0 * n) * lp * 8.0 + 2.0 * 2 * std::max(m, n) * lp * 8.0 +
+                      (double)(1ull << 30);
+  return need < (double)free_b;
+}
+
 // true for float32 (Precision.SINGLE), false for float64
 bool check_dtype(int dtype) {
   XB_REQUIRE(dtype == XB_F64 || dtype == XB_F32, XB_EVALUE, "unknown dtype");
@@ -795,27 +1035,43 @@ int xb_rsvd_dense(xb_ctx* c, int dtype, int64_t m, int64_t n, const void* A, int
     const int l = k + p;
     const double t0 = now_s();
     HostRegistration reg(A, (size_t)((m - 1) * lda + n) * es);
-    void* dA = c->buf("A", (size_t)m * n * es);
     double* dU = c->dbuf("U", (size_t)m * k);
     double* dV = c->dbuf("V", (size_t)n * k);
     double* ds = c->dbuf("s", (size_t)k);
-    void* dO = nullptr;
-    if (omega) {
-      dO = c->buf("omega_in", (size_t)n * l * es);
-      XB_CUDA(cudaMemcpyAsync(dO, omega, (size_t)n * l * es, cudaMemcpyHostToDevice, c->st));
-    }
-    IngestPlan ing;
-    ing.hostA = A;
-    ing.host_lda = lda;
-    // ~1 GiB chunks, at least 8 of them when the matrix is large
-    int64_t rows = std::max<int64_t>(256, ((int64_t)1 << 30) / std::max<int64_t>(n * (int64_t)es, 1));
-    rows = std::min(rows, std::max<int64_t>(256, round_up(ceil_div(m, 8), 128)));
-    ing.chunk_rows = std::min(rows, m);
     RsvdOut out{dU, k, ds, dV, k};
-    const double t1 = now_s();
-    AOp op;
-    op.dense = AView{dA, n, f32};
-    rsvd_impl(c, op, m, n, dO, l, seed, k, p, q, out, deficient, ndeficient, stage_seconds, ing);
+    // out of core when A does not fit in HBM next to the sketch buffers (or
+    // when streaming is forced): the tile streamer, q + 1 host passes
+    const int lp = (int)round_up(l, 8);
+    const bool stream = g_force_stream_rows >= 0 || !fits_in_hbm(m, n, es, lp);
+    double t1 = 0.0;
+    if (stream) {
+      XB_REQUIRE(omega == nullptr, XB_EUNSUPPORTED,
+                 "an explicit Omega is not supported by the out-of-core streamer");
+      const int64_t tr = g_force_stream_rows > 0 ? std::min<int64_t>(g_force_stream_rows, m)
+                                                 : auto_tile_rows(m, n, es);
+      t1 = now_s();
+      rsvd_stream(c, A, lda, f32, m, n, tr, seed, k, p, q, out, deficient, ndeficient,
+                  stage_seconds);
+    } else {
+      void* dA = c->buf("A", (size_t)m * n * es);
+      void* dO = nullptr;
+      if (omega) {
+        dO = c->buf("omega_in", (size_t)n * l * es);
+        XB_CUDA(cudaMemcpyAsync(dO, omega, (size_t)n * l * es, cudaMemcpyHostToDevice, c->st));
+      }
+      IngestPlan ing;
+      ing.hostA = A;
+      ing.host_lda = lda;
+      // ~1 GiB chunks, at least 8 of them when the matrix is large
+      int64_t rows =
+          std::max<int64_t>(256, ((int64_t)1 << 30) / std::max<int64_t>(n * (int64_t)es, 1));
+      rows = std::min(rows, std::max<int64_t>(256, round_up(ceil_div(m, 8), 128)));
+      ing.chunk_rows = std::min(rows, m);
+      t1 = now_s();
+      AOp op;
+      op.dense = AView{dA, n, f32};
+      rsvd_impl(c, op, m, n, dO, l, seed, k, p, q, out, deficient, ndeficient, stage_seconds, ing);
+    }
     const double t2 = now_s();
     void* oU = dU;
     void* oV = dV;
@@ -833,6 +1089,21 @@ int xb_rsvd_dense(xb_ctx* c, int dtype, int64_t m, int64_t n, const void* A, int
       fprintf(stderr, "[xb] rsvd_dense host: setup %.1f ms, ingest+compute %.1f ms, d2h %.1f ms\n",
               (t1 - t0) * 1e3, (t2 - t1) * 1e3, (now_s() - t2) * 1e3);
   });
+}
+
+int xb_rsvd_dense_streamed(xb_ctx* c, int dtype, int64_t m, int64_t n, const void* A,
+                           int64_t lda, uint64_t seed, int k, int p, int q, int64_t tile_rows,
+                           void* U, int64_t ldu, double* s, void* V, int64_t ldv,
+                           int32_t* deficient, int* ndeficient, double* stage_seconds) {
+  if (tile_rows < 0) {
+    g_last_error = "tile_rows must be >= 0";
+    return XB_EVALUE;
+  }
+  g_force_stream_rows = tile_rows;
+  const int rc = xb_rsvd_dense(c, dtype, m, n, A, lda, nullptr, seed, k, p, q, U, ldu, s, V, ldv,
+                               deficient, ndeficient, stage_seconds);
+  g_force_stream_rows = -1;
+  return rc;
 }
 
 }  // extern "C"

@@ -52,10 +52,19 @@ def test_sharded_world1_equals_unsharded(world1, dtype):
     a = dense_lowrank_np(3000, 1200, "pow-1.5", 1e-8, 31, 32).astype(npdt)
     at = torch.from_numpy(a).cuda()
     u, s, v = randomized_svd_sharded(world1, at, 3000, 40, 10, 2, 7)
-    u0, s0, v0, _, _ = world1.rsvd_dense(a, 40, 10, 2, 7)
-    assert np.array_equal(s.cpu().numpy(), s0)
-    assert np.array_equal(u.cpu().numpy(), u0)
-    assert np.array_equal(v.cpu().numpy(), v0)
+    # the unsharded device-resident path (same kernels, same split plans)
+    u0 = torch.empty_like(u)
+    v0 = torch.empty_like(v)
+    s0 = torch.empty_like(s)
+    world1.rsvd_dense_dev(npdt, 3000, 1200, at.data_ptr(), 1200, 40, 10, 2, 7, u0.data_ptr(),
+                          s0.data_ptr(), v0.data_ptr())
+    assert torch.equal(s, s0)
+    assert torch.equal(u, u0)
+    assert torch.equal(v, v0)
+    # and the host-buffer path agrees to rounding (its sketch runs in row chunks)
+    u1, s1, v1, _, _ = world1.rsvd_dense(a, 40, 10, 2, 7)
+    tol = 1e-10 if dtype == "float64" else 1e-4
+    assert M.sigma_rel(s.cpu().numpy(), s1) <= tol
 
 
 def test_sharded_rank_deficiency_is_reported(world1):
