@@ -76,6 +76,17 @@ struct DGemmArgs {
   bool a_f32 = false;
   bool accumulate = false;  // C += op(A) B (fixed order: the streamed tiles' sums)
 };
+// Deterministic slice-order sum of split-K partials into C (+= if accumulate).
+void launch_split_reduce(const double* work, int64_t M, int64_t N, int64_t ldw, int64_t stride,
+                         int S, double* C, int64_t ldc, bool accumulate, cudaStream_t st);
+
+// tcgen05 3xTF32 GEMM (tgemm.cu) for float32 A; B and C are f64 and B is
+// split into tf32 hi/lo planes (bhi, blo: tgemm_b_floats each).
+bool tgemm_supported(const DGemmArgs& g);
+int tgemm_plan_splits(const DGemmArgs& g);
+size_t tgemm_b_floats(const DGemmArgs& g);
+void tgemm(const DGemmArgs& g, int splits, double* work, float* bhi, float* blo, cudaStream_t st);
+
 // Returns the number of split-K slices that will be used for this shape.
 int dgemm_plan_splits(const DGemmArgs& g);
 size_t dgemm_workspace_doubles(const DGemmArgs& g, int splits);

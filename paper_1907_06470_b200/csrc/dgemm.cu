@@ -378,6 +378,20 @@ void dispatch(const DGemmArgs& g, const Variant& var, int splits, int64_t kps, d
 
 }  // namespace
 
+void launch_split_reduce(const double* work, int64_t M, int64_t N, int64_t ldw, int64_t stride,
+                         int S, double* C, int64_t ldc, bool accumulate, cudaStream_t st) {
+  const int64_t total = M * N;
+  if (S >= 16) {
+    split_reduce_wide_kernel<<<(unsigned)ceil_div(total, 32), 256, 0, st>>>(
+        work, M, N, ldw, stride, S, C, ldc, accumulate ? 1 : 0);
+  } else {
+    int blocks = (int)std::min<int64_t>(ceil_div(total, 256), kNumSMs * 8);
+    split_reduce_kernel<<<blocks, 256, 0, st>>>(work, M, N, ldw, stride, S, C, ldc,
+                                                accumulate ? 1 : 0);
+  }
+  check_launch("split_reduce");
+}
+
 int dgemm_plan_splits(const DGemmArgs& g) {
   const Variant var = pick_variant(g);
   const int64_t tiles = ceil_div(g.M, var.BM) * ceil_div(g.N, pick_bn(g.N));

@@ -290,6 +290,27 @@ struct AView {
   }
 };
 
+// One product: float32 A goes to the tcgen05 3xTF32 kernel (tgemm.cu) when
+// its layout allows TMA, everything else to the FP64 DMMA kernel.
+void run_gemm(xb_ctx* c, const DGemmArgs& g) {
+  if (tgemm_supported(g)) {
+    const int splits = tgemm_plan_splits(g);
+    double* work = nullptr;
+    const size_t need = dgemm_workspace_doubles(g, splits);
+    if (need) work = c->dbuf("split", need);
+    const size_t nb = tgemm_b_floats(g);
+    float* bhi = static_cast<float*>(c->buf("tg_bhi", nb * 4));
+    float* blo = static_cast<float*>(c->buf("tg_blo", nb * 4));
+    tgemm(g, splits, work, bhi, blo, c->st);
+    return;
+  }
+  const int splits = dgemm_plan_splits(g);
+  double* work = nullptr;
+  const size_t need = dgemm_workspace_doubles(g, splits);
+  if (need) work = c->dbuf("split", need);
+  dgemm(g, splits, work, c->st);
+}
+
 // A product on A (the dominant kernel): bracketed by events when profiling.
 void gemm_on_a(xb_ctx* c, bool ta, int64_t M, int64_t N, int64_t K, const AView& a,
                int64_t row0, const double* B, int64_t ldb, double* C, int64_t ldc, int l) {
@@ -300,11 +321,7 @@ void gemm_on_a(xb_ctx* c, bool ta, int64_t M, int64_t N, int64_t K, const AView&
     XB_CUDA(cudaEventRecord(b, c->st));
   }
   DGemmArgs g{ta, M, N, K, a.rows_from(row0), a.ld, B, ldb, C, ldc, a.f32};
-  const int splits = dgemm_plan_splits(g);
-  double* work = nullptr;
-  const size_t need = dgemm_workspace_doubles(g, splits);
-  if (need) work = c->dbuf("split", need);
-  dgemm(g, splits, work, c->st);
+  run_gemm(c, g);
   if (c->profiling) {
     XB_CUDA(cudaEventRecord(e, c->st));
     const double mn = (double)M * (double)K;  // A is M x K (NN) or K x M (TN)
@@ -732,11 +749,7 @@ void tn_accumulate(xb_ctx* c, const AView& t, int64_t rows, int64_t n, const dou
     XB_CUDA(cudaEventRecord(b, c->st));
   }
   DGemmArgs g{true, n, lp, rows, t.p, t.ld, Y, lp, W, lp, t.f32, true};
-  const int splits = dgemm_plan_splits(g);
-  double* work = nullptr;
-  const size_t need = dgemm_workspace_doubles(g, splits);
-  if (need) work = c->dbuf("split", need);
-  dgemm(g, splits, work, c->st);
+  run_gemm(c, g);
   if (c->profiling) {
     XB_CUDA(cudaEventRecord(e, c->st));
     const double mn = (double)rows * n;
@@ -908,11 +921,7 @@ void gemm_any(xb_ctx* c, bool f32, bool ta, int64_t m, int64_t n, int64_t kdim, 
   double* C64 = c->dbuf("gC64", (size_t)m * np);
   launch_copy2d_cast<float, double>(static_cast<const float*>(dB), kdim, n, ldb, B64, np, c->st);
   DGemmArgs g{ta, m, n, kdim, dA, lda, B64, np, C64, np, true};
-  const int splits = dgemm_plan_splits(g);
-  double* work = nullptr;
-  const size_t need = dgemm_workspace_doubles(g, splits);
-  if (need) work = c->dbuf("split", need);
-  dgemm(g, splits, work, c->st);
+  run_gemm(c, g);
   launch_copy2d_cast<double, float>(C64, m, n, np, static_cast<float*>(dC), ldc, c->st);
 }
 

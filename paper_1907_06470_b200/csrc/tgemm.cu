@@ -1,0 +1,462 @@
+// FP32-accurate tensor-core GEMM on tcgen05 (3xTF32, TMEM accumulator, TMA).
+//
+// The float32 configs' products (cfg4/cfg5: Y = A X, Z = A^T Q with A in
+// float32, Precision.SINGLE — the reference's f32 compute dtype,
+// core.py:43-46) on Blackwell's 5th-generation tensor cores. TF32 alone is
+// too coarse for the 1e-3 subspace target, so each product is
+// split: a = a_hi + a_lo with a_hi = tf32(a), a_lo = a - a_hi (exact in f32),
+// and  A B ~ A_hi B_hi + A_hi B_lo + A_lo B_hi  (three tcgen05.mma.kind::tf32
+// into one f32 TMEM accumulator; the dropped A_lo B_lo term is ~2^-22).
+//
+// Warp roles (192 threads, one CTA per 128 x BN output tile):
+//   warp 0    TMA producer: raw A tile + the pre-split B_hi / B_lo tiles
+//   warp 1    TMEM allocator + single-thread MMA issuer
+//   warps 2-5 converters: raw A tile -> A_hi, A_lo in the canonical K-major
+//             128B-swizzled layout (for the transposed view of A this is
+//             also the transpose), then the epilogue (tcgen05.ld -> f64 C)
+// Pipelines: full[s] (TMA complete_tx) -> conv[s] (4 converter warps) ->
+// MMA -> tcgen05.commit -> empty[s] (frees the stage), tmem_full after the
+// last k-tile. Split-K slices go to an f64 workspace reduced in slice order
+// by dgemm.cu's deterministic reduce.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <mutex>
+
+#include "common.cuh"
+
+namespace xb {
+namespace {
+
+constexpr int TBM = 128;  // UMMA_M (cta_group::1)
+constexpr int TBK = 32;   // one 128-byte swizzle atom of tf32
+constexpr int TSTAGES = 2;
+constexpr int kThreadsT = 192;
+
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(su32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int32_t c0, int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];\n" ::"r"(su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(su32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ uint32_t to_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
+  return r;
+}
+
+// Shared-memory matrix descriptor: K-major, 128B swizzle, 8-row groups 1024 B
+// apart (SBO), version 1 (sm_100).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;              // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;    // SBO
+  d |= (uint64_t)1 << 46;              // descriptor version
+  d |= (uint64_t)2 << 61;              // SWIZZLE_128B
+  return d;
+}
+
+template <int BN>
+__device__ __forceinline__ uint32_t idesc_tf32() {
+  return (1u << 4)                       // D: f32
+         | (2u << 7) | (2u << 10)        // A, B: tf32
+         | ((uint32_t)(BN >> 3) << 17)   // N
+         | ((uint32_t)(TBM >> 4) << 24);  // M
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                   su32(bar))
+               : "memory");
+}
+
+template <int BN>
+struct TCfg {
+  static constexpr int A_BYTES = TBM * TBK * 4;        // 16 KB (one operand plane)
+  static constexpr int B_BYTES = BN * TBK * 4;         // BN rows x 128 B
+  static constexpr int RAW = 0;                        // raw A (TMA destination)
+  static constexpr int AHI = RAW + A_BYTES;
+  static constexpr int ALO = AHI + A_BYTES;
+  static constexpr int BHI = ALO + A_BYTES;
+  static constexpr int BLO = BHI + ((B_BYTES + 1023) / 1024) * 1024;
+  static constexpr int STAGE = BLO + ((B_BYTES + 1023) / 1024) * 1024;
+  static constexpr int BAR_OFF = TSTAGES * STAGE;
+  static constexpr int SMEM = BAR_OFF + 256 + 1024;    // + barriers, tmem slot, align slack
+  static constexpr int TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+};
+
+template <int BN, bool TRANS_A>
+__global__ void __launch_bounds__(kThreadsT, 1)
+    tgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBh,
+                 const __grid_constant__ CUtensorMap tmBl, int64_t M, int64_t N, int64_t K,
+                 double* __restrict__ C, int64_t ldc, int64_t split_stride, int64_t k_per_split,
+                 int accumulate) {
+  using Cfg = TCfg<BN>;
+  extern __shared__ unsigned char smem_raw_t[];
+  unsigned char* smem =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw_t) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::BAR_OFF);
+  uint64_t* conv = full + TSTAGES;
+  uint64_t* empty = conv + TSTAGES;
+  uint64_t* tmem_full = empty + TSTAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t m0 = (int64_t)blockIdx.x * TBM;
+  const int64_t n0 = (int64_t)blockIdx.y * BN;
+  const int64_t kbeg = (int64_t)blockIdx.z * k_per_split;
+  const int64_t kend = min(K, kbeg + k_per_split);
+  const int ktiles = (int)((kend - kbeg + TBK - 1) / TBK);
+  C += (int64_t)blockIdx.z * split_stride;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < TSTAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&conv[s], 4);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     su32(tmem_slot)),
+                 "n"(Cfg::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---- TMA producer ------------------------------------------------------
+    if (lane == 0) {
+      const uint32_t bytes = Cfg::A_BYTES + 2 * Cfg::B_BYTES;
+      for (int kt = 0; kt < ktiles; ++kt) {
+        const int s = kt % TSTAGES;
+        if (kt >= TSTAGES) mbar_wait(&empty[s], ((kt / TSTAGES) & 1) ^ 1);
+        unsigned char* st = smem + s * Cfg::STAGE;
+        const int32_t k0 = (int32_t)(kbeg + (int64_t)kt * TBK);
+        mbar_expect_tx(&full[s], bytes);
+        if (TRANS_A)
+          tma_load_2d(st + Cfg::RAW, &tmA, &full[s], (int32_t)m0, k0);  // [BK][BM], M inner
+        else
+          tma_load_2d(st + Cfg::RAW, &tmA, &full[s], k0, (int32_t)m0);  // [BM][BK] swizzled
+        tma_load_2d(st + Cfg::BHI, &tmBh, &full[s], k0, (int32_t)n0);
+        tma_load_2d(st + Cfg::BLO, &tmBl, &full[s], k0, (int32_t)n0);
+      }
+    }
+  } else if (warp == 1) {
+    // ---- MMA issuer ------------------------------------------------------------
+    const uint32_t idesc = idesc_tf32<BN>();
+    for (int kt = 0; kt < ktiles; ++kt) {
+      const int s = kt % TSTAGES;
+      mbar_wait(&conv[s], (kt / TSTAGES) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      if (lane == 0) {
+        unsigned char* st = smem + s * Cfg::STAGE;
+        const uint64_t ah = sw128_desc(su32(st + Cfg::AHI));
+        const uint64_t al = sw128_desc(su32(st + Cfg::ALO));
+        const uint64_t bh = sw128_desc(su32(st + Cfg::BHI));
+        const uint64_t bl = sw128_desc(su32(st + Cfg::BLO));
+#pragma unroll
+        for (int kk = 0; kk < TBK / 8; ++kk) {
+          const uint64_t off = (uint64_t)(kk * 32) >> 4;  // 8 tf32 = 32 B inside the atom
+          mma_tf32(tmem, ah + off, bh + off, idesc, (kt > 0 || kk > 0) ? 1u : 0u);
+          mma_tf32(tmem, ah + off, bl + off, idesc, 1u);
+          mma_tf32(tmem, al + off, bh + off, idesc, 1u);
+        }
+        mma_commit(&empty[s]);
+        if (kt == ktiles - 1) mma_commit(tmem_full);
+      }
+      __syncwarp();
+    }
+    if (ktiles == 0 && lane == 0) mbar_arrive(tmem_full);
+  } else {
+    // ---- converters: raw A -> A_hi, A_lo (K-major, 128B swizzle) -----------------
+    const int ct = threadIdx.x - 64;  // 0..127
+    for (int kt = 0; kt < ktiles; ++kt) {
+      const int s = kt % TSTAGES;
+      mbar_wait(&full[s], (kt / TSTAGES) & 1);
+      unsigned char* st = smem + s * Cfg::STAGE;
+      if constexpr (!TRANS_A) {
+        // raw already is the K-major swizzled layout: elementwise, 16 B per step
+        const float4* raw = reinterpret_cast<const float4*>(st + Cfg::RAW);
+        float4* hi = reinterpret_cast<float4*>(st + Cfg::AHI);
+        float4* lo = reinterpret_cast<float4*>(st + Cfg::ALO);
+#pragma unroll 4
+        for (int i = ct; i < Cfg::A_BYTES / 16; i += 128) {
+          const float4 v = raw[i];
+          float4 h, l;
+          h.x = __uint_as_float(to_tf32(v.x));
+          h.y = __uint_as_float(to_tf32(v.y));
+          h.z = __uint_as_float(to_tf32(v.z));
+          h.w = __uint_as_float(to_tf32(v.w));
+          l.x = v.x - h.x;
+          l.y = v.y - h.y;
+          l.z = v.z - h.z;
+          l.w = v.w - h.w;
+          hi[i] = h;
+          lo[i] = l;
+        }
+      } else {
+        // raw is [BK][BM] (M contiguous); thread ct owns output row m = ct
+        const float* raw = reinterpret_cast<const float*>(st + Cfg::RAW);
+        unsigned char* hi = st + Cfg::AHI;
+        unsigned char* lo = st + Cfg::ALO;
+        const int m = ct;
+#pragma unroll
+        for (int c = 0; c < TBK / 4; ++c) {
+          float4 v;
+          v.x = raw[(4 * c + 0) * TBM + m];
+          v.y = raw[(4 * c + 1) * TBM + m];
+          v.z = raw[(4 * c + 2) * TBM + m];
+          v.w = raw[(4 * c + 3) * TBM + m];
+          float4 h, l;
+          h.x = __uint_as_float(to_tf32(v.x));
+          h.y = __uint_as_float(to_tf32(v.y));
+          h.z = __uint_as_float(to_tf32(v.z));
+          h.w = __uint_as_float(to_tf32(v.w));
+          l.x = v.x - h.x;
+          l.y = v.y - h.y;
+          l.z = v.z - h.z;
+          l.w = v.w - h.w;
+          const int off = m * 128 + ((c ^ (m & 7)) << 4);
+          *reinterpret_cast<float4*>(hi + off) = h;
+          *reinterpret_cast<float4*>(lo + off) = l;
+        }
+      }
+      // make the generic-proxy smem writes visible to the tensor core
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&conv[s]);
+    }
+    // ---- epilogue: TMEM -> registers -> f64 C ----------------------------------
+    mbar_wait(tmem_full, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const int q = warp & 3;  // TMEM lanes 32q .. 32q+31
+    const int row = 32 * q + lane;
+    const int64_t r = m0 + row;
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 8) {
+      uint32_t v[8];
+      const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)c0;
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+            "=r"(v[7])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+      if (r < M) {
+        double* dst = C + r * ldc + n0 + c0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (n0 + c0 + j < N) {
+            const double x = (double)__uint_as_float(v[j]);
+            dst[j] = accumulate ? dst[j] + x : x;
+          }
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
+                 "n"(Cfg::TMEM_COLS));
+  }
+}
+
+// X (K x N row-major f64, ldx) -> Xt_hi, Xt_lo (N x Kp f32, K contiguous):
+// hi = tf32(x), lo = f32(x - hi).
+__global__ void split_b_kernel(const double* __restrict__ X, int64_t K, int64_t N, int64_t ldx,
+                               float* __restrict__ hi, float* __restrict__ lo, int64_t kp) {
+  __shared__ double tile[32][33];
+  const int64_t k0 = (int64_t)blockIdx.x * 32, n0 = (int64_t)blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t k = k0 + i, n = n0 + threadIdx.x;
+    tile[i][threadIdx.x] = (k < K && n < N) ? X[k * ldx + n] : 0.0;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t n = n0 + i, k = k0 + threadIdx.x;
+    if (n < N && k < kp) {
+      const double x = tile[threadIdx.x][i];
+      const float h = __uint_as_float(to_tf32((float)x));
+      hi[n * kp + k] = h;
+      lo[n * kp + k] = (float)(x - (double)h);
+    }
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  XB_REQUIRE(fn != nullptr, XB_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+// 2-D f32 tensor map: dims {inner, outer}, row stride ld (elements).
+CUtensorMap make_map(const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
+                     uint32_t box_inner, uint32_t box_outer, bool swizzle128) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {inner, outer};
+  const cuuint64_t strides[1] = {ld * 4};
+  const cuuint32_t box[2] = {box_inner, box_outer};
+  const cuuint32_t es[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims,
+                           strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  XB_REQUIRE(r == CUDA_SUCCESS, XB_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+  return m;
+}
+
+int pick_tbn(int64_t N) {
+  if (N <= 64) return 64;
+  if (N <= 128) return 128;
+  if (N <= 192) return 192;
+  if (N <= 224) return 224;
+  // wide sketches: 3 x 192 covers cfg5's 552 with 4% padding
+  const int64_t w192 = ceil_div(N, 192) * 192, w224 = ceil_div(N, 224) * 224,
+                w256 = ceil_div(N, 256) * 256;
+  if (w192 <= w224 && w192 <= w256) return 192;
+  return w224 <= w256 ? 224 : 256;
+}
+
+template <int BN, bool TRANS_A>
+void launch_t(const CUtensorMap& ta, const CUtensorMap& bh, const CUtensorMap& bl,
+              const DGemmArgs& g, int splits, int64_t kps, double* out, int64_t ldo,
+              int64_t stride, cudaStream_t st) {
+  using Cfg = TCfg<BN>;
+  auto kern = tgemm_kernel<BN, TRANS_A>;
+  XB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+  dim3 grid((unsigned)ceil_div(g.M, TBM), (unsigned)ceil_div(g.N, BN), (unsigned)splits);
+  const int acc_here = (splits == 1 && g.accumulate) ? 1 : 0;
+  kern<<<grid, kThreadsT, Cfg::SMEM, st>>>(ta, bh, bl, g.M, g.N, g.K, out, ldo, stride, kps,
+                                           acc_here);
+  check_launch("tgemm");
+}
+
+}  // namespace
+
+bool tgemm_supported(const DGemmArgs& g) {
+  if (!g.a_f32) return false;
+  if ((reinterpret_cast<uintptr_t>(g.A) & 15) != 0 || (g.lda % 4) != 0) return false;
+  if (g.M < 1 || g.N < 1 || g.K < 1) return false;
+  static const int env = [] {
+    const char* e = getenv("XB_F32_GEMM");
+    return (e && strcmp(e, "dmma") == 0) ? 0 : 1;
+  }();
+  return env == 1;
+}
+
+int tgemm_plan_splits(const DGemmArgs& g) {
+  const int bn = pick_tbn(g.N);
+  const int64_t tiles = ceil_div(g.M, TBM) * ceil_div(g.N, bn);
+  const int64_t kt = ceil_div(g.K, TBK);
+  // f32 accumulation chains of at most 32k terms per slice, and enough CTAs
+  int s = (int)std::max<int64_t>(1, ceil_div(g.K, 32768));
+  while (tiles * s < 2 * kNumSMs && kt / (s * 2) >= 8) s *= 2;
+  return std::max(1, std::min<int>(s, (int)kt));
+}
+
+size_t tgemm_b_floats(const DGemmArgs& g) { return (size_t)g.N * round_up(g.K, 4); }
+
+void tgemm(const DGemmArgs& g, int splits, double* work, float* bhi, float* blo, cudaStream_t st) {
+  const int64_t kp = round_up(g.K, 4);
+  {
+    dim3 grid((unsigned)ceil_div(kp, 32), (unsigned)ceil_div(g.N, 32));
+    split_b_kernel<<<grid, dim3(32, 8), 0, st>>>(g.B, g.K, g.N, g.ldb, bhi, blo, kp);
+    check_launch("split_b");
+  }
+  splits = std::max(1, std::min<int>(splits, (int)ceil_div(g.K, TBK)));
+  const int64_t kps = round_up(ceil_div(g.K, splits), TBK);
+  splits = (int)ceil_div(g.K, kps);
+  double* out = g.C;
+  int64_t ldo = g.ldc, stride = 0;
+  if (splits > 1) {
+    XB_REQUIRE(work != nullptr, XB_ECUDA, "tgemm: split-K workspace missing");
+    out = work;
+    ldo = round_up(g.N, 2);
+    stride = g.M * ldo;
+  }
+  const int bn = pick_tbn(g.N);
+  // A: NN -> [M][K] K-major, 128B-swizzled boxes {32, 128};
+  //    TN -> [K][M] M-contiguous, unswizzled boxes {128, 32} (the converter transposes)
+  const CUtensorMap ta = g.trans_a
+                             ? make_map(g.A, (uint64_t)g.M, (uint64_t)g.K, g.lda, TBM, TBK, false)
+                             : make_map(g.A, (uint64_t)g.K, (uint64_t)g.M, g.lda, TBK, TBM, true);
+  const CUtensorMap th = make_map(bhi, (uint64_t)kp, (uint64_t)g.N, kp, TBK, bn, true);
+  const CUtensorMap tl = make_map(blo, (uint64_t)kp, (uint64_t)g.N, kp, TBK, bn, true);
+#define XB_T(BN)                                                                  \
+  if (g.trans_a)                                                                  \
+    launch_t<BN, true>(ta, th, tl, g, splits, kps, out, ldo, stride, st);         \
+  else                                                                            \
+    launch_t<BN, false>(ta, th, tl, g, splits, kps, out, ldo, stride, st);        \
+  break;
+  switch (bn) {
+    case 64: XB_T(64)
+    case 128: XB_T(128)
+    case 192: XB_T(192)
+    case 224: XB_T(224)
+    default: XB_T(256)
+  }
+#undef XB_T
+  if (splits > 1) launch_split_reduce(work, g.M, g.N, ldo, stride, splits, g.C, g.ldc, g.accumulate, st);
+}
+
+}  // namespace xb
