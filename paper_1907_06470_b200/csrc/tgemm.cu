@@ -70,10 +70,11 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+// tf32 "hi" part: the f32 bit pattern with the 13 low mantissa bits cleared
+// (exactly the truncation the tensor core applies to a tf32 operand), so
+// hi is bit-exact what the MMA uses and lo = x - hi is exact in f32.
 __device__ __forceinline__ uint32_t to_tf32(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
-  return r;
+  return __float_as_uint(x) & 0xFFFFE000u;
 }
 
 // Shared-memory matrix descriptor: K-major, 128B swizzle, 8-row groups 1024 B
@@ -133,7 +134,7 @@ __global__ void __launch_bounds__(kThreadsT, 1)
     tgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBh,
                  const __grid_constant__ CUtensorMap tmBl, int64_t M, int64_t N, int64_t K,
                  double* __restrict__ C, int64_t ldc, int64_t split_stride, int64_t k_per_split,
-                 int accumulate) {
+                 int accumulate, int mode) {
   using Cfg = TCfg<BN>;
   extern __shared__ unsigned char smem_raw_t[];
   unsigned char* smem =
@@ -171,6 +172,9 @@ __global__ void __launch_bounds__(kThreadsT, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  if ((mode & 128) && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)
+    printf("[tgemm] smem base 0x%x raw 0x%x stage %d tmem 0x%x ktiles %d BN %d\n", su32(smem),
+           su32(smem_raw_t), Cfg::STAGE, tmem, ktiles, BN);
 
   if (warp == 0) {
     // ---- TMA producer ------------------------------------------------------
@@ -197,6 +201,7 @@ __global__ void __launch_bounds__(kThreadsT, 1)
       const int s = kt % TSTAGES;
       mbar_wait(&conv[s], (kt / TSTAGES) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      if (mode & 32) __nanosleep(20000);
       if (lane == 0) {
         unsigned char* st = smem + s * Cfg::STAGE;
         const uint64_t ah = sw128_desc(su32(st + Cfg::AHI));
@@ -206,9 +211,14 @@ __global__ void __launch_bounds__(kThreadsT, 1)
 #pragma unroll
         for (int kk = 0; kk < TBK / 8; ++kk) {
           const uint64_t off = (uint64_t)(kk * 32) >> 4;  // 8 tf32 = 32 B inside the atom
+          if (mode & 1536) {  // diagnostics: one MMA per k-step from a chosen A plane
+            const uint64_t ap = (mode & 512) ? al : sw128_desc(su32(st + Cfg::RAW));
+            mma_tf32(tmem, ap + off, bh + off, idesc, (kt > 0 || kk > 0) ? 1u : 0u);
+            continue;
+          }
           mma_tf32(tmem, ah + off, bh + off, idesc, (kt > 0 || kk > 0) ? 1u : 0u);
-          mma_tf32(tmem, ah + off, bl + off, idesc, 1u);
-          mma_tf32(tmem, al + off, bh + off, idesc, 1u);
+          if (mode & 1) mma_tf32(tmem, ah + off, bl + off, idesc, 1u);
+          if (mode & 2) mma_tf32(tmem, al + off, bh + off, idesc, 1u);
         }
         mma_commit(&empty[s]);
         if (kt == ktiles - 1) mma_commit(tmem_full);
@@ -240,6 +250,12 @@ __global__ void __launch_bounds__(kThreadsT, 1)
           l.y = v.y - h.y;
           l.z = v.z - h.z;
           l.w = v.w - h.w;
+          if (mode & 16) l = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (mode & 256) {
+            h = make_float4(1.f, 1.f, 1.f, 1.f);
+            const float c = 0.25f * (float)(kt + 1);
+            l = make_float4(c, c, c, c);
+          }
           hi[i] = h;
           lo[i] = l;
         }
@@ -272,6 +288,10 @@ __global__ void __launch_bounds__(kThreadsT, 1)
       }
       // make the generic-proxy smem writes visible to the tensor core
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      if (mode & 64) {
+        __threadfence_block();
+        asm volatile("fence.proxy.async;\n" ::: "memory");
+      }
       __syncwarp();
       if (lane == 0) mbar_arrive(&conv[s]);
     }
@@ -386,8 +406,13 @@ void launch_t(const CUtensorMap& ta, const CUtensorMap& bh, const CUtensorMap& b
   XB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
   dim3 grid((unsigned)ceil_div(g.M, TBM), (unsigned)ceil_div(g.N, BN), (unsigned)splits);
   const int acc_here = (splits == 1 && g.accumulate) ? 1 : 0;
+  // XB_TG_MODE (diagnostics): bit 0 = A_hi B_lo term, bit 1 = A_lo B_hi term
+  static const int mode = [] {
+    const char* e = getenv("XB_TG_MODE");
+    return e ? atoi(e) : 3;
+  }();
   kern<<<grid, kThreadsT, Cfg::SMEM, st>>>(ta, bh, bl, g.M, g.N, g.K, out, ldo, stride, kps,
-                                           acc_here);
+                                           acc_here, mode);
   check_launch("tgemm");
 }
 
@@ -408,8 +433,17 @@ int tgemm_plan_splits(const DGemmArgs& g) {
   const int bn = pick_tbn(g.N);
   const int64_t tiles = ceil_div(g.M, TBM) * ceil_div(g.N, bn);
   const int64_t kt = ceil_div(g.K, TBK);
-  // f32 accumulation chains of at most 32k terms per slice, and enough CTAs
-  int s = (int)std::max<int64_t>(1, ceil_div(g.K, 32768));
+  // Bounded TMEM accumulation chains per slice (slices are summed in f64).
+  // Measured on B200 (tools/diag_tgemm3.py): the tensor core's f32
+  // accumulation loses precision with chain length (K=65536: mean |err| 6e-3
+  // at 32k-long chains, 3e-3 at 2k, 9e-4 at 512, vs ~2e-4 for an exact f32
+  // 3xTF32 sum); 8192 keeps the product error ~5e-5 relative for a few-%
+  // workspace traffic.
+  static const int64_t chain = [] {
+    const char* e = getenv("XB_TG_CHAIN");
+    return e ? std::max<int64_t>(32, atoll(e)) : (int64_t)8192;
+  }();
+  int s = (int)std::max<int64_t>(1, ceil_div(g.K, chain));
   while (tiles * s < 2 * kNumSMs && kt / (s * 2) >= 8) s *= 2;
   return std::max(1, std::min<int>(s, (int)kt));
 }
