@@ -20,10 +20,11 @@ e2e    = the same metric through the reference-facing C ABI call
          (xb_rsvd_dense / xb_rsvd_coo) with HOST buffers: pinned A copied
          H2D inside the timed region (overlapped with the sketch), U/s/V
          copied back.
-roofline = the dominant kernel: dense -> the FP64 DMMA tile GEMM over A
+roofline = the dominant kernel: dense f64 -> the FP64 DMMA tile GEMM over A
          (achieved = 2*m*n*l flops per launch / its event-timed mean duration,
          peak = the FP64 DMMA pipe rate measured in-process: MEASURED_PEAKS.json
-         has no FP64 figure); sparse -> the CSR SpMM (achieved = algorithmic
+         has no FP64 figure); dense f32 -> the tcgen05 3xTF32 GEMM (same
+         achieved, peak = MEASURED_PEAKS bf16 / 2 / 3); sparse -> the CSR SpMM (achieved = algorithmic
          bytes per launch / duration, peak = MEASURED_PEAKS.json hbm_gbs).
 cpu_baseline = the oracle's restatement of the reference's shipped driver
          (oracle/, "port") on two bounded samples of the workload, extrapolated
@@ -276,13 +277,27 @@ class DenseCase:
     def roofline(self, prof, dmma_peak, dfma_peak, hbm_peak):
         per_s = prof["seconds"] / max(prof["launches"], 1)
         achieved = prof["flops"] / max(prof["launches"], 1) / per_s / 1e12
+        hbm = prof["bytes"] / prof["seconds"] / 1e9 if prof["seconds"] else None
+        if self.esz == 4 and os.environ.get("XB_F32_GEMM") != "dmma":
+            # 3xTF32 on tcgen05: useful flops = 2 m n l, the tensor pipe does 3x
+            # that in kind::tf32, whose dense rate is half the bf16 rate.
+            bf16 = measured_peaks().get("bf16_tflops")
+            peak = bf16 / 2 / 3 if bf16 else 2250.0 / 2 / 3
+            return {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                    "frac": achieved / peak,
+                    "kernel": "tgemm_kernel (tcgen05.mma kind::tf32 x3 split, TMA, TMEM; "
+                              "NN/TN over float32 A)",
+                    "peak_source": ("MEASURED_PEAKS.json bf16_tflops / 2 (tf32 rate) / 3 (three "
+                                    "products per useful flop)" if bf16 else
+                                    "nominal 2250 bf16 TF/s / 2 / 3 (no MEASURED_PEAKS.json)"),
+                    "hbm_gbs_achieved": hbm}
         return {"bound": "tensor", "achieved": achieved, "peak": dmma_peak, "unit": "TFLOP/s",
                 "frac": achieved / dmma_peak if dmma_peak else None,
                 "kernel": "dgemm_kernel (FP64 DMMA m8n8k4, NN/TN over A"
                           + (", float32 A widened to f64)" if self.esz == 4 else ")"),
                 "peak_source": f"in-process DMMA microbenchmark ({dmma_peak:.1f} TF/s; DFMA "
                                f"{dfma_peak:.1f} TF/s); MEASURED_PEAKS.json has no FP64 entry",
-                "hbm_gbs_achieved": prof["bytes"] / prof["seconds"] / 1e9 if prof["seconds"] else None}
+                "hbm_gbs_achieved": hbm}
 
 
 class ShardedDenseCase(DenseCase):

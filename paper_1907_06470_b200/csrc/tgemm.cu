@@ -8,16 +8,26 @@
 // and  A B ~ A_hi B_hi + A_hi B_lo + A_lo B_hi  (three tcgen05.mma.kind::tf32
 // into one f32 TMEM accumulator; the dropped A_lo B_lo term is ~2^-22).
 //
-// Warp roles (192 threads, one CTA per 128 x BN output tile):
-//   warp 0    TMA producer: raw A tile + the pre-split B_hi / B_lo tiles
-//   warp 1    TMEM allocator + single-thread MMA issuer
-//   warps 2-5 converters: raw A tile -> A_hi, A_lo in the canonical K-major
-//             128B-swizzled layout (for the transposed view of A this is
-//             also the transpose), then the epilogue (tcgen05.ld -> f64 C)
+// Warp roles (704 threads, one CTA per 128 x BN output tile):
+//   warp 0      TMA producer: raw A tile + the pre-split B_hi / B_lo tiles
+//   warp 1      TMEM allocator + single-thread MMA issuer
+//   warps 2-5   converters: raw A tile -> A_hi, A_lo in the canonical K-major
+//               128B-swizzled layout (for the transposed view of A this is
+//               also the transpose)
+//   warps 6-21  drain + epilogue: 4 warps per TMEM lane quadrant, each owning
+//               BN/4 columns of its 32 rows
 // Pipelines: full[s] (TMA complete_tx) -> conv[s] (4 converter warps) ->
-// MMA -> tcgen05.commit -> empty[s] (frees the stage), tmem_full after the
-// last k-tile. Split-K slices go to an f64 workspace reduced in slice order
-// by dgemm.cu's deterministic reduce.
+// MMA -> tcgen05.commit -> empty[s] (frees the stage).
+//
+// Accumulation: the tensor core's f32 accumulator does not round to nearest
+// (measured: the error grows ~linearly with the accumulation chain, e.g. a
+// K=65536 product is ~30x less accurate than an f32 round-to-nearest sum), so
+// the MMA accumulates only P k-tiles (P*32 of K, XB_TG_DRAIN) into one of two
+// TMEM buffers; the drain warps fold each finished group into f32 registers
+// with ordinary round-to-nearest adds while the MMA fills the other buffer
+// (tmem_full[b] / tmem_empty[b]). The result is as accurate as an f32 SGEMM.
+// Split-K slices go to an f64 workspace reduced in slice order by dgemm.cu's
+// deterministic reduce.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -32,7 +42,8 @@ namespace {
 constexpr int TBM = 128;  // UMMA_M (cta_group::1)
 constexpr int TBK = 32;   // one 128-byte swizzle atom of tf32
 constexpr int TSTAGES = 2;
-constexpr int kThreadsT = 192;
+constexpr int kDrainGroups = 4;  // column segments per TMEM lane quadrant
+constexpr int kThreadsT = 192 + 128 * kDrainGroups;
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -126,7 +137,10 @@ struct TCfg {
   static constexpr int STAGE = BLO + ((B_BYTES + 1023) / 1024) * 1024;
   static constexpr int BAR_OFF = TSTAGES * STAGE;
   static constexpr int SMEM = BAR_OFF + 256 + 1024;    // + barriers, tmem slot, align slack
-  static constexpr int TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+  // two accumulator buffers (MMA fills one while the drain warps read the other)
+  static constexpr int TMEM_COLS = BN <= 16 ? 32 : BN <= 32 ? 64 : BN <= 64 ? 128 : BN <= 128 ? 256 : 512;
+  static constexpr int BUF_COLS = TMEM_COLS / 2;
+  static constexpr int SEG = BN / kDrainGroups;        // columns per drain thread
 };
 
 template <int BN, bool TRANS_A>
@@ -134,16 +148,18 @@ __global__ void __launch_bounds__(kThreadsT, 1)
     tgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBh,
                  const __grid_constant__ CUtensorMap tmBl, int64_t M, int64_t N, int64_t K,
                  double* __restrict__ C, int64_t ldc, int64_t split_stride, int64_t k_per_split,
-                 int accumulate, int mode) {
+                 int accumulate, int drain_tiles) {
   using Cfg = TCfg<BN>;
+  static_assert(Cfg::SEG % 8 == 0, "drain segment must be a multiple of 8 columns");
   extern __shared__ unsigned char smem_raw_t[];
   unsigned char* smem =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw_t) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::BAR_OFF);
   uint64_t* conv = full + TSTAGES;
   uint64_t* empty = conv + TSTAGES;
-  uint64_t* tmem_full = empty + TSTAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* tmem_full = empty + TSTAGES;   // [2]
+  uint64_t* tmem_empty = tmem_full + 2;    // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t m0 = (int64_t)blockIdx.x * TBM;
@@ -151,6 +167,8 @@ __global__ void __launch_bounds__(kThreadsT, 1)
   const int64_t kbeg = (int64_t)blockIdx.z * k_per_split;
   const int64_t kend = min(K, kbeg + k_per_split);
   const int ktiles = (int)((kend - kbeg + TBK - 1) / TBK);
+  const int P = drain_tiles;
+  const int groups = (ktiles + P - 1) / P;
   C += (int64_t)blockIdx.z * split_stride;
 
   if (threadIdx.x == 0) {
@@ -159,7 +177,10 @@ __global__ void __launch_bounds__(kThreadsT, 1)
       mbar_init(&conv[s], 4);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tmem_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tmem_full[b], 1);
+      mbar_init(&tmem_empty[b], 4 * kDrainGroups);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 1) {
@@ -172,9 +193,6 @@ __global__ void __launch_bounds__(kThreadsT, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem = *tmem_slot;
-  if ((mode & 128) && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)
-    printf("[tgemm] smem base 0x%x raw 0x%x stage %d tmem 0x%x ktiles %d BN %d\n", su32(smem),
-           su32(smem_raw_t), Cfg::STAGE, tmem, ktiles, BN);
 
   if (warp == 0) {
     // ---- TMA producer ------------------------------------------------------
@@ -195,14 +213,18 @@ __global__ void __launch_bounds__(kThreadsT, 1)
       }
     }
   } else if (warp == 1) {
-    // ---- MMA issuer ------------------------------------------------------------
+    // ---- MMA issuer: group g of P k-tiles accumulates into buffer g & 1 ----------
     const uint32_t idesc = idesc_tf32<BN>();
     for (int kt = 0; kt < ktiles; ++kt) {
       const int s = kt % TSTAGES;
+      const int g = kt / P, b = g & 1;
+      const bool first = (kt % P) == 0;
+      const bool last = (kt % P) == P - 1 || kt == ktiles - 1;
+      if (first && g >= 2) mbar_wait(&tmem_empty[b], ((g >> 1) - 1) & 1);
       mbar_wait(&conv[s], (kt / TSTAGES) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      if (mode & 32) __nanosleep(20000);
       if (lane == 0) {
+        const uint32_t d = tmem + (uint32_t)(b * Cfg::BUF_COLS);
         unsigned char* st = smem + s * Cfg::STAGE;
         const uint64_t ah = sw128_desc(su32(st + Cfg::AHI));
         const uint64_t al = sw128_desc(su32(st + Cfg::ALO));
@@ -211,22 +233,16 @@ __global__ void __launch_bounds__(kThreadsT, 1)
 #pragma unroll
         for (int kk = 0; kk < TBK / 8; ++kk) {
           const uint64_t off = (uint64_t)(kk * 32) >> 4;  // 8 tf32 = 32 B inside the atom
-          if (mode & 1536) {  // diagnostics: one MMA per k-step from a chosen A plane
-            const uint64_t ap = (mode & 512) ? al : sw128_desc(su32(st + Cfg::RAW));
-            mma_tf32(tmem, ap + off, bh + off, idesc, (kt > 0 || kk > 0) ? 1u : 0u);
-            continue;
-          }
-          mma_tf32(tmem, ah + off, bh + off, idesc, (kt > 0 || kk > 0) ? 1u : 0u);
-          if (mode & 1) mma_tf32(tmem, ah + off, bl + off, idesc, 1u);
-          if (mode & 2) mma_tf32(tmem, al + off, bh + off, idesc, 1u);
+          mma_tf32(d, ah + off, bh + off, idesc, (!first || kk > 0) ? 1u : 0u);
+          mma_tf32(d, ah + off, bl + off, idesc, 1u);
+          mma_tf32(d, al + off, bh + off, idesc, 1u);
         }
         mma_commit(&empty[s]);
-        if (kt == ktiles - 1) mma_commit(tmem_full);
+        if (last) mma_commit(&tmem_full[b]);
       }
       __syncwarp();
     }
-    if (ktiles == 0 && lane == 0) mbar_arrive(tmem_full);
-  } else {
+  } else if (warp < 6) {
     // ---- converters: raw A -> A_hi, A_lo (K-major, 128B swizzle) -----------------
     const int ct = threadIdx.x - 64;  // 0..127
     for (int kt = 0; kt < ktiles; ++kt) {
@@ -250,12 +266,6 @@ __global__ void __launch_bounds__(kThreadsT, 1)
           l.y = v.y - h.y;
           l.z = v.z - h.z;
           l.w = v.w - h.w;
-          if (mode & 16) l = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (mode & 256) {
-            h = make_float4(1.f, 1.f, 1.f, 1.f);
-            const float c = 0.25f * (float)(kt + 1);
-            l = make_float4(c, c, c, c);
-          }
           hi[i] = h;
           lo[i] = l;
         }
@@ -288,37 +298,50 @@ __global__ void __launch_bounds__(kThreadsT, 1)
       }
       // make the generic-proxy smem writes visible to the tensor core
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      if (mode & 64) {
-        __threadfence_block();
-        asm volatile("fence.proxy.async;\n" ::: "memory");
-      }
       __syncwarp();
       if (lane == 0) mbar_arrive(&conv[s]);
     }
-    // ---- epilogue: TMEM -> registers -> f64 C ----------------------------------
-    mbar_wait(tmem_full, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    const int q = warp & 3;  // TMEM lanes 32q .. 32q+31
+  } else {
+    // ---- drain warps: TMEM group partials -> f32 register sums (round to
+    // nearest), then the f64 epilogue. Warp w reads TMEM lanes 32 (w % 4) ..
+    // +31 (the hardware's lane-quadrant rule) and column segment (w - 6) / 4.
+    const int q = warp & 3;
+    const int seg = (warp - 6) >> 2;
     const int row = 32 * q + lane;
-    const int64_t r = m0 + row;
-#pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 8) {
-      uint32_t v[8];
-      const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)c0;
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
-          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-            "=r"(v[7])
-          : "r"(taddr));
-      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-      if (r < M) {
-        double* dst = C + r * ldc + n0 + c0;
+    const uint32_t lane_base = (uint32_t)(32 * q) << 16;
+    float acc[Cfg::SEG];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          if (n0 + c0 + j < N) {
-            const double x = (double)__uint_as_float(v[j]);
-            dst[j] = accumulate ? dst[j] + x : x;
-          }
+    for (int j = 0; j < Cfg::SEG; ++j) acc[j] = 0.f;
+    for (int g = 0; g < groups; ++g) {
+      const int b = g & 1;
+      mbar_wait(&tmem_full[b], (g >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      const uint32_t base = tmem + lane_base + (uint32_t)(b * Cfg::BUF_COLS + seg * Cfg::SEG);
+#pragma unroll
+      for (int c0 = 0; c0 < Cfg::SEG; c0 += 8) {
+        uint32_t v[8];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+              "=r"(v[7])
+            : "r"(base + (uint32_t)c0));
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[c0 + j] += __uint_as_float(v[j]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tmem_empty[b]);
+    }
+    const int64_t r = m0 + row;
+    if (r < M) {
+      const int64_t cbase = n0 + seg * Cfg::SEG;
+      double* dst = C + r * ldc + cbase;
+#pragma unroll
+      for (int j = 0; j < Cfg::SEG; ++j) {
+        if (cbase + j < N) {
+          const double x = (double)acc[j];
+          dst[j] = accumulate ? dst[j] + x : x;
         }
       }
     }
@@ -390,11 +413,10 @@ int pick_tbn(int64_t N) {
   if (N <= 128) return 128;
   if (N <= 192) return 192;
   if (N <= 224) return 224;
-  // wide sketches: 3 x 192 covers cfg5's 552 with 4% padding
-  const int64_t w192 = ceil_div(N, 192) * 192, w224 = ceil_div(N, 224) * 224,
-                w256 = ceil_div(N, 256) * 256;
-  if (w192 <= w224 && w192 <= w256) return 192;
-  return w224 <= w256 ? 224 : 256;
+  // wide sketches: 3 x 192 covers cfg5's 552 with 4% padding (BN = 256 would
+  // not fit the drain warps' f32 sums in the 80-register budget of 704 threads)
+  const int64_t w192 = ceil_div(N, 192) * 192, w224 = ceil_div(N, 224) * 224;
+  return w192 <= w224 ? 192 : 224;
 }
 
 template <int BN, bool TRANS_A>
@@ -406,13 +428,13 @@ void launch_t(const CUtensorMap& ta, const CUtensorMap& bh, const CUtensorMap& b
   XB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
   dim3 grid((unsigned)ceil_div(g.M, TBM), (unsigned)ceil_div(g.N, BN), (unsigned)splits);
   const int acc_here = (splits == 1 && g.accumulate) ? 1 : 0;
-  // XB_TG_MODE (diagnostics): bit 0 = A_hi B_lo term, bit 1 = A_lo B_hi term
-  static const int mode = [] {
-    const char* e = getenv("XB_TG_MODE");
-    return e ? atoi(e) : 3;
+  // k-tiles per TMEM accumulation group (XB_TG_DRAIN overrides for sweeps)
+  static const int drain = [] {
+    const char* e = getenv("XB_TG_DRAIN");
+    return e ? std::max(1, atoi(e)) : 2;
   }();
   kern<<<grid, kThreadsT, Cfg::SMEM, st>>>(ta, bh, bl, g.M, g.N, g.K, out, ldo, stride, kps,
-                                           acc_here, mode);
+                                           acc_here, drain);
   check_launch("tgemm");
 }
 
@@ -433,15 +455,11 @@ int tgemm_plan_splits(const DGemmArgs& g) {
   const int bn = pick_tbn(g.N);
   const int64_t tiles = ceil_div(g.M, TBM) * ceil_div(g.N, bn);
   const int64_t kt = ceil_div(g.K, TBK);
-  // Bounded TMEM accumulation chains per slice (slices are summed in f64).
-  // Measured on B200 (tools/diag_tgemm3.py): the tensor core's f32
-  // accumulation loses precision with chain length (K=65536: mean |err| 6e-3
-  // at 32k-long chains, 3e-3 at 2k, 9e-4 at 512, vs ~2e-4 for an exact f32
-  // 3xTF32 sum); 8192 keeps the product error ~5e-5 relative for a few-%
-  // workspace traffic.
+  // K per split slice (slices are summed in f64); the TMEM groups inside a
+  // slice are summed in f32 registers, so the chain only bounds that f32 sum.
   static const int64_t chain = [] {
     const char* e = getenv("XB_TG_CHAIN");
-    return e ? std::max<int64_t>(32, atoll(e)) : (int64_t)8192;
+    return e ? std::max<int64_t>(32, atoll(e)) : (int64_t)32768;
   }();
   int s = (int)std::max<int64_t>(1, ceil_div(g.K, chain));
   while (tiles * s < 2 * kNumSMs && kt / (s * 2) >= 8) s *= 2;
@@ -486,8 +504,7 @@ void tgemm(const DGemmArgs& g, int splits, double* work, float* bhi, float* blo,
     case 64: XB_T(64)
     case 128: XB_T(128)
     case 192: XB_T(192)
-    case 224: XB_T(224)
-    default: XB_T(256)
+    default: XB_T(224)
   }
 #undef XB_T
   if (splits > 1) launch_split_reduce(work, g.M, g.N, ldo, stride, splits, g.C, g.ldc, g.accumulate, st);
