@@ -232,6 +232,33 @@ def run_reference(args):
 
 # -- device workloads -----------------------------------------------------------------
 
+def gemm_roofline(prof, esz, dmma_peak, dfma_peak):
+    """The GEMM over A: 2 m n l useful flops per launch / event-timed duration."""
+    per_s = prof["seconds"] / max(prof["launches"], 1)
+    achieved = prof["flops"] / max(prof["launches"], 1) / per_s / 1e12
+    hbm = prof["bytes"] / prof["seconds"] / 1e9 if prof["seconds"] else None
+    if esz == 4 and os.environ.get("XB_F32_GEMM") != "dmma":
+        # 3xTF32 on tcgen05: useful flops = 2 m n l, the tensor pipe does 3x
+        # that in kind::tf32, whose dense rate is half the bf16 rate.
+        bf16 = measured_peaks().get("bf16_tflops")
+        peak = bf16 / 2 / 3 if bf16 else 2250.0 / 2 / 3
+        return {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak,
+                "kernel": "tgemm_kernel (tcgen05.mma kind::tf32 x3 split, TMA, TMEM; "
+                          "NN/TN over float32 A)",
+                "peak_source": ("MEASURED_PEAKS.json bf16_tflops / 2 (tf32 rate) / 3 (three "
+                                "products per useful flop)" if bf16 else
+                                "nominal 2250 bf16 TF/s / 2 / 3 (no MEASURED_PEAKS.json)"),
+                "hbm_gbs_achieved": hbm}
+    return {"bound": "tensor", "achieved": achieved, "peak": dmma_peak, "unit": "TFLOP/s",
+            "frac": achieved / dmma_peak if dmma_peak else None,
+            "kernel": "dgemm_kernel (FP64 DMMA m8n8k4, NN/TN over A"
+                      + (", float32 A widened to f64)" if esz == 4 else ")"),
+            "peak_source": f"in-process DMMA microbenchmark ({dmma_peak:.1f} TF/s; DFMA "
+                           f"{dfma_peak:.1f} TF/s); MEASURED_PEAKS.json has no FP64 entry",
+            "hbm_gbs_achieved": hbm}
+
+
 class DenseCase:
     """Dense A resident on the device (torch tensor) + pinned host copy for e2e."""
 
@@ -275,29 +302,7 @@ class DenseCase:
         return w.m * w.n * self.esz, (w.m + w.n) * w.k * self.esz + w.k * 8
 
     def roofline(self, prof, dmma_peak, dfma_peak, hbm_peak):
-        per_s = prof["seconds"] / max(prof["launches"], 1)
-        achieved = prof["flops"] / max(prof["launches"], 1) / per_s / 1e12
-        hbm = prof["bytes"] / prof["seconds"] / 1e9 if prof["seconds"] else None
-        if self.esz == 4 and os.environ.get("XB_F32_GEMM") != "dmma":
-            # 3xTF32 on tcgen05: useful flops = 2 m n l, the tensor pipe does 3x
-            # that in kind::tf32, whose dense rate is half the bf16 rate.
-            bf16 = measured_peaks().get("bf16_tflops")
-            peak = bf16 / 2 / 3 if bf16 else 2250.0 / 2 / 3
-            return {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                    "frac": achieved / peak,
-                    "kernel": "tgemm_kernel (tcgen05.mma kind::tf32 x3 split, TMA, TMEM; "
-                              "NN/TN over float32 A)",
-                    "peak_source": ("MEASURED_PEAKS.json bf16_tflops / 2 (tf32 rate) / 3 (three "
-                                    "products per useful flop)" if bf16 else
-                                    "nominal 2250 bf16 TF/s / 2 / 3 (no MEASURED_PEAKS.json)"),
-                    "hbm_gbs_achieved": hbm}
-        return {"bound": "tensor", "achieved": achieved, "peak": dmma_peak, "unit": "TFLOP/s",
-                "frac": achieved / dmma_peak if dmma_peak else None,
-                "kernel": "dgemm_kernel (FP64 DMMA m8n8k4, NN/TN over A"
-                          + (", float32 A widened to f64)" if self.esz == 4 else ")"),
-                "peak_source": f"in-process DMMA microbenchmark ({dmma_peak:.1f} TF/s; DFMA "
-                               f"{dfma_peak:.1f} TF/s); MEASURED_PEAKS.json has no FP64 entry",
-                "hbm_gbs_achieved": hbm}
+        return gemm_roofline(prof, self.esz, dmma_peak, dfma_peak)
 
 
 class ShardedDenseCase(DenseCase):
@@ -377,14 +382,12 @@ class StreamedCase:
             e1.record()
             torch.cuda.synchronize()
             best = max(best, (1 << 30) / (e0.elapsed_time(e1) * 1e-3) / 1e9)
-        per_s = prof["seconds"] / max(prof["launches"], 1)
-        achieved = prof["flops"] / max(prof["launches"], 1) / per_s / 1e12
-        return {"bound": "tensor", "achieved": achieved, "peak": dmma_peak, "unit": "TFLOP/s",
-                "frac": achieved / dmma_peak if dmma_peak else None,
-                "kernel": "dgemm_kernel on streamed f32 tiles (NN A_i X and TN W += A_i^T Y_i)",
-                "host_link_gbs_peak": best,
-                "note": "the streamed passes are bounded by the host link, not the kernel: see "
-                        "stream_gbs vs host_link_gbs_peak"}
+        r = gemm_roofline(prof, 4, dmma_peak, dfma_peak)
+        r["kernel"] += " on streamed f32 row tiles (NN A_i X and TN W += A_i^T Y_i)"
+        r["host_link_gbs_peak"] = best
+        r["note"] = ("the streamed passes are bounded by the host link, not the kernel: see "
+                     "stream_gbs vs host_link_gbs_peak")
+        return r
 
 
 class SparseCase:

@@ -42,7 +42,13 @@ struct xb_ctx {
   cudaStream_t st = nullptr;  // compute
   cudaStream_t cp = nullptr;  // host <-> device copies
   int64_t launches = 0;
-  std::map<std::string, std::pair<void*, size_t>> bufs;
+  struct Buf {
+    void* p;
+    size_t bytes;
+    uint64_t gen;  // the ABI call that last used it
+  };
+  std::map<std::string, Buf> bufs;
+  uint64_t gen = 0;  // bumped on entry to every ABI call
   std::vector<cudaEvent_t> events;
   // per-kernel profiling of the products on A (xb_profile_*)
   bool profiling = false;
@@ -79,18 +85,44 @@ struct xb_ctx {
     prof_pending.clear();
   }
 
+  // Named device buffers cached across calls. When HBM runs out, buffers no
+  // earlier step of the current call has touched are released and the
+  // allocation retried (a previous call's shapes must not pin memory).
   void* buf(const std::string& name, size_t bytes) {
     auto it = bufs.find(name);
-    if (it != bufs.end() && it->second.second >= bytes) return it->second.first;
+    if (it != bufs.end() && it->second.bytes >= bytes) {
+      it->second.gen = gen;
+      return it->second.p;
+    }
     if (it != bufs.end()) {
       XB_CUDA(cudaStreamSynchronize(st));
-      XB_CUDA(cudaFree(it->second.first));
+      XB_CUDA(cudaFree(it->second.p));
       bufs.erase(it);
     }
     void* p = nullptr;
-    XB_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 256)));
-    bufs[name] = {p, bytes};
+    const size_t sz = std::max<size_t>(bytes, 256);
+    if (cudaMalloc(&p, sz) != cudaSuccess) {
+      cudaGetLastError();
+      XB_CUDA(cudaStreamSynchronize(st));
+      XB_CUDA(cudaStreamSynchronize(cp));
+      for (auto i = bufs.begin(); i != bufs.end();) {
+        if (i->second.gen != gen) {
+          XB_CUDA(cudaFree(i->second.p));
+          i = bufs.erase(i);
+        } else {
+          ++i;
+        }
+      }
+      XB_REQUIRE(cudaMalloc(&p, sz) == cudaSuccess, XB_ENOMEM,
+                 "device allocation of " + std::to_string(sz) + " bytes (" + name + ") failed");
+    }
+    bufs[name] = {p, bytes, gen};
     return p;
+  }
+  size_t cached_bytes() const {
+    size_t t = 0;
+    for (auto& kv : bufs) t += kv.second.bytes;
+    return t;
   }
   double* dbuf(const std::string& name, size_t count) {
     return static_cast<double*>(buf(name, count * sizeof(double)));
@@ -198,6 +230,7 @@ struct LaunchScope {
   int64_t* prev;
   explicit LaunchScope(xb_ctx* c) : prev(g_launch_counter) {
     g_launch_counter = &c->launches;
+    ++c->gen;
     cudaSetDevice(c->device);
   }
   ~LaunchScope() { g_launch_counter = prev; }
@@ -573,9 +606,13 @@ void rsvd_impl(xb_ctx* c, const AOp& op, int64_t m, int64_t n, const void* d_ome
     for (int64_t r0 = 0; r0 < m; r0 += ing.chunk_rows) {
       const int64_t rows = std::min(ing.chunk_rows, m - r0);
       const size_t es = a.esz();
-      XB_CUDA(cudaMemcpy2DAsync(const_cast<void*>(a.rows_from(r0)), a.ld * es,
-                                static_cast<const char*>(ing.hostA) + (size_t)r0 * ing.host_lda * es,
-                                ing.host_lda * es, n * es, rows, cudaMemcpyHostToDevice, c->cp));
+      const char* hsrc = static_cast<const char*>(ing.hostA) + (size_t)r0 * ing.host_lda * es;
+      if (ing.host_lda == n && a.ld == n)  // contiguous rows: one linear DMA
+        XB_CUDA(cudaMemcpyAsync(const_cast<void*>(a.rows_from(r0)), hsrc, (size_t)rows * n * es,
+                                cudaMemcpyHostToDevice, c->cp));
+      else
+        XB_CUDA(cudaMemcpy2DAsync(const_cast<void*>(a.rows_from(r0)), a.ld * es, hsrc,
+                                  ing.host_lda * es, n * es, rows, cudaMemcpyHostToDevice, c->cp));
       cudaEvent_t e;
       XB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       XB_CUDA(cudaEventRecord(e, c->cp));
@@ -587,6 +624,10 @@ void rsvd_impl(xb_ctx* c, const AOp& op, int64_t m, int64_t n, const void* d_ome
     XB_CUDA(cudaStreamSynchronize(c->cp));
     float ms = 0.f;
     XB_CUDA(cudaEventElapsedTime(&ms, t0, t1));
+    if (getenv("XB_TRACE"))
+      fprintf(stderr, "[xb] ingest: %lld chunks, host pinned %d, %.1f ms (%.1f GB/s)\n",
+              (long long)landed.size(), (int)is_pinned(ing.hostA), ms,
+              (double)m * n * a.esz() / (ms * 1e-3) / 1e9);
     local_stage[kParse] += ms * 1e-3;  // ingest (H2D), overlapped with the sketch
     for (auto e : landed) cudaEventDestroy(e);
     cudaEventDestroy(t0);
@@ -889,12 +930,15 @@ int64_t auto_tile_rows(int64_t m, int64_t n, size_t es) {
 }
 
 // Does A (m x n of `es` bytes) fit in HBM next to the factorisation's buffers?
-bool fits_in_hbm(int64_t m, int64_t n, size_t es, int lp) {
+// Does A fit in HBM next to the sketch buffers? This context's cached
+// buffers count as available (buf() releases stale ones on demand).
+bool fits_in_hbm(const xb_ctx* c, int64_t m, int64_t n, size_t es, int lp) {
   size_t free_b = 0, total_b = 0;
   if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
     cudaGetLastError();
     return true;
   }
+  free_b += c->cached_bytes();
   const double need = (double)m * n * es + (4.0 * m + 5.0 * n) * lp * 8.0 + 2.0 * 2 * std::max(m, n) * lp * 8.0 +
                       (double)(1ull << 30);
   return need < (double)free_b;
@@ -956,7 +1000,7 @@ int xb_destroy(xb_ctx* c) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->st);
     cudaStreamSynchronize(c->cp);
-    for (auto& kv : c->bufs) cudaFree(kv.second.first);
+    for (auto& kv : c->bufs) cudaFree(kv.second.p);
     for (auto e : c->events) cudaEventDestroy(e);
     if (c->stage_host) cudaFreeHost(c->stage_host);
     if (c->comm) nccl_comm_destroy(c->comm);
@@ -1051,7 +1095,7 @@ int xb_rsvd_dense(xb_ctx* c, int dtype, int64_t m, int64_t n, const void* A, int
     // out of core when A does not fit in HBM next to the sketch buffers (or
     // when streaming is forced): the tile streamer, q + 1 host passes
     const int lp = (int)round_up(l, 8);
-    const bool stream = g_force_stream_rows >= 0 || !fits_in_hbm(m, n, es, lp);
+    const bool stream = g_force_stream_rows >= 0 || !fits_in_hbm(c, m, n, es, lp);
     double t1 = 0.0;
     if (stream) {
       XB_REQUIRE(omega == nullptr, XB_EUNSUPPORTED,

@@ -29,13 +29,14 @@ def main():
     ctx = _lib.load(0)
     g = torch.Generator(device="cuda")
     g.manual_seed(w.cfg)
-    a = torch.randn(w.m, w.n, generator=g, device="cuda", dtype=torch.float64)
-    u = torch.empty((w.m, w.k), dtype=torch.float64, device="cuda")
-    v = torch.empty((w.n, w.k), dtype=torch.float64, device="cuda")
+    dt = torch.float64 if w.precision == "double" else torch.float32
+    a = torch.randn(w.m, w.n, generator=g, device="cuda", dtype=dt)
+    u = torch.empty((w.m, w.k), dtype=dt, device="cuda")
+    v = torch.empty((w.n, w.k), dtype=dt, device="cuda")
     s = torch.empty((w.k,), dtype=torch.float64, device="cuda")
     torch.cuda.synchronize()
     for i in range(args.warmup + args.steps):
-        _, stages = ctx.rsvd_dense_dev(np.float64, w.m, w.n, a.data_ptr(), w.n, w.k, w.p, w.q,
+        _, stages = ctx.rsvd_dense_dev(np.float64 if w.precision == "double" else np.float32, w.m, w.n, a.data_ptr(), w.n, w.k, w.p, w.q,
                                        w.cfg, u.data_ptr(), s.data_ptr(), v.data_ptr())
     print("stage seconds", np.round(stages, 5).tolist(), "launches", ctx.launches)
 
