@@ -1,5 +1,6 @@
 // l x l kernels of the hot path (single CTA, latency-bound, l <= ~160 in
-// shared memory, larger l from an L2-resident global scratch).
+// shared memory; larger l on cooperative multi-CTA grids over L2-resident
+// global scratch).
 //
 //  chol_inv  G = R^T R (upper R, f64) and R^{-1}: the small step of CholQR2,
 //            which replaces the reference's Householder thin_qr
@@ -98,6 +99,183 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   for (int i = warp; i < l; i += kWarps)
     for (int c = lane; c < l; c += 32) Rinv[(int64_t)i * ldr + c] = (c >= i) ? W[(int64_t)i * l + c] : 0.0;
+}
+
+// ---------------------------------------------------------------------------
+// chol_coop: the same factorisation for sketch widths whose l x l matrix does
+// not fit one CTA's shared memory (l > ~160; config 5: l = 550). A single CTA
+// streaming the matrix through L2 one column at a time took ~18 ms at l = 550;
+// this is a blocked (32-wide) right-looking Cholesky over a cooperative grid:
+//   A  CTA 0 factors the diagonal block W_JJ = R_JJ^T R_JJ (pivot test as
+//      above) and inverts it, D_J = R_JJ^{-1}
+//   B  all CTAs: panel R_J,>J = D_J^T W_J,>J (one thread per column)
+//   C  all CTAs: trailing update W_>J,>J -= R_J,>J^T R_J,>J (32 x 32 tiles)
+// then R^{-1} by block diagonals: X_JJ = D_J, X_IJ = -D_I sum_{I<K<=J} R_IK X_KJ
+// (all (I, I+d) blocks of one diagonal d in parallel). Indices >= l are padded
+// with the identity. Scratch: W, X (lp x lp) and D (nb x 32 x 32), lp = 32 nb.
+constexpr int kCB = 32;
+constexpr int kCT = 256;
+
+__global__ void __launch_bounds__(kCT)
+    chol_coop_kernel(const double* __restrict__ G, int64_t ldg, int l, double tau,
+                     double* __restrict__ R, double* __restrict__ Rinv, int64_t ldr,
+                     int* __restrict__ flag, double* __restrict__ ws) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  const int nb = (l + kCB - 1) / kCB, lp = nb * kCB;
+  double* W = ws;
+  double* X = W + (int64_t)lp * lp;
+  double* D = X + (int64_t)lp * lp;
+  __shared__ double sa[kCB][kCB + 1], sb[kCB][kCB + 1], sc[kCB][kCB + 1];
+  const int tid = threadIdx.x;
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + tid;
+  const int64_t gthreads = (int64_t)gridDim.x * blockDim.x;
+  const int64_t ll = (int64_t)lp * lp;
+  const int tr = tid >> 3, tc = (tid & 7) * 4;  // tile coordinates: row, 4 columns
+
+  for (int64_t idx = gt; idx < ll; idx += gthreads) {
+    const int i = (int)(idx / lp), c = (int)(idx - (int64_t)i * lp);
+    W[idx] = (i < l && c < l) ? (c >= i ? G[(int64_t)i * ldg + c] : 0.0) : (i == c ? 1.0 : 0.0);
+  }
+  grid.sync();
+
+  for (int jb = 0; jb < nb; ++jb) {
+    const int j0 = jb * kCB;
+    // A: diagonal block (warp 0 of CTA 0; lane = column)
+    if (blockIdx.x == 0 && tid < 32) {
+      const int lane = tid;
+      for (int r = 0; r < kCB; ++r) sa[r][lane] = W[(int64_t)(j0 + r) * lp + j0 + lane];
+      __syncwarp();
+      bool fail = false;
+      for (int j = 0; j < kCB; ++j) {
+        const double piv = sa[j][j];
+        const int gi = j0 + j;
+        const double d0 = gi < l ? G[(int64_t)gi * ldg + gi] : 1.0;
+        const bool ok = (piv > tau * d0) && (piv > 0.0);
+        const double pe = ok ? piv : fmax(fabs(d0), DBL_MIN);  // keep going; result discarded
+        fail |= !ok;
+        const double rjj = sqrt(pe);
+        const double v = lane > j ? sa[j][lane] / rjj : (lane == j ? rjj : 0.0);
+        __syncwarp();
+        sa[j][lane] = v;
+        __syncwarp();
+        for (int i = j + 1; i < kCB; ++i)
+          if (lane >= i) sa[i][lane] -= sa[j][i] * sa[j][lane];
+        __syncwarp();
+      }
+      if (fail && lane == 0) *flag = 1;
+      // column `lane` of R_JJ^{-1} (lane-private: no synchronisation inside)
+      sb[lane][lane] = 1.0 / sa[lane][lane];
+      for (int i = lane - 1; i >= 0; --i) {
+        double acc = 0.0;
+        for (int p = i + 1; p <= lane; ++p) acc += sa[i][p] * sb[p][lane];
+        sb[i][lane] = -acc / sa[i][i];
+      }
+      for (int i = lane + 1; i < kCB; ++i) sb[i][lane] = 0.0;
+      __syncwarp();
+      for (int r = 0; r < kCB; ++r) {
+        W[(int64_t)(j0 + r) * lp + j0 + lane] = lane >= r ? sa[r][lane] : 0.0;
+        D[(int64_t)jb * kCB * kCB + r * kCB + lane] = sb[r][lane];
+      }
+    }
+    grid.sync();
+    // B: panel rows j0.., columns beyond the block: x = D_J^T w
+    const int ncols = lp - j0 - kCB;
+    const double* Dj = D + (int64_t)jb * kCB * kCB;
+    for (int64_t cc = gt; cc < ncols; cc += gthreads) {
+      const int c = j0 + kCB + (int)cc;
+      double w[kCB];
+#pragma unroll
+      for (int s2 = 0; s2 < kCB; ++s2) w[s2] = W[(int64_t)(j0 + s2) * lp + c];
+#pragma unroll
+      for (int r = 0; r < kCB; ++r) {
+        double acc = 0.0;
+#pragma unroll
+        for (int s2 = 0; s2 <= r; ++s2) acc += __ldg(&Dj[s2 * kCB + r]) * w[s2];
+        W[(int64_t)(j0 + r) * lp + c] = acc;
+      }
+    }
+    grid.sync();
+    // C: trailing tiles (a <= b) of the blocks after jb
+    const int n = nb - jb - 1;
+    const int tiles = n * (n + 1) / 2;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      int a = 0, rem = t;
+      while (rem >= n - a) {
+        rem -= n - a;
+        ++a;
+      }
+      const int b = a + rem;
+      const int ci = (jb + 1 + a) * kCB, cb = (jb + 1 + b) * kCB;
+      for (int e = tid; e < kCB * kCB; e += kCT) {
+        const int r = e >> 5, x = e & 31;
+        sa[r][x] = W[(int64_t)(j0 + r) * lp + ci + x];
+        sb[r][x] = W[(int64_t)(j0 + r) * lp + cb + x];
+      }
+      __syncthreads();
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 8
+      for (int s2 = 0; s2 < kCB; ++s2) {
+        const double ar = sa[s2][tr];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[q] += ar * sb[s2][tc + q];
+      }
+      double* dst = W + (int64_t)(ci + tr) * lp + cb + tc;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) dst[q] -= acc[q];
+      __syncthreads();
+    }
+    grid.sync();
+  }
+
+  // R^{-1} by block diagonals
+  for (int64_t idx = gt; idx < ll; idx += gthreads) {
+    const int i = (int)(idx / lp), c = (int)(idx - (int64_t)i * lp);
+    const int bi = i / kCB, bc = c / kCB;
+    X[idx] = bi == bc ? D[(int64_t)bi * kCB * kCB + (i % kCB) * kCB + (c % kCB)] : 0.0;
+  }
+  grid.sync();
+  for (int d = 1; d < nb; ++d) {
+    for (int t = blockIdx.x; t < nb - d; t += gridDim.x) {
+      const int I = t, J = t + d;
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int K = I + 1; K <= J; ++K) {
+        for (int e = tid; e < kCB * kCB; e += kCT) {
+          const int r = e >> 5, x = e & 31;
+          sa[r][x] = W[(int64_t)(I * kCB + r) * lp + K * kCB + x];
+          sb[r][x] = X[(int64_t)(K * kCB + r) * lp + J * kCB + x];
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int p = 0; p < kCB; ++p) {
+          const double ar = sa[tr][p];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[q] += ar * sb[p][tc + q];
+        }
+        __syncthreads();
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) sc[tr][tc + q] = acc[q];
+      for (int e = tid; e < kCB * kCB; e += kCT) sa[e >> 5][e & 31] = D[(int64_t)I * kCB * kCB + e];
+      __syncthreads();
+      double out[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int p = tr; p < kCB; ++p) {
+        const double ar = sa[tr][p];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) out[q] -= ar * sc[p][tc + q];
+      }
+      double* dst = X + (int64_t)(I * kCB + tr) * lp + J * kCB + tc;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) dst[q] = out[q];
+      __syncthreads();
+    }
+    grid.sync();
+  }
+  for (int64_t idx = gt; idx < (int64_t)l * l; idx += gthreads) {
+    const int i = (int)(idx / l), c = (int)(idx - (int64_t)i * l);
+    R[(int64_t)i * ldr + c] = c >= i ? W[(int64_t)i * lp + c] : 0.0;
+    Rinv[(int64_t)i * ldr + c] = c >= i ? X[(int64_t)i * lp + c] : 0.0;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -393,9 +571,29 @@ __global__ void __launch_bounds__(256)
 
 void launch_chol_inv(const double* G, int64_t ldg, int l, double tau, double* R, double* Rinv,
                      int64_t ldr, int* flag, cudaStream_t st) {
-  XB_REQUIRE(l <= 1024, XB_EUNSUPPORTED, "chol_inv: l > 1024");
+  XB_REQUIRE(l <= 4096, XB_EUNSUPPORTED, "chol_inv: l > 4096");
   const size_t bytes = (size_t)l * l * sizeof(double);
+  // XB_CHOL=coop forces the cooperative version (tests), =single the 1-CTA one
+  static const int mode = [] {
+    const char* e = getenv("XB_CHOL");
+    return e ? (strcmp(e, "coop") == 0 ? 1 : (strcmp(e, "single") == 0 ? 2 : 0)) : 0;
+  }();
   const int use_smem = bytes + 26 * 1024 <= max_dyn_smem();
+  if (mode == 1 || (mode == 0 && !use_smem) || l > 1024) {
+    const int nb = (l + kCB - 1) / kCB, lp = nb * kCB;
+    double* ws = nullptr;
+    const size_t wbytes = (2 * (size_t)lp * lp + (size_t)nb * kCB * kCB) * sizeof(double);
+    XB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws), wbytes, st));
+    int per_sm = 0;
+    XB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, chol_coop_kernel, kCT, 0));
+    const int blocks = std::max(1, std::min(kNumSMs, kNumSMs * per_sm));
+    void* args[] = {(void*)&G, (void*)&ldg, (void*)&l, (void*)&tau, (void*)&R,
+                    (void*)&Rinv, (void*)&ldr, (void*)&flag, (void*)&ws};
+    XB_CUDA(cudaLaunchCooperativeKernel((void*)chol_coop_kernel, dim3(blocks), dim3(kCT), args, 0, st));
+    check_launch("chol_coop");
+    XB_CUDA(cudaFreeAsync(ws, st));
+    return;
+  }
   double* gw = nullptr;
   if (!use_smem) XB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&gw), bytes, st));
   const size_t dyn = use_smem ? bytes : 0;

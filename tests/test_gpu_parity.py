@@ -119,6 +119,30 @@ def test_thin_qr_large_well_conditioned(lib):
     assert np.max(np.abs(q - qo)) <= 1e-11
 
 
+@pytest.mark.parametrize("l", [200, 552, 1000])
+def test_thin_qr_wide_cooperative_cholesky(lib, l):
+    """l x l Grams beyond one CTA's shared memory: the blocked cooperative
+    Cholesky + block-diagonal triangular inverse (small.cu chol_coop)."""
+    rng = np.random.default_rng(l)
+    a = rng.standard_normal((4 * l, l)) * np.logspace(0, -2, l)
+    q, r, d = lib.thin_qr(a)
+    qo, ro, do = OK.thin_qr_fast(a, np.float64, np.float64)
+    assert d == () and do == ()
+    assert M.ortho_defect(q) <= 1e-13
+    assert np.max(np.abs(q - qo)) <= 1e-10
+    assert np.array_equal(np.triu(r), r)
+    assert np.max(np.abs(q @ r - a)) <= 1e-12 * np.max(np.abs(a))
+
+
+def test_thin_qr_wide_rank_deficient(lib):
+    rng = np.random.default_rng(6)
+    a = rng.standard_normal((2000, 300)) @ rng.standard_normal((300, 400))
+    q, r, d = lib.thin_qr(a)
+    assert M.ortho_defect(q) <= 1e-10
+    assert np.max(np.abs(q @ r - a)) <= 1e-11 * np.max(np.abs(a))
+    assert len(d) >= 50 and all(j >= 300 for j in d)
+
+
 def test_thin_qr_rank_deficient_uses_fallback(lib):
     rng = np.random.default_rng(5)
     b = rng.standard_normal((3000, 18))

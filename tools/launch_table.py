@@ -1,0 +1,35 @@
+"""Per-kernel totals from an ncu --metrics gpu__time_duration.sum --csv launch list.
+
+    python tools/launch_table.py gpurun_out/launches5.csv [--steps 2]
+"""
+
+import collections
+import csv
+import sys
+
+
+def main():
+    path = sys.argv[1]
+    steps = int(sys.argv[sys.argv.index("--steps") + 1]) if "--steps" in sys.argv else 1
+    rows = list(csv.reader(open(path)))
+    hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
+    h = rows[hi]
+    ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    tot, cnt = collections.defaultdict(float), collections.Counter()
+    scale = {"ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0}
+    for r in rows[hi + 1:]:
+        if len(r) <= vi:
+            continue
+        v = float(r[vi].replace(",", "")) * scale.get(r[ui], 1e-6)
+        name = r[ki].split("(")[0][:70]
+        tot[name] += v
+        cnt[name] += 1
+    total = sum(tot.values())
+    print(f"| kernel | launches/step | ms/step | share |\n|---|---|---|---|")
+    for k, v in sorted(tot.items(), key=lambda x: -x[1]):
+        print(f"| `{k}` | {cnt[k] / steps:g} | {v / steps:.2f} | {100 * v / total:.1f}% |")
+    print(f"| total | {sum(cnt.values()) / steps:g} | {total / steps:.1f} | |")
+
+
+if __name__ == "__main__":
+    main()
