@@ -9,15 +9,19 @@
 // into one f32 TMEM accumulator; the dropped A_lo B_lo term is ~2^-22).
 //
 // Warp roles (704 threads, one CTA per 128 x BN output tile):
-//   warp 0      TMA producer: raw A tile + the pre-split B_hi / B_lo tiles
+//   warp 0      TMA producer: raw A tile + the pre-split B_hi / B_lo tiles,
+//               a 3-4 deep shared-memory ring
 //   warp 1      TMEM allocator + single-thread MMA issuer
-//   warps 2-5   converters: raw A tile -> A_hi, A_lo in the canonical K-major
-//               128B-swizzled layout (for the transposed view of A this is
-//               also the transpose)
+//   warps 2-5   converters: raw A tile -> A_hi, A_lo written straight into
+//               TMEM (tcgen05.st; thread = tile row, so for the transposed
+//               view of A this is also the transpose). The MMA takes A from
+//               TMEM and only B from shared memory: with A in shared memory
+//               too, operand reads nearly saturated the shared-memory port and
+//               the converted planes limited the ring to 2 stages.
 //   warps 6-21  drain + epilogue: 4 warps per TMEM lane quadrant, each owning
 //               BN/4 columns of its 32 rows
-// Pipelines: full[s] (TMA complete_tx) -> conv[s] (4 converter warps) ->
-// MMA -> tcgen05.commit -> empty[s] (frees the stage).
+// Barriers: full[s] (TMA) -> conv[s] (converters; A slot kt % 2 filled) ->
+// MMA -> commit empty[s] (stage free) + aempty[kt % 2] (A slot free).
 //
 // Accumulation: the tensor core's f32 accumulator does not round to nearest
 // (measured: the error grows ~linearly with the accumulation chain, e.g. a
@@ -41,7 +45,6 @@ namespace {
 
 constexpr int TBM = 128;  // UMMA_M (cta_group::1)
 constexpr int TBK = 32;   // one 128-byte swizzle atom of tf32
-constexpr int TSTAGES = 2;
 constexpr int kDrainGroups = 4;  // column segments per TMEM lane quadrant
 constexpr int kThreadsT = 192 + 128 * kDrainGroups;
 
@@ -125,17 +128,6 @@ __device__ __forceinline__ uint32_t idesc_tf32() {
          | ((uint32_t)(TBM >> 4) << 24);  // M
 }
 
-__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
-                                         uint32_t acc) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(tmem_d),
-      "l"(a), "l"(b), "r"(idesc), "r"(acc));
-}
-
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
                    su32(bar))
@@ -144,21 +136,47 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
 
 template <int BN>
 struct TCfg {
-  static constexpr int A_BYTES = TBM * TBK * 4;        // 16 KB (one operand plane)
-  static constexpr int B_BYTES = BN * TBK * 4;         // BN rows x 128 B
-  static constexpr int RAW = 0;                        // raw A (TMA destination)
-  static constexpr int AHI = RAW + A_BYTES;
-  static constexpr int ALO = AHI + A_BYTES;
-  static constexpr int BHI = ALO + A_BYTES;
-  static constexpr int BLO = BHI + ((B_BYTES + 1023) / 1024) * 1024;
-  static constexpr int STAGE = BLO + ((B_BYTES + 1023) / 1024) * 1024;
-  static constexpr int BAR_OFF = TSTAGES * STAGE;
+  static constexpr int A_BYTES = TBM * TBK * 4;        // 16 KB raw A tile (TMA destination)
+  static constexpr int B_BYTES = BN * TBK * 4;         // BN rows x 128 B per B plane
+  static constexpr int B_AL = ((B_BYTES + 1023) / 1024) * 1024;
+  static constexpr int RAW = 0;
+  static constexpr int BHI = RAW + A_BYTES;
+  static constexpr int BLO = BHI + B_AL;
+  static constexpr int STAGE = BLO + B_AL;
+  static constexpr int STAGES = (200 * 1024) / STAGE > 4 ? 4 : (200 * 1024) / STAGE;
+  static constexpr int BAR_OFF = STAGES * STAGE;
   static constexpr int SMEM = BAR_OFF + 256 + 1024;    // + barriers, tmem slot, align slack
-  // two accumulator buffers (MMA fills one while the drain warps read the other)
-  static constexpr int TMEM_COLS = BN <= 16 ? 32 : BN <= 32 ? 64 : BN <= 64 ? 128 : BN <= 128 ? 256 : 512;
-  static constexpr int BUF_COLS = TMEM_COLS / 2;
+  // TMEM columns: two accumulator buffers [0, BN), [BN, 2 BN) (the MMA fills
+  // one while the drain warps fold the other), then two A slots of 64
+  // columns (A_hi: 32 tf32 columns, A_lo: 32) written by the converters.
+  static constexpr int ACOL = 2 * BN;
+  static constexpr int USED = ACOL + 2 * 64;
+  static constexpr int TMEM_COLS = USED <= 32 ? 32 : USED <= 64 ? 64 : USED <= 128 ? 128 : USED <= 256 ? 256 : 512;
   static constexpr int SEG = BN / kDrainGroups;        // columns per drain thread
+  static_assert(USED <= 512, "TMEM: accumulators + A slots exceed 512 columns");
 };
+
+__device__ __forceinline__ void mma_tf32_ta(uint32_t tmem_d, uint32_t tmem_a, uint64_t b,
+                                            uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+// 16 consecutive TMEM columns of this thread's lane <- v[0..15]
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16};\n" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]),
+      "r"(v[15])
+      : "memory");
+}
 
 template <int BN, bool TRANS_A>
 __global__ void __launch_bounds__(kThreadsT, 1)
@@ -167,16 +185,18 @@ __global__ void __launch_bounds__(kThreadsT, 1)
                  double* __restrict__ C, int64_t ldc, int64_t split_stride, int64_t k_per_split,
                  int accumulate, int drain_tiles, int mtile0) {
   using Cfg = TCfg<BN>;
+  constexpr int NS = Cfg::STAGES;
   static_assert(Cfg::SEG % 8 == 0, "drain segment must be a multiple of 8 columns");
   extern __shared__ unsigned char smem_raw_t[];
   // 1024-byte alignment by pointer arithmetic on the shared array, so the
   // compiler keeps shared-space (LDS/STS) accesses
   unsigned char* smem = smem_raw_t + ((1024u - (su32(smem_raw_t) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::BAR_OFF);
-  uint64_t* conv = full + TSTAGES;
-  uint64_t* empty = conv + TSTAGES;
-  uint64_t* tmem_full = empty + TSTAGES;   // [2]
-  uint64_t* tmem_empty = tmem_full + 2;    // [2]
+  uint64_t* conv = full + NS;
+  uint64_t* empty = conv + NS;
+  uint64_t* aempty = empty + NS;         // [2] TMEM A slot free (MMA commit)
+  uint64_t* tmem_full = aempty + 2;      // [2]
+  uint64_t* tmem_empty = tmem_full + 2;  // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -192,12 +212,13 @@ __global__ void __launch_bounds__(kThreadsT, 1)
   C += (int64_t)blockIdx.z * split_stride;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < TSTAGES; ++s) {
+    for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&conv[s], 4);
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
+      mbar_init(&aempty[b], 1);
       mbar_init(&tmem_full[b], 1);
       mbar_init(&tmem_empty[b], 4 * kDrainGroups);
     }
@@ -219,8 +240,8 @@ __global__ void __launch_bounds__(kThreadsT, 1)
     if (lane == 0) {
       const uint32_t bytes = Cfg::A_BYTES + 2 * Cfg::B_BYTES;
       for (int kt = 0; kt < ktiles; ++kt) {
-        const int s = kt % TSTAGES;
-        if (kt >= TSTAGES) mbar_wait_park(&empty[s], ((kt / TSTAGES) & 1) ^ 1);
+        const int s = kt % NS;
+        if (kt >= NS) mbar_wait_park(&empty[s], ((kt / NS) & 1) ^ 1);
         unsigned char* st = smem + s * Cfg::STAGE;
         const int32_t k0 = (int32_t)(kbeg + (int64_t)kt * TBK);
         mbar_expect_tx(&full[s], bytes);
@@ -233,91 +254,80 @@ __global__ void __launch_bounds__(kThreadsT, 1)
       }
     }
   } else if (warp == 1) {
-    // ---- MMA issuer: group g of P k-tiles accumulates into buffer g & 1 ----------
+    // ---- MMA issuer: A_hi/A_lo from TMEM, B_hi/B_lo from shared memory;
+    // group g of P k-tiles accumulates into buffer g & 1 ----------------------
     const uint32_t idesc = idesc_tf32<BN>();
     for (int kt = 0; kt < ktiles; ++kt) {
-      const int s = kt % TSTAGES;
+      const int s = kt % NS, a = kt & 1;
       const int g = kt / P, b = g & 1;
       const bool first = (kt % P) == 0;
       const bool last = (kt % P) == P - 1 || kt == ktiles - 1;
       if (first && g >= 2) mbar_wait(&tmem_empty[b], ((g >> 1) - 1) & 1);
-      mbar_wait(&conv[s], (kt / TSTAGES) & 1);
+      mbar_wait(&conv[s], (kt / NS) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       if (lane == 0) {
-        const uint32_t d = tmem + (uint32_t)(b * Cfg::BUF_COLS);
+        const uint32_t d = tmem + (uint32_t)(b * BN);
+        const uint32_t ahi = tmem + (uint32_t)(Cfg::ACOL + a * 64);
         unsigned char* st = smem + s * Cfg::STAGE;
-        const uint64_t ah = sw128_desc(su32(st + Cfg::AHI));
-        const uint64_t al = sw128_desc(su32(st + Cfg::ALO));
         const uint64_t bh = sw128_desc(su32(st + Cfg::BHI));
         const uint64_t bl = sw128_desc(su32(st + Cfg::BLO));
 #pragma unroll
         for (int kk = 0; kk < TBK / 8; ++kk) {
           const uint64_t off = (uint64_t)(kk * 32) >> 4;  // 8 tf32 = 32 B inside the atom
-          mma_tf32(d, ah + off, bh + off, idesc, (!first || kk > 0) ? 1u : 0u);
-          mma_tf32(d, ah + off, bl + off, idesc, 1u);
-          mma_tf32(d, al + off, bh + off, idesc, 1u);
+          const uint32_t ah = ahi + (uint32_t)(kk * 8), al = ah + 32;
+          mma_tf32_ta(d, ah, bh + off, idesc, (!first || kk > 0) ? 1u : 0u);
+          mma_tf32_ta(d, ah, bl + off, idesc, 1u);
+          mma_tf32_ta(d, al, bh + off, idesc, 1u);
         }
         mma_commit(&empty[s]);
+        mma_commit(&aempty[a]);
         if (last) mma_commit(&tmem_full[b]);
       }
       __syncwarp();
     }
   } else if (warp < 6) {
-    // ---- converters: raw A -> A_hi, A_lo (K-major, 128B swizzle) -----------------
-    const int ct = threadIdx.x - 64;  // 0..127
+    // ---- converters: raw A -> A_hi, A_lo in TMEM (lane = tile row) -----------
+    // warp w may touch TMEM lanes 32 (w % 4) .. +31: warps 2-5 cover all four
+    const int m = 32 * (warp & 3) + lane;
+    const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
     for (int kt = 0; kt < ktiles; ++kt) {
-      const int s = kt % TSTAGES;
-      mbar_wait_park(&full[s], (kt / TSTAGES) & 1);
-      unsigned char* st = smem + s * Cfg::STAGE;
-      if constexpr (!TRANS_A) {
-        // raw already is the K-major swizzled layout: elementwise, 16 B per step
-        const float4* raw = reinterpret_cast<const float4*>(st + Cfg::RAW);
-        float4* hi = reinterpret_cast<float4*>(st + Cfg::AHI);
-        float4* lo = reinterpret_cast<float4*>(st + Cfg::ALO);
-#pragma unroll 4
-        for (int i = ct; i < Cfg::A_BYTES / 16; i += 128) {
-          const float4 v = raw[i];
-          float4 h, l;
-          h.x = __uint_as_float(to_tf32(v.x));
-          h.y = __uint_as_float(to_tf32(v.y));
-          h.z = __uint_as_float(to_tf32(v.z));
-          h.w = __uint_as_float(to_tf32(v.w));
-          l.x = v.x - h.x;
-          l.y = v.y - h.y;
-          l.z = v.z - h.z;
-          l.w = v.w - h.w;
-          hi[i] = h;
-          lo[i] = l;
-        }
-      } else {
-        // raw is [BK][BM] (M contiguous); thread ct owns output row m = ct
-        const float* raw = reinterpret_cast<const float*>(st + Cfg::RAW);
-        unsigned char* hi = st + Cfg::AHI;
-        unsigned char* lo = st + Cfg::ALO;
-        const int m = ct;
+      const int s = kt % NS, a = kt & 1;
+      mbar_wait_park(&full[s], (kt / NS) & 1);
+      if (kt >= 2) mbar_wait_park(&aempty[a], ((kt >> 1) - 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      const unsigned char* raw = smem + s * Cfg::STAGE + Cfg::RAW;
+      const uint32_t tbase = tmem + lane_base + (uint32_t)(Cfg::ACOL + a * 64);
 #pragma unroll
-        for (int c = 0; c < TBK / 4; ++c) {
+      for (int half = 0; half < 2; ++half) {
+        uint32_t hi[16], lo[16];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int chunk = half * 4 + c;  // 16-byte chunk = k 4 chunk .. +3
           float4 v;
-          v.x = raw[(4 * c + 0) * TBM + m];
-          v.y = raw[(4 * c + 1) * TBM + m];
-          v.z = raw[(4 * c + 2) * TBM + m];
-          v.w = raw[(4 * c + 3) * TBM + m];
-          float4 h, l;
-          h.x = __uint_as_float(to_tf32(v.x));
-          h.y = __uint_as_float(to_tf32(v.y));
-          h.z = __uint_as_float(to_tf32(v.z));
-          h.w = __uint_as_float(to_tf32(v.w));
-          l.x = v.x - h.x;
-          l.y = v.y - h.y;
-          l.z = v.z - h.z;
-          l.w = v.w - h.w;
-          const int off = m * 128 + ((c ^ (m & 7)) << 4);
-          *reinterpret_cast<float4*>(hi + off) = h;
-          *reinterpret_cast<float4*>(lo + off) = l;
+          if constexpr (!TRANS_A) {
+            // [BM][BK] rows of 128 B, 16-byte chunks XOR-swizzled by row % 8
+            v = *reinterpret_cast<const float4*>(raw + m * 128 + ((chunk ^ (m & 7)) << 4));
+          } else {
+            // [BK][BM], M contiguous
+            const float* rf = reinterpret_cast<const float*>(raw);
+            v.x = rf[(4 * chunk + 0) * TBM + m];
+            v.y = rf[(4 * chunk + 1) * TBM + m];
+            v.z = rf[(4 * chunk + 2) * TBM + m];
+            v.w = rf[(4 * chunk + 3) * TBM + m];
+          }
+          const float x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const uint32_t h = to_tf32(x[e]);
+            hi[4 * c + e] = h;
+            lo[4 * c + e] = __float_as_uint(x[e] - __uint_as_float(h));
+          }
         }
+        tmem_st16(tbase + (uint32_t)(half * 16), hi);
+        tmem_st16(tbase + (uint32_t)(32 + half * 16), lo);
       }
-      // make the generic-proxy smem writes visible to the tensor core
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&conv[s]);
     }
@@ -336,7 +346,7 @@ __global__ void __launch_bounds__(kThreadsT, 1)
       const int b = g & 1;
       mbar_wait_park(&tmem_full[b], (g >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      const uint32_t base = tmem + lane_base + (uint32_t)(b * Cfg::BUF_COLS + seg * Cfg::SEG);
+      const uint32_t base = tmem + lane_base + (uint32_t)(b * BN + seg * Cfg::SEG);
 #pragma unroll
       for (int c0 = 0; c0 < Cfg::SEG; c0 += 8) {
         uint32_t v[8];
@@ -432,11 +442,10 @@ int pick_tbn(int64_t N) {
   if (N <= 64) return 64;
   if (N <= 128) return 128;
   if (N <= 192) return 192;
-  if (N <= 224) return 224;
-  // wide sketches: 3 x 192 covers cfg5's 552 with 4% padding (BN = 256 would
-  // not fit the drain warps' f32 sums in the 80-register budget of 704 threads)
-  const int64_t w192 = ceil_div(N, 192) * 192, w224 = ceil_div(N, 224) * 224;
-  return w192 <= w224 ? 192 : 224;
+  // wide sketches: 3 x 192 covers cfg5's 552 with 4% padding. BN is capped
+  // at 192 by TMEM (2 accumulators + 2 A slots <= 512 columns).
+  const int64_t w128 = ceil_div(N, 128) * 128, w192 = ceil_div(N, 192) * 192;
+  return w192 <= w128 ? 192 : 128;
 }
 
 template <int BN, bool TRANS_A>
@@ -527,8 +536,7 @@ void tgemm(const DGemmArgs& g, int splits, double* work, float* bhi, float* blo,
   switch (bn) {
     case 64: XB_T(64)
     case 128: XB_T(128)
-    case 192: XB_T(192)
-    default: XB_T(224)
+    default: XB_T(192)
   }
 #undef XB_T
   if (splits > 1) launch_split_reduce(work, g.M, g.N, ldo, stride, splits, g.C, g.ldc, g.accumulate, st);
