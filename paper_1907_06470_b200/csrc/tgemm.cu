@@ -75,6 +75,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int32_t c0, int32_t c1, int32_t c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3, %4}], [%5];\n" ::"r"(su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(su32(bar))
+      : "memory");
+}
+
 // Waiters off the MMA's critical path (drain warps, converters, producer):
 // try_wait with a suspend-time hint parks the warp in hardware until the
 // phase completes instead of spinning (measured: 16 spinning drain warps
@@ -183,7 +192,8 @@ __global__ void __launch_bounds__(kThreadsT, 1)
     tgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBh,
                  const __grid_constant__ CUtensorMap tmBl, int64_t M, int64_t N, int64_t K,
                  double* __restrict__ C, int64_t ldc, int64_t split_stride, int64_t k_per_split,
-                 int accumulate, int drain_tiles, int mtile0) {
+                 int accumulate, int drain_tiles, int tiles_n, int tiles_m, int splits,
+                 int group_m) {
   using Cfg = TCfg<BN>;
   constexpr int NS = Cfg::STAGES;
   static_assert(Cfg::SEG % 8 == 0, "drain segment must be a multiple of 8 columns");
@@ -200,16 +210,29 @@ __global__ void __launch_bounds__(kThreadsT, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // n-tiles fastest: the CTAs sharing an A tile run together (one HBM read
-  // of A per product, the other n-tiles hit L2)
-  const int64_t m0 = ((int64_t)blockIdx.y + mtile0) * TBM;
-  const int64_t n0 = (int64_t)blockIdx.x * BN;
-  const int64_t kbeg = (int64_t)blockIdx.z * k_per_split;
+  // Raster (1-D grid): n-tile fastest (the CTAs sharing an A tile run
+  // together: one HBM read of A), then m-tiles within a group of group_m,
+  // then splits, then groups. Co-resident CTAs thus touch only ~group_m x 128
+  // rows of A (a wide row-major A has every row in its own 2 MB page; with
+  // all m-tiles marching along K together the TLB thrashed: 122 vs 224 TF/s
+  // at K = 2^20) while group_m m-tiles still share each B k-tile in L2.
+  int64_t L = blockIdx.x;
+  const int nt = (int)(L % tiles_n);
+  L /= tiles_n;
+  const int64_t per_group = (int64_t)group_m * splits;
+  const int64_t mg = L / per_group;
+  const int64_t w = L - mg * per_group;
+  const int gsz = (int)min((int64_t)group_m, (int64_t)tiles_m - mg * group_m);
+  const int split = (int)(w / gsz);
+  const int64_t mt = mg * group_m + (w - (int64_t)split * gsz);
+  const int64_t m0 = mt * TBM;
+  const int64_t n0 = (int64_t)nt * BN;
+  const int64_t kbeg = (int64_t)split * k_per_split;
   const int64_t kend = min(K, kbeg + k_per_split);
   const int ktiles = (int)((kend - kbeg + TBK - 1) / TBK);
   const int P = drain_tiles;
   const int groups = (ktiles + P - 1) / P;
-  C += (int64_t)blockIdx.z * split_stride;
+  C += (int64_t)split * split_stride;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
@@ -249,8 +272,9 @@ __global__ void __launch_bounds__(kThreadsT, 1)
           tma_load_2d(st + Cfg::RAW, &tmA, &full[s], (int32_t)m0, k0);  // [BK][BM], M inner
         else
           tma_load_2d(st + Cfg::RAW, &tmA, &full[s], k0, (int32_t)m0);  // [BM][BK] swizzled
-        tma_load_2d(st + Cfg::BHI, &tmBh, &full[s], k0, (int32_t)n0);
-        tma_load_2d(st + Cfg::BLO, &tmBl, &full[s], k0, (int32_t)n0);
+        // B planes are k-blocked ([K/32][N][32]): one contiguous BN x 128 B tile
+        tma_load_3d(st + Cfg::BHI, &tmBh, &full[s], 0, (int32_t)n0, k0 / TBK);
+        tma_load_3d(st + Cfg::BLO, &tmBl, &full[s], 0, (int32_t)n0, k0 / TBK);
       }
     }
   } else if (warp == 1) {
@@ -385,8 +409,9 @@ __global__ void __launch_bounds__(kThreadsT, 1)
   }
 }
 
-// X (K x N row-major f64, ldx) -> Xt_hi, Xt_lo (N x Kp f32, K contiguous):
-// hi = tf32(x), lo = f32(x - hi).
+// X (K x N row-major f64, ldx) -> hi, lo (f32, k-blocked [Kp/32][N][32]:
+// each k-tile of B is one contiguous N x 128 B slab), hi = tf32(x),
+// lo = f32(x - hi); rows K..Kp-1 are zero.
 __global__ void split_b_kernel(const double* __restrict__ X, int64_t K, int64_t N, int64_t ldx,
                                float* __restrict__ hi, float* __restrict__ lo, int64_t kp) {
   __shared__ double tile[32][33];
@@ -401,8 +426,9 @@ __global__ void split_b_kernel(const double* __restrict__ X, int64_t K, int64_t 
     if (n < N && k < kp) {
       const double x = tile[threadIdx.x][i];
       const float h = __uint_as_float(to_tf32((float)x));
-      hi[n * kp + k] = h;
-      lo[n * kp + k] = (float)(x - (double)h);
+      const int64_t o = ((int64_t)blockIdx.x * N + n) * 32 + threadIdx.x;
+      hi[o] = h;
+      lo[o] = (float)(x - (double)h);
     }
   }
 }
@@ -438,6 +464,21 @@ CUtensorMap make_map(const void* base, uint64_t inner, uint64_t outer, uint64_t 
   return m;
 }
 
+// k-blocked B plane [KB][N][32] f32: dims {32, N, KB}, boxes {32, bn, 1}, 128B swizzle
+CUtensorMap make_map_kblocked(const void* base, uint64_t n, uint64_t kb, uint32_t bn) {
+  CUtensorMap m;
+  const cuuint64_t dims[3] = {(cuuint64_t)TBK, n, kb};
+  const cuuint64_t strides[2] = {TBK * 4, n * TBK * 4};
+  const cuuint32_t box[3] = {(cuuint32_t)TBK, bn, 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims,
+                           strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  XB_REQUIRE(r == CUDA_SUCCESS, XB_ECUDA, "cuTensorMapEncodeTiled (3-D) failed: " + std::to_string(r));
+  return m;
+}
+
 int pick_tbn(int64_t N) {
   if (N <= 64) return 64;
   if (N <= 128) return 128;
@@ -455,20 +496,24 @@ void launch_t(const CUtensorMap& ta, const CUtensorMap& bh, const CUtensorMap& b
   using Cfg = TCfg<BN>;
   auto kern = tgemm_kernel<BN, TRANS_A>;
   XB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
-  const int64_t mtiles = ceil_div(g.M, TBM);
+  const int64_t mtiles = ceil_div(g.M, TBM), ntiles = ceil_div(g.N, BN);
   const int acc_here = (splits == 1 && g.accumulate) ? 1 : 0;
   // k-tiles per TMEM accumulation group (XB_TG_DRAIN overrides for sweeps)
   static const int drain = [] {
     const char* e = getenv("XB_TG_DRAIN");
     return e ? std::max(1, atoi(e)) : 2;
   }();
-  for (int64_t t0 = 0; t0 < mtiles; t0 += 65535) {  // grid.y limit
-    dim3 grid((unsigned)ceil_div(g.N, BN), (unsigned)std::min<int64_t>(65535, mtiles - t0),
-              (unsigned)splits);
-    kern<<<grid, kThreadsT, Cfg::SMEM, st>>>(ta, bh, bl, g.M, g.N, g.K, out, ldo, stride, kps,
-                                             acc_here, drain, (int)t0);
-    check_launch("tgemm");
-  }
+  // m-tiles per raster group (XB_TG_GROUP overrides for sweeps)
+  static const int group = [] {
+    const char* e = getenv("XB_TG_GROUP");
+    return e ? std::max(1, atoi(e)) : 8;
+  }();
+  const int64_t total = ntiles * mtiles * splits;
+  XB_REQUIRE(total < ((int64_t)1 << 31), XB_EUNSUPPORTED, "tgemm: too many tiles for one launch");
+  kern<<<(unsigned)total, kThreadsT, Cfg::SMEM, st>>>(
+      ta, bh, bl, g.M, g.N, g.K, out, ldo, stride, kps, acc_here, drain, (int)ntiles, (int)mtiles,
+      splits, (int)std::min<int64_t>(group, mtiles));
+  check_launch("tgemm");
 }
 
 }  // namespace
@@ -499,10 +544,10 @@ int tgemm_plan_splits(const DGemmArgs& g) {
   return std::max(1, std::min<int>(s, (int)kt));
 }
 
-size_t tgemm_b_floats(const DGemmArgs& g) { return (size_t)g.N * round_up(g.K, 4); }
+size_t tgemm_b_floats(const DGemmArgs& g) { return (size_t)g.N * round_up(g.K, TBK); }
 
 void tgemm(const DGemmArgs& g, int splits, double* work, float* bhi, float* blo, cudaStream_t st) {
-  const int64_t kp = round_up(g.K, 4);
+  const int64_t kp = round_up(g.K, TBK);
   {
     dim3 grid((unsigned)ceil_div(kp, 32), (unsigned)ceil_div(g.N, 32));
     split_b_kernel<<<grid, dim3(32, 8), 0, st>>>(g.B, g.K, g.N, g.ldb, bhi, blo, kp);
@@ -525,8 +570,8 @@ void tgemm(const DGemmArgs& g, int splits, double* work, float* bhi, float* blo,
   const CUtensorMap ta = g.trans_a
                              ? make_map(g.A, (uint64_t)g.M, (uint64_t)g.K, g.lda, TBM, TBK, false)
                              : make_map(g.A, (uint64_t)g.K, (uint64_t)g.M, g.lda, TBK, TBM, true);
-  const CUtensorMap th = make_map(bhi, (uint64_t)kp, (uint64_t)g.N, kp, TBK, bn, true);
-  const CUtensorMap tl = make_map(blo, (uint64_t)kp, (uint64_t)g.N, kp, TBK, bn, true);
+  const CUtensorMap th = make_map_kblocked(bhi, (uint64_t)g.N, (uint64_t)(kp / TBK), bn);
+  const CUtensorMap tl = make_map_kblocked(blo, (uint64_t)g.N, (uint64_t)(kp / TBK), bn);
 #define XB_T(BN)                                                                  \
   if (g.trans_a)                                                                  \
     launch_t<BN, true>(ta, th, tl, g, splits, kps, out, ldo, stride, st);         \

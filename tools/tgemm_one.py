@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--k", type=int, default=262144)
     ap.add_argument("--trans", action="store_true")
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--pad", type=int, default=0, help="extra elements per row of A (lda)")
     args = ap.parse_args()
     import torch
 
@@ -27,10 +28,11 @@ def main():
 
     ctx = _lib.load(0)
     M, N, K = args.m, args.n, args.k
-    a = torch.randn((K, M) if args.trans else (M, K), device="cuda")
+    rows, cols = (K, M) if args.trans else (M, K)
+    a = torch.randn(rows, cols + args.pad, device="cuda")[:, :cols]
     b = torch.randn(K, N, device="cuda")
     c = torch.empty(M, N, device="cuda")
-    lda = a.shape[1]
+    lda = a.stride(0)
     for _ in range(args.reps):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
