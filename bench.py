@@ -480,15 +480,29 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     stage_tot = np.zeros(8)
+    step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     with ClockSampler(local) as clocks:
         ev0.record(stream)
-        for _ in range(args.steps):
+        step_ev[0].record(stream)
+        for i in range(args.steps):
             stage_tot += case.step()
+            step_ev[i + 1].record(stream)
         ev1.record(stream)
         torch.cuda.synchronize()
     launches = ctx.launches - launches0
+    step_ms = [step_ev[i].elapsed_time(step_ev[i + 1]) for i in range(args.steps)]
     prof = ctx.profile_read()
     ctx.profile(False)
+    clock_note = "sampled during the timed region"
+    if world == 1 and not clocks.summary()["samples"]:
+        # timed region shorter than one nvidia-smi sample: sample over extra
+        # untimed steps of the same workload instead
+        with ClockSampler(local) as clocks:
+            t_end = time.perf_counter() + 0.6
+            while time.perf_counter() < t_end:
+                case.step()
+            torch.cuda.synchronize()
+        clock_note = "timed region < 1 sample; sampled over extra untimed steps"
     ms = ev0.elapsed_time(ev1) / args.steps
     if world > 1:
         t = torch.tensor([ms], device=device)
@@ -551,7 +565,8 @@ def run_ours(args):
                    "l": w.l, "omega": f"gaussian_band(seed={w.cfg}) generated on device each step",
                    "l2": l2, "parallelism": f"rows{world}"},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-        "clocks": clocks.summary(),
+        "clocks": dict(clocks.summary(), note=clock_note),
+        "step_ms": [round(x, 3) for x in step_ms],
         "stage_ms": {nm: 1e3 * t / args.steps for nm, t in zip(STAGE_NAMES, stage_tot)},
     }
     if isinstance(case, StreamedCase):

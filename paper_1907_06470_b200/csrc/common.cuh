@@ -115,8 +115,11 @@ void launch_csr_transpose(const Csr& a, int64_t* tptr, int32_t* trow, double* tv
 // R^{-1} (ld = ldr, zero outside l x l), sets *flag = 1 when a pivot falls
 // below tau * G_jj (not numerically positive definite). Diag of R is added
 // to rdiag (multiplied in when accumulate != 0).
+// ws: chol_work_doubles(l) doubles of device scratch (nullptr: stream-ordered
+// allocation per call)
+size_t chol_work_doubles(int l);
 void launch_chol_inv(const double* G, int64_t ldg, int l, double tau, double* R, double* Rinv,
-                     int64_t ldr, int* flag, cudaStream_t st);
+                     int64_t ldr, int* flag, double* ws, cudaStream_t st);
 // Householder QR fallback (single CTA): if *flag != 0, recompute Q (rows x l,
 // ldq) and R (l x l, ldr) from X (rows x l, ldx) with the reference's
 // reflector convention; work needs rows * l doubles.

@@ -117,6 +117,7 @@ struct xb_ctx {
                  "device allocation of " + std::to_string(sz) + " bytes (" + name + ") failed");
     }
     bufs[name] = {p, bytes, gen};
+    if (getenv("XB_TRACE")) fprintf(stderr, "[xb] alloc %s %zu B\n", name.c_str(), sz);
     return p;
   }
   size_t cached_bytes() const {
@@ -364,7 +365,7 @@ void gemm_on_a(xb_ctx* c, bool ta, int64_t M, int64_t N, int64_t K, const AView&
 
 struct Small {
   int l, lp;
-  double *G, *R1, *R1i, *R2, *R2i, *Rs;
+  double *G, *R1, *R1i, *R2, *R2i, *Rs, *cw;
   int* flag;
   // row-sharded mode: the communicator that sums Grams, and a sticky flag
   // for Cholesky breakdowns (no single-device Householder fallback applies
@@ -385,6 +386,7 @@ Small small_bufs(xb_ctx* c, int l) {
   s.R2i = c->dbuf("R2i", ll);
   s.Rs = c->dbuf("Rscratch", ll);
   s.flag = c->ibuf("flag", 4);
+  s.cw = c->dbuf("chol_ws", chol_work_doubles(l));
   XB_CUDA(cudaMemsetAsync(s.R1, 0, ll * sizeof(double), c->st));
   XB_CUDA(cudaMemsetAsync(s.R1i, 0, ll * sizeof(double), c->st));
   XB_CUDA(cudaMemsetAsync(s.R2, 0, ll * sizeof(double), c->st));
@@ -407,10 +409,10 @@ void cholqr2(xb_ctx* c, const Small& s, const double* X, int64_t rows, double* T
   int* flag = sharded ? s.shard_err : s.flag;
   if (!sharded) XB_CUDA(cudaMemsetAsync(s.flag, 0, sizeof(int), st));
   gram(c, s, X, rows, sharded);                                // G1 = X^T X
-  launch_chol_inv(s.G, lp, l, 1e-12, s.R1, s.R1i, lp, flag, st);
+  launch_chol_inv(s.G, lp, l, 1e-12, s.R1, s.R1i, lp, flag, s.cw, st);
   gemm(c, false, rows, lp, lp, X, lp, s.R1i, lp, T, lp);       // T = X R1^-1
   gram(c, s, T, rows, sharded);                                // G2 = T^T T
-  launch_chol_inv(s.G, lp, l, 1e-4, s.R2, s.R2i, lp, flag, st);
+  launch_chol_inv(s.G, lp, l, 1e-4, s.R2, s.R2i, lp, flag, s.cw, st);
   gemm(c, false, rows, lp, lp, T, lp, s.R2i, lp, Q, lp);       // Q = T R2^-1
   double* R = Rout ? Rout : s.Rs;
   if (Rout) gemm(c, false, lp, lp, lp, s.R2, lp, s.R1, lp, Rout, lp);  // R = R2 R1
@@ -435,7 +437,7 @@ void cholqr1(xb_ctx* c, const Small& s, const double* X, int64_t rows, double* Q
   int* flag = sharded ? s.shard_err : s.flag;
   if (!sharded) XB_CUDA(cudaMemsetAsync(s.flag, 0, sizeof(int), st));
   gram(c, s, X, rows, sharded);                                // G = X^T X
-  launch_chol_inv(s.G, lp, l, 1e-8, s.R1, s.R1i, lp, flag, st);
+  launch_chol_inv(s.G, lp, l, 1e-8, s.R1, s.R1i, lp, flag, s.cw, st);
   gemm(c, false, rows, lp, lp, X, lp, s.R1i, lp, Q, lp);       // Q = X R^-1
   if (sharded) return;
   double* hw = c->dbuf("hh_work", (size_t)2 * rows * l);

@@ -19,6 +19,7 @@
 #include <cfloat>
 #include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include "common.cuh"
 
@@ -427,6 +428,76 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = lane; i < k; i += 32) Wk[(int64_t)r * ldw + i] = gsign[i] * J[(int64_t)gperm[i] * l + r];
 }
 
+// Shared tail of the cooperative Jacobi kernels: singular values = column
+// norms of X, stable descending order, the sign rule of kernels.py:556-561,
+// U_B = X[:, perm] / s (sign-fixed) and the first k columns of J.
+__device__ void jacobi_finish_grid(const double* X, const double* J, int l, int k,
+                                   double* __restrict__ Ub, int64_t ldu, double* __restrict__ s_out,
+                                   double* __restrict__ Wk, int64_t ldw, double* gnorm, int* gperm,
+                                   int* gsign) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  const int64_t ll = (int64_t)l * l;
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t gthreads = (int64_t)gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31;
+  const int gwarp = (int)(gtid >> 5);
+  const int nwarps = (int)(gthreads >> 5);
+  grid.sync();
+  for (int c = gwarp; c < l; c += nwarps) {
+    double a = 0.0;
+    for (int r = lane; r < l; r += 32) a += X[(int64_t)c * l + r] * X[(int64_t)c * l + r];
+    a = warp_sum32(a);
+    if (lane == 0) gnorm[c] = sqrt(a);
+  }
+  grid.sync();
+  for (int64_t j = gtid; j < l; j += gthreads) {
+    const double sj = gnorm[j];
+    int rank = 0;
+    for (int i = 0; i < l; ++i) {
+      const double si = gnorm[i];
+      rank += (si > sj) || (si == sj && i < (int)j);
+    }
+    gperm[rank] = (int)j;
+  }
+  grid.sync();
+  for (int i = gwarp; i < l; i += nwarps) {
+    const int c = gperm[i];
+    double best = -1.0;
+    int brow = 0;
+    for (int r = lane; r < l; r += 32) {
+      const double v = fabs(X[(int64_t)c * l + r]);
+      if (v > best) {
+        best = v;
+        brow = r;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int orow = __shfl_xor_sync(0xffffffffu, brow, o);
+      if (ob > best || (ob == best && orow < brow)) {
+        best = ob;
+        brow = orow;
+      }
+    }
+    if (lane == 0) gsign[i] = (X[(int64_t)c * l + brow] < 0.0) ? -1 : 1;
+  }
+  grid.sync();
+  for (int64_t i = gtid; i < l; i += gthreads) s_out[i] = gnorm[gperm[i]];
+  for (int64_t idx = gtid; idx < ll; idx += gthreads) {
+    const int r = (int)(idx / l), i = (int)(idx - (int64_t)r * l);
+    const int c = gperm[i];
+    const double sc = gnorm[c];
+    const double inv = sc > 0.0 ? 1.0 / sc : 0.0;
+    Ub[(int64_t)r * ldu + i] = gsign[i] * X[(int64_t)c * l + r] * inv;
+  }
+  for (int64_t idx = gtid; idx < (int64_t)l * k; idx += gthreads) {
+    const int r = (int)(idx / k), i = (int)(idx - (int64_t)r * k);
+    Wk[(int64_t)r * ldw + i] = gsign[i] * J[(int64_t)gperm[i] * l + r];
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Cooperative multi-CTA Jacobi for large l (l x l does not fit one SM's
 // shared memory: cfg4 l=220, cfg5 l=550). X and J live in global memory
@@ -513,64 +584,188 @@ __global__ void __launch_bounds__(256)
     if (*(volatile int*)&rotflag[sweep] == 0) break;
   }
   if (gtid == 0) *status = (sweep >= max_sweeps) ? 1 : 0;
-  for (int c = gwarp; c < l; c += nwarps) {
-    double a = 0.0;
-    for (int r = lane; r < l; r += 32) a += X[(int64_t)c * l + r] * X[(int64_t)c * l + r];
-    a = warp_sum32(a);
-    if (lane == 0) gnorm[c] = sqrt(a);
-  }
-  grid.sync();
-  for (int64_t j = gtid; j < l; j += gthreads) {
-    const double sj = gnorm[j];
-    int rank = 0;
-    for (int i = 0; i < l; ++i) {
-      const double si = gnorm[i];
-      rank += (si > sj) || (si == sj && i < (int)j);
-    }
-    gperm[rank] = (int)j;
-  }
-  grid.sync();
-  for (int i = gwarp; i < l; i += nwarps) {
-    const int c = gperm[i];
-    double best = -1.0;
-    int brow = 0;
-    for (int r = lane; r < l; r += 32) {
-      const double v = fabs(X[(int64_t)c * l + r]);
-      if (v > best) {
-        best = v;
-        brow = r;
-      }
-    }
+  jacobi_finish_grid(X, J, l, k, Ub, ldu, s_out, Wk, ldw, gnorm, gperm, gsign);
+}
+
+// ---------------------------------------------------------------------------
+// Blocked one-sided Jacobi on a cooperative grid (replaces the column-pair
+// cooperative kernel for every l that does not fit one CTA: cfg4 l=220,
+// cfg5 l=550). Columns form nb blocks of `bs`; each outer round pairs blocks
+// round-robin and one CTA takes a block pair: it loads the <= 2 bs columns of
+// X and of J into shared memory, runs one inner cyclic sweep over all pairs
+// of those columns (all 256 threads busy: 256 / bs lanes per pair) rotating
+// both in place, and writes them back. Rounds per sweep drop from l - 1 (each a grid barrier with
+// L2-latency-bound column traffic) to nb - 1. Convergence: a sweep in which
+// no pair needed a rotation (|g| <= tol sqrt(a b)), as in the scalar kernels.
+constexpr int kJT = 256;
+
+template <int LANES>
+__device__ __forceinline__ void lanes_sum3(double& a, double& b, double& c) {
+  if constexpr (LANES == 16) {
+    group_sum3(a, b, c);
+  } else {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-      const int orow = __shfl_xor_sync(0xffffffffu, brow, o);
-      if (ob > best || (ob == best && orow < brow)) {
-        best = ob;
-        brow = orow;
-      }
+      a += __shfl_xor_sync(0xffffffffu, a, o);
+      b += __shfl_xor_sync(0xffffffffu, b, o);
+      c += __shfl_xor_sync(0xffffffffu, c, o);
     }
-    if (lane == 0) gsign[i] = (X[(int64_t)c * l + brow] < 0.0) ? -1 : 1;
   }
-  grid.sync();
-  for (int64_t i = gtid; i < l; i += gthreads) s_out[i] = gnorm[gperm[i]];
+}
+
+template <int LANES>
+__global__ void __launch_bounds__(kJT, 1)
+    jacobi_block_kernel(const double* __restrict__ Rm, int64_t ldr, int l, int k,
+                        double* __restrict__ Ub, int64_t ldu, double* __restrict__ s_out,
+                        double* __restrict__ Wk, int64_t ldw, double* __restrict__ work,
+                        int* __restrict__ status, double tol, int max_sweeps, int bs) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) double smj[];
+  const int64_t ll = (int64_t)l * l;
+  double* X = work;
+  double* J = work + ll;
+  double* gnorm = work + 2 * ll;
+  int* gperm = reinterpret_cast<int*>(gnorm + l);
+  int* gsign = gperm + l;
+  int* rotflag = gsign + l;
+  const int W2 = 2 * bs;               // max columns per CTA
+  double* xs = smj;                    // [W2][l] column-major: X[:, S]
+  double* js = xs + (int64_t)W2 * l;   // [W2][l]: J[:, S]
+  __shared__ int scol[64];
+  __shared__ int s_rot;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + tid;
+  const int64_t gthreads = (int64_t)gridDim.x * blockDim.x;
   for (int64_t idx = gtid; idx < ll; idx += gthreads) {
-    const int r = (int)(idx / l), i = (int)(idx - (int64_t)r * l);
-    const int c = gperm[i];
-    const double sc = gnorm[c];
-    const double inv = sc > 0.0 ? 1.0 / sc : 0.0;
-    Ub[(int64_t)r * ldu + i] = gsign[i] * X[(int64_t)c * l + r] * inv;
+    const int c = (int)(idx / l), r = (int)(idx - (int64_t)c * l);
+    X[idx] = Rm[(int64_t)c * ldr + r];
+    J[idx] = (r == c) ? 1.0 : 0.0;
   }
-  for (int64_t idx = gtid; idx < (int64_t)l * k; idx += gthreads) {
-    const int r = (int)(idx / k), i = (int)(idx - (int64_t)r * k);
-    Wk[(int64_t)r * ldw + i] = gsign[i] * J[(int64_t)gperm[i] * l + r];
+  for (int64_t i = gtid; i < max_sweeps; i += gthreads) rotflag[i] = 0;
+  grid.sync();
+  const int nb = (l + bs - 1) / bs;
+  const int NB2 = nb + (nb & 1);
+  const int grp = tid / LANES, gl = tid % LANES;  // kJT / LANES pairs in flight
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    for (int round = 0; round < NB2 - 1; ++round) {
+      for (int pi = blockIdx.x; pi < NB2 / 2; pi += gridDim.x) {
+        const int pa = pi, pb = NB2 - 1 - pi;
+        const int bi = pa == 0 ? 0 : 1 + (pa - 1 + round) % (NB2 - 1);
+        const int bj = 1 + (pb - 1 + round) % (NB2 - 1);
+        // column set S = block bi (+ block bj unless it is the dummy)
+        if (tid == 0) {
+          int w = 0;
+          for (int blk = 0; blk < 2; ++blk) {
+            const int bb = blk == 0 ? min(bi, bj) : max(bi, bj);
+            if (bb >= nb) continue;
+            for (int c = bb * bs; c < min(l, (bb + 1) * bs); ++c) scol[w++] = c;
+          }
+          s_rot = 0;
+          scol[63] = w;
+        }
+        __syncthreads();
+        const int w = scol[63];
+        for (int c = warp; c < w; c += kJT / 32) {
+          const double* xg = X + (int64_t)scol[c] * l;
+          const double* jg = J + (int64_t)scol[c] * l;
+          double* xd = xs + (int64_t)c * l;
+          double* jd = js + (int64_t)c * l;
+          for (int r = lane; r < l; r += 32) {
+            xd[r] = __ldcg(xg + r);
+            jd[r] = __ldcg(jg + r);
+          }
+        }
+        __syncthreads();
+        // one inner cyclic sweep over the w columns (circle ordering); the
+        // rotations act on X[:, S] and J[:, S] in shared memory
+        const int w2 = w + (w & 1);
+        for (int ir = 0; ir < w2 - 1; ++ir) {
+          for (int q0 = grp; q0 < w2 / 2; q0 += kJT / LANES) {
+            const int qa = q0, qb = w2 - 1 - q0;
+            int p = qa == 0 ? 0 : 1 + (qa - 1 + ir) % (w2 - 1);
+            int q = 1 + (qb - 1 + ir) % (w2 - 1);
+            if (p > q) {
+              const int t = p;
+              p = q;
+              q = t;
+            }
+            if (q >= w) continue;
+            double* xp = xs + (int64_t)p * l;
+            double* xq = xs + (int64_t)q * l;
+            // two independent accumulator sets: the loop is LDS-latency bound
+            double a0 = 0.0, b0 = 0.0, g0 = 0.0, a1 = 0.0, b1 = 0.0, g1 = 0.0;
+            int r = gl;
+            for (; r + LANES < l; r += 2 * LANES) {
+              const double u = xp[r], v = xq[r], u2 = xp[r + LANES], v2 = xq[r + LANES];
+              a0 = fma(u, u, a0);
+              b0 = fma(v, v, b0);
+              g0 = fma(u, v, g0);
+              a1 = fma(u2, u2, a1);
+              b1 = fma(v2, v2, b1);
+              g1 = fma(u2, v2, g1);
+            }
+            if (r < l) {
+              const double u = xp[r], v = xq[r];
+              a0 = fma(u, u, a0);
+              b0 = fma(v, v, b0);
+              g0 = fma(u, v, g0);
+            }
+            double a = a0 + a1, b = b0 + b1, g = g0 + g1;
+            lanes_sum3<LANES>(a, b, g);
+            if (g != 0.0 && fabs(g) > tol * sqrt(a * b)) {
+              const double zeta = (b - a) / (2.0 * g);
+              const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+              const double cs = 1.0 / sqrt(1.0 + t * t);
+              const double sn = cs * t;
+              double* jp = js + (int64_t)p * l;
+              double* jq = js + (int64_t)q * l;
+              for (int rr = gl; rr < l; rr += LANES) {
+                const double u = xp[rr], v = xq[rr];
+                const double uj = jp[rr], vj = jq[rr];
+                xp[rr] = cs * u - sn * v;
+                xq[rr] = sn * u + cs * v;
+                jp[rr] = cs * uj - sn * vj;
+                jq[rr] = sn * uj + cs * vj;
+              }
+              if (gl == 0) s_rot = 1;
+            }
+          }
+          __syncthreads();
+        }
+        if (s_rot) {
+          for (int c = warp; c < w; c += kJT / 32) {
+            double* xg = X + (int64_t)scol[c] * l;
+            double* jg = J + (int64_t)scol[c] * l;
+            const double* xd = xs + (int64_t)c * l;
+            const double* jd = js + (int64_t)c * l;
+            for (int r = lane; r < l; r += 32) {
+              __stcg(xg + r, xd[r]);
+              __stcg(jg + r, jd[r]);
+            }
+          }
+          if (tid == 0) rotflag[sweep] = 1;
+        }
+        __syncthreads();
+      }
+      grid.sync();
+    }
+    if (*(volatile int*)&rotflag[sweep] == 0) break;
   }
+  if (gtid == 0) *status = (sweep >= max_sweeps) ? 1 : 0;
+  jacobi_finish_grid(X, J, l, k, Ub, ldu, s_out, Wk, ldw, gnorm, gperm, gsign);
 }
 
 }  // namespace
 
+size_t chol_work_doubles(int l) {
+  const size_t nb = (size_t)(l + kCB - 1) / kCB, lp = nb * kCB;
+  return std::max(2 * lp * lp + nb * kCB * kCB, (size_t)l * l);
+}
+
 void launch_chol_inv(const double* G, int64_t ldg, int l, double tau, double* R, double* Rinv,
-                     int64_t ldr, int* flag, cudaStream_t st) {
+                     int64_t ldr, int* flag, double* ws_in, cudaStream_t st) {
   XB_REQUIRE(l <= 4096, XB_EUNSUPPORTED, "chol_inv: l > 4096");
   const size_t bytes = (size_t)l * l * sizeof(double);
   // XB_CHOL=coop forces the cooperative version (tests), =single the 1-CTA one
@@ -580,10 +775,9 @@ void launch_chol_inv(const double* G, int64_t ldg, int l, double tau, double* R,
   }();
   const int use_smem = bytes + 26 * 1024 <= max_dyn_smem();
   if (mode == 1 || (mode == 0 && !use_smem) || l > 1024) {
-    const int nb = (l + kCB - 1) / kCB, lp = nb * kCB;
-    double* ws = nullptr;
-    const size_t wbytes = (2 * (size_t)lp * lp + (size_t)nb * kCB * kCB) * sizeof(double);
-    XB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws), wbytes, st));
+    double* ws = ws_in;
+    if (!ws)
+      XB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws), chol_work_doubles(l) * sizeof(double), st));
     int per_sm = 0;
     XB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, chol_coop_kernel, kCT, 0));
     const int blocks = std::max(1, std::min(kNumSMs, kNumSMs * per_sm));
@@ -591,17 +785,18 @@ void launch_chol_inv(const double* G, int64_t ldg, int l, double tau, double* R,
                     (void*)&Rinv, (void*)&ldr, (void*)&flag, (void*)&ws};
     XB_CUDA(cudaLaunchCooperativeKernel((void*)chol_coop_kernel, dim3(blocks), dim3(kCT), args, 0, st));
     check_launch("chol_coop");
-    XB_CUDA(cudaFreeAsync(ws, st));
+    if (!ws_in) XB_CUDA(cudaFreeAsync(ws, st));
     return;
   }
-  double* gw = nullptr;
-  if (!use_smem) XB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&gw), bytes, st));
+  double* gw = use_smem ? nullptr : ws_in;
+  const bool own = !use_smem && !gw;
+  if (own) XB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&gw), bytes, st));
   const size_t dyn = use_smem ? bytes : 0;
   XB_CUDA(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)dyn));
   chol_inv_kernel<<<1, kThreads, dyn, st>>>(G, ldg, l, tau, R, Rinv, ldr, flag, gw, use_smem);
   check_launch("chol_inv");
-  if (gw) XB_CUDA(cudaFreeAsync(gw, st));
+  if (own) XB_CUDA(cudaFreeAsync(gw, st));
 }
 
 constexpr int kMaxSweeps = 60;
@@ -620,17 +815,57 @@ void launch_jacobi_svd(const double* R, int64_t ldr, int l, int k, double* Ub, i
   // XB_JACOBI=coop) the cooperative grid version
   static const int mode = [] {
     const char* e = getenv("XB_JACOBI");
-    return e ? (strcmp(e, "coop") == 0 ? 1 : (strcmp(e, "single") == 0 ? 2 : 0)) : 0;
+    return e ? (strcmp(e, "coop") == 0 ? 1
+                : strcmp(e, "single") == 0 ? 2
+                : strcmp(e, "pairs") == 0 ? 3 : 0)
+             : 0;
   }();
-  const bool coop = mode == 1 || (mode == 0 && one > lim);
+  // blocked cooperative kernel from l > 64 (l = 120: 3.3 ms vs 5.4 ms for
+  // the single-CTA kernel), single CTA below
+  const bool coop = mode == 1 || mode == 3 || (mode == 0 && (one > lim || l > 64));
   if (coop) {
+    int max_sweeps = kMaxSweeps;
+    if (mode != 3) {
+      // blocked: bs columns per block (XB_JACOBI_BS, default 4: l = 552 ran
+      // 28.9 ms at bs 4, 33 ms at 8, 68 ms at 16; l = 120 3.3 ms), halved until
+      // the 2 bs columns of a block pair fit in shared memory
+      static const int bs0 = [] {
+        const char* e = getenv("XB_JACOBI_BS");
+        return e ? std::max(2, std::min(16, atoi(e))) : 4;
+      }();
+      int bs = bs0;
+      auto need = [&](int b) { return (size_t)2 * (2 * b) * l * sizeof(double); };
+      while (bs > 2 && need(bs) > lim) bs /= 2;
+      XB_REQUIRE(need(bs) <= lim, XB_EUNSUPPORTED, "jacobi: l too large for the blocked kernel");
+      const int dyn = (int)need(bs);
+      // lanes per column pair: all 256 threads busy on the bs pairs of an inner round
+      const bool l32 = kJT / bs >= 32;
+      void* kern = l32 ? (void*)jacobi_block_kernel<32> : (void*)jacobi_block_kernel<16>;
+      XB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+      const int nb = (l + bs - 1) / bs;
+      const int blocks = std::max(1, std::min((nb + 1) / 2, kNumSMs));
+      void* args[] = {(void*)&R,  (void*)&ldr, (void*)&l,      (void*)&k,   (void*)&Ub,
+                      (void*)&ldu, (void*)&s,  (void*)&Wk,     (void*)&ldw, (void*)&work,
+                      (void*)&status, (void*)&tol, (void*)&max_sweeps, (void*)&bs};
+      XB_CUDA(cudaLaunchCooperativeKernel(kern, dim3(blocks), dim3(kJT), args, dyn, st));
+      if (getenv("XB_TRACE")) {
+        XB_CUDA(cudaStreamSynchronize(st));
+        std::vector<int> rf(max_sweeps);
+        XB_CUDA(cudaMemcpy(rf.data(), reinterpret_cast<int*>(work + 2 * (int64_t)l * l + l) + 2 * l,
+                           max_sweeps * sizeof(int), cudaMemcpyDeviceToHost));
+        int sw = 0;
+        while (sw < max_sweeps && rf[sw]) ++sw;
+        fprintf(stderr, "[xb] jacobi_block l=%d bs=%d: %d sweeps with rotations\n", l, bs, sw);
+      }
+      check_launch("jacobi_block");
+      return;
+    }
     int dev = 0, per_sm = 0;
     XB_CUDA(cudaGetDevice(&dev));
     XB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_coop_kernel, 256, 0));
     const int npairs = (l + (l & 1)) / 2;
     int blocks = std::max(1, std::min((npairs + 7) / 8, kNumSMs * std::max(per_sm, 1)));
     blocks = std::min(blocks, kNumSMs);
-    int max_sweeps = kMaxSweeps;
     void* args[] = {(void*)&R, (void*)&ldr, (void*)&l, (void*)&k, (void*)&Ub, (void*)&ldu,
                     (void*)&s, (void*)&Wk, (void*)&ldw, (void*)&work, (void*)&status,
                     (void*)&tol, (void*)&max_sweeps};
