@@ -75,6 +75,11 @@ struct DGemmArgs {
   int64_t ldc;
   bool a_f32 = false;
   bool accumulate = false;  // C += op(A) B (fixed order: the streamed tiles' sums)
+  // triangle structure (f64 DMMA path only):
+  //   1 = only output tiles touching the upper triangle are computed (a Gram
+  //       read through its upper triangle; strictly-lower tiles are left
+  //       undefined), 2 = B is upper triangular (K is clipped per N-tile)
+  int tri = 0;
 };
 // Deterministic slice-order sum of split-K partials into C (+= if accumulate).
 void launch_split_reduce(const double* work, int64_t M, int64_t N, int64_t ldw, int64_t stride,

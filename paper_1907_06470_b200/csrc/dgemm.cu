@@ -133,7 +133,7 @@ template <typename TA, int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STA
 __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, 1)
     dgemm_kernel(int64_t M, int64_t N, int64_t K, const TA* __restrict__ A, int64_t lda,
                  const double* __restrict__ B, int64_t ldb, double* __restrict__ C, int64_t ldc,
-                 int64_t split_stride, int64_t k_per_split, int accumulate) {
+                 int64_t split_stride, int64_t k_per_split, int accumulate, int tri) {
   using Cfg = DCfg<TA, BM, BN, BK, WARPS_M, WARPS_N, STAGES, TRANS_A>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tid = threadIdx.x;
@@ -142,8 +142,12 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, 1)
   const int wm = warp / WARPS_N, wn = warp % WARPS_N;
   const int64_t m0 = (int64_t)blockIdx.x * BM;
   const int64_t n0 = (int64_t)blockIdx.y * BN;
+  // tri 1: tiles strictly below the diagonal are never read (SYRK-like Gram)
+  if (tri == 1 && m0 > n0 + BN - 1) return;
   const int64_t kbeg = (int64_t)blockIdx.z * k_per_split;
-  const int64_t kend = min(K, kbeg + k_per_split);
+  int64_t kend = min(K, kbeg + k_per_split);
+  // tri 2: B upper triangular, rows k >= n0 + BN of this N-tile are zero
+  if (tri == 2) kend = min(kend, n0 + BN);
   C += (int64_t)blockIdx.z * split_stride;
 
   double acc[Cfg::FM][Cfg::FN][2];
@@ -152,7 +156,7 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, 1)
 #pragma unroll
     for (int j = 0; j < Cfg::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  const int ktiles = (int)ceil_div(kend - kbeg, BK);
+  const int ktiles = kend > kbeg ? (int)ceil_div(kend - kbeg, BK) : 0;
 
   auto stage_a = [&](int stage) {
     return reinterpret_cast<TA*>(smem_raw + (size_t)stage * Cfg::STAGE_BYTES);
@@ -299,7 +303,7 @@ void run_cfg(const DGemmArgs& g, int splits, int64_t k_per_split, double* out, i
     // with split-K the slices go to the workspace and the reduce accumulates
     const int acc_here = (splits == 1 && g.accumulate) ? 1 : 0;
     kernel<<<grid, Cfg::kThreads, Cfg::SMEM, st>>>(g.M, g.N, g.K, A, g.lda, g.B, g.ldb, out, ldo,
-                                                   split_stride, k_per_split, acc_here);
+                                                   split_stride, k_per_split, acc_here, g.tri);
     check_launch("dgemm");
   };
   if (a16 && b16)

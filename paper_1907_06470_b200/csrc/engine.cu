@@ -304,8 +304,9 @@ struct StageClock {
 // ---- building blocks ---------------------------------------------------------
 
 void gemm(xb_ctx* c, bool ta, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
-          const double* B, int64_t ldb, double* C, int64_t ldc) {
+          const double* B, int64_t ldb, double* C, int64_t ldc, int tri = 0) {
   DGemmArgs g{ta, M, N, K, A, lda, B, ldb, C, ldc};
+  g.tri = tri;
   const int splits = dgemm_plan_splits(g);
   double* work = nullptr;
   const size_t need = dgemm_workspace_doubles(g, splits);
@@ -398,7 +399,8 @@ Small small_bufs(xb_ctx* c, int l) {
 // If Rout != null it receives R = R2 R1 (lp x lp, zero padded).
 // G = X^T X over this rank's rows, summed over ranks when X is row-sharded.
 void gram(xb_ctx* c, const Small& s, const double* X, int64_t rows, bool sharded) {
-  gemm(c, true, s.lp, s.lp, rows, X, s.lp, X, s.lp, s.G, s.lp);
+  // upper-triangle tiles only: the Cholesky kernels read G's upper triangle
+  gemm(c, true, s.lp, s.lp, rows, X, s.lp, X, s.lp, s.G, s.lp, /*tri=*/1);
   if (sharded) nccl_allreduce_sum(s.comm, s.G, (size_t)s.lp * s.lp, c->st);
 }
 
@@ -410,10 +412,10 @@ void cholqr2(xb_ctx* c, const Small& s, const double* X, int64_t rows, double* T
   if (!sharded) XB_CUDA(cudaMemsetAsync(s.flag, 0, sizeof(int), st));
   gram(c, s, X, rows, sharded);                                // G1 = X^T X
   launch_chol_inv(s.G, lp, l, 1e-12, s.R1, s.R1i, lp, flag, s.cw, st);
-  gemm(c, false, rows, lp, lp, X, lp, s.R1i, lp, T, lp);       // T = X R1^-1
+  gemm(c, false, rows, lp, lp, X, lp, s.R1i, lp, T, lp, 2);    // T = X R1^-1 (R1^-1 upper)
   gram(c, s, T, rows, sharded);                                // G2 = T^T T
   launch_chol_inv(s.G, lp, l, 1e-4, s.R2, s.R2i, lp, flag, s.cw, st);
-  gemm(c, false, rows, lp, lp, T, lp, s.R2i, lp, Q, lp);       // Q = T R2^-1
+  gemm(c, false, rows, lp, lp, T, lp, s.R2i, lp, Q, lp, 2);    // Q = T R2^-1
   double* R = Rout ? Rout : s.Rs;
   if (Rout) gemm(c, false, lp, lp, lp, s.R2, lp, s.R1, lp, Rout, lp);  // R = R2 R1
   if (sharded) return;  // breakdown is reported through shard_err
@@ -438,7 +440,7 @@ void cholqr1(xb_ctx* c, const Small& s, const double* X, int64_t rows, double* Q
   if (!sharded) XB_CUDA(cudaMemsetAsync(s.flag, 0, sizeof(int), st));
   gram(c, s, X, rows, sharded);                                // G = X^T X
   launch_chol_inv(s.G, lp, l, 1e-8, s.R1, s.R1i, lp, flag, s.cw, st);
-  gemm(c, false, rows, lp, lp, X, lp, s.R1i, lp, Q, lp);       // Q = X R^-1
+  gemm(c, false, rows, lp, lp, X, lp, s.R1i, lp, Q, lp, 2);    // Q = X R^-1
   if (sharded) return;
   double* hw = c->dbuf("hh_work", (size_t)2 * rows * l);
   launch_householder_fallback(X, lp, rows, l, lp, Q, lp, s.Rs, lp, hw, s.flag, st);
