@@ -132,6 +132,8 @@ void launch_householder_fallback(const double* X, int64_t ldx, int64_t rows, int
                                  int64_t ldq, double* R, int64_t ldr, double* work,
                                  const int* flag, cudaStream_t st);
 // Deficient-column flags from R (l x l, ldr): |R_jj| <= eps * ||R||_F.
+// M (l x l, ld) := identity when *flag != 0
+void launch_identity_if(double* M, int64_t ld, int l, const int* flag, cudaStream_t st);
 void launch_deficient(const double* R, int64_t ldr, int l, double eps, int* count, int* cols,
                       cudaStream_t st);
 

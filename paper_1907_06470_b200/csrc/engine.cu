@@ -668,14 +668,36 @@ void rsvd_impl(xb_ctx* c, const AOp& op, int64_t m, int64_t n, const void* d_ome
   op_tn(c, op, m, n, Qm, Zn, lp, l);  // B^T = A^T Q
 
   clk.enter(kSvdPrep);
-  cholqr2(c, s, Zn, n, Tn, Qn, Rf);  // B^T = Q_B R_B
+  // float32 configs: ONE CholQR pass of B^T and Q_B is never formed,
+  // V = B^T (R_B^-1 W_k). Q_B's orthogonality loss u kappa(B)^2 (~1e-11 at
+  // cfg5's kappa ~ 550) is far below the f32 target (1e-3 angle), and R_B
+  // from the f64 Gram carries sigma to u kappa. float64 keeps CholQR2.
+  const bool fused_lift = a.f32;
+  double* lift = nullptr;
+  if (fused_lift) {
+    XB_CUDA(cudaMemsetAsync(s.flag, 0, sizeof(int), st));
+    gram(c, s, Zn, n, false);
+    launch_chol_inv(s.G, lp, l, 1e-8, Rf, s.R1i, lp, s.flag, s.cw, st);
+    // Cholesky breakdown: Householder Q replaces B^T in place, R^-1 := I
+    double* hw = c->dbuf("hh_work", (size_t)2 * n * l);
+    launch_householder_fallback(Zn, lp, n, l, lp, Zn, lp, Rf, lp, hw, s.flag, st);
+    launch_identity_if(s.R1i, lp, l, s.flag, st);
+  } else {
+    cholqr2(c, s, Zn, n, Tn, Qn, Rf);  // B^T = Q_B R_B
+  }
 
   clk.enter(kSvd);
   launch_jacobi_svd(Rf, lp, l, k, Ub, lp, sv, Wk, kp, jw, jstat, st);
 
   clk.enter(kPost);
   gemm(c, false, m, k, lp, Qm, lp, Ub, lp, out.U, out.ldu);  // U = Q U_B[:, :k]
-  gemm(c, false, n, k, lp, Qn, lp, Wk, kp, out.V, out.ldv);  // V = Q_B W_k
+  if (fused_lift) {
+    lift = c->dbuf("lift", (size_t)lp * kp);
+    gemm(c, false, lp, kp, lp, s.R1i, lp, Wk, kp, lift, kp);   // R_B^-1 W_k
+    gemm(c, false, n, k, lp, Zn, lp, lift, kp, out.V, out.ldv);  // V = B^T R_B^-1 W_k
+  } else {
+    gemm(c, false, n, k, lp, Qn, lp, Wk, kp, out.V, out.ldv);  // V = Q_B W_k
+  }
   XB_CUDA(cudaMemcpyAsync(out.s, sv, k * sizeof(double), cudaMemcpyDeviceToDevice, st));
 
   int hstat = 0, hshard = 0;

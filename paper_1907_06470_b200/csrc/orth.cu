@@ -210,7 +210,23 @@ __global__ void round_f32_kernel(double* __restrict__ p, int64_t rows, int64_t c
   }
 }
 
+// M (l x l, ld) := I when *flag (the Householder fallback replaced R^-1 Q).
+__global__ void identity_if_kernel(double* __restrict__ M, int64_t ld, int l, const int* flag) {
+  if (*flag == 0) return;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)l * l;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx / l, c = idx - i * l;
+    M[i * ld + c] = (i == c) ? 1.0 : 0.0;
+  }
+}
+
 }  // namespace
+
+void launch_identity_if(double* M, int64_t ld, int l, const int* flag, cudaStream_t st) {
+  identity_if_kernel<<<(unsigned)std::min<int64_t>(ceil_div((int64_t)l * l, 256), 1024), 256, 0, st>>>(
+      M, ld, l, flag);
+  check_launch("identity_if");
+}
 
 void launch_householder_fallback(const double* X, int64_t ldx, int64_t rows, int l, int lpad, double* Q,
                                  int64_t ldq, double* R, int64_t ldr, double* work,

@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--trans", action="store_true")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--pad", type=int, default=0, help="extra elements per row of A (lda)")
+    ap.add_argument("--f64", action="store_true", help="float64 A (the DMMA path)")
     args = ap.parse_args()
     import torch
 
@@ -29,14 +30,15 @@ def main():
     ctx = _lib.load(0)
     M, N, K = args.m, args.n, args.k
     rows, cols = (K, M) if args.trans else (M, K)
-    a = torch.randn(rows, cols + args.pad, device="cuda")[:, :cols]
-    b = torch.randn(K, N, device="cuda")
-    c = torch.empty(M, N, device="cuda")
+    dt = torch.float64 if args.f64 else torch.float32
+    a = torch.randn(rows, cols + args.pad, device="cuda", dtype=dt)[:, :cols]
+    b = torch.randn(K, N, device="cuda", dtype=dt)
+    c = torch.empty(M, N, device="cuda", dtype=dt)
     lda = a.stride(0)
     for _ in range(args.reps):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        ctx.gemm_dev(np.float32, args.trans, M, N, K, a.data_ptr(), lda, b.data_ptr(), N,
+        ctx.gemm_dev(np.float64 if args.f64 else np.float32, args.trans, M, N, K, a.data_ptr(), lda, b.data_ptr(), N,
                      c.data_ptr(), N)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
