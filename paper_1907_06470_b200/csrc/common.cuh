@@ -92,6 +92,26 @@ int tgemm_plan_splits(const DGemmArgs& g);
 size_t tgemm_b_floats(const DGemmArgs& g);
 void tgemm(const DGemmArgs& g, int splits, double* work, float* bhi, float* blo, cudaStream_t st);
 
+// FP64 products on the int8 tensor cores (ozgemm.cu, Ozaki slices).
+bool oz_enabled();
+int oz_slices();
+void oz_row_exp(const double* X, int64_t rows, int64_t cols, int64_t ldx, int32_t* e,
+                cudaStream_t st);
+void oz_col_exp(const double* X, int64_t rows, int64_t cols, int64_t ldx, int32_t* e,
+                unsigned long long* scratch, cudaStream_t st);
+void oz_slice_rows(const double* X, int64_t rows, int64_t cols, int64_t ldx, const int32_t* e,
+                   int8_t* P, int64_t rows_p, int64_t kp, int S, cudaStream_t st);
+// kblocked: [rows_p/32][cols_p][32] (a left operand), else [cols_p][rows_p] (a right operand)
+void oz_slice_cols_t(const double* X, int64_t rows, int64_t cols, int64_t ldx, const int32_t* e,
+                     int8_t* P, int64_t cols_p, int64_t rows_p, int S, bool kblocked,
+                     cudaStream_t st);
+size_t oz_workspace_doubles(int64_t M, int64_t N, int64_t K);
+// C (M x N) = L R: L slices k-blocked [S][kp/32][rows_p][32] (row exponents
+// eL), R slices [S][np][kp] (the transposed right operand, column exponents eR).
+void ozgemm(const int8_t* L, int64_t rows_p, int64_t kp, const int32_t* eL, const int8_t* R,
+            int64_t np, const int32_t* eR, int64_t M, int64_t N, int64_t K, double* C, int64_t ldc,
+            bool accumulate, int S, double* work, cudaStream_t st);
+
 // Returns the number of split-K slices that will be used for this shape.
 int dgemm_plan_splits(const DGemmArgs& g);
 size_t dgemm_workspace_doubles(const DGemmArgs& g, int splits);

@@ -475,8 +475,21 @@ struct IngestPlan {
 // The operator A: dense (f64/f32, DMMA tile GEMM) or sparse (CSR of A and of
 // A^T, gather SpMM). The reference dispatches the same way on density
 // (kernels.py:79-112).
+// Ozaki int8 slices of a dense f64 A, made once per factorisation: row
+// slices for Y = A X and column slices of A^T for Z = A^T Q (ozgemm.cu).
+struct OzA {
+  int S = 0;  // 0: not sliced (DMMA path)
+  int8_t* rows = nullptr;   // [S][kpn/32][mp][32]
+  int32_t* erow = nullptr;  // m
+  int64_t kpn = 0, mp = 0;
+  int8_t* colsT = nullptr;  // [S][kpm/32][np][32]
+  int32_t* ecol = nullptr;  // n
+  int64_t kpm = 0, np = 0;
+};
+
 struct AOp {
   bool sparse = false;
+  OzA oz;
   AView dense{nullptr, 0, false};
   Csr csr, csrt;  // A (m x n) and A^T (n x m)
   // row-sharded A: this rank holds m local rows of an
@@ -502,11 +515,75 @@ void spmm_on_a(xb_ctx* c, const Csr& s, const double* X, double* Y, int lp, int 
   }
 }
 
+// Slice A once for the int8 tensor-core products (when the slices fit next
+// to everything else in HBM); otherwise the products stay on DMMA.
+void oz_prepare(xb_ctx* c, AOp& op, int64_t m, int64_t n) {
+  const AView& a = op.dense;
+  if (op.sparse || a.f32 || !oz_enabled()) return;
+  const int S = oz_slices();
+  const int64_t kpn = round_up(n, 32), kpm = round_up(m, 32);
+  const double need = (double)S * ((double)round_up(m, 128) * kpn + (double)round_up(n, 128) * kpm);
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  const double have = (double)free_b + (double)c->cached_bytes();
+  if (need + 2e9 > have) return;
+  OzA z;
+  z.S = S;
+  z.kpn = kpn;
+  z.kpm = kpm;
+  z.mp = round_up(m, 128);
+  z.np = round_up(n, 128);
+  z.rows = static_cast<int8_t*>(c->buf("oz_rows", (size_t)S * z.mp * kpn));
+  z.colsT = static_cast<int8_t*>(c->buf("oz_colsT", (size_t)S * z.np * kpm));
+  z.erow = c->ibuf("oz_erow", m);
+  z.ecol = c->ibuf("oz_ecol", n);
+  auto* scr = static_cast<unsigned long long*>(c->buf("oz_scr", (size_t)std::max(m, n) * 8));
+  const double* A = static_cast<const double*>(a.p);
+  oz_row_exp(A, m, n, a.ld, z.erow, c->st);
+  oz_slice_rows(A, m, n, a.ld, z.erow, z.rows, z.mp, kpn, S, c->st);
+  oz_col_exp(A, m, n, a.ld, z.ecol, scr, c->st);
+  oz_slice_cols_t(A, m, n, a.ld, z.ecol, z.colsT, z.np, kpm, S, true, c->st);
+  op.oz = z;
+}
+
+// One product on the int8 slices: right operand X (K x lp, f64) sliced per
+// column, then the Ozaki GEMM. tn: Z (n x lp) = A^T X, else Y (m x lp) = A X.
+void oz_product(xb_ctx* c, const OzA& z, bool tn, int64_t m, int64_t n, const double* X,
+                double* Y, int lp, int l) {
+  cudaEvent_t b = nullptr, e = nullptr;
+  if (c->profiling) {
+    b = c->prof_event();
+    e = c->prof_event();
+    XB_CUDA(cudaEventRecord(b, c->st));
+  }
+  const int64_t Mo = tn ? n : m, Kk = tn ? m : n, kp = tn ? z.kpm : z.kpn;
+  const int64_t np = round_up(lp, 8);
+  int32_t* ex = c->ibuf("oz_ex", np);
+  auto* scr = static_cast<unsigned long long*>(c->buf("oz_xscr", np * 8));
+  int8_t* xs = static_cast<int8_t*>(c->buf("oz_xs", (size_t)z.S * np * kp));
+  oz_col_exp(X, Kk, lp, lp, ex, scr, c->st);
+  oz_slice_cols_t(X, Kk, lp, lp, ex, xs, np, kp, z.S, false, c->st);
+  const size_t wd = oz_workspace_doubles(Mo, lp, Kk);
+  double* work = wd ? c->dbuf("split", wd) : nullptr;
+  ozgemm(tn ? z.colsT : z.rows, tn ? z.np : z.mp, kp, tn ? z.ecol : z.erow, xs, np, ex, Mo, lp,
+         Kk, Y, lp, false, z.S, work, c->st);
+  if (c->profiling) {
+    XB_CUDA(cudaEventRecord(e, c->st));
+    const double mn = (double)m * (double)n;
+    c->prof_pending.push_back({b, e, 2.0 * mn * l, mn * z.S});
+  }
+}
+
 // Y (m x lp) = A X
 void op_nn(xb_ctx* c, const AOp& op, int64_t m, int64_t n, const double* X, double* Y, int lp,
            int l) {
   if (op.sparse)
     spmm_on_a(c, op.csr, X, Y, lp, l);
+  else if (op.oz.S)
+    oz_product(c, op.oz, false, m, n, X, Y, lp, l);
   else
     gemm_on_a(c, false, m, lp, n, op.dense, 0, X, lp, Y, lp, l);
 }
@@ -516,6 +593,8 @@ void op_tn(xb_ctx* c, const AOp& op, int64_t m, int64_t n, const double* Q, doub
            int l) {
   if (op.sparse)
     spmm_on_a(c, op.csrt, Q, Z, lp, l);
+  else if (op.oz.S)
+    oz_product(c, op.oz, true, m, n, Q, Z, lp, l);
   else
     gemm_on_a(c, true, n, lp, m, op.dense, 0, Q, lp, Z, lp, l);
   // row-sharded: Z = sum_g A_g^T Q_g, the one n x l exchange per product
@@ -526,9 +605,10 @@ void op_tn(xb_ctx* c, const AOp& op, int64_t m, int64_t n, const double* Q, doub
 // by the products over A; everything downstream of a product is f64. With an
 // f32 A, Omega is rounded through float32 first, as the reference stores it
 // at the storage dtype (pipeline.py:281-282).
-void rsvd_impl(xb_ctx* c, const AOp& op, int64_t m, int64_t n, const void* d_omega,
+void rsvd_impl(xb_ctx* c, const AOp& op_in, int64_t m, int64_t n, const void* d_omega,
                int64_t ld_omega, uint64_t seed, int k, int p, int q, const RsvdOut& out,
                int32_t* deficient, int* ndeficient, double* stage_seconds, const IngestPlan& ing) {
+  AOp op = op_in;
   const AView& a = op.dense;
   // m = rows held here (all of A unless row-sharded)
   check_dims(op.comm ? op.m_global : m, n, k, p, q);
@@ -636,7 +716,9 @@ void rsvd_impl(xb_ctx* c, const AOp& op, int64_t m, int64_t n, const void* d_ome
     for (auto e : landed) cudaEventDestroy(e);
     cudaEventDestroy(t0);
     cudaEventDestroy(t1);
+    oz_prepare(c, op, m, n);  // the remaining products on the int8 slices
   } else {
+    oz_prepare(c, op, m, n);
     op_nn(c, op, m, n, Om, Ym, lp, l);
   }
   // intermediate QRs (a basis for the next product) are single-pass, the
@@ -982,6 +1064,33 @@ bool check_dtype(int dtype) {
 void gemm_any(xb_ctx* c, bool f32, bool ta, int64_t m, int64_t n, int64_t kdim, const void* dA,
               int64_t lda, const void* dB, int64_t ldb, void* dC, int64_t ldc) {
   if (!f32) {
+    static const bool oz_dbg = getenv("XB_GEMM_OZ") != nullptr;
+    if (oz_dbg && m > 0 && n > 0 && kdim > 0) {
+      // diagnostics (tools/oz_check.py): the same product on the int8 slices
+      const int S = oz_slices();
+      const double* A = static_cast<const double*>(dA);
+      const double* B = static_cast<const double*>(dB);
+      const int64_t kp = round_up(kdim, 32), np = round_up(n, 8), mp = round_up(m, 128);
+      int8_t* L = static_cast<int8_t*>(c->buf("dbg_L", (size_t)S * mp * kp));
+      int8_t* R = static_cast<int8_t*>(c->buf("dbg_R", (size_t)S * np * kp));
+      int32_t* eL = c->ibuf("dbg_eL", m);
+      int32_t* eR = c->ibuf("dbg_eR", np);
+      auto* scr = static_cast<unsigned long long*>(c->buf("dbg_scr", (size_t)std::max(m, np) * 8));
+      if (ta) {
+        oz_col_exp(A, kdim, m, lda, eL, scr, c->st);
+        oz_slice_cols_t(A, kdim, m, lda, eL, L, mp, kp, S, true, c->st);
+      } else {
+        oz_row_exp(A, m, kdim, lda, eL, c->st);
+        oz_slice_rows(A, m, kdim, lda, eL, L, mp, kp, S, c->st);
+      }
+      oz_col_exp(B, kdim, n, ldb, eR, scr, c->st);
+      oz_slice_cols_t(B, kdim, n, ldb, eR, R, np, kp, S, false, c->st);
+      const size_t wd = oz_workspace_doubles(m, n, kdim);
+      double* work = wd ? c->dbuf("split", wd) : nullptr;
+      ozgemm(L, mp, kp, eL, R, np, eR, m, n, kdim, static_cast<double*>(dC), ldc, false, S, work,
+             c->st);
+      return;
+    }
     gemm(c, ta, m, n, kdim, static_cast<const double*>(dA), lda, static_cast<const double*>(dB),
          ldb, static_cast<double*>(dC), ldc);
     return;

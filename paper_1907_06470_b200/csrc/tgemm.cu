@@ -39,76 +39,16 @@
 #include <mutex>
 
 #include "common.cuh"
+#include "tc_util.cuh"
 
 namespace xb {
 namespace {
+using namespace tc;
 
 constexpr int TBM = 128;  // UMMA_M (cta_group::1)
 constexpr int TBK = 32;   // one 128-byte swizzle atom of tf32
 constexpr int kDrainGroups = 4;  // column segments per TMEM lane quadrant
 constexpr int kThreadsT = 192 + 128 * kDrainGroups;
-
-__device__ __forceinline__ uint32_t su32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(su32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
-                                            int32_t c0, int32_t c1, int32_t c2) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
-      "%3, %4}], [%5];\n" ::"r"(su32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(su32(bar))
-      : "memory");
-}
-
-// Waiters off the MMA's critical path (drain warps, converters, producer):
-// try_wait with a suspend-time hint parks the warp in hardware until the
-// phase completes instead of spinning (measured: 16 spinning drain warps
-// issued ~50x more instructions than the converters and saturated the
-// barrier pipe).
-__device__ __forceinline__ void mbar_wait_park(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAITP_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
-      "@!p bra WAITP_%=;\n"
-      "}\n" ::"r"(su32(bar)),
-      "r"(parity), "r"(1000000u)
-      : "memory");
-}
-
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
-                                            int32_t c0, int32_t c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
-      "%3}], [%4];\n" ::"r"(su32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(su32(bar))
-      : "memory");
-}
 
 // tf32 "hi" part: the f32 bit pattern with the 13 low mantissa bits cleared
 // (exactly the truncation the tensor core applies to a tf32 operand), so
@@ -137,11 +77,6 @@ __device__ __forceinline__ uint32_t idesc_tf32() {
          | ((uint32_t)(TBM >> 4) << 24);  // M
 }
 
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                   su32(bar))
-               : "memory");
-}
 
 template <int BN>
 struct TCfg {
@@ -431,21 +366,6 @@ __global__ void split_b_kernel(const double* __restrict__ X, int64_t K, int64_t 
       lo[o] = (float)(x - (double)h);
     }
   }
-}
-
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
-            cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  });
-  XB_REQUIRE(fn != nullptr, XB_ECUDA, "cuTensorMapEncodeTiled unavailable");
-  return fn;
 }
 
 // 2-D f32 tensor map: dims {inner, outer}, row stride ld (elements).
