@@ -95,10 +95,13 @@ void tgemm(const DGemmArgs& g, int splits, double* work, float* bhi, float* blo,
 // FP64 products on the int8 tensor cores (ozgemm.cu, Ozaki slices).
 bool oz_enabled();
 int oz_slices();
-void oz_row_exp(const double* X, int64_t rows, int64_t cols, int64_t ldx, int32_t* e,
+// Row / column slice exponents. wide (optional): set to 1 when some row
+// (column) has max |x| > 64 x its RMS (the slices would lose accuracy).
+// oz_col_exp scratch: 2 cols words when wide != nullptr, else cols.
+void oz_row_exp(const double* X, int64_t rows, int64_t cols, int64_t ldx, int32_t* e, int* wide,
                 cudaStream_t st);
 void oz_col_exp(const double* X, int64_t rows, int64_t cols, int64_t ldx, int32_t* e,
-                unsigned long long* scratch, cudaStream_t st);
+                unsigned long long* scratch, int* wide, cudaStream_t st);
 void oz_slice_rows(const double* X, int64_t rows, int64_t cols, int64_t ldx, const int32_t* e,
                    int8_t* P, int64_t rows_p, int64_t kp, int S, cudaStream_t st);
 // kblocked: [rows_p/32][cols_p][32] (a left operand), else [cols_p][rows_p] (a right operand)

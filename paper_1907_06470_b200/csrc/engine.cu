@@ -520,6 +520,9 @@ void spmm_on_a(xb_ctx* c, const Csr& s, const double* X, double* Y, int lp, int 
 void oz_prepare(xb_ctx* c, AOp& op, int64_t m, int64_t n) {
   const AView& a = op.dense;
   if (op.sparse || a.f32 || !oz_enabled()) return;
+  // small matrices stay on DMMA: slicing A costs ~1.5 passes over it and the
+  // products are launch-bound (cfg1, 4096 x 2048: 1.2 ms DMMA vs 1.8 ms)
+  if ((double)m * (double)n < (double)(1 << 24) || std::min(m, n) < 1024) return;
   const int S = oz_slices();
   const int64_t kpn = round_up(n, 32), kpm = round_up(m, 32);
   const double need = (double)S * ((double)round_up(m, 128) * kpn + (double)round_up(n, 128) * kpm);
@@ -536,15 +539,22 @@ void oz_prepare(xb_ctx* c, AOp& op, int64_t m, int64_t n) {
   z.kpm = kpm;
   z.mp = round_up(m, 128);
   z.np = round_up(n, 128);
-  z.rows = static_cast<int8_t*>(c->buf("oz_rows", (size_t)S * z.mp * kpn));
-  z.colsT = static_cast<int8_t*>(c->buf("oz_colsT", (size_t)S * z.np * kpm));
   z.erow = c->ibuf("oz_erow", m);
   z.ecol = c->ibuf("oz_ecol", n);
-  auto* scr = static_cast<unsigned long long*>(c->buf("oz_scr", (size_t)std::max(m, n) * 8));
+  int* wide = c->ibuf("oz_wide", 1);
+  auto* scr = static_cast<unsigned long long*>(c->buf("oz_scr", (size_t)2 * std::max(m, n) * 8));
   const double* A = static_cast<const double*>(a.p);
-  oz_row_exp(A, m, n, a.ld, z.erow, c->st);
+  // exponents + dynamic-range guard first (one small read-back per call)
+  XB_CUDA(cudaMemsetAsync(wide, 0, sizeof(int), c->st));
+  oz_row_exp(A, m, n, a.ld, z.erow, wide, c->st);
+  oz_col_exp(A, m, n, a.ld, z.ecol, scr, wide, c->st);
+  int hwide = 0;
+  XB_CUDA(cudaMemcpyAsync(&hwide, wide, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+  XB_CUDA(cudaStreamSynchronize(c->st));
+  if (hwide) return;  // some row/column of A spans > 64x its RMS: DMMA keeps f64 accuracy
+  z.rows = static_cast<int8_t*>(c->buf("oz_rows", (size_t)S * z.mp * kpn));
+  z.colsT = static_cast<int8_t*>(c->buf("oz_colsT", (size_t)S * z.np * kpm));
   oz_slice_rows(A, m, n, a.ld, z.erow, z.rows, z.mp, kpn, S, c->st);
-  oz_col_exp(A, m, n, a.ld, z.ecol, scr, c->st);
   oz_slice_cols_t(A, m, n, a.ld, z.ecol, z.colsT, z.np, kpm, S, true, c->st);
   op.oz = z;
 }
@@ -564,7 +574,7 @@ void oz_product(xb_ctx* c, const OzA& z, bool tn, int64_t m, int64_t n, const do
   int32_t* ex = c->ibuf("oz_ex", np);
   auto* scr = static_cast<unsigned long long*>(c->buf("oz_xscr", np * 8));
   int8_t* xs = static_cast<int8_t*>(c->buf("oz_xs", (size_t)z.S * np * kp));
-  oz_col_exp(X, Kk, lp, lp, ex, scr, c->st);
+  oz_col_exp(X, Kk, lp, lp, ex, scr, nullptr, c->st);
   oz_slice_cols_t(X, Kk, lp, lp, ex, xs, np, kp, z.S, false, c->st);
   const size_t wd = oz_workspace_doubles(Mo, lp, Kk);
   double* work = wd ? c->dbuf("split", wd) : nullptr;
@@ -1077,13 +1087,13 @@ void gemm_any(xb_ctx* c, bool f32, bool ta, int64_t m, int64_t n, int64_t kdim, 
       int32_t* eR = c->ibuf("dbg_eR", np);
       auto* scr = static_cast<unsigned long long*>(c->buf("dbg_scr", (size_t)std::max(m, np) * 8));
       if (ta) {
-        oz_col_exp(A, kdim, m, lda, eL, scr, c->st);
+        oz_col_exp(A, kdim, m, lda, eL, scr, nullptr, c->st);
         oz_slice_cols_t(A, kdim, m, lda, eL, L, mp, kp, S, true, c->st);
       } else {
-        oz_row_exp(A, m, kdim, lda, eL, c->st);
+        oz_row_exp(A, m, kdim, lda, eL, nullptr, c->st);
         oz_slice_rows(A, m, kdim, lda, eL, L, mp, kp, S, c->st);
       }
-      oz_col_exp(B, kdim, n, ldb, eR, scr, c->st);
+      oz_col_exp(B, kdim, n, ldb, eR, scr, nullptr, c->st);
       oz_slice_cols_t(B, kdim, n, ldb, eR, R, np, kp, S, false, c->st);
       const size_t wd = oz_workspace_doubles(m, n, kdim);
       double* work = wd ? c->dbuf("split", wd) : nullptr;

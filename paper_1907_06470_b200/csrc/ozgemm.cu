@@ -12,10 +12,13 @@
 //     (L R)_ij = 2^(e_i+f_j) sum_{d=2}^{S+1} 2^-7d sum_{t+u=d} (a_t b_u)_ij
 // (pairs with t + u > S + 1 are dropped: each is below 2^-7(S+2) of the
 // row/column scale). Every (a_t b_u) is exact in int32 while
-// K_chunk * 127^2 * (pairs per level <= S) < 2^31, i.e. K_chunk <= 16384;
+// K_chunk * 127^2 * (pairs per level <= S) < 2^31, i.e. K_chunk <= 16384
+// (slices are rounded to nearest, so |a_t| <= 64 for t >= 2 and the bound
+// is loose);
 // longer reductions are split over K into f64 slices summed in slice order.
-// Result: an f64-scale product with error ~2^-7S relative to the row/column
-// max-norm scale (S = 6: 2^-42), below the rSVD's 1e-10 / 1e-8 targets.
+// Result: an f64-scale product with error ~2^-(8S-1) relative to the
+// row/column max-norm scale (S = 6: 2^-47), far below the rSVD's 1e-10 /
+// 1e-8 targets.
 //
 // Layout: left operand slices L[t] (k-blocked [kp/32][rows_p][32] int8: each
 // 128-row k-tile is contiguous) with row exponents; right operand slices R[u] (np x kp int8, K contiguous: the
@@ -268,49 +271,83 @@ __global__ void __launch_bounds__(OTHREADS, 1)
 
 // ---- slicing ---------------------------------------------------------------------
 
-// max |x| over each row (one warp per row) -> exponent e with max < 2^e
+// exponent e with 128 m 2^-e < 127.5 (so rint keeps the first slice in int8)
+__device__ __forceinline__ int slice_exp(double m) {
+  if (!(m > 0.0)) return 0;
+  int e = ilogb(m) + 1;  // m 2^-e in [0.5, 1)
+  if (scalbn(m, 7 - e) >= 127.5) ++e;
+  return e;
+}
+
+// max |x| over each row (one warp per row) -> slice exponent. The slices
+// carry a fixed number of bits relative to the row maximum, so a row whose
+// maximum towers over its RMS (max^2 > kOzRange^2 * mean square) loses
+// relative accuracy; such matrices raise *wide and stay on DMMA.
+constexpr double kOzRange = 64.0;
+
 __global__ void row_exp_kernel(const double* __restrict__ X, int64_t rows, int64_t cols,
-                               int64_t ldx, int32_t* __restrict__ e) {
+                               int64_t ldx, int32_t* __restrict__ e, int* __restrict__ wide) {
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= rows) return;
   const double* r = X + w * ldx;
-  double m = 0.0;
-  for (int64_t c = lane; c < cols; c += 32) m = fmax(m, fabs(r[c]));
+  double m = 0.0, ss = 0.0;
+  for (int64_t c = lane; c < cols; c += 32) {
+    const double v = r[c];
+    m = fmax(m, fabs(v));
+    ss = fma(v, v, ss);
+  }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if (lane == 0) e[w] = m > 0.0 ? ilogb(m) + 1 : 0;
+  for (int o = 16; o > 0; o >>= 1) {
+    m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  }
+  if (lane == 0) {
+    e[w] = slice_exp(m);
+    if (wide && m * m > kOzRange * kOzRange * (ss / (double)cols)) atomicOr(wide, 1);
+  }
 }
 
-// max |x| over each column: per-block partial maxima, atomicMax on the bit
-// pattern (order-preserving for non-negative doubles)
+// max |x| and sum of squares over each column: per-block partials, atomicMax
+// on the bit pattern (order-preserving for non-negative doubles); the sums
+// only feed the range guard (order does not matter for a threshold test)
 __global__ void col_max_kernel(const double* __restrict__ X, int64_t rows, int64_t cols,
-                               int64_t ldx, unsigned long long* __restrict__ cmax) {
+                               int64_t ldx, unsigned long long* __restrict__ cmax,
+                               double* __restrict__ css) {
   const int64_t c = (int64_t)blockIdx.x * 32 + threadIdx.x;
   const int64_t r0 = (int64_t)blockIdx.y * 256;
   if (c >= cols) return;
-  double m = 0.0;
-  for (int64_t r = r0 + threadIdx.y; r < min(rows, r0 + 256); r += blockDim.y)
-    m = fmax(m, fabs(X[r * ldx + c]));
+  double m = 0.0, ss = 0.0;
+  for (int64_t r = r0 + threadIdx.y; r < min(rows, r0 + 256); r += blockDim.y) {
+    const double v = X[r * ldx + c];
+    m = fmax(m, fabs(v));
+    ss = fma(v, v, ss);
+  }
   atomicMax(cmax + c, (unsigned long long)__double_as_longlong(m));
+  if (css) atomicAdd(css + c, ss);
 }
 
-__global__ void col_exp_kernel(const unsigned long long* __restrict__ cmax, int64_t cols,
-                               int32_t* __restrict__ e) {
+__global__ void col_exp_kernel(const unsigned long long* __restrict__ cmax,
+                               const double* __restrict__ css, int64_t rows, int64_t cols,
+                               int32_t* __restrict__ e, int* __restrict__ wide) {
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= cols) return;
   const double m = __longlong_as_double((long long)cmax[c]);
-  e[c] = m > 0.0 ? ilogb(m) + 1 : 0;
+  e[c] = slice_exp(m);
+  if (wide && css && m * m > kOzRange * kOzRange * (css[c] / (double)rows)) atomicOr(wide, 1);
 }
 
-// S signed 7-bit slices of x * 2^-e (|x 2^-e| < 1): a_t = trunc(128 r), r <- 128 r - a_t
+// S signed slices of x * 2^-e: a_t = rint(128 r), r <- 128 r - a_t. The
+// exponent keeps |128 x 2^-e| < 127.5 so a_1 fits int8; later residuals are
+// <= 1/2, so a_t (t >= 2) carries 8 bits and |a_t| <= 64 (7 + 8 (S-1) bits
+// in all: 47 at S = 6).
 template <int S>
 __device__ __forceinline__ void slice7(double x, int e, int8_t* out, int64_t plane) {
   double r = scalbn(x, -e);
 #pragma unroll
   for (int t = 0; t < S; ++t) {
     const double y = r * 128.0;
-    const double a = trunc(y);
+    const double a = rint(y);
     out[t * plane] = (int8_t)(int)a;
     r = y - a;
   }
@@ -342,7 +379,7 @@ __global__ void slice_rows_kernel(const double* __restrict__ X, int64_t rows, in
 #pragma unroll
         for (int t = 0; t < S; ++t) {
           const double y = rr * 128.0;
-          const double a = trunc(y);
+          const double a = rint(y);
           w[t] |= (uint64_t)(uint8_t)(int8_t)(int)a << (8 * q);
           rr = y - a;
         }
@@ -443,21 +480,23 @@ bool oz_enabled() {
   return on;
 }
 
-void oz_row_exp(const double* X, int64_t rows, int64_t cols, int64_t ldx, int32_t* e,
+void oz_row_exp(const double* X, int64_t rows, int64_t cols, int64_t ldx, int32_t* e, int* wide,
                 cudaStream_t st) {
   if (rows <= 0) return;
-  row_exp_kernel<<<(unsigned)ceil_div(rows * 32, 256), 256, 0, st>>>(X, rows, cols, ldx, e);
+  row_exp_kernel<<<(unsigned)ceil_div(rows * 32, 256), 256, 0, st>>>(X, rows, cols, ldx, e, wide);
   check_launch("row_exp");
 }
 
 void oz_col_exp(const double* X, int64_t rows, int64_t cols, int64_t ldx, int32_t* e,
-                unsigned long long* scratch, cudaStream_t st) {
+                unsigned long long* scratch, int* wide, cudaStream_t st) {
   if (cols <= 0) return;
-  XB_CUDA(cudaMemsetAsync(scratch, 0, cols * sizeof(unsigned long long), st));
+  // scratch: cols max words, then (when wide != nullptr) cols sums
+  double* css = wide ? reinterpret_cast<double*>(scratch + cols) : nullptr;
+  XB_CUDA(cudaMemsetAsync(scratch, 0, (wide ? 2 : 1) * cols * sizeof(unsigned long long), st));
   dim3 grid((unsigned)ceil_div(cols, 32), (unsigned)std::max<int64_t>(1, ceil_div(rows, 256)));
-  col_max_kernel<<<grid, dim3(32, 8), 0, st>>>(X, rows, cols, ldx, scratch);
+  col_max_kernel<<<grid, dim3(32, 8), 0, st>>>(X, rows, cols, ldx, scratch, css);
   check_launch("col_max");
-  col_exp_kernel<<<(unsigned)ceil_div(cols, 256), 256, 0, st>>>(scratch, cols, e);
+  col_exp_kernel<<<(unsigned)ceil_div(cols, 256), 256, 0, st>>>(scratch, css, rows, cols, e, wide);
   check_launch("col_exp");
 }
 
