@@ -108,6 +108,11 @@ void oz_slice_rows(const double* X, int64_t rows, int64_t cols, int64_t ldx, con
 void oz_slice_cols_t(const double* X, int64_t rows, int64_t cols, int64_t ldx, const int32_t* e,
                      int8_t* P, int64_t cols_p, int64_t rows_p, int S, bool kblocked,
                      cudaStream_t st);
+// Row slices [S][kpn/32][mp][32] and column slices [S][kpm/32][np][32] of X
+// (m x n) in one pass (mp, np multiples of 128; kpn, kpm of 32).
+void oz_slice_both(const double* X, int64_t m, int64_t n, int64_t ldx, const int32_t* er,
+                   const int32_t* ec, int8_t* PR, int64_t mp, int64_t kpn, int8_t* PC, int64_t np,
+                   int64_t kpm, int S, cudaStream_t st);
 size_t oz_workspace_doubles(int64_t M, int64_t N, int64_t K);
 // C (M x N) = L R: L slices k-blocked [S][kp/32][rows_p][32] (row exponents
 // eL), R slices [S][np][kp] (the transposed right operand, column exponents eR).

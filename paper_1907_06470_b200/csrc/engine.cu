@@ -554,8 +554,7 @@ void oz_prepare(xb_ctx* c, AOp& op, int64_t m, int64_t n) {
   if (hwide) return;  // some row/column of A spans > 64x its RMS: DMMA keeps f64 accuracy
   z.rows = static_cast<int8_t*>(c->buf("oz_rows", (size_t)S * z.mp * kpn));
   z.colsT = static_cast<int8_t*>(c->buf("oz_colsT", (size_t)S * z.np * kpm));
-  oz_slice_rows(A, m, n, a.ld, z.erow, z.rows, z.mp, kpn, S, c->st);
-  oz_slice_cols_t(A, m, n, a.ld, z.ecol, z.colsT, z.np, kpm, S, true, c->st);
+  oz_slice_both(A, m, n, a.ld, z.erow, z.ecol, z.rows, z.mp, kpn, z.colsT, z.np, kpm, S, c->st);
   op.oz = z;
 }
 

@@ -1,24 +1,23 @@
 // FP64 products on the int8 tensor cores (tcgen05.mma.kind::i8): an
-// Ozaki-scheme split of both operands into S signed 7-bit slices with
+// Ozaki-scheme split of both operands into S signed 8-bit digit slices with
 // power-of-two row / column scales, exact int32 slice products, and an f64
 // recombination in the epilogue.
 //
 // FP64 has no tcgen05 kind on sm_100a; the legacy DMMA path (mma.sync.f64,
 // dgemm.cu) peaks at ~37 TF/s. The int8 tensor pipe runs ~120x faster, so
 // the S(S+1)/2 slice products (21 for S = 6) still leave a several-fold
-// margin. Numerics: with row scale 2^e_i (max_k |L_ik| < 2^e_i) and column
-// scale 2^f_j,
-//     L_ik = 2^e_i sum_t a_t,ik 2^-7t + r_ik,   |r_ik| < 2^(e_i - 7S)
-//     (L R)_ij = 2^(e_i+f_j) sum_{d=2}^{S+1} 2^-7d sum_{t+u=d} (a_t b_u)_ij
-// (pairs with t + u > S + 1 are dropped: each is below 2^-7(S+2) of the
-// row/column scale). Every (a_t b_u) is exact in int32 while
-// K_chunk * 127^2 * (pairs per level <= S) < 2^31, i.e. K_chunk <= 16384
-// (slices are rounded to nearest, so |a_t| <= 64 for t >= 2 and the bound
-// is loose);
-// longer reductions are split over K into f64 slices summed in slice order.
-// Result: an f64-scale product with error ~2^-(8S-1) relative to the
-// row/column max-norm scale (S = 6: 2^-47), far below the rSVD's 1e-10 /
-// 1e-8 targets.
+// margin. Numerics (t, u, d 0-based): with row scale 2^e_i (|L_ik| 2^-e_i
+// < 126/128) and column scale 2^f_j,
+//     L_ik = 2^e_i sum_t a_t,ik 2^-(7+8t) + r_ik,   |r_ik| <= 2^(e_i-8S)
+// (a_0 in [-127, 127], balanced a_t in [-128, 127] below: 7 + 8 (S-1) = 47
+// bits at S = 6, round to nearest), and
+//     (L R)_ij = 2^(e_i+f_j) sum_{d<S} 2^-(14+8d) sum_{t+u=d} (a_t b_u)_ij
+// (pairs with t + u >= S are dropped: below 2^-8S of the row/column scale).
+// Every (a_t b_u) is exact in int32 while K_chunk * 2^14 * (pairs per level
+// <= S) < 2^31, i.e. K_chunk <= 16384; longer reductions are split over K
+// into f64 slices summed in slice order. The error is relative to the
+// row/column max-norm scale, so the engine keeps matrices whose rows or
+// columns span more than 64x their RMS on DMMA (row_exp / col_exp guard).
 //
 // Layout: left operand slices L[t] (k-blocked [kp/32][rows_p][32] int8: each
 // 128-row k-tile is contiguous) with row exponents; right operand slices R[u] (np x kp int8, K contiguous: the
@@ -243,7 +242,7 @@ __global__ void __launch_bounds__(OTHREADS, 1)
                 "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
               : "r"(tmem + lane_base + (uint32_t)(d * OBN + c0)));
           asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-          const double sc = ldexp(1.0, -7 * (d + 2));
+          const double sc = ldexp(1.0, -14 - 8 * d);  // level d weight
 #pragma unroll
           for (int j = 0; j < 16; ++j) acc[j] = fma((double)(int)v[j], sc, acc[j]);
         }
@@ -271,12 +270,28 @@ __global__ void __launch_bounds__(OTHREADS, 1)
 
 // ---- slicing ---------------------------------------------------------------------
 
-// exponent e with 128 m 2^-e < 127.5 (so rint keeps the first slice in int8)
+// exponent e with 128 m 2^-e < 126 (the top digit stays within int8 after
+// the lower balanced digits borrow from it)
 __device__ __forceinline__ int slice_exp(double m) {
   if (!(m > 0.0)) return 0;
   int e = ilogb(m) + 1;  // m 2^-e in [0.5, 1)
-  if (scalbn(m, 7 - e) >= 127.5) ++e;
+  if (scalbn(m, 7 - e) >= 126.0) ++e;
   return e;
+}
+
+// Digits of x 2^-e rounded to 7 + 8 (S-1) bits: V = rint(x 2^(7 + 8(S-1) - e))
+// = sum_t a_t 2^(8(S-1-t)), a_0 in [-127, 127] (top, weight 2^-7) and
+// balanced a_t in [-128, 127] below (weight 2^-(7 + 8t)).
+template <int S>
+__device__ __forceinline__ void slice_digits(double x, int e, int (&a)[S]) {
+  long long v = llrint(scalbn(x, 7 + 8 * (S - 1) - e));
+#pragma unroll
+  for (int t = S - 1; t >= 1; --t) {
+    const int d = (int)((v + 128) & 255) - 128;
+    a[t] = d;
+    v = (v - d) >> 8;
+  }
+  a[0] = (int)v;
 }
 
 // max |x| over each row (one warp per row) -> slice exponent. The slices
@@ -337,20 +352,12 @@ __global__ void col_exp_kernel(const unsigned long long* __restrict__ cmax,
   if (wide && css && m * m > kOzRange * kOzRange * (css[c] / (double)rows)) atomicOr(wide, 1);
 }
 
-// S signed slices of x * 2^-e: a_t = rint(128 r), r <- 128 r - a_t. The
-// exponent keeps |128 x 2^-e| < 127.5 so a_1 fits int8; later residuals are
-// <= 1/2, so a_t (t >= 2) carries 8 bits and |a_t| <= 64 (7 + 8 (S-1) bits
-// in all: 47 at S = 6).
 template <int S>
 __device__ __forceinline__ void slice7(double x, int e, int8_t* out, int64_t plane) {
-  double r = scalbn(x, -e);
+  int a[S];
+  slice_digits<S>(x, e, a);
 #pragma unroll
-  for (int t = 0; t < S; ++t) {
-    const double y = r * 128.0;
-    const double a = rint(y);
-    out[t * plane] = (int8_t)(int)a;
-    r = y - a;
-  }
+  for (int t = 0; t < S; ++t) out[t * plane] = (int8_t)a[t];
 }
 
 // row slices, k-blocked: X (rows x cols, ldx) -> P[t][kp/32][rows_p][32],
@@ -375,14 +382,10 @@ __global__ void slice_rows_kernel(const double* __restrict__ X, int64_t rows, in
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const int64_t c = c0 + q;
-        double rr = c < cols ? scalbn(X[r * ldx + c], -er) : 0.0;
+        int a[S];
+        slice_digits<S>(c < cols ? X[r * ldx + c] : 0.0, er, a);
 #pragma unroll
-        for (int t = 0; t < S; ++t) {
-          const double y = rr * 128.0;
-          const double a = rint(y);
-          w[t] |= (uint64_t)(uint8_t)(int8_t)(int)a << (8 * q);
-          rr = y - a;
-        }
+        for (int t = 0; t < S; ++t) w[t] |= (uint64_t)(uint8_t)(int8_t)a[t] << (8 * q);
       }
     }
     int8_t* out = P + (kb * rows_p + r) * 32 + j * 8;
@@ -413,6 +416,65 @@ __global__ void slice_cols_t_kernel(const double* __restrict__ X, int64_t rows, 
       const int64_t o = KBLOCK ? ((r >> 5) * cols_p + c) * 32 + (r & 31) : c * rows_p + r;
       slice7<S>(tile[threadIdx.x][i], ec, P + o, plane);
     }
+  }
+}
+
+// Both left-operand slice sets of A in one pass (one read of A): the row
+// slices [S][kpn/32][mp][32] (row exponents, for Y = A X) and the column
+// slices [S][kpm/32][np][32] (column exponents, for Z = A^T Q). A 32 x 32
+// tile of A is one k-block of either layout, so each thread packs 4
+// consecutive bytes and a tile's writes are 1 KB contiguous per slice.
+template <int S>
+__global__ void __launch_bounds__(256)
+    slice_both_kernel(const double* __restrict__ X, int64_t m, int64_t n, int64_t ldx,
+                      const int32_t* __restrict__ er, const int32_t* __restrict__ ec,
+                      int8_t* __restrict__ PR, int64_t mp, int64_t kpn, int8_t* __restrict__ PC,
+                      int64_t np, int64_t kpm) {
+  __shared__ double tile[32][33];
+  __shared__ int ser[32], sec[32];
+  const int64_t r0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y, t = ty * 32 + tx;
+  for (int i = ty; i < 32; i += 8) {
+    const int64_t r = r0 + i, c = c0 + tx;
+    tile[i][tx] = (r < m && c < n) ? X[r * ldx + c] : 0.0;
+  }
+  if (ty == 0) {
+    ser[tx] = (r0 + tx < m) ? er[r0 + tx] : 0;
+    sec[tx] = (c0 + tx < n) ? ec[c0 + tx] : 0;
+  }
+  __syncthreads();
+  const int a = t >> 3, b4 = (t & 7) * 4;
+  if (r0 < mp && c0 < kpn) {  // row layout: (row a, cols b4..b4+3)
+    const int64_t planeR = mp * kpn;
+    uint32_t w[S];
+#pragma unroll
+    for (int q = 0; q < S; ++q) w[q] = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int d[S];
+      slice_digits<S>(tile[a][b4 + j], ser[a], d);
+#pragma unroll
+      for (int q = 0; q < S; ++q) w[q] |= (uint32_t)(uint8_t)(int8_t)d[q] << (8 * j);
+    }
+    int8_t* o = PR + ((c0 >> 5) * mp + r0 + a) * 32 + b4;
+#pragma unroll
+    for (int q = 0; q < S; ++q) *reinterpret_cast<uint32_t*>(o + q * planeR) = w[q];
+  }
+  if (c0 < np && r0 < kpm) {  // column layout: (col a, rows b4..b4+3)
+    const int64_t planeC = np * kpm;
+    uint32_t w[S];
+#pragma unroll
+    for (int q = 0; q < S; ++q) w[q] = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int d[S];
+      slice_digits<S>(tile[b4 + j][a], sec[a], d);
+#pragma unroll
+      for (int q = 0; q < S; ++q) w[q] |= (uint32_t)(uint8_t)(int8_t)d[q] << (8 * j);
+    }
+    int8_t* o = PC + ((r0 >> 5) * np + c0 + a) * 32 + b4;
+#pragma unroll
+    for (int q = 0; q < S; ++q) *reinterpret_cast<uint32_t*>(o + q * planeC) = w[q];
   }
 }
 
@@ -532,6 +594,20 @@ void oz_slice_cols_t(const double* X, int64_t rows, int64_t cols, int64_t ldx, c
   OZ_DISPATCH(S, OZ_SC)
 #undef OZ_SC
   check_launch("slice_cols_t");
+}
+
+void oz_slice_both(const double* X, int64_t m, int64_t n, int64_t ldx, const int32_t* er,
+                   const int32_t* ec, int8_t* PR, int64_t mp, int64_t kpn, int8_t* PC, int64_t np,
+                   int64_t kpm, int S, cudaStream_t st) {
+  XB_REQUIRE(mp % 32 == 0 && np % 32 == 0 && kpn % 32 == 0 && kpm % 32 == 0 && mp >= kpm &&
+                 np >= kpn && ceil_div(np, 32) < 65536,
+             XB_EUNSUPPORTED, "oz_slice_both: layout");
+  dim3 grid((unsigned)(mp / 32), (unsigned)(np / 32));
+#define OZ_SB(SS) \
+  slice_both_kernel<SS><<<grid, dim3(32, 8), 0, st>>>(X, m, n, ldx, er, ec, PR, mp, kpn, PC, np, kpm)
+  OZ_DISPATCH(S, OZ_SB)
+#undef OZ_SB
+  check_launch("slice_both");
 }
 
 int oz_plan_splits(int64_t K) { return (int)std::max<int64_t>(1, ceil_div(K, 16384)); }

@@ -50,9 +50,9 @@ def test_ozaki_gemm_accuracy():
                          capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
     worst = float(out.stdout.strip().splitlines()[-1])
-    # 47 significant bits per operand (S = 6 slices): elementwise error
-    # relative to |A| |B| stays near 1e-13 (f64 GEMM: ~1e-16)
-    assert worst <= 1e-12, worst
+    # 47 significant bits per operand (S = 6 digit slices): elementwise error
+    # relative to |A| |B| measured ~1e-14 (f64 GEMM: ~1e-16)
+    assert worst <= 1e-13, worst
 
 
 def test_wide_dynamic_range_rows_stay_on_dmma(lib):
