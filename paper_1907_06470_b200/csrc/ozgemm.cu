@@ -282,16 +282,23 @@ __device__ __forceinline__ int slice_exp(double m) {
 // Digits of x 2^-e rounded to 7 + 8 (S-1) bits: V = rint(x 2^(7 + 8(S-1) - e))
 // = sum_t a_t 2^(8(S-1-t)), a_0 in [-127, 127] (top, weight 2^-7) and
 // balanced a_t in [-128, 127] below (weight 2^-(7 + 8t)).
+// 2^k as a double (exact for normal k; the slicing scales are far inside)
+__device__ __forceinline__ double pow2(int k) {
+  return __longlong_as_double((long long)(1023 + max(-1022, min(1023, k))) << 52);
+}
+
 template <int S>
 __device__ __forceinline__ void slice_digits(double x, int e, int (&a)[S]) {
-  long long v = llrint(scalbn(x, 7 + 8 * (S - 1) - e));
+  const long long v = __double2ll_rn(x * pow2(7 + 8 * (S - 1) - e));
+  // balanced base-256 digits without a carry chain: adding 128 at every lower
+  // digit position makes them plain bytes u_t (a_t = u_t - 128, i.e. the
+  // byte with its top bit flipped); the top digit is what remains above
+  constexpr unsigned long long kBias = 0x8080808080ULL >> (8 * (6 - S));
+  const unsigned long long u = (unsigned long long)v + kBias;
+  a[0] = (int)((long long)u >> (8 * (S - 1)));
 #pragma unroll
-  for (int t = S - 1; t >= 1; --t) {
-    const int d = (int)((v + 128) & 255) - 128;
-    a[t] = d;
-    v = (v - d) >> 8;
-  }
-  a[0] = (int)v;
+  for (int t = 1; t < S; ++t)
+    a[t] = (int)(int8_t)(uint8_t)(((u >> (8 * (S - 1 - t))) & 0xFF) ^ 0x80);
 }
 
 // max |x| over each row (one warp per row) -> slice exponent. The slices

@@ -45,25 +45,28 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ double pivs[1024];
   __shared__ double tmp[1024];
   double* W = use_smem ? sm : gw;
+  // odd row stride: the inverse reads W by columns (an even stride of 120
+  // doubles put 16 lanes on one bank pair)
+  const int64_t lw = l | 1;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // load the upper triangle (row-major, stride l)
   for (int i = warp; i < l; i += kWarps)
-    for (int c = lane; c < l; c += 32) W[(int64_t)i * l + c] = (c >= i) ? G[(int64_t)i * ldg + c] : 0.0;
+    for (int c = lane; c < l; c += 32) W[(int64_t)i * lw + c] = (c >= i) ? G[(int64_t)i * ldg + c] : 0.0;
   for (int j = tid; j < l; j += kThreads) diag0[j] = G[(int64_t)j * ldg + j];
   __syncthreads();
   // Cholesky: unscaled right-looking elimination, one barrier per column.
   bool failed = false;
   for (int j = 0; j < l; ++j) {
-    const double piv = W[(int64_t)j * l + j];
+    const double piv = W[(int64_t)j * lw + j];
     const bool ok = (piv > tau * diag0[j]) && (piv > 0.0);
     const double pe = ok ? piv : fmax(fabs(diag0[j]), DBL_MIN);  // keep going; result discarded
     failed |= !ok;
     if (tid == 0) pivs[j] = pe;
     const double inv = 1.0 / pe;
-    const double* rowj = W + (int64_t)j * l;
+    const double* rowj = W + (int64_t)j * lw;
     for (int i = j + 1 + warp; i < l; i += kWarps) {
       const double f = rowj[i] * inv;
-      double* rowi = W + (int64_t)i * l;
+      double* rowi = W + (int64_t)i * lw;
       for (int c = i + lane; c < l; c += 32) rowi[c] -= f * rowj[c];
     }
     __syncthreads();
@@ -73,13 +76,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   for (int j = warp; j < l; j += kWarps) {
     const double rs = 1.0 / sqrt(pivs[j]);
     for (int c = lane; c < l; c += 32) {
-      const double v = (c >= j) ? W[(int64_t)j * l + c] * rs : 0.0;
-      W[(int64_t)j * l + c] = v;
+      const double v = (c >= j) ? W[(int64_t)j * lw + c] * rs : 0.0;
+      W[(int64_t)j * lw + c] = v;
       R[(int64_t)j * ldr + c] = v;
     }
   }
   __syncthreads();
-  for (int j = tid; j < l; j += kThreads) pivs[j] = W[(int64_t)j * l + j];  // R's diagonal
+  for (int j = tid; j < l; j += kThreads) pivs[j] = W[(int64_t)j * lw + j];  // R's diagonal
   __syncthreads();
   // In-place upper-triangular inverse, column by column (dtrti2 order):
   // X[0:j, j] = -X[0:j, 0:j] R[0:j, j] / R[j][j], X[j][j] = 1 / R[j][j].
@@ -88,18 +91,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   for (int j = 0; j < l; ++j) {
     for (int i = warp; i < j; i += kWarps) {
       double acc = 0.0;
-      for (int p = i + lane; p < j; p += 32) acc += W[(int64_t)i * l + p] * W[(int64_t)p * l + j];
+      for (int p = i + lane; p < j; p += 32) acc += W[(int64_t)i * lw + p] * W[(int64_t)p * lw + j];
       acc = warp_sum32(acc);
       if (lane == 0) tmp[i] = acc;
     }
     __syncthreads();
     const double ajj = 1.0 / pivs[j];
-    for (int i = tid; i < j; i += kThreads) W[(int64_t)i * l + j] = -tmp[i] * ajj;
-    if (tid == 0) W[(int64_t)j * l + j] = ajj;
+    for (int i = tid; i < j; i += kThreads) W[(int64_t)i * lw + j] = -tmp[i] * ajj;
+    if (tid == 0) W[(int64_t)j * lw + j] = ajj;
     __syncthreads();
   }
   for (int i = warp; i < l; i += kWarps)
-    for (int c = lane; c < l; c += 32) Rinv[(int64_t)i * ldr + c] = (c >= i) ? W[(int64_t)i * l + c] : 0.0;
+    for (int c = lane; c < l; c += 32) Rinv[(int64_t)i * ldr + c] = (c >= i) ? W[(int64_t)i * lw + c] : 0.0;
 }
 
 // ---------------------------------------------------------------------------
@@ -767,7 +770,7 @@ size_t chol_work_doubles(int l) {
 void launch_chol_inv(const double* G, int64_t ldg, int l, double tau, double* R, double* Rinv,
                      int64_t ldr, int* flag, double* ws_in, cudaStream_t st) {
   XB_REQUIRE(l <= 4096, XB_EUNSUPPORTED, "chol_inv: l > 4096");
-  const size_t bytes = (size_t)l * l * sizeof(double);
+  const size_t bytes = (size_t)l * (l | 1) * sizeof(double);
   // XB_CHOL=coop forces the cooperative version (tests), =single the 1-CTA one
   static const int mode = [] {
     const char* e = getenv("XB_CHOL");
