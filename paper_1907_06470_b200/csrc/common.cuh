@@ -102,20 +102,21 @@ void oz_row_exp(const double* X, int64_t rows, int64_t cols, int64_t ldx, int32_
                 cudaStream_t st);
 void oz_col_exp(const double* X, int64_t rows, int64_t cols, int64_t ldx, int32_t* e,
                 unsigned long long* scratch, int* wide, cudaStream_t st);
-void oz_slice_rows(const double* X, int64_t rows, int64_t cols, int64_t ldx, const int32_t* e,
-                   int8_t* P, int64_t rows_p, int64_t kp, int S, cudaStream_t st);
-// kblocked: [rows_p/32][cols_p][32] (a left operand), else [cols_p][rows_p] (a right operand)
-void oz_slice_cols_t(const double* X, int64_t rows, int64_t cols, int64_t ldx, const int32_t* e,
-                     int8_t* P, int64_t cols_p, int64_t rows_p, int S, bool kblocked,
-                     cudaStream_t st);
-// Row slices [S][kpn/32][mp][32] and column slices [S][kpm/32][np][32] of X
-// (m x n) in one pass (mp, np multiples of 128; kpn, kpm of 32).
+// Right-operand slices of X (K x N, ldx, column exponents e): 64-row
+// interleaved tiles, zero padded to np (multiple of 64) x kp (of 32).
+void oz_slice_right(const double* X, int64_t K, int64_t N, int64_t ldx, const int32_t* e,
+                    int8_t* P, int64_t np, int64_t kp, int S, cudaStream_t st);
+// Left-operand slices of X (m x n) in one pass: PR = row-scaled slices of X
+// (mp x kpn), PC = column-scaled slices of X^T (np x kpm); 128-row
+// interleaved tiles (mp, np multiples of 128 with mp >= kpm, np >= kpn;
+// kpn, kpm multiples of 32). Either output may be null.
 void oz_slice_both(const double* X, int64_t m, int64_t n, int64_t ldx, const int32_t* er,
                    const int32_t* ec, int8_t* PR, int64_t mp, int64_t kpn, int8_t* PC, int64_t np,
                    int64_t kpm, int S, cudaStream_t st);
 size_t oz_workspace_doubles(int64_t M, int64_t N, int64_t K);
-// C (M x N) = L R: L slices k-blocked [S][kp/32][rows_p][32] (row exponents
-// eL), R slices [S][np][kp] (the transposed right operand, column exponents eR).
+// C (M x N) = L R: L = left slices (rows_p x kp, 128-row interleaved tiles,
+// row exponents eL), R = right slices (np x kp, 64-row tiles, column
+// exponents eR).
 void ozgemm(const int8_t* L, int64_t rows_p, int64_t kp, const int32_t* eL, const int8_t* R,
             int64_t np, const int32_t* eR, int64_t M, int64_t N, int64_t K, double* C, int64_t ldc,
             bool accumulate, int S, double* work, cudaStream_t st);

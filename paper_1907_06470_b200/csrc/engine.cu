@@ -569,12 +569,12 @@ void oz_product(xb_ctx* c, const OzA& z, bool tn, int64_t m, int64_t n, const do
     XB_CUDA(cudaEventRecord(b, c->st));
   }
   const int64_t Mo = tn ? n : m, Kk = tn ? m : n, kp = tn ? z.kpm : z.kpn;
-  const int64_t np = round_up(lp, 8);
+  const int64_t np = round_up(lp, 64);
   int32_t* ex = c->ibuf("oz_ex", np);
   auto* scr = static_cast<unsigned long long*>(c->buf("oz_xscr", np * 8));
   int8_t* xs = static_cast<int8_t*>(c->buf("oz_xs", (size_t)z.S * np * kp));
   oz_col_exp(X, Kk, lp, lp, ex, scr, nullptr, c->st);
-  oz_slice_cols_t(X, Kk, lp, lp, ex, xs, np, kp, z.S, false, c->st);
+  oz_slice_right(X, Kk, lp, lp, ex, xs, np, kp, z.S, c->st);
   const size_t wd = oz_workspace_doubles(Mo, lp, Kk);
   double* work = wd ? c->dbuf("split", wd) : nullptr;
   ozgemm(tn ? z.colsT : z.rows, tn ? z.np : z.mp, kp, tn ? z.ecol : z.erow, xs, np, ex, Mo, lp,
@@ -1079,21 +1079,23 @@ void gemm_any(xb_ctx* c, bool f32, bool ta, int64_t m, int64_t n, int64_t kdim, 
       const int S = oz_slices();
       const double* A = static_cast<const double*>(dA);
       const double* B = static_cast<const double*>(dB);
-      const int64_t kp = round_up(kdim, 32), np = round_up(n, 8), mp = round_up(m, 128);
+      const int64_t kp = round_up(kdim, 32), np = round_up(n, 64), mp = round_up(m, 128);
       int8_t* L = static_cast<int8_t*>(c->buf("dbg_L", (size_t)S * mp * kp));
       int8_t* R = static_cast<int8_t*>(c->buf("dbg_R", (size_t)S * np * kp));
       int32_t* eL = c->ibuf("dbg_eL", m);
       int32_t* eR = c->ibuf("dbg_eR", np);
       auto* scr = static_cast<unsigned long long*>(c->buf("dbg_scr", (size_t)std::max(m, np) * 8));
-      if (ta) {
+      if (ta) {  // op(A) = A^T, A stored kdim x m: column slices of the stored A
         oz_col_exp(A, kdim, m, lda, eL, scr, nullptr, c->st);
-        oz_slice_cols_t(A, kdim, m, lda, eL, L, mp, kp, S, true, c->st);
+        oz_slice_both(A, kdim, m, lda, nullptr, eL, nullptr, round_up(kdim, 128), round_up(m, 32),
+                      L, mp, kp, S, c->st);
       } else {
         oz_row_exp(A, m, kdim, lda, eL, nullptr, c->st);
-        oz_slice_rows(A, m, kdim, lda, eL, L, mp, kp, S, c->st);
+        oz_slice_both(A, m, kdim, lda, eL, nullptr, L, mp, kp, nullptr, round_up(kdim, 128),
+                      round_up(m, 32), S, c->st);
       }
       oz_col_exp(B, kdim, n, ldb, eR, scr, nullptr, c->st);
-      oz_slice_cols_t(B, kdim, n, ldb, eR, R, np, kp, S, false, c->st);
+      oz_slice_right(B, kdim, n, ldb, eR, R, np, kp, S, c->st);
       const size_t wd = oz_workspace_doubles(m, n, kdim);
       double* work = wd ? c->dbuf("split", wd) : nullptr;
       ozgemm(L, mp, kp, eL, R, np, eR, m, n, kdim, static_cast<double*>(dC), ldc, false, S, work,

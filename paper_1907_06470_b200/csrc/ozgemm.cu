@@ -71,6 +71,23 @@ struct OCfg {
   static_assert(USED <= 512, "TMEM budget");
 };
 
+// Slice layout in HBM = the layout the MMA / tcgen05.cp read from shared
+// memory, so each k-tile arrives with ONE linear bulk copy per operand
+// (TMA tensor boxes of 32-byte rows ran ~1 request per row: the copies, not
+// the tensor pipe, bounded the kernel at 2.6 ms for cfg2's products). For
+// row tiles of TR rows x 32 bytes of K: no-swizzle K-major core matrices of
+// 8 rows x 16 B (128 B each), the two K-chunks 128 B apart (LBO), 8-row
+// groups 256 B apart (SBO); the S slices of one (k-block, row tile) are
+// consecutive TR x 32 B tiles.
+template <int TR>
+__device__ __forceinline__ int64_t il_off(int64_t row, int64_t k, int t, int S, int64_t rows_p) {
+  const int64_t kb = k >> 5;
+  const int kc = (int)((k >> 4) & 1), kin = (int)(k & 15);
+  const int64_t tile = kb * (rows_p / TR) + row / TR;
+  const int rr = (int)(row % TR);
+  return (tile * S + t) * (TR * 32) + ((rr >> 3) * 2 + kc) * 128 + (rr & 7) * 16 + kin;
+}
+
 template <int S>
 __device__ __forceinline__ uint32_t idesc_i8() {
   return (2u << 4)                          // D: s32
@@ -115,21 +132,14 @@ __device__ __forceinline__ void commit_elect(uint64_t* bar) {
       : "memory");
 }
 
-__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar,
-                                            int32_t c0, int32_t c1, int32_t c2, int32_t c3) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
-      "%3, %4, %5}], [%6];\n" ::"r"(su32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(su32(bar))
-      : "memory");
-}
 
 template <int S>
 __global__ void __launch_bounds__(OTHREADS, 1)
-    ozgemm_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_constant__ CUtensorMap tmR,
-                  const int32_t* __restrict__ eL, const int32_t* __restrict__ eR, int64_t M,
-                  int64_t N, int64_t K, double* __restrict__ C, int64_t ldc, int64_t split_stride,
-                  int64_t k_per_split, int accumulate, int tiles_n) {
+    ozgemm_kernel(const int8_t* __restrict__ L, const int8_t* __restrict__ R, int64_t rows_p,
+                  int64_t np, const int32_t* __restrict__ eL, const int32_t* __restrict__ eR,
+                  int64_t M, int64_t N, int64_t K, double* __restrict__ C, int64_t ldc,
+                  int64_t split_stride,
+                  int64_t k_per_split, int accumulate, int tiles_n, int dbg) {
   using Cfg = OCfg<S>;
   constexpr int NS = Cfg::NS;
   extern __shared__ unsigned char smem_raw_o[];
@@ -168,18 +178,17 @@ __global__ void __launch_bounds__(OTHREADS, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    // ---- TMA producer: S left-slice tiles (4-D box over the k-blocked
-    // slices) and S right-slice tiles per k-tile ------------------------------
+    // ---- producer: one bulk copy per operand per k-tile --------------------------
     if (lane == 0) {
-      const int32_t kb0 = (int32_t)(kbeg / OBK);
+      const int64_t kb0 = kbeg / OBK, lt = rows_p / OBM, rt = np / OBN;
       for (int kt = 0; kt < ktiles; ++kt) {
         const int s = kt % NS;
         if (kt >= NS) mbar_wait_park(&empty[s], ((kt / NS) & 1) ^ 1);
         unsigned char* st = smem + s * Cfg::STAGE;
         mbar_expect_tx(&full[s], Cfg::STAGE);
-        tma_load_4d(st, &tmL, &full[s], 0, (int32_t)m0, kb0 + kt, 0);
-        tma_load_3d(st + S * Cfg::ATILE, &tmR, &full[s], (int32_t)(kbeg + (int64_t)kt * OBK),
-                    (int32_t)n0, 0);
+        bulk_load(st, L + ((kb0 + kt) * lt + mt) * (S * Cfg::ATILE), S * Cfg::ATILE, &full[s]);
+        bulk_load(st + S * Cfg::ATILE, R + ((kb0 + kt) * rt + nt) * (S * Cfg::RTILE),
+                  S * Cfg::RTILE, &full[s]);
       }
     }
   } else if (warp == 1) {
@@ -195,17 +204,21 @@ __global__ void __launch_bounds__(OTHREADS, 1)
       const uint32_t aslot = tm + (uint32_t)(Cfg::ACC_COLS + a * Cfg::ASLOT);
       const uint32_t abase = sbase + (uint32_t)(s * Cfg::STAGE);
       const uint32_t rbase = abase + (uint32_t)(S * Cfg::ATILE);
+      if (!(dbg & 1)) {
 #pragma unroll
-      for (int t = 0; t < S; ++t)
-        cp_128x256b(aslot + (uint32_t)(t * (OBK / 4)), smem_desc(abase + t * Cfg::ATILE, 256, 6));
+        for (int t = 0; t < S; ++t)
+          cp_128x256b(aslot + (uint32_t)(t * (OBK / 4)),
+                      smem_desc(abase + t * Cfg::ATILE, 256, 0, 128));
+      }
       const uint32_t first = kt > 0 ? 1u : 0u;
 #pragma unroll
       for (int t = 0; t < S; ++t) {
+        if (dbg & 2) break;
 #pragma unroll
         for (int u = 0; u < S - t; ++u) {
           const int d = t + u;  // level (t + 1) + (u + 1) - 2
           mma_i8(tm + (uint32_t)(d * OBN), aslot + (uint32_t)(t * (OBK / 4)),
-                 smem_desc(rbase + u * Cfg::RTILE, 256, 6), idesc, t > 0 ? 1u : first);
+                 smem_desc(rbase + u * Cfg::RTILE, 256, 0, 128), idesc, t > 0 ? 1u : first);
         }
       }
       commit_elect(&empty[s]);
@@ -367,70 +380,12 @@ __device__ __forceinline__ void slice7(double x, int e, int8_t* out, int64_t pla
   for (int t = 0; t < S; ++t) out[t * plane] = (int8_t)a[t];
 }
 
-// row slices, k-blocked: X (rows x cols, ldx) -> P[t][kp/32][rows_p][32],
-// zero padded; one thread per 8 consecutive k of a row (8-byte stores)
-template <int S>
-__global__ void slice_rows_kernel(const double* __restrict__ X, int64_t rows, int64_t cols,
-                                  int64_t ldx, const int32_t* __restrict__ e,
-                                  int8_t* __restrict__ P, int64_t rows_p, int64_t kp) {
-  const int64_t plane = rows_p * kp;
-  const int64_t total = plane / 8;
-  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int j = (int)(idx & 3);
-    const int64_t rk = idx >> 2;
-    const int64_t r = rk % rows_p, kb = rk / rows_p;
-    const int64_t c0 = kb * 32 + j * 8;
-    uint64_t w[S];
-#pragma unroll
-    for (int t = 0; t < S; ++t) w[t] = 0;
-    if (r < rows) {
-      const int er = e[r];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int64_t c = c0 + q;
-        int a[S];
-        slice_digits<S>(c < cols ? X[r * ldx + c] : 0.0, er, a);
-#pragma unroll
-        for (int t = 0; t < S; ++t) w[t] |= (uint64_t)(uint8_t)(int8_t)a[t] << (8 * q);
-      }
-    }
-    int8_t* out = P + (kb * rows_p + r) * 32 + j * 8;
-#pragma unroll
-    for (int t = 0; t < S; ++t) *reinterpret_cast<uint64_t*>(out + t * plane) = w[t];
-  }
-}
-
-// column slices, transposed: X (rows x cols) -> P[t] scaled per column, as
-// (KBLOCK) [rows_p/32][cols_p][32] or (plain) [cols_p][rows_p]; 32 x 32
-// tiles through shared memory
-template <int S, bool KBLOCK>
-__global__ void slice_cols_t_kernel(const double* __restrict__ X, int64_t rows, int64_t cols,
-                                    int64_t ldx, const int32_t* __restrict__ e,
-                                    int8_t* __restrict__ P, int64_t cols_p, int64_t rows_p) {
-  __shared__ double tile[32][33];
-  const int64_t r0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
-  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-    const int64_t r = r0 + i, c = c0 + threadIdx.x;
-    tile[i][threadIdx.x] = (r < rows && c < cols) ? X[r * ldx + c] : 0.0;
-  }
-  __syncthreads();
-  const int64_t plane = cols_p * rows_p;
-  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-    const int64_t c = c0 + i, r = r0 + threadIdx.x;
-    if (c < cols_p && r < rows_p) {
-      const int ec = c < cols ? e[c] : 0;
-      const int64_t o = KBLOCK ? ((r >> 5) * cols_p + c) * 32 + (r & 31) : c * rows_p + r;
-      slice7<S>(tile[threadIdx.x][i], ec, P + o, plane);
-    }
-  }
-}
-
-// Both left-operand slice sets of A in one pass (one read of A): the row
-// slices [S][kpn/32][mp][32] (row exponents, for Y = A X) and the column
-// slices [S][kpm/32][np][32] (column exponents, for Z = A^T Q). A 32 x 32
-// tile of A is one k-block of either layout, so each thread packs 4
-// consecutive bytes and a tile's writes are 1 KB contiguous per slice.
+// Slices of a left operand straight from A, in one pass over A (one read):
+// PR = the row-scaled slices of A (rows of A, K = columns; for Y = A X) and
+// PC = the column-scaled slices of A^T (columns of A, K = rows; for
+// Z = A^T Q), both in the interleaved tile layout (il_off<128>). Either may be
+// null. A 32 x 32 tile of A is one k-block of either layout; each thread packs
+// 4 consecutive K bytes.
 template <int S>
 __global__ void __launch_bounds__(256)
     slice_both_kernel(const double* __restrict__ X, int64_t m, int64_t n, int64_t ldx,
@@ -446,13 +401,12 @@ __global__ void __launch_bounds__(256)
     tile[i][tx] = (r < m && c < n) ? X[r * ldx + c] : 0.0;
   }
   if (ty == 0) {
-    ser[tx] = (r0 + tx < m) ? er[r0 + tx] : 0;
-    sec[tx] = (c0 + tx < n) ? ec[c0 + tx] : 0;
+    ser[tx] = (er && r0 + tx < m) ? er[r0 + tx] : 0;
+    sec[tx] = (ec && c0 + tx < n) ? ec[c0 + tx] : 0;
   }
   __syncthreads();
   const int a = t >> 3, b4 = (t & 7) * 4;
-  if (r0 < mp && c0 < kpn) {  // row layout: (row a, cols b4..b4+3)
-    const int64_t planeR = mp * kpn;
+  if (PR && r0 < mp && c0 < kpn) {  // row layout: (row r0+a, k = c0+b4..+3)
     uint32_t w[S];
 #pragma unroll
     for (int q = 0; q < S; ++q) w[q] = 0;
@@ -463,12 +417,11 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
       for (int q = 0; q < S; ++q) w[q] |= (uint32_t)(uint8_t)(int8_t)d[q] << (8 * j);
     }
-    int8_t* o = PR + ((c0 >> 5) * mp + r0 + a) * 32 + b4;
 #pragma unroll
-    for (int q = 0; q < S; ++q) *reinterpret_cast<uint32_t*>(o + q * planeR) = w[q];
+    for (int q = 0; q < S; ++q)
+      *reinterpret_cast<uint32_t*>(PR + il_off<128>(r0 + a, c0 + b4, q, S, mp)) = w[q];
   }
-  if (c0 < np && r0 < kpm) {  // column layout: (col a, rows b4..b4+3)
-    const int64_t planeC = np * kpm;
+  if (PC && c0 < np && r0 < kpm) {  // column layout: (row c0+a of A^T, k = r0+b4..+3)
     uint32_t w[S];
 #pragma unroll
     for (int q = 0; q < S; ++q) w[q] = 0;
@@ -479,16 +432,51 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
       for (int q = 0; q < S; ++q) w[q] |= (uint32_t)(uint8_t)(int8_t)d[q] << (8 * j);
     }
-    int8_t* o = PC + ((r0 >> 5) * np + c0 + a) * 32 + b4;
 #pragma unroll
-    for (int q = 0; q < S; ++q) *reinterpret_cast<uint32_t*>(o + q * planeC) = w[q];
+    for (int q = 0; q < S; ++q)
+      *reinterpret_cast<uint32_t*>(PC + il_off<128>(c0 + a, r0 + b4, q, S, np)) = w[q];
+  }
+}
+
+// Right operand: X (K x N, ldx) -> column-scaled slices of X^T in the
+// interleaved layout of 64-row tiles (il_off<64>), zero padded to (np, kp).
+template <int S>
+__global__ void __launch_bounds__(256)
+    slice_right_kernel(const double* __restrict__ X, int64_t K, int64_t N, int64_t ldx,
+                       const int32_t* __restrict__ e, int8_t* __restrict__ P, int64_t np,
+                       int64_t kp) {
+  __shared__ double tile[32][33];
+  __shared__ int se[32];
+  const int64_t k0 = (int64_t)blockIdx.x * 32, n0 = (int64_t)blockIdx.y * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y, t = ty * 32 + tx;
+  for (int i = ty; i < 32; i += 8) {
+    const int64_t k = k0 + i, c = n0 + tx;
+    tile[i][tx] = (k < K && c < N) ? X[k * ldx + c] : 0.0;
+  }
+  if (ty == 0) se[tx] = (n0 + tx < N) ? e[n0 + tx] : 0;
+  __syncthreads();
+  const int a = t >> 3, b4 = (t & 7) * 4;
+  if (n0 + a < np && k0 < kp) {
+    uint32_t w[S];
+#pragma unroll
+    for (int q = 0; q < S; ++q) w[q] = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int d[S];
+      slice_digits<S>(tile[b4 + j][a], se[a], d);
+#pragma unroll
+      for (int q = 0; q < S; ++q) w[q] |= (uint32_t)(uint8_t)(int8_t)d[q] << (8 * j);
+    }
+#pragma unroll
+    for (int q = 0; q < S; ++q)
+      *reinterpret_cast<uint32_t*>(P + il_off<64>(n0 + a, k0 + b4, q, S, np)) = w[q];
   }
 }
 
 template <int S>
-void launch_oz(const CUtensorMap& tl, const CUtensorMap& tr, const int32_t* eL, const int32_t* eR,
-               int64_t M, int64_t N, int64_t K, double* out, int64_t ldo, int64_t stride,
-               int64_t kps, int splits, int acc, cudaStream_t st) {
+void launch_oz(const int8_t* L, const int8_t* R, int64_t rows_p, int64_t np, const int32_t* eL,
+               const int32_t* eR, int64_t M, int64_t N, int64_t K, double* out, int64_t ldo,
+               int64_t stride, int64_t kps, int splits, int acc, cudaStream_t st) {
   using Cfg = OCfg<S>;
   auto kern = ozgemm_kernel<S>;
   XB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
@@ -496,39 +484,13 @@ void launch_oz(const CUtensorMap& tl, const CUtensorMap& tr, const int32_t* eL, 
   XB_REQUIRE(tn * tm < ((int64_t)1 << 31) && splits < 65536, XB_EUNSUPPORTED,
              "ozgemm: grid too large");
   dim3 grid((unsigned)(tn * tm), (unsigned)splits);
-  kern<<<grid, OTHREADS, Cfg::SMEM, st>>>(tl, tr, eL, eR, M, N, K, out, ldo, stride, kps, acc,
-                                          (int)tn);
+  static const int dbg = [] {
+    const char* e = getenv("XB_OZ_DBG");
+    return e ? atoi(e) : 0;
+  }();
+  kern<<<grid, OTHREADS, Cfg::SMEM, st>>>(L, R, rows_p, np, eL, eR, M, N, K, out, ldo, stride,
+                                          kps, acc, (int)tn, dbg);
   check_launch("ozgemm");
-}
-
-// k-blocked left slices [S][kp/32][rows_p][32]: dims {32, rows_p, kb, S},
-// boxes {32, 128, 1, S} (one 24 KB load per k-tile), 32-byte swizzle
-CUtensorMap make_map_left(const int8_t* base, uint64_t rows_p, uint64_t kb, int S) {
-  CUtensorMap m;
-  const cuuint64_t dims[4] = {32, rows_p, kb, (cuuint64_t)S};
-  const cuuint64_t strides[3] = {32, rows_p * 32, kb * rows_p * 32};
-  const cuuint32_t box[4] = {32, (cuuint32_t)OBM, 1, (cuuint32_t)S};
-  const cuuint32_t es[4] = {1, 1, 1, 1};
-  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(base), dims,
-                           strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  XB_REQUIRE(r == CUDA_SUCCESS, XB_ECUDA, "cuTensorMapEncodeTiled (left slices) failed: " + std::to_string(r));
-  return m;
-}
-
-CUtensorMap make_map_slices(const int8_t* base, uint64_t kp, uint64_t np, int S) {
-  CUtensorMap m;
-  const cuuint64_t dims[3] = {kp, np, (cuuint64_t)S};
-  const cuuint64_t strides[2] = {kp, kp * np};
-  const cuuint32_t box[3] = {(cuuint32_t)OBK, (cuuint32_t)OBN, (cuuint32_t)S};
-  const cuuint32_t es[3] = {1, 1, 1};
-  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3,
-                           const_cast<int8_t*>(base), dims, strides, box, es,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
-                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  XB_REQUIRE(r == CUDA_SUCCESS, XB_ECUDA, "cuTensorMapEncodeTiled (slices) failed: " + std::to_string(r));
-  return m;
 }
 
 }  // namespace
@@ -577,37 +539,22 @@ void oz_col_exp(const double* X, int64_t rows, int64_t cols, int64_t ldx, int32_
     default: CALL(6); break; \
   }
 
-void oz_slice_rows(const double* X, int64_t rows, int64_t cols, int64_t ldx, const int32_t* e,
-                   int8_t* P, int64_t rows_p, int64_t kp, int S, cudaStream_t st) {
-  XB_REQUIRE(kp % 32 == 0, XB_EUNSUPPORTED, "oz_slice_rows: kp % 32");
-  const int blocks = (int)std::min<int64_t>(ceil_div(rows_p * kp / 8, 256), kNumSMs * 16);
-#define OZ_SR(SS) slice_rows_kernel<SS><<<blocks, 256, 0, st>>>(X, rows, cols, ldx, e, P, rows_p, kp)
-  OZ_DISPATCH(S, OZ_SR)
-#undef OZ_SR
-  check_launch("slice_rows");
-}
-
-void oz_slice_cols_t(const double* X, int64_t rows, int64_t cols, int64_t ldx, const int32_t* e,
-                     int8_t* P, int64_t cols_p, int64_t rows_p, int S, bool kblocked,
-                     cudaStream_t st) {
-  dim3 grid((unsigned)ceil_div(rows_p, 32), (unsigned)ceil_div(cols_p, 32));
-#define OZ_SC(SS)                                                                             \
-  if (kblocked)                                                                               \
-    slice_cols_t_kernel<SS, true><<<grid, dim3(32, 8), 0, st>>>(X, rows, cols, ldx, e, P,     \
-                                                                cols_p, rows_p);              \
-  else                                                                                        \
-    slice_cols_t_kernel<SS, false><<<grid, dim3(32, 8), 0, st>>>(X, rows, cols, ldx, e, P,    \
-                                                                 cols_p, rows_p)
-  OZ_DISPATCH(S, OZ_SC)
-#undef OZ_SC
-  check_launch("slice_cols_t");
+void oz_slice_right(const double* X, int64_t K, int64_t N, int64_t ldx, const int32_t* e,
+                    int8_t* P, int64_t np, int64_t kp, int S, cudaStream_t st) {
+  XB_REQUIRE(np % OBN == 0 && kp % OBK == 0 && np / 32 < 65536, XB_EUNSUPPORTED,
+             "oz_slice_right: layout");
+  dim3 grid((unsigned)(kp / 32), (unsigned)(np / 32));
+#define OZ_SX(SS) slice_right_kernel<SS><<<grid, dim3(32, 8), 0, st>>>(X, K, N, ldx, e, P, np, kp)
+  OZ_DISPATCH(S, OZ_SX)
+#undef OZ_SX
+  check_launch("slice_right");
 }
 
 void oz_slice_both(const double* X, int64_t m, int64_t n, int64_t ldx, const int32_t* er,
                    const int32_t* ec, int8_t* PR, int64_t mp, int64_t kpn, int8_t* PC, int64_t np,
                    int64_t kpm, int S, cudaStream_t st) {
-  XB_REQUIRE(mp % 32 == 0 && np % 32 == 0 && kpn % 32 == 0 && kpm % 32 == 0 && mp >= kpm &&
-                 np >= kpn && ceil_div(np, 32) < 65536,
+  XB_REQUIRE(mp % OBM == 0 && np % OBM == 0 && kpn % 32 == 0 && kpm % 32 == 0 && mp >= kpm &&
+                 np >= kpn && np / 32 < 65536,
              XB_EUNSUPPORTED, "oz_slice_both: layout");
   dim3 grid((unsigned)(mp / 32), (unsigned)(np / 32));
 #define OZ_SB(SS) \
@@ -623,10 +570,9 @@ void ozgemm(const int8_t* L, int64_t rows_p, int64_t kp, const int32_t* eL, cons
             int64_t np, const int32_t* eR, int64_t M, int64_t N, int64_t K, double* C, int64_t ldc,
             bool accumulate, int S, double* work, cudaStream_t st) {
   if (M <= 0 || N <= 0) return;
-  XB_REQUIRE(kp % 32 == 0 && rows_p >= M, XB_EUNSUPPORTED, "ozgemm: slice layout");
-  XB_REQUIRE(rows_p % OBM == 0, XB_EUNSUPPORTED, "ozgemm: rows_p % 128");
-  const CUtensorMap tl = make_map_left(L, (uint64_t)rows_p, (uint64_t)(kp / OBK), S);
-  const CUtensorMap tr = make_map_slices(R, (uint64_t)kp, (uint64_t)np, S);
+  XB_REQUIRE(kp % OBK == 0 && rows_p % OBM == 0 && rows_p >= M && np % OBN == 0 && np >= N &&
+                 kp >= K,
+             XB_EUNSUPPORTED, "ozgemm: slice layout");
   int splits = oz_plan_splits(K);
   const int64_t kps = round_up(ceil_div(K, splits), OBK);
   splits = (int)ceil_div(K, kps);
@@ -639,7 +585,7 @@ void ozgemm(const int8_t* L, int64_t rows_p, int64_t kp, const int32_t* eL, cons
     stride = M * ldo;
   }
   const int acc = (splits == 1 && accumulate) ? 1 : 0;
-#define OZ_RUN(SS) launch_oz<SS>(tl, tr, eL, eR, M, N, K, out, ldo, stride, kps, splits, acc, st)
+#define OZ_RUN(SS) launch_oz<SS>(L, R, rows_p, np, eL, eR, M, N, K, out, ldo, stride, kps, splits, acc, st)
   OZ_DISPATCH(S, OZ_RUN)
 #undef OZ_RUN
   if (splits > 1) launch_split_reduce(work, M, N, ldo, stride, splits, C, ldc, accumulate, st);

@@ -79,17 +79,29 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
-// Shared-memory matrix descriptor (sm_100 version 1), K-major, swizzled:
-// layout 2 = SWIZZLE_128B (8-row groups 1024 B apart), 6 = SWIZZLE_32B
-// (8-row groups 256 B apart).
-__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t sbo_bytes, uint32_t layout) {
+// Shared-memory matrix descriptor (sm_100 version 1), K-major. layout 0 =
+// no swizzle (interleaved 8-row x 16 B core matrices: lbo = their stride
+// along K, sbo = along M/N), 2 = SWIZZLE_128B (8-row groups sbo = 1024 B
+// apart), 6 = SWIZZLE_32B (sbo = 256 B); lbo is unused when swizzled.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t sbo_bytes, uint32_t layout,
+                                              uint32_t lbo_bytes = 16) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-  d |= (uint64_t)1 << 16;  // LBO (unused for swizzled K-major)
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
   d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32;
   d |= (uint64_t)1 << 46;  // descriptor version
   d |= (uint64_t)layout << 61;
   return d;
+}
+
+// 1-D bulk copy global -> shared, completing on an mbarrier (tx bytes)
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
+                                          uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          su32(dst)),
+      "l"(src), "r"(bytes), "r"(su32(bar))
+      : "memory");
 }
 
 inline PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
