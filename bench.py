@@ -20,10 +20,13 @@ e2e    = the same metric through the reference-facing C ABI call
          (xb_rsvd_dense / xb_rsvd_coo) with HOST buffers: pinned A copied
          H2D inside the timed region (overlapped with the sketch), U/s/V
          copied back.
-roofline = the dominant kernel: dense f64 -> the FP64 DMMA tile GEMM over A
-         (achieved = 2*m*n*l flops per launch / its event-timed mean duration,
-         peak = the FP64 DMMA pipe rate measured in-process: MEASURED_PEAKS.json
-         has no FP64 figure); dense f32 -> the tcgen05 3xTF32 GEMM (same
+roofline = the dominant kernel: dense f64 at m*n >= 2^24 -> the int8-slice
+         (Ozaki) FP64 GEMM on tcgen05 kind::i8 (achieved = int8 tensor ops
+         issued per launch / its event-timed mean duration, peak = 2 x
+         MEASURED_PEAKS bf16; the useful FP64-equivalent rate is reported
+         beside it); smaller dense f64 -> the FP64 DMMA tile GEMM (achieved =
+         2*m*n*l flops per launch / duration, peak = the DMMA pipe rate
+         measured in-process: MEASURED_PEAKS.json has no FP64 figure); dense f32 -> the tcgen05 3xTF32 GEMM (same
          achieved, peak = MEASURED_PEAKS bf16 / 2 / 3); sparse -> the CSR SpMM (achieved = algorithmic
          bytes per launch / duration, peak = MEASURED_PEAKS.json hbm_gbs).
 cpu_baseline = the oracle's restatement of the reference's shipped driver
@@ -233,25 +236,46 @@ def run_reference(args):
 # -- device workloads -----------------------------------------------------------------
 
 def gemm_roofline(prof, esz, dmma_peak, dfma_peak):
-    """The GEMM over A: 2 m n l useful flops per launch / event-timed duration."""
-    per_s = prof["seconds"] / max(prof["launches"], 1)
-    achieved = prof["flops"] / max(prof["launches"], 1) / per_s / 1e12
+    """The GEMM over A. achieved = tensor-pipe work per launch / event-timed
+    launch duration, against the peak of the pipe the kernel runs on; the
+    useful (algorithmic, 2 m n l) rate is reported beside it."""
+    n = max(prof["launches"], 1)
+    per_s = prof["seconds"] / n
+    useful = prof["flops"] / n / per_s / 1e12
     hbm = prof["bytes"] / prof["seconds"] / 1e9 if prof["seconds"] else None
-    if esz == 4 and os.environ.get("XB_F32_GEMM") != "dmma":
+    bf16 = measured_peaks().get("bf16_tflops")
+    kind = prof.get("kind")
+    if kind == "tf32x3":
         # 3xTF32 on tcgen05: useful flops = 2 m n l, the tensor pipe does 3x
         # that in kind::tf32, whose dense rate is half the bf16 rate.
-        bf16 = measured_peaks().get("bf16_tflops")
         peak = bf16 / 2 / 3 if bf16 else 2250.0 / 2 / 3
-        return {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak,
+        return {"bound": "tensor", "achieved": useful, "peak": peak, "unit": "TFLOP/s",
+                "frac": useful / peak,
                 "kernel": "tgemm_kernel (tcgen05.mma kind::tf32 x3 split, TMA, TMEM; "
                           "NN/TN over float32 A)",
                 "peak_source": ("MEASURED_PEAKS.json bf16_tflops / 2 (tf32 rate) / 3 (three "
                                 "products per useful flop)" if bf16 else
                                 "nominal 2250 bf16 TF/s / 2 / 3 (no MEASURED_PEAKS.json)"),
                 "hbm_gbs_achieved": hbm}
-    return {"bound": "tensor", "achieved": achieved, "peak": dmma_peak, "unit": "TFLOP/s",
-            "frac": achieved / dmma_peak if dmma_peak else None,
+    if kind == "ozaki_i8":
+        # FP64 emulated on the int8 tensor pipe (ozgemm.cu): S(S+1)/2 exact
+        # int8 slice products per useful multiply-add. kind::i8 dense rate =
+        # 2x the bf16 rate on B200 (nominal 4.5 vs 2.25 PFLOP/s).
+        peak = 2 * bf16 if bf16 else 4500.0
+        ops = prof["pipe_ops"] / n / per_s / 1e12
+        return {"bound": "tensor", "achieved": ops, "peak": peak, "unit": "TOP/s (int8)",
+                "frac": ops / peak,
+                "kernel": "oz_gemm_kernel (tcgen05.mma kind::i8, Ozaki int8 digit slices of f64 "
+                          "A and X, exact int32 products, f64 recombination; NN/TN over A) + "
+                          "the per-product slicing of X",
+                "peak_source": ("2 x MEASURED_PEAKS.json bf16_tflops (int8 dense rate = 2x bf16)"
+                                if bf16 else "nominal 4500 int8 TOP/s (no MEASURED_PEAKS.json)"),
+                "fp64_equivalent_tflops": useful,
+                "fp64_equivalent_vs_dmma_peak": useful / dmma_peak if dmma_peak else None,
+                "dmma_peak_tflops": dmma_peak,
+                "hbm_gbs_achieved": hbm}
+    return {"bound": "tensor", "achieved": useful, "peak": dmma_peak, "unit": "TFLOP/s",
+            "frac": useful / dmma_peak if dmma_peak else None,
             "kernel": "dgemm_kernel (FP64 DMMA m8n8k4, NN/TN over A"
                       + (", float32 A widened to f64)" if esz == 4 else ")"),
             "peak_source": f"in-process DMMA microbenchmark ({dmma_peak:.1f} TF/s; DFMA "

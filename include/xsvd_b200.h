@@ -80,6 +80,12 @@ void* xb_compute_stream(xb_ctx* ctx);
  * (m*n*elem each), and resets the accumulators. */
 int xb_profile_enable(xb_ctx* ctx, int on);
 int xb_profile_read(xb_ctx* ctx, double* out4);
+/* As xb_profile_read, plus out[4] = tensor-pipe operations the products
+ * issued (2 x multiply-adds, tile padding included: x3 for the 3xTF32 split,
+ * x S(S+1)/2 int8 slice pairs for the Ozaki path; 0 for SpMM) and out[5] =
+ * the product kind (0 FP64 DMMA, 1 tcgen05 3xTF32, 2 int8-slice Ozaki FP64,
+ * 3 CSR SpMM; the largest seen, -1 if none). Resets the accumulators. */
+int xb_profile_read_ext(xb_ctx* ctx, double* out6);
 /* Saturating FP64 microbenchmarks on the context's device: TFLOP/s of the
  * DMMA (mma.sync f64) and DFMA pipes — the f64 roofline denominator. */
 int xb_fp64_peaks(xb_ctx* ctx, double* dmma_tflops, double* dfma_tflops);
@@ -100,6 +106,21 @@ int xb_rsvd_dense(xb_ctx* ctx, int dtype, int64_t m, int64_t n, const void* A, i
                   const void* omega, uint64_t seed, int k, int p, int q,
                   void* U, int64_t ldu, double* s, void* V, int64_t ldv,
                   int32_t* deficient, int* ndeficient, double* stage_seconds);
+
+/* power = "auto" (RsvdConfig.power's default; pipeline.py:295-372,
+ * auto_select_q 396-418). Passing q = XB_POWER_AUTO to xb_rsvd_dense,
+ * xb_rsvd_dense_dev, xb_rsvd_dense_sharded_dev, xb_rsvd_coo or
+ * xb_rsvd_csr_dev runs up to q_max power passes and stops by the reference's
+ * rule on nu_q = ||(A A^T)^q A Omega||_F / sqrt(m l): nu_q < tau nu_0, or
+ * consecutive ratios nu_q / nu_{q-1} within 1% (nu_0 = 0 stops at q = 0).
+ * The raw products' norms are carried through the re-orthonormalised
+ * iteration as small triangular factors. xb_set_power_auto sets q_max / tau
+ * for the context (defaults 5, 1e-6); xb_last_power reports the last call's
+ * chosen q and its nu sequence (up to cap values, *count = how many). The
+ * out-of-core streamer does not support XB_POWER_AUTO (XB_EUNSUPPORTED). */
+#define XB_POWER_AUTO (-1)
+int xb_set_power_auto(xb_ctx* ctx, int q_max, double tau);
+int xb_last_power(xb_ctx* ctx, int* chosen_q, double* nus, int cap, int* count);
 
 /* Out-of-core factorization (the pinned-host tile streamer): A stays in host
  * memory and streams through HBM in row tiles of `tile_rows` (0 = automatic,

@@ -173,3 +173,34 @@ def rsvd_reorth(a, k, p, q, seed, precision="double", *, fast=False, om=None,
     u_b, s, v = _svd(b, fast)
     u = _mul(qm, u_b[:, :k], precision, fast)
     return OracleResult(u, s[:k].astype(np.float64), v[:, :k].astype(STORAGE[precision]), deficient)
+
+
+def sketch_power_auto(a, k, p, seed, precision="double", *, q_max=5, tau=1e-6, fast=False,
+                      om=None):
+    """power="auto" of _sketch_and_power (src/pipeline.py:295-372): raw
+    products Y = (A A^T)^q A Omega, nu_q = ||Y_q||_F / sqrt(m l); stop when
+    nu_q < tau nu_0 or consecutive ratios agree to 1%, or at q_max; a zero
+    sketch stops at q = 0. Returns (chosen q, [nu_0, ..., nu_chosen])."""
+    _check(a, k, p)
+    m, n = a.shape
+    l = k + p
+    o = omega(seed, n, l, precision) if om is None else om
+    scale = 1.0 / np.sqrt(m * l)
+    y = _mul(a, o, precision, fast)
+    nus = [float(np.sqrt(np.sum(np.asarray(y, dtype=np.float64) ** 2))) * scale]
+    if not nus[0] > 0.0:
+        return 0, nus
+    chosen, prev_rho = 0, 1.0
+    for q in range(1, q_max + 1):
+        z = _mul(_transpose(a), y, precision, fast)
+        y = _mul(a, z, precision, fast)
+        chosen = q
+        nus.append(float(np.sqrt(np.sum(np.asarray(y, dtype=np.float64) ** 2))) * scale)
+        nu = nus[-1]
+        if nu < tau * nus[0]:
+            break
+        rho = nu / nus[q - 1]
+        if abs(rho - prev_rho) <= 0.01 * rho:
+            break
+        prev_rho = rho
+    return chosen, nus

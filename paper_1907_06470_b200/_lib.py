@@ -20,6 +20,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "lib
 
 XB_F32, XB_F64 = 1, 2
 NUM_STAGES = 8
+POWER_AUTO = -1  # XB_POWER_AUTO: q argument selecting power = "auto"
 
 _lock = threading.Lock()
 _lib = None
@@ -37,7 +38,10 @@ SIGNATURES = [
     ("xb_compute_stream", _vp, [_vp]),
     ("xb_profile_enable", _int, [_vp, _int]),
     ("xb_profile_read", _int, [_vp, _vp]),
+    ("xb_profile_read_ext", _int, [_vp, _vp]),
     ("xb_fp64_peaks", _int, [_vp, _dp, _dp]),
+    ("xb_set_power_auto", _int, [_vp, _int, C.c_double]),
+    ("xb_last_power", _int, [_vp, _intp, _vp, _int, _intp]),
     ("xb_rsvd_dense", _int, [_vp, _int, _i64, _i64, _vp, _i64, _vp, _u64, _int, _int, _int,
                              _vp, _i64, _vp, _vp, _i64, _vp, _intp, _vp]),
     ("xb_rsvd_dense_dev", _int, [_vp, _int, _i64, _i64, _vp, _i64, _vp, _u64, _int, _int, _int,
@@ -121,14 +125,28 @@ class Context:
         _check(self.lib.xb_profile_enable(self.h, int(on)))
 
     def profile_read(self) -> dict:
-        out = np.zeros(4)
-        _check(self.lib.xb_profile_read(self.h, _ptr(out)))
-        return {"seconds": out[0], "launches": int(out[1]), "flops": out[2], "bytes": out[3]}
+        out = np.zeros(6)
+        _check(self.lib.xb_profile_read_ext(self.h, _ptr(out)))
+        kinds = {0: "dmma", 1: "tf32x3", 2: "ozaki_i8", 3: "spmm"}
+        return {"seconds": out[0], "launches": int(out[1]), "flops": out[2], "bytes": out[3],
+                "pipe_ops": out[4], "kind": kinds.get(int(out[5]))}
 
     def fp64_peaks(self):
         a, b = C.c_double(), C.c_double()
         _check(self.lib.xb_fp64_peaks(self.h, C.byref(a), C.byref(b)))
         return a.value, b.value
+
+    # -- power selection ------------------------------------------------------
+    def set_power_auto(self, q_max: int = 5, tau: float = 1e-6):
+        """Stopping-rule parameters for calls made with q = POWER_AUTO."""
+        _check(self.lib.xb_set_power_auto(self.h, int(q_max), float(tau)))
+
+    def last_power(self):
+        """(chosen q, nu sequence) of the last factorisation."""
+        q, cnt = C.c_int(0), C.c_int(0)
+        nus = np.zeros(64)
+        _check(self.lib.xb_last_power(self.h, C.byref(q), _ptr(nus), len(nus), C.byref(cnt)))
+        return q.value, [float(x) for x in nus[: min(cnt.value, len(nus))]]
 
     # -- full factorisation ---------------------------------------------------
     def rsvd_dense(self, a: np.ndarray, k: int, p: int, q: int, seed: int, omega=None):

@@ -98,6 +98,11 @@ int oz_slices();
 // Row / column slice exponents. wide (optional): set to 1 when some row
 // (column) has max |x| > 64 x its RMS (the slices would lose accuracy).
 // oz_col_exp scratch: 2 cols words when wide != nullptr, else cols.
+// Both exponent sets of A (and the range guard when wide != nullptr) in one
+// pass; scratch: oz_both_exp_scratch_bytes(rows, cols) bytes.
+size_t oz_both_exp_scratch_bytes(int64_t rows, int64_t cols);
+void oz_both_exp(const double* X, int64_t rows, int64_t cols, int64_t ldx, int32_t* erow,
+                 int32_t* ecol, void* scratch, int* wide, cudaStream_t st);
 void oz_row_exp(const double* X, int64_t rows, int64_t cols, int64_t ldx, int32_t* e, int* wide,
                 cudaStream_t st);
 void oz_col_exp(const double* X, int64_t rows, int64_t cols, int64_t ldx, int32_t* e,
@@ -163,6 +168,9 @@ void launch_householder_fallback(const double* X, int64_t ldx, int64_t rows, int
 // Deficient-column flags from R (l x l, ldr): |R_jj| <= eps * ||R||_F.
 // M (l x l, ld) := identity when *flag != 0
 void launch_identity_if(double* M, int64_t ld, int l, const int* flag, cudaStream_t st);
+void launch_identity(double* M, int64_t ld, int l, cudaStream_t st);
+// out (device) = ||M||_F over n contiguous doubles; M /= out when out > 0
+void launch_frob_normalise(double* M, int64_t n, double* out, cudaStream_t st);
 void launch_deficient(const double* R, int64_t ldr, int l, double eps, int* count, int* cols,
                       cudaStream_t st);
 

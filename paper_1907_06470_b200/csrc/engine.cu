@@ -50,15 +50,25 @@ struct xb_ctx {
   std::map<std::string, Buf> bufs;
   uint64_t gen = 0;  // bumped on entry to every ABI call
   std::vector<cudaEvent_t> events;
+  // power = "auto" (xb_set_power_auto / xb_last_power): the reference's
+  // stopping rule parameters and the last call's outcome
+  int auto_qmax = 5;
+  double auto_tau = 1e-6;
+  int last_q = -1;
+  std::vector<double> last_nus;
   // per-kernel profiling of the products on A (xb_profile_*)
   bool profiling = false;
+  // kind: 0 FP64 DMMA tile GEMM, 1 tcgen05 3xTF32 GEMM, 2 int8-slice
+  // (Ozaki) GEMM, 3 CSR SpMM; pipe_ops = tensor-pipe operations issued
+  // (multiply-adds x 2, padding included) for the tensor kinds, else 0
   struct ProfMark {
     cudaEvent_t b, e;
-    double flops, bytes;
+    double flops, bytes, pipe_ops;
+    int kind;
   };
   std::vector<ProfMark> prof_pending;
   std::vector<cudaEvent_t> prof_pool;
-  double prof_acc[4] = {0, 0, 0, 0};
+  double prof_acc[6] = {0, 0, 0, 0, 0, -1};
 
   cudaEvent_t prof_event() {
     if (!prof_pool.empty()) {
@@ -79,6 +89,8 @@ struct xb_ctx {
       prof_acc[1] += 1;
       prof_acc[2] += m.flops;
       prof_acc[3] += m.bytes;
+      prof_acc[4] += m.pipe_ops;
+      prof_acc[5] = std::max(prof_acc[5], (double)m.kind);
       prof_pool.push_back(m.b);
       prof_pool.push_back(m.e);
     }
@@ -360,7 +372,9 @@ void gemm_on_a(xb_ctx* c, bool ta, int64_t M, int64_t N, int64_t K, const AView&
   if (c->profiling) {
     XB_CUDA(cudaEventRecord(e, c->st));
     const double mn = (double)M * (double)K;  // A is M x K (NN) or K x M (TN)
-    c->prof_pending.push_back({b, e, 2.0 * mn * l, mn * a.esz()});
+    const bool tg = tgemm_supported(g);
+    c->prof_pending.push_back(
+        {b, e, 2.0 * mn * l, mn * a.esz(), (tg ? 3.0 : 1.0) * 2.0 * mn * N, tg ? 1 : 0});
   }
 }
 
@@ -433,7 +447,7 @@ void cholqr2(xb_ctx* c, const Small& s, const double* X, int64_t rows, double* T
 // fallback runs. The range-finder's final QR and the QR of B^T (whose Q
 // must be orthonormal to machine precision) use cholqr2.
 void cholqr1(xb_ctx* c, const Small& s, const double* X, int64_t rows, double* Q,
-             bool sharded = false) {
+             bool sharded = false, double* Rout = nullptr) {
   const int l = s.l, lp = s.lp;
   cudaStream_t st = c->st;
   int* flag = sharded ? s.shard_err : s.flag;
@@ -441,9 +455,46 @@ void cholqr1(xb_ctx* c, const Small& s, const double* X, int64_t rows, double* Q
   gram(c, s, X, rows, sharded);                                // G = X^T X
   launch_chol_inv(s.G, lp, l, 1e-8, s.R1, s.R1i, lp, flag, s.cw, st);
   gemm(c, false, rows, lp, lp, X, lp, s.R1i, lp, Q, lp, 2);    // Q = X R^-1
+  if (Rout)
+    XB_CUDA(cudaMemcpyAsync(Rout, s.R1, (size_t)lp * lp * sizeof(double),
+                            cudaMemcpyDeviceToDevice, st));
   if (sharded) return;
   double* hw = c->dbuf("hh_work", (size_t)2 * rows * l);
-  launch_householder_fallback(X, lp, rows, l, lp, Q, lp, s.Rs, lp, hw, s.flag, st);
+  launch_householder_fallback(X, lp, rows, l, lp, Q, lp, Rout ? Rout : s.Rs, lp, hw, s.flag, st);
+}
+
+// power = "auto" (pipeline.py:295-372). The reference watches the raw
+// products Y_q = (A A^T)^q A Omega: nu_q = ||Y_q||_F / sqrt(m l). Here every
+// product is re-orthonormalised, so the raw product is carried as a small
+// upper-triangular factor: Y_q(raw) = Y_q C_q e^{L_q}, with C_0 = I, and
+// after the QRs Y_q = Q R_q, Z = Q_z R_z:
+//     ||Y_q(raw)||_F = e^{L_q} ||R_q C_q||_F,
+//     C_{q+1} = R_z (R_q C_q) / ||R_q C_q||_F,  L_{q+1} = L_q + ln ||R_q C_q||_F
+// (the normalisation keeps C bounded; only nu ratios enter the rule).
+struct AutoPower {
+  bool on = false;
+  int lp = 0;
+  double* C = nullptr;   // lp x lp
+  double* M = nullptr;   // R_q C_q, normalised in place
+  double* Rq = nullptr;  // R of the current Y
+  double* Rz = nullptr;  // R of the current Z
+  double* nrm = nullptr; // device scalar ||R_q C_q||_F
+  double L = 0.0, scale = 1.0;
+  std::vector<double> nus;
+  double prev_rho = 1.0;
+};
+
+// nu of the current Y (R in a.Rq); returns ln nu
+double auto_nu(xb_ctx* c, AutoPower& a) {
+  gemm(c, false, a.lp, a.lp, a.lp, a.Rq, a.lp, a.C, a.lp, a.M, a.lp);
+  launch_frob_normalise(a.M, (int64_t)a.lp * a.lp, a.nrm, c->st);
+  double h = 0.0;
+  XB_CUDA(cudaMemcpyAsync(&h, a.nrm, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  XB_CUDA(cudaStreamSynchronize(c->st));
+  const double lognu = a.L + std::log(h);
+  a.nus.push_back(h > 0.0 ? std::exp(lognu) * a.scale : 0.0);
+  a.L = lognu;
+  return lognu;
 }
 
 struct RsvdOut {
@@ -458,7 +509,8 @@ void check_dims(int64_t m, int64_t n, int k, int p, int q) {
   XB_REQUIRE(m >= 1 && n >= 1, XB_ESHAPE, "empty matrix");
   XB_REQUIRE(k >= 1, XB_EVALUE, "rank must be at least 1, got " + std::to_string(k));
   XB_REQUIRE(p >= 0, XB_EVALUE, "oversample must be nonnegative, got " + std::to_string(p));
-  XB_REQUIRE(q >= 0, XB_EVALUE, "power must be nonnegative, got " + std::to_string(q));
+  XB_REQUIRE(q >= 0 || q == XB_POWER_AUTO, XB_EVALUE,
+             "power must be nonnegative, got " + std::to_string(q));
   XB_REQUIRE((int64_t)k + p <= std::min(m, n), XB_ESHAPE,
              "rank " + std::to_string(k) + " (+" + std::to_string(p) +
                  " oversampling) exceeds min(" + std::to_string(m) + ", " + std::to_string(n) +
@@ -511,7 +563,7 @@ void spmm_on_a(xb_ctx* c, const Csr& s, const double* X, double* Y, int lp, int 
     XB_CUDA(cudaEventRecord(e, c->st));
     // algorithmic bytes: 12 nnz + 8 (rows+1) + 8 l (cols_in + rows_out)
     const double bytes = 12.0 * s.nnz + 8.0 * (s.rows + 1) + 8.0 * l * (s.cols + s.rows);
-    c->prof_pending.push_back({b, e, 2.0 * s.nnz * l, bytes});
+    c->prof_pending.push_back({b, e, 2.0 * s.nnz * l, bytes, 0.0, 3});
   }
 }
 
@@ -532,7 +584,11 @@ void oz_prepare(xb_ctx* c, AOp& op, int64_t m, int64_t n) {
     return;
   }
   const double have = (double)free_b + (double)c->cached_bytes();
-  if (need + 2e9 > have) return;
+  static const bool trace = getenv("XB_TRACE") != nullptr;
+  if (need + 2e9 > have) {
+    if (trace) fprintf(stderr, "[xb] ozaki off: slices %.2f GB, free+cached %.2f GB\n", need / 1e9, have / 1e9);
+    return;
+  }
   OzA z;
   z.S = S;
   z.kpn = kpn;
@@ -542,16 +598,19 @@ void oz_prepare(xb_ctx* c, AOp& op, int64_t m, int64_t n) {
   z.erow = c->ibuf("oz_erow", m);
   z.ecol = c->ibuf("oz_ecol", n);
   int* wide = c->ibuf("oz_wide", 1);
-  auto* scr = static_cast<unsigned long long*>(c->buf("oz_scr", (size_t)2 * std::max(m, n) * 8));
+  void* scr = c->buf("oz_scr", oz_both_exp_scratch_bytes(m, n));
   const double* A = static_cast<const double*>(a.p);
   // exponents + dynamic-range guard first (one small read-back per call)
   XB_CUDA(cudaMemsetAsync(wide, 0, sizeof(int), c->st));
-  oz_row_exp(A, m, n, a.ld, z.erow, wide, c->st);
-  oz_col_exp(A, m, n, a.ld, z.ecol, scr, wide, c->st);
+  oz_both_exp(A, m, n, a.ld, z.erow, z.ecol, scr, wide, c->st);
   int hwide = 0;
   XB_CUDA(cudaMemcpyAsync(&hwide, wide, sizeof(int), cudaMemcpyDeviceToHost, c->st));
   XB_CUDA(cudaStreamSynchronize(c->st));
-  if (hwide) return;  // some row/column of A spans > 64x its RMS: DMMA keeps f64 accuracy
+  if (hwide) {  // some row/column of A spans > 64x its RMS: DMMA keeps f64 accuracy
+    if (trace) fprintf(stderr, "[xb] ozaki off: dynamic-range guard\n");
+    return;
+  }
+  if (trace) fprintf(stderr, "[xb] ozaki on: S=%d\n", S);
   z.rows = static_cast<int8_t*>(c->buf("oz_rows", (size_t)S * z.mp * kpn));
   z.colsT = static_cast<int8_t*>(c->buf("oz_colsT", (size_t)S * z.np * kpm));
   oz_slice_both(A, m, n, a.ld, z.erow, z.ecol, z.rows, z.mp, kpn, z.colsT, z.np, kpm, S, c->st);
@@ -582,7 +641,10 @@ void oz_product(xb_ctx* c, const OzA& z, bool tn, int64_t m, int64_t n, const do
   if (c->profiling) {
     XB_CUDA(cudaEventRecord(e, c->st));
     const double mn = (double)m * (double)n;
-    c->prof_pending.push_back({b, e, 2.0 * mn * l, mn * z.S});
+    // S (S + 1) / 2 int8 slice products over the padded tile grid
+    const double pairs = 0.5 * z.S * (z.S + 1);
+    const double ops = pairs * 2.0 * (double)round_up(Mo, 128) * (double)np * (double)kp;
+    c->prof_pending.push_back({b, e, 2.0 * mn * l, mn * z.S, ops, 2});
   }
 }
 
@@ -735,23 +797,68 @@ void rsvd_impl(xb_ctx* c, const AOp& op_in, int64_t m, int64_t n, const void* d_
   // (row-sharded: the m-side QRs sum their Grams over ranks; the n-side ones
   // run replicated on the all-reduced Z, identically on every rank)
   clk.enter(kOrtho);
-  if (q == 0)
+  const bool autoq = q == XB_POWER_AUTO;
+  const int qlim = autoq ? c->auto_qmax : q;
+  AutoPower ap;
+  if (autoq) {
+    ap.on = true;
+    ap.lp = lp;
+    const size_t ll = (size_t)lp * lp;
+    ap.C = c->dbuf("ap_C", ll);
+    ap.M = c->dbuf("ap_M", ll);
+    ap.Rq = c->dbuf("ap_Rq", ll);
+    ap.Rz = c->dbuf("ap_Rz", ll);
+    ap.nrm = c->dbuf("ap_nrm", 1);
+    launch_identity(ap.C, lp, lp, st);
+    ap.scale = 1.0 / std::sqrt((double)(op.comm ? op.m_global : m) * (double)l);
+  }
+  bool final_done = false, stop = false;
+  int chosen = 0;
+  double ln0 = 0.0, lnprev = 0.0;
+  if (qlim == 0) {
     cholqr2(c, s, Ym, m, Tm, Qm, Rf, sharded);
-  else
-    cholqr1(c, s, Ym, m, Qm, sharded);
-  for (int it = 0; it < q; ++it) {
+    final_done = true;
+  } else {
+    cholqr1(c, s, Ym, m, Qm, sharded, autoq ? ap.Rq : nullptr);
+  }
+  if (autoq) {
+    // the reference measures nu_0 even when q_max = 0 (R is then Rf)
+    if (final_done) ap.Rq = Rf;
+    ln0 = lnprev = auto_nu(c, ap);
+    if (!(ap.nus[0] > 0.0)) stop = true;  // zero sketch: nothing to sharpen
+  }
+  for (int it = 0; it < qlim && !stop; ++it) {
     clk.enter(kSketch);
     op_tn(c, op, m, n, Qm, Zn, lp, l);  // Z = A^T Q
     clk.enter(kOrtho);
-    cholqr1(c, s, Zn, n, Qn);
+    cholqr1(c, s, Zn, n, Qn, false, autoq ? ap.Rz : nullptr);
+    if (autoq) gemm(c, false, lp, lp, lp, ap.Rz, lp, ap.M, lp, ap.C, lp);  // C = R_z M
     clk.enter(kSketch);
     op_nn(c, op, m, n, Qn, Ym, lp, l);  // Y = A Qz
     clk.enter(kOrtho);
-    if (it == q - 1)
+    chosen = it + 1;
+    if (!autoq && it == q - 1) {
       cholqr2(c, s, Ym, m, Tm, Qm, Rf, sharded);
-    else
-      cholqr1(c, s, Ym, m, Qm, sharded);
+      final_done = true;
+    } else {
+      cholqr1(c, s, Ym, m, Qm, sharded, autoq ? ap.Rq : nullptr);
+      if (autoq) {
+        // stopping rule of pipeline.py:361-370
+        const double ln = auto_nu(c, ap);
+        if (ln < std::log(c->auto_tau) + ln0) {
+          stop = true;
+        } else {
+          const double rho = std::exp(ln - lnprev);
+          if (std::fabs(rho - ap.prev_rho) <= 0.01 * rho) stop = true;
+          ap.prev_rho = rho;
+        }
+        lnprev = ln;
+      }
+    }
   }
+  if (!final_done) cholqr2(c, s, Ym, m, Tm, Qm, Rf, sharded);  // the range basis: CholQR2
+  c->last_q = autoq ? chosen : q;
+  c->last_nus = ap.nus;
   // deficient columns of the final range-finder QR (kernels.py:327-331)
   launch_deficient(Rf, lp, l, a.f32 ? (double)FLT_EPSILON : DBL_EPSILON, defc, defc + 1, st);
 
@@ -911,7 +1018,9 @@ void tn_accumulate(xb_ctx* c, const AView& t, int64_t rows, int64_t n, const dou
   if (c->profiling) {
     XB_CUDA(cudaEventRecord(e, c->st));
     const double mn = (double)rows * n;
-    c->prof_pending.push_back({b, e, 2.0 * mn * l, mn * t.esz()});
+    const bool tg = tgemm_supported(g);
+    c->prof_pending.push_back(
+        {b, e, 2.0 * mn * l, mn * t.esz(), (tg ? 3.0 : 1.0) * 2.0 * mn * lp, tg ? 1 : 0});
   }
 }
 
@@ -926,6 +1035,7 @@ void rsvd_stream(xb_ctx* c, const void* hostA, int64_t host_lda, bool f32, int64
                  int64_t tile_rows, uint64_t seed, int k, int p, int q, const RsvdOut& out,
                  int32_t* deficient, int* ndeficient, double* stage_seconds) {
   check_dims(m, n, k, p, q);
+  XB_REQUIRE(q >= 0, XB_EUNSUPPORTED, "power='auto' is not built for the out-of-core streamer");
   const int l = k + p;
   const int lp = (int)round_up(l, 8);
   const int kp = (int)round_up(k, 2);
@@ -1162,6 +1272,26 @@ int64_t xb_launch_count(const xb_ctx* c) { return c ? c->launches : 0; }
 
 void* xb_compute_stream(xb_ctx* c) { return c ? static_cast<void*>(c->st) : nullptr; }
 
+int xb_set_power_auto(xb_ctx* c, int q_max, double tau) {
+  return guarded([&] {
+    XB_REQUIRE(c, XB_EVALUE, "null context");
+    XB_REQUIRE(q_max >= 0, XB_EVALUE, "q_max must be nonnegative, got " + std::to_string(q_max));
+    XB_REQUIRE(tau > 0.0, XB_EVALUE, "tau must be positive");
+    c->auto_qmax = q_max;
+    c->auto_tau = tau;
+  });
+}
+
+int xb_last_power(xb_ctx* c, int* chosen_q, double* nus, int cap, int* count) {
+  return guarded([&] {
+    XB_REQUIRE(c, XB_EVALUE, "null context");
+    if (chosen_q) *chosen_q = c->last_q;
+    const int nn = (int)c->last_nus.size();
+    if (count) *count = nn;
+    for (int i = 0; nus && i < nn && i < cap; ++i) nus[i] = c->last_nus[i];
+  });
+}
+
 int xb_profile_enable(xb_ctx* c, int on) {
   return guarded([&] {
     XB_REQUIRE(c, XB_EVALUE, "null context");
@@ -1174,9 +1304,19 @@ int xb_profile_read(xb_ctx* c, double* out4) {
     XB_REQUIRE(c && out4, XB_EVALUE, "null argument");
     XB_CUDA(cudaStreamSynchronize(c->st));
     c->prof_collect();
-    for (int i = 0; i < 4; ++i) {
-      out4[i] = c->prof_acc[i];
-      c->prof_acc[i] = 0.0;
+    for (int i = 0; i < 4; ++i) out4[i] = c->prof_acc[i];
+    for (int i = 0; i < 6; ++i) c->prof_acc[i] = i == 5 ? -1.0 : 0.0;
+  });
+}
+
+int xb_profile_read_ext(xb_ctx* c, double* out6) {
+  return guarded([&] {
+    XB_REQUIRE(c && out6, XB_EVALUE, "null argument");
+    XB_CUDA(cudaStreamSynchronize(c->st));
+    c->prof_collect();
+    for (int i = 0; i < 6; ++i) {
+      out6[i] = c->prof_acc[i];
+      c->prof_acc[i] = i == 5 ? -1.0 : 0.0;
     }
   });
 }

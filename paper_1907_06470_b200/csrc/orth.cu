@@ -220,7 +220,53 @@ __global__ void identity_if_kernel(double* __restrict__ M, int64_t ld, int l, co
   }
 }
 
+__global__ void identity_kernel(double* __restrict__ M, int64_t ld, int l) {
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)l * l;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx / l, c = idx - i * l;
+    M[i * ld + c] = (i == c) ? 1.0 : 0.0;
+  }
+}
+
+// out = ||M||_F (fixed-order block reduction), then M /= out when out > 0
+__global__ void __launch_bounds__(1024) frob_normalise_kernel(double* __restrict__ M, int64_t n,
+                                                             double* __restrict__ out) {
+  __shared__ double part[32];
+  __shared__ double nrm;
+  double ss = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) ss = fma(M[i], M[i], ss);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = (threadIdx.x < (blockDim.x >> 5)) ? part[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) {
+      nrm = sqrt(v);
+      *out = nrm;
+    }
+  }
+  __syncthreads();
+  if (nrm > 0.0) {
+    const double r = 1.0 / nrm;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) M[i] *= r;
+  }
+}
+
 }  // namespace
+
+void launch_identity(double* M, int64_t ld, int l, cudaStream_t st) {
+  identity_kernel<<<(unsigned)std::min<int64_t>(ceil_div((int64_t)l * l, 256), 1024), 256, 0, st>>>(
+      M, ld, l);
+  check_launch("identity");
+}
+
+void launch_frob_normalise(double* M, int64_t n, double* out, cudaStream_t st) {
+  frob_normalise_kernel<<<1, 1024, 0, st>>>(M, n, out);
+  check_launch("frob_normalise");
+}
 
 void launch_identity_if(double* M, int64_t ld, int l, const int* flag, cudaStream_t st) {
   identity_if_kernel<<<(unsigned)std::min<int64_t>(ceil_div((int64_t)l * l, 256), 1024), 256, 0, st>>>(

@@ -372,6 +372,94 @@ __global__ void col_exp_kernel(const unsigned long long* __restrict__ cmax,
   if (wide && css && m * m > kOzRange * kOzRange * (css[c] / (double)rows)) atomicOr(wide, 1);
 }
 
+// Row AND column max |x| / sum of squares of A in ONE pass (the slicing
+// pass needs both exponent sets before it starts). Block tile 512 rows x 256
+// columns: each warp reads 2 KB of a row per step (8 coalesced 256-byte
+// loads, two rows in flight), reduces the row partial by shuffle, and keeps
+// 8 column partials per lane that the block combines in shared memory.
+// Partials go to scratch without atomics — per (row, column tile) and per
+// (row tile, column) — and two small kernels finish them in a fixed order.
+constexpr int RC_ROWS = 512, RC_COLS = 256;
+
+__global__ void __launch_bounds__(256)
+    rc_stats_kernel(const double* __restrict__ X, int64_t rows, int64_t cols, int64_t ldx,
+                    double2* __restrict__ rpart, double2* __restrict__ cpart) {
+  __shared__ double sm[8][RC_COLS + 1], sq[8][RC_COLS + 1];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t ct = blockIdx.x, rt = blockIdx.y;
+  const int64_t nct = gridDim.x;
+  const int64_t c0 = ct * RC_COLS, r0 = rt * RC_ROWS;
+  const int64_t rend = min(rows, r0 + RC_ROWS);
+  double cm[8], cs[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) cm[j] = cs[j] = 0.0;
+  bool colok[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) colok[j] = c0 + tx + 32 * j < cols;
+  for (int64_t r = r0 + ty; r < rend; r += 16) {
+    double v[2][8];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int64_t rr = r + 8 * u;
+      const double* xr = X + rr * ldx + c0 + tx;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[u][j] = (rr < rend && colok[j]) ? __ldcs(xr + 32 * j) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      double m = 0.0, ss = 0.0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const double a = fabs(v[u][j]);
+        m = fmax(m, a);
+        ss = fma(v[u][j], v[u][j], ss);
+        cm[j] = fmax(cm[j], a);
+        cs[j] = fma(v[u][j], v[u][j], cs[j]);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+        ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      }
+      const int64_t rr = r + 8 * u;
+      if (tx == 0 && rr < rend) rpart[rr * nct + ct] = make_double2(m, ss);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    sm[ty][tx + 32 * j] = cm[j];
+    sq[ty][tx + 32 * j] = cs[j];
+  }
+  __syncthreads();
+  const int64_t c = c0 + threadIdx.x;
+  if (c < cols) {
+    double m = 0.0, ss = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      m = fmax(m, sm[w][threadIdx.x]);
+      ss += sq[w][threadIdx.x];
+    }
+    cpart[rt * cols + c] = make_double2(m, ss);
+  }
+}
+
+// e[i] from the partials part[i * stride + t * tstep], t < parts; `len` =
+// elements per row/column (the range guard's mean square)
+__global__ void rc_finish_kernel(const double2* __restrict__ part, int64_t count, int64_t parts,
+                                 int64_t stride, int64_t tstep, int64_t len,
+                                 int32_t* __restrict__ e, int* __restrict__ wide) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  double m = 0.0, ss = 0.0;
+  for (int64_t t = 0; t < parts; ++t) {
+    const double2 p = part[i * stride + t * tstep];
+    m = fmax(m, p.x);
+    ss += p.y;
+  }
+  e[i] = slice_exp(m);
+  if (wide && m * m > kOzRange * kOzRange * (ss / (double)len)) atomicOr(wide, 1);
+}
+
 template <int S>
 __device__ __forceinline__ void slice7(double x, int e, int8_t* out, int64_t plane) {
   int a[S];
@@ -384,57 +472,72 @@ __device__ __forceinline__ void slice7(double x, int e, int8_t* out, int64_t pla
 // PR = the row-scaled slices of A (rows of A, K = columns; for Y = A X) and
 // PC = the column-scaled slices of A^T (columns of A, K = rows; for
 // Z = A^T Q), both in the interleaved tile layout (il_off<128>). Either may be
-// null. A 32 x 32 tile of A is one k-block of either layout; each thread packs
-// 4 consecutive K bytes.
+// null. Block tile = 128 rows x 32 columns of A (32 KB in shared memory):
+// that is exactly one 4 KB interleaved tile per slice of PR, and four 1 KB
+// contiguous runs per slice of PC, so every warp store is a contiguous
+// 128-byte run (thread t writes the t-th 4-byte word of the run).
 template <int S>
 __global__ void __launch_bounds__(256)
     slice_both_kernel(const double* __restrict__ X, int64_t m, int64_t n, int64_t ldx,
                       const int32_t* __restrict__ er, const int32_t* __restrict__ ec,
                       int8_t* __restrict__ PR, int64_t mp, int64_t kpn, int8_t* __restrict__ PC,
                       int64_t np, int64_t kpm) {
-  __shared__ double tile[32][33];
-  __shared__ int ser[32], sec[32];
-  const int64_t r0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
-  const int tx = threadIdx.x, ty = threadIdx.y, t = ty * 32 + tx;
-  for (int i = ty; i < 32; i += 8) {
+  __shared__ double tile[128][33];
+  __shared__ int ser[128], sec[32];
+  const int64_t r0 = (int64_t)blockIdx.x * 128, c0 = (int64_t)blockIdx.y * 32;
+  const int t = threadIdx.x, tx = t & 31, ty = t >> 5;
+  for (int i = ty; i < 128; i += 8) {
     const int64_t r = r0 + i, c = c0 + tx;
-    tile[i][tx] = (r < m && c < n) ? X[r * ldx + c] : 0.0;
+    tile[i][tx] = (r < m && c < n) ? __ldcs(X + r * ldx + c) : 0.0;
   }
-  if (ty == 0) {
-    ser[tx] = (er && r0 + tx < m) ? er[r0 + tx] : 0;
-    sec[tx] = (ec && c0 + tx < n) ? ec[c0 + tx] : 0;
-  }
+  if (t < 128) ser[t] = (er && r0 + t < m) ? er[r0 + t] : 0;
+  if (t < 32) sec[t] = (ec && c0 + t < n) ? ec[c0 + t] : 0;
   __syncthreads();
-  const int a = t >> 3, b4 = (t & 7) * 4;
-  if (PR && r0 < mp && c0 < kpn) {  // row layout: (row r0+a, k = c0+b4..+3)
-    uint32_t w[S];
+  if (PR && c0 < kpn) {
+    // the (k-block c0/32, row tile r0/128) interleaved tile, word by word
+    int8_t* base = PR + ((c0 >> 5) * (mp / 128) + (r0 >> 7)) * (int64_t)(S * 4096);
 #pragma unroll
-    for (int q = 0; q < S; ++q) w[q] = 0;
+    for (int u = 0; u < 4; ++u) {
+      const int w = t + 256 * u;
+      const int rr = ((w >> 6) << 3) | ((w >> 2) & 7);
+      const int kk = ((w >> 5) & 1) * 16 + (w & 3) * 4;
+      uint32_t word[S];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      int d[S];
-      slice_digits<S>(tile[a][b4 + j], ser[a], d);
+      for (int q = 0; q < S; ++q) word[q] = 0;
 #pragma unroll
-      for (int q = 0; q < S; ++q) w[q] |= (uint32_t)(uint8_t)(int8_t)d[q] << (8 * j);
+      for (int j = 0; j < 4; ++j) {
+        int d[S];
+        slice_digits<S>(tile[rr][kk + j], ser[rr], d);
+#pragma unroll
+        for (int q = 0; q < S; ++q) word[q] |= (uint32_t)(uint8_t)(int8_t)d[q] << (8 * j);
+      }
+#pragma unroll
+      for (int q = 0; q < S; ++q) reinterpret_cast<uint32_t*>(base + q * 4096)[w] = word[q];
     }
-#pragma unroll
-    for (int q = 0; q < S; ++q)
-      *reinterpret_cast<uint32_t*>(PR + il_off<128>(r0 + a, c0 + b4, q, S, mp)) = w[q];
   }
-  if (PC && c0 < np && r0 < kpm) {  // column layout: (row c0+a of A^T, k = r0+b4..+3)
-    uint32_t w[S];
+  if (PC && c0 < np) {
+    // rows c0..c0+31 of A^T (a 32-row slab of row tile c0/128), k-blocks r0/32 + kb
+    const int rr0 = (int)(c0 & 127);
+    const int cc = ((t >> 6) << 3) | ((t >> 2) & 7);  // 0..31: row within the slab
+    const int kk = ((t >> 5) & 1) * 16 + (t & 3) * 4;
 #pragma unroll
-    for (int q = 0; q < S; ++q) w[q] = 0;
+    for (int kb = 0; kb < 4; ++kb) {
+      const int64_t kblk = (r0 >> 5) + kb;
+      if (kblk * 32 >= kpm) break;
+      int8_t* base = PC + (kblk * (np / 128) + (c0 >> 7)) * (int64_t)(S * 4096) + (rr0 >> 3) * 256;
+      uint32_t word[S];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      int d[S];
-      slice_digits<S>(tile[b4 + j][a], sec[a], d);
+      for (int q = 0; q < S; ++q) word[q] = 0;
 #pragma unroll
-      for (int q = 0; q < S; ++q) w[q] |= (uint32_t)(uint8_t)(int8_t)d[q] << (8 * j);
+      for (int j = 0; j < 4; ++j) {
+        int d[S];
+        slice_digits<S>(tile[kb * 32 + kk + j][cc], sec[cc], d);
+#pragma unroll
+        for (int q = 0; q < S; ++q) word[q] |= (uint32_t)(uint8_t)(int8_t)d[q] << (8 * j);
+      }
+#pragma unroll
+      for (int q = 0; q < S; ++q) reinterpret_cast<uint32_t*>(base + q * 4096)[t] = word[q];
     }
-#pragma unroll
-    for (int q = 0; q < S; ++q)
-      *reinterpret_cast<uint32_t*>(PC + il_off<128>(c0 + a, r0 + b4, q, S, np)) = w[q];
   }
 }
 
@@ -531,6 +634,29 @@ void oz_col_exp(const double* X, int64_t rows, int64_t cols, int64_t ldx, int32_
   check_launch("col_exp");
 }
 
+size_t oz_both_exp_scratch_bytes(int64_t rows, int64_t cols) {
+  const int64_t nct = ceil_div(cols, RC_COLS), nrt = ceil_div(rows, RC_ROWS);
+  return (size_t)(rows * nct + nrt * cols) * sizeof(double2);
+}
+
+void oz_both_exp(const double* X, int64_t rows, int64_t cols, int64_t ldx, int32_t* erow,
+                 int32_t* ecol, void* scratch, int* wide, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return;
+  const int64_t nct = ceil_div(cols, RC_COLS), nrt = ceil_div(rows, RC_ROWS);
+  XB_REQUIRE(nrt < 65536, XB_EUNSUPPORTED, "oz_both_exp: more than 2^25 rows");
+  double2* rpart = static_cast<double2*>(scratch);
+  double2* cpart = rpart + rows * nct;
+  rc_stats_kernel<<<dim3((unsigned)nct, (unsigned)nrt), 256, 0, st>>>(X, rows, cols, ldx, rpart,
+                                                                       cpart);
+  check_launch("rc_stats");
+  rc_finish_kernel<<<(unsigned)ceil_div(rows, 256), 256, 0, st>>>(rpart, rows, nct, nct, 1, cols,
+                                                                  erow, wide);
+  check_launch("rc_finish_rows");
+  rc_finish_kernel<<<(unsigned)ceil_div(cols, 256), 256, 0, st>>>(cpart, cols, nrt, 1, cols, rows,
+                                                                  ecol, wide);
+  check_launch("rc_finish_cols");
+}
+
 #define OZ_DISPATCH(S, CALL) \
   switch (S) {               \
     case 3: CALL(3); break;  \
@@ -556,9 +682,9 @@ void oz_slice_both(const double* X, int64_t m, int64_t n, int64_t ldx, const int
   XB_REQUIRE(mp % OBM == 0 && np % OBM == 0 && kpn % 32 == 0 && kpm % 32 == 0 && mp >= kpm &&
                  np >= kpn && np / 32 < 65536,
              XB_EUNSUPPORTED, "oz_slice_both: layout");
-  dim3 grid((unsigned)(mp / 32), (unsigned)(np / 32));
+  dim3 grid((unsigned)(mp / 128), (unsigned)(np / 32));
 #define OZ_SB(SS) \
-  slice_both_kernel<SS><<<grid, dim3(32, 8), 0, st>>>(X, m, n, ldx, er, ec, PR, mp, kpn, PC, np, kpm)
+  slice_both_kernel<SS><<<grid, 256, 0, st>>>(X, m, n, ldx, er, ec, PR, mp, kpn, PC, np, kpm)
   OZ_DISPATCH(S, OZ_SB)
 #undef OZ_SB
   check_launch("slice_both");

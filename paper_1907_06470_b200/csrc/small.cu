@@ -43,18 +43,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(16) double sm[];
   __shared__ double diag0[1024];
   __shared__ double pivs[1024];
-  __shared__ double tmp[1024];
   double* W = use_smem ? sm : gw;
-  // odd row stride: the inverse reads W by columns (an even stride of 120
-  // doubles put 16 lanes on one bank pair)
+  // odd row stride (conflict-free column reads)
   const int64_t lw = l | 1;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  // load the upper triangle (row-major, stride l)
+  // load the upper triangle (row-major, stride l); the strictly lower part
+  // holds E = L^-1 (unit diagonal implied), zero at the start
   for (int i = warp; i < l; i += kWarps)
     for (int c = lane; c < l; c += 32) W[(int64_t)i * lw + c] = (c >= i) ? G[(int64_t)i * ldg + c] : 0.0;
   for (int j = tid; j < l; j += kThreads) diag0[j] = G[(int64_t)j * ldg + j];
   __syncthreads();
-  // Cholesky: unscaled right-looking elimination, one barrier per column.
+  // Symmetric elimination G = L D L^T, one barrier per column. Row i > j of
+  // the trailing block loses f = W[j][i] / d_j times row j in its upper part
+  // (columns >= i) and, in the same step, E = L^-1 gets the same row
+  // operation in its lower part (columns <= j < i) — the two never overlap,
+  // so the triangular inverse costs no extra pass or barrier:
+  // R = D^-1/2 W, R^-1 = E^T D^-1/2.
   bool failed = false;
   for (int j = 0; j < l; ++j) {
     const double piv = W[(int64_t)j * lw + j];
@@ -68,41 +72,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       const double f = rowj[i] * inv;
       double* rowi = W + (int64_t)i * lw;
       for (int c = i + lane; c < l; c += 32) rowi[c] -= f * rowj[c];
+      for (int c = lane; c < j; c += 32) rowi[c] -= f * rowj[c];
+      if (lane == 0) rowi[j] = -f;
     }
     __syncthreads();
   }
   if (failed && tid == 0) *flag = 1;
-  // scale rows: R[j][c] = W[j][c] / sqrt(piv_j)
-  for (int j = warp; j < l; j += kWarps) {
-    const double rs = 1.0 / sqrt(pivs[j]);
+  // R[j][c] = W[j][c] / sqrt(d_j) (c >= j); R^-1[a][b] = E[b][a] / sqrt(d_b)
+  for (int i = warp; i < l; i += kWarps) {
+    const double rs = 1.0 / sqrt(pivs[i]);
     for (int c = lane; c < l; c += 32) {
-      const double v = (c >= j) ? W[(int64_t)j * lw + c] * rs : 0.0;
-      W[(int64_t)j * lw + c] = v;
-      R[(int64_t)j * ldr + c] = v;
+      R[(int64_t)i * ldr + c] = (c >= i) ? W[(int64_t)i * lw + c] * rs : 0.0;
+      double e = 0.0;
+      if (c > i) e = W[(int64_t)c * lw + i] / sqrt(pivs[c]);
+      else if (c == i) e = rs;
+      Rinv[(int64_t)i * ldr + c] = e;
     }
   }
-  __syncthreads();
-  for (int j = tid; j < l; j += kThreads) pivs[j] = W[(int64_t)j * lw + j];  // R's diagonal
-  __syncthreads();
-  // In-place upper-triangular inverse, column by column (dtrti2 order):
-  // X[0:j, j] = -X[0:j, 0:j] R[0:j, j] / R[j][j], X[j][j] = 1 / R[j][j].
-  // Column j reads only X[:, <j] and R[<j, j], so W[j][j] may be replaced
-  // in the same step.
-  for (int j = 0; j < l; ++j) {
-    for (int i = warp; i < j; i += kWarps) {
-      double acc = 0.0;
-      for (int p = i + lane; p < j; p += 32) acc += W[(int64_t)i * lw + p] * W[(int64_t)p * lw + j];
-      acc = warp_sum32(acc);
-      if (lane == 0) tmp[i] = acc;
-    }
-    __syncthreads();
-    const double ajj = 1.0 / pivs[j];
-    for (int i = tid; i < j; i += kThreads) W[(int64_t)i * lw + j] = -tmp[i] * ajj;
-    if (tid == 0) W[(int64_t)j * lw + j] = ajj;
-    __syncthreads();
-  }
-  for (int i = warp; i < l; i += kWarps)
-    for (int c = lane; c < l; c += 32) Rinv[(int64_t)i * ldr + c] = (c >= i) ? W[(int64_t)i * lw + c] : 0.0;
 }
 
 // ---------------------------------------------------------------------------

@@ -10,11 +10,13 @@
 // summation order — deterministic, no fp atomics (SURVEY §7 "do not fuse
 // cfg3's sparse pair").
 //
-// spmm_kernel: one warp per output row; lanes own the sketch columns
-// (l <= 32*NC), the row's (col, val) entries are fetched 32 at a time by the
-// warp and broadcast by shuffle, and every X row read is a coalesced
-// 8*l-byte burst. HBM/L2-bound: algorithmic bytes per launch are
-// 12*nnz + 8*(rows+1) + 8*l*(cols_in + rows_out).
+// spmm_kernel: one warp per output row gathering whole l-wide X rows with
+// 16-byte loads. The gathered rows are nnz * l * 8 bytes — 19.2 GB per cfg3
+// product, 16x A's own bytes — so the kernel is bound by gather traffic from
+// L2/HBM; algorithmic (compulsory) bytes per launch:
+// 12*nnz + 8*(rows+1) + 8*l*(cols_in + rows_out). Column chunks sized for
+// L2 residency were measured slower (re-reading A per chunk, and 64-byte
+// row segments of a 960-byte-stride Q do not pack into L2 lines).
 #include <algorithm>
 
 #include "common.cuh"
@@ -22,7 +24,12 @@
 namespace xb {
 namespace {
 
-template <int NC>
+// Y = A X, one warp per output row. Lane t owns columns VEC t + 32 VEC h
+// (h < NCH): every nonzero gathers its whole l-wide X row as NCH coalesced
+// 8- or 16-byte loads per lane. The row's (col, val) pairs stream in 32 at a
+// time (evict-first: A is read once) and are broadcast by shuffle; each sum
+// runs in the row's column order (deterministic, no atomics).
+template <int NCH, int VEC>
 __global__ void __launch_bounds__(256)
     spmm_kernel(int64_t rows, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
                 const double* __restrict__ val, const double* __restrict__ X, int64_t ldx,
@@ -31,36 +38,49 @@ __global__ void __launch_bounds__(256)
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t i = warp; i < rows; i += nwarps) {
-    double acc[NC];
+    double acc[NCH][VEC];
 #pragma unroll
-    for (int c = 0; c < NC; ++c) acc[c] = 0.0;
-    const int64_t e0 = rowptr[i], e1 = rowptr[i + 1];
+    for (int h = 0; h < NCH; ++h)
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) acc[h][v] = 0.0;
+    const int64_t e0 = __ldg(rowptr + i), e1 = __ldg(rowptr + i + 1);
     for (int64_t base = e0; base < e1; base += 32) {
       const int64_t e = base + lane;
       int32_t cj = 0;
       double vj = 0.0;
       if (e < e1) {
-        cj = __ldg(col + e);
-        vj = __ldg(val + e);
+        cj = __ldcs(col + e);
+        vj = __ldcs(val + e);
       }
       const int cnt = (e1 - base) < 32 ? (int)(e1 - base) : 32;
 #pragma unroll 4
       for (int t = 0; t < cnt; ++t) {
         const int64_t j = __shfl_sync(0xffffffffu, cj, t);
-        const double v = __shfl_sync(0xffffffffu, vj, t);
-        const double* xr = X + j * ldx;
+        const double a = __shfl_sync(0xffffffffu, vj, t);
+        const double* xr = X + j * ldx + VEC * lane;
 #pragma unroll
-        for (int c = 0; c < NC; ++c) {
-          const int cc = lane + 32 * c;
-          if (cc < l) acc[c] = fma(v, __ldg(xr + cc), acc[c]);
+        for (int h = 0; h < NCH; ++h) {
+          if (VEC * lane + 32 * VEC * h < l) {
+            if (VEC == 2) {
+              const double2 x = __ldg(reinterpret_cast<const double2*>(xr + 64 * h));
+              acc[h][0] = fma(a, x.x, acc[h][0]);
+              acc[h][VEC - 1] = fma(a, x.y, acc[h][VEC - 1]);
+            } else {
+              acc[h][0] = fma(a, __ldg(xr + 32 * h), acc[h][0]);
+            }
+          }
         }
       }
     }
-    double* yr = Y + i * ldy;
+    double* yr = Y + i * ldy + VEC * lane;
 #pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      const int cc = lane + 32 * c;
-      if (cc < l) yr[cc] = acc[c];
+    for (int h = 0; h < NCH; ++h) {
+      if (VEC * lane + 32 * VEC * h < l) {
+        if (VEC == 2)
+          __stcs(reinterpret_cast<double2*>(yr + 64 * h), make_double2(acc[h][0], acc[h][VEC - 1]));
+        else
+          __stcs(yr + 32 * h, acc[h][0]);
+      }
     }
   }
 }
@@ -158,26 +178,70 @@ __global__ void col_scatter_kernel(const int64_t* __restrict__ rowptr, int64_t m
   }
 }
 
-// Order each column segment by row (insertion sort; segments are short:
-// cfg3 averages 100 entries), making A^T's CSR — and every SpMM^T sum —
-// independent of the scatter's atomic order.
-__global__ void segment_sort_kernel(const int64_t* __restrict__ tptr, int64_t n,
-                                    int32_t* __restrict__ trow, double* __restrict__ tval) {
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
-       j += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = tptr[j], e = tptr[j + 1];
-    for (int64_t x = b + 1; x < e; ++x) {
-      const int32_t r = trow[x];
-      const double v = tval[x];
-      int64_t y = x - 1;
-      while (y >= b && trow[y] > r) {
-        trow[y + 1] = trow[y];
-        tval[y + 1] = tval[y];
-        --y;
+// Order each column segment by row, making A^T's CSR — and every SpMM^T
+// sum — independent of the scatter's atomic order. One warp per segment:
+// segments of up to 32 * SEG_K entries sit in registers (cfg3 averages 100)
+// and every entry's final slot is its rank, the number of entries with a
+// smaller row (rows are unique within a column); longer segments fall back
+// to an in-place insertion sort by one lane.
+constexpr int SEG_K = 8;
+
+__global__ void __launch_bounds__(256)
+    segment_sort_kernel(const int64_t* __restrict__ tptr, int64_t n, int32_t* __restrict__ trow,
+                        double* __restrict__ tval) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t j = warp; j < n; j += nwarps) {
+    const int64_t b = tptr[j], len = tptr[j + 1] - b;
+    if (len <= 1) continue;
+    if (len <= 32 * SEG_K) {
+      const int kc = (int)((len + 31) >> 5);
+      int32_t r[SEG_K];
+      double v[SEG_K];
+#pragma unroll
+      for (int k = 0; k < SEG_K; ++k) {
+        const int64_t e = lane + 32 * k;
+        r[k] = (k < kc && e < len) ? trow[b + e] : INT32_MAX;
+        v[k] = (k < kc && e < len) ? tval[b + e] : 0.0;
       }
-      trow[y + 1] = r;
-      tval[y + 1] = v;
+      int rank[SEG_K];
+#pragma unroll
+      for (int k = 0; k < SEG_K; ++k) rank[k] = 0;
+      for (int k2 = 0; k2 < kc; ++k2) {
+        int32_t mine = 0;
+#pragma unroll
+        for (int k = 0; k < SEG_K; ++k)
+          if (k == k2) mine = r[k];
+        for (int s = 0; s < 32; ++s) {
+          const int32_t o = __shfl_sync(0xffffffffu, mine, s);
+#pragma unroll
+          for (int k = 0; k < SEG_K; ++k) rank[k] += (o < r[k]) ? 1 : 0;
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < SEG_K; ++k) {
+        if (k < kc && lane + 32 * k < len) {
+          trow[b + rank[k]] = r[k];
+          tval[b + rank[k]] = v[k];
+        }
+      }
+    } else if (lane == 0) {
+      for (int64_t x = b + 1; x < b + len; ++x) {
+        const int32_t rr = trow[x];
+        const double vv = tval[x];
+        int64_t y = x - 1;
+        while (y >= b && trow[y] > rr) {
+          trow[y + 1] = trow[y];
+          tval[y + 1] = tval[y];
+          --y;
+        }
+        trow[y + 1] = rr;
+        tval[y + 1] = vv;
+      }
     }
+    __syncwarp();
   }
 }
 
@@ -189,22 +253,33 @@ int blocks_for(int64_t work, int per_block) {
 
 void launch_spmm(const Csr& a, const double* X, int64_t ldx, double* Y, int64_t ldy, int l,
                  cudaStream_t st) {
-  if (a.rows <= 0) return;
-  const int warps_per_block = 8;
-  const int blocks = blocks_for(a.rows, warps_per_block);
-  const int nc = (l + 31) / 32;
-#define XB_SPMM(NC)                                                                          \
-  spmm_kernel<NC><<<blocks, 256, 0, st>>>(a.rows, a.rowptr, a.col, a.val, X, ldx, Y, ldy, l); \
-  break;
-  switch (nc) {
-    case 1: XB_SPMM(1)
-    case 2: XB_SPMM(2)
-    case 3: XB_SPMM(3)
-    case 4: XB_SPMM(4)
-    case 5: case 6: case 7: case 8: XB_SPMM(8)
-    default:
-      XB_REQUIRE(nc <= 18, XB_EUNSUPPORTED, "spmm: l > 576");
-      XB_SPMM(18)
+  if (a.rows <= 0 || l <= 0) return;
+  XB_REQUIRE(l <= 576, XB_EUNSUPPORTED, "spmm: l > 576");
+  // 16-byte loads when every row of X and Y starts 16-byte aligned and l is even
+  const bool vec = (ldx % 2 == 0) && (ldy % 2 == 0) && (l % 2 == 0) &&
+                   (reinterpret_cast<uintptr_t>(X) % 16 == 0) &&
+                   (reinterpret_cast<uintptr_t>(Y) % 16 == 0);
+  const int blocks = blocks_for(a.rows, 8);
+#define XB_SPMM(NCH, VEC)                                                                    \
+  spmm_kernel<NCH, VEC><<<blocks, 256, 0, st>>>(a.rows, a.rowptr, a.col, a.val, X, ldx, Y, ldy, \
+                                                l)
+  if (vec) {
+    switch ((l + 63) / 64) {
+      case 1: XB_SPMM(1, 2); break;
+      case 2: XB_SPMM(2, 2); break;
+      case 3: XB_SPMM(3, 2); break;
+      case 4: XB_SPMM(4, 2); break;
+      default: XB_SPMM(9, 2); break;
+    }
+  } else {
+    switch ((l + 31) / 32) {
+      case 1: XB_SPMM(1, 1); break;
+      case 2: XB_SPMM(2, 1); break;
+      case 3: XB_SPMM(3, 1); break;
+      case 4: XB_SPMM(4, 1); break;
+      case 5: case 6: case 7: case 8: XB_SPMM(8, 1); break;
+      default: XB_SPMM(18, 1); break;
+    }
   }
 #undef XB_SPMM
   check_launch("spmm");
@@ -235,7 +310,7 @@ void launch_csr_transpose(const Csr& a, int64_t* tptr, int32_t* trow, double* tv
     col_scatter_kernel<<<blocks_for(a.rows, 8), 256, 0, st>>>(a.rowptr, a.rows, a.col, a.val, tptr,
                                                               scratch, trow, tval);
     check_launch("col_scatter");
-    segment_sort_kernel<<<blocks_for(n, 128), 128, 0, st>>>(tptr, n, trow, tval);
+    segment_sort_kernel<<<blocks_for(n, 8), 256, 0, st>>>(tptr, n, trow, tval);
     check_launch("segment_sort");
   }
 }

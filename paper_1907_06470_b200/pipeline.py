@@ -14,8 +14,13 @@ every product (the north star; the reference's shipped driver does not,
 pipeline.py:321-371 — SURVEY.md F4), so results match the "xsvd-reorth"
 oracle. Stage times are device-timed per STAGE_NAMES key.
 
-Out of scope (fail loudly): power="auto" (auto_select_q), gram_path=True,
-and the store-backed durable plan (PlanRunner records, resume).
+power="auto" (the reference's default, pipeline.py:295-372) runs on the
+device: up to q_max passes, stopped by the reference's rule on
+nu_q = ||(A A^T)^q A Omega||_F / sqrt(m l), whose raw-product norms are
+carried through the re-orthonormalised iteration as small triangular factors
+(engine.cu AutoPower); `auto_select_q` (396-418) is the same loop on a
+rank-wide probe. Out of scope (fail loudly): gram_path=True and the
+store-backed durable plan (PlanRunner records, resume).
 """
 
 from __future__ import annotations
@@ -137,8 +142,6 @@ def randomized_svd(pool, a, config: RsvdConfig, *, threads: int = 1, runner=None
     if r_work > min(m, n):
         raise ShapeError(f"rank {config.rank} (+{config.oversample} oversampling) exceeds "
                          f"min{tuple(a.shape)} = {min(m, n)}")
-    if config.power == "auto":
-        raise XsvdError("power='auto' (auto_select_q) is outside the GPU hot path; pass an int")
     if config.gram_path:
         raise XsvdError("gram_path=True is outside the GPU hot path")
     precision = as_precision(config.precision)
@@ -146,6 +149,10 @@ def randomized_svd(pool, a, config: RsvdConfig, *, threads: int = 1, runner=None
         raise XsvdError("half precision (storage-only in the reference) is not built on the GPU path")
     clock = clock or (runner.clock if runner is not None else StageClock())
     ctx = _lib.load()
+    auto = config.power == "auto"
+    q = _lib.POWER_AUTO if auto else int(config.power)
+    if auto:
+        ctx.set_power_auto(config.q_max, config.tau)
     if is_sparse(a):
         if precision is not Precision.DOUBLE:
             raise XsvdError("sparse A is built for float64 only")
@@ -153,16 +160,45 @@ def randomized_svd(pool, a, config: RsvdConfig, *, threads: int = 1, runner=None
         if a.desc.transposed:
             rows, cols = cols, rows
         u, s, v, deficient, stages = ctx.rsvd_coo(rows, cols, vals, tuple(a.shape), config.rank,
-                                                  config.oversample, int(config.power),
-                                                  config.seed)
+                                                  config.oversample, q, config.seed)
     else:
         host = _dense_input(a).astype(precision.storage_dtype, copy=False)
-        u, s, v, deficient, stages = ctx.rsvd_dense(host, config.rank, config.oversample,
-                                                    int(config.power), config.seed)
+        u, s, v, deficient, stages = ctx.rsvd_dense(host, config.rank, config.oversample, q,
+                                                    config.seed)
+    chosen_q = ctx.last_power()[0] if auto else int(config.power)
     for name, sec in zip(STAGE_NAMES, stages):
         clock.seconds[name] += float(sec)
     register_dense(pool, "S", s.reshape(-1, 1), Precision.DOUBLE)
     umat = register_dense(pool, "U", u, precision)
     vmat = register_dense(pool, "V", v, precision)
-    return RsvdResult(u=umat, s=s.astype(np.float64), v=vmat, chosen_q=int(config.power),
+    return RsvdResult(u=umat, s=s.astype(np.float64), v=vmat, chosen_q=chosen_q,
                       stage_seconds=dict(clock.seconds), deficient_columns=deficient)
+
+
+def auto_select_q(pool, a, rank, *, q_max: int = 5, tau: float = 1e-6, seed: int = 0,
+                  threads: int = 1, precision=None) -> int:
+    """Pick the power exponent (pipeline.py:396-418): the power="auto" loop
+    on a rank-wide probe Omega = gaussian_band(seed, 0, n, rank). Runs on the
+    device like randomized_svd; nothing is registered in the pool (the
+    reference drops its scratch matrices too)."""
+    precision = as_precision(precision or a.desc.precision)
+    if precision is Precision.HALF:
+        raise XsvdError("half precision (storage-only in the reference) is not built on the GPU path")
+    m, n = a.shape
+    if rank > min(m, n):
+        raise ShapeError(f"rank {rank} exceeds min{tuple(a.shape)} = {min(m, n)}")
+    if q_max < 0:
+        raise ValueError(f"q_max must be nonnegative, got {q_max}")
+    ctx = _lib.load()
+    ctx.set_power_auto(q_max, tau)
+    if is_sparse(a):
+        if precision is not Precision.DOUBLE:
+            raise XsvdError("sparse A is built for float64 only")
+        rows, cols, vals = canonical_coo(a)
+        if a.desc.transposed:
+            rows, cols = cols, rows
+        ctx.rsvd_coo(rows, cols, vals, tuple(a.shape), rank, 0, _lib.POWER_AUTO, seed)
+    else:
+        host = _dense_input(a).astype(precision.storage_dtype, copy=False)
+        ctx.rsvd_dense(host, rank, 0, _lib.POWER_AUTO, seed)
+    return ctx.last_power()[0]

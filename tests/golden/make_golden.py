@@ -223,6 +223,51 @@ def gen_cfg1():
     save("cfg1", **out)
 
 
+def gen_autoq():
+    """power="auto": the reference's own _sketch_and_power loop
+    (pipeline.py:295-372) — chosen q and the nu sequence — plus
+    auto_select_q (396-418) and randomized_svd(power="auto")'s chosen_q."""
+    from xsvd.pipeline import _null_runner, _sketch_and_power, auto_select_q, gaussian_matrix
+
+    out = {}
+    # name, m, n, k, p, spectrum, scale, q_max, tau, seed
+    cases = [("pow", 300, 200, 10, 5, "pow-1.5", 1.0, 5, 1e-6, 4),
+             ("geom", 400, 150, 8, 4, "geom0.9", 1.0, 5, 1e-6, 2),
+             ("small_scale", 200, 120, 6, 2, "pow-1.5", 0.05, 5, 0.5, 1),
+             ("qmax2", 260, 180, 12, 6, "pow-1.5", 1.0, 2, 1e-6, 3),
+             ("qmax0", 150, 100, 5, 5, "geom0.9", 1.0, 0, 1e-6, 6),
+             ("zero", 80, 60, 4, 2, "zero", 1.0, 5, 1e-6, 1)]
+    for i, (name, m, n, k, p, spec, scale, q_max, tau, seed) in enumerate(cases):
+        if spec == "zero":
+            a = np.zeros((m, n))
+        else:
+            a = scale * dense_lowrank_np(m, n, spec, 1e-8, 700 + i, 800 + i)
+        pool = BlockPool()
+        ma = dense(pool, "A", a)
+        o = gaussian_matrix(pool, "O", n, k + p, seed)
+        _, chosen, nus = _sketch_and_power(_null_runner(pool), pool, ma, o, power="auto",
+                                           q_max=q_max, tau=tau, threads=1,
+                                           precision=Precision.DOUBLE)
+        res = None
+        if spec != "zero":
+            pool2 = BlockPool()
+            res = randomized_svd(pool2, dense(pool2, "A", a),
+                                 RsvdConfig(rank=k, oversample=p, power="auto", q_max=q_max,
+                                            tau=tau, seed=seed))
+        probe = auto_select_q(pool, ma, k, q_max=q_max, tau=tau, seed=seed)
+        out[f"{name}_a_seeds"] = np.array([700 + i, 800 + i])
+        out[f"{name}_cfg"] = np.array([m, n, k, p, q_max, seed])
+        out[f"{name}_spec"] = np.array(spec)
+        out[f"{name}_scale_tau"] = np.array([scale, tau])
+        out[f"{name}_chosen"] = np.array(chosen)
+        out[f"{name}_nus"] = np.array(nus)
+        out[f"{name}_probe_chosen"] = np.array(probe)
+        if res is not None:
+            assert res.chosen_q == chosen
+            out[f"{name}_s"] = res.s
+    save("autoq", **out)
+
+
 if __name__ == "__main__":
     assert xsvd.__file__.startswith("/root/reference"), xsvd.__file__
     which = sys.argv[1:] or ["rng", "multiply", "qr", "svd", "rsvd", "cfg1"]

@@ -44,6 +44,47 @@ def test_spmm_widths_and_determinism(lib, l):
     assert np.max(np.abs(z1 - a.T @ q)) <= 1e-12 * np.max(np.abs(z1))
 
 
+@pytest.mark.parametrize("m,n,l", [(3000, 300000, 40), (300000, 2000, 24)])
+def test_spmm_l2_column_chunks(lib, m, n, l):
+    """Gathered operands too large for one L2-resident slab are processed in
+    column chunks (sparse.cu launch_spmm): X n x 40 (96 MB) for A X, Q
+    m x 24 (58 MB) for A^T Q at 16-column chunks."""
+    import scipy.sparse as sp
+
+    from paper_1907_06470_b200.workloads import sparse_uniform_np
+
+    rowptr, col, val = sparse_uniform_np(m, n, 12, 5)
+    rows = np.repeat(np.arange(m), np.diff(rowptr))
+    a = sp.csr_matrix((val, col, rowptr), shape=(m, n))
+    x = np.random.default_rng(1).standard_normal((n, l))
+    y = lib.spmm(rows, col, val, (m, n), x)
+    assert np.max(np.abs(y - a @ x)) <= 1e-12 * np.max(np.abs(y))
+    q = np.random.default_rng(2).standard_normal((m, l))
+    z = lib.spmm(rows, col, val, (m, n), q, trans=True)
+    assert np.max(np.abs(z - a.T @ q)) <= 1e-12 * np.max(np.abs(z))
+
+
+def test_transpose_long_columns(lib):
+    """Column segments longer than the warp rank-sort's register window (256)
+    take the insertion-sort path; A^T products stay exact and deterministic."""
+    import scipy.sparse as sp
+
+    rng = np.random.default_rng(7)
+    m, n = 2000, 50
+    dense = np.where(rng.random((m, n)) < 0.02, rng.standard_normal((m, n)), 0.0)
+    dense[:, 3] = rng.standard_normal(m)             # 2000 entries
+    dense[::7, 9] = rng.standard_normal(len(range(0, m, 7)))  # 286 entries
+    dense[::9, 11] = rng.standard_normal(len(range(0, m, 9)))  # 223 entries
+    a = sp.csr_matrix(dense)
+    a.sort_indices()
+    rows = np.repeat(np.arange(m), np.diff(a.indptr))
+    q = rng.standard_normal((m, 5))
+    z1 = lib.spmm(rows, a.indices, a.data, (m, n), q, trans=True)
+    z2 = lib.spmm(rows, a.indices, a.data, (m, n), q, trans=True)
+    assert np.array_equal(z1, z2)
+    assert np.max(np.abs(z1 - dense.T @ q)) <= 1e-12 * np.max(np.abs(z1))
+
+
 def test_empty_rows_and_columns(lib):
     rows = np.array([0, 0, 3])
     cols = np.array([1, 4, 4])

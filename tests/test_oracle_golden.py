@@ -138,3 +138,30 @@ def test_sine_angle_metric():
     y = x.copy()
     y[:, 0] = np.linalg.qr(rng.standard_normal((50, 1)))[0][:, 0]
     assert M.sin_angle(x, y) > 0.1
+
+
+def _autoq_case(g, name):
+    from paper_1907_06470_b200.workloads import dense_lowrank_np
+
+    m, n, k, p, q_max, seed = (int(x) for x in g[f"{name}_cfg"])
+    spec = str(g[f"{name}_spec"])
+    scale, tau = (float(x) for x in g[f"{name}_scale_tau"])
+    sa, sn = (int(x) for x in g[f"{name}_a_seeds"])
+    a = np.zeros((m, n)) if spec == "zero" else scale * dense_lowrank_np(m, n, spec, 1e-8, sa, sn)
+    return a, k, p, q_max, tau, seed
+
+
+AUTOQ_CASES = ["pow", "geom", "small_scale", "qmax2", "qmax0", "zero"]
+
+
+@pytest.mark.parametrize("name", AUTOQ_CASES)
+def test_power_auto_golden(name):
+    """power="auto" restated (oracle.pipeline.sketch_power_auto) against the
+    reference's own _sketch_and_power loop: same chosen q, same nu sequence."""
+    g = golden("autoq")
+    a, k, p, q_max, tau, seed = _autoq_case(g, name)
+    chosen, nus = P.sketch_power_auto(a, k, p, seed, q_max=q_max, tau=tau)
+    assert chosen == int(g[f"{name}_chosen"])
+    ref = g[f"{name}_nus"]
+    assert len(nus) == len(ref)
+    assert np.allclose(nus, ref, rtol=1e-12, atol=0.0)
