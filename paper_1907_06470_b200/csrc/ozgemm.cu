@@ -375,13 +375,13 @@ __global__ void col_exp_kernel(const unsigned long long* __restrict__ cmax,
 // Row AND column max |x| / sum of squares of A in ONE pass (the slicing
 // pass needs both exponent sets before it starts). Block tile 512 rows x 256
 // columns: each warp reads 2 KB of a row per step (8 coalesced 256-byte
-// loads, two rows in flight), reduces the row partial by shuffle, and keeps
+// loads), reduces the row partial by shuffle, and keeps
 // 8 column partials per lane that the block combines in shared memory.
 // Partials go to scratch without atomics — per (row, column tile) and per
 // (row tile, column) — and two small kernels finish them in a fixed order.
 constexpr int RC_ROWS = 512, RC_COLS = 256;
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 4)
     rc_stats_kernel(const double* __restrict__ X, int64_t rows, int64_t cols, int64_t ldx,
                     double2* __restrict__ rpart, double2* __restrict__ cpart) {
   __shared__ double sm[8][RC_COLS + 1], sq[8][RC_COLS + 1];
@@ -396,34 +396,26 @@ __global__ void __launch_bounds__(256)
   bool colok[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) colok[j] = c0 + tx + 32 * j < cols;
-  for (int64_t r = r0 + ty; r < rend; r += 16) {
-    double v[2][8];
+  for (int64_t r = r0 + ty; r < rend; r += 8) {
+    const double* xr = X + r * ldx + c0 + tx;
+    double v[8];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int64_t rr = r + 8 * u;
-      const double* xr = X + rr * ldx + c0 + tx;
+    for (int j = 0; j < 8; ++j) v[j] = colok[j] ? __ldcs(xr + 32 * j) : 0.0;
+    double m = 0.0, ss = 0.0;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) v[u][j] = (rr < rend && colok[j]) ? __ldcs(xr + 32 * j) : 0.0;
+    for (int j = 0; j < 8; ++j) {
+      const double a = fabs(v[j]);
+      m = fmax(m, a);
+      ss = fma(v[j], v[j], ss);
+      cm[j] = fmax(cm[j], a);
+      cs[j] = fma(v[j], v[j], cs[j]);
     }
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      double m = 0.0, ss = 0.0;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const double a = fabs(v[u][j]);
-        m = fmax(m, a);
-        ss = fma(v[u][j], v[u][j], ss);
-        cm[j] = fmax(cm[j], a);
-        cs[j] = fma(v[u][j], v[u][j], cs[j]);
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-        ss += __shfl_xor_sync(0xffffffffu, ss, o);
-      }
-      const int64_t rr = r + 8 * u;
-      if (tx == 0 && rr < rend) rpart[rr * nct + ct] = make_double2(m, ss);
+    for (int o = 16; o > 0; o >>= 1) {
+      m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+      ss += __shfl_xor_sync(0xffffffffu, ss, o);
     }
+    if (tx == 0) rpart[r * nct + ct] = make_double2(m, ss);
   }
 #pragma unroll
   for (int j = 0; j < 8; ++j) {

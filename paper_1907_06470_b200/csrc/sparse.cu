@@ -53,8 +53,45 @@ __global__ void __launch_bounds__(256)
         vj = __ldcs(val + e);
       }
       const int cnt = (e1 - base) < 32 ? (int)(e1 - base) : 32;
-#pragma unroll 4
-      for (int t = 0; t < cnt; ++t) {
+      // batches of 4 nonzeros: all 4 * NCH loads are issued before the FMAs
+      // (the gather is latency-bound; this keeps them in flight together)
+      int t = 0;
+      for (; t + 4 <= cnt; t += 4) {
+        int64_t j[4];
+        double a[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          j[u] = __shfl_sync(0xffffffffu, cj, t + u);
+          a[u] = __shfl_sync(0xffffffffu, vj, t + u);
+        }
+        double x[4][NCH][VEC];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const double* xr = X + j[u] * ldx + VEC * lane;
+#pragma unroll
+          for (int h = 0; h < NCH; ++h) {
+            if (VEC * lane + 32 * VEC * h < l) {
+              if (VEC == 2) {
+                const double2 v = __ldg(reinterpret_cast<const double2*>(xr + 64 * h));
+                x[u][h][0] = v.x;
+                x[u][h][VEC - 1] = v.y;
+              } else {
+                x[u][h][0] = __ldg(xr + 32 * h);
+              }
+            } else {
+#pragma unroll
+              for (int v = 0; v < VEC; ++v) x[u][h][v] = 0.0;
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int h = 0; h < NCH; ++h)
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) acc[h][v] = fma(a[u], x[u][h][v], acc[h][v]);
+      }
+      for (; t < cnt; ++t) {
         const int64_t j = __shfl_sync(0xffffffffu, cj, t);
         const double a = __shfl_sync(0xffffffffu, vj, t);
         const double* xr = X + j * ldx + VEC * lane;
