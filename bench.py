@@ -35,7 +35,9 @@ cpu_baseline = the oracle's restatement of the reference's shipped driver
 
 --impl reference prints the reference arm: the same port timed on all host
 threads (the reference is pure Python and cannot travel to the GPU box).
-Multi-GPU (torchrun, N>1): A's rows are sharded over ranks; see DESIGN.md.
+Multi-GPU (torchrun, N>1): a tall A's rows (configs 1-2) or a wide A's
+columns (config 5) are sharded over ranks, NCCL all-reduce inside the
+library; see DESIGN.md §5.
 """
 
 from __future__ import annotations
@@ -353,6 +355,31 @@ class ShardedDenseCase(DenseCase):
             self.u.data_ptr(), self.s.data_ptr(), self.v.data_ptr())[1]
 
 
+class ColShardedDenseCase(DenseCase):
+    """Column-block sharded wide A over N ranks (config 5's layout): the m x l
+    partials of A_g X_g and the n-side sketch Grams are all-reduced (NCCL)
+    inside the library; A_g^T Q stays local."""
+
+    def __init__(self, ctx, w, device, rank, world):
+        import torch
+
+        from paper_1907_06470_b200.distributed import col_shards, init_comm
+
+        super().__init__(ctx, w, device)
+        self.c0, self.c1 = col_shards(w.n, world)[rank]
+        self.a = self.a[:, self.c0:self.c1].contiguous()
+        torch.cuda.empty_cache()
+        self.n_local = self.c1 - self.c0
+        self.v = torch.empty((self.n_local, w.k), dtype=self.torch_dtype, device=device)
+        init_comm(ctx)
+
+    def step(self):
+        w = self.w
+        return self.ctx.rsvd_dense_colsharded_dev(
+            self.np_dtype, w.m, w.n, self.n_local, self.c0, self.a.data_ptr(), self.n_local, w.k,
+            w.p, w.q, w.cfg, self.u.data_ptr(), self.s.data_ptr(), self.v.data_ptr())[1]
+
+
 class StreamedCase:
     """Config 4's out-of-core path: A (f32) in pinned host memory, streamed
     through HBM in 2 GiB row tiles, q + 1 fused passes per factorisation. The
@@ -486,7 +513,9 @@ def run_ours(args):
     elif world > 1:
         if w.density != "dense":
             raise SystemExit("multi-GPU sharding is built for dense A (configs 1, 2, 5)")
-        case = ShardedDenseCase(ctx, w, device, rank, world)
+        # wide A (config 5) splits by columns, tall A by rows
+        case = (ColShardedDenseCase if w.n > w.m else ShardedDenseCase)(ctx, w, device, rank,
+                                                                        world)
     elif w.density == "sparse":
         case = SparseCase(ctx, w, device)
     else:
@@ -587,7 +616,8 @@ def run_ours(args):
                 + " (built on the device/host outside the timed region)",
         "config": {"workload": w.name, "m": w.m, "n": w.n, "k": w.k, "p": w.p, "q": w.q,
                    "l": w.l, "omega": f"gaussian_band(seed={w.cfg}) generated on device each step",
-                   "l2": l2, "parallelism": f"rows{world}"},
+                   "l2": l2,
+                   "parallelism": f"{'cols' if world > 1 and w.n > w.m else 'rows'}{world}"},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
         "clocks": dict(clocks.summary(), note=clock_note),
         "step_ms": [round(x, 3) for x in step_ms],

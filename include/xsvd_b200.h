@@ -159,6 +159,19 @@ int xb_rsvd_dense_sharded_dev(xb_ctx* ctx, int dtype, int64_t m_global, int64_t 
                               int64_t ldv, int32_t* deficient, int* ndeficient,
                               double* stage_seconds);
 
+/* Column-block sharding (SURVEY §8e, config 5's layout): rank g passes its
+ * columns [col0, col0 + n_local) of the m x n_global matrix A (m x n_local,
+ * leading dim lda). Y_g = A_g Omega_g partials (m x l) are summed with one
+ * NCCL all-reduce per product over A; Z_g = A_g^T Q is local, and the l x l
+ * Grams of the row-sharded n-side sketches (Z, B^T) are summed the same way.
+ * Omega_g = rows [col0, col0 + n_local) of gaussian_band(seed, 0, n_global,
+ * k + p). U (m x k) and s are replicated; V is returned for the local rows. */
+int xb_rsvd_dense_colsharded_dev(xb_ctx* ctx, int dtype, int64_t m, int64_t n_global,
+                                 int64_t n_local, int64_t col0, const void* dA, int64_t lda,
+                                 uint64_t seed, int k, int p, int q, void* dU, int64_t ldu,
+                                 double* d_s, void* dV, int64_t ldv, int32_t* deficient,
+                                 int* ndeficient, double* stage_seconds);
+
 /*
  * Sparse A — replaces randomized_svd on a SPARSE StoredMatrix, i.e. the
  * sparse x dense and dense x sparse products of kernels.py:85-112 (Y = A X,

@@ -16,7 +16,8 @@ from .core import (CANONICAL_CELL, BlockPartition, DenseBlock, Density, MatrixDe
                    Precision, SparseBlock, transpose_view, wider)
 from .errors import BudgetError, ConvergenceError, ShapeError, XsvdError
 from .kernels import MultiplyStats, QRResult, SmallSVDResult, block_multiply, gram, svd_small, thin_qr
-from .pipeline import (STAGE_NAMES, RsvdConfig, RsvdResult, StageClock, auto_select_q, gaussian_matrix,
+from .pipeline import (STAGE_NAMES, RsvdConfig, RsvdResult, StageClock, auto_select_q, full_svd,
+                       gaussian_matrix,
                        randomized_svd)
 from .pool import BlockPool, StoredMatrix, create_matrix, matrix_from_coo, matrix_from_dense
 
@@ -25,6 +26,6 @@ __all__ = [
     "DenseBlock", "Density", "MatrixDescriptor", "MultiplyStats", "Precision", "QRResult",
     "RsvdConfig", "RsvdResult", "STAGE_NAMES", "ShapeError", "SmallSVDResult", "SparseBlock",
     "StageClock", "StoredMatrix", "XsvdError", "block_multiply", "create_matrix",
-    "auto_select_q", "gaussian_matrix", "gram", "matrix_from_coo", "matrix_from_dense", "randomized_svd",
+    "auto_select_q", "full_svd", "gaussian_matrix", "gram", "matrix_from_coo", "matrix_from_dense", "randomized_svd",
     "svd_small", "thin_qr", "transpose_view", "wider",
 ]

@@ -52,6 +52,9 @@ SIGNATURES = [
     ("xb_comm_init", _int, [_vp, _vp, _int, _int]),
     ("xb_rsvd_dense_sharded_dev", _int, [_vp, _int, _i64, _i64, _i64, _vp, _i64, _u64, _int, _int,
                                          _int, _vp, _i64, _vp, _vp, _i64, _vp, _intp, _vp]),
+    ("xb_rsvd_dense_colsharded_dev", _int, [_vp, _int, _i64, _i64, _i64, _i64, _vp, _i64, _u64,
+                                            _int, _int, _int, _vp, _i64, _vp, _vp, _i64, _vp,
+                                            _intp, _vp]),
     ("xb_rsvd_coo", _int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _u64, _int, _int, _int,
                            _vp, _i64, _vp, _vp, _i64, _vp, _intp, _vp]),
     ("xb_rsvd_csr_dev", _int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _u64, _int, _int, _int,
@@ -233,6 +236,17 @@ class Context:
         stages = np.zeros(NUM_STAGES)
         _check(self.lib.xb_rsvd_dense_sharded_dev(
             self.h, dtype_code(dtype), m_global, n, m_local, C.c_void_p(a_ptr), lda,
+            int(seed) & (2**64 - 1), k, p, q, C.c_void_p(u_ptr), k, C.c_void_p(s_ptr),
+            C.c_void_p(v_ptr), k, _ptr(deficient), C.byref(ndef), _ptr(stages)))
+        return tuple(int(x) for x in deficient[: ndef.value]), stages
+
+    def rsvd_dense_colsharded_dev(self, dtype, m, n_global, n_local, col0, a_ptr, lda, k, p, q,
+                                  seed, u_ptr, s_ptr, v_ptr):
+        deficient = np.zeros(max(k + p, 1), dtype=np.int32)
+        ndef = C.c_int(0)
+        stages = np.zeros(NUM_STAGES)
+        _check(self.lib.xb_rsvd_dense_colsharded_dev(
+            self.h, dtype_code(dtype), m, n_global, n_local, col0, C.c_void_p(a_ptr), lda,
             int(seed) & (2**64 - 1), k, p, q, C.c_void_p(u_ptr), k, C.c_void_p(s_ptr),
             C.c_void_p(v_ptr), k, _ptr(deficient), C.byref(ndef), _ptr(stages)))
         return tuple(int(x) for x in deficient[: ndef.value]), stages

@@ -549,6 +549,12 @@ struct AOp {
   // are summed over `comm`
   void* comm = nullptr;
   int64_t m_global = 0;
+  // column-sharded A: this rank holds columns
+  // [col0, col0 + n) of an m x n_global matrix; the products over A (Y = A X)
+  // and the Grams of the n-side sketches are summed over `comm`, the m-side
+  // QRs run replicated
+  bool col_shard = false;
+  int64_t n_global = 0, col0 = 0;
 };
 
 void spmm_on_a(xb_ctx* c, const Csr& s, const double* X, double* Y, int lp, int l) {
@@ -657,6 +663,8 @@ void op_nn(xb_ctx* c, const AOp& op, int64_t m, int64_t n, const double* X, doub
     oz_product(c, op.oz, false, m, n, X, Y, lp, l);
   else
     gemm_on_a(c, false, m, lp, n, op.dense, 0, X, lp, Y, lp, l);
+  // column-sharded: Y = sum_g A_g X_g, the one m x l exchange per product
+  if (op.comm && op.col_shard) nccl_allreduce_sum(op.comm, Y, (size_t)m * lp, c->st);
 }
 
 // Z (n x lp) = A^T Q
@@ -669,7 +677,7 @@ void op_tn(xb_ctx* c, const AOp& op, int64_t m, int64_t n, const double* Q, doub
   else
     gemm_on_a(c, true, n, lp, m, op.dense, 0, Q, lp, Z, lp, l);
   // row-sharded: Z = sum_g A_g^T Q_g, the one n x l exchange per product
-  if (op.comm) nccl_allreduce_sum(op.comm, Z, (size_t)n * lp, c->st);
+  if (op.comm && !op.col_shard) nccl_allreduce_sum(op.comm, Z, (size_t)n * lp, c->st);
 }
 
 // One factorisation. A (device, f64 or f32 dense, or f64 CSR) is only touched
@@ -681,9 +689,11 @@ void rsvd_impl(xb_ctx* c, const AOp& op_in, int64_t m, int64_t n, const void* d_
                int32_t* deficient, int* ndeficient, double* stage_seconds, const IngestPlan& ing) {
   AOp op = op_in;
   const AView& a = op.dense;
-  // m = rows held here (all of A unless row-sharded)
-  check_dims(op.comm ? op.m_global : m, n, k, p, q);
-  const bool sharded = op.comm != nullptr;
+  // m = rows held here (all of A unless row-sharded), n = columns held here
+  // (all unless column-sharded)
+  const bool sharded = op.comm != nullptr && !op.col_shard;  // m-side sums
+  const bool csharded = op.comm != nullptr && op.col_shard;  // n-side sums
+  check_dims(sharded ? op.m_global : m, csharded ? op.n_global : n, k, p, q);
   const int l = k + p;
   const int lp = (int)round_up(l, 8);
   const int kp = (int)round_up(k, 2);
@@ -727,7 +737,7 @@ void rsvd_impl(xb_ctx* c, const AOp& op_in, int64_t m, int64_t n, const void* d_
     c->dbuf("hh_work", (size_t)2 * std::max(m, n) * l);
   }
   Small s = small_bufs(c, l);
-  if (sharded) {
+  if (op.comm) {
     s.comm = op.comm;
     s.shard_err = c->ibuf("shard_err", 4);
     XB_CUDA(cudaMemsetAsync(s.shard_err, 0, sizeof(int), st));
@@ -745,7 +755,8 @@ void rsvd_impl(xb_ctx* c, const AOp& op_in, int64_t m, int64_t n, const void* d_
     else
       launch_copy2d(static_cast<const double*>(d_omega), n, l, ld_omega, Om, lp, st);
   } else {
-    launch_gaussian<double>(seed, 0, n, l, Om, lp, lp, st);
+    // this rank's rows of Omega when column-sharded (rows are keyed by index)
+    launch_gaussian<double>(seed, csharded ? op.col0 : 0, n, l, Om, lp, lp, st);
     if (a.f32) launch_round_f32(Om, n, l, lp, st);
   }
 
@@ -831,7 +842,7 @@ void rsvd_impl(xb_ctx* c, const AOp& op_in, int64_t m, int64_t n, const void* d_
     clk.enter(kSketch);
     op_tn(c, op, m, n, Qm, Zn, lp, l);  // Z = A^T Q
     clk.enter(kOrtho);
-    cholqr1(c, s, Zn, n, Qn, false, autoq ? ap.Rz : nullptr);
+    cholqr1(c, s, Zn, n, Qn, csharded, autoq ? ap.Rz : nullptr);
     if (autoq) gemm(c, false, lp, lp, lp, ap.Rz, lp, ap.M, lp, ap.C, lp);  // C = R_z M
     clk.enter(kSketch);
     op_nn(c, op, m, n, Qn, Ym, lp, l);  // Y = A Qz
@@ -874,14 +885,16 @@ void rsvd_impl(xb_ctx* c, const AOp& op_in, int64_t m, int64_t n, const void* d_
   double* lift = nullptr;
   if (fused_lift) {
     XB_CUDA(cudaMemsetAsync(s.flag, 0, sizeof(int), st));
-    gram(c, s, Zn, n, false);
-    launch_chol_inv(s.G, lp, l, 1e-8, Rf, s.R1i, lp, s.flag, s.cw, st);
-    // Cholesky breakdown: Householder Q replaces B^T in place, R^-1 := I
-    double* hw = c->dbuf("hh_work", (size_t)2 * n * l);
-    launch_householder_fallback(Zn, lp, n, l, lp, Zn, lp, Rf, lp, hw, s.flag, st);
-    launch_identity_if(s.R1i, lp, l, s.flag, st);
+    gram(c, s, Zn, n, csharded);
+    launch_chol_inv(s.G, lp, l, 1e-8, Rf, s.R1i, lp, csharded ? s.shard_err : s.flag, s.cw, st);
+    if (!csharded) {
+      // Cholesky breakdown: Householder Q replaces B^T in place, R^-1 := I
+      double* hw = c->dbuf("hh_work", (size_t)2 * n * l);
+      launch_householder_fallback(Zn, lp, n, l, lp, Zn, lp, Rf, lp, hw, s.flag, st);
+      launch_identity_if(s.R1i, lp, l, s.flag, st);
+    }
   } else {
-    cholqr2(c, s, Zn, n, Tn, Qn, Rf);  // B^T = Q_B R_B
+    cholqr2(c, s, Zn, n, Tn, Qn, Rf, csharded);  // B^T = Q_B R_B
   }
 
   clk.enter(kSvd);
@@ -901,7 +914,7 @@ void rsvd_impl(xb_ctx* c, const AOp& op_in, int64_t m, int64_t n, const void* d_
   int hstat = 0, hshard = 0;
   std::vector<int> hdef(lp + 1, 0);
   XB_CUDA(cudaMemcpyAsync(&hstat, jstat, sizeof(int), cudaMemcpyDeviceToHost, st));
-  if (sharded)
+  if (op.comm)
     XB_CUDA(cudaMemcpyAsync(&hshard, s.shard_err, sizeof(int), cudaMemcpyDeviceToHost, st));
   XB_CUDA(cudaMemcpyAsync(hdef.data(), defc, (lp + 1) * sizeof(int), cudaMemcpyDeviceToHost, st));
   clk.finish(stage_seconds ? local_stage : nullptr);
@@ -914,7 +927,7 @@ void rsvd_impl(xb_ctx* c, const AOp& op_in, int64_t m, int64_t n, const void* d_
     for (int i = 0; i < hdef[0] && i < l; ++i) deficient[i] = hdef[1 + i];
   XB_REQUIRE(hstat == 0, XB_ECONV, "Jacobi SVD of the projected factor did not converge in 60 sweeps");
   XB_REQUIRE(hshard == 0, XB_ECONV,
-             "row-sharded sketch is numerically rank deficient (Cholesky breakdown); the "
+             "sharded sketch is numerically rank deficient (Cholesky breakdown); the "
              "single-device Householder fallback does not apply to a sharded sketch");
 }
 
@@ -1531,6 +1544,38 @@ int xb_rsvd_dense_sharded_dev(xb_ctx* c, int dtype, int64_t m_global, int64_t n,
     if (f32) {
       launch_copy2d_cast<double, float>(Ud, m_local, k, k, static_cast<float*>(dU), ldu, c->st);
       launch_copy2d_cast<double, float>(Vd, n, k, k, static_cast<float*>(dV), ldv, c->st);
+      XB_CUDA(cudaStreamSynchronize(c->st));
+    }
+  });
+}
+
+int xb_rsvd_dense_colsharded_dev(xb_ctx* c, int dtype, int64_t m, int64_t n_global,
+                                 int64_t n_local, int64_t col0, const void* dA, int64_t lda,
+                                 uint64_t seed, int k, int p, int q, void* dU, int64_t ldu,
+                                 double* d_s, void* dV, int64_t ldv, int32_t* deficient,
+                                 int* ndeficient, double* stage_seconds) {
+  return guarded([&] {
+    XB_REQUIRE(c, XB_EVALUE, "null context");
+    XB_REQUIRE(c->comm, XB_EVALUE, "xb_comm_init has not been called on this context");
+    LaunchScope ls(c);
+    const bool f32 = check_dtype(dtype);
+    XB_REQUIRE(n_local >= 1 && col0 >= 0 && col0 + n_local <= n_global, XB_ESHAPE,
+               "bad local column block");
+    XB_REQUIRE(lda >= n_local && ldu >= k && ldv >= k, XB_EVALUE, "leading dimension too small");
+    AOp op;
+    op.dense = AView{dA, lda, f32};
+    op.comm = c->comm;
+    op.col_shard = true;
+    op.n_global = n_global;
+    op.col0 = col0;
+    double* Ud = f32 ? c->dbuf("Ud", (size_t)m * k) : static_cast<double*>(dU);
+    double* Vd = f32 ? c->dbuf("Vd", (size_t)n_local * k) : static_cast<double*>(dV);
+    RsvdOut out{Ud, f32 ? k : ldu, d_s, Vd, f32 ? k : ldv};
+    rsvd_impl(c, op, m, n_local, nullptr, k + p, seed, k, p, q, out, deficient, ndeficient,
+              stage_seconds, IngestPlan{});
+    if (f32) {
+      launch_copy2d_cast<double, float>(Ud, m, k, k, static_cast<float*>(dU), ldu, c->st);
+      launch_copy2d_cast<double, float>(Vd, n_local, k, k, static_cast<float*>(dV), ldv, c->st);
       XB_CUDA(cudaStreamSynchronize(c->st));
     }
   });

@@ -17,30 +17,29 @@
 // <= S) < 2^31, i.e. K_chunk <= 16384; longer reductions are split over K
 // into f64 slices summed in slice order. The error is relative to the
 // row/column max-norm scale, so the engine keeps matrices whose rows or
-// columns span more than 64x their RMS on DMMA (row_exp / col_exp guard).
+// columns span more than 64x their RMS on DMMA (the rc_stats range guard).
 //
-// Layout: left operand slices L[t] (k-blocked [kp/32][rows_p][32] int8: each
-// 128-row k-tile is contiguous) with row exponents; right operand slices R[u] (np x kp int8, K contiguous: the
-// transposed right matrix) with column exponents. For Y = A X the left
-// slices are A's rows (made once per factorisation); for Z = A^T Q they are
-// A's columns (a transposed slice set, also made once), so both products run
-// the same NN kernel with K-major operands (kind::i8 has no MN-major mode).
+// Layout (il_off): every operand is stored in HBM exactly as the MMA reads
+// it from shared memory — per (k-block of 32, row tile) the S slices are S
+// consecutive tiles of rows x 32 bytes in no-swizzle K-major core matrices —
+// so each k-tile arrives with ONE linear bulk copy per operand. Left slices
+// (128-row tiles) carry per-row exponents, right slices (64-row tiles of the
+// transposed right operand) per-column exponents. For Y = A X the left
+// slices are A's rows, for Z = A^T Q A's columns (both made once per
+// factorisation by slice_both_kernel from one read of A); kind::i8 has no
+// MN-major mode, hence the two sets.
 //
-// Kernel (one CTA per 128 x 48 output tile, 448 threads):
-//   warp 0      TMA producer: the S right-slice tiles (48 x 32 B each,
-//               32-byte swizzle) of each k-tile, an 8-deep ring
-//   warp 1      TMEM allocator + single-thread MMA issuer: per k-tile the
-//               S(S+1)/2 pairs (t, u) accumulate into level d = t + u - 2
-//               (S int32 accumulators of 48 columns; 4 TMEM A slots)
-//   warps 2-13  loaders (3 per TMEM lane quadrant): each thread owns one tile
-//               row; it reads its 32-byte row segment of 2 left slices
-//               straight from global memory (6 k-tiles in flight in
-//               registers) and stores them into a
-//               TMEM A slot (tcgen05.st) -- the MMA takes A from TMEM, so
-//               shared memory only carries the right slices (an SS-mode A
-//               would need ~190 B/clk of shared-memory reads). Then the
-//               epilogue: per level tcgen05.ld, int32 -> f64, * 2^-7d, sum,
-//               * 2^(e_i + f_j), store (or += / split-K slice).
+// Kernel (one CTA per 128 x 64 output tile, 192 threads, 1 CTA per SM):
+//   warp 0      producer: per k-tile one bulk copy of the S left slices and
+//               one of the S right slices into a ring of NS stages
+//   warp 1      TMEM allocator + MMA issuer: tcgen05.cp moves the left
+//               slices of the stage into a TMEM A slot (two slots, double
+//               buffered), then the S(S+1)/2 pairs (t, u), t + u < S,
+//               accumulate into level d = t + u (S int32 accumulators of 64
+//               columns); tcgen05.commit frees the stage
+//   warps 2-5   epilogue (one TMEM lane quadrant each): per level
+//               tcgen05.ld, int32 -> f64, * 2^-(14+8d), sum, * 2^(e_i + f_j),
+//               store (or += / split-K slice)
 #include <algorithm>
 
 #include "common.cuh"

@@ -202,3 +202,36 @@ def auto_select_q(pool, a, rank, *, q_max: int = 5, tau: float = 1e-6, seed: int
         host = _dense_input(a).astype(precision.storage_dtype, copy=False)
         ctx.rsvd_dense(host, rank, 0, _lib.POWER_AUTO, seed)
     return ctx.last_power()[0]
+
+
+def full_svd(pool, a, config=None, *, threads: int = 1, runner=None, clock=None):
+    """Exact thin SVD, no sketching (pipeline.py:628-716), every step on the
+    device: thin QR of the tall orientation (CholQR2 with the Householder
+    fallback), the SVD of the min(m, n)-square R (Jacobi), and the big factor
+    Q U_R (GEMM). Sparse input is densified first (_densify, 419-436). The
+    small factor of the tall orientation is V (m >= n) or U (m < n), like
+    the reference; results are registered as "U", "S", "V"."""
+    m, n = a.shape
+    precision = as_precision(config.precision if config is not None else a.desc.precision)
+    if precision is Precision.HALF:
+        raise XsvdError("half precision (storage-only in the reference) is not built on the GPU path")
+    dt = np.float64 if precision is Precision.DOUBLE else np.float32
+    clock = clock or (runner.clock if runner is not None else StageClock())
+    ctx = _lib.load()
+    with clock.timing(STAGE_SVD_PREP):
+        arr = np.asarray(stored_to_array(a), dtype=dt)
+        tall = np.ascontiguousarray(arr if m >= n else arr.T)
+    with clock.timing(STAGE_ORTHO):
+        q, r, deficient = ctx.thin_qr(tall)
+    with clock.timing(STAGE_SVD):
+        u_r, s, v_r = ctx.svd_small(r)
+    with clock.timing(STAGE_POST):
+        big = ctx.gemm(q, np.ascontiguousarray(u_r, dtype=dt))
+    small, big_id, small_id = v_r, ("U" if m >= n else "V"), ("V" if m >= n else "U")
+    register_dense(pool, "S", s.reshape(-1, 1), Precision.DOUBLE)
+    mats = {big_id: register_dense(pool, big_id, big.astype(precision.storage_dtype, copy=False),
+                                   precision),
+            small_id: register_dense(pool, small_id,
+                                     small.astype(precision.storage_dtype, copy=False), precision)}
+    return RsvdResult(u=mats["U"], s=np.asarray(s, dtype=np.float64), v=mats["V"], chosen_q=0,
+                      stage_seconds=dict(clock.seconds), deficient_columns=tuple(deficient))

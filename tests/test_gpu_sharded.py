@@ -77,3 +77,49 @@ def test_sharded_rank_deficiency_is_reported(world1):
     a = rng.standard_normal((500, 8)) @ rng.standard_normal((8, 300))  # rank 8 < l = 20
     with pytest.raises(ConvergenceError):
         randomized_svd_sharded(world1, torch.from_numpy(a).cuda(), 500, 15, 5, 1, 1)
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_colsharded_world1_equals_unsharded(world1, dtype):
+    """Config 5's column layout through NCCL (world 1): identical to the
+    unsharded engine (all-reduces are identities, same kernels)."""
+    import torch
+
+    from paper_1907_06470_b200.distributed import randomized_svd_colsharded
+    from paper_1907_06470_b200.workloads import dense_lowrank_np
+
+    npdt = np.float64 if dtype == "float64" else np.float32
+    a = dense_lowrank_np(1100, 3200, "pow-1.5", 1e-8, 41, 42).astype(npdt)
+    at = torch.from_numpy(a).cuda()
+    u, s, v = randomized_svd_colsharded(world1, at, 3200, 0, 40, 10, 2, 7)
+    u0 = torch.empty_like(u)
+    v0 = torch.empty_like(v)
+    s0 = torch.empty_like(s)
+    world1.rsvd_dense_dev(npdt, 1100, 3200, at.data_ptr(), 3200, 40, 10, 2, 7, u0.data_ptr(),
+                          s0.data_ptr(), v0.data_ptr())
+    assert torch.equal(s, s0)
+    assert torch.equal(u, u0)
+    assert torch.equal(v, v0)
+
+
+def test_colsharded_block_offsets_omega(world1):
+    """A column block at col0 > 0 uses Omega's rows col0.. (keyed by index):
+    the world-1 call on A[:, c0:] equals the oracle run with that Omega block."""
+    import torch
+
+    from oracle import pipeline as OP
+    from oracle import rng as R
+    from paper_1907_06470_b200.distributed import randomized_svd_colsharded
+    from paper_1907_06470_b200.workloads import dense_lowrank_np
+
+    m, n, c0, k, p, q, seed = 600, 2000, 700, 20, 10, 1, 3
+    a = dense_lowrank_np(m, n, "pow-1.5", 1e-8, 51, 52)
+    blk = np.ascontiguousarray(a[:, c0:])
+    # world 1 sees only its block: n_global = c0 + block width keeps Omega's rows c0..n-1
+    u, s, v = randomized_svd_colsharded(world1, torch.from_numpy(blk).cuda(), n, c0, k, p, q,
+                                        seed)
+    om = R.gaussian_band(seed, 0, n, k + p)[c0:]
+    ref = OP.rsvd_reorth(blk, k, p, q, seed, "double", fast=True, om=om)
+    assert M.sigma_rel(s.cpu().numpy(), ref.s) <= 1e-10
+    assert M.sin_angle(u.cpu().numpy(), ref.u) <= 1e-8
+    assert M.sin_angle(v.cpu().numpy(), ref.v) <= 1e-8
