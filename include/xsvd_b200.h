@@ -119,6 +119,11 @@ int xb_rsvd_dense(xb_ctx* ctx, int dtype, int64_t m, int64_t n, const void* A, i
  * chosen q and its nu sequence (up to cap values, *count = how many). The
  * out-of-core streamer does not support XB_POWER_AUTO (XB_EUNSUPPORTED). */
 #define XB_POWER_AUTO (-1)
+/* RsvdConfig.gram_path (pipeline.py:526-580) for the next factorisations on
+ * this context: B^T of the power matrix (Q^T (A A^T)^q A)^T by 2q more thin
+ * products, the l x l Gram B B^T factored by Jacobi, sigma = sqrt(eig)^(1/(2q+1)),
+ * V = B^T U_B with unit columns. Not supported by the out-of-core streamer. */
+int xb_set_gram_path(xb_ctx* ctx, int on);
 int xb_set_power_auto(xb_ctx* ctx, int q_max, double tau);
 int xb_last_power(xb_ctx* ctx, int* chosen_q, double* nus, int cap, int* count);
 

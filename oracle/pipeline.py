@@ -204,3 +204,32 @@ def sketch_power_auto(a, k, p, seed, precision="double", *, q_max=5, tau=1e-6, f
             break
         prev_rho = rho
     return chosen, nus
+
+
+def rsvd_reorth_gram(a, k, p, q, seed, precision="double", *, fast=True, om=None):
+    """xsvd-reorth range finder + the gram_path projection and small SVD of
+    src/pipeline.py:526-580: B^T = (Q^T (A A^T)^q A)^T by 2q raw products,
+    G = B B^T, svd_small(G) (eigen-decomposition, sign rule), sigma =
+    sqrt(max(eig, 0))^(1/(2q+1)) (q > 0), V = B^T U_B with unit columns."""
+    _check(a, k, p)
+    m, n = a.shape
+    l = k + p
+    o = omega(seed, n, l, precision) if om is None else om
+    qm, _, deficient = _qr(_mul(a, o, precision, fast), precision, fast)
+    for _ in range(q):
+        qz, _, _ = _qr(_mul(_transpose(a), qm, precision, fast), precision, fast)
+        qm, _, deficient = _qr(_mul(a, qz, precision, fast), precision, fast)
+    w = _mul(_transpose(a), qm, precision, fast)             # B^T
+    for _ in range(q):
+        w = _mul(_transpose(a), _mul(a, w, precision, fast), precision, fast)
+    w = np.asarray(w, dtype=np.float64)
+    g = w.T @ w
+    u_b, eig, _ = _svd(g, fast)
+    sig = np.sqrt(np.maximum(eig, 0.0))
+    s = sig ** (1.0 / (2 * q + 1)) if q > 0 else sig
+    v = w @ u_b
+    norms = np.sqrt(np.sum(v * v, axis=0))
+    nz = norms > 0
+    v[:, nz] /= norms[nz]
+    u = _mul(qm, u_b[:, :k], precision, fast)
+    return OracleResult(u, s[:k].astype(np.float64), v[:, :k].astype(STORAGE[precision]), deficient)

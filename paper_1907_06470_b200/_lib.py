@@ -42,6 +42,7 @@ SIGNATURES = [
     ("xb_fp64_peaks", _int, [_vp, _dp, _dp]),
     ("xb_set_power_auto", _int, [_vp, _int, C.c_double]),
     ("xb_last_power", _int, [_vp, _intp, _vp, _int, _intp]),
+    ("xb_set_gram_path", _int, [_vp, _int]),
     ("xb_rsvd_dense", _int, [_vp, _int, _i64, _i64, _vp, _i64, _vp, _u64, _int, _int, _int,
                              _vp, _i64, _vp, _vp, _i64, _vp, _intp, _vp]),
     ("xb_rsvd_dense_dev", _int, [_vp, _int, _i64, _i64, _vp, _i64, _vp, _u64, _int, _int, _int,
@@ -143,6 +144,10 @@ class Context:
     def set_power_auto(self, q_max: int = 5, tau: float = 1e-6):
         """Stopping-rule parameters for calls made with q = POWER_AUTO."""
         _check(self.lib.xb_set_power_auto(self.h, int(q_max), float(tau)))
+
+    def set_gram_path(self, on: bool):
+        """RsvdConfig.gram_path for the following factorisations."""
+        _check(self.lib.xb_set_gram_path(self.h, int(bool(on))))
 
     def last_power(self):
         """(chosen q, nu sequence) of the last factorisation."""

@@ -169,6 +169,10 @@ void launch_householder_fallback(const double* X, int64_t ldx, int64_t rows, int
 // M (l x l, ld) := identity when *flag != 0
 void launch_identity_if(double* M, int64_t ld, int l, const int* flag, cudaStream_t st);
 void launch_identity(double* M, int64_t ld, int l, cudaStream_t st);
+// gram_path helpers: s_i = sqrt(max(s_i, 0))^exponent; V[:, j] /= sqrt(D_jj) (D_jj > 0)
+void launch_gram_sigma(double* s, int l, double exponent, cudaStream_t st);
+void launch_scale_cols_by_diag(double* V, int64_t ldv, int64_t rows, int k, const double* D,
+                               int64_t ldd, cudaStream_t st);
 // out (device) = ||M||_F over n contiguous doubles; M /= out when out > 0
 void launch_frob_normalise(double* M, int64_t n, double* out, cudaStream_t st);
 void launch_deficient(const double* R, int64_t ldr, int l, double eps, int* count, int* cols,

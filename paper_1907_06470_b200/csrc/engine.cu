@@ -56,6 +56,9 @@ struct xb_ctx {
   double auto_tau = 1e-6;
   int last_q = -1;
   std::vector<double> last_nus;
+  // RsvdConfig.gram_path (xb_set_gram_path): project the power matrix and
+  // factor its Gram (pipeline.py:526-580)
+  bool gram_path = false;
   // per-kernel profiling of the products on A (xb_profile_*)
   bool profiling = false;
   // kind: 0 FP64 DMMA tile GEMM, 1 tcgen05 3xTF32 GEMM, 2 int8-slice
@@ -875,6 +878,30 @@ void rsvd_impl(xb_ctx* c, const AOp& op_in, int64_t m, int64_t n, const void* d_
 
   clk.enter(kProject);
   op_tn(c, op, m, n, Qm, Zn, lp, l);  // B^T = A^T Q
+  if (c->gram_path) {
+    // gram_path (pipeline.py:526-580): B^T of the power matrix,
+    // (Q^T (A A^T)^q A)^T, as 2q thin products (raw, as the reference), then
+    // the l x l Gram G = B B^T, its SVD (= eigen-decomposition, Jacobi on the
+    // symmetric G), sigma = sqrt(eig)^(1/(2q+1)), V = B^T U_B with unit
+    // columns, U = Q U_B.
+    const int qg = c->last_q;
+    for (int i = 0; i < qg; ++i) {
+      op_nn(c, op, m, n, Zn, Tm, lp, l);  // A B^T
+      op_tn(c, op, m, n, Tm, Zn, lp, l);  // A^T (A B^T)
+    }
+    clk.enter(kSvdPrep);
+    gemm(c, true, lp, lp, n, Zn, lp, Zn, lp, s.G, lp);  // full G (Jacobi reads all of it)
+    if (csharded) nccl_allreduce_sum(s.comm, s.G, (size_t)lp * lp, st);
+    clk.enter(kSvd);
+    launch_jacobi_svd(s.G, lp, l, k, Ub, lp, sv, Wk, kp, jw, jstat, st);
+    launch_gram_sigma(sv, l, qg > 0 ? 1.0 / (2 * qg + 1) : 1.0, st);
+    clk.enter(kPost);
+    gemm(c, false, m, k, lp, Qm, lp, Ub, lp, out.U, out.ldu);    // U = Q U_B[:, :k]
+    gemm(c, false, n, k, lp, Zn, lp, Ub, lp, out.V, out.ldv);    // V = B^T U_B[:, :k]
+    gemm(c, true, k, k, n, out.V, out.ldv, out.V, out.ldv, s.Rs, k);  // column norms^2
+    if (csharded) nccl_allreduce_sum(s.comm, s.Rs, (size_t)k * k, st);
+    launch_scale_cols_by_diag(out.V, out.ldv, n, k, s.Rs, k, st);
+  } else {
 
   clk.enter(kSvdPrep);
   // float32 configs: ONE CholQR pass of B^T and Q_B is never formed,
@@ -908,6 +935,7 @@ void rsvd_impl(xb_ctx* c, const AOp& op_in, int64_t m, int64_t n, const void* d_
     gemm(c, false, n, k, lp, Zn, lp, lift, kp, out.V, out.ldv);  // V = B^T R_B^-1 W_k
   } else {
     gemm(c, false, n, k, lp, Qn, lp, Wk, kp, out.V, out.ldv);  // V = Q_B W_k
+  }
   }
   XB_CUDA(cudaMemcpyAsync(out.s, sv, k * sizeof(double), cudaMemcpyDeviceToDevice, st));
 
@@ -1049,6 +1077,7 @@ void rsvd_stream(xb_ctx* c, const void* hostA, int64_t host_lda, bool f32, int64
                  int32_t* deficient, int* ndeficient, double* stage_seconds) {
   check_dims(m, n, k, p, q);
   XB_REQUIRE(q >= 0, XB_EUNSUPPORTED, "power='auto' is not built for the out-of-core streamer");
+  XB_REQUIRE(!c->gram_path, XB_EUNSUPPORTED, "gram_path is not built for the out-of-core streamer");
   const int l = k + p;
   const int lp = (int)round_up(l, 8);
   const int kp = (int)round_up(k, 2);
@@ -1302,6 +1331,13 @@ int xb_last_power(xb_ctx* c, int* chosen_q, double* nus, int cap, int* count) {
     const int nn = (int)c->last_nus.size();
     if (count) *count = nn;
     for (int i = 0; nus && i < nn && i < cap; ++i) nus[i] = c->last_nus[i];
+  });
+}
+
+int xb_set_gram_path(xb_ctx* c, int on) {
+  return guarded([&] {
+    XB_REQUIRE(c, XB_EVALUE, "null context");
+    c->gram_path = on != 0;
   });
 }
 

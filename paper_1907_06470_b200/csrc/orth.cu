@@ -255,6 +255,27 @@ __global__ void __launch_bounds__(1024) frob_normalise_kernel(double* __restrict
   }
 }
 
+// gram_path: s_i = sqrt(max(eig_i, 0))^e (pipeline.py:569-571)
+__global__ void gram_sigma_kernel(double* __restrict__ s, int l, double e) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < l) {
+    const double sp = sqrt(fmax(s[i], 0.0));
+    s[i] = e == 1.0 ? sp : pow(sp, e);
+  }
+}
+
+// V[:, j] /= sqrt(D[j][j]) where D[j][j] > 0 (unit columns, pipeline.py:573-575)
+__global__ void scale_cols_kernel(double* __restrict__ V, int64_t ldv, int64_t rows, int k,
+                                  const double* __restrict__ D, int64_t ldd) {
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < rows * k;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = idx / k;
+    const int j = (int)(idx - r * k);
+    const double d = D[(int64_t)j * ldd + j];
+    if (d > 0.0) V[r * ldv + j] /= sqrt(d);
+  }
+}
+
 }  // namespace
 
 void launch_identity(double* M, int64_t ld, int l, cudaStream_t st) {
@@ -266,6 +287,19 @@ void launch_identity(double* M, int64_t ld, int l, cudaStream_t st) {
 void launch_frob_normalise(double* M, int64_t n, double* out, cudaStream_t st) {
   frob_normalise_kernel<<<1, 1024, 0, st>>>(M, n, out);
   check_launch("frob_normalise");
+}
+
+void launch_gram_sigma(double* s, int l, double exponent, cudaStream_t st) {
+  gram_sigma_kernel<<<(l + 255) / 256, 256, 0, st>>>(s, l, exponent);
+  check_launch("gram_sigma");
+}
+
+void launch_scale_cols_by_diag(double* V, int64_t ldv, int64_t rows, int k, const double* D,
+                               int64_t ldd, cudaStream_t st) {
+  if (rows <= 0 || k <= 0) return;
+  scale_cols_kernel<<<(unsigned)std::min<int64_t>(ceil_div(rows * k, 256), 4096), 256, 0, st>>>(
+      V, ldv, rows, k, D, ldd);
+  check_launch("scale_cols");
 }
 
 void launch_identity_if(double* M, int64_t ld, int l, const int* flag, cudaStream_t st) {

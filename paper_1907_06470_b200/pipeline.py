@@ -19,7 +19,8 @@ device: up to q_max passes, stopped by the reference's rule on
 nu_q = ||(A A^T)^q A Omega||_F / sqrt(m l), whose raw-product norms are
 carried through the re-orthonormalised iteration as small triangular factors
 (engine.cu AutoPower); `auto_select_q` (396-418) is the same loop on a
-rank-wide probe. Out of scope (fail loudly): gram_path=True and the
+rank-wide probe. gram_path=True (526-580) projects the power matrix and
+factors its Gram on the device too. Out of scope (fail loudly): the
 store-backed durable plan (PlanRunner records, resume).
 """
 
@@ -142,8 +143,6 @@ def randomized_svd(pool, a, config: RsvdConfig, *, threads: int = 1, runner=None
     if r_work > min(m, n):
         raise ShapeError(f"rank {config.rank} (+{config.oversample} oversampling) exceeds "
                          f"min{tuple(a.shape)} = {min(m, n)}")
-    if config.gram_path:
-        raise XsvdError("gram_path=True is outside the GPU hot path")
     precision = as_precision(config.precision)
     if precision is Precision.HALF:
         raise XsvdError("half precision (storage-only in the reference) is not built on the GPU path")
@@ -153,18 +152,22 @@ def randomized_svd(pool, a, config: RsvdConfig, *, threads: int = 1, runner=None
     q = _lib.POWER_AUTO if auto else int(config.power)
     if auto:
         ctx.set_power_auto(config.q_max, config.tau)
-    if is_sparse(a):
-        if precision is not Precision.DOUBLE:
-            raise XsvdError("sparse A is built for float64 only")
-        rows, cols, vals = canonical_coo(a)
-        if a.desc.transposed:
-            rows, cols = cols, rows
-        u, s, v, deficient, stages = ctx.rsvd_coo(rows, cols, vals, tuple(a.shape), config.rank,
-                                                  config.oversample, q, config.seed)
-    else:
-        host = _dense_input(a).astype(precision.storage_dtype, copy=False)
-        u, s, v, deficient, stages = ctx.rsvd_dense(host, config.rank, config.oversample, q,
-                                                    config.seed)
+    ctx.set_gram_path(config.gram_path)
+    try:
+        if is_sparse(a):
+            if precision is not Precision.DOUBLE:
+                raise XsvdError("sparse A is built for float64 only")
+            rows, cols, vals = canonical_coo(a)
+            if a.desc.transposed:
+                rows, cols = cols, rows
+            u, s, v, deficient, stages = ctx.rsvd_coo(rows, cols, vals, tuple(a.shape), config.rank,
+                                                      config.oversample, q, config.seed)
+        else:
+            host = _dense_input(a).astype(precision.storage_dtype, copy=False)
+            u, s, v, deficient, stages = ctx.rsvd_dense(host, config.rank, config.oversample, q,
+                                                        config.seed)
+    finally:
+        ctx.set_gram_path(False)  # context state must not leak into other calls
     chosen_q = ctx.last_power()[0] if auto else int(config.power)
     for name, sec in zip(STAGE_NAMES, stages):
         clock.seconds[name] += float(sec)
@@ -191,6 +194,7 @@ def auto_select_q(pool, a, rank, *, q_max: int = 5, tau: float = 1e-6, seed: int
         raise ValueError(f"q_max must be nonnegative, got {q_max}")
     ctx = _lib.load()
     ctx.set_power_auto(q_max, tau)
+    ctx.set_gram_path(False)
     if is_sparse(a):
         if precision is not Precision.DOUBLE:
             raise XsvdError("sparse A is built for float64 only")

@@ -268,6 +268,30 @@ def gen_autoq():
     save("autoq", **out)
 
 
+def gen_gram():
+    """gram_path=True (pipeline.py:526-580) through the reference's own
+    randomized_svd: the cases of its tests (test_pipeline.py:244-282) plus a
+    decaying-spectrum matrix."""
+    out = {}
+    rng = np.random.default_rng(12)
+    cases = [("diag", np.diag([2.0, 1.0]), 2, 0, 1, 0),
+             ("rank8", rng.standard_normal((50, 8)) @ rng.standard_normal((8, 45)), 8, 0, 1, 0),
+             ("rank5_q0", np.random.default_rng(20).standard_normal((40, 5))
+              @ np.random.default_rng(21).standard_normal((5, 35)), 5, 0, 0, 0),
+             ("geom", dense_lowrank_np(300, 200, "geom0.9", 1e-8, 901, 902), 5, 5, 1, 3)]
+    for name, a, k, p, q, seed in cases:
+        pool = BlockPool()
+        ma = dense(pool, "A", a)
+        res = randomized_svd(pool, ma, RsvdConfig(rank=k, oversample=p, power=q, seed=seed,
+                                                  gram_path=True))
+        out[f"{name}_a"] = a
+        out[f"{name}_cfg"] = np.array([k, p, q, seed])
+        out[f"{name}_s"] = res.s
+        out[f"{name}_u"] = res.u.to_array()
+        out[f"{name}_v"] = res.v.to_array()
+    save("gram", **out)
+
+
 if __name__ == "__main__":
     assert xsvd.__file__.startswith("/root/reference"), xsvd.__file__
     which = sys.argv[1:] or ["rng", "multiply", "qr", "svd", "rsvd", "cfg1"]

@@ -165,3 +165,20 @@ def test_power_auto_golden(name):
     ref = g[f"{name}_nus"]
     assert len(nus) == len(ref)
     assert np.allclose(nus, ref, rtol=1e-12, atol=0.0)
+
+
+GRAM_CASES = ["diag", "rank8", "rank5_q0", "geom"]
+
+
+@pytest.mark.parametrize("name", GRAM_CASES)
+def test_gram_path_golden(name):
+    """gram_path restated (oracle.pipeline.rsvd_reorth_gram) against the
+    reference's randomized_svd(gram_path=True) on exact-rank / well-resolved
+    inputs, where the shipped and re-orthonormalised range finders agree."""
+    g = golden("gram")
+    k, p, q, seed = (int(x) for x in g[f"{name}_cfg"])
+    r = P.rsvd_reorth_gram(g[f"{name}_a"], k, p, q, seed)
+    ref_s = g[f"{name}_s"]
+    assert np.max(np.abs(r.s - ref_s)) / ref_s[0] <= 1e-12
+    assert M.sin_angle(r.u, g[f"{name}_u"]) <= 1e-12
+    assert M.sin_angle(r.v, g[f"{name}_v"]) <= 1e-12
