@@ -24,7 +24,8 @@
  *
  * Status codes map onto the reference exception taxonomy (errors.py):
  *   XB_ESHAPE -> ShapeError, XB_EVALUE -> ValueError, XB_ENOMEM -> BudgetError,
- *   XB_ECONV -> ConvergenceError, XB_ECUDA / XB_ENCCL / XB_EUNSUPPORTED -> XsvdError.
+ *   XB_ECONV -> ConvergenceError, XB_EPARSE -> ParseError (with the 1-based
+ *   line, returned separately), XB_ECUDA / XB_ENCCL / XB_EUNSUPPORTED -> XsvdError.
  */
 #ifndef XSVD_B200_H
 #define XSVD_B200_H
@@ -46,7 +47,8 @@ enum xb_status {
   XB_ECONV = 4,
   XB_ECUDA = 5,
   XB_ENCCL = 6,
-  XB_EUNSUPPORTED = 7
+  XB_EUNSUPPORTED = 7,
+  XB_EPARSE = 8
 };
 
 /* Precision.DOUBLE / Precision.SINGLE storage dtypes (core.py:26-46). */
@@ -196,6 +198,29 @@ int xb_rsvd_csr_dev(xb_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const int64_
                     uint64_t seed, int k, int p, int q, double* dU, int64_t ldu, double* d_s,
                     double* dV, int64_t ldv, int32_t* deficient, int* ndeficient,
                     double* stage_seconds);
+/* Matrix Market coordinate input (formats.py:143-323, 381-395), parsed
+ * natively with `threads` host threads (0 = all). Triplets are 0-based, in
+ * the reference's order (per `chunk_lines` body lines, 0 = 500000: the
+ * chunk's entries in file order, then its mirrored off-diagonal entries when
+ * the file is symmetric); duplicates are NOT summed here (the pool /
+ * device CSR builder does that). Malformed input returns XB_EPARSE with the
+ * 1-based line in *err_line and the reference's message in xb_last_error.
+ * Feed the arrays to xb_rsvd_coo / xb_spmm_coo (sorted by the library) or
+ * register them in a pool; release with xb_coo_free. field: 0 real,
+ * 1 integer, 2 pattern (values 1.0). */
+typedef struct {
+  int64_t rows, cols, nnz;
+  int64_t* r;
+  int64_t* c;
+  double* v;
+  int field, symmetric;
+} xb_coo;
+int xb_mm_info(const char* path, int64_t* rows, int64_t* cols, int64_t* entries, int* field,
+               int* symmetric, int64_t* err_line);
+int xb_mm_read(const char* path, int threads, int64_t chunk_lines, xb_coo* out,
+               int64_t* err_line);
+void xb_coo_free(xb_coo* coo);
+
 /* Sparse product step (block_multiply with a sparse left operand,
  * kernels.py:85-97, or its transposed view, pool.py:420-445): Y = op(A) X
  * with op(A) = A (trans = 0, X n x l, Y m x l) or A^T (trans = 1, X m x l,

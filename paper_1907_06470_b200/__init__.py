@@ -14,7 +14,8 @@ libxsvdb200.so, C ABI in include/xsvd_b200.h). There is no CPU fallback.
 
 from .core import (CANONICAL_CELL, BlockPartition, DenseBlock, Density, MatrixDescriptor,
                    Precision, SparseBlock, transpose_view, wider)
-from .errors import BudgetError, ConvergenceError, ShapeError, XsvdError
+from .errors import BudgetError, ConvergenceError, ParseError, ShapeError, XsvdError
+from .formats import parse_matrix_market, read_matrix_market_info, write_matrix_market
 from .kernels import MultiplyStats, QRResult, SmallSVDResult, block_multiply, gram, svd_small, thin_qr
 from .pipeline import (STAGE_NAMES, RsvdConfig, RsvdResult, StageClock, auto_select_q, full_svd,
                        gaussian_matrix,
@@ -23,7 +24,8 @@ from .pool import BlockPool, StoredMatrix, create_matrix, matrix_from_coo, matri
 
 __all__ = [
     "BlockPartition", "BlockPool", "BudgetError", "CANONICAL_CELL", "ConvergenceError",
-    "DenseBlock", "Density", "MatrixDescriptor", "MultiplyStats", "Precision", "QRResult",
+    "DenseBlock", "Density", "MatrixDescriptor", "MultiplyStats", "ParseError", "Precision",
+    "QRResult", "parse_matrix_market", "read_matrix_market_info", "write_matrix_market",
     "RsvdConfig", "RsvdResult", "STAGE_NAMES", "ShapeError", "SmallSVDResult", "SparseBlock",
     "StageClock", "StoredMatrix", "XsvdError", "block_multiply", "create_matrix",
     "auto_select_q", "full_svd", "gaussian_matrix", "gram", "matrix_from_coo", "matrix_from_dense", "randomized_svd",

@@ -67,7 +67,55 @@ SIGNATURES = [
     ("xb_gemm_dev", _int, [_vp, _int, _int, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64]),
     ("xb_thin_qr", _int, [_vp, _int, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp, _intp]),
     ("xb_svd_small", _int, [_vp, _i64, _i64, _vp, _i64, _vp, _vp, _vp]),
+    ("xb_mm_info", _int, [C.c_char_p, _vp, _vp, _vp, _intp, _intp, _vp]),
+    ("xb_mm_read", _int, [C.c_char_p, _int, _i64, _vp, _vp]),
+    ("xb_coo_free", None, [_vp]),
 ]
+
+
+class XbCoo(C.Structure):
+    """xb_coo (include/xsvd_b200.h)."""
+    _fields_ = [("rows", C.c_int64), ("cols", C.c_int64), ("nnz", C.c_int64),
+                ("r", C.POINTER(C.c_int64)), ("c", C.POINTER(C.c_int64)),
+                ("v", C.POINTER(C.c_double)), ("field", C.c_int), ("symmetric", C.c_int)]
+
+
+FIELDS = {0: "real", 1: "integer", 2: "pattern"}
+
+
+def mm_info(path: str) -> dict:
+    """Matrix Market header + size line (xb_mm_info; no device needed)."""
+    lib = lib_handle()
+    rows, cols, ent, line = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
+    field, sym = C.c_int(), C.c_int()
+    st = lib.xb_mm_info(os.fsencode(path), C.byref(rows), C.byref(cols), C.byref(ent),
+                        C.byref(field), C.byref(sym), C.byref(line))
+    if st != 0:
+        raise_for_status(st, lib.xb_last_error().decode(errors="replace"), line.value or None)
+    return {"rows": rows.value, "cols": cols.value, "entries": ent.value,
+            "field": FIELDS[field.value], "symmetric": bool(sym.value)}
+
+
+def mm_read(path: str, threads: int = 0, chunk_lines: int = 0):
+    """Parse a Matrix Market coordinate file natively (xb_mm_read): returns
+    (rows, cols, r, c, v, info) with 0-based int64 triplets in the
+    reference's order, duplicates not yet summed."""
+    lib = lib_handle()
+    coo = XbCoo()
+    line = C.c_int64()
+    st = lib.xb_mm_read(os.fsencode(path), int(threads), int(chunk_lines), C.byref(coo),
+                        C.byref(line))
+    if st != 0:
+        raise_for_status(st, lib.xb_last_error().decode(errors="replace"), line.value or None)
+    try:
+        n = coo.nnz
+        r = np.ctypeslib.as_array(coo.r, shape=(n,)).copy() if n else np.zeros(0, np.int64)
+        c = np.ctypeslib.as_array(coo.c, shape=(n,)).copy() if n else np.zeros(0, np.int64)
+        v = np.ctypeslib.as_array(coo.v, shape=(n,)).copy() if n else np.zeros(0)
+    finally:
+        lib.xb_coo_free(C.byref(coo))
+    return coo.rows, coo.cols, r, c, v, {"field": FIELDS[coo.field],
+                                         "symmetric": bool(coo.symmetric)}
 
 
 def lib_handle():

@@ -19,6 +19,32 @@ struct Error : std::runtime_error {
   Error(int s, const std::string& msg) : std::runtime_error(msg), status(s) {}
 };
 
+// A malformed text input (XB_EPARSE) with its 1-based line (mmio.cu).
+struct ParseFaultError : Error {
+  int64_t line;
+  ParseFaultError(int64_t l, const std::string& m);
+};
+
+// The C boundary: run f, turn exceptions into a status + thread-local
+// message (xb_last_error). set_last_error lives in engine.cu.
+void set_last_error(const std::string& msg);
+template <typename F>
+int guarded_api(F&& f) {
+  try {
+    f();
+    return XB_OK;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return e.status;
+  } catch (const std::bad_alloc&) {
+    set_last_error("host allocation failed");
+    return XB_ENOMEM;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return XB_ECUDA;
+  }
+}
+
 #define XB_CUDA(call)                                                                   \
   do {                                                                                  \
     cudaError_t _e = (call);                                                            \

@@ -1860,3 +1860,7 @@ int xb_svd_small(xb_ctx* c, int64_t r, int64_t n, const double* B, int64_t ldb, 
 }
 
 }  // extern "C"
+
+namespace xb {
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+}  // namespace xb

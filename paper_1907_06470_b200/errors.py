@@ -27,10 +27,24 @@ class ConvergenceError(XsvdError):
         self.residual = residual
 
 
+class ParseError(XsvdError):
+    """A text input (Matrix Market header or body) is malformed; carries the
+    1-based line where the problem was found (errors.py:12-23)."""
+
+    def __init__(self, message, line=None):
+        if line is not None:
+            message = f"line {line}: {message}"
+        super().__init__(message)
+        self.line = line
+
+
 XB_ESHAPE, XB_EVALUE, XB_ENOMEM, XB_ECONV, XB_ECUDA, XB_ENCCL, XB_EUNSUPPORTED = 1, 2, 3, 4, 5, 6, 7
+XB_EPARSE = 8
 
 
-def raise_for_status(status: int, message: str):
+def raise_for_status(status: int, message: str, line=None):
+    if status == XB_EPARSE:
+        raise ParseError(message, line)
     if status == XB_ESHAPE:
         raise ShapeError(message)
     if status == XB_EVALUE:

@@ -292,6 +292,81 @@ def gen_gram():
     save("gram", **out)
 
 
+def gen_mm():
+    """Matrix Market parsing (formats.py:143-395) by the reference: accepted
+    files -> the pooled matrix's sorted, duplicate-summed COO; rejected files
+    -> the ParseError line and message."""
+    import tempfile
+
+    from xsvd import ParseError
+    from xsvd.formats import parse_matrix_market, read_matrix_market_info
+
+    rng = np.random.default_rng(5)
+    n = 3000
+    keys = rng.choice(300 * 200, size=n, replace=True)  # with duplicates
+    rows, cols, vals = keys // 200 + 1, keys % 200 + 1, rng.standard_normal(n)
+    big = ["%%MatrixMarket matrix coordinate real general", "% generated", f"300 200 {n}"]
+    big += [f"{r} {c} {v:.17g}" for r, c, v in zip(rows, cols, vals)]
+    sym_keys = rng.choice(150 * 150, size=800, replace=False)
+    sr, sc = sym_keys // 150 + 1, sym_keys % 150 + 1
+    lo = np.maximum(sr, sc), np.minimum(sr, sc)
+    sym = ["%%MatrixMarket matrix coordinate real symmetric", f"150 150 {len(sym_keys)}"]
+    sym += [f"{a} {b} {v:.6e}" for a, b, v in zip(lo[0], lo[1], rng.standard_normal(800))]
+    texts = {
+        "general": "\n".join(big) + "\n",
+        "symmetric": "\n".join(sym) + "\n",
+        "pattern": "%%MatrixMarket matrix coordinate pattern general\n4 5 4\n1 2\n4 5\n2 2\n1 2\n",
+        "integer": "%%MatrixMarket matrix coordinate integer general\n3 3 3\n3 1 -3\n1.0 2 4e0\n2 3 +7\n",
+        "no_final_newline": "%%MatrixMarket matrix coordinate real general\n2 2 2\n1 1 1.5\n2 2 -0.25",
+        "crlf": "%%MatrixMarket matrix coordinate real general\r\n2 2 1\r\n2 1 3.5\r\n",
+        "zero_entries": "%%MatrixMarket matrix coordinate real general\n4 3 0\n",
+        "bad_banner": "1 1 1\n1 1 2.0\n",
+        "complex": "%%MatrixMarket matrix coordinate complex general\n1 1 1\n1 1 1.0 0.0\n",
+        "array": "%%MatrixMarket matrix array real general\n2 2\n1\n2\n3\n4\n",
+        "blank_before_size": "%%MatrixMarket matrix coordinate real general\n% c\n\n2 2 1\n1 2 9.0\n",
+        "bad_size": "%%MatrixMarket matrix coordinate real general\n2 x 1\n1 1 2.0\n",
+        "neg_dims": "%%MatrixMarket matrix coordinate real general\n0 2 1\n1 1 2.0\n",
+        "bad_token": "%%MatrixMarket matrix coordinate real general\n2 2 2\n1 1 1\n1 x 2.0\n",
+        "bad_value": "%%MatrixMarket matrix coordinate real general\n2 2 2\n1 1 1\n2 2 abc\n",
+        "row_oob": "%%MatrixMarket matrix coordinate real general\n2 2 1\n3 1 2.0\n",
+        "col_oob": "%%MatrixMarket matrix coordinate real general\n2 2 1\n1 0 2.0\n",
+        "frac_index": "%%MatrixMarket matrix coordinate real general\n2 2 1\n1.5 1 2.0\n",
+        "fields": "%%MatrixMarket matrix coordinate real general\n2 2 2\n1 1 2.0\n2 2\n",
+        "blank_body": "%%MatrixMarket matrix coordinate real general\n2 2 2\n1 1 2.0\n\n2 2 1.0\n",
+        "too_few": "%%MatrixMarket matrix coordinate real general\n2 2 5\n1 1 2.0\n",
+        "too_many": "%%MatrixMarket matrix coordinate real general\n2 2 1\n1 1 2.0\n2 2 3.0\n",
+        "above_diag": "%%MatrixMarket matrix coordinate real symmetric\n3 3 2\n2 1 1.0\n1 3 2.0\n",
+        "no_size": "%%MatrixMarket matrix coordinate real general\n% only comments\n",
+        "empty": "",
+    }
+    out = {}
+    with tempfile.TemporaryDirectory() as d:
+        for name, text in texts.items():
+            path = os.path.join(d, name + ".mtx")
+            with open(path, "w", newline="") as f:
+                f.write(text)
+            out[f"{name}_text"] = np.array(text)
+            pool = BlockPool()
+            try:
+                mat = parse_matrix_market(path, pool, "m", precision=Precision.DOUBLE)
+                r, c, v = mat.read_cell_sparse(0, mat.shape[0], 0, mat.shape[1])
+                out[f"{name}_shape"] = np.array(mat.shape)
+                out[f"{name}_r"], out[f"{name}_c"], out[f"{name}_v"] = r, c, v
+                info = read_matrix_market_info(path)
+                out[f"{name}_info"] = np.array([info["rows"], info["cols"], info["entries"],
+                                                int(info["symmetric"])])
+            except ParseError as e:
+                out[f"{name}_err_line"] = np.array(-1 if e.line is None else e.line)
+                out[f"{name}_err_msg"] = np.array(str(e))
+            except Exception as e:  # noqa: BLE001 - recorded, not hidden
+                # the reference's pandas path raises a bare ValueError for a
+                # non-numeric index under pandas 3 (its own test expects a
+                # ParseError there, tests/test_formats.py:98-115)
+                out[f"{name}_err_line"] = np.array(-2)
+                out[f"{name}_err_msg"] = np.array(f"{type(e).__name__}: {e}")
+    save("mm", **out)
+
+
 if __name__ == "__main__":
     assert xsvd.__file__.startswith("/root/reference"), xsvd.__file__
     which = sys.argv[1:] or ["rng", "multiply", "qr", "svd", "rsvd", "cfg1"]
