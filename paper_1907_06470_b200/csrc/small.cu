@@ -286,6 +286,70 @@ __device__ __forceinline__ void group_sum3(double& a, double& b, double& c) {
   }
 }
 
+// Single-CTA Jacobi tail: singular values = column norms of X, stable
+// descending order, U_B columns sign-fixed (largest |entry| positive,
+// earliest row on ties, kernels.py:556-561), W_k = matching columns of J.
+__device__ void jacobi_tail_1cta(const double* X, const double* J, int l, int k,
+                                 double* __restrict__ Ub, int64_t ldu, double* __restrict__ s_out,
+                                 double* __restrict__ Wk, int64_t ldw, double* gnorm, int* gperm,
+                                 int* gsign) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int kThreadsB = blockDim.x, kWarpsB = blockDim.x >> 5;
+  // singular values = column norms
+  for (int c = warp; c < l; c += kWarpsB) {
+    double a = 0.0;
+    for (int r = lane; r < l; r += 32) a += X[(int64_t)c * l + r] * X[(int64_t)c * l + r];
+    a = warp_sum32(a);
+    if (lane == 0) gnorm[c] = sqrt(a);
+  }
+  __syncthreads();
+  // stable descending order: rank = #{i: s_i > s_j} + #{i < j: s_i == s_j}
+  for (int j = tid; j < l; j += kThreadsB) {
+    const double sj = gnorm[j];
+    int rank = 0;
+    for (int i = 0; i < l; ++i) {
+      const double si = gnorm[i];
+      rank += (si > sj) || (si == sj && i < j);
+    }
+    gperm[rank] = j;
+  }
+  __syncthreads();
+  // sign rule on U_B columns: largest |entry| positive, earliest row on ties
+  for (int i = warp; i < l; i += kWarpsB) {
+    const int c = gperm[i];
+    double best = -1.0;
+    int brow = 0;
+    for (int r = lane; r < l; r += 32) {
+      const double v = fabs(X[(int64_t)c * l + r]);
+      if (v > best) {
+        best = v;
+        brow = r;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int orow = __shfl_xor_sync(0xffffffffu, brow, o);
+      if (ob > best || (ob == best && orow < brow)) {
+        best = ob;
+        brow = orow;
+      }
+    }
+    if (lane == 0) gsign[i] = (X[(int64_t)c * l + brow] < 0.0) ? -1 : 1;
+  }
+  __syncthreads();
+  for (int i = tid; i < l; i += kThreadsB) s_out[i] = gnorm[gperm[i]];
+  for (int r = warp; r < l; r += kWarpsB)
+    for (int i = lane; i < l; i += 32) {
+      const int c = gperm[i];
+      const double sc = gnorm[c];
+      const double inv = sc > 0.0 ? 1.0 / sc : 0.0;
+      Ub[(int64_t)r * ldu + i] = gsign[i] * X[(int64_t)c * l + r] * inv;
+    }
+  for (int r = warp; r < l; r += kWarpsB)
+    for (int i = lane; i < k; i += 32) Wk[(int64_t)r * ldw + i] = gsign[i] * J[(int64_t)gperm[i] * l + r];
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
     jacobi_kernel(const double* __restrict__ Rm, int64_t ldr, int l, int k, double* __restrict__ Ub,
                   int64_t ldu, double* __restrict__ s_out, double* __restrict__ Wk, int64_t ldw,
@@ -362,59 +426,111 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (!rotated) break;
   }
   if (tid == 0) *status = (sweep >= max_sweeps) ? 1 : 0;
-  // singular values = column norms
-  for (int c = warp; c < l; c += kWarps) {
-    double a = 0.0;
-    for (int r = lane; r < l; r += 32) a += X[(int64_t)c * l + r] * X[(int64_t)c * l + r];
-    a = warp_sum32(a);
-    if (lane == 0) gnorm[c] = sqrt(a);
-  }
-  __syncthreads();
-  // stable descending order: rank = #{i: s_i > s_j} + #{i < j: s_i == s_j}
-  for (int j = tid; j < l; j += kThreads) {
-    const double sj = gnorm[j];
-    int rank = 0;
-    for (int i = 0; i < l; ++i) {
-      const double si = gnorm[i];
-      rank += (si > sj) || (si == sj && i < j);
-    }
-    gperm[rank] = j;
-  }
-  __syncthreads();
-  // sign rule on U_B columns: largest |entry| positive, earliest row on ties
-  for (int i = warp; i < l; i += kWarps) {
-    const int c = gperm[i];
-    double best = -1.0;
-    int brow = 0;
+  jacobi_tail_1cta(X, J, l, k, Ub, ldu, s_out, Wk, ldw, gnorm, gperm, gsign);
+}
+
+// Single-CTA one-sided Jacobi with the pair's columns in REGISTERS
+// (l <= 16 NR <= 128, X and J both in shared memory: 2 l^2 doubles <= 225 KB).
+// Round-robin (circle) ordering: every round rotates the l/2 disjoint column
+// pairs in parallel, one 16-lane group per pair; each lane loads its NR
+// elements of x_p, x_q once, forms the three dot products, rotates in
+// registers and stores once (then the same for J) — one shared-memory pass
+// per column per round and one barrier per round.
+template <int NR>
+__global__ void __launch_bounds__(kThreads, 1)
+    jacobi_rr_kernel(const double* __restrict__ Rm, int64_t ldr, int l, int k,
+                     double* __restrict__ Ub, int64_t ldu, double* __restrict__ s_out,
+                     double* __restrict__ Wk, int64_t ldw, double* __restrict__ work,
+                     int* __restrict__ status, double tol, int max_sweeps) {
+  extern __shared__ __align__(16) double sm[];
+  const int64_t ll = (int64_t)l * l;
+  double* X = sm;
+  double* J = sm + ll;
+  double* gnorm = work + ll;
+  int* gperm = reinterpret_cast<int*>(gnorm + l);
+  int* gsign = gperm + l;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int grp = tid / kGroup, gl = tid % kGroup;
+  for (int c = warp; c < l; c += kWarps)
     for (int r = lane; r < l; r += 32) {
-      const double v = fabs(X[(int64_t)c * l + r]);
-      if (v > best) {
-        best = v;
-        brow = r;
-      }
+      X[(int64_t)c * l + r] = Rm[(int64_t)c * ldr + r];
+      J[(int64_t)c * l + r] = (r == c) ? 1.0 : 0.0;
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-      const int orow = __shfl_xor_sync(0xffffffffu, brow, o);
-      if (ob > best || (ob == best && orow < brow)) {
-        best = ob;
-        brow = orow;
-      }
-    }
-    if (lane == 0) gsign[i] = (X[(int64_t)c * l + brow] < 0.0) ? -1 : 1;
-  }
   __syncthreads();
-  for (int i = tid; i < l; i += kThreads) s_out[i] = gnorm[gperm[i]];
-  for (int r = warp; r < l; r += kWarps)
-    for (int i = lane; i < l; i += 32) {
-      const int c = gperm[i];
-      const double sc = gnorm[c];
-      const double inv = sc > 0.0 ? 1.0 / sc : 0.0;
-      Ub[(int64_t)r * ldu + i] = gsign[i] * X[(int64_t)c * l + r] * inv;
+  const int L2 = l + (l & 1);
+  const int npairs = L2 / 2;
+  const double tol2 = tol * tol;
+  const unsigned hmask = (threadIdx.x & 16) ? 0xffff0000u : 0x0000ffffu;
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    int rot = 0;
+    for (int round = 0; round < L2 - 1; ++round) {
+      if (grp < npairs) {
+        const int pa = grp, pb = L2 - 1 - grp;  // circle method: position 0 fixed
+        int p = pa == 0 ? 0 : 1 + (pa - 1 + round) % (L2 - 1);
+        int q = 1 + (pb - 1 + round) % (L2 - 1);
+        if (p > q) {
+          const int t = p;
+          p = q;
+          q = t;
+        }
+        if (q < l) {
+          double* xp = X + (int64_t)p * l;
+          double* xq = X + (int64_t)q * l;
+          double u[NR], v[NR];
+          double a = 0.0, b = 0.0, g = 0.0;
+#pragma unroll
+          for (int i = 0; i < NR; ++i) {
+            const int r = gl + kGroup * i;
+            u[i] = r < l ? xp[r] : 0.0;
+            v[i] = r < l ? xq[r] : 0.0;
+            a = fma(u[i], u[i], a);
+            b = fma(v[i], v[i], b);
+            g = fma(u[i], v[i], g);
+          }
+#pragma unroll
+          for (int o = kGroup / 2; o > 0; o >>= 1) {
+            a += __shfl_xor_sync(hmask, a, o);
+            b += __shfl_xor_sync(hmask, b, o);
+            g += __shfl_xor_sync(hmask, g, o);
+          }
+          if (g != 0.0 && g * g > tol2 * (a * b)) {
+            const double zeta = (b - a) / (2.0 * g);
+            const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+            const double cs = rsqrt(fma(t, t, 1.0));
+            const double sn = cs * t;
+#pragma unroll
+            for (int i = 0; i < NR; ++i) {
+              const int r = gl + kGroup * i;
+              if (r < l) {
+                xp[r] = cs * u[i] - sn * v[i];
+                xq[r] = sn * u[i] + cs * v[i];
+              }
+            }
+            double* jp = J + (int64_t)p * l;
+            double* jq = J + (int64_t)q * l;
+#pragma unroll
+            for (int i = 0; i < NR; ++i) {
+              const int r = gl + kGroup * i;
+              if (r < l) {
+                const double ju = jp[r], jv = jq[r];
+                jp[r] = cs * ju - sn * jv;
+                jq[r] = sn * ju + cs * jv;
+              }
+            }
+            rot = 1;
+          }
+        }
+      }
+      __syncthreads();
     }
-  for (int r = warp; r < l; r += kWarps)
-    for (int i = lane; i < k; i += 32) Wk[(int64_t)r * ldw + i] = gsign[i] * J[(int64_t)gperm[i] * l + r];
+    if (!__syncthreads_or(rot)) break;
+  }
+  if (tid == 0) {
+    status[0] = (sweep >= max_sweeps) ? 1 : 0;
+    status[1] = sweep;  // sweeps run (diagnostics, XB_TRACE)
+  }
+  jacobi_tail_1cta(X, J, l, k, Ub, ldu, s_out, Wk, ldw, gnorm, gperm, gsign);
 }
 
 // Shared tail of the cooperative Jacobi kernels: singular values = column
@@ -806,11 +922,35 @@ void launch_jacobi_svd(const double* R, int64_t ldr, int l, int k, double* Ub, i
     const char* e = getenv("XB_JACOBI");
     return e ? (strcmp(e, "coop") == 0 ? 1
                 : strcmp(e, "single") == 0 ? 2
-                : strcmp(e, "pairs") == 0 ? 3 : 0)
+                : strcmp(e, "pairs") == 0 ? 3
+                : strcmp(e, "rr") == 0 ? 4 : 0)
              : 0;
   }();
   // blocked cooperative kernel from l > 64 (l = 120: 3.3 ms vs 5.4 ms for
   // the single-CTA kernel), single CTA below
+  // register single-CTA kernel while X and J fit in shared memory (l <= 128)
+  if ((mode == 0 || mode == 4) && l <= 128 && 2 * one <= lim) {
+    const int dyn = (int)(2 * one);
+#define XB_JRR(NR)                                                                            \
+  do {                                                                                        \
+    XB_CUDA(cudaFuncSetAttribute(jacobi_rr_kernel<NR>,                                        \
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));          \
+    jacobi_rr_kernel<NR><<<1, kThreads, dyn, st>>>(R, ldr, l, k, Ub, ldu, s, Wk, ldw, work,   \
+                                                   status, tol, kMaxSweeps);                  \
+  } while (0)
+    if (l <= 32) XB_JRR(2);
+    else if (l <= 64) XB_JRR(4);
+    else XB_JRR(8);
+#undef XB_JRR
+    check_launch("jacobi_rr");
+    if (getenv("XB_TRACE")) {
+      int hs[2] = {0, 0};
+      XB_CUDA(cudaMemcpyAsync(hs, status, sizeof(hs), cudaMemcpyDeviceToHost, st));
+      XB_CUDA(cudaStreamSynchronize(st));
+      fprintf(stderr, "[xb] jacobi_rr l=%d: %d sweeps\n", l, hs[1]);
+    }
+    return;
+  }
   const bool coop = mode == 1 || mode == 3 || (mode == 0 && (one > lim || l > 64));
   if (coop) {
     int max_sweeps = kMaxSweeps;
