@@ -89,7 +89,7 @@ struct TCfg {
   static constexpr int STAGE = BLO + B_AL;
   static constexpr int STAGES = (200 * 1024) / STAGE > 4 ? 4 : (200 * 1024) / STAGE;
   static constexpr int BAR_OFF = STAGES * STAGE;
-  static constexpr int SMEM = BAR_OFF + 256 + 1024;    // + barriers, tmem slot, align slack
+  static constexpr int SMEM = BAR_OFF + 256 + 1024;    // + barriers (<= 3 NS + 8 + NS), tmem slot, align slack
   // TMEM columns: two accumulator buffers [0, BN), [BN, 2 BN) (the MMA fills
   // one while the drain warps fold the other), then two A slots of 64
   // columns (A_hi: 32 tf32 columns, A_lo: 32) written by the converters.
@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(kThreadsT, 1)
                  const __grid_constant__ CUtensorMap tmBl, int64_t M, int64_t N, int64_t K,
                  double* __restrict__ C, int64_t ldc, int64_t split_stride, int64_t k_per_split,
                  int accumulate, int drain_tiles, int tiles_n, int tiles_m, int splits,
-                 int group_m) {
+                 int group_m, int cl) {
   using Cfg = TCfg<BN>;
   constexpr int NS = Cfg::STAGES;
   static_assert(Cfg::SEG % 8 == 0, "drain segment must be a multiple of 8 columns");
@@ -142,7 +142,12 @@ __global__ void __launch_bounds__(kThreadsT, 1)
   uint64_t* aempty = empty + NS;         // [2] TMEM A slot free (MMA commit)
   uint64_t* tmem_full = aempty + 2;      // [2]
   uint64_t* tmem_empty = tmem_full + 2;  // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+  uint64_t* cempty = tmem_empty + 2;     // [NS] cluster leader: stage free in all cl CTAs
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cempty + NS);
+  // cluster of cl CTAs = the n-tiles of one (m-tile, split): the leader
+  // (rank 0) multicasts the raw A tile to all of them, so A is read once
+  // per m-tile from L2/HBM instead of once per n-tile
+  const uint32_t crank = cl > 1 ? cluster_ctarank() : 0u;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // Raster (1-D grid): n-tile fastest (the CTAs sharing an A tile run
@@ -180,6 +185,7 @@ __global__ void __launch_bounds__(kThreadsT, 1)
       mbar_init(&tmem_full[b], 1);
       mbar_init(&tmem_empty[b], 4 * kDrainGroups);
     }
+    for (int s = 0; s < NS; ++s) mbar_init(&cempty[s], cl);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 1) {
@@ -189,7 +195,10 @@ __global__ void __launch_bounds__(kThreadsT, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-  __syncthreads();
+  if (cl > 1)
+    cluster_sync_all();  // every CTA's barriers initialised before any multicast
+  else
+    __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
@@ -199,14 +208,20 @@ __global__ void __launch_bounds__(kThreadsT, 1)
       const uint32_t bytes = Cfg::A_BYTES + 2 * Cfg::B_BYTES;
       for (int kt = 0; kt < ktiles; ++kt) {
         const int s = kt % NS;
-        if (kt >= NS) mbar_wait_park(&empty[s], ((kt / NS) & 1) ^ 1);
+        if (kt >= NS) {
+          mbar_wait_park(&empty[s], ((kt / NS) & 1) ^ 1);
+          // the leader may refill the A slot only when every CTA freed it
+          if (cl > 1 && crank == 0) mbar_wait_park(&cempty[s], ((kt / NS) & 1) ^ 1);
+        }
         unsigned char* st = smem + s * Cfg::STAGE;
         const int32_t k0 = (int32_t)(kbeg + (int64_t)kt * TBK);
         mbar_expect_tx(&full[s], bytes);
-        if (TRANS_A)
-          tma_load_2d(st + Cfg::RAW, &tmA, &full[s], (int32_t)m0, k0);  // [BK][BM], M inner
-        else
-          tma_load_2d(st + Cfg::RAW, &tmA, &full[s], k0, (int32_t)m0);  // [BM][BK] swizzled
+        const int32_t ca = TRANS_A ? (int32_t)m0 : k0, cb = TRANS_A ? k0 : (int32_t)m0;
+        // TRANS_A: [BK][BM] M inner; else [BM][BK] swizzled
+        if (cl == 1)
+          tma_load_2d(st + Cfg::RAW, &tmA, &full[s], ca, cb);
+        else if (crank == 0)
+          tma_load_2d_mc(st + Cfg::RAW, &tmA, &full[s], ca, cb, (uint16_t)((1u << cl) - 1));
         // B planes are k-blocked ([K/32][N][32]): one contiguous BN x 128 B tile
         tma_load_3d(st + Cfg::BHI, &tmBh, &full[s], 0, (int32_t)n0, k0 / TBK);
         tma_load_3d(st + Cfg::BLO, &tmBl, &full[s], 0, (int32_t)n0, k0 / TBK);
@@ -216,6 +231,7 @@ __global__ void __launch_bounds__(kThreadsT, 1)
     // ---- MMA issuer: A_hi/A_lo from TMEM, B_hi/B_lo from shared memory;
     // group g of P k-tiles accumulates into buffer g & 1 ----------------------
     const uint32_t idesc = idesc_tf32<BN>();
+    const uint32_t cempty0 = cl > 1 ? mapa_rank(cempty, 0) : 0u;  // leader's cempty[0]
     for (int kt = 0; kt < ktiles; ++kt) {
       const int s = kt % NS, a = kt & 1;
       const int g = kt / P, b = g & 1;
@@ -239,6 +255,7 @@ __global__ void __launch_bounds__(kThreadsT, 1)
           mma_tf32_ta(d, al, bh + off, idesc, 1u);
         }
         mma_commit(&empty[s]);
+        if (cl > 1) mma_commit_cluster(cempty0 + (uint32_t)(s * sizeof(uint64_t)));
         mma_commit(&aempty[a]);
         if (last) mma_commit(&tmem_full[b]);
       }
@@ -336,7 +353,12 @@ __global__ void __launch_bounds__(kThreadsT, 1)
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-  __syncthreads();
+  // no CTA leaves while a cluster peer may still multicast into it or
+  // arrive on its barriers
+  if (cl > 1)
+    cluster_sync_all();
+  else
+    __syncthreads();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
@@ -430,9 +452,33 @@ void launch_t(const CUtensorMap& ta, const CUtensorMap& bh, const CUtensorMap& b
   }();
   const int64_t total = ntiles * mtiles * splits;
   XB_REQUIRE(total < ((int64_t)1 << 31), XB_EUNSUPPORTED, "tgemm: too many tiles for one launch");
-  kern<<<(unsigned)total, kThreadsT, Cfg::SMEM, st>>>(
-      ta, bh, bl, g.M, g.N, g.K, out, ldo, stride, kps, acc_here, drain, (int)ntiles, (int)mtiles,
-      splits, (int)std::min<int64_t>(group, mtiles));
+  // TN: the n-tiles of an (m-tile, split) form one cluster sharing the A
+  // tile by TMA multicast — cfg5's A^T Q launches read 123-136 GB from DRAM
+  // instead of 201-226 GB for a 68.7 GB A, at the same speed. NN keeps
+  // independent CTAs: there the B planes dominate the re-reads and the
+  // lockstep of a cluster measured 5-10 % slower. XB_TG_CLUSTER: 0 = never,
+  // 2 = also NN.
+  static const int cluster_mode = [] {
+    const char* e = getenv("XB_TG_CLUSTER");
+    return e ? atoi(e) : 1;
+  }();
+  const bool want = cluster_mode == 2 || (cluster_mode == 1 && TRANS_A);
+  const int cl = (want && ntiles >= 2 && ntiles <= 4) ? (int)ntiles : 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)total);
+  cfg.blockDim = dim3(kThreadsT);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)cl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  XB_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, bh, bl, g.M, g.N, g.K, out, ldo, stride, kps,
+                             acc_here, drain, (int)ntiles, (int)mtiles, splits,
+                             (int)std::min<int64_t>(group, mtiles), cl));
   check_launch("tgemm");
 }
 
