@@ -62,7 +62,7 @@ struct OCfg {
   static constexpr int STAGE = S * (ATILE + RTILE);
   static constexpr int NS = (200 * 1024) / STAGE;    // ring depth (5 at S = 6)
   static constexpr int BAR_OFF = NS * STAGE;
-  static constexpr int SMEM = BAR_OFF + 256 + 1024;
+  static constexpr int SMEM = BAR_OFF + 512 + 1024;  // barriers (3 NS + 1) + TMEM slot, align slack
   static constexpr int ACC_COLS = S * OBN;           // level accumulators
   static constexpr int ASLOT = S * (OBK / 4);        // TMEM columns per A slot
   static constexpr int USED = ACC_COLS + 2 * ASLOT;
@@ -121,6 +121,28 @@ __device__ __forceinline__ void cp_128x256b(uint32_t taddr, uint64_t sdesc) {
       "l"(sdesc));
 }
 
+// commit arriving on a barrier given by its shared::cluster address
+__device__ __forceinline__ void commit_elect_cluster(uint32_t cbar) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+      "}\n" ::"r"(cbar)
+      : "memory");
+}
+
+// 1-D bulk copy multicast to the CTAs of `mask` (same shared offset, each
+// completing on its own barrier at the same offset)
+__device__ __forceinline__ void bulk_load_mc(void* dst, const void* src, uint32_t bytes,
+                                             uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], "
+      "[%1], %2, [%3], %4;\n" ::"r"(su32(dst)),
+      "l"(src), "r"(bytes), "r"(su32(bar)), "h"(mask)
+      : "memory");
+}
+
 __device__ __forceinline__ void commit_elect(uint64_t* bar) {
   asm volatile(
       "{\n"
@@ -138,7 +160,7 @@ __global__ void __launch_bounds__(OTHREADS, 1)
                   int64_t np, const int32_t* __restrict__ eL, const int32_t* __restrict__ eR,
                   int64_t M, int64_t N, int64_t K, double* __restrict__ C, int64_t ldc,
                   int64_t split_stride,
-                  int64_t k_per_split, int accumulate, int tiles_n, int dbg) {
+                  int64_t k_per_split, int accumulate, int tiles_n, int dbg, int cl) {
   using Cfg = OCfg<S>;
   constexpr int NS = Cfg::NS;
   extern __shared__ unsigned char smem_raw_o[];
@@ -146,7 +168,11 @@ __global__ void __launch_bounds__(OTHREADS, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::BAR_OFF);
   uint64_t* empty = full + NS;
   uint64_t* tmem_full = empty + NS;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* cempty = tmem_full + 1;  // [NS] cluster leader: stage free in all cl CTAs
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cempty + NS);
+  // cluster of cl CTAs = the n-tiles of one (m-tile, split): the leader
+  // multicasts the left slices, which are then read from L2 once per m-tile
+  const uint32_t crank = cl > 1 ? cluster_ctarank() : 0u;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nt = (int)(blockIdx.x % tiles_n);
@@ -163,6 +189,7 @@ __global__ void __launch_bounds__(OTHREADS, 1)
       mbar_init(&empty[s], 1);
     }
     mbar_init(tmem_full, 1);
+    for (int s = 0; s < NS; ++s) mbar_init(&cempty[s], cl);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 1) {
@@ -172,7 +199,10 @@ __global__ void __launch_bounds__(OTHREADS, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-  __syncthreads();
+  if (cl > 1)
+    cluster_sync_all();  // every CTA's barriers initialised before any multicast
+  else
+    __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
@@ -182,10 +212,17 @@ __global__ void __launch_bounds__(OTHREADS, 1)
       const int64_t kb0 = kbeg / OBK, lt = rows_p / OBM, rt = np / OBN;
       for (int kt = 0; kt < ktiles; ++kt) {
         const int s = kt % NS;
-        if (kt >= NS) mbar_wait_park(&empty[s], ((kt / NS) & 1) ^ 1);
+        if (kt >= NS) {
+          mbar_wait_park(&empty[s], ((kt / NS) & 1) ^ 1);
+          if (cl > 1 && crank == 0) mbar_wait_park(&cempty[s], ((kt / NS) & 1) ^ 1);
+        }
         unsigned char* st = smem + s * Cfg::STAGE;
         mbar_expect_tx(&full[s], Cfg::STAGE);
-        bulk_load(st, L + ((kb0 + kt) * lt + mt) * (S * Cfg::ATILE), S * Cfg::ATILE, &full[s]);
+        const int8_t* lsrc = L + ((kb0 + kt) * lt + mt) * (S * Cfg::ATILE);
+        if (cl == 1)
+          bulk_load(st, lsrc, S * Cfg::ATILE, &full[s]);
+        else if (crank == 0)
+          bulk_load_mc(st, lsrc, S * Cfg::ATILE, &full[s], (uint16_t)((1u << cl) - 1));
         bulk_load(st + S * Cfg::ATILE, R + ((kb0 + kt) * rt + nt) * (S * Cfg::RTILE),
                   S * Cfg::RTILE, &full[s]);
       }
@@ -195,6 +232,7 @@ __global__ void __launch_bounds__(OTHREADS, 1)
     // the S(S+1)/2 slice products (cp and mma run in issue order) -------------
     const uint32_t idesc = idesc_i8<S>();
     const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+    const uint32_t cempty0 = cl > 1 ? mapa_rank(cempty, 0) : 0u;  // leader's cempty[0]
     const uint32_t sbase = su32(smem);
     for (int kt = 0; kt < ktiles; ++kt) {
       const int s = kt % NS, a = kt & 1;
@@ -221,6 +259,7 @@ __global__ void __launch_bounds__(OTHREADS, 1)
         }
       }
       commit_elect(&empty[s]);
+      if (cl > 1) commit_elect_cluster(cempty0 + (uint32_t)(s * sizeof(uint64_t)));
       if (kt == ktiles - 1) commit_elect(tmem_full);
       __syncwarp();
     }
@@ -272,7 +311,10 @@ __global__ void __launch_bounds__(OTHREADS, 1)
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-  __syncthreads();
+  if (cl > 1)
+    cluster_sync_all();  // no CTA leaves while a peer may still multicast / arrive
+  else
+    __syncthreads();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
@@ -582,8 +624,27 @@ void launch_oz(const int8_t* L, const int8_t* R, int64_t rows_p, int64_t np, con
     const char* e = getenv("XB_OZ_DBG");
     return e ? atoi(e) : 0;
   }();
-  kern<<<grid, OTHREADS, Cfg::SMEM, st>>>(L, R, rows_p, np, eL, eR, M, N, K, out, ldo, stride,
-                                          kps, acc, (int)tn, dbg);
+  // the n-tiles of an (m-tile, split) share the left slices by multicast
+  // (XB_OZ_CLUSTER=0 disables)
+  static const bool cluster_on = [] {
+    const char* e = getenv("XB_OZ_CLUSTER");
+    return !(e && atoi(e) == 0);
+  }();
+  const int cl = (cluster_on && tn >= 2 && tn <= 4) ? (int)tn : 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(OTHREADS);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)cl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  XB_CUDA(cudaLaunchKernelEx(&cfg, kern, L, R, rows_p, np, eL, eR, M, N, K, out, ldo, stride,
+                             kps, acc, (int)tn, dbg, cl));
   check_launch("ozgemm");
 }
 
