@@ -24,7 +24,9 @@ roofline = the dominant kernel: dense f64 at m*n >= 2^24 -> the int8-slice
          (Ozaki) FP64 GEMM on tcgen05 kind::i8 (achieved = int8 tensor ops
          issued per launch / its event-timed mean duration, peak = 2 x
          MEASURED_PEAKS bf16; the useful FP64-equivalent rate is reported
-         beside it); smaller dense f64 -> the FP64 DMMA tile GEMM (achieved =
+         beside it); dense f32 at m*n >= 2^24 -> the int8-slice GEMM of float32
+         A (ozf_kernel; same int8 accounting, 6 slice products per useful
+         flop); smaller dense f64 -> the FP64 DMMA tile GEMM (achieved =
          2*m*n*l flops per launch / duration, peak = the DMMA pipe rate
          measured in-process: MEASURED_PEAKS.json has no FP64 figure); dense f32 -> the tcgen05 3xTF32 GEMM (same
          achieved, peak = MEASURED_PEAKS bf16 / 2 / 3); sparse -> the CSR SpMM (achieved = algorithmic
@@ -258,6 +260,23 @@ def gemm_roofline(prof, esz, dmma_peak, dfma_peak):
                 "peak_source": ("MEASURED_PEAKS.json bf16_tflops / 2 (tf32 rate) / 3 (three "
                                 "products per useful flop)" if bf16 else
                                 "nominal 2250 bf16 TF/s / 2 / 3 (no MEASURED_PEAKS.json)"),
+                "hbm_gbs_achieved": hbm}
+    if kind == "ozaki_f32_i8":
+        # float32 A on the int8 tensor pipe (ozgemm.cu ozf_kernel): A's tiles
+        # sliced into 3 digits inside the GEMM, 6 exact int8 slice products
+        # per useful multiply-add; int8 dense rate = 2x the bf16 rate.
+        peak = 2 * bf16 if bf16 else 4500.0
+        ops = prof["pipe_ops"] / n / per_s / 1e12
+        tf32_3 = bf16 / 6 if bf16 else 2250.0 / 6
+        return {"bound": "tensor", "achieved": ops, "peak": peak, "unit": "TOP/s (int8)",
+                "frac": ops / peak,
+                "kernel": "ozf_kernel (tcgen05.mma kind::i8; float32 A sliced into 3 digits by "
+                          "converter warps straight into TMEM, 6 slice products, f64 "
+                          "recombination; NN/TN over A) + the per-product slicing of X",
+                "peak_source": ("2 x MEASURED_PEAKS.json bf16_tflops (int8 dense rate = 2x bf16)"
+                                if bf16 else "nominal 4500 int8 TOP/s (no MEASURED_PEAKS.json)"),
+                "fp32_equivalent_tflops": useful,
+                "fp32_equivalent_vs_tf32x3_peak": useful / tf32_3,
                 "hbm_gbs_achieved": hbm}
     if kind == "ozaki_i8":
         # FP64 emulated on the int8 tensor pipe (ozgemm.cu): S(S+1)/2 exact

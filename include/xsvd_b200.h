@@ -86,7 +86,8 @@ int xb_profile_read(xb_ctx* ctx, double* out4);
  * issued (2 x multiply-adds, tile padding included: x3 for the 3xTF32 split,
  * x S(S+1)/2 int8 slice pairs for the Ozaki path; 0 for SpMM) and out[5] =
  * the product kind (0 FP64 DMMA, 1 tcgen05 3xTF32, 2 int8-slice Ozaki FP64,
- * 3 CSR SpMM; the largest seen, -1 if none). Resets the accumulators. */
+ * 3 CSR SpMM, 4 int8-slice GEMM of float32 A with the slices made in the
+ * kernel; the largest seen, -1 if none). Resets the accumulators. */
 int xb_profile_read_ext(xb_ctx* ctx, double* out6);
 /* Saturating FP64 microbenchmarks on the context's device: TFLOP/s of the
  * DMMA (mma.sync f64) and DFMA pipes — the f64 roofline denominator. */
@@ -143,7 +144,10 @@ int xb_rsvd_dense_streamed(xb_ctx* ctx, int dtype, int64_t m, int64_t n, const v
 
 /* Same factorization with A, omega, U, V, s already in device memory
  * (the HBM-resident measurement; deficient/ndeficient/stage_seconds stay
- * host pointers). */
+ * host pointers). Every *_dev entry orders the library's compute stream
+ * after the work already queued on the legacy default stream (where e.g.
+ * torch produces the inputs); producers on other streams must be
+ * synchronised by the caller. */
 int xb_rsvd_dense_dev(xb_ctx* ctx, int dtype, int64_t m, int64_t n, const void* dA, int64_t lda,
                       const void* d_omega, uint64_t seed, int k, int p, int q,
                       void* dU, int64_t ldu, double* d_s, void* dV, int64_t ldv,

@@ -179,7 +179,7 @@ class Context:
     def profile_read(self) -> dict:
         out = np.zeros(6)
         _check(self.lib.xb_profile_read_ext(self.h, _ptr(out)))
-        kinds = {0: "dmma", 1: "tf32x3", 2: "ozaki_i8", 3: "spmm"}
+        kinds = {0: "dmma", 1: "tf32x3", 2: "ozaki_i8", 3: "spmm", 4: "ozaki_f32_i8"}
         return {"seconds": out[0], "launches": int(out[1]), "flops": out[2], "bytes": out[3],
                 "pipe_ops": out[4], "kind": kinds.get(int(out[5]))}
 

@@ -129,6 +129,8 @@ int oz_slices();
 size_t oz_both_exp_scratch_bytes(int64_t rows, int64_t cols);
 void oz_both_exp(const double* X, int64_t rows, int64_t cols, int64_t ldx, int32_t* erow,
                  int32_t* ecol, void* scratch, int* wide, cudaStream_t st);
+void oz_both_exp_f32(const float* X, int64_t rows, int64_t cols, int64_t ldx, int32_t* erow,
+                     int32_t* ecol, void* scratch, int* wide, cudaStream_t st);
 void oz_row_exp(const double* X, int64_t rows, int64_t cols, int64_t ldx, int32_t* e, int* wide,
                 cudaStream_t st);
 void oz_col_exp(const double* X, int64_t rows, int64_t cols, int64_t ldx, int32_t* e,
@@ -145,6 +147,17 @@ void oz_slice_both(const double* X, int64_t m, int64_t n, int64_t ldx, const int
                    const int32_t* ec, int8_t* PR, int64_t mp, int64_t kpn, int8_t* PC, int64_t np,
                    int64_t kpm, int S, cudaStream_t st);
 size_t oz_workspace_doubles(int64_t M, int64_t N, int64_t K);
+// float32 A on the int8 pipe (3 digit slices made inside the GEMM): C = op(A) X
+// with eL the row (NN) / column (TN) exponents of A, R / eR the 3 right
+// slices of X (oz_slice_right_f, np = round_up(N, ozf_tile_n(N))).
+int ozf_tile_n(int64_t N);
+int ozf_plan_splits(int64_t M, int64_t N, int64_t K);
+size_t ozf_workspace_doubles(int64_t M, int64_t N, int64_t K);
+void oz_slice_right_f(const double* X, int64_t K, int64_t N, int64_t ldx, const int32_t* e,
+                      int8_t* P, int64_t np, int64_t kp, cudaStream_t st);
+void ozf_gemm(const float* A, int64_t lda, bool trans_a, const int32_t* eL, const int8_t* R,
+              int64_t np, const int32_t* eR, int64_t M, int64_t N, int64_t K, double* C,
+              int64_t ldc, bool accumulate, int splits, double* work, cudaStream_t st);
 // C (M x N) = L R: L = left slices (rows_p x kp, 128-row interleaved tiles,
 // row exponents eL), R = right slices (np x kp, 64-row tiles, column
 // exponents eR).

@@ -42,6 +42,7 @@ struct xb_ctx {
   cudaStream_t st = nullptr;  // compute
   cudaStream_t cp = nullptr;  // host <-> device copies
   int64_t launches = 0;
+  cudaEvent_t caller_ev = nullptr;  // orders the compute stream after the caller's
   struct Buf {
     void* p;
     size_t bytes;
@@ -62,7 +63,7 @@ struct xb_ctx {
   // per-kernel profiling of the products on A (xb_profile_*)
   bool profiling = false;
   // kind: 0 FP64 DMMA tile GEMM, 1 tcgen05 3xTF32 GEMM, 2 int8-slice
-  // (Ozaki) GEMM, 3 CSR SpMM; pipe_ops = tensor-pipe operations issued
+  // (Ozaki) GEMM, 3 CSR SpMM, 4 int8-slice GEMM of float32 A; pipe_ops = tensor-pipe operations issued
   // (multiply-adds x 2, padding included) for the tensor kinds, else 0
   struct ProfMark {
     cudaEvent_t b, e;
@@ -240,6 +241,16 @@ void d2h_rows(xb_ctx* c, void* dst, size_t ld_dst, const void* src, size_t ld_sr
     }
     slot ^= 1;
   }
+}
+
+// *_dev entry points take the caller's device buffers: their producers may
+// still be running on the caller's legacy default stream (e.g. torch's),
+// while the library computes on its own non-blocking stream. Order the
+// compute stream after everything already queued there.
+void after_caller_stream(xb_ctx* c) {
+  if (!c->caller_ev) XB_CUDA(cudaEventCreateWithFlags(&c->caller_ev, cudaEventDisableTiming));
+  XB_CUDA(cudaEventRecord(c->caller_ev, cudaStreamLegacy));
+  XB_CUDA(cudaStreamWaitEvent(c->st, c->caller_ev, 0));
 }
 
 struct LaunchScope {
@@ -540,6 +551,9 @@ struct OzA {
   int8_t* colsT = nullptr;  // [S][kpm/32][np][32]
   int32_t* ecol = nullptr;  // n
   int64_t kpm = 0, np = 0;
+  // float32 A: digit slices made inside the GEMM (ozf_gemm); only the
+  // row / column exponents are stored
+  bool f32 = false;
 };
 
 struct AOp {
@@ -578,9 +592,48 @@ void spmm_on_a(xb_ctx* c, const Csr& s, const double* X, double* Y, int lp, int 
 
 // Slice A once for the int8 tensor-core products (when the slices fit next
 // to everything else in HBM); otherwise the products stay on DMMA.
+// float32 A on the int8 pipe (ozf_gemm): exponents + range guard only;
+// XB_F32_GEMM=tf32 keeps the 3xTF32 tcgen05 kernel.
+bool ozf_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("XB_F32_GEMM");
+    return !(e && (strcmp(e, "tf32") == 0 || strcmp(e, "dmma") == 0));
+  }();
+  return on;
+}
+
+void ozf_prepare(xb_ctx* c, AOp& op, int64_t m, int64_t n) {
+  const AView& a = op.dense;
+  if ((double)m * (double)n < (double)(1 << 24) || std::min(m, n) < 1024) return;
+  if ((reinterpret_cast<uintptr_t>(a.p) & 15) != 0 || a.ld % 4 != 0) return;
+  static const bool trace = getenv("XB_TRACE") != nullptr;
+  OzA z;
+  z.erow = c->ibuf("oz_erow", m);
+  z.ecol = c->ibuf("oz_ecol", n);
+  int* wide = c->ibuf("oz_wide", 1);
+  void* scr = c->buf("oz_scr", oz_both_exp_scratch_bytes(m, n));
+  XB_CUDA(cudaMemsetAsync(wide, 0, sizeof(int), c->st));
+  oz_both_exp_f32(static_cast<const float*>(a.p), m, n, a.ld, z.erow, z.ecol, scr, wide, c->st);
+  int hwide = 0;
+  XB_CUDA(cudaMemcpyAsync(&hwide, wide, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+  XB_CUDA(cudaStreamSynchronize(c->st));
+  if (hwide) {
+    if (trace) fprintf(stderr, "[xb] ozaki f32 off: dynamic-range guard\n");
+    return;
+  }
+  if (trace) fprintf(stderr, "[xb] ozaki f32 on: 3 digit slices in the GEMM\n");
+  z.S = 3;
+  z.f32 = true;
+  op.oz = z;
+}
+
 void oz_prepare(xb_ctx* c, AOp& op, int64_t m, int64_t n) {
   const AView& a = op.dense;
-  if (op.sparse || a.f32 || !oz_enabled()) return;
+  if (op.sparse || !oz_enabled()) return;
+  if (a.f32) {
+    if (ozf_enabled()) ozf_prepare(c, op, m, n);
+    return;
+  }
   // small matrices stay on DMMA: slicing A costs ~1.5 passes over it and the
   // products are launch-bound (cfg1, 4096 x 2048: 1.2 ms DMMA vs 1.8 ms)
   if ((double)m * (double)n < (double)(1 << 24) || std::min(m, n) < 1024) return;
@@ -626,6 +679,36 @@ void oz_prepare(xb_ctx* c, AOp& op, int64_t m, int64_t n) {
   op.oz = z;
 }
 
+// float32 A: right operand X sliced per column (3 digits), the GEMM slices
+// A's tiles on the fly. tn: Z (n x lp) = A^T X, else Y (m x lp) = A X.
+void ozf_product(xb_ctx* c, const AView& a, const OzA& z, bool tn, int64_t m, int64_t n,
+                 const double* X, double* Y, int lp, int l) {
+  cudaEvent_t b = nullptr, e = nullptr;
+  if (c->profiling) {
+    b = c->prof_event();
+    e = c->prof_event();
+    XB_CUDA(cudaEventRecord(b, c->st));
+  }
+  const int64_t Mo = tn ? n : m, Kk = tn ? m : n;
+  const int64_t np = round_up(lp, ozf_tile_n(lp)), kp = round_up(Kk, 32);
+  int32_t* ex = c->ibuf("ozf_ex", np);
+  auto* scr = static_cast<unsigned long long*>(c->buf("oz_xscr", np * 8));
+  int8_t* xs = static_cast<int8_t*>(c->buf("ozf_xs", (size_t)3 * np * kp));
+  oz_col_exp(X, Kk, lp, lp, ex, scr, nullptr, c->st);
+  oz_slice_right_f(X, Kk, lp, lp, ex, xs, np, kp, c->st);
+  const size_t wd = ozf_workspace_doubles(Mo, lp, Kk);
+  double* work = wd ? c->dbuf("split", wd) : nullptr;
+  ozf_gemm(static_cast<const float*>(a.p), a.ld, tn, tn ? z.ecol : z.erow, xs, np, ex, Mo, lp, Kk,
+           Y, lp, false, ozf_plan_splits(Mo, lp, Kk), work, c->st);
+  if (c->profiling) {
+    XB_CUDA(cudaEventRecord(e, c->st));
+    const double mn = (double)m * (double)n;
+    // 6 int8 slice products over the padded tile grid
+    const double ops = 6.0 * 2.0 * (double)round_up(Mo, 128) * (double)np * (double)kp;
+    c->prof_pending.push_back({b, e, 2.0 * mn * l, mn * 4.0, ops, 4});
+  }
+}
+
 // One product on the int8 slices: right operand X (K x lp, f64) sliced per
 // column, then the Ozaki GEMM. tn: Z (n x lp) = A^T X, else Y (m x lp) = A X.
 void oz_product(xb_ctx* c, const OzA& z, bool tn, int64_t m, int64_t n, const double* X,
@@ -662,6 +745,8 @@ void op_nn(xb_ctx* c, const AOp& op, int64_t m, int64_t n, const double* X, doub
            int l) {
   if (op.sparse)
     spmm_on_a(c, op.csr, X, Y, lp, l);
+  else if (op.oz.f32)
+    ozf_product(c, op.dense, op.oz, false, m, n, X, Y, lp, l);
   else if (op.oz.S)
     oz_product(c, op.oz, false, m, n, X, Y, lp, l);
   else
@@ -675,6 +760,8 @@ void op_tn(xb_ctx* c, const AOp& op, int64_t m, int64_t n, const double* Q, doub
            int l) {
   if (op.sparse)
     spmm_on_a(c, op.csrt, Q, Z, lp, l);
+  else if (op.oz.f32)
+    ozf_product(c, op.dense, op.oz, true, m, n, Q, Z, lp, l);
   else if (op.oz.S)
     oz_product(c, op.oz, true, m, n, Q, Z, lp, l);
   else
@@ -1262,6 +1349,28 @@ void gemm_any(xb_ctx* c, bool f32, bool ta, int64_t m, int64_t n, int64_t kdim, 
   double* B64 = c->dbuf("gB64", (size_t)std::max<int64_t>(1, kdim * np));
   double* C64 = c->dbuf("gC64", (size_t)m * np);
   launch_copy2d_cast<float, double>(static_cast<const float*>(dB), kdim, n, ldb, B64, np, c->st);
+  static const bool ozf_dbg = getenv("XB_GEMM_OZF") != nullptr;
+  if (ozf_dbg && m > 0 && n > 0 && kdim > 0) {
+    // diagnostics (tools/ozf_check.py): float32 A on the int8 pipe
+    const float* A = static_cast<const float*>(dA);
+    const int64_t rows = ta ? kdim : m, cols = ta ? m : kdim;
+    int32_t* er = c->ibuf("dbg_er", rows);
+    int32_t* ec = c->ibuf("dbg_ec", cols);
+    void* scr = c->buf("dbg_rc", oz_both_exp_scratch_bytes(rows, cols));
+    oz_both_exp_f32(A, rows, cols, lda, er, ec, scr, nullptr, c->st);
+    const int64_t kp = round_up(kdim, 32), npf = round_up(n, ozf_tile_n(n));
+    int32_t* eR = c->ibuf("dbg_eR", npf);
+    auto* scr2 = static_cast<unsigned long long*>(c->buf("dbg_scr", (size_t)npf * 8));
+    int8_t* R = static_cast<int8_t*>(c->buf("dbg_Rf", (size_t)3 * npf * kp));
+    const size_t wd = ozf_workspace_doubles(m, n, kdim);
+    double* work = wd ? c->dbuf("split", wd) : nullptr;
+    oz_col_exp(B64, kdim, n, np, eR, scr2, nullptr, c->st);
+    oz_slice_right_f(B64, kdim, n, np, eR, R, npf, kp, c->st);
+    ozf_gemm(A, lda, ta, ta ? ec : er, R, npf, eR, m, n, kdim, C64, np, false,
+             ozf_plan_splits(m, n, kdim), work, c->st);
+    launch_copy2d_cast<double, float>(C64, m, n, np, static_cast<float*>(dC), ldc, c->st);
+    return;
+  }
   DGemmArgs g{ta, m, n, kdim, dA, lda, B64, np, C64, np, true};
   run_gemm(c, g);
   launch_copy2d_cast<double, float>(C64, m, n, np, static_cast<float*>(dC), ldc, c->st);
@@ -1306,6 +1415,7 @@ int xb_destroy(xb_ctx* c) {
       if (e) cudaEventDestroy(e);
     cudaStreamDestroy(c->st);
     cudaStreamDestroy(c->cp);
+    if (c->caller_ev) cudaEventDestroy(c->caller_ev);
     delete c;
   });
 }
@@ -1385,6 +1495,7 @@ int xb_rsvd_dense_dev(xb_ctx* c, int dtype, int64_t m, int64_t n, const void* dA
   return guarded([&] {
     XB_REQUIRE(c, XB_EVALUE, "null context");
     LaunchScope ls(c);
+    after_caller_stream(c);
     const bool f32 = check_dtype(dtype);
     XB_REQUIRE(lda >= n && ldu >= k && ldv >= k, XB_EVALUE, "leading dimension too small");
     AOp a;
@@ -1565,6 +1676,7 @@ int xb_rsvd_dense_sharded_dev(xb_ctx* c, int dtype, int64_t m_global, int64_t n,
     XB_REQUIRE(c, XB_EVALUE, "null context");
     XB_REQUIRE(c->comm, XB_EVALUE, "xb_comm_init has not been called on this context");
     LaunchScope ls(c);
+    after_caller_stream(c);
     const bool f32 = check_dtype(dtype);
     XB_REQUIRE(m_local >= 1 && m_local <= m_global, XB_ESHAPE, "bad local row count");
     XB_REQUIRE(lda >= n && ldu >= k && ldv >= k, XB_EVALUE, "leading dimension too small");
@@ -1594,6 +1706,7 @@ int xb_rsvd_dense_colsharded_dev(xb_ctx* c, int dtype, int64_t m, int64_t n_glob
     XB_REQUIRE(c, XB_EVALUE, "null context");
     XB_REQUIRE(c->comm, XB_EVALUE, "xb_comm_init has not been called on this context");
     LaunchScope ls(c);
+    after_caller_stream(c);
     const bool f32 = check_dtype(dtype);
     XB_REQUIRE(n_local >= 1 && col0 >= 0 && col0 + n_local <= n_global, XB_ESHAPE,
                "bad local column block");
@@ -1625,6 +1738,7 @@ int xb_rsvd_csr_dev(xb_ctx* c, int64_t m, int64_t n, int64_t nnz, const int64_t*
   return guarded([&] {
     XB_REQUIRE(c, XB_EVALUE, "null context");
     LaunchScope ls(c);
+    after_caller_stream(c);
     check_dims(m, n, k, p, q);
     XB_REQUIRE(ldu >= k && ldv >= k, XB_EVALUE, "leading dimension too small");
     AOp op = sparse_op(c, m, n, nnz, d_rowptr, d_col, d_val);
@@ -1732,6 +1846,7 @@ int xb_gemm_dev(xb_ctx* c, int dtype, int trans_a, int64_t m, int64_t n, int64_t
   return guarded([&] {
     XB_REQUIRE(c, XB_EVALUE, "null context");
     LaunchScope ls(c);
+    after_caller_stream(c);
     const bool f32 = check_dtype(dtype);
     XB_REQUIRE(m >= 0 && n >= 0 && kdim >= 0, XB_ESHAPE, "negative dimension");
     XB_REQUIRE(ldc >= n && ldb >= n && lda >= (trans_a ? m : kdim), XB_EVALUE,

@@ -422,8 +422,9 @@ __global__ void col_exp_kernel(const unsigned long long* __restrict__ cmax,
 // (row tile, column) — and two small kernels finish them in a fixed order.
 constexpr int RC_ROWS = 512, RC_COLS = 256;
 
+template <typename T>
 __global__ void __launch_bounds__(256, 4)
-    rc_stats_kernel(const double* __restrict__ X, int64_t rows, int64_t cols, int64_t ldx,
+    rc_stats_kernel(const T* __restrict__ X, int64_t rows, int64_t cols, int64_t ldx,
                     double2* __restrict__ rpart, double2* __restrict__ cpart) {
   __shared__ double sm[8][RC_COLS + 1], sq[8][RC_COLS + 1];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
@@ -438,10 +439,10 @@ __global__ void __launch_bounds__(256, 4)
 #pragma unroll
   for (int j = 0; j < 8; ++j) colok[j] = c0 + tx + 32 * j < cols;
   for (int64_t r = r0 + ty; r < rend; r += 8) {
-    const double* xr = X + r * ldx + c0 + tx;
+    const T* xr = X + r * ldx + c0 + tx;
     double v[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) v[j] = colok[j] ? __ldcs(xr + 32 * j) : 0.0;
+    for (int j = 0; j < 8; ++j) v[j] = colok[j] ? (double)__ldcs(xr + 32 * j) : 0.0;
     double m = 0.0, ss = 0.0;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
@@ -576,7 +577,7 @@ __global__ void __launch_bounds__(256)
 
 // Right operand: X (K x N, ldx) -> column-scaled slices of X^T in the
 // interleaved layout of 64-row tiles (il_off<64>), zero padded to (np, kp).
-template <int S>
+template <int S, int TR>
 __global__ void __launch_bounds__(256)
     slice_right_kernel(const double* __restrict__ X, int64_t K, int64_t N, int64_t ldx,
                        const int32_t* __restrict__ e, int8_t* __restrict__ P, int64_t np,
@@ -605,7 +606,7 @@ __global__ void __launch_bounds__(256)
     }
 #pragma unroll
     for (int q = 0; q < S; ++q)
-      *reinterpret_cast<uint32_t*>(P + il_off<64>(n0 + a, k0 + b4, q, S, np)) = w[q];
+      *reinterpret_cast<uint32_t*>(P + il_off<TR>(n0 + a, k0 + b4, q, S, np)) = w[q];
   }
 }
 
@@ -646,6 +647,324 @@ void launch_oz(const int8_t* L, const int8_t* R, int64_t rows_p, int64_t np, con
   XB_CUDA(cudaLaunchKernelEx(&cfg, kern, L, R, rows_p, np, eL, eR, M, N, K, out, ldo, stride,
                              kps, acc, (int)tn, dbg, cl));
   check_launch("ozgemm");
+}
+
+// ---- float32 A on the int8 pipe: slices made on the fly ---------------------
+//
+// The f32 configs' products (Y = A X, Z = A^T Q with A in float32) with A
+// sliced into FS = 3 int8 digits (22 bits relative to its row / column
+// scale, round to nearest) INSIDE the GEMM: the raw f32 A
+// tile arrives by TMA exactly as in tgemm.cu, converter warps turn each
+// row's 32 values into 3 packed digit planes and store them into a TMEM A
+// slot (tcgen05.st), and the MMA warp issues the 6 pairs (t, u), t + u < 3,
+// of tcgen05.mma.kind::i8 (M=128, N=BN, K=32) against the right slices
+// (the sketch X, sliced per product) into three int32 level accumulators.
+// int32 sums are exact, so no mid-chain draining is needed (K per split
+// <= 32768); the epilogue weights the levels in f64. The products are as
+// accurate as an f32 SGEMM or better, at half the tensor work of 3xTF32
+// (6 int8 products = 1.5 tf32-product equivalents per useful flop) and
+// far less energy per flop.
+constexpr int FS = 3;
+constexpr int FBM = 128, FBK = 32;
+constexpr int FEPI = 4;                      // epilogue warps
+constexpr int FCONV = 8;                     // converter warps (2 per TMEM lane quadrant)
+constexpr int FTHREADS = 64 + 32 * (FCONV + FEPI);  // producer, MMA, converters, epilogue
+
+template <int BN>
+struct FCfg {
+  static constexpr int A_BYTES = FBM * FBK * 4;            // raw f32 A tile (TMA)
+  static constexpr int R_BYTES = FS * BN * FBK;            // FS right slices, BN rows x 32 B
+  static constexpr int STAGE = ((A_BYTES + R_BYTES + 1023) / 1024) * 1024;
+  static constexpr int NS = (200 * 1024) / STAGE > 6 ? 6 : (200 * 1024) / STAGE;
+  static constexpr int BAR_OFF = NS * STAGE;
+  static constexpr int SMEM = BAR_OFF + 512 + 1024;
+  static constexpr int ACC_COLS = FS * BN;
+  static constexpr int ASLOT = FS * (FBK / 4);             // 24 TMEM columns
+  static constexpr int NA = 3;                             // A slots (converters run 3 ahead)
+  static constexpr int USED = ACC_COLS + NA * ASLOT;
+  static_assert(USED <= 512, "TMEM budget");
+};
+
+template <int BN>
+__device__ __forceinline__ uint32_t idesc_i8n() {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+         ((uint32_t)(FBM >> 4) << 24);
+}
+
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+      : "memory");
+}
+
+template <int BN, bool TRANS_A>
+__global__ void __launch_bounds__(FTHREADS, 1)
+    ozf_kernel(const __grid_constant__ CUtensorMap tmA, const int8_t* __restrict__ R, int64_t np,
+               const int32_t* __restrict__ eL, const int32_t* __restrict__ eR, int64_t M,
+               int64_t N, int64_t K, double* __restrict__ C, int64_t ldc, int64_t split_stride,
+               int64_t k_per_split, int accumulate, int tiles_n, int tiles_m, int splits,
+               int group_m, int cl) {
+  using Cfg = FCfg<BN>;
+  constexpr int NS = Cfg::NS;
+  extern __shared__ unsigned char smem_raw_f[];
+  unsigned char* smem = smem_raw_f + ((1024u - (su32(smem_raw_f) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::BAR_OFF);
+  uint64_t* conv = full + NS;
+  uint64_t* empty = conv + NS;
+  uint64_t* aempty = empty + NS;  // [NA]
+  uint64_t* tmem_full = aempty + Cfg::NA;
+  uint64_t* cempty = tmem_full + 1;  // [NS] cluster leader: stage free in all cl CTAs
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cempty + NS);
+  // cluster = the n-tiles of one (m-tile, split); the leader multicasts the
+  // raw A tile (read once per m-tile instead of once per n-tile)
+  const uint32_t crank = cl > 1 ? cluster_ctarank() : 0u;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // raster as tgemm.cu: n fastest, m within groups of group_m, then splits
+  int64_t Lb = blockIdx.x;
+  const int nt = (int)(Lb % tiles_n);
+  Lb /= tiles_n;
+  const int64_t per_group = (int64_t)group_m * splits;
+  const int64_t mg = Lb / per_group;
+  const int64_t w = Lb - mg * per_group;
+  const int gsz = (int)min((int64_t)group_m, (int64_t)tiles_m - mg * group_m);
+  const int split = (int)(w / gsz);
+  const int64_t mt = mg * group_m + (w - (int64_t)split * gsz);
+  const int64_t m0 = mt * FBM, n0 = (int64_t)nt * BN;
+  const int64_t kbeg = (int64_t)split * k_per_split;
+  const int64_t kend = min(K, kbeg + k_per_split);
+  const int ktiles = kend > kbeg ? (int)((kend - kbeg + FBK - 1) / FBK) : 0;
+  C += (int64_t)split * split_stride;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&conv[s], FCONV);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < Cfg::NA; ++a) mbar_init(&aempty[a], 1);
+    mbar_init(tmem_full, 1);
+    for (int s = 0; s < NS; ++s) mbar_init(&cempty[s], cl);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+        su32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  if (cl > 1)
+    cluster_sync_all();
+  else
+    __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---- producer: raw A tile (TMA) + the right slices (one bulk copy) ------
+    if (lane == 0) {
+      const int64_t kb0 = kbeg / FBK, rt = np / BN;
+      for (int kt = 0; kt < ktiles; ++kt) {
+        const int s = kt % NS;
+        if (kt >= NS) {
+          mbar_wait_park(&empty[s], ((kt / NS) & 1) ^ 1);
+          if (cl > 1 && crank == 0) mbar_wait_park(&cempty[s], ((kt / NS) & 1) ^ 1);
+        }
+        unsigned char* st = smem + s * Cfg::STAGE;
+        const int32_t k0 = (int32_t)(kbeg + (int64_t)kt * FBK);
+        mbar_expect_tx(&full[s], Cfg::A_BYTES + Cfg::R_BYTES);
+        // TRANS_A: [BK][BM], M inner; else [BM][BK], 128B swizzle
+        const int32_t ca = TRANS_A ? (int32_t)m0 : k0, cb = TRANS_A ? k0 : (int32_t)m0;
+        if (cl == 1)
+          tma_load_2d(st, &tmA, &full[s], ca, cb);
+        else if (crank == 0)
+          tma_load_2d_mc(st, &tmA, &full[s], ca, cb, (uint16_t)((1u << cl) - 1));
+        bulk_load(st + Cfg::A_BYTES, R + ((kb0 + kt) * rt + nt) * (int64_t)Cfg::R_BYTES,
+                  Cfg::R_BYTES, &full[s]);
+      }
+    }
+  } else if (warp == 1) {
+    // ---- MMA: A digit planes from TMEM, right slices from shared memory ------
+    const uint32_t idesc = idesc_i8n<BN>();
+    const uint32_t cempty0 = cl > 1 ? mapa_rank(cempty, 0) : 0u;
+    for (int kt = 0; kt < ktiles; ++kt) {
+      const int s = kt % NS, a = kt % Cfg::NA;
+      mbar_wait(&conv[s], (kt / NS) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      const uint32_t aslot = tmem + (uint32_t)(Cfg::ACC_COLS + a * Cfg::ASLOT);
+      const uint32_t rbase = su32(smem + s * Cfg::STAGE + Cfg::A_BYTES);
+      const uint32_t first = kt > 0 ? 1u : 0u;
+#pragma unroll
+      for (int t = 0; t < FS; ++t)
+#pragma unroll
+        for (int u = 0; u < FS - t; ++u)
+          mma_i8(tmem + (uint32_t)((t + u) * BN), aslot + (uint32_t)(t * (FBK / 4)),
+                 smem_desc(rbase + u * BN * FBK, 256, 0, 128), idesc, t > 0 ? 1u : first);
+      commit_elect(&empty[s]);
+      if (cl > 1) commit_elect_cluster(cempty0 + (uint32_t)(s * sizeof(uint64_t)));
+      commit_elect(&aempty[a]);
+      if (kt == ktiles - 1) commit_elect(tmem_full);
+      __syncwarp();
+    }
+  } else if (warp < 2 + FCONV) {
+    // ---- converters: row m's 16 f32 values (half h of the k-tile) -> 3 packed
+    // digit planes in TMEM. v = rint(x 2^(22 - e)), |v| < 2^22 (7 + 8 + 7
+    // bits), comes out of ONE fma: x 2^(22-e) + 1.5 2^23 has ulp 1, so its bit
+    // pattern minus the constant's is v, rounded to nearest even (no F2I).
+    // u = v + 0x8080 makes the two lower balanced digits plain bytes with
+    // the top bit flipped (w = u ^ 0x8080 restores them); byte 2 of w is the
+    // top digit. Byte permutes gather 4 elements' digits per TMEM word.
+    const int m = 32 * (warp & 3) + lane;
+    const int h = (warp - 2) >> 2;  // k 16 h .. 16 h + 15
+    const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
+    const int e = (m0 + m < M) ? eL[m0 + m] : 0;
+    const float sc = __int_as_float((127 + min(127, max(-126, 22 - e))) << 23);  // 2^(22-e)
+    constexpr float kMagic = 12582912.0f;                       // 1.5 2^23
+    const int kOff = __float_as_int(kMagic) - 0x8080;
+    for (int kt = 0; kt < ktiles; ++kt) {
+      const int s = kt % NS, a = kt % Cfg::NA;
+      mbar_wait_park(&full[s], (kt / NS) & 1);
+      if (kt >= Cfg::NA) mbar_wait_park(&aempty[a], ((kt / Cfg::NA) - 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      const unsigned char* raw = smem + s * Cfg::STAGE;
+      uint32_t wd[FS][4];
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {  // 16-byte chunk c = k 4c .. 4c+3
+        const int c = 4 * h + cc;
+        float4 v;
+        if constexpr (!TRANS_A) {
+          v = *reinterpret_cast<const float4*>(raw + m * 128 + ((c ^ (m & 7)) << 4));
+        } else {
+          const float* rf = reinterpret_cast<const float*>(raw);
+          v.x = rf[(4 * c + 0) * FBM + m];
+          v.y = rf[(4 * c + 1) * FBM + m];
+          v.z = rf[(4 * c + 2) * FBM + m];
+          v.w = rf[(4 * c + 3) * FBM + m];
+        }
+        const uint32_t w0 = (uint32_t)(__float_as_int(fmaf(v.x, sc, kMagic)) - kOff) ^ 0x8080u;
+        const uint32_t w1 = (uint32_t)(__float_as_int(fmaf(v.y, sc, kMagic)) - kOff) ^ 0x8080u;
+        const uint32_t w2 = (uint32_t)(__float_as_int(fmaf(v.z, sc, kMagic)) - kOff) ^ 0x8080u;
+        const uint32_t w3 = (uint32_t)(__float_as_int(fmaf(v.w, sc, kMagic)) - kOff) ^ 0x8080u;
+        const uint32_t lo = __byte_perm(w0, w1, 0x5140), hi = __byte_perm(w2, w3, 0x5140);
+        wd[2][cc] = __byte_perm(lo, hi, 0x5410);  // byte 0: lowest digit
+        wd[1][cc] = __byte_perm(lo, hi, 0x7632);  // byte 1
+        wd[0][cc] = __byte_perm(__byte_perm(w0, w1, 0x62), __byte_perm(w2, w3, 0x62), 0x5410);
+      }
+      const uint32_t tbase =
+          tmem + lane_base + (uint32_t)(Cfg::ACC_COLS + a * Cfg::ASLOT + 4 * h);
+#pragma unroll
+      for (int t = 0; t < FS; ++t) {
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(
+                         tbase + (uint32_t)(t * (FBK / 4))),
+                     "r"(wd[t][0]), "r"(wd[t][1]), "r"(wd[t][2]), "r"(wd[t][3])
+                     : "memory");
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&conv[s]);
+    }
+  } else {
+    // ---- epilogue: levels -> f64, * 2^-(14+8d), sum, * 2^(e_i + f_j) ---------
+    const int q = warp & 3;
+    const int row = 32 * q + lane;
+    const int64_t grow = m0 + row;
+    const bool rvalid = grow < M;
+    const uint32_t lane_base = (uint32_t)(32 * q) << 16;
+    if (ktiles > 0) {
+      mbar_wait_park(tmem_full, 0);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    }
+    const int er = rvalid ? eL[grow] : 0;
+    double* dst = C + (rvalid ? grow : 0) * ldc;
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 16) {
+      double acc[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) acc[j] = 0.0;
+      if (ktiles > 0) {
+#pragma unroll 1
+        for (int d = 0; d < FS; ++d) {
+          uint32_t v[16];
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+              "%11, %12, %13, %14, %15}, [%16];\n"
+              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+                "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+              : "r"(tmem + lane_base + (uint32_t)(d * BN + c0)));
+          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+          // A digits carry 22 bits (x 2^(e-22)), the right slices 23 (x 2^(f-23)):
+          // level d = t + u weighs 2^(e + f) 2^-(13 + 8 d)
+          const double sc = ldexp(1.0, -13 - 8 * d);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) acc[j] = fma((double)(int)v[j], sc, acc[j]);
+        }
+      }
+      if (rvalid) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int64_t col = n0 + c0 + j;
+          if (col < N) {
+            const double x = scalbn(acc[j], er + eR[col]);
+            dst[col] = accumulate ? dst[col] + x : x;
+          }
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  if (cl > 1)
+    cluster_sync_all();
+  else
+    __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+  }
+}
+
+int pick_fbn(int64_t N) {
+  if (N <= 64) return 64;
+  if (N <= 128) return 128;
+  const int64_t w128 = ceil_div(N, 128) * 128, w144 = ceil_div(N, 144) * 144;
+  return w144 < w128 ? 144 : 128;
+}
+
+template <int BN, bool TRANS_A>
+void launch_ozf(const CUtensorMap& ta, const int8_t* R, int64_t np, const int32_t* eL,
+                const int32_t* eR, int64_t M, int64_t N, int64_t K, double* out, int64_t ldo,
+                int64_t stride, int64_t kps, int splits, int acc, cudaStream_t st) {
+  using Cfg = FCfg<BN>;
+  auto kern = ozf_kernel<BN, TRANS_A>;
+  XB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+  const int64_t tn = ceil_div(N, BN), tm = ceil_div(M, FBM);
+  const int64_t total = tn * tm * splits;
+  XB_REQUIRE(total < ((int64_t)1 << 31), XB_EUNSUPPORTED, "ozf: too many tiles");
+  // XB_OZF_CLUSTER=1: the n-tiles share the A tile by multicast (halves the
+  // L2 traffic but measured 10 % slower: the cluster's lockstep costs more
+  // than the L2 reads, which are not the limit here); off by default
+  static const int cmode = [] {
+    const char* e = getenv("XB_OZF_CLUSTER");
+    return e ? atoi(e) : 0;
+  }();
+  const int cl = (cmode && tn >= 2 && tn <= 4) ? (int)tn : 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)total);
+  cfg.blockDim = dim3(FTHREADS);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)cl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  XB_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, R, np, eL, eR, M, N, K, out, ldo, stride, kps, acc,
+                             (int)tn, (int)tm, splits, (int)std::min<int64_t>(8, tm), cl));
+  check_launch("ozf");
 }
 
 }  // namespace
@@ -691,15 +1010,16 @@ size_t oz_both_exp_scratch_bytes(int64_t rows, int64_t cols) {
   return (size_t)(rows * nct + nrt * cols) * sizeof(double2);
 }
 
-void oz_both_exp(const double* X, int64_t rows, int64_t cols, int64_t ldx, int32_t* erow,
-                 int32_t* ecol, void* scratch, int* wide, cudaStream_t st) {
+template <typename T>
+void oz_both_exp_t(const T* X, int64_t rows, int64_t cols, int64_t ldx, int32_t* erow,
+                   int32_t* ecol, void* scratch, int* wide, cudaStream_t st) {
   if (rows <= 0 || cols <= 0) return;
   const int64_t nct = ceil_div(cols, RC_COLS), nrt = ceil_div(rows, RC_ROWS);
   XB_REQUIRE(nrt < 65536, XB_EUNSUPPORTED, "oz_both_exp: more than 2^25 rows");
   double2* rpart = static_cast<double2*>(scratch);
   double2* cpart = rpart + rows * nct;
-  rc_stats_kernel<<<dim3((unsigned)nct, (unsigned)nrt), 256, 0, st>>>(X, rows, cols, ldx, rpart,
-                                                                       cpart);
+  rc_stats_kernel<T><<<dim3((unsigned)nct, (unsigned)nrt), 256, 0, st>>>(X, rows, cols, ldx,
+                                                                          rpart, cpart);
   check_launch("rc_stats");
   rc_finish_kernel<<<(unsigned)ceil_div(rows, 256), 256, 0, st>>>(rpart, rows, nct, nct, 1, cols,
                                                                   erow, wide);
@@ -707,6 +1027,16 @@ void oz_both_exp(const double* X, int64_t rows, int64_t cols, int64_t ldx, int32
   rc_finish_kernel<<<(unsigned)ceil_div(cols, 256), 256, 0, st>>>(cpart, cols, nrt, 1, cols, rows,
                                                                   ecol, wide);
   check_launch("rc_finish_cols");
+}
+
+void oz_both_exp(const double* X, int64_t rows, int64_t cols, int64_t ldx, int32_t* erow,
+                 int32_t* ecol, void* scratch, int* wide, cudaStream_t st) {
+  oz_both_exp_t<double>(X, rows, cols, ldx, erow, ecol, scratch, wide, st);
+}
+
+void oz_both_exp_f32(const float* X, int64_t rows, int64_t cols, int64_t ldx, int32_t* erow,
+                     int32_t* ecol, void* scratch, int* wide, cudaStream_t st) {
+  oz_both_exp_t<float>(X, rows, cols, ldx, erow, ecol, scratch, wide, st);
 }
 
 #define OZ_DISPATCH(S, CALL) \
@@ -722,7 +1052,7 @@ void oz_slice_right(const double* X, int64_t K, int64_t N, int64_t ldx, const in
   XB_REQUIRE(np % OBN == 0 && kp % OBK == 0 && np / 32 < 65536, XB_EUNSUPPORTED,
              "oz_slice_right: layout");
   dim3 grid((unsigned)(kp / 32), (unsigned)(np / 32));
-#define OZ_SX(SS) slice_right_kernel<SS><<<grid, dim3(32, 8), 0, st>>>(X, K, N, ldx, e, P, np, kp)
+#define OZ_SX(SS) slice_right_kernel<SS, 64><<<grid, dim3(32, 8), 0, st>>>(X, K, N, ldx, e, P, np, kp)
   OZ_DISPATCH(S, OZ_SX)
 #undef OZ_SX
   check_launch("slice_right");
@@ -767,6 +1097,78 @@ void ozgemm(const int8_t* L, int64_t rows_p, int64_t kp, const int32_t* eL, cons
   OZ_DISPATCH(S, OZ_RUN)
 #undef OZ_RUN
   if (splits > 1) launch_split_reduce(work, M, N, ldo, stride, splits, C, ldc, accumulate, st);
+}
+
+int ozf_tile_n(int64_t N) { return pick_fbn(N); }
+
+int ozf_plan_splits(int64_t M, int64_t N, int64_t K) {
+  // exact int32 levels: K per split <= 32768 (3 pairs x 2^14 x K < 2^31)
+  const int bn = pick_fbn(N);
+  const int64_t tiles = ceil_div(M, FBM) * ceil_div(N, bn);
+  const int64_t kt = ceil_div(K, FBK);
+  int s = (int)std::max<int64_t>(1, ceil_div(K, 32768));
+  while (tiles * s < 2 * kNumSMs && kt / (s * 2) >= 8) s *= 2;
+  return std::max(1, std::min<int>(s, (int)kt));
+}
+
+void oz_slice_right_f(const double* X, int64_t K, int64_t N, int64_t ldx, const int32_t* e,
+                      int8_t* P, int64_t np, int64_t kp, cudaStream_t st) {
+  const int bn = pick_fbn(N);
+  XB_REQUIRE(np % bn == 0 && kp % 32 == 0 && np / 32 < 65536, XB_EUNSUPPORTED,
+             "oz_slice_right_f: layout");
+  // np = 144 k is not a multiple of 32: the last block row is partial
+  dim3 grid((unsigned)(kp / 32), (unsigned)ceil_div(np, 32));
+  if (bn == 64)
+    slice_right_kernel<FS, 64><<<grid, dim3(32, 8), 0, st>>>(X, K, N, ldx, e, P, np, kp);
+  else if (bn == 128)
+    slice_right_kernel<FS, 128><<<grid, dim3(32, 8), 0, st>>>(X, K, N, ldx, e, P, np, kp);
+  else
+    slice_right_kernel<FS, 144><<<grid, dim3(32, 8), 0, st>>>(X, K, N, ldx, e, P, np, kp);
+  check_launch("slice_right_f");
+}
+
+void ozf_gemm(const float* A, int64_t lda, bool trans_a, const int32_t* eL, const int8_t* R,
+              int64_t np, const int32_t* eR, int64_t M, int64_t N, int64_t K, double* C,
+              int64_t ldc, bool accumulate, int splits, double* work, cudaStream_t st) {
+  if (M <= 0 || N <= 0) return;
+  const int bn = pick_fbn(N);
+  XB_REQUIRE(np % bn == 0 && np >= N, XB_EUNSUPPORTED, "ozf: right slice layout");
+  XB_REQUIRE((reinterpret_cast<uintptr_t>(A) & 15) == 0 && lda % 4 == 0, XB_EUNSUPPORTED,
+             "ozf: A must be 16-byte aligned with lda % 4 == 0");
+  splits = std::max(1, std::min<int>(splits, (int)ceil_div(K, FBK)));
+  const int64_t kps = round_up(ceil_div(K, splits), FBK);
+  splits = (int)ceil_div(K, kps);
+  double* out = C;
+  int64_t ldo = ldc, stride = 0;
+  if (splits > 1) {
+    XB_REQUIRE(work != nullptr, XB_ECUDA, "ozf: split-K workspace missing");
+    out = work;
+    ldo = round_up(N, 2);
+    stride = M * ldo;
+  }
+  const int acc = (splits == 1 && accumulate) ? 1 : 0;
+  // A: NN [M][K] K-major 128B-swizzled boxes {32, 128}; TN [K][M] boxes {128, 32}
+  const CUtensorMap ta = trans_a ? make_map(A, (uint64_t)M, (uint64_t)K, lda, FBM, FBK, false)
+                                 : make_map(A, (uint64_t)K, (uint64_t)M, lda, FBK, FBM, true);
+#define OZF(BN)                                                                             \
+  if (trans_a)                                                                              \
+    launch_ozf<BN, true>(ta, R, np, eL, eR, M, N, K, out, ldo, stride, kps, splits, acc, st); \
+  else                                                                                      \
+    launch_ozf<BN, false>(ta, R, np, eL, eR, M, N, K, out, ldo, stride, kps, splits, acc, st);
+  if (bn == 64) {
+    OZF(64)
+  } else if (bn == 128) {
+    OZF(128)
+  } else {
+    OZF(144)
+  }
+#undef OZF
+  if (splits > 1) launch_split_reduce(work, M, N, ldo, stride, splits, C, ldc, accumulate, st);
+}
+
+size_t ozf_workspace_doubles(int64_t M, int64_t N, int64_t K) {
+  const int s = ozf_plan_splits(M, N, K);
+  return s > 1 ? (size_t)s * M * round_up(N, 2) : 0;
 }
 
 size_t oz_workspace_doubles(int64_t M, int64_t N, int64_t K) {
