@@ -667,7 +667,8 @@ void launch_oz(const int8_t* L, const int8_t* R, int64_t rows_p, int64_t np, con
 constexpr int FS = 3;
 constexpr int FBM = 128, FBK = 32;
 constexpr int FEPI = 4;                      // epilogue warps
-constexpr int FCONV = 8;                     // converter warps (2 per TMEM lane quadrant)
+constexpr int FCONV = 16;                    // converter warps (4 per TMEM lane quadrant)
+constexpr int FCPW = 8 / (FCONV / 4);        // 16-byte chunks (4 k values) per converter warp
 constexpr int FTHREADS = 64 + 32 * (FCONV + FEPI);  // producer, MMA, converters, epilogue
 
 template <int BN>
@@ -808,7 +809,7 @@ __global__ void __launch_bounds__(FTHREADS, 1)
       __syncwarp();
     }
   } else if (warp < 2 + FCONV) {
-    // ---- converters: row m's 16 f32 values (half h of the k-tile) -> 3 packed
+    // ---- converters: row m's 4 FCPW f32 values (part h of the k-tile) -> 3 packed
     // digit planes in TMEM. v = rint(x 2^(22 - e)), |v| < 2^22 (7 + 8 + 7
     // bits), comes out of ONE fma: x 2^(22-e) + 1.5 2^23 has ulp 1, so its bit
     // pattern minus the constant's is v, rounded to nearest even (no F2I).
@@ -816,7 +817,7 @@ __global__ void __launch_bounds__(FTHREADS, 1)
     // the top bit flipped (w = u ^ 0x8080 restores them); byte 2 of w is the
     // top digit. Byte permutes gather 4 elements' digits per TMEM word.
     const int m = 32 * (warp & 3) + lane;
-    const int h = (warp - 2) >> 2;  // k 16 h .. 16 h + 15
+    const int h = (warp - 2) >> 2;  // k 4 FCPW h .. 4 FCPW (h + 1) - 1
     const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
     const int e = (m0 + m < M) ? eL[m0 + m] : 0;
     const float sc = __int_as_float((127 + min(127, max(-126, 22 - e))) << 23);  // 2^(22-e)
@@ -828,10 +829,10 @@ __global__ void __launch_bounds__(FTHREADS, 1)
       if (kt >= Cfg::NA) mbar_wait_park(&aempty[a], ((kt / Cfg::NA) - 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       const unsigned char* raw = smem + s * Cfg::STAGE;
-      uint32_t wd[FS][4];
+      uint32_t wd[FS][FCPW];
 #pragma unroll
-      for (int cc = 0; cc < 4; ++cc) {  // 16-byte chunk c = k 4c .. 4c+3
-        const int c = 4 * h + cc;
+      for (int cc = 0; cc < FCPW; ++cc) {  // 16-byte chunk c = k 4c .. 4c+3
+        const int c = FCPW * h + cc;
         float4 v;
         if constexpr (!TRANS_A) {
           v = *reinterpret_cast<const float4*>(raw + m * 128 + ((c ^ (m & 7)) << 4));
@@ -852,13 +853,19 @@ __global__ void __launch_bounds__(FTHREADS, 1)
         wd[0][cc] = __byte_perm(__byte_perm(w0, w1, 0x62), __byte_perm(w2, w3, 0x62), 0x5410);
       }
       const uint32_t tbase =
-          tmem + lane_base + (uint32_t)(Cfg::ACC_COLS + a * Cfg::ASLOT + 4 * h);
+          tmem + lane_base + (uint32_t)(Cfg::ACC_COLS + a * Cfg::ASLOT + FCPW * h);
 #pragma unroll
       for (int t = 0; t < FS; ++t) {
-        asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(
-                         tbase + (uint32_t)(t * (FBK / 4))),
-                     "r"(wd[t][0]), "r"(wd[t][1]), "r"(wd[t][2]), "r"(wd[t][3])
-                     : "memory");
+        if constexpr (FCPW == 4)
+          asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(
+                           tbase + (uint32_t)(t * (FBK / 4))),
+                       "r"(wd[t][0]), "r"(wd[t][1]), "r"(wd[t][2]), "r"(wd[t][FCPW - 1])
+                       : "memory");
+        else
+          asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};\n" ::"r"(
+                           tbase + (uint32_t)(t * (FBK / 4))),
+                       "r"(wd[t][0]), "r"(wd[t][FCPW - 1])
+                       : "memory");
       }
       asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
