@@ -422,47 +422,92 @@ __global__ void col_exp_kernel(const unsigned long long* __restrict__ cmax,
 // (row tile, column) — and two small kernels finish them in a fixed order.
 constexpr int RC_ROWS = 512, RC_COLS = 256;
 
+// Row AND column max |x| / sum of squares of A in ONE pass. Block tile =
+// 512 rows x 256 columns: each warp reads 256 columns of a row per step —
+// 8 coalesced 8-byte loads per lane for double; for float 2 16-byte loads
+// per lane and 2 rows in flight — reduces the row partial by shuffle, and
+// keeps 8 column partials per lane that the block combines in shared
+// memory. Partials go to scratch without atomics — per (row, column tile)
+// and per (row tile, column) — and two small kernels finish them in a
+// fixed order.
+template <typename T>
+__device__ __forceinline__ int rc_col(int tx, int j) {
+  // the column (within the tile) of a lane's j-th value
+  if constexpr (sizeof(T) == 4)
+    return 4 * tx + (j & 3) + 128 * (j >> 2);
+  else
+    return tx + 32 * j;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256, 4)
     rc_stats_kernel(const T* __restrict__ X, int64_t rows, int64_t cols, int64_t ldx,
                     double2* __restrict__ rpart, double2* __restrict__ cpart) {
+  constexpr bool F = sizeof(T) == 4;
+  constexpr int U = F ? 2 : 1;  // rows in flight per warp
   __shared__ double sm[8][RC_COLS + 1], sq[8][RC_COLS + 1];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int64_t ct = blockIdx.x, rt = blockIdx.y;
   const int64_t nct = gridDim.x;
   const int64_t c0 = ct * RC_COLS, r0 = rt * RC_ROWS;
   const int64_t rend = min(rows, r0 + RC_ROWS);
+  // float rows are 16-byte loaded when the whole tile row is in range and aligned
+  const bool vec = F && c0 + RC_COLS <= cols && (ldx % 4) == 0 &&
+                   (reinterpret_cast<uintptr_t>(X) % 16) == 0;
   double cm[8], cs[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) cm[j] = cs[j] = 0.0;
   bool colok[8];
 #pragma unroll
-  for (int j = 0; j < 8; ++j) colok[j] = c0 + tx + 32 * j < cols;
-  for (int64_t r = r0 + ty; r < rend; r += 8) {
-    const T* xr = X + r * ldx + c0 + tx;
-    double v[8];
+  for (int j = 0; j < 8; ++j) colok[j] = c0 + rc_col<T>(tx, j) < cols;
+  for (int64_t rb = r0 + ty; rb < rend; rb += 8 * U) {
+    T v[U][8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) v[j] = colok[j] ? (double)__ldcs(xr + 32 * j) : 0.0;
-    double m = 0.0, ss = 0.0;
+    for (int u = 0; u < U; ++u) {
+      const int64_t r = rb + 8 * u;
+      const T* xr = X + r * ldx + c0;
+      if constexpr (F) {
+        if (vec) {
+          float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+          if (r < rend) {
+            a = __ldcs(reinterpret_cast<const float4*>(xr) + tx);
+            b = __ldcs(reinterpret_cast<const float4*>(xr + 128) + tx);
+          }
+          v[u][0] = a.x; v[u][1] = a.y; v[u][2] = a.z; v[u][3] = a.w;
+          v[u][4] = b.x; v[u][5] = b.y; v[u][6] = b.z; v[u][7] = b.w;
+          continue;
+        }
+      }
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const double a = fabs(v[j]);
-      m = fmax(m, a);
-      ss = fma(v[j], v[j], ss);
-      cm[j] = fmax(cm[j], a);
-      cs[j] = fma(v[j], v[j], cs[j]);
+      for (int j = 0; j < 8; ++j) {
+        const int cc = rc_col<T>(tx, j);
+        v[u][j] = (r < rend && colok[j]) ? __ldcs(xr + cc) : T(0);
+      }
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-      ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    for (int u = 0; u < U; ++u) {
+      double m = 0.0, ss = 0.0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const double x = (double)v[u][j], a = fabs(x);
+        m = fmax(m, a);
+        ss = fma(x, x, ss);
+        cm[j] = fmax(cm[j], a);
+        cs[j] = fma(x, x, cs[j]);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+        ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      }
+      const int64_t r = rb + 8 * u;
+      if (tx == 0 && r < rend) rpart[r * nct + ct] = make_double2(m, ss);
     }
-    if (tx == 0) rpart[r * nct + ct] = make_double2(m, ss);
   }
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    sm[ty][tx + 32 * j] = cm[j];
-    sq[ty][tx + 32 * j] = cs[j];
+    sm[ty][rc_col<T>(tx, j)] = cm[j];
+    sq[ty][rc_col<T>(tx, j)] = cs[j];
   }
   __syncthreads();
   const int64_t c = c0 + threadIdx.x;
