@@ -994,14 +994,19 @@ void launch_ozf(const CUtensorMap& ta, const int8_t* R, int64_t np, const int32_
   const int64_t tn = ceil_div(N, BN), tm = ceil_div(M, FBM);
   const int64_t total = tn * tm * splits;
   XB_REQUIRE(total < ((int64_t)1 << 31), XB_EUNSUPPORTED, "ozf: too many tiles");
-  // XB_OZF_CLUSTER=1: the n-tiles share the A tile by multicast (halves the
-  // L2 traffic but measured 10 % slower: the cluster's lockstep costs more
-  // than the L2 reads, which are not the limit here); off by default
-  static const int cmode = [] {
+  // NN: the n-tiles of an (m-tile, split) form a cluster and the leader
+  // multicasts the A tile. At cfg5 (16384 x 1M, power-capped) the NN launch
+  // reads 116 instead of 235 GB from DRAM and runs 53 instead of 64 ms (the
+  // saved DRAM energy buys clock); for TN (A read ~once anyway) the
+  // lockstep costs ~3 %, so TN stays unclustered. XB_OZF_CLUSTER: 0 never,
+  // 1 NN (default), 2 cluster launch without multicast, 3 NN and TN.
+  static const int cenv = [] {
     const char* e = getenv("XB_OZF_CLUSTER");
-    return e ? atoi(e) : 0;
+    return e ? atoi(e) : 1;
   }();
-  const int cl = (cmode && tn >= 2 && tn <= 4) ? (int)tn : 1;
+  const int cmode = (cenv == 3 || (cenv != 0 && !TRANS_A)) ? (cenv == 2 ? 2 : 1) : 0;
+  const int cdim = (cmode && tn >= 2 && tn <= 4) ? (int)tn : 1;
+  const int cl = cmode == 2 ? 1 : cdim;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)total);
   cfg.blockDim = dim3(FTHREADS);
@@ -1009,7 +1014,7 @@ void launch_ozf(const CUtensorMap& ta, const int8_t* R, int64_t np, const int32_
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = (unsigned)cl;
+  attr[0].val.clusterDim.x = (unsigned)cdim;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
