@@ -340,6 +340,45 @@ void gemm(xb_ctx* c, bool ta, int64_t M, int64_t N, int64_t K, const double* A, 
   dgemm(g, splits, work, c->st);
 }
 
+// C = op(A) B for f64 device operands on the int8 tensor pipe (Ozaki
+// slices of both operands, ozgemm.cu): exponents, slicing and the GEMM.
+// Used for the n-side orthonormalisation products of float32 configs (the
+// 1e-4 / 1e-3 targets leave a large margin over the ~1e-14 product error)
+// and by the XB_GEMM_OZ diagnostics.
+void oz_gemm64(xb_ctx* c, bool ta, int64_t m, int64_t n, int64_t kdim, const double* A,
+               int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc) {
+  const int S = oz_slices();
+  const int64_t kp = round_up(kdim, 32), np = round_up(n, 64), mp = round_up(m, 128);
+  int8_t* L = static_cast<int8_t*>(c->buf("ozg_L", (size_t)S * mp * kp));
+  int8_t* R = static_cast<int8_t*>(c->buf("ozg_R", (size_t)S * np * kp));
+  int32_t* eL = c->ibuf("ozg_eL", m);
+  int32_t* eR = c->ibuf("ozg_eR", np);
+  auto* scr = static_cast<unsigned long long*>(c->buf("ozg_scr", (size_t)std::max(m, np) * 8));
+  if (ta) {  // op(A) = A^T, A stored kdim x m: column slices of the stored A
+    oz_col_exp(A, kdim, m, lda, eL, scr, nullptr, c->st);
+    oz_slice_both(A, kdim, m, lda, nullptr, eL, nullptr, round_up(kdim, 128), round_up(m, 32), L,
+                  mp, kp, S, c->st);
+  } else {
+    oz_row_exp(A, m, kdim, lda, eL, nullptr, c->st);
+    oz_slice_both(A, m, kdim, lda, eL, nullptr, L, mp, kp, nullptr, round_up(kdim, 128),
+                  round_up(m, 32), S, c->st);
+  }
+  oz_col_exp(B, kdim, n, ldb, eR, scr, nullptr, c->st);
+  oz_slice_right(B, kdim, n, ldb, eR, R, np, kp, S, c->st);
+  const size_t wd = oz_workspace_doubles(m, n, kdim);
+  double* work = wd ? c->dbuf("split", wd) : nullptr;
+  ozgemm(L, mp, kp, eL, R, np, eR, m, n, kdim, C, ldc, false, S, work, c->st);
+}
+
+// gemm() or, when `oz` and the big operand has >= 2^24 elements, oz_gemm64
+void gemm_big(xb_ctx* c, bool oz, bool ta, int64_t M, int64_t N, int64_t K, const double* A,
+              int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc, int tri = 0) {
+  if (oz && oz_enabled() && (double)M * (double)K >= (double)(1 << 24) && M >= 64 && K >= 64)
+    oz_gemm64(c, ta, M, N, K, A, lda, B, ldb, C, ldc);
+  else
+    gemm(c, ta, M, N, K, A, lda, B, ldb, C, ldc, tri);
+}
+
 // The caller's A in device memory: f64, or f32 (Precision.SINGLE storage).
 struct AView {
   const void* p;
@@ -401,6 +440,9 @@ struct Small {
   // to a sharded sketch)
   void* comm = nullptr;
   int* shard_err = nullptr;
+  // float32 configs: the big Gram / X R^-1 products of the single-pass QRs
+  // on the int8 pipe (gemm_big)
+  bool oz = false;
 };
 
 Small small_bufs(xb_ctx* c, int l) {
@@ -426,9 +468,10 @@ Small small_bufs(xb_ctx* c, int l) {
 // Q (rows x lp) = CholQR2(X), zero padding columns l..lp-1 preserved.
 // If Rout != null it receives R = R2 R1 (lp x lp, zero padded).
 // G = X^T X over this rank's rows, summed over ranks when X is row-sharded.
-void gram(xb_ctx* c, const Small& s, const double* X, int64_t rows, bool sharded) {
+void gram(xb_ctx* c, const Small& s, const double* X, int64_t rows, bool sharded,
+          bool oz = false) {
   // upper-triangle tiles only: the Cholesky kernels read G's upper triangle
-  gemm(c, true, s.lp, s.lp, rows, X, s.lp, X, s.lp, s.G, s.lp, /*tri=*/1);
+  gemm_big(c, oz, true, s.lp, s.lp, rows, X, s.lp, X, s.lp, s.G, s.lp, /*tri=*/1);
   if (sharded) nccl_allreduce_sum(s.comm, s.G, (size_t)s.lp * s.lp, c->st);
 }
 
@@ -466,9 +509,9 @@ void cholqr1(xb_ctx* c, const Small& s, const double* X, int64_t rows, double* Q
   cudaStream_t st = c->st;
   int* flag = sharded ? s.shard_err : s.flag;
   if (!sharded) XB_CUDA(cudaMemsetAsync(s.flag, 0, sizeof(int), st));
-  gram(c, s, X, rows, sharded);                                // G = X^T X
+  gram(c, s, X, rows, sharded, s.oz);                          // G = X^T X
   launch_chol_inv(s.G, lp, l, 1e-8, s.R1, s.R1i, lp, flag, s.cw, st);
-  gemm(c, false, rows, lp, lp, X, lp, s.R1i, lp, Q, lp, 2);    // Q = X R^-1
+  gemm_big(c, s.oz, false, rows, lp, lp, X, lp, s.R1i, lp, Q, lp, 2);  // Q = X R^-1
   if (Rout)
     XB_CUDA(cudaMemcpyAsync(Rout, s.R1, (size_t)lp * lp * sizeof(double),
                             cudaMemcpyDeviceToDevice, st));
@@ -827,6 +870,13 @@ void rsvd_impl(xb_ctx* c, const AOp& op_in, int64_t m, int64_t n, const void* d_
     c->dbuf("hh_work", (size_t)2 * std::max(m, n) * l);
   }
   Small s = small_bufs(c, l);
+  {
+    static const bool qr_oz = [] {
+      const char* e = getenv("XB_QR_OZ");
+      return !(e && atoi(e) == 0);
+    }();
+    s.oz = qr_oz && a.f32 && !op.sparse;
+  }
   if (op.comm) {
     s.comm = op.comm;
     s.shard_err = c->ibuf("shard_err", 4);
@@ -999,7 +1049,7 @@ void rsvd_impl(xb_ctx* c, const AOp& op_in, int64_t m, int64_t n, const void* d_
   double* lift = nullptr;
   if (fused_lift) {
     XB_CUDA(cudaMemsetAsync(s.flag, 0, sizeof(int), st));
-    gram(c, s, Zn, n, csharded);
+    gram(c, s, Zn, n, csharded, s.oz);
     launch_chol_inv(s.G, lp, l, 1e-8, Rf, s.R1i, lp, csharded ? s.shard_err : s.flag, s.cw, st);
     if (!csharded) {
       // Cholesky breakdown: Householder Q replaces B^T in place, R^-1 := I
@@ -1019,7 +1069,7 @@ void rsvd_impl(xb_ctx* c, const AOp& op_in, int64_t m, int64_t n, const void* d_
   if (fused_lift) {
     lift = c->dbuf("lift", (size_t)lp * kp);
     gemm(c, false, lp, kp, lp, s.R1i, lp, Wk, kp, lift, kp);   // R_B^-1 W_k
-    gemm(c, false, n, k, lp, Zn, lp, lift, kp, out.V, out.ldv);  // V = B^T R_B^-1 W_k
+    gemm_big(c, s.oz, false, n, k, lp, Zn, lp, lift, kp, out.V, out.ldv);  // V = B^T R_B^-1 W_k
   } else {
     gemm(c, false, n, k, lp, Qn, lp, Wk, kp, out.V, out.ldv);  // V = Q_B W_k
   }
@@ -1315,30 +1365,8 @@ void gemm_any(xb_ctx* c, bool f32, bool ta, int64_t m, int64_t n, int64_t kdim, 
     static const bool oz_dbg = getenv("XB_GEMM_OZ") != nullptr;
     if (oz_dbg && m > 0 && n > 0 && kdim > 0) {
       // diagnostics (tools/oz_check.py): the same product on the int8 slices
-      const int S = oz_slices();
-      const double* A = static_cast<const double*>(dA);
-      const double* B = static_cast<const double*>(dB);
-      const int64_t kp = round_up(kdim, 32), np = round_up(n, 64), mp = round_up(m, 128);
-      int8_t* L = static_cast<int8_t*>(c->buf("dbg_L", (size_t)S * mp * kp));
-      int8_t* R = static_cast<int8_t*>(c->buf("dbg_R", (size_t)S * np * kp));
-      int32_t* eL = c->ibuf("dbg_eL", m);
-      int32_t* eR = c->ibuf("dbg_eR", np);
-      auto* scr = static_cast<unsigned long long*>(c->buf("dbg_scr", (size_t)std::max(m, np) * 8));
-      if (ta) {  // op(A) = A^T, A stored kdim x m: column slices of the stored A
-        oz_col_exp(A, kdim, m, lda, eL, scr, nullptr, c->st);
-        oz_slice_both(A, kdim, m, lda, nullptr, eL, nullptr, round_up(kdim, 128), round_up(m, 32),
-                      L, mp, kp, S, c->st);
-      } else {
-        oz_row_exp(A, m, kdim, lda, eL, nullptr, c->st);
-        oz_slice_both(A, m, kdim, lda, eL, nullptr, L, mp, kp, nullptr, round_up(kdim, 128),
-                      round_up(m, 32), S, c->st);
-      }
-      oz_col_exp(B, kdim, n, ldb, eR, scr, nullptr, c->st);
-      oz_slice_right(B, kdim, n, ldb, eR, R, np, kp, S, c->st);
-      const size_t wd = oz_workspace_doubles(m, n, kdim);
-      double* work = wd ? c->dbuf("split", wd) : nullptr;
-      ozgemm(L, mp, kp, eL, R, np, eR, m, n, kdim, static_cast<double*>(dC), ldc, false, S, work,
-             c->st);
+      oz_gemm64(c, ta, m, n, kdim, static_cast<const double*>(dA), lda,
+                static_cast<const double*>(dB), ldb, static_cast<double*>(dC), ldc);
       return;
     }
     gemm(c, ta, m, n, kdim, static_cast<const double*>(dA), lda, static_cast<const double*>(dB),
