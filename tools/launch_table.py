@@ -15,10 +15,11 @@ def main():
     hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
     h = rows[hi]
     ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    mi = h.index("Metric Name") if "Metric Name" in h else None
     tot, cnt = collections.defaultdict(float), collections.Counter()
     scale = {"ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0}
     for r in rows[hi + 1:]:
-        if len(r) <= vi:
+        if len(r) <= vi or (mi is not None and r[mi] != "gpu__time_duration.sum"):
             continue
         v = float(r[vi].replace(",", "")) * scale.get(r[ui], 1e-6)
         name = r[ki].split("(")[0][:70]
@@ -32,4 +33,7 @@ def main():
 
 
 if __name__ == "__main__":
+    import signal
+
+    signal.signal(signal.SIGPIPE, signal.SIG_DFL)  # quiet under | head
     main()
