@@ -101,6 +101,8 @@ class ClockSampler:
         self.lines = []
 
     def __enter__(self):
+        if os.environ.get("XB_BENCH_NO_CLOCKS"):  # diagnostics: timing without the sampler
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
