@@ -446,7 +446,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int64_t ll = (int64_t)l * l;
   double* X = sm;
   double* J = sm + ll;
-  double* nrm = sm + 2 * ll;  // l squared column norms
   double* gnorm = work + ll;
   int* gperm = reinterpret_cast<int*>(gnorm + l);
   int* gsign = gperm + l;
@@ -465,17 +464,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   int sweep = 0;
   for (; sweep < max_sweeps; ++sweep) {
     int rot = 0;
-    // squared column norms, recomputed exactly at every sweep start and
-    // carried through the sweep by the rotation identity
-    // ||x_p'||^2 = ||x_p||^2 - t g, ||x_q'||^2 = ||x_q||^2 + t g
-    // (LAPACK dgesvj's device), so a pair forms ONE dot product per round
-    for (int c = warp; c < l; c += kWarps) {
-      double a = 0.0;
-      for (int r = lane; r < l; r += 32) a = fma(X[(int64_t)c * l + r], X[(int64_t)c * l + r], a);
-      a = warp_sum32(a);
-      if (lane == 0) nrm[c] = a;
-    }
-    __syncthreads();
     for (int round = 0; round < L2 - 1; ++round) {
       if (grp < npairs) {
         const int pa = grp, pb = L2 - 1 - grp;  // circle method: position 0 fixed
@@ -490,22 +478,35 @@ __global__ void __launch_bounds__(kThreads, 1)
           double* xp = X + (int64_t)p * l;
           double* xq = X + (int64_t)q * l;
           double u[NR], v[NR];
-          double g = 0.0;
+          double a = 0.0, b = 0.0, g = 0.0;
 #pragma unroll
           for (int i = 0; i < NR; ++i) {
             const int r = gl + kGroup * i;
             u[i] = r < l ? xp[r] : 0.0;
             v[i] = r < l ? xq[r] : 0.0;
+            a = fma(u[i], u[i], a);
+            b = fma(v[i], v[i], b);
             g = fma(u[i], v[i], g);
           }
 #pragma unroll
-          for (int o = kGroup / 2; o > 0; o >>= 1) g += __shfl_xor_sync(hmask, g, o);
-          const double a = nrm[p], b = nrm[q];
+          for (int o = kGroup / 2; o > 0; o >>= 1) {
+            a += __shfl_xor_sync(hmask, a, o);
+            b += __shfl_xor_sync(hmask, b, o);
+            g += __shfl_xor_sync(hmask, g, o);
+          }
           if (g != 0.0 && g * g > tol2 * (a * b)) {
             const double zeta = (b - a) / (2.0 * g);
             const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
             const double cs = rsqrt(fma(t, t, 1.0));
             const double sn = cs * t;
+#pragma unroll
+            for (int i = 0; i < NR; ++i) {
+              const int r = gl + kGroup * i;
+              if (r < l) {
+                xp[r] = cs * u[i] - sn * v[i];
+                xq[r] = sn * u[i] + cs * v[i];
+              }
+            }
             double* jp = J + (int64_t)p * l;
             double* jq = J + (int64_t)q * l;
 #pragma unroll
@@ -513,15 +514,9 @@ __global__ void __launch_bounds__(kThreads, 1)
               const int r = gl + kGroup * i;
               if (r < l) {
                 const double ju = jp[r], jv = jq[r];
-                xp[r] = cs * u[i] - sn * v[i];
-                xq[r] = sn * u[i] + cs * v[i];
                 jp[r] = cs * ju - sn * jv;
                 jq[r] = sn * ju + cs * jv;
               }
-            }
-            if (gl == 0) {
-              nrm[p] = fma(-t, g, a);
-              nrm[q] = fma(t, g, b);
             }
             rot = 1;
           }
@@ -933,10 +928,9 @@ void launch_jacobi_svd(const double* R, int64_t ldr, int l, int k, double* Ub, i
   }();
   // blocked cooperative kernel from l > 64 (l = 120: 3.3 ms vs 5.4 ms for
   // the single-CTA kernel), single CTA below
-  // register single-CTA kernel while X, J and the norms fit in shared memory
-  // (l <= 120)
-  if ((mode == 0 || mode == 4) && l <= 128 && 2 * one + (size_t)l * 8 <= lim) {
-    const int dyn = (int)(2 * one + (size_t)l * 8);
+  // register single-CTA kernel while X and J fit in shared memory (l <= 128)
+  if ((mode == 0 || mode == 4) && l <= 128 && 2 * one <= lim) {
+    const int dyn = (int)(2 * one);
 #define XB_JRR(NR)                                                                            \
   do {                                                                                        \
     XB_CUDA(cudaFuncSetAttribute(jacobi_rr_kernel<NR>,                                        \
