@@ -231,6 +231,12 @@ __global__ void __launch_bounds__(OTHREADS, 1)
     // ---- MMA warp: tcgen05.cp of the left slices into a TMEM A slot, then
     // the S(S+1)/2 slice products (cp and mma run in issue order) -------------
     const uint32_t idesc = idesc_i8<S>();
+    // instruction descriptors for N = 64, 128, 192, 256 (1-4 right slices)
+    uint32_t idesc_n[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      idesc_n[i] = (idesc & ~(0x3Fu << 17)) | ((uint32_t)(((i + 1) * OBN) >> 3) << 17);
+    const bool grouped = !(dbg & 4);
     const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
     const uint32_t cempty0 = cl > 1 ? mapa_rank(cempty, 0) : 0u;  // leader's cempty[0]
     const uint32_t sbase = su32(smem);
@@ -248,14 +254,29 @@ __global__ void __launch_bounds__(OTHREADS, 1)
                       smem_desc(abase + t * Cfg::ATILE, 256, 0, 128));
       }
       const uint32_t first = kt > 0 ? 1u : 0u;
+      // Grouped: the right slices u0..u0+3 sit back to back in shared memory
+      // (one 256-row K-major operand) and the level accumulators back to
+      // back in TMEM, so ONE N=256 MMA of A slice t writes the pairs
+      // (t, u0..u0+3) into levels t+u0..t+u0+3 — 8 MMAs per k-tile instead
+      // of S(S+1)/2 = 21 for S = 6 (XB_OZ_GROUPED=0: one MMA per pair).
 #pragma unroll
       for (int t = 0; t < S; ++t) {
         if (dbg & 2) break;
+        if (grouped) {
 #pragma unroll
-        for (int u = 0; u < S - t; ++u) {
-          const int d = t + u;  // level (t + 1) + (u + 1) - 2
-          mma_i8(tm + (uint32_t)(d * OBN), aslot + (uint32_t)(t * (OBK / 4)),
-                 smem_desc(rbase + u * Cfg::RTILE, 256, 0, 128), idesc, t > 0 ? 1u : first);
+          for (int u0 = 0; u0 < S - t; u0 += 4) {
+            const int nsl = (S - t - u0) < 4 ? (S - t - u0) : 4;
+            mma_i8(tm + (uint32_t)((t + u0) * OBN), aslot + (uint32_t)(t * (OBK / 4)),
+                   smem_desc(rbase + u0 * Cfg::RTILE, 256, 0, 128), idesc_n[nsl - 1],
+                   t > 0 ? 1u : first);
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < S - t; ++u) {
+            const int d = t + u;  // level (t + 1) + (u + 1) - 2
+            mma_i8(tm + (uint32_t)(d * OBN), aslot + (uint32_t)(t * (OBK / 4)),
+                   smem_desc(rbase + u * Cfg::RTILE, 256, 0, 128), idesc, t > 0 ? 1u : first);
+          }
         }
       }
       commit_elect(&empty[s]);
@@ -668,7 +689,8 @@ void launch_oz(const int8_t* L, const int8_t* R, int64_t rows_p, int64_t np, con
   dim3 grid((unsigned)(tn * tm), (unsigned)splits);
   static const int dbg = [] {
     const char* e = getenv("XB_OZ_DBG");
-    return e ? atoi(e) : 0;
+    const char* g = getenv("XB_OZ_GROUPED");
+    return (e ? atoi(e) : 0) | ((g && atoi(g) == 0) ? 4 : 0);
   }();
   // the n-tiles of an (m-tile, split) share the left slices by multicast
   // (XB_OZ_CLUSTER=0 disables)
