@@ -863,12 +863,18 @@ __global__ void __launch_bounds__(FTHREADS, 1)
       const uint32_t aslot = tmem + (uint32_t)(Cfg::ACC_COLS + a * Cfg::ASLOT);
       const uint32_t rbase = su32(smem + s * Cfg::STAGE + Cfg::A_BYTES);
       const uint32_t first = kt > 0 ? 1u : 0u;
+      // grouped as in ozgemm_kernel: G = 256 / BN consecutive right slices per
+      // MMA land in consecutive level accumulators
+      constexpr int G = 256 / BN;
 #pragma unroll
       for (int t = 0; t < FS; ++t)
 #pragma unroll
-        for (int u = 0; u < FS - t; ++u)
-          mma_i8(tmem + (uint32_t)((t + u) * BN), aslot + (uint32_t)(t * (FBK / 4)),
-                 smem_desc(rbase + u * BN * FBK, 256, 0, 128), idesc, t > 0 ? 1u : first);
+        for (int u0 = 0; u0 < FS - t; u0 += G) {
+          const int nsl = (FS - t - u0) < G ? (FS - t - u0) : G;
+          const uint32_t id = (idesc & ~(0x3Fu << 17)) | ((uint32_t)((nsl * BN) >> 3) << 17);
+          mma_i8(tmem + (uint32_t)((t + u0) * BN), aslot + (uint32_t)(t * (FBK / 4)),
+                 smem_desc(rbase + u0 * BN * FBK, 256, 0, 128), id, t > 0 ? 1u : first);
+        }
       commit_elect(&empty[s]);
       if (cl > 1) commit_elect_cluster(cempty0 + (uint32_t)(s * sizeof(uint64_t)));
       commit_elect(&aempty[a]);
@@ -1002,6 +1008,8 @@ __global__ void __launch_bounds__(FTHREADS, 1)
 int pick_fbn(int64_t N) {
   if (N <= 64) return 64;
   if (N <= 128) return 128;
+  // (measured: forcing 128-column tiles with 2-slice grouped MMAs is slower
+  // at cfg5, 77 vs 52 ms NN, so 144 wins whenever it pads less)
   const int64_t w128 = ceil_div(N, 128) * 128, w144 = ceil_div(N, 144) * 144;
   return w144 < w128 ? 144 : 128;
 }
