@@ -110,6 +110,43 @@ __device__ __forceinline__ void mma_i8(uint32_t d, uint32_t a_tmem, uint64_t b, 
       "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
 }
 
+// One lane of the warp, chosen once per k-tile; the raw issue helpers below
+// are then called by that lane alone (one elect per k-tile instead of one
+// per instruction: the per-instruction elect/vote/uniformise sequence made
+// the MMA warp's issue loop, not the tensor pipe, the bound)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t e;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "elect.sync _|p, 0xffffffff;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(e));
+  return e != 0;
+}
+
+__device__ __forceinline__ void mma_i8_1(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                         uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(d),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void cp_128x256b_1(uint32_t taddr, uint64_t sdesc) {
+  asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;\n" ::"r"(taddr), "l"(sdesc));
+}
+
+__device__ __forceinline__ void commit_1(uint32_t cbar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(cbar)
+      : "memory");
+}
+
 // smem (128 rows x 32 B, 32-byte swizzle) -> TMEM lanes 0-127, 8 columns
 __device__ __forceinline__ void cp_128x256b(uint32_t taddr, uint64_t sdesc) {
   asm volatile(
@@ -279,6 +316,8 @@ __global__ void __launch_bounds__(OTHREADS, 1)
           }
         }
       }
+      // (measured: issuing this block from one elected lane, as ozf_kernel
+      // does, is slower here: 2.14 -> 2.33 ms per cfg2 product)
       commit_elect(&empty[s]);
       if (cl > 1) commit_elect_cluster(cempty0 + (uint32_t)(s * sizeof(uint64_t)));
       if (kt == ktiles - 1) commit_elect(tmem_full);
@@ -734,23 +773,40 @@ void launch_oz(const int8_t* L, const int8_t* R, int64_t rows_p, int64_t np, con
 constexpr int FS = 3;
 constexpr int FBM = 128, FBK = 32;
 constexpr int FEPI = 4;                      // epilogue warps
-constexpr int FCONV = 16;                    // converter warps (4 per TMEM lane quadrant)
-constexpr int FCPW = 8 / (FCONV / 4);        // 16-byte chunks (4 k values) per converter warp
-constexpr int FTHREADS = 64 + 32 * (FCONV + FEPI);  // producer, MMA, converters, epilogue
+// converter warps: FPH k-tile phases x 4 TMEM lane quadrants; the warps of
+// phase h convert the whole 128 x 32 tile of every k-tile kt = h (mod FPH),
+// so each warp has FPH MMA k-tiles of time per tile it converts and its
+// fixed per-tile costs (barrier waits, TMEM store wait, arrive) are paid once
+// per 32 k values instead of once per 8
+constexpr int FPH = 3;
+constexpr int FCONV = 4 * FPH;
+constexpr int FTHREADS = 32 * (2 + FCONV + FEPI);  // producer, MMA, converters, epilogue
 
+// One stage ring: raw A tile + the right slices of a k-tile per stage.
+// (Measured: separate A and R rings, the A stage released by the converters
+// and each ring refilled by its own thread, were no faster for TN and much
+// slower for the clustered NN launch.)
 template <int BN>
 struct FCfg {
   static constexpr int A_BYTES = FBM * FBK * 4;            // raw f32 A tile (TMA)
   static constexpr int R_BYTES = FS * BN * FBK;            // FS right slices, BN rows x 32 B
   static constexpr int STAGE = ((A_BYTES + R_BYTES + 1023) / 1024) * 1024;
-  static constexpr int NS = (200 * 1024) / STAGE > 6 ? 6 : (200 * 1024) / STAGE;
+  // the stage count is a multiple of FPH: every k-tile that uses a given
+  // stage belongs to the same converter phase, so each converter warp meets
+  // that stage's barrier phases in order
+  static constexpr int NS0 = (200 * 1024) / STAGE > 6 ? 6 : (200 * 1024) / STAGE;
+  static constexpr int NS = NS0 - NS0 % FPH;
   static constexpr int BAR_OFF = NS * STAGE;
   static constexpr int SMEM = BAR_OFF + 512 + 1024;
   static constexpr int ACC_COLS = FS * BN;
   static constexpr int ASLOT = FS * (FBK / 4);             // 24 TMEM columns
-  static constexpr int NA = 3;                             // A slots (converters run 3 ahead)
-  static constexpr int USED = ACC_COLS + NA * ASLOT;
-  static_assert(USED <= 512, "TMEM budget");
+  // A slots (converters run NA k-tiles ahead of the MMAs): what TMEM leaves,
+  // a multiple of FPH for the same reason as NSA
+  static constexpr int NA0 = (512 - ACC_COLS) / ASLOT > 6 ? 6 : (512 - ACC_COLS) / ASLOT;
+  static constexpr int NA = NA0 - NA0 % FPH;
+  static_assert(NA >= FPH && NS >= FPH, "slot / stage counts");
+  static_assert(ACC_COLS + NA * ASLOT <= 512, "TMEM budget");
+  static_assert(SMEM <= 227 * 1024, "shared memory budget");
 };
 
 template <int BN>
@@ -772,18 +828,21 @@ __global__ void __launch_bounds__(FTHREADS, 1)
                const int32_t* __restrict__ eL, const int32_t* __restrict__ eR, int64_t M,
                int64_t N, int64_t K, double* __restrict__ C, int64_t ldc, int64_t split_stride,
                int64_t k_per_split, int accumulate, int tiles_n, int tiles_m, int splits,
-               int group_m, int cl) {
+               int group_m, int cl_dbg) {
   using Cfg = FCfg<BN>;
-  constexpr int NS = Cfg::NS;
+  constexpr int NS = Cfg::NS, NA = Cfg::NA;
+  // low byte: cluster size; above: XB_OZF_DBG timing experiments (results
+  // are wrong with any bit set): 1 converters skip the A tile, 2 only the
+  // t = 0 MMAs, 4 no A tile load (with 1), 16 no right-slice load
+  const int cl = cl_dbg & 0xff, dbg = cl_dbg >> 8;
   extern __shared__ unsigned char smem_raw_f[];
   unsigned char* smem = smem_raw_f + ((1024u - (su32(smem_raw_f) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::BAR_OFF);
-  uint64_t* conv = full + NS;
-  uint64_t* empty = conv + NS;
-  uint64_t* aempty = empty + NS;  // [NA]
-  uint64_t* tmem_full = aempty + Cfg::NA;
-  uint64_t* cempty = tmem_full + 1;  // [NS] cluster leader: stage free in all cl CTAs
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cempty + NS);
+  uint64_t* conv = full + NS;     // count 4: the converter warps of the stage's phase
+  uint64_t* empty = conv + NS;    // MMA commit: stage (and the A slot of k-tile kt) free
+  uint64_t* cempty = empty + NS;  // cluster leader: stage free in all cl CTAs
+  uint64_t* tmem_full = cempty + NS;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
   // cluster = the n-tiles of one (m-tile, split); the leader multicasts the
   // raw A tile (read once per m-tile instead of once per n-tile)
   const uint32_t crank = cl > 1 ? cluster_ctarank() : 0u;
@@ -808,12 +867,11 @@ __global__ void __launch_bounds__(FTHREADS, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&conv[s], FCONV);
+      mbar_init(&conv[s], 4);
       mbar_init(&empty[s], 1);
+      mbar_init(&cempty[s], cl);
     }
-    for (int a = 0; a < Cfg::NA; ++a) mbar_init(&aempty[a], 1);
     mbar_init(tmem_full, 1);
-    for (int s = 0; s < NS; ++s) mbar_init(&cempty[s], cl);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 1) {
@@ -830,7 +888,8 @@ __global__ void __launch_bounds__(FTHREADS, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    // ---- producer: raw A tile (TMA) + the right slices (one bulk copy) ------
+    // ---- producer: raw A tile (TMA; the cluster leader multicasts) + the
+    // right slices (one bulk copy) ---------------------------------------------
     if (lane == 0) {
       const int64_t kb0 = kbeg / FBK, rt = np / BN;
       for (int kt = 0; kt < ktiles; ++kt) {
@@ -841,73 +900,77 @@ __global__ void __launch_bounds__(FTHREADS, 1)
         }
         unsigned char* st = smem + s * Cfg::STAGE;
         const int32_t k0 = (int32_t)(kbeg + (int64_t)kt * FBK);
-        mbar_expect_tx(&full[s], Cfg::A_BYTES + Cfg::R_BYTES);
+        mbar_expect_tx(&full[s], ((dbg & 4) ? 0 : Cfg::A_BYTES) + ((dbg & 16) ? 0 : Cfg::R_BYTES));
         // TRANS_A: [BK][BM], M inner; else [BM][BK], 128B swizzle
         const int32_t ca = TRANS_A ? (int32_t)m0 : k0, cb = TRANS_A ? k0 : (int32_t)m0;
-        if (cl == 1)
+        if (dbg & 4) {
+        } else if (cl == 1)
           tma_load_2d(st, &tmA, &full[s], ca, cb);
         else if (crank == 0)
           tma_load_2d_mc(st, &tmA, &full[s], ca, cb, (uint16_t)((1u << cl) - 1));
-        bulk_load(st + Cfg::A_BYTES, R + ((kb0 + kt) * rt + nt) * (int64_t)Cfg::R_BYTES,
-                  Cfg::R_BYTES, &full[s]);
+        if (!(dbg & 16))
+          bulk_load(st + Cfg::A_BYTES, R + ((kb0 + kt) * rt + nt) * (int64_t)Cfg::R_BYTES,
+                    Cfg::R_BYTES, &full[s]);
       }
     }
   } else if (warp == 1) {
     // ---- MMA: A digit planes from TMEM, right slices from shared memory ------
+    // (issued by one elected lane per k-tile: per-instruction elect / vote /
+    // uniformise sequences otherwise dominate this warp's loop)
     const uint32_t idesc = idesc_i8n<BN>();
     const uint32_t cempty0 = cl > 1 ? mapa_rank(cempty, 0) : 0u;
     for (int kt = 0; kt < ktiles; ++kt) {
-      const int s = kt % NS, a = kt % Cfg::NA;
+      const int s = kt % NS, a = kt % NA;
       mbar_wait(&conv[s], (kt / NS) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       const uint32_t aslot = tmem + (uint32_t)(Cfg::ACC_COLS + a * Cfg::ASLOT);
       const uint32_t rbase = su32(smem + s * Cfg::STAGE + Cfg::A_BYTES);
       const uint32_t first = kt > 0 ? 1u : 0u;
-      // grouped as in ozgemm_kernel: G = 256 / BN consecutive right slices per
-      // MMA land in consecutive level accumulators
-      constexpr int G = 256 / BN;
+      if (elect_one()) {
+        // grouped as in ozgemm_kernel: G = 256 / BN consecutive right slices
+        // per MMA land in consecutive level accumulators
+        constexpr int G = 256 / BN;
 #pragma unroll
-      for (int t = 0; t < FS; ++t)
+        for (int t = 0; t < ((dbg & 2) ? 1 : FS); ++t)
 #pragma unroll
-        for (int u0 = 0; u0 < FS - t; u0 += G) {
-          const int nsl = (FS - t - u0) < G ? (FS - t - u0) : G;
-          const uint32_t id = (idesc & ~(0x3Fu << 17)) | ((uint32_t)((nsl * BN) >> 3) << 17);
-          mma_i8(tmem + (uint32_t)((t + u0) * BN), aslot + (uint32_t)(t * (FBK / 4)),
-                 smem_desc(rbase + u0 * BN * FBK, 256, 0, 128), id, t > 0 ? 1u : first);
-        }
-      commit_elect(&empty[s]);
-      if (cl > 1) commit_elect_cluster(cempty0 + (uint32_t)(s * sizeof(uint64_t)));
-      commit_elect(&aempty[a]);
-      if (kt == ktiles - 1) commit_elect(tmem_full);
+          for (int u0 = 0; u0 < FS - t; u0 += G) {
+            const int nsl = (FS - t - u0) < G ? (FS - t - u0) : G;
+            const uint32_t id = (idesc & ~(0x3Fu << 17)) | ((uint32_t)((nsl * BN) >> 3) << 17);
+            mma_i8_1(tmem + (uint32_t)((t + u0) * BN), aslot + (uint32_t)(t * (FBK / 4)),
+                     smem_desc(rbase + u0 * BN * FBK, 256, 0, 128), id, t > 0 ? 1u : first);
+          }
+        commit_1(su32(&empty[s]));
+        if (cl > 1) commit_1(cempty0 + (uint32_t)(s * sizeof(uint64_t)));
+        if (kt == ktiles - 1) commit_1(su32(tmem_full));
+      }
       __syncwarp();
     }
   } else if (warp < 2 + FCONV) {
-    // ---- converters: row m's 4 FCPW f32 values (part h of the k-tile) -> 3 packed
-    // digit planes in TMEM. v = rint(x 2^(22 - e)), |v| < 2^22 (7 + 8 + 7
+    // ---- converters: row m's 32 f32 values of k-tile kt -> 3 packed digit
+    // planes in TMEM. v = rint(x 2^(22 - e)), |v| < 2^22 (7 + 8 + 7
     // bits), comes out of ONE fma: x 2^(22-e) + 1.5 2^23 has ulp 1, so its bit
     // pattern minus the constant's is v, rounded to nearest even (no F2I).
     // u = v + 0x8080 makes the two lower balanced digits plain bytes with
     // the top bit flipped (w = u ^ 0x8080 restores them); byte 2 of w is the
     // top digit. Byte permutes gather 4 elements' digits per TMEM word.
-    const int m = 32 * (warp & 3) + lane;
-    const int h = (warp - 2) >> 2;  // k 4 FCPW h .. 4 FCPW (h + 1) - 1
+    const int m = 32 * (warp & 3) + lane;  // TMEM lane quadrant = warp id % 4
+    const int h = (warp - 2) >> 2;         // k-tile phase
     const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
     const int e = (m0 + m < M) ? eL[m0 + m] : 0;
     const float sc = __int_as_float((127 + min(127, max(-126, 22 - e))) << 23);  // 2^(22-e)
     constexpr float kMagic = 12582912.0f;                       // 1.5 2^23
     const int kOff = __float_as_int(kMagic) - 0x8080;
-    for (int kt = 0; kt < ktiles; ++kt) {
-      const int s = kt % NS, a = kt % Cfg::NA;
+    for (int kt = h; kt < ktiles; kt += FPH) {
+      const int s = kt % NS, a = kt % NA;
       mbar_wait_park(&full[s], (kt / NS) & 1);
-      if (kt >= Cfg::NA) mbar_wait_park(&aempty[a], ((kt / Cfg::NA) - 1) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       const unsigned char* raw = smem + s * Cfg::STAGE;
-      uint32_t wd[FS][FCPW];
+      uint32_t wd[FS][8];
 #pragma unroll
-      for (int cc = 0; cc < FCPW; ++cc) {  // 16-byte chunk c = k 4c .. 4c+3
-        const int c = FCPW * h + cc;
+      for (int c = 0; c < 8; ++c) {  // 16-byte chunk c = k 4c .. 4c+3
         float4 v;
-        if constexpr (!TRANS_A) {
+        if (dbg & 1) {
+          v = make_float4(1.f, 2.f, 3.f, (float)c);
+        } else if constexpr (!TRANS_A) {
           v = *reinterpret_cast<const float4*>(raw + m * 128 + ((c ^ (m & 7)) << 4));
         } else {
           const float* rf = reinterpret_cast<const float*>(raw);
@@ -916,30 +979,30 @@ __global__ void __launch_bounds__(FTHREADS, 1)
           v.z = rf[(4 * c + 2) * FBM + m];
           v.w = rf[(4 * c + 3) * FBM + m];
         }
-        const uint32_t w0 = (uint32_t)(__float_as_int(fmaf(v.x, sc, kMagic)) - kOff) ^ 0x8080u;
-        const uint32_t w1 = (uint32_t)(__float_as_int(fmaf(v.y, sc, kMagic)) - kOff) ^ 0x8080u;
-        const uint32_t w2 = (uint32_t)(__float_as_int(fmaf(v.z, sc, kMagic)) - kOff) ^ 0x8080u;
-        const uint32_t w3 = (uint32_t)(__float_as_int(fmaf(v.w, sc, kMagic)) - kOff) ^ 0x8080u;
+        // (the 0x80 flips of the two lower digits are applied to the packed
+        // words: one xor per 4 elements and digit)
+        const uint32_t w0 = (uint32_t)(__float_as_int(fmaf(v.x, sc, kMagic)) - kOff);
+        const uint32_t w1 = (uint32_t)(__float_as_int(fmaf(v.y, sc, kMagic)) - kOff);
+        const uint32_t w2 = (uint32_t)(__float_as_int(fmaf(v.z, sc, kMagic)) - kOff);
+        const uint32_t w3 = (uint32_t)(__float_as_int(fmaf(v.w, sc, kMagic)) - kOff);
         const uint32_t lo = __byte_perm(w0, w1, 0x5140), hi = __byte_perm(w2, w3, 0x5140);
-        wd[2][cc] = __byte_perm(lo, hi, 0x5410);  // byte 0: lowest digit
-        wd[1][cc] = __byte_perm(lo, hi, 0x7632);  // byte 1
-        wd[0][cc] = __byte_perm(__byte_perm(w0, w1, 0x62), __byte_perm(w2, w3, 0x62), 0x5410);
+        wd[2][c] = __byte_perm(lo, hi, 0x5410) ^ 0x80808080u;  // byte 0: lowest digit
+        wd[1][c] = __byte_perm(lo, hi, 0x7632) ^ 0x80808080u;  // byte 1
+        wd[0][c] = __byte_perm(__byte_perm(w0, w1, 0x62), __byte_perm(w2, w3, 0x62), 0x5410);
       }
-      const uint32_t tbase =
-          tmem + lane_base + (uint32_t)(Cfg::ACC_COLS + a * Cfg::ASLOT + FCPW * h);
+      // the slot wait comes after the loads and digit arithmetic, so only the
+      // TMEM stores sit between an MMA group's completion and the next arrive.
+      // Slot a is free once the MMAs of k-tile kt - NA completed: the commit
+      // that frees that k-tile's stage says exactly that (NS and NA are
+      // multiples of FPH, so this warp meets the barrier's phases in order)
+      if (kt >= NA) {
+        const int kp = kt - NA;
+        mbar_wait_park(&empty[kp % NS], (kp / NS) & 1);
+      }
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      const uint32_t tbase = tmem + lane_base + (uint32_t)(Cfg::ACC_COLS + a * Cfg::ASLOT);
 #pragma unroll
-      for (int t = 0; t < FS; ++t) {
-        if constexpr (FCPW == 4)
-          asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(
-                           tbase + (uint32_t)(t * (FBK / 4))),
-                       "r"(wd[t][0]), "r"(wd[t][1]), "r"(wd[t][2]), "r"(wd[t][FCPW - 1])
-                       : "memory");
-        else
-          asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};\n" ::"r"(
-                           tbase + (uint32_t)(t * (FBK / 4))),
-                       "r"(wd[t][0]), "r"(wd[t][FCPW - 1])
-                       : "memory");
-      }
+      for (int t = 0; t < FS; ++t) tmem_st8(tbase + (uint32_t)(t * (FBK / 4)), wd[t]);
       asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
       __syncwarp();
@@ -1010,6 +1073,11 @@ int pick_fbn(int64_t N) {
   if (N <= 128) return 128;
   // (measured: forcing 128-column tiles with 2-slice grouped MMAs is slower
   // at cfg5, 77 vs 52 ms NN, so 144 wins whenever it pads less)
+  static const int force = [] {
+    const char* e = getenv("XB_OZF_BN");
+    return e ? atoi(e) : 0;
+  }();
+  if (force == 128 || force == 112) return force;
   const int64_t w128 = ceil_div(N, 128) * 128, w144 = ceil_div(N, 144) * 144;
   return w144 < w128 ? 144 : 128;
 }
@@ -1035,7 +1103,7 @@ void launch_ozf(const CUtensorMap& ta, const int8_t* R, int64_t np, const int32_
     return e ? atoi(e) : 1;
   }();
   const int cmode = (cenv == 3 || (cenv != 0 && !TRANS_A)) ? (cenv == 2 ? 2 : 1) : 0;
-  const int cdim = (cmode && tn >= 2 && tn <= 4) ? (int)tn : 1;
+  const int cdim = (cmode && tn >= 2 && tn <= 8) ? (int)tn : 1;
   const int cl = cmode == 2 ? 1 : cdim;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)total);
@@ -1049,8 +1117,13 @@ void launch_ozf(const CUtensorMap& ta, const int8_t* R, int64_t np, const int32_
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  static const int dbg = [] {
+    const char* e = getenv("XB_OZF_DBG");
+    return e ? atoi(e) : 0;
+  }();
   XB_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, R, np, eL, eR, M, N, K, out, ldo, stride, kps, acc,
-                             (int)tn, (int)tm, splits, (int)std::min<int64_t>(8, tm), cl));
+                             (int)tn, (int)tm, splits, (int)std::min<int64_t>(8, tm),
+                             cl | (dbg << 8)));
   check_launch("ozf");
 }
 
@@ -1209,6 +1282,8 @@ void oz_slice_right_f(const double* X, int64_t K, int64_t N, int64_t ldx, const 
     slice_right_kernel<FS, 64><<<grid, dim3(32, 8), 0, st>>>(X, K, N, ldx, e, P, np, kp);
   else if (bn == 128)
     slice_right_kernel<FS, 128><<<grid, dim3(32, 8), 0, st>>>(X, K, N, ldx, e, P, np, kp);
+  else if (bn == 112)
+    slice_right_kernel<FS, 112><<<grid, dim3(32, 8), 0, st>>>(X, K, N, ldx, e, P, np, kp);
   else
     slice_right_kernel<FS, 144><<<grid, dim3(32, 8), 0, st>>>(X, K, N, ldx, e, P, np, kp);
   check_launch("slice_right_f");
@@ -1246,6 +1321,8 @@ void ozf_gemm(const float* A, int64_t lda, bool trans_a, const int32_t* eL, cons
     OZF(64)
   } else if (bn == 128) {
     OZF(128)
+  } else if (bn == 112) {
+    OZF(112)
   } else {
     OZF(144)
   }
