@@ -32,11 +32,12 @@
 // Kernel (one CTA per 128 x 64 output tile, 192 threads, 1 CTA per SM):
 //   warp 0      producer: per k-tile one bulk copy of the S left slices and
 //               one of the S right slices into a ring of NS stages
-//   warp 1      TMEM allocator + MMA issuer: tcgen05.cp moves the left
-//               slices of the stage into a TMEM A slot (two slots, double
-//               buffered), then the S(S+1)/2 pairs (t, u), t + u < S,
-//               accumulate into level d = t + u (S int32 accumulators of 64
-//               columns); tcgen05.commit frees the stage
+//   warp 1      TMEM allocator + MMA issuer: the S(S+1)/2 pairs (t, u),
+//               t + u < S, accumulate into level d = t + u (S int32
+//               accumulators of 64 columns), grouped 4 right slices per MMA,
+//               both operands from shared memory (optionally the left slices
+//               staged in a TMEM A slot by tcgen05.cp, XB_OZ_TC);
+//               tcgen05.commit frees the stage
 //   warps 2-5   epilogue (one TMEM lane quadrant each): per level
 //               tcgen05.ld, int32 -> f64, * 2^-(14+8d), sum, * 2^(e_i + f_j),
 //               store (or += / split-K slice)
@@ -147,6 +148,19 @@ __device__ __forceinline__ void commit_1(uint32_t cbar) {
       : "memory");
 }
 
+// A from shared memory (descriptor) instead of TMEM
+__device__ __forceinline__ void mma_i8_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                          uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
 // smem (128 rows x 32 B, 32-byte swizzle) -> TMEM lanes 0-127, 8 columns
 __device__ __forceinline__ void cp_128x256b(uint32_t taddr, uint64_t sdesc) {
   asm volatile(
@@ -191,7 +205,7 @@ __device__ __forceinline__ void commit_elect(uint64_t* bar) {
 }
 
 
-template <int S>
+template <int S, int TC>
 __global__ void __launch_bounds__(OTHREADS, 1)
     ozgemm_kernel(const int8_t* __restrict__ L, const int8_t* __restrict__ R, int64_t rows_p,
                   int64_t np, const int32_t* __restrict__ eL, const int32_t* __restrict__ eR,
@@ -274,6 +288,9 @@ __global__ void __launch_bounds__(OTHREADS, 1)
     for (int i = 0; i < 4; ++i)
       idesc_n[i] = (idesc & ~(0x3Fu << 17)) | ((uint32_t)(((i + 1) * OBN) >> 3) << 17);
     const bool grouped = !(dbg & 4);
+    // left slices 0 .. TC-1 are staged in TMEM by tcgen05.cp; the rest feed
+    // their MMAs from shared memory
+    constexpr int tc = TC;
     const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
     const uint32_t cempty0 = cl > 1 ? mapa_rank(cempty, 0) : 0u;  // leader's cempty[0]
     const uint32_t sbase = su32(smem);
@@ -287,8 +304,9 @@ __global__ void __launch_bounds__(OTHREADS, 1)
       if (!(dbg & 1)) {
 #pragma unroll
         for (int t = 0; t < S; ++t)
-          cp_128x256b(aslot + (uint32_t)(t * (OBK / 4)),
-                      smem_desc(abase + t * Cfg::ATILE, 256, 0, 128));
+          if (t < tc)
+            cp_128x256b(aslot + (uint32_t)(t * (OBK / 4)),
+                        smem_desc(abase + t * Cfg::ATILE, 256, 0, 128));
       }
       const uint32_t first = kt > 0 ? 1u : 0u;
       // Grouped: the right slices u0..u0+3 sit back to back in shared memory
@@ -303,9 +321,15 @@ __global__ void __launch_bounds__(OTHREADS, 1)
 #pragma unroll
           for (int u0 = 0; u0 < S - t; u0 += 4) {
             const int nsl = (S - t - u0) < 4 ? (S - t - u0) : 4;
-            mma_i8(tm + (uint32_t)((t + u0) * OBN), aslot + (uint32_t)(t * (OBK / 4)),
-                   smem_desc(rbase + u0 * Cfg::RTILE, 256, 0, 128), idesc_n[nsl - 1],
-                   t > 0 ? 1u : first);
+            if (t < tc)
+              mma_i8(tm + (uint32_t)((t + u0) * OBN), aslot + (uint32_t)(t * (OBK / 4)),
+                     smem_desc(rbase + u0 * Cfg::RTILE, 256, 0, 128), idesc_n[nsl - 1],
+                     t > 0 ? 1u : first);
+            else
+              mma_i8_ss(tm + (uint32_t)((t + u0) * OBN),
+                        smem_desc(abase + t * Cfg::ATILE, 256, 0, 128),
+                        smem_desc(rbase + u0 * Cfg::RTILE, 256, 0, 128), idesc_n[nsl - 1],
+                        t > 0 ? 1u : first);
           }
         } else {
 #pragma unroll
@@ -720,7 +744,16 @@ void launch_oz(const int8_t* L, const int8_t* R, int64_t rows_p, int64_t np, con
                const int32_t* eR, int64_t M, int64_t N, int64_t K, double* out, int64_t ldo,
                int64_t stride, int64_t kps, int splits, int acc, cudaStream_t st) {
   using Cfg = OCfg<S>;
-  auto kern = ozgemm_kernel<S>;
+  // Left slices straight from shared memory (TC = 0) by default. Staging
+  // them in TMEM with tcgen05.cp (XB_OZ_TC=S) saves shared-memory reads for
+  // the slices two MMAs use, but the copies execute in order with the MMAs
+  // on the tensor pipe: cfg2 product 2.14 ms at 66 % tensor-active staged
+  // (2 staged: 1.92 ms) vs 1.90 ms at 84 % unstaged.
+  static const bool staged = [] {
+    const char* e = getenv("XB_OZ_TC");
+    return e && atoi(e) == S;
+  }();
+  auto kern = staged ? ozgemm_kernel<S, S> : ozgemm_kernel<S, 0>;
   XB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
   const int64_t tn = ceil_div(N, OBN), tm = ceil_div(M, OBM);
   XB_REQUIRE(tn * tm < ((int64_t)1 << 31) && splits < 65536, XB_EUNSUPPORTED,
