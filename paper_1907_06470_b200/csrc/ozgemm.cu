@@ -42,6 +42,7 @@
 //               tcgen05.ld, int32 -> f64, * 2^-(14+8d), sum, * 2^(e_i + f_j),
 //               store (or += / split-K slice)
 #include <algorithm>
+#include <cfloat>
 
 #include "common.cuh"
 #include "tc_util.cuh"
@@ -606,6 +607,118 @@ __global__ void __launch_bounds__(256, 4)
   }
 }
 
+// float A (the f32 configs' 64 GB pass): the same partials with float
+// arithmetic — the generic kernel's f32 -> f64 conversion and f64 max / fma
+// per element made it issue-bound at ~3 TB/s (ncu: 79 % issue slots busy,
+// DRAM 36 %). max |x| is exact in float; the sums of squares are float per
+// lane and row (256 terms) and per column and tile (512 terms), which is
+// plenty for a range guard, and an overflowing one reads as "wide" (DMMA),
+// never as a false "narrow". Each warp takes 8 rows per step (16 loads of
+// 16 bytes in flight per lane) and reduces the 8 row partials across lanes
+// by halving exchanges (9 shuffles per quantity instead of 40).
+__global__ void __launch_bounds__(256, 2)
+    rc_stats_f32_kernel(const float* __restrict__ X, int64_t rows, int64_t cols, int64_t ldx,
+                        double2* __restrict__ rpart, double2* __restrict__ cpart) {
+  __shared__ float sm[8][RC_COLS + 1], sq[8][RC_COLS + 1];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t ct = blockIdx.x, rt = blockIdx.y;
+  const int64_t nct = gridDim.x;
+  const int64_t c0 = ct * RC_COLS, r0 = rt * RC_ROWS;
+  const int64_t rend = min(rows, r0 + RC_ROWS);
+  const bool full_cols = c0 + RC_COLS <= cols;
+  float cm[8], cs[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) cm[j] = cs[j] = 0.f;
+  for (int64_t rb = r0 + 8 * ty; rb < rend; rb += 64) {
+    float v[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int64_t r = rb + i;
+      const float* xr = X + r * ldx + c0;
+      if (full_cols) {
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+        if (r < rend) {
+          a = __ldcs(reinterpret_cast<const float4*>(xr) + tx);
+          b = __ldcs(reinterpret_cast<const float4*>(xr + 128) + tx);
+        }
+        v[i][0] = a.x; v[i][1] = a.y; v[i][2] = a.z; v[i][3] = a.w;
+        v[i][4] = b.x; v[i][5] = b.y; v[i][6] = b.z; v[i][7] = b.w;
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int cc = rc_col<float>(tx, j);
+          v[i][j] = (r < rend && c0 + cc < cols) ? __ldcs(xr + cc) : 0.f;
+        }
+      }
+    }
+    float rm[8], rs[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      rm[i] = 0.f;
+      rs[i] = 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float x = v[i][j], a = fabsf(x);
+        rm[i] = fmaxf(rm[i], a);
+        rs[i] = fmaf(x, x, rs[i]);
+        cm[j] = fmaxf(cm[j], a);
+        cs[j] = fmaf(x, x, cs[j]);
+      }
+    }
+    // halving exchanges: after xor 16 / 8 / 4 a lane holds 4 / 2 / 1 of the
+    // rows (row index from lane bits 4, 3, 2), then xor 2, 1 finish it
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const bool hi = tx & 16;
+      const float sendm = hi ? rm[k] : rm[k + 4], sends = hi ? rs[k] : rs[k + 4];
+      const float gm = __shfl_xor_sync(0xffffffffu, sendm, 16);
+      const float gs = __shfl_xor_sync(0xffffffffu, sends, 16);
+      rm[k] = fmaxf(hi ? rm[k + 4] : rm[k], gm);
+      rs[k] = (hi ? rs[k + 4] : rs[k]) + gs;
+    }
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const bool hi = tx & 8;
+      const float sendm = hi ? rm[k] : rm[k + 2], sends = hi ? rs[k] : rs[k + 2];
+      const float gm = __shfl_xor_sync(0xffffffffu, sendm, 8);
+      const float gs = __shfl_xor_sync(0xffffffffu, sends, 8);
+      rm[k] = fmaxf(hi ? rm[k + 2] : rm[k], gm);
+      rs[k] = (hi ? rs[k + 2] : rs[k]) + gs;
+    }
+    {
+      const bool hi = tx & 4;
+      const float sendm = hi ? rm[0] : rm[1], sends = hi ? rs[0] : rs[1];
+      const float gm = __shfl_xor_sync(0xffffffffu, sendm, 4);
+      const float gs = __shfl_xor_sync(0xffffffffu, sends, 4);
+      rm[0] = fmaxf(hi ? rm[1] : rm[0], gm);
+      rs[0] = (hi ? rs[1] : rs[0]) + gs;
+    }
+#pragma unroll
+    for (int o = 2; o > 0; o >>= 1) {
+      rm[0] = fmaxf(rm[0], __shfl_xor_sync(0xffffffffu, rm[0], o));
+      rs[0] += __shfl_xor_sync(0xffffffffu, rs[0], o);
+    }
+    const int64_t r = rb + ((tx >> 4) & 1) * 4 + ((tx >> 3) & 1) * 2 + ((tx >> 2) & 1);
+    if ((tx & 3) == 0 && r < rend) rpart[r * nct + ct] = make_double2(rm[0], rs[0]);
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    sm[ty][rc_col<float>(tx, j)] = cm[j];
+    sq[ty][rc_col<float>(tx, j)] = cs[j];
+  }
+  __syncthreads();
+  const int64_t c = c0 + threadIdx.x;
+  if (c < cols) {
+    double m = 0.0, ss = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      m = fmax(m, (double)sm[w][threadIdx.x]);
+      ss += (double)sq[w][threadIdx.x];
+    }
+    cpart[rt * cols + c] = make_double2(m, ss);
+  }
+}
+
 // e[i] from the partials part[i * stride + t * tstep], t < parts; `len` =
 // elements per row/column (the range guard's mean square)
 __global__ void rc_finish_kernel(const double2* __restrict__ part, int64_t count, int64_t parts,
@@ -620,7 +733,10 @@ __global__ void rc_finish_kernel(const double2* __restrict__ part, int64_t count
     ss += p.y;
   }
   e[i] = slice_exp(m);
-  if (wide && m * m > kOzRange * kOzRange * (ss / (double)len)) atomicOr(wide, 1);
+  // (a non-finite sum of squares — float partials that overflowed — counts
+  // as wide)
+  if (wide && (!(ss <= DBL_MAX) || m * m > kOzRange * kOzRange * (ss / (double)len)))
+    atomicOr(wide, 1);
 }
 
 template <int S>
@@ -1211,8 +1327,21 @@ void oz_both_exp_t(const T* X, int64_t rows, int64_t cols, int64_t ldx, int32_t*
   XB_REQUIRE(nrt < 65536, XB_EUNSUPPORTED, "oz_both_exp: more than 2^25 rows");
   double2* rpart = static_cast<double2*>(scratch);
   double2* cpart = rpart + rows * nct;
-  rc_stats_kernel<T><<<dim3((unsigned)nct, (unsigned)nrt), 256, 0, st>>>(X, rows, cols, ldx,
+  if constexpr (sizeof(T) == 4) {
+    static const bool generic = [] {
+      const char* e = getenv("XB_RC_GENERIC");
+      return e && atoi(e) != 0;
+    }();
+    if (!generic && ldx % 4 == 0 && (reinterpret_cast<uintptr_t>(X) % 16) == 0)
+      rc_stats_f32_kernel<<<dim3((unsigned)nct, (unsigned)nrt), 256, 0, st>>>(X, rows, cols, ldx,
+                                                                             rpart, cpart);
+    else
+      rc_stats_kernel<T><<<dim3((unsigned)nct, (unsigned)nrt), 256, 0, st>>>(X, rows, cols, ldx,
+                                                                            rpart, cpart);
+  } else {
+    rc_stats_kernel<T><<<dim3((unsigned)nct, (unsigned)nrt), 256, 0, st>>>(X, rows, cols, ldx,
                                                                           rpart, cpart);
+  }
   check_launch("rc_stats");
   rc_finish_kernel<<<(unsigned)ceil_div(rows, 256), 256, 0, st>>>(rpart, rows, nct, nct, 1, cols,
                                                                   erow, wide);
