@@ -607,7 +607,7 @@ __global__ void __launch_bounds__(256, 4)
   }
 }
 
-// float A (the f32 configs' 64 GB pass): the same partials with float
+// Fast path, float A (the f32 configs' 64 GB pass): the same partials with float
 // arithmetic — the generic kernel's f32 -> f64 conversion and f64 max / fma
 // per element made it issue-bound at ~3 TB/s (ncu: 79 % issue slots busy,
 // DRAM 36 %). max |x| is exact in float; the sums of squares are float per
@@ -615,96 +615,102 @@ __global__ void __launch_bounds__(256, 4)
 // plenty for a range guard, and an overflowing one reads as "wide" (DMMA),
 // never as a false "narrow". Each warp takes 8 rows per step (16 loads of
 // 16 bytes in flight per lane) and reduces the 8 row partials across lanes
-// by halving exchanges (9 shuffles per quantity instead of 40).
+// by halving exchanges (9 shuffles per quantity instead of 40). Double A
+// takes the same kernel with f64 arithmetic and 4 rows per step (32 loads
+// of 8 bytes in flight per lane; the generic kernel kept 8).
+template <typename T>
+__device__ __forceinline__ T rc_absmax(T a, T b) {
+  if constexpr (sizeof(T) == 4)
+    return fmaxf(a, b);
+  else
+    return fmax(a, b);
+}
+
+template <typename T>
 __global__ void __launch_bounds__(256, 2)
-    rc_stats_f32_kernel(const float* __restrict__ X, int64_t rows, int64_t cols, int64_t ldx,
-                        double2* __restrict__ rpart, double2* __restrict__ cpart) {
-  __shared__ float sm[8][RC_COLS + 1], sq[8][RC_COLS + 1];
+    rc_stats_fast_kernel(const T* __restrict__ X, int64_t rows, int64_t cols, int64_t ldx,
+                         double2* __restrict__ rpart, double2* __restrict__ cpart) {
+  constexpr bool F = sizeof(T) == 4;
+  constexpr int RR = F ? 8 : 4;  // rows per warp step
+  __shared__ T sm[8][RC_COLS + 1], sq[8][RC_COLS + 1];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int64_t ct = blockIdx.x, rt = blockIdx.y;
   const int64_t nct = gridDim.x;
   const int64_t c0 = ct * RC_COLS, r0 = rt * RC_ROWS;
   const int64_t rend = min(rows, r0 + RC_ROWS);
   const bool full_cols = c0 + RC_COLS <= cols;
-  float cm[8], cs[8];
+  T cm[8], cs[8];
 #pragma unroll
-  for (int j = 0; j < 8; ++j) cm[j] = cs[j] = 0.f;
-  for (int64_t rb = r0 + 8 * ty; rb < rend; rb += 64) {
-    float v[8][8];
+  for (int j = 0; j < 8; ++j) cm[j] = cs[j] = T(0);
+  for (int64_t rb = r0 + RR * ty; rb < rend; rb += 8 * RR) {
+    T v[RR][8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < RR; ++i) {
       const int64_t r = rb + i;
-      const float* xr = X + r * ldx + c0;
-      if (full_cols) {
-        float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
-        if (r < rend) {
-          a = __ldcs(reinterpret_cast<const float4*>(xr) + tx);
-          b = __ldcs(reinterpret_cast<const float4*>(xr + 128) + tx);
-        }
-        v[i][0] = a.x; v[i][1] = a.y; v[i][2] = a.z; v[i][3] = a.w;
-        v[i][4] = b.x; v[i][5] = b.y; v[i][6] = b.z; v[i][7] = b.w;
-      } else {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int cc = rc_col<float>(tx, j);
-          v[i][j] = (r < rend && c0 + cc < cols) ? __ldcs(xr + cc) : 0.f;
+      const T* xr = X + r * ldx + c0;
+      if constexpr (F) {
+        if (full_cols) {
+          float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+          if (r < rend) {
+            a = __ldcs(reinterpret_cast<const float4*>(xr) + tx);
+            b = __ldcs(reinterpret_cast<const float4*>(xr + 128) + tx);
+          }
+          v[i][0] = a.x; v[i][1] = a.y; v[i][2] = a.z; v[i][3] = a.w;
+          v[i][4] = b.x; v[i][5] = b.y; v[i][6] = b.z; v[i][7] = b.w;
+          continue;
         }
       }
-    }
-    float rm[8], rs[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      rm[i] = 0.f;
-      rs[i] = 0.f;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const float x = v[i][j], a = fabsf(x);
-        rm[i] = fmaxf(rm[i], a);
-        rs[i] = fmaf(x, x, rs[i]);
-        cm[j] = fmaxf(cm[j], a);
-        cs[j] = fmaf(x, x, cs[j]);
+        const int cc = rc_col<T>(tx, j);
+        v[i][j] = (r < rend && (full_cols || c0 + cc < cols)) ? __ldcs(xr + cc) : T(0);
       }
     }
-    // halving exchanges: after xor 16 / 8 / 4 a lane holds 4 / 2 / 1 of the
-    // rows (row index from lane bits 4, 3, 2), then xor 2, 1 finish it
+    T rm[RR], rs[RR];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const bool hi = tx & 16;
-      const float sendm = hi ? rm[k] : rm[k + 4], sends = hi ? rs[k] : rs[k + 4];
-      const float gm = __shfl_xor_sync(0xffffffffu, sendm, 16);
-      const float gs = __shfl_xor_sync(0xffffffffu, sends, 16);
-      rm[k] = fmaxf(hi ? rm[k + 4] : rm[k], gm);
-      rs[k] = (hi ? rs[k + 4] : rs[k]) + gs;
-    }
+    for (int i = 0; i < RR; ++i) {
+      rm[i] = T(0);
+      rs[i] = T(0);
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const bool hi = tx & 8;
-      const float sendm = hi ? rm[k] : rm[k + 2], sends = hi ? rs[k] : rs[k + 2];
-      const float gm = __shfl_xor_sync(0xffffffffu, sendm, 8);
-      const float gs = __shfl_xor_sync(0xffffffffu, sends, 8);
-      rm[k] = fmaxf(hi ? rm[k + 2] : rm[k], gm);
-      rs[k] = (hi ? rs[k + 2] : rs[k]) + gs;
+      for (int j = 0; j < 8; ++j) {
+        const T x = v[i][j], a = x < T(0) ? -x : x;
+        rm[i] = rc_absmax(rm[i], a);
+        rs[i] = fma(x, x, rs[i]);
+        cm[j] = rc_absmax(cm[j], a);
+        cs[j] = fma(x, x, cs[j]);
+      }
     }
-    {
-      const bool hi = tx & 4;
-      const float sendm = hi ? rm[0] : rm[1], sends = hi ? rs[0] : rs[1];
-      const float gm = __shfl_xor_sync(0xffffffffu, sendm, 4);
-      const float gs = __shfl_xor_sync(0xffffffffu, sends, 4);
-      rm[0] = fmaxf(hi ? rm[1] : rm[0], gm);
-      rs[0] = (hi ? rs[1] : rs[0]) + gs;
-    }
+    // halving exchanges: at offset o a lane keeps the upper or lower half of
+    // its remaining rows (by lane bit o) and takes the partner's partials of
+    // that half; once one row is left the remaining offsets reduce it fully
+    int ri = 0;
 #pragma unroll
-    for (int o = 2; o > 0; o >>= 1) {
-      rm[0] = fmaxf(rm[0], __shfl_xor_sync(0xffffffffu, rm[0], o));
-      rs[0] += __shfl_xor_sync(0xffffffffu, rs[0], o);
+    for (int n = RR, o = 16; o > 0; o >>= 1) {
+      if (n > 1) {
+        const bool hi = tx & o;
+#pragma unroll
+        for (int k = 0; k < n / 2; ++k) {
+          const T sendm = hi ? rm[k] : rm[k + n / 2], sends = hi ? rs[k] : rs[k + n / 2];
+          const T gm = __shfl_xor_sync(0xffffffffu, sendm, o);
+          const T gs = __shfl_xor_sync(0xffffffffu, sends, o);
+          rm[k] = rc_absmax(hi ? rm[k + n / 2] : rm[k], gm);
+          rs[k] = (hi ? rs[k + n / 2] : rs[k]) + gs;
+        }
+        if (hi) ri += n / 2;
+        n /= 2;
+      } else {
+        rm[0] = rc_absmax(rm[0], __shfl_xor_sync(0xffffffffu, rm[0], o));
+        rs[0] += __shfl_xor_sync(0xffffffffu, rs[0], o);
+      }
     }
-    const int64_t r = rb + ((tx >> 4) & 1) * 4 + ((tx >> 3) & 1) * 2 + ((tx >> 2) & 1);
-    if ((tx & 3) == 0 && r < rend) rpart[r * nct + ct] = make_double2(rm[0], rs[0]);
+    const int64_t r = rb + ri;
+    if ((tx & (32 / RR - 1)) == 0 && r < rend)
+      rpart[r * nct + ct] = make_double2((double)rm[0], (double)rs[0]);
   }
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    sm[ty][rc_col<float>(tx, j)] = cm[j];
-    sq[ty][rc_col<float>(tx, j)] = cs[j];
+    sm[ty][rc_col<T>(tx, j)] = cm[j];
+    sq[ty][rc_col<T>(tx, j)] = cs[j];
   }
   __syncthreads();
   const int64_t c = c0 + threadIdx.x;
@@ -765,9 +771,18 @@ __global__ void __launch_bounds__(256)
   __shared__ int ser[128], sec[32];
   const int64_t r0 = (int64_t)blockIdx.x * 128, c0 = (int64_t)blockIdx.y * 32;
   const int t = threadIdx.x, tx = t & 31, ty = t >> 5;
-  for (int i = ty; i < 128; i += 8) {
-    const int64_t r = r0 + i, c = c0 + tx;
-    tile[i][tx] = (r < m && c < n) ? __ldcs(X + r * ldx + c) : 0.0;
+  {
+    // all 16 loads of a thread in flight before the shared-memory stores (a
+    // load -> store loop left one load in flight: 58 % of DRAM bandwidth)
+    double v[16];
+    const int64_t c = c0 + tx;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const int64_t r = r0 + ty + 8 * k;
+      v[k] = (r < m && c < n) ? __ldcs(X + r * ldx + c) : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) tile[ty + 8 * k][tx] = v[k];
   }
   if (t < 128) ser[t] = (er && r0 + t < m) ? er[r0 + t] : 0;
   if (t < 32) sec[t] = (ec && c0 + t < n) ? ec[c0 + t] : 0;
@@ -1327,21 +1342,16 @@ void oz_both_exp_t(const T* X, int64_t rows, int64_t cols, int64_t ldx, int32_t*
   XB_REQUIRE(nrt < 65536, XB_EUNSUPPORTED, "oz_both_exp: more than 2^25 rows");
   double2* rpart = static_cast<double2*>(scratch);
   double2* cpart = rpart + rows * nct;
-  if constexpr (sizeof(T) == 4) {
-    static const bool generic = [] {
-      const char* e = getenv("XB_RC_GENERIC");
-      return e && atoi(e) != 0;
-    }();
-    if (!generic && ldx % 4 == 0 && (reinterpret_cast<uintptr_t>(X) % 16) == 0)
-      rc_stats_f32_kernel<<<dim3((unsigned)nct, (unsigned)nrt), 256, 0, st>>>(X, rows, cols, ldx,
-                                                                             rpart, cpart);
-    else
-      rc_stats_kernel<T><<<dim3((unsigned)nct, (unsigned)nrt), 256, 0, st>>>(X, rows, cols, ldx,
-                                                                            rpart, cpart);
-  } else {
+  static const bool generic = [] {
+    const char* e = getenv("XB_RC_GENERIC");
+    return e && atoi(e) != 0;
+  }();
+  if (!generic && (sizeof(T) == 8 || (ldx % 4 == 0 && (reinterpret_cast<uintptr_t>(X) % 16) == 0)))
+    rc_stats_fast_kernel<T><<<dim3((unsigned)nct, (unsigned)nrt), 256, 0, st>>>(X, rows, cols, ldx,
+                                                                               rpart, cpart);
+  else
     rc_stats_kernel<T><<<dim3((unsigned)nct, (unsigned)nrt), 256, 0, st>>>(X, rows, cols, ldx,
                                                                           rpart, cpart);
-  }
   check_launch("rc_stats");
   rc_finish_kernel<<<(unsigned)ceil_div(rows, 256), 256, 0, st>>>(rpart, rows, nct, nct, 1, cols,
                                                                   erow, wide);
