@@ -181,6 +181,13 @@ struct Csr {
 // Y (rows x l, ldy) = A X, X (cols x l, ldx). Deterministic gather SpMM.
 void launch_spmm(const Csr& a, const double* X, int64_t ldx, double* Y, int64_t ldy, int l,
                  cudaStream_t st);
+// The same over per-row entry ranges [lo[i], hi[i]); accumulate: Y += A X.
+void launch_spmm_seg(const Csr& a, const int64_t* lo, const int64_t* hi, const double* X,
+                     int64_t ldx, double* Y, int64_t ldy, int l, bool accumulate,
+                     cudaStream_t st);
+// off[b rows + i] = first entry of row i with column >= b bw, b = 0..nb
+// (segments sorted by column).
+void launch_seg_split(const Csr& a, int nb, int64_t bw, int64_t* off, cudaStream_t st);
 // COO (rows sorted, int64 indices) -> CSR rowptr + int32 columns.
 void launch_coo_to_csr(const int64_t* rows, const int64_t* cols, int64_t nnz, int64_t m,
                        int64_t* rowptr, int32_t* col32, cudaStream_t st);

@@ -640,6 +640,10 @@ void spmm_on_a(xb_ctx* c, const Csr& s, const double* X, double* Y, int lp, int 
     const char* e = getenv("XB_SPMM_PANEL");
     return e ? atoi(e) : 0;
   }();
+  static const int blocks_env = [] {
+    const char* e = getenv("XB_SPMM_BLOCKS");
+    return e ? atoi(e) : 0;
+  }();
   int w = 0;
   if (panel_env > 0) {
     w = panel_env;
@@ -653,6 +657,22 @@ void spmm_on_a(xb_ctx* c, const Csr& s, const double* X, double* Y, int lp, int 
       launch_copy2d(X + h0, s.cols, wc, lp, P, wc, c->st);
       launch_spmm(s, P, wc, Y + h0, lp, wc, c->st);
     }
+  } else if (blocks_env >= 0 && (double)s.cols * lp * 8.0 > 256e6) {
+    // Row blocks of the gathered operand: for A^T Q the 960 MB Q has no
+    // L2-sized column panel, so A^T's segments (sorted by A row) are cut at
+    // ~100 MB row blocks of Q and Z accumulates the blocks in order: every
+    // pass gathers from one L2-sized window of Q (deterministic; the sum
+    // order is block by block, each in row order). XB_SPMM_BLOCKS: -1 off,
+    // 0 auto, n forced.
+    const int nb = blocks_env > 0 ? blocks_env
+                                  : (int)std::ceil((double)s.cols * lp * 8.0 / 100e6);
+    const int64_t bw = ceil_div(s.cols, (int64_t)nb);
+    int64_t* off = static_cast<int64_t*>(
+        c->buf("spmm_off", (size_t)(nb + 1) * s.rows * sizeof(int64_t)));
+    launch_seg_split(s, nb, bw, off, c->st);
+    for (int b = 0; b < nb; ++b)
+      launch_spmm_seg(s, off + (int64_t)b * s.rows, off + (int64_t)(b + 1) * s.rows, X, lp, Y, lp,
+                      lp, b > 0, c->st);
   } else {
     launch_spmm(s, X, lp, Y, lp, lp, c->st);
   }

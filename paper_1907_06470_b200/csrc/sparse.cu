@@ -31,9 +31,10 @@ namespace {
 // runs in the row's column order (deterministic, no atomics).
 template <int NCH, int VEC>
 __global__ void __launch_bounds__(256)
-    spmm_kernel(int64_t rows, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+    spmm_kernel(int64_t rows, const int64_t* __restrict__ seg_lo,
+                const int64_t* __restrict__ seg_hi, const int32_t* __restrict__ col,
                 const double* __restrict__ val, const double* __restrict__ X, int64_t ldx,
-                double* __restrict__ Y, int64_t ldy, int l) {
+                double* __restrict__ Y, int64_t ldy, int l, int accumulate) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -43,7 +44,7 @@ __global__ void __launch_bounds__(256)
     for (int h = 0; h < NCH; ++h)
 #pragma unroll
       for (int v = 0; v < VEC; ++v) acc[h][v] = 0.0;
-    const int64_t e0 = __ldg(rowptr + i), e1 = __ldg(rowptr + i + 1);
+    const int64_t e0 = __ldg(seg_lo + i), e1 = __ldg(seg_hi + i);
     for (int64_t base = e0; base < e1; base += 32) {
       const int64_t e = base + lane;
       int32_t cj = 0;
@@ -113,11 +114,44 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
     for (int h = 0; h < NCH; ++h) {
       if (VEC * lane + 32 * VEC * h < l) {
-        if (VEC == 2)
-          __stcs(reinterpret_cast<double2*>(yr + 64 * h), make_double2(acc[h][0], acc[h][VEC - 1]));
-        else
+        if (VEC == 2) {
+          double2 o = make_double2(acc[h][0], acc[h][VEC - 1]);
+          if (accumulate) {
+            const double2 p = *reinterpret_cast<const double2*>(yr + 64 * h);
+            o.x = p.x + o.x;
+            o.y = p.y + o.y;
+          }
+          if (accumulate)
+            *reinterpret_cast<double2*>(yr + 64 * h) = o;
+          else
+            __stcs(reinterpret_cast<double2*>(yr + 64 * h), o);
+        } else if (accumulate) {
+          yr[32 * h] += acc[h][0];
+        } else {
           __stcs(yr + 32 * h, acc[h][0]);
+        }
       }
+    }
+  }
+}
+
+// Row-block split of a CSR whose segments are sorted by column index:
+// off[b * rows + i] = first entry of row i with col >= b * bw (b <= nb), so
+// block b of row i is [off[b rows + i], off[(b+1) rows + i]).
+__global__ void seg_split_kernel(int64_t rows, const int64_t* __restrict__ rowptr,
+                                 const int32_t* __restrict__ col, int nb, int64_t bw,
+                                 int64_t* __restrict__ off) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e0 = rowptr[i], e1 = rowptr[i + 1];
+    for (int b = 0; b <= nb; ++b) {
+      const int64_t key = (int64_t)b * bw;
+      int64_t lo = e0, hi = e1;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if ((int64_t)col[mid] < key) lo = mid + 1; else hi = mid;
+      }
+      off[(int64_t)b * rows + i] = lo;
     }
   }
 }
@@ -288,8 +322,9 @@ int blocks_for(int64_t work, int per_block) {
 
 }  // namespace
 
-void launch_spmm(const Csr& a, const double* X, int64_t ldx, double* Y, int64_t ldy, int l,
-                 cudaStream_t st) {
+void launch_spmm_seg(const Csr& a, const int64_t* lo, const int64_t* hi, const double* X,
+                     int64_t ldx, double* Y, int64_t ldy, int l, bool accumulate,
+                     cudaStream_t st) {
   if (a.rows <= 0 || l <= 0) return;
   XB_REQUIRE(l <= 576, XB_EUNSUPPORTED, "spmm: l > 576");
   // 16-byte loads when every row of X and Y starts 16-byte aligned and l is even
@@ -297,9 +332,10 @@ void launch_spmm(const Csr& a, const double* X, int64_t ldx, double* Y, int64_t 
                    (reinterpret_cast<uintptr_t>(X) % 16 == 0) &&
                    (reinterpret_cast<uintptr_t>(Y) % 16 == 0);
   const int blocks = blocks_for(a.rows, 8);
-#define XB_SPMM(NCH, VEC)                                                                    \
-  spmm_kernel<NCH, VEC><<<blocks, 256, 0, st>>>(a.rows, a.rowptr, a.col, a.val, X, ldx, Y, ldy, \
-                                                l)
+  const int acc = accumulate ? 1 : 0;
+#define XB_SPMM(NCH, VEC)                                                                      \
+  spmm_kernel<NCH, VEC><<<blocks, 256, 0, st>>>(a.rows, lo, hi, a.col, a.val, X, ldx, Y, ldy, l, \
+                                                acc)
   if (vec) {
     switch ((l + 63) / 64) {
       case 1: XB_SPMM(1, 2); break;
@@ -320,6 +356,17 @@ void launch_spmm(const Csr& a, const double* X, int64_t ldx, double* Y, int64_t 
   }
 #undef XB_SPMM
   check_launch("spmm");
+}
+
+void launch_spmm(const Csr& a, const double* X, int64_t ldx, double* Y, int64_t ldy, int l,
+                 cudaStream_t st) {
+  launch_spmm_seg(a, a.rowptr, a.rowptr + 1, X, ldx, Y, ldy, l, false, st);
+}
+
+void launch_seg_split(const Csr& a, int nb, int64_t bw, int64_t* off, cudaStream_t st) {
+  if (a.rows <= 0) return;
+  seg_split_kernel<<<blocks_for(a.rows, 256), 256, 0, st>>>(a.rows, a.rowptr, a.col, nb, bw, off);
+  check_launch("seg_split");
 }
 
 void launch_coo_to_csr(const int64_t* rows, const int64_t* cols, int64_t nnz, int64_t m,
