@@ -161,9 +161,11 @@ void ozf_gemm(const float* A, int64_t lda, bool trans_a, const int32_t* eL, cons
 // C (M x N) = L R: L = left slices (rows_p x kp, 128-row interleaved tiles,
 // row exponents eL), R = right slices (np x kp, 64-row tiles, column
 // exponents eR).
+// tri 1: C is a Gram (only tiles on / above the diagonal are computed; the
+// rest of C is left unspecified); tri 2: R is upper triangular.
 void ozgemm(const int8_t* L, int64_t rows_p, int64_t kp, const int32_t* eL, const int8_t* R,
             int64_t np, const int32_t* eR, int64_t M, int64_t N, int64_t K, double* C, int64_t ldc,
-            bool accumulate, int S, double* work, cudaStream_t st);
+            bool accumulate, int S, double* work, cudaStream_t st, int tri = 0);
 
 // Returns the number of split-K slices that will be used for this shape.
 int dgemm_plan_splits(const DGemmArgs& g);

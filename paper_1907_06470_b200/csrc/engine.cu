@@ -350,7 +350,7 @@ void gemm(xb_ctx* c, bool ta, int64_t M, int64_t N, int64_t K, const double* A, 
 // 1e-4 / 1e-3 targets leave a large margin over the ~1e-14 product error)
 // and by the XB_GEMM_OZ diagnostics.
 void oz_gemm64(xb_ctx* c, bool ta, int64_t m, int64_t n, int64_t kdim, const double* A,
-               int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc) {
+               int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc, int tri = 0) {
   const int S = oz_slices();
   const int64_t kp = round_up(kdim, 32), np = round_up(n, 64), mp = round_up(m, 128);
   int8_t* L = static_cast<int8_t*>(c->buf("ozg_L", (size_t)S * mp * kp));
@@ -367,18 +367,21 @@ void oz_gemm64(xb_ctx* c, bool ta, int64_t m, int64_t n, int64_t kdim, const dou
     oz_slice_both(A, m, kdim, lda, eL, nullptr, L, mp, kp, nullptr, round_up(kdim, 128),
                   round_up(m, 32), S, c->st);
   }
-  oz_col_exp(B, kdim, n, ldb, eR, scr, nullptr, c->st);
+  if (ta && A == B && lda == ldb && m == n)  // Gram: the same column exponents
+    XB_CUDA(cudaMemcpyAsync(eR, eL, (size_t)m * sizeof(int32_t), cudaMemcpyDeviceToDevice, c->st));
+  else
+    oz_col_exp(B, kdim, n, ldb, eR, scr, nullptr, c->st);
   oz_slice_right(B, kdim, n, ldb, eR, R, np, kp, S, c->st);
   const size_t wd = oz_workspace_doubles(m, n, kdim);
   double* work = wd ? c->dbuf("split", wd) : nullptr;
-  ozgemm(L, mp, kp, eL, R, np, eR, m, n, kdim, C, ldc, false, S, work, c->st);
+  ozgemm(L, mp, kp, eL, R, np, eR, m, n, kdim, C, ldc, false, S, work, c->st, tri);
 }
 
 // gemm() or, when `oz` and the big operand has >= 2^24 elements, oz_gemm64
 void gemm_big(xb_ctx* c, bool oz, bool ta, int64_t M, int64_t N, int64_t K, const double* A,
               int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc, int tri = 0) {
   if (oz && oz_enabled() && (double)M * (double)K >= (double)(1 << 24) && M >= 64 && K >= 64)
-    oz_gemm64(c, ta, M, N, K, A, lda, B, ldb, C, ldc);
+    oz_gemm64(c, ta, M, N, K, A, lda, B, ldb, C, ldc, tri);
   else
     gemm(c, ta, M, N, K, A, lda, B, ldb, C, ldc, tri);
 }

@@ -230,8 +230,13 @@ __global__ void __launch_bounds__(OTHREADS, 1)
   const int nt = (int)(blockIdx.x % tiles_n);
   const int64_t mt = blockIdx.x / tiles_n;
   const int64_t m0 = mt * OBM, n0 = (int64_t)nt * OBN;
+  // dbg 64: Gram, only tiles on or above the diagonal are ever read;
+  // dbg 128: the right operand is upper triangular (rows k >= n0 + OBN of
+  // this n-tile are zero). Both come without clusters (cl = 1).
+  if ((dbg & 64) && n0 + OBN - 1 < m0) return;
   const int64_t kbeg = (int64_t)blockIdx.y * k_per_split;
-  const int64_t kend = min(K, kbeg + k_per_split);
+  int64_t kend = min(K, kbeg + k_per_split);
+  if (dbg & 128) kend = min(kend, n0 + OBN);
   const int ktiles = kend > kbeg ? (int)((kend - kbeg + OBK - 1) / OBK) : 0;
   C += (int64_t)blockIdx.y * split_stride;
 
@@ -873,7 +878,7 @@ __global__ void __launch_bounds__(256)
 template <int S>
 void launch_oz(const int8_t* L, const int8_t* R, int64_t rows_p, int64_t np, const int32_t* eL,
                const int32_t* eR, int64_t M, int64_t N, int64_t K, double* out, int64_t ldo,
-               int64_t stride, int64_t kps, int splits, int acc, cudaStream_t st) {
+               int64_t stride, int64_t kps, int splits, int acc, int tri, cudaStream_t st) {
   using Cfg = OCfg<S>;
   // Left slices straight from shared memory (TC = 0) by default. Staging
   // them in TMEM with tcgen05.cp (XB_OZ_TC=S) saves shared-memory reads for
@@ -901,7 +906,7 @@ void launch_oz(const int8_t* L, const int8_t* R, int64_t rows_p, int64_t np, con
     const char* e = getenv("XB_OZ_CLUSTER");
     return !(e && atoi(e) == 0);
   }();
-  const int cl = (cluster_on && tn >= 2 && tn <= 4) ? (int)tn : 1;
+  const int cl = (cluster_on && tri == 0 && tn >= 2 && tn <= 4) ? (int)tn : 1;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(OTHREADS);
@@ -915,7 +920,8 @@ void launch_oz(const int8_t* L, const int8_t* R, int64_t rows_p, int64_t np, con
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   XB_CUDA(cudaLaunchKernelEx(&cfg, kern, L, R, rows_p, np, eL, eR, M, N, K, out, ldo, stride,
-                             kps, acc, (int)tn, dbg, cl));
+                             kps, acc, (int)tn,
+                             dbg | (tri == 1 ? 64 : 0) | (tri == 2 ? 128 : 0), cl));
   check_launch("ozgemm");
 }
 
@@ -1408,7 +1414,7 @@ int oz_plan_splits(int64_t K) { return (int)std::max<int64_t>(1, ceil_div(K, 163
 
 void ozgemm(const int8_t* L, int64_t rows_p, int64_t kp, const int32_t* eL, const int8_t* R,
             int64_t np, const int32_t* eR, int64_t M, int64_t N, int64_t K, double* C, int64_t ldc,
-            bool accumulate, int S, double* work, cudaStream_t st) {
+            bool accumulate, int S, double* work, cudaStream_t st, int tri) {
   if (M <= 0 || N <= 0) return;
   XB_REQUIRE(kp % OBK == 0 && rows_p % OBM == 0 && rows_p >= M && np % OBN == 0 && np >= N &&
                  kp >= K,
@@ -1425,7 +1431,8 @@ void ozgemm(const int8_t* L, int64_t rows_p, int64_t kp, const int32_t* eL, cons
     stride = M * ldo;
   }
   const int acc = (splits == 1 && accumulate) ? 1 : 0;
-#define OZ_RUN(SS) launch_oz<SS>(L, R, rows_p, np, eL, eR, M, N, K, out, ldo, stride, kps, splits, acc, st)
+#define OZ_RUN(SS) \
+  launch_oz<SS>(L, R, rows_p, np, eL, eR, M, N, K, out, ldo, stride, kps, splits, acc, tri, st)
   OZ_DISPATCH(S, OZ_RUN)
 #undef OZ_RUN
   if (splits > 1) launch_split_reduce(work, M, N, ldo, stride, splits, C, ldc, accumulate, st);
