@@ -38,6 +38,26 @@ class ParseError(XsvdError):
         self.line = line
 
 
+class FormatError(XsvdError):
+    """A block file or descriptor is not in the expected format (errors.py:26)."""
+
+
+class BlockAbsentError(XsvdError):
+    """A block or descriptor is missing from the store (errors.py:30)."""
+
+
+class BlockCorruptError(XsvdError):
+    """A stored block fails its header or checksum checks (errors.py:34)."""
+
+
+class PlanNotFoundError(XsvdError):
+    """No resumable plan under the workdir (errors.py:53)."""
+
+
+class ConfigMismatchError(XsvdError):
+    """A resume was asked under settings other than the plan's (errors.py:57)."""
+
+
 XB_ESHAPE, XB_EVALUE, XB_ENOMEM, XB_ECONV, XB_ECUDA, XB_ENCCL, XB_EUNSUPPORTED = 1, 2, 3, 4, 5, 6, 7
 XB_EPARSE = 8
 

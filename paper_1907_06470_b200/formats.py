@@ -4,6 +4,8 @@ parse_matrix_market(path, pool, matrix_id, *, precision=SINGLE,
                     spill_bytes=..., chunk_lines=...) -> StoredMatrix
 read_matrix_market_info(path) -> {"rows", "cols", "entries", "field", "symmetric"}
 write_matrix_market(path, mat)
+write_block_file(path, mat) / read_block_file(path, pool, matrix_id=None)
+    (the one-file block export, implemented in store.py)
 
 Parsing runs in the library's native multi-threaded reader (csrc/mmio.cu,
 xb_mm_read): same acceptance rules, messages and 1-based line numbers
@@ -22,6 +24,7 @@ import numpy as np
 from . import _lib
 from .core import Precision, as_precision
 from .pool import canonical_coo, matrix_from_coo
+from .store import read_block_file, write_block_file  # noqa: F401  (formats.py:471-519)
 
 DEFAULT_SPILL_BYTES = 256 << 20
 DEFAULT_CHUNK_LINES = 500_000

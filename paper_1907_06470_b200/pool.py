@@ -17,17 +17,21 @@ import numpy as np
 
 from .core import (BlockPartition, Density, DenseBlock, MatrixDescriptor, Precision, SparseBlock,
                    as_precision, transpose_view)
-from .errors import ShapeError, XsvdError
+from .errors import BlockAbsentError, BudgetError, ShapeError, XsvdError
 
 
 class BlockPool:
+    """In-core tiles; with a `store.BlockStore`, tiles missing from memory are
+    loaded from it (pool.py:271-278) and `flush_matrix` persists dirty tiles
+    synchronously (pool.py:315-335), which is what durable step records rely
+    on. No byte budget / eviction: HBM residency is the library's job."""
+
     def __init__(self, store=None, budget=None):
-        if store is not None:
-            raise XsvdError("the GPU pool mirror is in-core only (no BlockStore)")
-        self.store = None
+        self.store = store
         self.budget = budget
         self._descs: dict[str, MatrixDescriptor] = {}
         self._tiles: dict[tuple, object] = {}
+        self._dirty: set = set()
         self._lock = threading.Lock()
 
     def register(self, desc):
@@ -43,18 +47,41 @@ class BlockPool:
     def put(self, matrix_id, ti, tj, block, *, dirty=True):
         with self._lock:
             self._tiles[(matrix_id, ti, tj)] = block
+            if dirty:
+                self._dirty.add((matrix_id, ti, tj))
 
     def get(self, matrix_id, ti, tj, *, pin=False):
-        return self._tiles[(matrix_id, ti, tj)]
+        key = (matrix_id, ti, tj)
+        with self._lock:
+            block = self._tiles.get(key)
+            if block is not None:
+                return block
+            if self.store is None:
+                raise BlockAbsentError(f"block {matrix_id}[{ti},{tj}] not resident (no store)")
+            block = self.store.load_block(matrix_id, ti, tj)
+            self._tiles[key] = block
+            return block
 
     def drop_matrix(self, matrix_id, *, delete_files=False):
         with self._lock:
             for key in [k for k in self._tiles if k[0] == matrix_id]:
                 del self._tiles[key]
+            self._dirty = {k for k in self._dirty if k[0] != matrix_id}
             self._descs.pop(matrix_id, None)
+            if delete_files and self.store is not None:
+                self.store.delete_matrix_blocks(matrix_id)
 
     def flush_matrix(self, matrix_id, *, evict=False):
-        return None
+        """On return every tile of the matrix is durable (pool.py:315-335)."""
+        with self._lock:
+            for key in sorted(k for k in self._dirty if k[0] == matrix_id):
+                if self.store is None:
+                    raise BudgetError("cannot persist blocks without a workdir")
+                self.store.store_block(key[0], key[1], key[2], self._tiles[key])
+                self._dirty.discard(key)
+            if evict:
+                for key in [k for k in self._tiles if k[0] == matrix_id]:
+                    del self._tiles[key]
 
     def close(self):
         return None
@@ -130,10 +157,18 @@ def stored_to_array(mat) -> np.ndarray:
     return out.T if d.transposed else out
 
 
+def _register(pool, desc):
+    """Register and, with a store, persist the descriptor (pool.py:548-550)."""
+    desc = pool.register(desc)
+    if getattr(pool, "store", None) is not None:
+        pool.store.save_descriptor(desc)
+    return desc
+
+
 def create_matrix(pool, matrix_id, rows, cols, *, precision, density=Density.DENSE, nnz=None):
     desc = MatrixDescriptor(matrix_id, rows, cols, density, as_precision(precision),
                             nnz=nnz or 0)
-    return StoredMatrix(pool.register(desc), pool)
+    return StoredMatrix(_register(pool, desc), pool)
 
 
 def matrix_from_dense(pool, matrix_id, array, *, precision, grid=None) -> StoredMatrix:
@@ -144,8 +179,8 @@ def matrix_from_dense(pool, matrix_id, array, *, precision, grid=None) -> Stored
     precision = as_precision(precision)
     part = BlockPartition.single(m, n) if grid is None else BlockPartition.grid(m, n, *grid)
     pool.drop_matrix(matrix_id)  # results overwrite a previous matrix of the same id
-    desc = pool.register(MatrixDescriptor(matrix_id, m, n, Density.DENSE, precision,
-                                          partition=part))
+    desc = _register(pool, MatrixDescriptor(matrix_id, m, n, Density.DENSE, precision,
+                                            partition=part))
     mat = StoredMatrix(desc, pool)
     for ti in range(part.n_row_tiles):
         r0, r1 = part.row_span(ti)
@@ -171,8 +206,8 @@ def matrix_from_coo(pool, matrix_id, rows, cols, coo_rows, coo_cols, coo_values,
         boundary[1:] |= c[1:] != c[:-1]
         starts = np.flatnonzero(boundary)
         r, c, v = r[starts], c[starts], np.add.reduceat(v, starts)
-    desc = pool.register(MatrixDescriptor(matrix_id, rows, cols, Density.SPARSE, precision,
-                                          nnz=len(v)))
+    desc = _register(pool, MatrixDescriptor(matrix_id, rows, cols, Density.SPARSE, precision,
+                                            nnz=len(v)))
     mat = StoredMatrix(desc, pool)
     idt = np.uint32 if max(rows, cols) < 2**32 else np.uint64
     mat.set_tile(0, 0, SparseBlock(0, rows, 0, cols, r.astype(idt), c.astype(idt), v))
