@@ -349,9 +349,17 @@ void gemm(xb_ctx* c, bool ta, int64_t M, int64_t N, int64_t K, const double* A, 
 // Used for the n-side orthonormalisation products of float32 configs (the
 // 1e-4 / 1e-3 targets leave a large margin over the ~1e-14 product error)
 // and by the XB_GEMM_OZ diagnostics.
+static int oz_qr_slices() {
+  static const int s = [] {
+    const char* e = getenv("XB_OZ_QR_SLICES");
+    return e ? std::max(3, std::min(6, atoi(e))) : oz_slices();
+  }();
+  return s;
+}
+
 void oz_gemm64(xb_ctx* c, bool ta, int64_t m, int64_t n, int64_t kdim, const double* A,
                int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc, int tri = 0) {
-  const int S = oz_slices();
+  const int S = oz_qr_slices();
   const int64_t kp = round_up(kdim, 32), np = round_up(n, 64), mp = round_up(m, 128);
   int8_t* L = static_cast<int8_t*>(c->buf("ozg_L", (size_t)S * mp * kp));
   int8_t* R = static_cast<int8_t*>(c->buf("ozg_R", (size_t)S * np * kp));
