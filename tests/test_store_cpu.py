@@ -178,3 +178,60 @@ def test_config_json_round_trip():
                      precision=Precision.SINGLE, gram_path=True)
     back = RsvdConfig.from_json(cfg.to_json())
     assert back.digest() == cfg.digest()
+
+
+def test_truncation_fuzz_never_returns_wrong_data(tmp_path):
+    """Any prefix of a stored sparse tile is corrupt or absent, never data
+    (reference tests/test_store.py:98-110)."""
+    from paper_1907_06470_b200 import BlockAbsentError
+
+    store = BlockStore(str(tmp_path))
+    mat = _gold_mats(BlockPool())["sp"]
+    store.store_block("s", 0, 0, mat.tile(0, 0))
+    path = store.block_path("s", 0, 0)
+    raw = open(path, "rb").read()
+    rng = np.random.default_rng(4)
+    for cut in list(rng.integers(0, len(raw), 30)) + [0, 63, 64, len(raw) - 1]:
+        open(path, "wb").write(raw[:int(cut)])
+        with pytest.raises((BlockCorruptError, BlockAbsentError)):
+            store.load_block("s", 0, 0)
+    open(path, "wb").write(raw)
+    np.testing.assert_array_equal(store.load_block("s", 0, 0).values, mat.tile(0, 0).values)
+
+
+def test_crash_at_every_barrier_is_conservative(tmp_path):
+    """A kill at any write barrier never leaves a done record without intact
+    outputs (reference tests/test_store.py:204-243)."""
+    from paper_1907_06470_b200 import Density, MatrixDescriptor, StepRecord
+
+    class Crash(Exception):
+        pass
+
+    def write_all(store):
+        store.save_descriptor(MatrixDescriptor("m", 4, 4, Density.DENSE, Precision.DOUBLE))
+        from paper_1907_06470_b200 import DenseBlock
+
+        store.store_block("m", 0, 0, DenseBlock(0, 4, 0, 4, np.eye(4)))
+        store.write_step(StepRecord("p", 0, "op", [], ["m"], status="done"))
+
+    seen = []
+    probe = BlockStore(str(tmp_path / "probe"))
+    probe.fault_hook = lambda name, path: seen.append(name)
+    write_all(probe)
+    assert {"payload-written", "payload-synced", "payload-visible", "record-written",
+            "record-synced", "record-visible"} <= set(seen)
+    for i, target in enumerate(seen):
+        store = BlockStore(str(tmp_path / f"crash_{i}"))
+        count = [0]
+
+        def hook(name, path, i=i):
+            if count[0] == i:
+                raise Crash()
+            count[0] += 1
+
+        store.fault_hook = hook
+        with pytest.raises(Crash):
+            write_all(store)
+        store.fault_hook = None
+        recs = store.scan_plan()
+        assert 0 not in recs or recs[0].status != "done" or store.verify_block("m", 0, 0)
