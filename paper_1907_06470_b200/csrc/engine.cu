@@ -346,20 +346,24 @@ void gemm(xb_ctx* c, bool ta, int64_t M, int64_t N, int64_t K, const double* A, 
 
 // C = op(A) B for f64 device operands on the int8 tensor pipe (Ozaki
 // slices of both operands, ozgemm.cu): exponents, slicing and the GEMM.
-// Used for the n-side orthonormalisation products of float32 configs (the
-// 1e-4 / 1e-3 targets leave a large margin over the ~1e-14 product error)
-// and by the XB_GEMM_OZ diagnostics.
+// Used for the n-side orthonormalisation products of float32 configs at
+// oz_qr_slices() (the 1e-4 / 1e-3 targets leave a large margin) and by the
+// XB_GEMM_OZ diagnostics at the f64 count, oz_slices().
+// Slice count of the float32 configs' f64 products on the int8 pipe (n-side
+// QR Grams, X R^-1, the V lift). 4 slices carry >= 28 bits, beyond the f32
+// data; measured at a cfg5-like 2048 x 65536 (tools/probe_qr_slices.py,
+// profiles/r01_qr_slices.md): sigma 3.9e-8 / angle 2.5e-5 at 4 slices vs
+// 3.6e-8 / 3.4e-5 at 6 (targets 1e-4 / 1e-3); 3 slices 1.2e-7 / 9.7e-5.
 static int oz_qr_slices() {
   static const int s = [] {
     const char* e = getenv("XB_OZ_QR_SLICES");
-    return e ? std::max(3, std::min(6, atoi(e))) : oz_slices();
+    return e ? std::max(3, std::min(6, atoi(e))) : 4;
   }();
   return s;
 }
 
 void oz_gemm64(xb_ctx* c, bool ta, int64_t m, int64_t n, int64_t kdim, const double* A,
-               int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc, int tri = 0) {
-  const int S = oz_qr_slices();
+               int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc, int tri, int S) {
   const int64_t kp = round_up(kdim, 32), np = round_up(n, 64), mp = round_up(m, 128);
   int8_t* L = static_cast<int8_t*>(c->buf("ozg_L", (size_t)S * mp * kp));
   int8_t* R = static_cast<int8_t*>(c->buf("ozg_R", (size_t)S * np * kp));
@@ -389,7 +393,7 @@ void oz_gemm64(xb_ctx* c, bool ta, int64_t m, int64_t n, int64_t kdim, const dou
 void gemm_big(xb_ctx* c, bool oz, bool ta, int64_t M, int64_t N, int64_t K, const double* A,
               int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc, int tri = 0) {
   if (oz && oz_enabled() && (double)M * (double)K >= (double)(1 << 24) && M >= 64 && K >= 64)
-    oz_gemm64(c, ta, M, N, K, A, lda, B, ldb, C, ldc, tri);
+    oz_gemm64(c, ta, M, N, K, A, lda, B, ldb, C, ldc, tri, oz_qr_slices());
   else
     gemm(c, ta, M, N, K, A, lda, B, ldb, C, ldc, tri);
 }
@@ -1432,7 +1436,8 @@ void gemm_any(xb_ctx* c, bool f32, bool ta, int64_t m, int64_t n, int64_t kdim, 
     if (oz_dbg && m > 0 && n > 0 && kdim > 0) {
       // diagnostics (tools/oz_check.py): the same product on the int8 slices
       oz_gemm64(c, ta, m, n, kdim, static_cast<const double*>(dA), lda,
-                static_cast<const double*>(dB), ldb, static_cast<double*>(dC), ldc);
+                static_cast<const double*>(dB), ldb, static_cast<double*>(dC), ldc, 0,
+                oz_slices());
       return;
     }
     gemm(c, ta, m, n, kdim, static_cast<const double*>(dA), lda, static_cast<const double*>(dB),
