@@ -229,10 +229,11 @@ void launch_deficient(const double* R, int64_t ldr, int l, double eps, int* coun
 // One-sided Jacobi SVD of M = R^T (R: l x l upper, ldr): produces
 //   s[l] (descending), Ub (l x l, ldu: columns = sorted, sign-fixed left
 //   singular vectors of M), Wk (l x k, ldw: matching right singular vectors,
-//   same signs), status (0 ok, 1 no convergence).
+//   same signs), status (0 ok, 1 no convergence). tol: rotation threshold on
+//   |x_p . x_q| / (|x_p| |x_q|); <= 0 selects the f64 default max(1e-15, l eps).
 void launch_jacobi_svd(const double* R, int64_t ldr, int l, int k, double* Ub, int64_t ldu,
                        double* s, double* Wk, int64_t ldw, double* work, int* status,
-                       cudaStream_t st);
+                       cudaStream_t st, double tol = -1.0);
 
 // NCCL (dlopen'ed, comm.cu): unique id, communicator, in-place sum.
 void nccl_unique_id(unsigned char out[128]);

@@ -354,6 +354,17 @@ void gemm(xb_ctx* c, bool ta, int64_t M, int64_t N, int64_t K, const double* A, 
 // data; measured at a cfg5-like 2048 x 65536 (tools/probe_qr_slices.py,
 // profiles/r01_qr_slices.md): sigma 3.9e-8 / angle 2.5e-5 at 4 slices vs
 // 3.6e-8 / 3.4e-5 at 6 (targets 1e-4 / 1e-3); 3 slices 1.2e-7 / 9.7e-5.
+// Jacobi rotation threshold for the small SVD of a float32 factorisation
+// (XB_JACOBI_TOL_F32; <= 0 keeps the f64 threshold). float64 always uses
+// the f64 threshold.
+static double jacobi_tol(bool f32) {
+  static const double t = [] {
+    const char* e = getenv("XB_JACOBI_TOL_F32");
+    return e ? atof(e) : -1.0;
+  }();
+  return f32 ? t : -1.0;
+}
+
 static int oz_qr_slices() {
   static const int s = [] {
     const char* e = getenv("XB_OZ_QR_SLICES");
@@ -1132,7 +1143,7 @@ void rsvd_impl(xb_ctx* c, const AOp& op_in, int64_t m, int64_t n, const void* d_
   }
 
   clk.enter(kSvd);
-  launch_jacobi_svd(Rf, lp, l, k, Ub, lp, sv, Wk, kp, jw, jstat, st);
+  launch_jacobi_svd(Rf, lp, l, k, Ub, lp, sv, Wk, kp, jw, jstat, st, jacobi_tol(a.f32));
 
   clk.enter(kPost);
   gemm(c, false, m, k, lp, Qm, lp, Ub, lp, out.U, out.ldu);  // U = Q U_B[:, :k]
@@ -1378,7 +1389,7 @@ void rsvd_stream(xb_ctx* c, const void* hostA, int64_t host_lda, bool f32, int64
   clk.enter(kSvdPrep);
   cholqr2(c, s, Zn, n, Tn, Qn, Rf);
   clk.enter(kSvd);
-  launch_jacobi_svd(Rf, lp, l, k, Ub, lp, sv, Wk, kp, jw, jstat, st);
+  launch_jacobi_svd(Rf, lp, l, k, Ub, lp, sv, Wk, kp, jw, jstat, st, jacobi_tol(f32));
   clk.enter(kPost);
   gemm(c, false, m, k, lp, Qm, lp, Ub, lp, out.U, out.ldu);
   gemm(c, false, n, k, lp, Qn, lp, Wk, kp, out.V, out.ldv);

@@ -912,10 +912,10 @@ size_t jacobi_work_doubles(int l) {
 
 void launch_jacobi_svd(const double* R, int64_t ldr, int l, int k, double* Ub, int64_t ldu,
                        double* s, double* Wk, int64_t ldw, double* work, int* status,
-                       cudaStream_t st) {
+                       cudaStream_t st, double tol_req) {
   const size_t lim = max_dyn_smem() - 512;  // static: s_rot
   const size_t one = (size_t)l * l * sizeof(double);
-  const double tol = fmax(1e-15, (double)l * DBL_EPSILON);
+  const double tol = tol_req > 0.0 ? tol_req : fmax(1e-15, (double)l * DBL_EPSILON);
   // one CTA while M's columns fit in shared memory, else (or on request,
   // XB_JACOBI=coop) the cooperative grid version
   static const int mode = [] {
