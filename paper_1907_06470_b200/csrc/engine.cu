@@ -354,13 +354,16 @@ void gemm(xb_ctx* c, bool ta, int64_t M, int64_t N, int64_t K, const double* A, 
 // data; measured at a cfg5-like 2048 x 65536 (tools/probe_qr_slices.py,
 // profiles/r01_qr_slices.md): sigma 3.9e-8 / angle 2.5e-5 at 4 slices vs
 // 3.6e-8 / 3.4e-5 at 6 (targets 1e-4 / 1e-3); 3 slices 1.2e-7 / 9.7e-5.
-// Jacobi rotation threshold for the small SVD of a float32 factorisation
-// (XB_JACOBI_TOL_F32; <= 0 keeps the f64 threshold). float64 always uses
-// the f64 threshold.
+// Jacobi rotation threshold for the small SVD of a float32 factorisation:
+// columns orthogonal to 1e-8 (relative) are far past the f32 targets and
+// save the last quadratic sweep (cfg5-like probe, l = 550: 11 -> 10 sweeps,
+// sigma 3.86e-8 and angles 2.5e-5 unchanged to 3 digits; cfg5 SVD0 stage
+// 38.6 -> 32.2 ms). XB_JACOBI_TOL_F32 overrides (<= 0: the f64 threshold).
+// float64 always uses the f64 threshold.
 static double jacobi_tol(bool f32) {
   static const double t = [] {
     const char* e = getenv("XB_JACOBI_TOL_F32");
-    return e ? atof(e) : -1.0;
+    return e ? atof(e) : 1e-8;
   }();
   return f32 ? t : -1.0;
 }
