@@ -359,13 +359,17 @@ void gemm(xb_ctx* c, bool ta, int64_t M, int64_t N, int64_t K, const double* A, 
 // save the last quadratic sweep (cfg5-like probe, l = 550: 11 -> 10 sweeps,
 // sigma 3.86e-8 and angles 2.5e-5 unchanged to 3 digits; cfg5 SVD0 stage
 // 38.6 -> 32.2 ms). XB_JACOBI_TOL_F32 overrides (<= 0: the f64 threshold).
-// float64 always uses the f64 threshold.
+// float64 uses max(1e-15, l eps) unless XB_JACOBI_TOL_F64 (experiments).
 static double jacobi_tol(bool f32) {
   static const double t = [] {
     const char* e = getenv("XB_JACOBI_TOL_F32");
     return e ? atof(e) : 1e-8;
   }();
-  return f32 ? t : -1.0;
+  static const double t64 = [] {
+    const char* e = getenv("XB_JACOBI_TOL_F64");
+    return e ? atof(e) : -1.0;
+  }();
+  return f32 ? t : t64;
 }
 
 static int oz_qr_slices() {
