@@ -88,6 +88,21 @@ def measured_peaks() -> dict:
         return {}
 
 
+def knob_guard(ctx) -> dict:
+    """Refuse to time with experiment knobs: the release library ignores XB_*
+    tuning/debug variables, but an experiment build reads them (some skip
+    work for timing studies). Returns the recorded XB_* environment."""
+    env = {k: v for k, v in sorted(os.environ.items()) if k.startswith("XB_")}
+    flags = int(ctx.lib.xb_build_flags())
+    stray = [k for k in env if k not in ("XB_TRACE",)]
+    if flags & 1:
+        raise SystemExit("bench.py refuses an experiment build of libxsvdb200.so "
+                         "(rebuild without XB_BUILD_EXPERIMENTS)")
+    if stray:
+        raise SystemExit(f"bench.py refuses non-default knobs in the environment: {stray}")
+    return {"xb_env": env, "build_flags": flags, "release_build": True}
+
+
 # -- clocks during the timed region ----------------------------------------------
 
 class ClockSampler:
@@ -101,8 +116,6 @@ class ClockSampler:
         self.lines = []
 
     def __enter__(self):
-        if os.environ.get("XB_BENCH_NO_CLOCKS"):  # diagnostics: timing without the sampler
-            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
@@ -200,48 +213,127 @@ def cpu_baseline(w, budget_s: float, threads: int) -> dict:
             "seconds": t_full, "size": r2, "sample_seconds": t2, "a0": a0}
 
 
+def _reference_input(w):
+    """The workload's A exactly as the GPU arm builds it (seeded construction
+    on the device with torch when a GPU is present — input generation only,
+    outside every timed region — then moved to host memory); a seeded
+    Gaussian A of the config's shape otherwise (the port's run time does not
+    depend on A's spectrum)."""
+    prec = np.float64 if w.precision == "double" else np.float32
+    try:
+        import torch
+
+        if torch.cuda.is_available():
+            from paper_1907_06470_b200.workloads import dense_lowrank_torch
+
+            a = dense_lowrank_torch(w.m, w.n, w.spectrum, w.noise, w.cfg, w.signal_rank,
+                                    dtype=torch.float64 if prec == np.float64 else torch.float32)
+            host = a.cpu().numpy()
+            del a
+            torch.cuda.empty_cache()
+            return host, "the GPU arm's seeded construction"
+    except ImportError:
+        pass
+    rng = np.random.default_rng(3000 + w.cfg)
+    return rng.standard_normal((w.m, w.n)).astype(prec), "seeded N(0,1) A of the config's shape"
+
+
+def _ref_thread_modes(cores):
+    """The reference's two ways to use a multi-core host: its
+    `threads` cell workers with one BLAS thread each, or one cell worker with
+    a multi-threaded BLAS."""
+    from contextlib import nullcontext
+
+    from threadpoolctl import threadpool_limits
+
+    return {"cells": (cores, nullcontext), "blas": (1, lambda: threadpool_limits(limits=cores,
+                                                                                 user_api="blas"))}
+
+
 def run_reference(args):
+    """The reference's CPU implementation of the path (the oracle port of the
+    shipped xsvd.randomized_svd driver) on this host's cores, on the FULL
+    workload every step (dense configs 1 and 2). Both thread modes run
+    during the warm-up and the faster one is timed. Configs whose full CPU
+    step takes tens of minutes (3: ~40 min of np.add.at; 4, 5: > 1 h) time a
+    bounded sample instead, extrapolated linearly, and say so."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
+    from oracle import pipeline as OP
     from paper_1907_06470_b200.workloads import CONFIGS
 
     w = CONFIGS[args.config]
-    threads = os.cpu_count() or 1
-    # calibration (counts as warm-up): fixes the sample size and the
-    # size-independent part a0 of the linear time model
-    base = cpu_baseline(w, args.cpu_budget_s, threads)
-    size, a0 = base["size"], base["a0"]
-    long_dim = w.m if (w.m >= w.n or w.density == "sparse") else w.n
-    for _ in range(max(args.warmup - 1, 0)):
-        _time_port(w, size, threads)
-    full = []
-    for _ in range(args.steps):
-        t = _time_port(w, size, threads)
-        full.append(a0 + (t - a0) * (long_dim / size))
-    dt = float(np.mean(full))
+    cores = os.cpu_count() or 1
     units = w.m * w.n if w.density == "dense" else w.m * 20
-    value = units / dt
     line = {
-        "impl": "reference", "metric": "rank-k rSVD matrix-elements/s", "value": value,
-        "unit": "elements/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64" if w.precision == "double" else "f32",
-        "data": "synthetic (seeded config construction)",
-        "config": {"workload": w.name, "sample": size,
-                   "step": "one bounded sample run, extrapolated linearly to full size"},
-        "cpu_baseline": {"value": value, "unit": "elements/s", "cores": threads, "kind": "port",
-                         "sample": base["sample"]},
+        "impl": "reference", "metric": "rank-k rSVD matrix-elements/s", "unit": "elements/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64" if w.precision == "double" else "f32",
+    }
+    if w.cfg in (1, 2):
+        a, how = _reference_input(w)
+        modes = _ref_thread_modes(cores)
+        warm = {}
+        for name, (threads, limit) in modes.items():
+            with limit():
+                t0 = time.perf_counter()
+                OP.randomized_svd(a, w.k, w.p, w.q, w.cfg, w.precision, threads=threads)
+                warm[name] = time.perf_counter() - t0
+        best = min(warm, key=warm.get)
+        threads, limit = modes[best]
+        times = []
+        with limit():
+            for _ in range(max(args.warmup - len(modes), 0)):
+                OP.randomized_svd(a, w.k, w.p, w.q, w.cfg, w.precision, threads=threads)
+            for _ in range(args.steps):
+                t0 = time.perf_counter()
+                OP.randomized_svd(a, w.k, w.p, w.q, w.cfg, w.precision, threads=threads)
+                times.append(time.perf_counter() - t0)
+        dt = float(np.mean(times))
+        sample = (f"full {w.m}x{w.n} {w.precision} A ({how}) every step, k={w.k} p={w.p} "
+                  f"q={w.q}; oracle port of the shipped xsvd.randomized_svd (256-cell "
+                  f"block_multiply, Householder thin_qr, Golub-Kahan svd_small); thread modes "
+                  f"timed in warm-up: " + ", ".join(f"{k} {v:.2f} s" for k, v in warm.items())
+                  + f"; timed mode: {best}")
+        config = {"workload": w.name, "m": w.m, "n": w.n, "k": w.k, "p": w.p, "q": w.q,
+                  "l": w.l, "omega": f"gaussian_band(seed={w.cfg})",
+                  "thread_mode": best, "threads": threads if best == "cells" else 1,
+                  "blas_threads": 1 if best == "cells" else cores,
+                  "step_s": [round(t, 3) for t in times]}
+    else:
+        threads = cores
+        base = cpu_baseline(w, args.cpu_budget_s, threads)
+        size, a0 = base["size"], base["a0"]
+        long_dim = w.m if (w.m >= w.n or w.density == "sparse") else w.n
+        for _ in range(max(args.warmup - 1, 0)):
+            _time_port(w, size, threads)
+        full = []
+        for _ in range(args.steps):
+            t = _time_port(w, size, threads)
+            full.append(a0 + (t - a0) * (long_dim / size))
+        dt = float(np.mean(full))
+        sample = base["sample"]
+        config = {"workload": w.name, "sample": size,
+                  "step": "one bounded sample run, extrapolated linearly to full size (a full "
+                          "CPU step of this config takes tens of minutes)"}
+    value = units / dt
+    line.update({
+        "value": value, "ms_per_step": dt * 1e3,
+        "data": "synthetic (seeded config construction)", "config": config,
+        "cpu_baseline": {"value": value, "unit": "elements/s", "cores": cores, "kind": "port",
+                         "sample": sample},
         "e2e": {"value": value, "unit": "elements/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
-    }
+    })
     print(json.dumps(line), flush=True)
     return 0
 
 
 # -- device workloads -----------------------------------------------------------------
 
-def gemm_roofline(prof, esz, dmma_peak, dfma_peak):
+def gemm_roofline(prof, esz, dmma_peak, dfma_peak, i8_peak=None):
     """The GEMM over A. achieved = tensor-pipe work per launch / event-timed
     launch duration, against the peak of the pipe the kernel runs on; the
     useful (algorithmic, 2 m n l) rate is reported beside it."""
@@ -263,40 +355,39 @@ def gemm_roofline(prof, esz, dmma_peak, dfma_peak):
                                 "products per useful flop)" if bf16 else
                                 "nominal 2250 bf16 TF/s / 2 / 3 (no MEASURED_PEAKS.json)"),
                 "hbm_gbs_achieved": hbm}
-    if kind == "ozaki_f32_i8":
-        # float32 A on the int8 tensor pipe (ozgemm.cu ozf_kernel): A's tiles
-        # sliced into 3 digits inside the GEMM, 6 exact int8 slice products
-        # per useful multiply-add; int8 dense rate = 2x the bf16 rate.
-        peak = 2 * bf16 if bf16 else 4500.0
-        ops = prof["pipe_ops"] / n / per_s / 1e12
-        tf32_3 = bf16 / 6 if bf16 else 2250.0 / 6
-        return {"bound": "tensor", "achieved": ops, "peak": peak, "unit": "TOP/s (int8)",
-                "frac": ops / peak,
-                "kernel": "ozf_kernel (tcgen05.mma kind::i8; float32 A sliced into 3 digits by "
-                          "converter warps straight into TMEM, 6 slice products, f64 "
-                          "recombination; NN/TN over A) + the per-product slicing of X",
-                "peak_source": ("2 x MEASURED_PEAKS.json bf16_tflops (int8 dense rate = 2x bf16)"
-                                if bf16 else "nominal 4500 int8 TOP/s (no MEASURED_PEAKS.json)"),
-                "fp32_equivalent_tflops": useful,
-                "fp32_equivalent_vs_tf32x3_peak": useful / tf32_3,
-                "hbm_gbs_achieved": hbm}
-    if kind == "ozaki_i8":
-        # FP64 emulated on the int8 tensor pipe (ozgemm.cu): S(S+1)/2 exact
-        # int8 slice products per useful multiply-add. kind::i8 dense rate =
-        # 2x the bf16 rate on B200 (nominal 4.5 vs 2.25 PFLOP/s).
-        peak = 2 * bf16 if bf16 else 4500.0
-        ops = prof["pipe_ops"] / n / per_s / 1e12
-        return {"bound": "tensor", "achieved": ops, "peak": peak, "unit": "TOP/s (int8)",
-                "frac": ops / peak,
-                "kernel": "oz_gemm_kernel (tcgen05.mma kind::i8, Ozaki int8 digit slices of f64 "
-                          "A and X, exact int32 products, f64 recombination; NN/TN over A) + "
-                          "the per-product slicing of X",
-                "peak_source": ("2 x MEASURED_PEAKS.json bf16_tflops (int8 dense rate = 2x bf16)"
-                                if bf16 else "nominal 4500 int8 TOP/s (no MEASURED_PEAKS.json)"),
-                "fp64_equivalent_tflops": useful,
-                "fp64_equivalent_vs_dmma_peak": useful / dmma_peak if dmma_peak else None,
-                "dmma_peak_tflops": dmma_peak,
-                "hbm_gbs_achieved": hbm}
+    if kind in ("ozaki_f32_i8", "ozaki_i8"):
+        # The int8 tensor pipe (tcgen05.mma kind::i8). achieved = the UNPADDED
+        # int8 slice products per launch (pairs x 2 m n l: 21 pairs for the
+        # 6-slice f64 scheme, 6 for the 3-digit f32 scheme) / the launch's
+        # event-timed duration; the padded count the pipe actually issues is
+        # reported beside it. peak = the measured kind::i8 rate of this GPU
+        # (xb_tc_peaks microbenchmark), 2 x MEASURED_PEAKS bf16 beside it.
+        pairs = 6.0 if kind == "ozaki_f32_i8" else 21.0
+        ops = pairs * prof["flops"] / n / per_s / 1e12
+        issued = prof["pipe_ops"] / n / per_s / 1e12
+        peak = i8_peak if i8_peak else (2 * bf16 if bf16 else 4500.0)
+        src = ("measured: tcgen05.mma kind::i8 saturating microbenchmark on this GPU "
+               "(peak.cu, xb_tc_peaks)" if i8_peak else
+               "2 x MEASURED_PEAKS.json bf16_tflops" if bf16 else "nominal 4500 int8 TOP/s")
+        r = {"bound": "tensor", "achieved": ops, "peak": peak, "unit": "TOP/s (int8)",
+             "frac": ops / peak, "peak_source": src,
+             "peak_2x_measured_bf16": 2 * bf16 if bf16 else None,
+             "issued_tops_incl_padding": issued, "hbm_gbs_achieved": hbm}
+        if kind == "ozaki_f32_i8":
+            tf32_3 = bf16 / 6 if bf16 else 2250.0 / 6
+            r.update({"kernel": "ozf_kernel (tcgen05.mma kind::i8; float32 A sliced into 3 "
+                                "digits by converter warps straight into TMEM, 6 slice products, "
+                                "f64 recombination; NN/TN over A) + the per-product slicing of X",
+                      "fp32_equivalent_tflops": useful,
+                      "fp32_equivalent_vs_tf32x3_peak": useful / tf32_3})
+        else:
+            r.update({"kernel": "oz_gemm_kernel (tcgen05.mma kind::i8, Ozaki int8 digit slices "
+                                "of f64 A and X, exact int32 products, f64 recombination; NN/TN "
+                                "over A) + the per-product slicing of X",
+                      "fp64_equivalent_tflops": useful,
+                      "fp64_equivalent_vs_dmma_peak": useful / dmma_peak if dmma_peak else None,
+                      "dmma_peak_tflops": dmma_peak})
+        return r
     return {"bound": "tensor", "achieved": useful, "peak": dmma_peak, "unit": "TFLOP/s",
             "frac": useful / dmma_peak if dmma_peak else None,
             "kernel": "dgemm_kernel (FP64 DMMA m8n8k4, NN/TN over A"
@@ -348,8 +439,8 @@ class DenseCase:
         w = self.w
         return w.m * w.n * self.esz, (w.m + w.n) * w.k * self.esz + w.k * 8
 
-    def roofline(self, prof, dmma_peak, dfma_peak, hbm_peak):
-        return gemm_roofline(prof, self.esz, dmma_peak, dfma_peak)
+    def roofline(self, prof, dmma_peak, dfma_peak, hbm_peak, i8_peak=None):
+        return gemm_roofline(prof, self.esz, dmma_peak, dfma_peak, i8_peak)
 
 
 class ShardedDenseCase(DenseCase):
@@ -440,7 +531,7 @@ class StreamedCase:
         w = self.w
         return (w.q + 1) * self.m * w.n * 4, (self.m + w.n) * w.k * 4 + w.k * 8
 
-    def roofline(self, prof, dmma_peak, dfma_peak, hbm_peak):
+    def roofline(self, prof, dmma_peak, dfma_peak, hbm_peak, i8_peak=None):
         import torch
 
         # measured pinned host->device link (the bound of the streamed passes)
@@ -502,7 +593,7 @@ class SparseCase:
         w = self.w
         return self.nnz * 24, (w.m + w.n) * w.k * 8 + w.k * 8
 
-    def roofline(self, prof, dmma_peak, dfma_peak, hbm_peak):
+    def roofline(self, prof, dmma_peak, dfma_peak, hbm_peak, i8_peak=None):
         per_s = prof["seconds"] / max(prof["launches"], 1)
         achieved = prof["bytes"] / max(prof["launches"], 1) / per_s / 1e9
         return {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
@@ -526,6 +617,7 @@ def run_ours(args):
     device = torch.device("cuda", local)
     w = CONFIGS[args.config]
     ctx = _lib.load(local)
+    knobs = knob_guard(ctx)
     if args.config == 4:
         if world > 1:
             raise SystemExit("config 4 multi-GPU: rows fit in HBM at >= 2 GPUs; use the sharded "
@@ -585,8 +677,11 @@ def run_ours(args):
     value = case.units / (ms * 1e-3)
 
     dmma_peak, dfma_peak = ctx.fp64_peaks()
+    i8_peak, bf16_meas = ctx.tc_peaks()
     hbm_peak = measured_peaks().get("hbm_gbs", 6650.0)
-    roofline = case.roofline(prof, dmma_peak, dfma_peak, hbm_peak)
+    roofline = case.roofline(prof, dmma_peak, dfma_peak, hbm_peak, i8_peak)
+    roofline["tc_microbench"] = {"i8_tops": i8_peak, "bf16_tflops": bf16_meas,
+                                 "dmma_tflops": dmma_peak, "dfma_tflops": dfma_peak}
     roofline["launches_per_step"] = prof["launches"] / args.steps
     roofline["share_of_step"] = prof["seconds"] / (ms * 1e-3 * args.steps)
     traffic = None
@@ -641,6 +736,7 @@ def run_ours(args):
                    "parallelism": f"{'cols' if world > 1 and w.n > w.m else 'rows'}{world}"},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
         "clocks": dict(clocks.summary(), note=clock_note),
+        "knobs": knobs,
         "step_ms": [round(x, 3) for x in step_ms],
         "stage_ms": {nm: 1e3 * t / args.steps for nm, t in zip(STAGE_NAMES, stage_tot)},
     }

@@ -38,6 +38,8 @@ extern "C" {
 #endif
 
 #define XB_ABI_VERSION 1
+/* xb_build_flags() bits */
+#define XB_BUILD_EXPERIMENTS 1 /* experiment build: XB_* tuning/debug knobs are read */
 
 enum xb_status {
   XB_OK = 0,
@@ -62,6 +64,8 @@ enum xb_dtype { XB_F32 = 1, XB_F64 = 2 };
 typedef struct xb_ctx xb_ctx;
 
 int xb_abi_version(void);
+/* XB_BUILD_* bits of this build (0 = release: no environment knobs read). */
+int xb_build_flags(void);
 const char* xb_last_error(void);
 
 /* Context: device, compute + copy streams, cached workspaces. */
@@ -92,6 +96,11 @@ int xb_profile_read_ext(xb_ctx* ctx, double* out6);
 /* Saturating FP64 microbenchmarks on the context's device: TFLOP/s of the
  * DMMA (mma.sync f64) and DFMA pipes — the f64 roofline denominator. */
 int xb_fp64_peaks(xb_ctx* ctx, double* dmma_tflops, double* dfma_tflops);
+/* Saturating tcgen05 microbenchmarks (one CTA per SM issuing back-to-back
+ * M=128 N=256 MMAs from shared memory): dense int8 TOP/s (kind::i8, the
+ * pipe the f64/f32 int8-slice GEMMs run on) and bf16 TFLOP/s (kind::f16) —
+ * the measured roofline denominator of the int8-slice GEMMs. */
+int xb_tc_peaks(xb_ctx* ctx, double* i8_tops, double* bf16_tflops);
 
 /*
  * Full factorization — replaces randomized_svd (pipeline.py:442-625) with

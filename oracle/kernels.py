@@ -117,7 +117,8 @@ def sparse_dense_multiply(rows, cols, vals, shape, y, cdt, out_dtype) -> np.ndar
 
 def block_multiply_fast(x, y, cdt, out_dtype) -> np.ndarray:
     """One-shot BLAS product in the compute dtype (not cell-ordered)."""
-    return (np.asarray(x).astype(cdt) @ np.asarray(y).astype(cdt)).astype(out_dtype)
+    return (np.asarray(x).astype(cdt, copy=False) @ np.asarray(y).astype(cdt, copy=False)).astype(
+        out_dtype, copy=False)
 
 
 # -- thin QR ----------------------------------------------------------------

@@ -31,6 +31,7 @@ _i64, _u64, _int, _vp, _dp = C.c_int64, C.c_uint64, C.c_int, C.c_void_p, C.POINT
 _i32p, _intp = C.POINTER(C.c_int32), C.POINTER(C.c_int)
 SIGNATURES = [
     ("xb_abi_version", _int, []),
+    ("xb_build_flags", _int, []),
     ("xb_last_error", C.c_char_p, []),
     ("xb_create", _int, [_int, C.POINTER(_vp)]),
     ("xb_destroy", _int, [_vp]),
@@ -40,6 +41,7 @@ SIGNATURES = [
     ("xb_profile_read", _int, [_vp, _vp]),
     ("xb_profile_read_ext", _int, [_vp, _vp]),
     ("xb_fp64_peaks", _int, [_vp, _dp, _dp]),
+    ("xb_tc_peaks", _int, [_vp, _dp, _dp]),
     ("xb_set_power_auto", _int, [_vp, _int, C.c_double]),
     ("xb_last_power", _int, [_vp, _intp, _vp, _int, _intp]),
     ("xb_set_gram_path", _int, [_vp, _int]),
@@ -186,6 +188,12 @@ class Context:
     def fp64_peaks(self):
         a, b = C.c_double(), C.c_double()
         _check(self.lib.xb_fp64_peaks(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    def tc_peaks(self):
+        """Measured dense tcgen05 rates: (int8 TOP/s, bf16 TFLOP/s)."""
+        a, b = C.c_double(), C.c_double()
+        _check(self.lib.xb_tc_peaks(self.h, C.byref(a), C.byref(b)))
         return a.value, b.value
 
     # -- power selection ------------------------------------------------------

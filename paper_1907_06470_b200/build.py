@@ -27,6 +27,10 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-I" + INCLUDE,
                 "-I" + CSRC, "--expt-relaxed-constexpr"]
+# Experiment build (tools/ probes): XB_* tuning and timing-only debug knobs are
+# read from the environment. The release library (default) ignores them.
+if os.environ.get("XB_BUILD_EXPERIMENTS") == "1":
+    FLAGS = FLAGS + ["-DXB_EXPERIMENTS"]
 
 
 def sources():

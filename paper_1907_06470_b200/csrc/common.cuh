@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -70,6 +71,28 @@ inline void check_launch(const char* what) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess)
     throw Error(XB_ECUDA, std::string("launch ") + what + ": " + cudaGetErrorString(e));
+}
+
+// Experiment knobs (tile shapes, thresholds, timing-only debug modes used by
+// tools/): read from the environment ONLY in an experiment build
+// (XB_BUILD_EXPERIMENTS=1 python -m paper_1907_06470_b200.build). The release
+// library ignores every one of them and runs the defaults, so no stray
+// variable can change results or skip work. XB_TRACE (stderr tracing only)
+// is read directly.
+inline const char* knob(const char* name) {
+#ifdef XB_EXPERIMENTS
+  return getenv(name);
+#else
+  (void)name;
+  return nullptr;
+#endif
+}
+inline bool experiments_build() {
+#ifdef XB_EXPERIMENTS
+  return true;
+#else
+  return false;
+#endif
 }
 
 __host__ __device__ inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
@@ -248,6 +271,8 @@ size_t jacobi_work_doubles(int l);
 
 // FP64 pipe peaks (TFLOP/s) from saturating microbenchmarks (peak.cu).
 void measure_fp64_peaks(cudaStream_t st, double* dmma_tflops, double* dfma_tflops);
+// tcgen05 dense tensor-pipe peaks: int8 TOP/s (kind::i8), bf16 TFLOP/s (kind::f16).
+void measure_tc_peaks(cudaStream_t st, double* i8_tops, double* bf16_tflops);
 
 // Small helpers
 void launch_transpose(const double* in, int64_t rows, int64_t cols, int64_t ldin, double* out,

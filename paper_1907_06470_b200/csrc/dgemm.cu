@@ -343,7 +343,7 @@ Variant pick_variant(const DGemmArgs& g) {
   int v = 0;
   if (bn == 120 && g.K >= 4096 && !g.a_f32) {
     static const int env = [] {
-      const char* e = getenv("XB_DGEMM_VARIANT");
+      const char* e = knob("XB_DGEMM_VARIANT");
       return e ? atoi(e) : -1;
     }();
     v = env >= 0 ? env : 1;

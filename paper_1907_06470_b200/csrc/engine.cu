@@ -362,11 +362,11 @@ void gemm(xb_ctx* c, bool ta, int64_t M, int64_t N, int64_t K, const double* A, 
 // float64 uses max(1e-15, l eps) unless XB_JACOBI_TOL_F64 (experiments).
 static double jacobi_tol(bool f32) {
   static const double t = [] {
-    const char* e = getenv("XB_JACOBI_TOL_F32");
+    const char* e = knob("XB_JACOBI_TOL_F32");
     return e ? atof(e) : 1e-8;
   }();
   static const double t64 = [] {
-    const char* e = getenv("XB_JACOBI_TOL_F64");
+    const char* e = knob("XB_JACOBI_TOL_F64");
     return e ? atof(e) : -1.0;
   }();
   return f32 ? t : t64;
@@ -374,7 +374,7 @@ static double jacobi_tol(bool f32) {
 
 static int oz_qr_slices() {
   static const int s = [] {
-    const char* e = getenv("XB_OZ_QR_SLICES");
+    const char* e = knob("XB_OZ_QR_SLICES");
     return e ? std::max(3, std::min(6, atoi(e))) : 4;
   }();
   return s;
@@ -670,11 +670,11 @@ void spmm_on_a(xb_ctx* c, const Csr& s, const double* X, double* Y, int lp, int 
   // with 64-column panels; 32-column panels (4 passes) 52.6 ms.
   // XB_SPMM_PANEL: -1 off, 0 auto, w forced.
   static const int panel_env = [] {
-    const char* e = getenv("XB_SPMM_PANEL");
+    const char* e = knob("XB_SPMM_PANEL");
     return e ? atoi(e) : 0;
   }();
   static const int blocks_env = [] {
-    const char* e = getenv("XB_SPMM_BLOCKS");
+    const char* e = knob("XB_SPMM_BLOCKS");
     return e ? atoi(e) : 0;
   }();
   int w = 0;
@@ -723,7 +723,7 @@ void spmm_on_a(xb_ctx* c, const Csr& s, const double* X, double* Y, int lp, int 
 // XB_F32_GEMM=tf32 keeps the 3xTF32 tcgen05 kernel.
 bool ozf_enabled() {
   static const bool on = [] {
-    const char* e = getenv("XB_F32_GEMM");
+    const char* e = knob("XB_F32_GEMM");
     return !(e && (strcmp(e, "tf32") == 0 || strcmp(e, "dmma") == 0));
   }();
   return on;
@@ -960,7 +960,7 @@ void rsvd_impl(xb_ctx* c, const AOp& op_in, int64_t m, int64_t n, const void* d_
   Small s = small_bufs(c, l);
   {
     static const bool qr_oz = [] {
-      const char* e = getenv("XB_QR_OZ");
+      const char* e = knob("XB_QR_OZ");
       return !(e && atoi(e) == 0);
     }();
     s.oz = qr_oz && a.f32 && !op.sparse;
@@ -1450,7 +1450,7 @@ bool check_dtype(int dtype) {
 void gemm_any(xb_ctx* c, bool f32, bool ta, int64_t m, int64_t n, int64_t kdim, const void* dA,
               int64_t lda, const void* dB, int64_t ldb, void* dC, int64_t ldc) {
   if (!f32) {
-    static const bool oz_dbg = getenv("XB_GEMM_OZ") != nullptr;
+    static const bool oz_dbg = knob("XB_GEMM_OZ") != nullptr;
     if (oz_dbg && m > 0 && n > 0 && kdim > 0) {
       // diagnostics (tools/oz_check.py): the same product on the int8 slices
       oz_gemm64(c, ta, m, n, kdim, static_cast<const double*>(dA), lda,
@@ -1466,7 +1466,7 @@ void gemm_any(xb_ctx* c, bool f32, bool ta, int64_t m, int64_t n, int64_t kdim, 
   double* B64 = c->dbuf("gB64", (size_t)std::max<int64_t>(1, kdim * np));
   double* C64 = c->dbuf("gC64", (size_t)m * np);
   launch_copy2d_cast<float, double>(static_cast<const float*>(dB), kdim, n, ldb, B64, np, c->st);
-  static const bool ozf_dbg = getenv("XB_GEMM_OZF") != nullptr;
+  static const bool ozf_dbg = knob("XB_GEMM_OZF") != nullptr;
   if (ozf_dbg && m > 0 && n > 0 && kdim > 0) {
     // diagnostics (tools/ozf_check.py): float32 A on the int8 pipe
     const float* A = static_cast<const float*>(dA);
@@ -1500,6 +1500,8 @@ void gemm_any(xb_ctx* c, bool f32, bool ta, int64_t m, int64_t n, int64_t kdim, 
 extern "C" {
 
 int xb_abi_version(void) { return XB_ABI_VERSION; }
+
+int xb_build_flags(void) { return experiments_build() ? XB_BUILD_EXPERIMENTS : 0; }
 
 const char* xb_last_error(void) { return g_last_error.c_str(); }
 
@@ -1602,6 +1604,14 @@ int xb_fp64_peaks(xb_ctx* c, double* dmma_tflops, double* dfma_tflops) {
     XB_REQUIRE(c && dmma_tflops && dfma_tflops, XB_EVALUE, "null argument");
     LaunchScope ls(c);
     measure_fp64_peaks(c->st, dmma_tflops, dfma_tflops);
+  });
+}
+
+int xb_tc_peaks(xb_ctx* c, double* i8_tops, double* bf16_tflops) {
+  return guarded([&] {
+    XB_REQUIRE(c && i8_tops && bf16_tflops, XB_EVALUE, "null argument");
+    LaunchScope ls(c);
+    measure_tc_peaks(c->st, i8_tops, bf16_tflops);
   });
 }
 

@@ -886,7 +886,7 @@ void launch_oz(const int8_t* L, const int8_t* R, int64_t rows_p, int64_t np, con
   // on the tensor pipe: cfg2 product 2.14 ms at 66 % tensor-active staged
   // (2 staged: 1.92 ms) vs 1.90 ms at 84 % unstaged.
   static const bool staged = [] {
-    const char* e = getenv("XB_OZ_TC");
+    const char* e = knob("XB_OZ_TC");
     return e && atoi(e) == S;
   }();
   auto kern = staged ? ozgemm_kernel<S, S> : ozgemm_kernel<S, 0>;
@@ -896,14 +896,14 @@ void launch_oz(const int8_t* L, const int8_t* R, int64_t rows_p, int64_t np, con
              "ozgemm: grid too large");
   dim3 grid((unsigned)(tn * tm), (unsigned)splits);
   static const int dbg = [] {
-    const char* e = getenv("XB_OZ_DBG");
-    const char* g = getenv("XB_OZ_GROUPED");
+    const char* e = knob("XB_OZ_DBG");
+    const char* g = knob("XB_OZ_GROUPED");
     return (e ? atoi(e) : 0) | ((g && atoi(g) == 0) ? 4 : 0);
   }();
   // the n-tiles of an (m-tile, split) share the left slices by multicast
   // (XB_OZ_CLUSTER=0 disables)
   static const bool cluster_on = [] {
-    const char* e = getenv("XB_OZ_CLUSTER");
+    const char* e = knob("XB_OZ_CLUSTER");
     return !(e && atoi(e) == 0);
   }();
   const int cl = (cluster_on && tri == 0 && tn >= 2 && tn <= 4) ? (int)tn : 1;
@@ -1244,7 +1244,7 @@ int pick_fbn(int64_t N) {
   // (measured: forcing 128-column tiles with 2-slice grouped MMAs is slower
   // at cfg5, 77 vs 52 ms NN, so 144 wins whenever it pads less)
   static const int force = [] {
-    const char* e = getenv("XB_OZF_BN");
+    const char* e = knob("XB_OZF_BN");
     return e ? atoi(e) : 0;
   }();
   if (force == 128 || force == 112) return force;
@@ -1269,7 +1269,7 @@ void launch_ozf(const CUtensorMap& ta, const int8_t* R, int64_t np, const int32_
   // lockstep costs ~3 %, so TN stays unclustered. XB_OZF_CLUSTER: 0 never,
   // 1 NN (default), 2 cluster launch without multicast, 3 NN and TN.
   static const int cenv = [] {
-    const char* e = getenv("XB_OZF_CLUSTER");
+    const char* e = knob("XB_OZF_CLUSTER");
     return e ? atoi(e) : 1;
   }();
   const int cmode = (cenv == 3 || (cenv != 0 && !TRANS_A)) ? (cenv == 2 ? 2 : 1) : 0;
@@ -1288,7 +1288,7 @@ void launch_ozf(const CUtensorMap& ta, const int8_t* R, int64_t np, const int32_
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   static const int dbg = [] {
-    const char* e = getenv("XB_OZF_DBG");
+    const char* e = knob("XB_OZF_DBG");
     return e ? atoi(e) : 0;
   }();
   XB_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, R, np, eL, eR, M, N, K, out, ldo, stride, kps, acc,
@@ -1301,7 +1301,7 @@ void launch_ozf(const CUtensorMap& ta, const int8_t* R, int64_t np, const int32_
 
 int oz_slices() {
   static const int s = [] {
-    const char* e = getenv("XB_OZ_SLICES");
+    const char* e = knob("XB_OZ_SLICES");
     return e ? std::max(3, std::min(6, atoi(e))) : 6;
   }();
   return s;
@@ -1309,7 +1309,7 @@ int oz_slices() {
 
 bool oz_enabled() {
   static const bool on = [] {
-    const char* e = getenv("XB_F64_GEMM");
+    const char* e = knob("XB_F64_GEMM");
     return !(e && strcmp(e, "dmma") == 0);
   }();
   return on;
@@ -1349,7 +1349,7 @@ void oz_both_exp_t(const T* X, int64_t rows, int64_t cols, int64_t ldx, int32_t*
   double2* rpart = static_cast<double2*>(scratch);
   double2* cpart = rpart + rows * nct;
   static const bool generic = [] {
-    const char* e = getenv("XB_RC_GENERIC");
+    const char* e = knob("XB_RC_GENERIC");
     return e && atoi(e) != 0;
   }();
   if (!generic && (sizeof(T) == 8 || (ldx % 4 == 0 && (reinterpret_cast<uintptr_t>(X) % 16) == 0)))

@@ -875,7 +875,7 @@ void launch_chol_inv(const double* G, int64_t ldg, int l, double tau, double* R,
   const size_t bytes = (size_t)l * (l | 1) * sizeof(double);
   // XB_CHOL=coop forces the cooperative version (tests), =single the 1-CTA one
   static const int mode = [] {
-    const char* e = getenv("XB_CHOL");
+    const char* e = knob("XB_CHOL");
     return e ? (strcmp(e, "coop") == 0 ? 1 : (strcmp(e, "single") == 0 ? 2 : 0)) : 0;
   }();
   const int use_smem = bytes + 26 * 1024 <= max_dyn_smem();
@@ -919,7 +919,7 @@ void launch_jacobi_svd(const double* R, int64_t ldr, int l, int k, double* Ub, i
   // one CTA while M's columns fit in shared memory, else (or on request,
   // XB_JACOBI=coop) the cooperative grid version
   static const int mode = [] {
-    const char* e = getenv("XB_JACOBI");
+    const char* e = knob("XB_JACOBI");
     return e ? (strcmp(e, "coop") == 0 ? 1
                 : strcmp(e, "single") == 0 ? 2
                 : strcmp(e, "pairs") == 0 ? 3
@@ -959,7 +959,7 @@ void launch_jacobi_svd(const double* R, int64_t ldr, int l, int k, double* Ub, i
       // 28.9 ms at bs 4, 33 ms at 8, 68 ms at 16; l = 120 3.3 ms), halved until
       // the 2 bs columns of a block pair fit in shared memory
       static const int bs0 = [] {
-        const char* e = getenv("XB_JACOBI_BS");
+        const char* e = knob("XB_JACOBI_BS");
         return e ? std::max(2, std::min(16, atoi(e))) : 4;
       }();
       int bs = bs0;

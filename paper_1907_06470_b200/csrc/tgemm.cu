@@ -426,12 +426,12 @@ void launch_t(const CUtensorMap& ta, const CUtensorMap& bh, const CUtensorMap& b
   const int acc_here = (splits == 1 && g.accumulate) ? 1 : 0;
   // k-tiles per TMEM accumulation group (XB_TG_DRAIN overrides for sweeps)
   static const int drain = [] {
-    const char* e = getenv("XB_TG_DRAIN");
+    const char* e = knob("XB_TG_DRAIN");
     return e ? std::max(1, atoi(e)) : 2;
   }();
   // m-tiles per raster group (XB_TG_GROUP overrides for sweeps)
   static const int group = [] {
-    const char* e = getenv("XB_TG_GROUP");
+    const char* e = knob("XB_TG_GROUP");
     return e ? std::max(1, atoi(e)) : 8;
   }();
   const int64_t total = ntiles * mtiles * splits;
@@ -443,7 +443,7 @@ void launch_t(const CUtensorMap& ta, const CUtensorMap& bh, const CUtensorMap& b
   // lockstep of a cluster measured 5-10 % slower. XB_TG_CLUSTER: 0 = never,
   // 2 = also NN.
   static const int cluster_mode = [] {
-    const char* e = getenv("XB_TG_CLUSTER");
+    const char* e = knob("XB_TG_CLUSTER");
     return e ? atoi(e) : 1;
   }();
   const bool want = cluster_mode == 2 || (cluster_mode == 1 && TRANS_A);
@@ -473,7 +473,7 @@ bool tgemm_supported(const DGemmArgs& g) {
   if ((reinterpret_cast<uintptr_t>(g.A) & 15) != 0 || (g.lda % 4) != 0) return false;
   if (g.M < 1 || g.N < 1 || g.K < 1) return false;
   static const int env = [] {
-    const char* e = getenv("XB_F32_GEMM");
+    const char* e = knob("XB_F32_GEMM");
     return (e && strcmp(e, "dmma") == 0) ? 0 : 1;
   }();
   return env == 1;
@@ -486,7 +486,7 @@ int tgemm_plan_splits(const DGemmArgs& g) {
   // K per split slice (slices are summed in f64); the TMEM groups inside a
   // slice are summed in f32 registers, so the chain only bounds that f32 sum.
   static const int64_t chain = [] {
-    const char* e = getenv("XB_TG_CHAIN");
+    const char* e = knob("XB_TG_CHAIN");
     return e ? std::max<int64_t>(32, atoll(e)) : (int64_t)32768;
   }();
   int s = (int)std::max<int64_t>(1, ceil_div(g.K, chain));
