@@ -173,6 +173,19 @@ int xb_rsvd_dense_dev(xb_ctx* ctx, int dtype, int64_t m, int64_t n, const void* 
  */
 int xb_comm_unique_id(unsigned char* out128);
 int xb_comm_init(xb_ctx* ctx, const unsigned char* id128, int world, int rank);
+/* Host-callback communicator (instead of NCCL): the library copies the
+ * operand to host memory and calls fn(user, op, buf, count) with
+ *   op XB_COLL_ALLREDUCE_SUM: buf holds count doubles, sum them over ranks
+ *                             in place;
+ *   op XB_COLL_ALLGATHER:     buf holds world*count doubles, this rank's
+ *                             slice at rank*count filled; fill the others.
+ * fn returns 0 on success. Used to run the sharded engine with several
+ * processes (any transport, e.g. torch.distributed gloo) — one GPU each or
+ * several sharing one GPU, since ranks only meet on the host. */
+#define XB_COLL_ALLREDUCE_SUM 0
+#define XB_COLL_ALLGATHER 1
+typedef int (*xb_host_collective_fn)(void* user, int op, double* buf, int64_t count);
+int xb_comm_init_host(xb_ctx* ctx, int world, int rank, xb_host_collective_fn fn, void* user);
 int xb_rsvd_dense_sharded_dev(xb_ctx* ctx, int dtype, int64_t m_global, int64_t n,
                               int64_t m_local, const void* dA, int64_t lda, uint64_t seed, int k,
                               int p, int q, void* dU, int64_t ldu, double* d_s, void* dV,
@@ -269,6 +282,13 @@ int xb_thin_qr(xb_ctx* ctx, int dtype, int64_t m, int64_t r, const void* Y, int6
 /* Small SVD — replaces svd_small (kernels.py:542-562): B (r x n, r <= n,
  * f64) = U diag(s) V^T, s non-increasing, each U column's largest-|entry|
  * positive (earliest row on ties). U r x r, s r, V n x r. */
+/* TSQR (tsqr.cu) of a device Y (m x r, f64, row-major), always run (the
+ * factorisations use it as the CholQR fallback): Q (m x r), R (r x r upper,
+ * diag >= 0), deficient columns |R_jj| <= eps ||R||_F (kernels.py:327-331);
+ * *seconds = the device time of the two tree passes (may be null). */
+int xb_tsqr_dev(xb_ctx* ctx, int64_t m, int64_t r, const double* dY, int64_t ldy, double* dQ,
+                int64_t ldq, double* dR, int64_t ldr, int32_t* deficient, int* ndeficient,
+                double* seconds);
 int xb_svd_small(xb_ctx* ctx, int64_t r, int64_t n, const double* B, int64_t ldb,
                  double* U, double* s, double* V);
 

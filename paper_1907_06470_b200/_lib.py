@@ -21,6 +21,8 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "lib
 XB_F32, XB_F64 = 1, 2
 NUM_STAGES = 8
 POWER_AUTO = -1  # XB_POWER_AUTO: q argument selecting power = "auto"
+COLL_ALLREDUCE_SUM, COLL_ALLGATHER = 0, 1  # xb_host_collective_fn ops
+HOST_COLLECTIVE = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_int64)
 
 _lock = threading.Lock()
 _lib = None
@@ -69,6 +71,8 @@ SIGNATURES = [
     ("xb_gemm_dev", _int, [_vp, _int, _int, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64]),
     ("xb_thin_qr", _int, [_vp, _int, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp, _intp]),
     ("xb_svd_small", _int, [_vp, _i64, _i64, _vp, _i64, _vp, _vp, _vp]),
+    ("xb_tsqr_dev", _int, [_vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _intp, _vp]),
+    ("xb_comm_init_host", _int, [_vp, _int, _int, _vp, _vp]),
     ("xb_mm_info", _int, [C.c_char_p, _vp, _vp, _vp, _intp, _intp, _vp]),
     ("xb_mm_read", _int, [C.c_char_p, _int, _i64, _vp, _vp]),
     ("xb_coo_free", None, [_vp]),
@@ -418,6 +422,37 @@ class Context:
         _check(self.lib.xb_thin_qr(self.h, dtype_code(y.dtype), m, r, _ptr(y), r, _ptr(q), r,
                                    _ptr(rr), _ptr(deficient), C.byref(ndef)))
         return q, rr, tuple(int(x) for x in deficient[: ndef.value])
+
+    def tsqr_dev(self, m, r, y_ptr, ldy, q_ptr, ldq, r_ptr, ldr):
+        """TSQR of a device Y (m x r f64, row-major) into device Q, R
+        (xb_tsqr_dev). Returns (deficient columns, device seconds)."""
+        deficient = np.zeros(max(r, 1), dtype=np.int32)
+        ndef = C.c_int(0)
+        sec = np.zeros(1)
+        _check(self.lib.xb_tsqr_dev(self.h, m, r, y_ptr, ldy, q_ptr, ldq, r_ptr, ldr,
+                                    _ptr(deficient), C.byref(ndef), _ptr(sec)))
+        return tuple(int(x) for x in deficient[: ndef.value]), float(sec[0])
+
+    def comm_init_host(self, world: int, rank: int, collective):
+        """Host-callback communicator: collective(op, buf) runs the caller's
+        collective on the float64 numpy array `buf` in place — op 0: sum over
+        ranks; op 1: all-gather (buf = world equal slices, this rank's
+        filled). Raises are reported to the library as a failed collective."""
+
+        def tramp(user, op, buf, count):
+            try:
+                n = int(count) * (world if op == COLL_ALLGATHER else 1)
+                arr = np.ctypeslib.as_array(C.cast(buf, C.POINTER(C.c_double)), shape=(n,))
+                collective(int(op), arr)
+                return 0
+            except BaseException:  # noqa: BLE001 - reported as a status code
+                import traceback
+
+                traceback.print_exc()
+                return 1
+
+        self._host_coll = HOST_COLLECTIVE(tramp)  # keep the trampoline alive
+        _check(self.lib.xb_comm_init_host(self.h, world, rank, self._host_coll, None))
 
     def svd_small(self, b: np.ndarray):
         b = np.ascontiguousarray(b, dtype=np.float64)

@@ -39,10 +39,12 @@ def sources():
 
 def _digest(paths):
     h = hashlib.sha256()
+    # relative names and flags without the checkout's absolute paths: the
+    # stamp must match on the GPU box, where the snapshot lives elsewhere
     for p in sorted(paths):
         with open(p, "rb") as f:
-            h.update(p.encode() + f.read())
-    h.update(" ".join(FLAGS).encode())
+            h.update(os.path.relpath(p, ROOT).encode() + f.read())
+    h.update(" ".join(f for f in FLAGS if not f.startswith("-I")).encode())
     return h.hexdigest()
 
 

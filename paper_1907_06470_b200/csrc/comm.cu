@@ -1,18 +1,26 @@
-// NCCL communicator for the row-sharded factorisation.
+// Communicators for the sharded factorisation.
 //
-// A's rows are split over the ranks (one process per GPU). The only
-// exchanges are sums: the l x l Gram of a row-sharded sketch (CholQR) and the
-// n x l partial products A_g^T Q_g. Both are ncclAllReduce(sum) on the
-// library's compute stream, so they are stream-ordered with the kernels
-// around them; NCCL's reductions give bitwise-identical results on every
-// rank, which keeps the replicated n-side QR and small SVD identical.
+// The exchanges are sums and one gather: the l x l Grams of a row-sharded
+// sketch (CholQR), the n x l partials A_g^T Q_g (row shards) or m x l
+// partials A_g X_g (column shards), and the all-gather of the local TSQR R
+// factors when a sharded sketch needs the Householder fallback.
 //
-// NCCL is dlopen'ed on first use ("libnccl.so.2": torch's bundled copy when
-// torch already loaded it, else the system one), so single-GPU users need no
-// NCCL at all.
+// * NcclComm — production: ncclAllReduce / ncclAllGather on the library's
+//   compute stream (stream-ordered with the kernels around them, no host
+//   round trip; NVLink/NVSwitch, NVLS when NCCL selects it). NCCL's
+//   reductions give bitwise-identical results on every rank, which keeps the
+//   replicated QRs and small SVD identical. libnccl is dlopen'ed on first
+//   use ("libnccl.so.2": torch's bundled copy when torch already loaded it,
+//   else the system one), so single-GPU users need no NCCL at all.
+// * HostComm — the caller's own collectives on host copies
+//   (xb_comm_init_host): the stream is drained, the operand copied to pinned
+//   memory, the callback run, the result copied back. Ranks meet only on the
+//   host, so several processes may share one GPU — how the real sharded
+//   engine is tested at world size 2 on a single-GPU box.
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <cstring>
 #include <mutex>
 
 #include "common.cuh"
@@ -25,6 +33,8 @@ struct NcclApi {
   ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
   ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
                             cudaStream_t) = nullptr;
   ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
   const char* (*getErrorString)(ncclResult_t) = nullptr;
@@ -43,12 +53,14 @@ NcclApi& api() {
     a.getUniqueId = reinterpret_cast<decltype(a.getUniqueId)>(dlsym(a.h, "ncclGetUniqueId"));
     a.commInitRank = reinterpret_cast<decltype(a.commInitRank)>(dlsym(a.h, "ncclCommInitRank"));
     a.allReduce = reinterpret_cast<decltype(a.allReduce)>(dlsym(a.h, "ncclAllReduce"));
+    a.allGather = reinterpret_cast<decltype(a.allGather)>(dlsym(a.h, "ncclAllGather"));
     a.commDestroy = reinterpret_cast<decltype(a.commDestroy)>(dlsym(a.h, "ncclCommDestroy"));
     a.getErrorString =
         reinterpret_cast<decltype(a.getErrorString)>(dlsym(a.h, "ncclGetErrorString"));
   });
-  XB_REQUIRE(a.h && a.getUniqueId && a.commInitRank && a.allReduce && a.commDestroy, XB_ENCCL,
-             "NCCL (libnccl.so.2) could not be loaded");
+  XB_REQUIRE(a.h && a.getUniqueId && a.commInitRank && a.allReduce && a.allGather &&
+                 a.commDestroy,
+             XB_ENCCL, "NCCL (libnccl.so.2) could not be loaded");
   return a;
 }
 
@@ -59,6 +71,62 @@ void check(ncclResult_t r, const char* what) {
   }
 }
 
+struct NcclComm final : Comm {
+  ncclComm_t comm = nullptr;
+  ~NcclComm() override {
+    if (comm) api().commDestroy(comm);
+  }
+  void allreduce_sum(double* buf, size_t count, cudaStream_t st) override {
+    if (count) check(api().allReduce(buf, buf, count, ncclDouble, ncclSum, comm, st), "ncclAllReduce");
+  }
+  void allgather(const double* send, double* recv, size_t count, cudaStream_t st) override {
+    if (count) check(api().allGather(send, recv, count, ncclDouble, comm, st), "ncclAllGather");
+  }
+};
+
+struct HostComm final : Comm {
+  xb_host_collective_fn fn = nullptr;
+  void* user = nullptr;
+  double* stage = nullptr;
+  size_t stage_count = 0;
+  ~HostComm() override {
+    if (stage) cudaFreeHost(stage);
+  }
+  double* staging(size_t count) {
+    if (count > stage_count) {
+      if (stage) XB_CUDA(cudaFreeHost(stage));
+      XB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&stage), count * sizeof(double),
+                            cudaHostAllocDefault));
+      stage_count = count;
+    }
+    return stage;
+  }
+  void call(int op, double* buf, size_t count) {
+    const int rc = fn(user, op, buf, (int64_t)count);
+    XB_REQUIRE(rc == 0, XB_ENCCL, "host collective callback failed (op " + std::to_string(op) +
+                                      ", rc " + std::to_string(rc) + ")");
+  }
+  void allreduce_sum(double* buf, size_t count, cudaStream_t st) override {
+    if (!count) return;
+    double* h = staging(count);
+    XB_CUDA(cudaMemcpyAsync(h, buf, count * sizeof(double), cudaMemcpyDeviceToHost, st));
+    XB_CUDA(cudaStreamSynchronize(st));
+    call(XB_COLL_ALLREDUCE_SUM, h, count);
+    XB_CUDA(cudaMemcpyAsync(buf, h, count * sizeof(double), cudaMemcpyHostToDevice, st));
+    XB_CUDA(cudaStreamSynchronize(st));  // h is reused by the next collective
+  }
+  void allgather(const double* send, double* recv, size_t count, cudaStream_t st) override {
+    if (!count) return;
+    double* h = staging(count * world);
+    XB_CUDA(cudaMemcpyAsync(h + (size_t)rank * count, send, count * sizeof(double),
+                            cudaMemcpyDeviceToHost, st));
+    XB_CUDA(cudaStreamSynchronize(st));
+    call(XB_COLL_ALLGATHER, h, count);
+    XB_CUDA(cudaMemcpyAsync(recv, h, count * world * sizeof(double), cudaMemcpyHostToDevice, st));
+    XB_CUDA(cudaStreamSynchronize(st));
+  }
+};
+
 }  // namespace
 
 void nccl_unique_id(unsigned char out[128]) {
@@ -68,21 +136,29 @@ void nccl_unique_id(unsigned char out[128]) {
   memcpy(out, &id, 128);
 }
 
-void* nccl_comm_init(const unsigned char id_bytes[128], int world, int rank) {
+Comm* nccl_comm_create(const unsigned char id_bytes[128], int world, int rank) {
   ncclUniqueId id;
   memcpy(&id, id_bytes, 128);
-  ncclComm_t comm = nullptr;
-  check(api().commInitRank(&comm, world, id, rank), "ncclCommInitRank");
-  return comm;
+  auto* c = new NcclComm();
+  c->world = world;
+  c->rank = rank;
+  ncclResult_t r = api().commInitRank(&c->comm, world, id, rank);
+  if (r != ncclSuccess) {
+    c->comm = nullptr;
+    delete c;
+    check(r, "ncclCommInitRank");
+  }
+  return c;
 }
 
-void nccl_comm_destroy(void* comm) {
-  if (comm) api().commDestroy(static_cast<ncclComm_t>(comm));
-}
-
-void nccl_allreduce_sum(void* comm, double* buf, size_t count, cudaStream_t st) {
-  check(api().allReduce(buf, buf, count, ncclDouble, ncclSum, static_cast<ncclComm_t>(comm), st),
-        "ncclAllReduce");
+Comm* host_comm_create(int world, int rank, xb_host_collective_fn fn, void* user) {
+  XB_REQUIRE(fn != nullptr, XB_EVALUE, "null collective callback");
+  auto* c = new HostComm();
+  c->world = world;
+  c->rank = rank;
+  c->fn = fn;
+  c->user = user;
+  return c;
 }
 
 }  // namespace xb

@@ -6,6 +6,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <functional>
 #include <stdexcept>
 #include <string>
 
@@ -236,6 +237,21 @@ void launch_chol_inv(const double* G, int64_t ldg, int l, double tau, double* R,
 void launch_householder_fallback(const double* X, int64_t ldx, int64_t rows, int l, int lpad, double* Q,
                                  int64_t ldq, double* R, int64_t ldr, double* work,
                                  const int* flag, cudaStream_t st);
+// TSQR (tsqr.cu): tree Householder QR of X (rows x l) -> Q (rows x lpad, zero
+// padding columns), R (l x l upper, diag >= 0); both passes return at once
+// when *flag == 0 (flag may be null: always run). Q may alias X.
+size_t tsqr_work_doubles(int64_t rows, int l);
+void launch_tsqr(const double* X, int64_t ldx, int64_t rows, int l, int lpad, double* Q,
+                 int64_t ldq, double* R, int64_t ldr, double* work, const int* flag,
+                 cudaStream_t st);
+// Row-sharded TSQR (local tree, all-gather of the local R factors, replicated
+// root, local Q); `allgather(send, recv, count)` enqueues on st.
+size_t tsqr_sharded_work_doubles(int64_t rows_local, int l, int world);
+void launch_tsqr_sharded(const double* X, int64_t ldx, int64_t rows, int l, int lpad, double* Q,
+                         int64_t ldq, double* R, int64_t ldr, double* work, const int* flag,
+                         int world, int rank,
+                         const std::function<void(const double*, double*, size_t)>& allgather,
+                         cudaStream_t st);
 // Deficient-column flags from R (l x l, ldr): |R_jj| <= eps * ||R||_F.
 // M (l x l, ld) := identity when *flag != 0
 void launch_identity_if(double* M, int64_t ld, int l, const int* flag, cudaStream_t st);
@@ -258,11 +274,21 @@ void launch_jacobi_svd(const double* R, int64_t ldr, int l, int k, double* Ub, i
                        double* s, double* Wk, int64_t ldw, double* work, int* status,
                        cudaStream_t st, double tol = -1.0);
 
-// NCCL (dlopen'ed, comm.cu): unique id, communicator, in-place sum.
+// The sharded factorisation's communicator (comm.cu): stream-ordered sums
+// and all-gathers of f64 device buffers. Backends: NCCL (dlopen'ed; the
+// production path over NVLink/NVSwitch) and a host-callback backend (the
+// caller's own collectives on host copies, e.g. torch.distributed/gloo —
+// used to run the real sharded engine with several processes on one GPU).
+struct Comm {
+  int world = 1, rank = 0;
+  virtual ~Comm() {}
+  virtual void allreduce_sum(double* buf, size_t count, cudaStream_t st) = 0;
+  // recv (world * count) <- every rank's send (count), rank order
+  virtual void allgather(const double* send, double* recv, size_t count, cudaStream_t st) = 0;
+};
 void nccl_unique_id(unsigned char out[128]);
-void* nccl_comm_init(const unsigned char id[128], int world, int rank);
-void nccl_comm_destroy(void* comm);
-void nccl_allreduce_sum(void* comm, double* buf, size_t count, cudaStream_t st);
+Comm* nccl_comm_create(const unsigned char id[128], int world, int rank);
+Comm* host_comm_create(int world, int rank, xb_host_collective_fn fn, void* user);
 
 // Opt-in dynamic shared memory per block on the current device.
 size_t max_dyn_smem();

@@ -148,8 +148,9 @@ struct xb_ctx {
   double* dbuf(const std::string& name, size_t count) {
     return static_cast<double*>(buf(name, count * sizeof(double)));
   }
-  // NCCL communicator for the row-sharded factorisation (xb_comm_init)
-  void* comm = nullptr;
+  // communicator for the sharded factorisations (xb_comm_init: NCCL;
+  // xb_comm_init_host: the caller's host collectives)
+  Comm* comm = nullptr;
   int world = 1, rank = 0;
   // pinned staging for device -> pageable-host copies (two ping-pong halves)
   void* stage_host = nullptr;
@@ -472,11 +473,9 @@ struct Small {
   int l, lp;
   double *G, *R1, *R1i, *R2, *R2i, *Rs, *cw;
   int* flag;
-  // row-sharded mode: the communicator that sums Grams, and a sticky flag
-  // for Cholesky breakdowns (no single-device Householder fallback applies
-  // to a sharded sketch)
-  void* comm = nullptr;
-  int* shard_err = nullptr;
+  // sharded sketch (rows over ranks): the communicator that sums its Grams
+  // and gathers the TSQR fallback's R factors
+  Comm* comm = nullptr;
   // float32 configs: the big Gram / X R^-1 products of the single-pass QRs
   // on the int8 pipe (gemm_big)
   bool oz = false;
@@ -509,15 +508,34 @@ void gram(xb_ctx* c, const Small& s, const double* X, int64_t rows, bool sharded
           bool oz = false) {
   // upper-triangle tiles only: the Cholesky kernels read G's upper triangle
   gemm_big(c, oz, true, s.lp, s.lp, rows, X, s.lp, X, s.lp, s.G, s.lp, /*tri=*/1);
-  if (sharded) nccl_allreduce_sum(s.comm, s.G, (size_t)s.lp * s.lp, c->st);
+  if (sharded) s.comm->allreduce_sum(s.G, (size_t)s.lp * s.lp, c->st);
+}
+
+// The fallback when a Cholesky pivot flagged (device-side test, no host
+// round trip): TSQR of X recomputes Q and R (tsqr.cu); for a sharded sketch
+// the local trees meet through an all-gather of their R factors.
+void qr_fallback(xb_ctx* c, const Small& s, const double* X, int64_t rows, double* Q, double* R,
+                 bool sharded) {
+  if (sharded) {
+    double* w = c->dbuf("tsqr_work", tsqr_sharded_work_doubles(rows, s.l, s.comm->world));
+    Comm* comm = s.comm;
+    cudaStream_t st = c->st;
+    launch_tsqr_sharded(X, s.lp, rows, s.l, s.lp, Q, s.lp, R, s.lp, w, s.flag, comm->world,
+                        comm->rank,
+                        [comm, st](const double* a, double* b, size_t n) { comm->allgather(a, b, n, st); },
+                        st);
+  } else {
+    double* w = c->dbuf("tsqr_work", tsqr_work_doubles(rows, s.l));
+    launch_tsqr(X, s.lp, rows, s.l, s.lp, Q, s.lp, R, s.lp, w, s.flag, c->st);
+  }
 }
 
 void cholqr2(xb_ctx* c, const Small& s, const double* X, int64_t rows, double* T, double* Q,
              double* Rout, bool sharded = false) {
   const int l = s.l, lp = s.lp;
   cudaStream_t st = c->st;
-  int* flag = sharded ? s.shard_err : s.flag;
-  if (!sharded) XB_CUDA(cudaMemsetAsync(s.flag, 0, sizeof(int), st));
+  int* flag = s.flag;
+  XB_CUDA(cudaMemsetAsync(s.flag, 0, sizeof(int), st));
   gram(c, s, X, rows, sharded);                                // G1 = X^T X
   launch_chol_inv(s.G, lp, l, 1e-12, s.R1, s.R1i, lp, flag, s.cw, st);
   gemm(c, false, rows, lp, lp, X, lp, s.R1i, lp, T, lp, 2);    // T = X R1^-1 (R1^-1 upper)
@@ -526,10 +544,7 @@ void cholqr2(xb_ctx* c, const Small& s, const double* X, int64_t rows, double* T
   gemm(c, false, rows, lp, lp, T, lp, s.R2i, lp, Q, lp, 2);    // Q = T R2^-1
   double* R = Rout ? Rout : s.Rs;
   if (Rout) gemm(c, false, lp, lp, lp, s.R2, lp, s.R1, lp, Rout, lp);  // R = R2 R1
-  if (sharded) return;  // breakdown is reported through shard_err
-  // Householder fallback runs only when a Cholesky flagged (device-side test)
-  double* hw = c->dbuf("hh_work", (size_t)2 * rows * l);
-  launch_householder_fallback(X, lp, rows, l, lp, Q, lp, R, lp, hw, s.flag, st);
+  qr_fallback(c, s, X, rows, Q, R, sharded);  // runs only when a Cholesky flagged
 }
 
 // Single-pass CholQR for the orthonormalisations INSIDE the power iteration.
@@ -544,17 +559,15 @@ void cholqr1(xb_ctx* c, const Small& s, const double* X, int64_t rows, double* Q
              bool sharded = false, double* Rout = nullptr) {
   const int l = s.l, lp = s.lp;
   cudaStream_t st = c->st;
-  int* flag = sharded ? s.shard_err : s.flag;
-  if (!sharded) XB_CUDA(cudaMemsetAsync(s.flag, 0, sizeof(int), st));
+  int* flag = s.flag;
+  XB_CUDA(cudaMemsetAsync(s.flag, 0, sizeof(int), st));
   gram(c, s, X, rows, sharded, s.oz);                          // G = X^T X
   launch_chol_inv(s.G, lp, l, 1e-8, s.R1, s.R1i, lp, flag, s.cw, st);
   gemm_big(c, s.oz, false, rows, lp, lp, X, lp, s.R1i, lp, Q, lp, 2);  // Q = X R^-1
   if (Rout)
     XB_CUDA(cudaMemcpyAsync(Rout, s.R1, (size_t)lp * lp * sizeof(double),
                             cudaMemcpyDeviceToDevice, st));
-  if (sharded) return;
-  double* hw = c->dbuf("hh_work", (size_t)2 * rows * l);
-  launch_householder_fallback(X, lp, rows, l, lp, Q, lp, Rout ? Rout : s.Rs, lp, hw, s.flag, st);
+  qr_fallback(c, s, X, rows, Q, Rout ? Rout : s.Rs, sharded);
 }
 
 // power = "auto" (pipeline.py:295-372). The reference watches the raw
@@ -644,7 +657,7 @@ struct AOp {
   // row-sharded A: this rank holds m local rows of an
   // m_global x n matrix; products over A^T and Grams of the m-side sketch
   // are summed over `comm`
-  void* comm = nullptr;
+  Comm* comm = nullptr;
   int64_t m_global = 0;
   // column-sharded A: this rank holds columns
   // [col0, col0 + n) of an m x n_global matrix; the products over A (Y = A X)
@@ -883,7 +896,7 @@ void op_nn(xb_ctx* c, const AOp& op, int64_t m, int64_t n, const double* X, doub
   else
     gemm_on_a(c, false, m, lp, n, op.dense, 0, X, lp, Y, lp, l);
   // column-sharded: Y = sum_g A_g X_g, the one m x l exchange per product
-  if (op.comm && op.col_shard) nccl_allreduce_sum(op.comm, Y, (size_t)m * lp, c->st);
+  if (op.comm && op.col_shard) op.comm->allreduce_sum(Y, (size_t)m * lp, c->st);
 }
 
 // Z (n x lp) = A^T Q
@@ -898,7 +911,7 @@ void op_tn(xb_ctx* c, const AOp& op, int64_t m, int64_t n, const double* Q, doub
   else
     gemm_on_a(c, true, n, lp, m, op.dense, 0, Q, lp, Z, lp, l);
   // row-sharded: Z = sum_g A_g^T Q_g, the one n x l exchange per product
-  if (op.comm && !op.col_shard) nccl_allreduce_sum(op.comm, Z, (size_t)n * lp, c->st);
+  if (op.comm && !op.col_shard) op.comm->allreduce_sum(Z, (size_t)n * lp, c->st);
 }
 
 // One factorisation. A (device, f64 or f32 dense, or f64 CSR) is only touched
@@ -955,7 +968,9 @@ void rsvd_impl(xb_ctx* c, const AOp& op_in, int64_t m, int64_t n, const void* d_
     upd(false, n, k, lp, false);
     if (ing.hostA) upd(false, ing.chunk_rows, lp, n, a.f32);
     if (need) c->dbuf("split", need);
-    c->dbuf("hh_work", (size_t)2 * std::max(m, n) * l);
+    // the TSQR fallback's workspace, so no allocation lands mid-stream
+    c->dbuf("tsqr_work", op_in.comm ? tsqr_sharded_work_doubles(std::max(m, n), l, op_in.comm->world)
+                                    : tsqr_work_doubles(std::max(m, n), l));
   }
   Small s = small_bufs(c, l);
   {
@@ -965,11 +980,7 @@ void rsvd_impl(xb_ctx* c, const AOp& op_in, int64_t m, int64_t n, const void* d_
     }();
     s.oz = qr_oz && a.f32 && !op.sparse;
   }
-  if (op.comm) {
-    s.comm = op.comm;
-    s.shard_err = c->ibuf("shard_err", 4);
-    XB_CUDA(cudaMemsetAsync(s.shard_err, 0, sizeof(int), st));
-  }
+  if (op.comm) s.comm = op.comm;
   XB_CUDA(cudaMemsetAsync(Ub, 0, (size_t)lp * lp * sizeof(double), st));
   XB_CUDA(cudaMemsetAsync(Wk, 0, (size_t)lp * kp * sizeof(double), st));
 
@@ -1116,7 +1127,7 @@ void rsvd_impl(xb_ctx* c, const AOp& op_in, int64_t m, int64_t n, const void* d_
     }
     clk.enter(kSvdPrep);
     gemm(c, true, lp, lp, n, Zn, lp, Zn, lp, s.G, lp);  // full G (Jacobi reads all of it)
-    if (csharded) nccl_allreduce_sum(s.comm, s.G, (size_t)lp * lp, st);
+    if (csharded) s.comm->allreduce_sum(s.G, (size_t)lp * lp, st);
     clk.enter(kSvd);
     launch_jacobi_svd(s.G, lp, l, k, Ub, lp, sv, Wk, kp, jw, jstat, st);
     launch_gram_sigma(sv, l, qg > 0 ? 1.0 / (2 * qg + 1) : 1.0, st);
@@ -1124,7 +1135,7 @@ void rsvd_impl(xb_ctx* c, const AOp& op_in, int64_t m, int64_t n, const void* d_
     gemm(c, false, m, k, lp, Qm, lp, Ub, lp, out.U, out.ldu);    // U = Q U_B[:, :k]
     gemm(c, false, n, k, lp, Zn, lp, Ub, lp, out.V, out.ldv);    // V = B^T U_B[:, :k]
     gemm(c, true, k, k, n, out.V, out.ldv, out.V, out.ldv, s.Rs, k);  // column norms^2
-    if (csharded) nccl_allreduce_sum(s.comm, s.Rs, (size_t)k * k, st);
+    if (csharded) s.comm->allreduce_sum(s.Rs, (size_t)k * k, st);
     launch_scale_cols_by_diag(out.V, out.ldv, n, k, s.Rs, k, st);
   } else {
 
@@ -1138,13 +1149,10 @@ void rsvd_impl(xb_ctx* c, const AOp& op_in, int64_t m, int64_t n, const void* d_
   if (fused_lift) {
     XB_CUDA(cudaMemsetAsync(s.flag, 0, sizeof(int), st));
     gram(c, s, Zn, n, csharded, s.oz);
-    launch_chol_inv(s.G, lp, l, 1e-8, Rf, s.R1i, lp, csharded ? s.shard_err : s.flag, s.cw, st);
-    if (!csharded) {
-      // Cholesky breakdown: Householder Q replaces B^T in place, R^-1 := I
-      double* hw = c->dbuf("hh_work", (size_t)2 * n * l);
-      launch_householder_fallback(Zn, lp, n, l, lp, Zn, lp, Rf, lp, hw, s.flag, st);
-      launch_identity_if(s.R1i, lp, l, s.flag, st);
-    }
+    launch_chol_inv(s.G, lp, l, 1e-8, Rf, s.R1i, lp, s.flag, s.cw, st);
+    // Cholesky breakdown: the TSQR Q replaces B^T in place, R^-1 := I
+    qr_fallback(c, s, Zn, n, Zn, Rf, csharded);
+    launch_identity_if(s.R1i, lp, l, s.flag, st);
   } else {
     cholqr2(c, s, Zn, n, Tn, Qn, Rf, csharded);  // B^T = Q_B R_B
   }
@@ -1164,11 +1172,9 @@ void rsvd_impl(xb_ctx* c, const AOp& op_in, int64_t m, int64_t n, const void* d_
   }
   XB_CUDA(cudaMemcpyAsync(out.s, sv, k * sizeof(double), cudaMemcpyDeviceToDevice, st));
 
-  int hstat = 0, hshard = 0;
+  int hstat = 0;
   std::vector<int> hdef(lp + 1, 0);
   XB_CUDA(cudaMemcpyAsync(&hstat, jstat, sizeof(int), cudaMemcpyDeviceToHost, st));
-  if (op.comm)
-    XB_CUDA(cudaMemcpyAsync(&hshard, s.shard_err, sizeof(int), cudaMemcpyDeviceToHost, st));
   XB_CUDA(cudaMemcpyAsync(hdef.data(), defc, (lp + 1) * sizeof(int), cudaMemcpyDeviceToHost, st));
   clk.finish(stage_seconds ? local_stage : nullptr);
   XB_CUDA(cudaStreamSynchronize(st));
@@ -1179,9 +1185,6 @@ void rsvd_impl(xb_ctx* c, const AOp& op_in, int64_t m, int64_t n, const void* d_
   if (deficient)
     for (int i = 0; i < hdef[0] && i < l; ++i) deficient[i] = hdef[1 + i];
   XB_REQUIRE(hstat == 0, XB_ECONV, "Jacobi SVD of the projected factor did not converge in 60 sweeps");
-  XB_REQUIRE(hshard == 0, XB_ECONV,
-             "sharded sketch is numerically rank deficient (Cholesky breakdown); the "
-             "single-device Householder fallback does not apply to a sharded sketch");
 }
 
 struct HostRegistration {
@@ -1324,7 +1327,7 @@ void rsvd_stream(xb_ctx* c, const void* hostA, int64_t host_lda, bool f32, int64
   double* jw = c->dbuf("jw", jacobi_work_doubles(lp));
   int* jstat = c->ibuf("jstat", 4);
   int* defc = c->ibuf("defc", (size_t)lp + 4);
-  c->dbuf("hh_work", (size_t)2 * std::max(m, n) * l);
+  c->dbuf("tsqr_work", tsqr_work_doubles(std::max(m, n), l));
   {
     size_t need = 0;
     auto upd = [&](bool ta, int64_t M, int64_t N, int64_t K, bool af32) {
@@ -1529,7 +1532,7 @@ int xb_destroy(xb_ctx* c) {
     for (auto& kv : c->bufs) cudaFree(kv.second.p);
     for (auto e : c->events) cudaEventDestroy(e);
     if (c->stage_host) cudaFreeHost(c->stage_host);
-    if (c->comm) nccl_comm_destroy(c->comm);
+    delete c->comm;
     for (auto e : c->stage_ev)
       if (e) cudaEventDestroy(e);
     cudaStreamDestroy(c->st);
@@ -1788,8 +1791,22 @@ int xb_comm_init(xb_ctx* c, const unsigned char* id128, int world, int rank) {
     XB_REQUIRE(c && id128, XB_EVALUE, "null argument");
     XB_REQUIRE(world >= 1 && rank >= 0 && rank < world, XB_EVALUE, "bad rank/world");
     LaunchScope ls(c);
-    if (c->comm) nccl_comm_destroy(c->comm);
-    c->comm = nccl_comm_init(id128, world, rank);
+    delete c->comm;
+    c->comm = nullptr;
+    c->comm = nccl_comm_create(id128, world, rank);
+    c->world = world;
+    c->rank = rank;
+  });
+}
+
+int xb_comm_init_host(xb_ctx* c, int world, int rank, xb_host_collective_fn fn, void* user) {
+  return guarded([&] {
+    XB_REQUIRE(c && fn, XB_EVALUE, "null argument");
+    XB_REQUIRE(world >= 1 && rank >= 0 && rank < world, XB_EVALUE, "bad rank/world");
+    LaunchScope ls(c);
+    delete c->comm;
+    c->comm = nullptr;
+    c->comm = host_comm_create(world, rank, fn, user);
     c->world = world;
     c->rank = rank;
   });
@@ -2027,7 +2044,7 @@ int xb_thin_qr(xb_ctx* c, int dtype, int64_t m, int64_t r, const void* Y, int64_
     double* dQ = c->dbuf("qrQ", (size_t)m * lp);
     double* dR = c->dbuf("qrR", (size_t)lp * lp);
     int* defc = c->ibuf("qrdef", (size_t)lp + 4);
-    c->dbuf("hh_work", (size_t)2 * m * l);
+    c->dbuf("tsqr_work", tsqr_work_doubles(m, l));
     XB_CUDA(cudaMemsetAsync(dY, 0, (size_t)m * lp * 8, c->st));
     // the reference factors in f64 whatever the storage precision (kernels.py:308-316)
     if (f32) {
@@ -2060,6 +2077,41 @@ int xb_thin_qr(xb_ctx* c, int dtype, int64_t m, int64_t r, const void* Y, int64_
   });
 }
 
+int xb_tsqr_dev(xb_ctx* c, int64_t m, int64_t r, const double* dY, int64_t ldy, double* dQ,
+                int64_t ldq, double* dR, int64_t ldr, int32_t* deficient, int* ndeficient,
+                double* seconds) {
+  return guarded([&] {
+    XB_REQUIRE(c && dY && dQ && dR, XB_EVALUE, "null argument");
+    LaunchScope ls(c);
+    after_caller_stream(c);
+    XB_REQUIRE(r >= 1 && m >= r, XB_ESHAPE,
+               "TSQR needs rows >= cols >= 1, got " + std::to_string(m) + "x" + std::to_string(r));
+    XB_REQUIRE(ldy >= r && ldq >= r && ldr >= r, XB_EVALUE, "leading dimension too small");
+    const int l = (int)r;
+    double* w = c->dbuf("tsqr_work", tsqr_work_doubles(m, l));
+    int* defc = c->ibuf("qrdef", (size_t)l + 4);
+    cudaEvent_t e0, e1;
+    XB_CUDA(cudaEventCreate(&e0));
+    XB_CUDA(cudaEventCreate(&e1));
+    XB_CUDA(cudaEventRecord(e0, c->st));
+    launch_tsqr(dY, ldy, m, l, l, dQ, ldq, dR, ldr, w, nullptr, c->st);
+    XB_CUDA(cudaEventRecord(e1, c->st));
+    launch_deficient(dR, ldr, l, DBL_EPSILON, defc, defc + 1, c->st);
+    std::vector<int> hdef(l + 1, 0);
+    XB_CUDA(cudaMemcpyAsync(hdef.data(), defc, (l + 1) * sizeof(int), cudaMemcpyDeviceToHost,
+                            c->st));
+    XB_CUDA(cudaStreamSynchronize(c->st));
+    float ms = 0.f;
+    XB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (seconds) *seconds = ms * 1e-3;
+    if (ndeficient) *ndeficient = hdef[0];
+    if (deficient)
+      for (int i = 0; i < hdef[0] && i < l; ++i) deficient[i] = hdef[1 + i];
+  });
+}
+
 int xb_svd_small(xb_ctx* c, int64_t r, int64_t n, const double* B, int64_t ldb, double* U,
                  double* s, double* V) {
   return guarded([&] {
@@ -2081,7 +2133,7 @@ int xb_svd_small(xb_ctx* c, int64_t r, int64_t n, const double* B, int64_t ldb, 
     double* dV = c->dbuf("svV", (size_t)n * l);
     double* jw = c->dbuf("jw", jacobi_work_doubles(lp));
     int* jstat = c->ibuf("jstat", 4);
-    c->dbuf("hh_work", (size_t)2 * n * l);
+    c->dbuf("tsqr_work", tsqr_work_doubles(n, l));
     XB_CUDA(cudaMemcpy2DAsync(dB, n * 8, B, ldb * 8, n * 8, r, cudaMemcpyHostToDevice, c->st));
     XB_CUDA(cudaMemsetAsync(dBt, 0, (size_t)n * lp * 8, c->st));
     XB_CUDA(cudaMemsetAsync(dUb, 0, (size_t)lp * lp * 8, c->st));

@@ -1,0 +1,614 @@
+// TSQR: the tall-skinny Householder QR as a reduction tree — the
+// orthonormaliser that takes over when a CholQR Gram is not numerically
+// positive definite (rank-deficient or very ill-conditioned sketches).
+//
+// The reference's thin_qr (kernels.py:297-351) is itself a flat tree: panels
+// of max(r, 256) rows, each stacked under the running R and re-factored by
+// Householder (_house / _householder_qr / _apply_reflectors, kernels.py:
+// 247-294), then Q rebuilt backwards through the stashed reflectors. Here the
+// same reflector convention (v[0] = 1, R_jj = +||x|| >= 0) runs as a G-ary
+// tree so every SM works:
+//
+//   level 0   the rows split into blocks of <= rmax rows; each CTA factors
+//             its block by blocked Householder (panels of NB columns: the
+//             panel in shared memory, compact-WY T factor, trailing update
+//             A -= V T^T V^T A by warps over 32-column chunks) and writes its
+//             l x l R into the stack of level 1;
+//   level L   groups of G = rmax / l stacked R factors, factored the same way,
+//             until one block is left: its R is the QR's R;
+//   Q         top-down: the root's reflectors applied to [I; 0], each block's
+//             l x l slice of its parent's Q placed on top of zeros and
+//             multiplied by the block's reflectors (right to left, panel by
+//             panel E -= V T V^T E), level 0 writing Q itself.
+//
+// Both passes are ONE cooperative kernel each (grid.sync() between levels),
+// and both return immediately when the Cholesky flag is 0, so the fallback
+// costs two empty launches on the fast path. All sums run in a fixed order:
+// results are bitwise reproducible.
+//
+// Row-sharded sketches: each rank factors its rows to a local
+// l x l R, the ranks' R factors are all-gathered (world*l x l), every rank
+// factors that stack identically (the root), forms its l x l slice of the
+// root's Q and finishes its local Q top-down — the "R-factor gather" of the
+// north star.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cfloat>
+#include <vector>
+
+#include "common.cuh"
+
+namespace xb {
+namespace {
+
+namespace cg = cooperative_groups;
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kMaxLevels = 40;
+constexpr int kRound = 128;  // trailing-update columns per round (4 x 32-column chunks)
+
+struct Level {
+  double* M;        // level matrix: rows x l, row-major, ld = l
+  double* T;        // compact-WY factors: nblk x npan x NB x NB
+  int64_t units;    // rows (level 0) or stacked R factors (levels >= 1)
+  int64_t usize;    // rows per unit: 1 or l
+  int64_t nblk;
+};
+
+struct Plan {
+  int l, nb, npan, levels, rmax;
+  int64_t rows;
+  Level lv[kMaxLevels];
+  double* Qb[2];    // Q of levels >= 1 (ping-pong), ld = l
+};
+
+__device__ __forceinline__ void block_rows(const Level& L, int64_t q, int64_t& s, int64_t& e) {
+  s = q * L.units / L.nblk * L.usize;
+  e = (q + 1) * L.units / L.nblk * L.usize;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <int NB>
+struct Smem {
+  double* Ps;    // NB x rs panel, column-major (explicit V after factoring)
+  double* part;  // NB x 256: trailing-update partial sums / w2
+  double* red;   // kWarps x NB
+  double* tot;   // NB
+  double* yjj;   // NB
+  double* Gm;    // NB x NB
+  double* Ts;    // NB x NB
+  int rs;
+};
+
+template <int NB>
+__device__ Smem<NB> carve(double* base, int rmax) {
+  Smem<NB> s;
+  s.rs = rmax + 1;
+  s.Ps = base;
+  s.part = s.Ps + (size_t)NB * s.rs;
+  s.red = s.part + NB * 256;
+  s.tot = s.red + kWarps * NB;
+  s.yjj = s.tot + NB;
+  s.Gm = s.yjj + NB;
+  s.Ts = s.Gm + NB * NB;
+  return s;
+}
+
+template <int NB>
+constexpr size_t smem_doubles(int rmax) {
+  return (size_t)NB * (rmax + 1) + NB * 256 + kWarps * NB + 2 * NB + 2 * NB * NB;
+}
+
+// Load panel columns [p0, p0 + nbc) of rows [p0, r) of A (row-major, lda)
+// into Ps (column-major); columns nbc..NB-1 are zero.
+template <int NB>
+__device__ void load_panel(const Smem<NB>& S, const double* A, int64_t lda, int64_t p0, int64_t r,
+                           int nbc) {
+  const int64_t rr = r - p0;
+  for (int64_t idx = threadIdx.x; idx < rr * NB; idx += kThreads) {
+    const int64_t i = idx / NB;
+    const int k = (int)(idx - i * NB);
+    S.Ps[(size_t)k * S.rs + i] = k < nbc ? A[(p0 + i) * lda + p0 + k] : 0.0;
+  }
+}
+
+// Householder factorisation of the panel in shared memory (the reference's
+// _house convention: v[0] = 1, beta, R_jj = mu >= 0). Leaves V below the
+// diagonal, R on and above it, and the betas on Ts's diagonal.
+template <int NB>
+__device__ void factor_panel(const Smem<NB>& S, int64_t rr, int nbc) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int jj = 0; jj < nbc; ++jj) {
+    double acc[NB];
+#pragma unroll
+    for (int c = 0; c < NB; ++c) acc[c] = 0.0;
+    const double* xcol = S.Ps + (size_t)jj * S.rs;
+    for (int64_t i = jj + 1 + tid; i < rr; i += kThreads) {
+      const double x = xcol[i];
+      acc[0] = fma(x, x, acc[0]);
+#pragma unroll
+      for (int c = 1; c < NB; ++c)
+        if (c > jj && c < nbc) acc[c] = fma(x, S.Ps[(size_t)c * S.rs + i], acc[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < NB; ++c) acc[c] = warp_sum(acc[c]);
+    if (lane == 0)
+#pragma unroll
+      for (int c = 0; c < NB; ++c) S.red[warp * NB + c] = acc[c];
+    __syncthreads();
+    if (tid < NB) {
+      double t = 0.0;
+      for (int w = 0; w < kWarps; ++w) t += S.red[w * NB + tid];
+      S.tot[tid] = t;
+      S.yjj[tid] = tid < nbc ? S.Ps[(size_t)tid * S.rs + jj] : 0.0;
+    }
+    __syncthreads();
+    const double sigma = S.tot[0], x0 = S.yjj[jj];
+    double v0 = 1.0, beta, mu;
+    if (sigma == 0.0) {
+      beta = (x0 >= 0.0) ? 0.0 : 2.0;
+      mu = (x0 >= 0.0) ? x0 : -x0;
+    } else {
+      mu = sqrt(x0 * x0 + sigma);
+      v0 = (x0 <= 0.0) ? (x0 - mu) : (-sigma / (x0 + mu));
+      beta = 2.0 * v0 * v0 / (sigma + v0 * v0);
+    }
+    const double iv = sigma != 0.0 ? 1.0 / v0 : 0.0;
+    double bw[NB];  // beta * w_c
+#pragma unroll
+    for (int c = 0; c < NB; ++c) bw[c] = (c > jj && c < nbc) ? beta * (S.yjj[c] + S.tot[c] * iv) : 0.0;
+    double* xc = S.Ps + (size_t)jj * S.rs;
+    for (int64_t i = jj + 1 + tid; i < rr; i += kThreads) {
+      const double v = xc[i] * iv;
+      xc[i] = v;
+#pragma unroll
+      for (int c = 1; c < NB; ++c)
+        if (c > jj && c < nbc) S.Ps[(size_t)c * S.rs + i] -= bw[c] * v;
+    }
+#pragma unroll
+    for (int c = 1; c < NB; ++c)
+      if (tid == c && c > jj && c < nbc) S.Ps[(size_t)c * S.rs + jj] = S.yjj[c] - bw[c];
+    if (tid == 0) {
+      xc[jj] = mu;
+      S.Ts[jj * NB + jj] = beta;
+    }
+    __syncthreads();
+  }
+}
+
+// Ps -> explicit V (zeros above the diagonal, ones on it; zero columns past
+// nbc), then T of H_0 ... H_{nbc-1} = I - V T V^T (Ts, upper triangular) from
+// the betas on Ts's diagonal and the Gram of V.
+template <int NB>
+__device__ void build_T(const Smem<NB>& S, int64_t rr, int nbc, bool betas_in_T) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int idx = tid; idx < NB * NB; idx += kThreads) {
+    const int k = idx / NB, i = idx - k * NB;  // column k, row i < NB
+    if (i < rr) {
+      double& p = S.Ps[(size_t)k * S.rs + i];
+      if (k >= nbc || i < k) p = 0.0;
+      else if (i == k) p = 1.0;
+    }
+  }
+  if (!betas_in_T) return;
+  __syncthreads();
+  for (int pr = warp; pr < NB * NB; pr += kWarps) {
+    const int a = pr / NB, b = pr - a * NB;
+    if (a >= b || b >= nbc) continue;
+    double t = 0.0;
+    for (int64_t i = b + lane; i < rr; i += 32) t = fma(S.Ps[(size_t)a * S.rs + i], S.Ps[(size_t)b * S.rs + i], t);
+    t = warp_sum(t);
+    if (lane == 0) S.Gm[a * NB + b] = t;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    for (int idx = lane; idx < NB * NB; idx += 32) {
+      const int i = idx / NB, j = idx - i * NB;
+      if (i != j || j >= nbc) S.Ts[idx] = 0.0;
+    }
+    __syncwarp();
+    for (int j = 1; j < nbc; ++j) {
+      const double bj = S.Ts[j * NB + j];
+      double t = 0.0;
+      if (lane < j) {
+        for (int k = lane; k < j; ++k) t = fma(S.Ts[lane * NB + k], S.Gm[k * NB + j], t);
+      }
+      __syncwarp();
+      if (lane < j) S.Ts[lane * NB + j] = -bj * t;
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+}
+
+// A[p0:r, cbeg:cend] -= V op(T) V^T A[p0:r, cbeg:cend]  (op = T^T when
+// `transT`: the factorisation's Q^T update; op = T: the Q build). V, T in
+// shared memory. Columns in rounds of 128: warps own (32-column chunk, row
+// slice) pairs; partial V^T A sums meet in shared memory in a fixed order.
+template <int NB, bool transT>
+__device__ void apply_wy(const Smem<NB>& S, double* A, int64_t lda, int64_t p0, int64_t r,
+                         int cbeg, int cend) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t rr = r - p0;
+  for (int c0 = cbeg; c0 < cend; c0 += kRound) {
+    const int nc = min(kRound, cend - c0);
+    const int C = (nc + 31) >> 5;
+    const int Sl = kWarps / C;
+    const int chunk = warp % C, slice = warp / C;
+    const int colr = chunk * 32 + lane;
+    const int col = c0 + colr;
+    const bool valid = colr < nc;
+    const bool active = slice < Sl;
+    const int64_t i0 = active ? slice * rr / Sl : 0, i1 = active ? (slice + 1) * rr / Sl : 0;
+    if (active) {
+      double acc[NB];
+#pragma unroll
+      for (int k = 0; k < NB; ++k) acc[k] = 0.0;
+#pragma unroll 4
+      for (int64_t i = i0; i < i1; ++i) {
+        const double a = valid ? A[(p0 + i) * lda + col] : 0.0;
+#pragma unroll
+        for (int k = 0; k < NB; ++k) acc[k] = fma(S.Ps[(size_t)k * S.rs + i], a, acc[k]);
+      }
+#pragma unroll
+      for (int k = 0; k < NB; ++k) S.part[k * 256 + slice * C * 32 + colr] = acc[k];
+    }
+    __syncthreads();
+    if (tid < C * 32 && tid < nc) {
+      double w[NB];
+#pragma unroll
+      for (int k = 0; k < NB; ++k) {
+        double t = 0.0;
+        for (int s = 0; s < Sl; ++s) t += S.part[k * 256 + s * C * 32 + tid];
+        w[k] = t;
+      }
+#pragma unroll
+      for (int k = 0; k < NB; ++k) {
+        double t = 0.0;
+        if (transT) {
+#pragma unroll
+          for (int j = 0; j <= k; ++j) t = fma(S.Ts[j * NB + k], w[j], t);
+        } else {
+#pragma unroll
+          for (int j = k; j < NB; ++j) t = fma(S.Ts[k * NB + j], w[j], t);
+        }
+        S.part[k * 256 + tid] = t;
+      }
+    }
+    __syncthreads();
+    if (active && valid) {
+      double w2[NB];
+#pragma unroll
+      for (int k = 0; k < NB; ++k) w2[k] = S.part[k * 256 + colr];
+#pragma unroll 4
+      for (int64_t i = i0; i < i1; ++i) {
+        double d = 0.0;
+#pragma unroll
+        for (int k = 0; k < NB; ++k) d = fma(S.Ps[(size_t)k * S.rs + i], w2[k], d);
+        A[(p0 + i) * lda + col] -= d;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Blocked Householder QR of block rows [0, r) of A (row-major, ld = l):
+// V below the diagonal, R on and above it; T factors to Tq.
+template <int NB>
+__device__ void factor_block(const Smem<NB>& S, double* A, int64_t r, int l, double* Tq) {
+  const int npan = (l + NB - 1) / NB;
+  for (int pi = 0; pi < npan; ++pi) {
+    const int p0 = pi * NB, nbc = min(NB, l - p0);
+    const int64_t rr = r - p0;
+    load_panel<NB>(S, A, l, p0, r, nbc);
+    __syncthreads();
+    factor_panel<NB>(S, rr, nbc);
+    // panel back to global (V below the diagonal, R on and above it)
+    for (int64_t idx = threadIdx.x; idx < rr * nbc; idx += kThreads) {
+      const int64_t i = idx / nbc;
+      const int k = (int)(idx - i * nbc);
+      A[(p0 + i) * l + p0 + k] = S.Ps[(size_t)k * S.rs + i];
+    }
+    __syncthreads();
+    build_T<NB>(S, rr, nbc, true);
+    for (int idx = threadIdx.x; idx < NB * NB; idx += kThreads)
+      Tq[(size_t)pi * NB * NB + idx] = S.Ts[idx];
+    if (p0 + nbc < l) apply_wy<NB, true>(S, A, l, p0, r, p0 + nbc, l);
+    __syncthreads();
+  }
+}
+
+// E (r x l, ld lde) <- Q_block E: the block's reflectors, last panel first.
+template <int NB>
+__device__ void apply_block_q(const Smem<NB>& S, const double* A, int64_t r, int l,
+                              const double* Tq, double* E, int64_t lde) {
+  const int npan = (l + NB - 1) / NB;
+  for (int pi = npan - 1; pi >= 0; --pi) {
+    const int p0 = pi * NB, nbc = min(NB, l - p0);
+    const int64_t rr = r - p0;
+    load_panel<NB>(S, A, l, p0, r, nbc);
+    for (int idx = threadIdx.x; idx < NB * NB; idx += kThreads)
+      S.Ts[idx] = Tq[(size_t)pi * NB * NB + idx];
+    __syncthreads();
+    build_T<NB>(S, rr, nbc, false);
+    __syncthreads();
+    apply_wy<NB, false>(S, E, lde, p0, r, 0, l);
+  }
+}
+
+template <int NB>
+__global__ void __launch_bounds__(kThreads) tsqr_factor_kernel(Plan P, const double* __restrict__ X,
+                                                             int64_t ldx, double* __restrict__ R,
+                                                             int64_t ldr, const int* flag) {
+  if (flag && *flag == 0) return;
+  extern __shared__ __align__(16) double smem_tsqr[];
+  const Smem<NB> S = carve<NB>(smem_tsqr, P.rmax);
+  cg::grid_group grid = cg::this_grid();
+  const int l = P.l;
+  for (int L = 0; L < P.levels; ++L) {
+    const Level& lv = P.lv[L];
+    for (int64_t q = blockIdx.x; q < lv.nblk; q += gridDim.x) {
+      int64_t s, e;
+      block_rows(lv, q, s, e);
+      const int64_t r = e - s;
+      double* A = lv.M + s * l;
+      if (L == 0) {
+        for (int64_t idx = threadIdx.x; idx < r * l; idx += kThreads) {
+          const int64_t i = idx / l;
+          const int c = (int)(idx - i * l);
+          A[idx] = X[(s + i) * ldx + c];
+        }
+        __syncthreads();
+      }
+      factor_block<NB>(S, A, r, l, lv.T + (size_t)q * P.npan * NB * NB);
+      const bool top = L + 1 == P.levels;
+      double* dst = top ? R : P.lv[L + 1].M + q * l * l;
+      const int64_t ldd = top ? ldr : l;
+      for (int64_t idx = threadIdx.x; idx < (int64_t)l * l; idx += kThreads) {
+        const int64_t i = idx / l;
+        const int c = (int)(idx - i * l);
+        dst[i * ldd + c] = c >= i ? A[i * l + c] : 0.0;
+      }
+      __syncthreads();
+    }
+    if (L + 1 < P.levels) grid.sync();
+  }
+}
+
+// Ein: the top block's l x l input (identity when null); Q: rows x lpad.
+template <int NB>
+__global__ void __launch_bounds__(kThreads) tsqr_q_kernel(Plan P, const double* __restrict__ Ein,
+                                                        int64_t lde, double* __restrict__ Q,
+                                                        int64_t ldq, int lpad, const int* flag) {
+  if (flag && *flag == 0) return;
+  extern __shared__ __align__(16) double smem_tsqr[];
+  const Smem<NB> S = carve<NB>(smem_tsqr, P.rmax);
+  cg::grid_group grid = cg::this_grid();
+  const int l = P.l;
+  for (int L = P.levels - 1; L >= 0; --L) {
+    const Level& lv = P.lv[L];
+    const bool top = L + 1 == P.levels;
+    double* out = L == 0 ? Q : P.Qb[L & 1];
+    const int64_t ldo = L == 0 ? ldq : l;
+    const double* in = top ? Ein : P.Qb[(L + 1) & 1];
+    const int64_t ldi = top ? lde : l;
+    for (int64_t q = blockIdx.x; q < lv.nblk; q += gridDim.x) {
+      int64_t s, e;
+      block_rows(lv, q, s, e);
+      const int64_t r = e - s;
+      double* E = out + s * ldo;
+      const double* Ei = top ? in : in + q * l * ldi;
+      const int wcols = L == 0 ? lpad : l;
+      for (int64_t idx = threadIdx.x; idx < r * wcols; idx += kThreads) {
+        const int64_t i = idx / wcols;
+        const int c = (int)(idx - i * wcols);
+        double v = 0.0;
+        if (i < l && c < l) v = Ei ? Ei[i * ldi + c] : (i == c ? 1.0 : 0.0);
+        E[i * ldo + c] = v;
+      }
+      __syncthreads();
+      apply_block_q<NB>(S, lv.M + s * l, r, l, lv.T + (size_t)q * P.npan * NB * NB, E, ldo);
+      __syncthreads();
+    }
+    if (L > 0) grid.sync();
+  }
+}
+
+// dst (drows x dcols) <- src (rows x cols) with zero fill, when *flag != 0
+__global__ void pad_copy_kernel(const double* __restrict__ src, int64_t lds, int64_t rows,
+                                int cols, double* __restrict__ dst, int64_t ldd, int64_t drows,
+                                int dcols, const int* flag) {
+  if (flag && *flag == 0) return;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < drows * dcols;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx / dcols;
+    const int c = (int)(idx - i * dcols);
+    dst[i * ldd + c] = (i < rows && c < cols) ? src[i * lds + c] : 0.0;
+  }
+}
+
+void launch_pad_copy(const double* src, int64_t lds, int64_t rows, int cols, double* dst,
+                     int64_t ldd, int64_t drows, int dcols, const int* flag, cudaStream_t st) {
+  const int64_t n = drows * dcols;
+  if (n <= 0) return;
+  pad_copy_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n, 256), 1024), 256, 0, st>>>(
+      src, lds, rows, cols, dst, ldd, drows, dcols, flag);
+  check_launch("tsqr_pad_copy");
+}
+
+int pick_nb(int l) {
+  for (int nb : {16, 8, 4, 2}) {
+    const int rmax = std::max(512, 2 * l);
+    size_t need = 0;
+    switch (nb) {
+      case 16: need = smem_doubles<16>(rmax); break;
+      case 8: need = smem_doubles<8>(rmax); break;
+      case 4: need = smem_doubles<4>(rmax); break;
+      default: need = smem_doubles<2>(rmax); break;
+    }
+    if (need * 8 <= max_dyn_smem()) return nb;
+  }
+  return 0;
+}
+
+size_t smem_bytes(int nb, int rmax) {
+  switch (nb) {
+    case 16: return smem_doubles<16>(rmax) * 8;
+    case 8: return smem_doubles<8>(rmax) * 8;
+    case 4: return smem_doubles<4>(rmax) * 8;
+    default: return smem_doubles<2>(rmax) * 8;
+  }
+}
+
+// The tree's shape for `rows` x l and its workspace layout (doubles).
+struct HostPlan {
+  Plan p;
+  size_t doubles = 0;
+};
+
+HostPlan make_plan(int64_t rows, int l, double* work) {
+  HostPlan h;
+  Plan& p = h.p;
+  p.l = l;
+  p.nb = pick_nb(l);
+  XB_REQUIRE(p.nb > 0, XB_EUNSUPPORTED,
+             "TSQR: l = " + std::to_string(l) + " columns exceed the shared-memory panel");
+  XB_REQUIRE(rows >= l, XB_ESHAPE, "TSQR needs rows >= cols");
+  p.npan = (l + p.nb - 1) / p.nb;
+  p.rmax = std::max(512, 2 * l);
+  p.rows = rows;
+  const int64_t G = std::max<int64_t>(2, p.rmax / l);
+  size_t off = 0;
+  auto take = [&](size_t n) {
+    double* q = work ? work + off : nullptr;
+    off += (n + 31) / 32 * 32;
+    return q;
+  };
+  int L = 0;
+  int64_t units = rows, usize = 1;
+  int64_t rows1 = 0;
+  while (true) {
+    XB_REQUIRE(L < kMaxLevels, XB_EUNSUPPORTED, "TSQR: tree too deep");
+    Level& lv = p.lv[L];
+    lv.units = units;
+    lv.usize = usize;
+    lv.nblk = L == 0 ? std::max<int64_t>(1, ceil_div(rows, (int64_t)p.rmax))
+                     : ceil_div(units, G);
+    lv.M = take((size_t)units * usize * l);
+    lv.T = take((size_t)lv.nblk * p.npan * p.nb * p.nb);
+    if (L == 1) rows1 = units * usize;
+    ++L;
+    if (lv.nblk == 1) break;
+    units = lv.nblk;
+    usize = l;
+  }
+  p.levels = L;
+  p.Qb[0] = take((size_t)std::max<int64_t>(rows1, 1) * l);
+  p.Qb[1] = take((size_t)std::max<int64_t>(rows1, 1) * l);
+  h.doubles = off;
+  return h;
+}
+
+template <int NB>
+void launch_pass(bool factor, const Plan& p, const double* X, int64_t ldx, double* R, int64_t ldr,
+                 const double* Ein, int64_t lde, double* Q, int64_t ldq, int lpad, const int* flag,
+                 cudaStream_t st) {
+  const size_t sm = smem_bytes(NB, p.rmax);
+  const void* fn = factor ? reinterpret_cast<const void*>(&tsqr_factor_kernel<NB>)
+                          : reinterpret_cast<const void*>(&tsqr_q_kernel<NB>);
+  static bool attr_set[2] = {false, false};
+  static size_t attr_bytes[2] = {0, 0};
+  if (!attr_set[factor] || attr_bytes[factor] < sm) {
+    XB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    attr_set[factor] = true;
+    attr_bytes[factor] = sm;
+  }
+  int per_sm = 0;
+  XB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, sm));
+  XB_REQUIRE(per_sm > 0, XB_ECUDA, "TSQR kernel cannot be resident");
+  int64_t most = 1;
+  for (int L = 0; L < p.levels; ++L) most = std::max(most, p.lv[L].nblk);
+  const int grid = (int)std::min<int64_t>(most, (int64_t)per_sm * kNumSMs);
+  Plan pc = p;
+  if (factor) {
+    void* args[] = {&pc, &X, &ldx, &R, &ldr, &flag};
+    XB_CUDA(cudaLaunchCooperativeKernel(fn, grid, kThreads, args, sm, st));
+  } else {
+    void* args[] = {&pc, &Ein, &lde, &Q, &ldq, &lpad, &flag};
+    XB_CUDA(cudaLaunchCooperativeKernel(fn, grid, kThreads, args, sm, st));
+  }
+  count_launch();
+}
+
+void run_pass(bool factor, const Plan& p, const double* X, int64_t ldx, double* R, int64_t ldr,
+              const double* Ein, int64_t lde, double* Q, int64_t ldq, int lpad, const int* flag,
+              cudaStream_t st) {
+  switch (p.nb) {
+    case 16: launch_pass<16>(factor, p, X, ldx, R, ldr, Ein, lde, Q, ldq, lpad, flag, st); break;
+    case 8: launch_pass<8>(factor, p, X, ldx, R, ldr, Ein, lde, Q, ldq, lpad, flag, st); break;
+    case 4: launch_pass<4>(factor, p, X, ldx, R, ldr, Ein, lde, Q, ldq, lpad, flag, st); break;
+    default: launch_pass<2>(factor, p, X, ldx, R, ldr, Ein, lde, Q, ldq, lpad, flag, st); break;
+  }
+}
+
+}  // namespace
+
+size_t tsqr_work_doubles(int64_t rows, int l) { return make_plan(rows, l, nullptr).doubles; }
+
+void launch_tsqr(const double* X, int64_t ldx, int64_t rows, int l, int lpad, double* Q,
+                 int64_t ldq, double* R, int64_t ldr, double* work, const int* flag,
+                 cudaStream_t st) {
+  const HostPlan h = make_plan(rows, l, work);
+  run_pass(true, h.p, X, ldx, R, ldr, nullptr, 0, nullptr, 0, 0, flag, st);
+  run_pass(false, h.p, nullptr, 0, nullptr, 0, nullptr, 0, Q, ldq, lpad, flag, st);
+}
+
+size_t tsqr_sharded_work_doubles(int64_t rows_local, int l, int world) {
+  const size_t loc = rows_local >= l ? make_plan(rows_local, l, nullptr).doubles : 0;
+  return loc + make_plan((int64_t)world * l, l, nullptr).doubles +
+         (size_t)(2 * world + 1) * l * l + 64;
+}
+
+// Row-sharded TSQR: local tree -> all-gather of the local R factors -> the
+// replicated root over the world*l x l stack -> local Q from this rank's
+// slice of the root's Q. `allgather(send, recv, count)` is the
+// communicator's stream-ordered all-gather (always called, also when `flag`
+// is 0, so every rank issues the same collectives).
+void launch_tsqr_sharded(const double* X, int64_t ldx, int64_t rows, int l, int lpad, double* Q,
+                         int64_t ldq, double* R, int64_t ldr, double* work, const int* flag,
+                         int world, int rank,
+                         const std::function<void(const double*, double*, size_t)>& allgather,
+                         cudaStream_t st) {
+  // fewer local rows than columns: the local "R" is X itself on top of zero
+  // rows (the stack's QR is unchanged), and the local Q is the first `rows`
+  // rows of this rank's slice of the root's Q
+  const bool tree = rows >= l;
+  HostPlan loc;
+  if (tree) loc = make_plan(rows, l, work);
+  double* w2 = work + loc.doubles;
+  const HostPlan root = make_plan((int64_t)world * l, l, w2);
+  double* Rloc = w2 + root.doubles;
+  double* Rall = Rloc + (size_t)l * l;
+  double* Qall = Rall + (size_t)world * l * l;
+  if (tree)
+    run_pass(true, loc.p, X, ldx, Rloc, l, nullptr, 0, nullptr, 0, 0, flag, st);
+  else
+    launch_pad_copy(X, ldx, rows, l, Rloc, l, l, l, flag, st);
+  allgather(Rloc, Rall, (size_t)l * l);
+  run_pass(true, root.p, Rall, l, R, ldr, nullptr, 0, nullptr, 0, 0, flag, st);
+  run_pass(false, root.p, nullptr, 0, nullptr, 0, nullptr, 0, Qall, l, l, flag, st);
+  if (tree)
+    run_pass(false, loc.p, nullptr, 0, nullptr, 0, Qall + (size_t)rank * l * l, l, Q, ldq, lpad,
+             flag, st);
+  else
+    launch_pad_copy(Qall + (size_t)rank * l * l, l, rows, l, Q, ldq, rows, lpad, flag, st);
+}
+
+}  // namespace xb
