@@ -15,6 +15,7 @@ import numpy as np
 import pytest
 
 from oracle import metrics as M
+from oracle import pipeline as OP
 
 pytestmark = pytest.mark.gpu
 
@@ -67,16 +68,23 @@ def test_sharded_world1_equals_unsharded(world1, dtype):
     assert M.sigma_rel(s.cpu().numpy(), s1) <= tol
 
 
-def test_sharded_rank_deficiency_is_reported(world1):
+def test_sharded_rank_deficient_sketch_uses_tsqr(world1):
+    """rank(A) = 8 < l = 20 on the sharded path: the all-reduced Gram's
+    Cholesky breaks down on every rank and the sharded TSQR (local tree, R
+    all-gather, replicated root) carries the factorisation; identical to the
+    unsharded engine at world 1 and to the oracle's leading sigma."""
     import torch
 
     from paper_1907_06470_b200.distributed import randomized_svd_sharded
-    from paper_1907_06470_b200.errors import ConvergenceError
 
     rng = np.random.default_rng(3)
     a = rng.standard_normal((500, 8)) @ rng.standard_normal((8, 300))  # rank 8 < l = 20
-    with pytest.raises(ConvergenceError):
-        randomized_svd_sharded(world1, torch.from_numpy(a).cuda(), 500, 15, 5, 1, 1)
+    u, s, v = randomized_svd_sharded(world1, torch.from_numpy(a).cuda(), 500, 15, 5, 1, 1)
+    ref = OP.rsvd_reorth(a, 15, 5, 1, 1, "double", fast=True)
+    s = s.cpu().numpy()
+    assert np.max(np.abs(s[:8] - ref.s[:8]) / ref.s[:8]) <= 1e-10
+    assert np.max(np.abs(s[8:])) <= 1e-10 * s[0]
+    assert M.ortho_defect(u.cpu().numpy()) <= 1e-12
 
 
 @pytest.mark.parametrize("dtype", ["float64", "float32"])
