@@ -213,6 +213,16 @@ int xb_rsvd_dense_colsharded_dev(xb_ctx* ctx, int dtype, int64_t m, int64_t n_gl
  * (row, col)-sorted without duplicates, float64 values (Precision.DOUBLE).
  * Host buffers; same outputs as xb_rsvd_dense.
  */
+/* Row-sharded sparse A (config 3's layout): this rank's m_local
+ * rows of the m_global x n matrix as device CSR (rowptr int64[m_local + 1]
+ * relative to the rank's first row, col int32, val f64). Y = A_g X is local,
+ * the n x l partials A_g^T Q_g are summed by the communicator; Omega and V
+ * replicated, U for the local rows. */
+int xb_rsvd_csr_sharded_dev(xb_ctx* ctx, int64_t m_global, int64_t n, int64_t m_local,
+                            int64_t nnz, const int64_t* d_rowptr, const int32_t* d_col,
+                            const double* d_val, uint64_t seed, int k, int p, int q, double* dU,
+                            int64_t ldu, double* d_s, double* dV, int64_t ldv,
+                            int32_t* deficient, int* ndeficient, double* stage_seconds);
 int xb_rsvd_coo(xb_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const int64_t* rows,
                 const int64_t* cols, const double* vals, const double* omega, uint64_t seed,
                 int k, int p, int q, double* U, int64_t ldu, double* s, double* V, int64_t ldv,

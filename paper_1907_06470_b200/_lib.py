@@ -62,6 +62,8 @@ SIGNATURES = [
                                             _intp, _vp]),
     ("xb_rsvd_coo", _int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _u64, _int, _int, _int,
                            _vp, _i64, _vp, _vp, _i64, _vp, _intp, _vp]),
+    ("xb_rsvd_csr_sharded_dev", _int, [_vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _u64, _int,
+                                       _int, _int, _vp, _i64, _vp, _vp, _i64, _vp, _intp, _vp]),
     ("xb_rsvd_csr_dev", _int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _u64, _int, _int, _int,
                                _vp, _i64, _vp, _vp, _i64, _vp, _intp, _vp]),
     ("xb_spmm_coo", _int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _int, _vp, _i64, _vp]),
@@ -359,6 +361,19 @@ class Context:
             self.h, m, n, nnz, C.c_void_p(rowptr_ptr), C.c_void_p(col_ptr), C.c_void_p(val_ptr),
             None, int(seed) & (2**64 - 1), k, p, q, C.c_void_p(u_ptr), k, C.c_void_p(s_ptr),
             C.c_void_p(v_ptr), k, _ptr(deficient), C.byref(ndef), _ptr(stages)))
+        return tuple(int(x) for x in deficient[: ndef.value]), stages
+
+    def rsvd_csr_sharded_dev(self, m_global, n, m_local, nnz, rowptr_ptr, col_ptr, val_ptr, k, p,
+                             q, seed, u_ptr, s_ptr, v_ptr):
+        """Row-sharded CSR factorisation (this rank's rows; xb_rsvd_csr_sharded_dev)."""
+        deficient = np.zeros(max(k + p, 1), dtype=np.int32)
+        ndef = C.c_int(0)
+        stages = np.zeros(NUM_STAGES)
+        _check(self.lib.xb_rsvd_csr_sharded_dev(
+            self.h, m_global, n, m_local, nnz, C.c_void_p(rowptr_ptr), C.c_void_p(col_ptr),
+            C.c_void_p(val_ptr), int(seed) & (2**64 - 1), k, p, q, C.c_void_p(u_ptr), k,
+            C.c_void_p(s_ptr), C.c_void_p(v_ptr), k, _ptr(deficient), C.byref(ndef),
+            _ptr(stages)))
         return tuple(int(x) for x in deficient[: ndef.value]), stages
 
     def spmm(self, rows, cols, vals, shape, x, trans=False):

@@ -1892,6 +1892,29 @@ int xb_rsvd_csr_dev(xb_ctx* c, int64_t m, int64_t n, int64_t nnz, const int64_t*
   });
 }
 
+int xb_rsvd_csr_sharded_dev(xb_ctx* c, int64_t m_global, int64_t n, int64_t m_local,
+                            int64_t nnz, const int64_t* d_rowptr, const int32_t* d_col,
+                            const double* d_val, uint64_t seed, int k, int p, int q, double* dU,
+                            int64_t ldu, double* d_s, double* dV, int64_t ldv,
+                            int32_t* deficient, int* ndeficient, double* stage_seconds) {
+  return guarded([&] {
+    XB_REQUIRE(c, XB_EVALUE, "null context");
+    XB_REQUIRE(c->comm, XB_EVALUE, "xb_comm_init has not been called on this context");
+    LaunchScope ls(c);
+    after_caller_stream(c);
+    XB_REQUIRE(m_local >= 1 && m_local <= m_global, XB_ESHAPE, "bad local row count");
+    XB_REQUIRE(ldu >= k && ldv >= k, XB_EVALUE, "leading dimension too small");
+    // this rank's rows of A as CSR (rowptr relative to its first row); the
+    // A^T partials (n x l) are summed over ranks after every TN product
+    AOp op = sparse_op(c, m_local, n, nnz, d_rowptr, d_col, d_val);
+    op.comm = c->comm;
+    op.m_global = m_global;
+    RsvdOut out{dU, ldu, d_s, dV, ldv};
+    rsvd_impl(c, op, m_local, n, nullptr, k + p, seed, k, p, q, out, deficient, ndeficient,
+              stage_seconds, IngestPlan{});
+  });
+}
+
 int xb_rsvd_coo(xb_ctx* c, int64_t m, int64_t n, int64_t nnz, const int64_t* rows,
                 const int64_t* cols, const double* vals, const double* omega, uint64_t seed,
                 int k, int p, int q, double* U, int64_t ldu, double* s, double* V, int64_t ldv,

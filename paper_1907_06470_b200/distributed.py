@@ -58,6 +58,55 @@ def init_comm(ctx: "_lib.Context", group=None) -> None:
     ctx.comm_init(uid, world, rank)
 
 
+def init_host_comm(ctx: "_lib.Context", group=None) -> None:
+    """Create the library's communicator on top of torch.distributed itself
+    (any backend, e.g. gloo): every exchange is a host all-reduce /
+    all-gather of the operand (xb_comm_init_host). Ranks meet only on the
+    host, so several processes may share one GPU — how the sharded engine is
+    tested on a single-GPU box. Production runs use init_comm (NCCL)."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+
+    def collective(op: int, buf: np.ndarray) -> None:
+        t = torch.from_numpy(buf)
+        if op == _lib.COLL_ALLREDUCE_SUM:
+            dist.all_reduce(t, group=group)
+        else:
+            parts = list(t.chunk(world))
+            mine = parts[rank].clone()
+            dist.all_gather(parts, mine, group=group)
+
+    ctx.comm_init_host(world, rank, collective)
+
+
+def csr_row_shard(rowptr: np.ndarray, col: np.ndarray, val: np.ndarray, r0: int, r1: int):
+    """Rows [r0, r1) of a CSR matrix as a CSR of their own (rowptr rebased)."""
+    a, b = int(rowptr[r0]), int(rowptr[r1])
+    return (np.ascontiguousarray(rowptr[r0:r1 + 1] - a, dtype=np.int64),
+            np.ascontiguousarray(col[a:b], dtype=np.int32), np.ascontiguousarray(val[a:b]))
+
+
+def randomized_svd_csr_sharded(ctx, rowptr, col, val, m_global: int, n: int, k: int, p: int,
+                               q: int, seed: int):
+    """Factorise the row-sharded sparse A: this rank's rows as device CSR
+    (torch tensors: rowptr int64 rebased to the rank's first row, col int32,
+    val float64). Returns (U_local, s, V) as torch tensors."""
+    import torch
+
+    m_local = rowptr.numel() - 1
+    dev = val.device
+    u = torch.empty((m_local, k), dtype=torch.float64, device=dev)
+    v = torch.empty((n, k), dtype=torch.float64, device=dev)
+    s = torch.empty((k,), dtype=torch.float64, device=dev)
+    torch.cuda.synchronize(dev)
+    ctx.rsvd_csr_sharded_dev(m_global, n, m_local, val.numel(), rowptr.data_ptr(), col.data_ptr(),
+                             val.data_ptr(), k, p, q, seed, u.data_ptr(), s.data_ptr(),
+                             v.data_ptr())
+    return u, s, v
+
+
 def randomized_svd_sharded(ctx, a_local, m_global: int, k: int, p: int, q: int, seed: int):
     """Factorise the row-sharded A (this rank's rows as a CUDA torch tensor).
 
