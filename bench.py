@@ -444,20 +444,31 @@ class DenseCase:
 
 
 class ShardedDenseCase(DenseCase):
-    """Row-block sharded dense A over N ranks (one process per GPU, NCCL
-    all-reduce of the A^T Q partials and sketch Grams inside the library)."""
+    """Row-block sharded dense A over N ranks (configs 1, 2 and 4 at N >= 2):
+    each rank builds only its own rows of the seeded construction on its
+    device (bitwise the rows of the whole A); the A^T Q partials and the
+    sketch Grams are all-reduced (NCCL) inside the library."""
 
     def __init__(self, ctx, w, device, rank, world):
         import torch
 
         from paper_1907_06470_b200.distributed import init_comm, row_shards
+        from paper_1907_06470_b200.workloads import dense_lowrank_torch
 
-        super().__init__(ctx, w, device)
+        self.ctx, self.w, self.device = ctx, w, device
+        self.torch_dtype = torch.float64 if w.precision == "double" else torch.float32
+        self.np_dtype = np.float64 if w.precision == "double" else np.float32
         self.r0, self.r1 = row_shards(w.m, world)[rank]
-        self.a = self.a[self.r0:self.r1].clone()
-        torch.cuda.empty_cache()
         self.m_local = self.r1 - self.r0
+        self.a = dense_lowrank_torch(w.m, w.n, w.spectrum, w.noise, w.cfg, w.signal_rank,
+                                     dtype=self.torch_dtype, device=device,
+                                     rows=(self.r0, self.r1))
+        torch.cuda.empty_cache()
         self.u = torch.empty((self.m_local, w.k), dtype=self.torch_dtype, device=device)
+        self.v = torch.empty((w.n, w.k), dtype=self.torch_dtype, device=device)
+        self.s = torch.empty((w.k,), dtype=torch.float64, device=device)
+        self.units = w.m * w.n
+        self.esz = 8 if w.precision == "double" else 4
         init_comm(ctx)
 
     def step(self):
@@ -468,21 +479,31 @@ class ShardedDenseCase(DenseCase):
 
 
 class ColShardedDenseCase(DenseCase):
-    """Column-block sharded wide A over N ranks (config 5's layout): the m x l
-    partials of A_g X_g and the n-side sketch Grams are all-reduced (NCCL)
-    inside the library; A_g^T Q stays local."""
+    """Column-block sharded wide A over N ranks (config 5's layout): each rank
+    builds its own columns; the m x l partials of A_g X_g and the n-side
+    sketch Grams are all-reduced (NCCL) inside the library; A_g^T Q stays
+    local."""
 
     def __init__(self, ctx, w, device, rank, world):
         import torch
 
         from paper_1907_06470_b200.distributed import col_shards, init_comm
+        from paper_1907_06470_b200.workloads import dense_lowrank_torch
 
-        super().__init__(ctx, w, device)
+        self.ctx, self.w, self.device = ctx, w, device
+        self.torch_dtype = torch.float64 if w.precision == "double" else torch.float32
+        self.np_dtype = np.float64 if w.precision == "double" else np.float32
         self.c0, self.c1 = col_shards(w.n, world)[rank]
-        self.a = self.a[:, self.c0:self.c1].contiguous()
-        torch.cuda.empty_cache()
         self.n_local = self.c1 - self.c0
+        self.a = dense_lowrank_torch(w.m, w.n, w.spectrum, w.noise, w.cfg, w.signal_rank,
+                                     dtype=self.torch_dtype, device=device,
+                                     cols=(self.c0, self.c1))
+        torch.cuda.empty_cache()
+        self.u = torch.empty((w.m, w.k), dtype=self.torch_dtype, device=device)
         self.v = torch.empty((self.n_local, w.k), dtype=self.torch_dtype, device=device)
+        self.s = torch.empty((w.k,), dtype=torch.float64, device=device)
+        self.units = w.m * w.n
+        self.esz = 8 if w.precision == "double" else 4
         init_comm(ctx)
 
     def step(self):
@@ -603,6 +624,40 @@ class SparseCase:
                 "algorithmic_bytes": "12 nnz + 8 (rows+1) + 8 l (cols_in + rows_out) per launch"}
 
 
+class ShardedSparseCase(SparseCase):
+    """Row-sharded CSR (config 3 at N >= 2): each rank holds its rows' CSR;
+    Y = A_g X is local and the n x l partials A_g^T Q_g are all-reduced
+    (NCCL) inside the library (xb_rsvd_csr_sharded_dev)."""
+
+    def __init__(self, ctx, w, device, rank, world):
+        import torch
+
+        from paper_1907_06470_b200.distributed import csr_row_shard, init_comm, row_shards
+        from paper_1907_06470_b200.workloads import sparse_uniform_np
+
+        self.ctx, self.w = ctx, w
+        rowptr, col, val = sparse_uniform_np(w.m, w.n, 20, 3000 + w.cfg)
+        self.r0, self.r1 = row_shards(w.m, world)[rank]
+        self.m_local = self.r1 - self.r0
+        lp, lc, lv = csr_row_shard(rowptr, col, val, self.r0, self.r1)
+        self.nnz_local = len(lv)
+        self.rowptr = torch.from_numpy(lp).to(device)
+        self.col = torch.from_numpy(lc).to(device)
+        self.val = torch.from_numpy(lv).to(device)
+        self.u = torch.empty((self.m_local, w.k), dtype=torch.float64, device=device)
+        self.v = torch.empty((w.n, w.k), dtype=torch.float64, device=device)
+        self.s = torch.empty((w.k,), dtype=torch.float64, device=device)
+        self.units = len(val)
+        init_comm(ctx)
+
+    def step(self):
+        w = self.w
+        return self.ctx.rsvd_csr_sharded_dev(
+            w.m, w.n, self.m_local, self.nnz_local, self.rowptr.data_ptr(), self.col.data_ptr(),
+            self.val.data_ptr(), w.k, w.p, w.q, w.cfg, self.u.data_ptr(), self.s.data_ptr(),
+            self.v.data_ptr())[1]
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -618,17 +673,17 @@ def run_ours(args):
     w = CONFIGS[args.config]
     ctx = _lib.load(local)
     knobs = knob_guard(ctx)
-    if args.config == 4:
-        if world > 1:
-            raise SystemExit("config 4 multi-GPU: rows fit in HBM at >= 2 GPUs; use the sharded "
-                             "path on a host with 256 GiB (DESIGN.md)")
+    if world > 1:
+        # wide A (config 5) splits by columns, tall A by rows;
+        # config 4's 256 GiB fits in HBM from 2 GPUs on (128 GiB of rows each),
+        # generated on each device from the seeds
+        if w.density == "sparse":
+            case = ShardedSparseCase(ctx, w, device, rank, world)
+        else:
+            case = (ColShardedDenseCase if w.n > w.m else ShardedDenseCase)(ctx, w, device, rank,
+                                                                            world)
+    elif args.config == 4:
         case = StreamedCase(ctx, w, device)
-    elif world > 1:
-        if w.density != "dense":
-            raise SystemExit("multi-GPU sharding is built for dense A (configs 1, 2, 5)")
-        # wide A (config 5) splits by columns, tall A by rows
-        case = (ColShardedDenseCase if w.n > w.m else ShardedDenseCase)(ctx, w, device, rank,
-                                                                        world)
     elif w.density == "sparse":
         case = SparseCase(ctx, w, device)
     else:

@@ -149,8 +149,11 @@ struct xb_ctx {
     return static_cast<double*>(buf(name, count * sizeof(double)));
   }
   // communicator for the sharded factorisations (xb_comm_init: NCCL;
-  // xb_comm_init_host: the caller's host collectives)
+  // xb_comm_init_host: the caller's host collectives), its stream (the
+  // exchanges overlap the products' later row chunks) and events
   Comm* comm = nullptr;
+  cudaStream_t cs = nullptr;
+  std::vector<cudaEvent_t> xev;
   int world = 1, rank = 0;
   // pinned staging for device -> pageable-host copies (two ping-pong halves)
   void* stage_host = nullptr;
@@ -823,95 +826,145 @@ void oz_prepare(xb_ctx* c, AOp& op, int64_t m, int64_t n) {
   op.oz = z;
 }
 
-// float32 A: right operand X sliced per column (3 digits), the GEMM slices
-// A's tiles on the fly. tn: Z (n x lp) = A^T X, else Y (m x lp) = A X.
-void ozf_product(xb_ctx* c, const AView& a, const OzA& z, bool tn, int64_t m, int64_t n,
-                 const double* X, double* Y, int lp, int l) {
+// The right operand of one product over A (the f64 sketch X, K x lp),
+// sliced once per product for the int8 paths: 3 digit planes for float32 A
+// (ozf_gemm), S slices for the f64 slices of A (ozgemm).
+struct RightOp {
+  int32_t* ex = nullptr;
+  int8_t* xs = nullptr;
+  int64_t np = 0;
+};
+
+RightOp prep_right(xb_ctx* c, const AOp& op, bool tn, int64_t m, int64_t n, const double* X,
+                   int lp) {
+  RightOp r;
+  if (op.sparse || (!op.oz.f32 && !op.oz.S)) return r;
+  const int64_t Kk = tn ? m : n;
+  auto* scr = static_cast<unsigned long long*>(c->buf("oz_xscr", (size_t)round_up(lp, 256) * 8));
+  if (op.oz.f32) {
+    r.np = round_up(lp, ozf_tile_n(lp));
+    const int64_t kp = round_up(Kk, 32);
+    r.ex = c->ibuf("ozf_ex", r.np);
+    r.xs = static_cast<int8_t*>(c->buf("ozf_xs", (size_t)3 * r.np * kp));
+    oz_col_exp(X, Kk, lp, lp, r.ex, scr, nullptr, c->st);
+    oz_slice_right_f(X, Kk, lp, lp, r.ex, r.xs, r.np, kp, c->st);
+  } else {
+    r.np = round_up(lp, 64);
+    const int64_t kp = tn ? op.oz.kpm : op.oz.kpn;
+    r.ex = c->ibuf("oz_ex", r.np);
+    r.xs = static_cast<int8_t*>(c->buf("oz_xs", (size_t)op.oz.S * r.np * kp));
+    oz_col_exp(X, Kk, lp, lp, r.ex, scr, nullptr, c->st);
+    oz_slice_right(X, Kk, lp, lp, r.ex, r.xs, r.np, kp, op.oz.S, c->st);
+  }
+  return r;
+}
+
+// Output rows [r0, r1) of one product over A: Y = A X (NN, rows of A) or
+// Z = A^T Q (TN, columns of A), written to Y + r0 * lp. r0 is a multiple of
+// 128 (the int8 slices' row tile) unless it is 0. Every kernel reads the
+// sub-range through pointer offsets, with its original strides.
+void product_rows(xb_ctx* c, const AOp& op, bool tn, int64_t m, int64_t n, const double* X,
+                  double* Y, int lp, int l, const RightOp& ro, int64_t r0, int64_t r1) {
+  if (r1 <= r0) return;
+  const int64_t Kk = tn ? m : n, rows = r1 - r0;
+  double* Yr = Y + r0 * lp;
+  if (op.sparse) {
+    Csr sub = tn ? op.csrt : op.csr;
+    sub.rowptr += r0;
+    sub.rows = rows;
+    spmm_on_a(c, sub, X, Yr, lp, l);
+    return;
+  }
+  if (!op.oz.f32 && !op.oz.S) {
+    const AView& a = op.dense;
+    const AView v{tn ? static_cast<const char*>(a.p) + (size_t)r0 * a.esz() : a.rows_from(r0), a.ld,
+                  a.f32};
+    gemm_on_a(c, tn, rows, lp, Kk, v, 0, X, lp, Yr, lp, l);
+    return;
+  }
   cudaEvent_t b = nullptr, e = nullptr;
   if (c->profiling) {
     b = c->prof_event();
     e = c->prof_event();
     XB_CUDA(cudaEventRecord(b, c->st));
   }
-  const int64_t Mo = tn ? n : m, Kk = tn ? m : n;
-  const int64_t np = round_up(lp, ozf_tile_n(lp)), kp = round_up(Kk, 32);
-  int32_t* ex = c->ibuf("ozf_ex", np);
-  auto* scr = static_cast<unsigned long long*>(c->buf("oz_xscr", np * 8));
-  int8_t* xs = static_cast<int8_t*>(c->buf("ozf_xs", (size_t)3 * np * kp));
-  oz_col_exp(X, Kk, lp, lp, ex, scr, nullptr, c->st);
-  oz_slice_right_f(X, Kk, lp, lp, ex, xs, np, kp, c->st);
-  const size_t wd = ozf_workspace_doubles(Mo, lp, Kk);
-  double* work = wd ? c->dbuf("split", wd) : nullptr;
-  ozf_gemm(static_cast<const float*>(a.p), a.ld, tn, tn ? z.ecol : z.erow, xs, np, ex, Mo, lp, Kk,
-           Y, lp, false, ozf_plan_splits(Mo, lp, Kk), work, c->st);
+  const OzA& z = op.oz;
+  if (z.f32) {
+    const AView& a = op.dense;
+    const float* A0 = static_cast<const float*>(a.p) + (tn ? r0 : r0 * a.ld);
+    const size_t wd = ozf_workspace_doubles(rows, lp, Kk);
+    double* work = wd ? c->dbuf("split", wd) : nullptr;
+    ozf_gemm(A0, a.ld, tn, (tn ? z.ecol : z.erow) + r0, ro.xs, ro.np, ro.ex, rows, lp, Kk, Yr, lp,
+             false, ozf_plan_splits(rows, lp, Kk), work, c->st);
+  } else {
+    const int64_t kp = tn ? z.kpm : z.kpn, rows_p = tn ? z.np : z.mp;
+    const int8_t* L = (tn ? z.colsT : z.rows) + (size_t)(r0 / 128) * z.S * 128 * 32;
+    const size_t wd = oz_workspace_doubles(rows, lp, Kk);
+    double* work = wd ? c->dbuf("split", wd) : nullptr;
+    ozgemm(L, rows_p, kp, (tn ? z.ecol : z.erow) + r0, ro.xs, ro.np, ro.ex, rows, lp, Kk, Yr, lp,
+           false, z.S, work, c->st);
+  }
   if (c->profiling) {
     XB_CUDA(cudaEventRecord(e, c->st));
-    const double mn = (double)m * (double)n;
-    // 6 int8 slice products over the padded tile grid
-    const double ops = 6.0 * 2.0 * (double)round_up(Mo, 128) * (double)np * (double)kp;
-    c->prof_pending.push_back({b, e, 2.0 * mn * l, mn * 4.0, ops, 4});
+    const double mn = (double)rows * (double)Kk;
+    if (z.f32) {  // 6 int8 slice products over the padded tile grid
+      const double ops = 6.0 * 2.0 * (double)round_up(rows, 128) * (double)ro.np *
+                         (double)round_up(Kk, 32);
+      c->prof_pending.push_back({b, e, 2.0 * mn * l, mn * 4.0, ops, 4});
+    } else {  // S (S + 1) / 2 int8 slice products
+      const double pairs = 0.5 * z.S * (z.S + 1);
+      const double ops = pairs * 2.0 * (double)round_up(rows, 128) * (double)ro.np *
+                         (double)(tn ? z.kpm : z.kpn);
+      c->prof_pending.push_back({b, e, 2.0 * mn * l, mn * z.S, ops, 2});
+    }
   }
 }
 
-// One product on the int8 slices: right operand X (K x lp, f64) sliced per
-// column, then the Ozaki GEMM. tn: Z (n x lp) = A^T X, else Y (m x lp) = A X.
-void oz_product(xb_ctx* c, const OzA& z, bool tn, int64_t m, int64_t n, const double* X,
-                double* Y, int lp, int l) {
-  cudaEvent_t b = nullptr, e = nullptr;
-  if (c->profiling) {
-    b = c->prof_event();
-    e = c->prof_event();
-    XB_CUDA(cudaEventRecord(b, c->st));
+// One product over A. Sharded products end in the one exchange of their
+// layout (row shards: the n x l partials of A^T Q; column shards: the m x l
+// partials of A X), overlapped with the product itself: the output rows are
+// produced in chunks on the compute stream and each chunk's all-reduce runs
+// on the communication stream while the next chunk computes.
+void product(xb_ctx* c, const AOp& op, bool tn, int64_t m, int64_t n, const double* X,
+             double* Y, int lp, int l, bool exchange) {
+  const int64_t rows = tn ? n : m;
+  const RightOp ro = prep_right(c, op, tn, m, n, X, lp);
+  if (!exchange) {
+    product_rows(c, op, tn, m, n, X, Y, lp, l, ro, 0, rows);
+    return;
   }
-  const int64_t Mo = tn ? n : m, Kk = tn ? m : n, kp = tn ? z.kpm : z.kpn;
-  const int64_t np = round_up(lp, 64);
-  int32_t* ex = c->ibuf("oz_ex", np);
-  auto* scr = static_cast<unsigned long long*>(c->buf("oz_xscr", np * 8));
-  int8_t* xs = static_cast<int8_t*>(c->buf("oz_xs", (size_t)z.S * np * kp));
-  oz_col_exp(X, Kk, lp, lp, ex, scr, nullptr, c->st);
-  oz_slice_right(X, Kk, lp, lp, ex, xs, np, kp, z.S, c->st);
-  const size_t wd = oz_workspace_doubles(Mo, lp, Kk);
-  double* work = wd ? c->dbuf("split", wd) : nullptr;
-  ozgemm(tn ? z.colsT : z.rows, tn ? z.np : z.mp, kp, tn ? z.ecol : z.erow, xs, np, ex, Mo, lp,
-         Kk, Y, lp, false, z.S, work, c->st);
-  if (c->profiling) {
-    XB_CUDA(cudaEventRecord(e, c->st));
-    const double mn = (double)m * (double)n;
-    // S (S + 1) / 2 int8 slice products over the padded tile grid
-    const double pairs = 0.5 * z.S * (z.S + 1);
-    const double ops = pairs * 2.0 * (double)round_up(Mo, 128) * (double)np * (double)kp;
-    c->prof_pending.push_back({b, e, 2.0 * mn * l, mn * z.S, ops, 2});
+  const int nch = rows >= 4 * 1024 ? 4 : 1;
+  const int64_t step = nch > 1 ? round_up(ceil_div(rows, (int64_t)nch), 128) : rows;
+  if (!c->cs) XB_CUDA(cudaStreamCreateWithFlags(&c->cs, cudaStreamNonBlocking));
+  while ((int)c->xev.size() < 8) {
+    cudaEvent_t ev;
+    XB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    c->xev.push_back(ev);
   }
+  int i = 0;
+  for (int64_t r0 = 0; r0 < rows; r0 += step, ++i) {
+    const int64_t r1 = std::min(rows, r0 + step);
+    product_rows(c, op, tn, m, n, X, Y, lp, l, ro, r0, r1);
+    XB_CUDA(cudaEventRecord(c->xev[i % 4], c->st));
+    XB_CUDA(cudaStreamWaitEvent(c->cs, c->xev[i % 4], 0));
+    op.comm->allreduce_sum(Y + r0 * lp, (size_t)(r1 - r0) * lp, c->cs);
+  }
+  XB_CUDA(cudaEventRecord(c->xev[4], c->cs));
+  XB_CUDA(cudaStreamWaitEvent(c->st, c->xev[4], 0));
 }
 
 // Y (m x lp) = A X
 void op_nn(xb_ctx* c, const AOp& op, int64_t m, int64_t n, const double* X, double* Y, int lp,
            int l) {
-  if (op.sparse)
-    spmm_on_a(c, op.csr, X, Y, lp, l);
-  else if (op.oz.f32)
-    ozf_product(c, op.dense, op.oz, false, m, n, X, Y, lp, l);
-  else if (op.oz.S)
-    oz_product(c, op.oz, false, m, n, X, Y, lp, l);
-  else
-    gemm_on_a(c, false, m, lp, n, op.dense, 0, X, lp, Y, lp, l);
   // column-sharded: Y = sum_g A_g X_g, the one m x l exchange per product
-  if (op.comm && op.col_shard) op.comm->allreduce_sum(Y, (size_t)m * lp, c->st);
+  product(c, op, false, m, n, X, Y, lp, l, op.comm && op.col_shard);
 }
 
 // Z (n x lp) = A^T Q
 void op_tn(xb_ctx* c, const AOp& op, int64_t m, int64_t n, const double* Q, double* Z, int lp,
            int l) {
-  if (op.sparse)
-    spmm_on_a(c, op.csrt, Q, Z, lp, l);
-  else if (op.oz.f32)
-    ozf_product(c, op.dense, op.oz, true, m, n, Q, Z, lp, l);
-  else if (op.oz.S)
-    oz_product(c, op.oz, true, m, n, Q, Z, lp, l);
-  else
-    gemm_on_a(c, true, n, lp, m, op.dense, 0, Q, lp, Z, lp, l);
   // row-sharded: Z = sum_g A_g^T Q_g, the one n x l exchange per product
-  if (op.comm && !op.col_shard) op.comm->allreduce_sum(Z, (size_t)n * lp, c->st);
+  product(c, op, true, m, n, Q, Z, lp, l, op.comm && !op.col_shard);
 }
 
 // One factorisation. A (device, f64 or f32 dense, or f64 CSR) is only touched
@@ -1533,6 +1586,11 @@ int xb_destroy(xb_ctx* c) {
     for (auto e : c->events) cudaEventDestroy(e);
     if (c->stage_host) cudaFreeHost(c->stage_host);
     delete c->comm;
+    if (c->cs) {
+      cudaStreamSynchronize(c->cs);
+      cudaStreamDestroy(c->cs);
+    }
+    for (auto e : c->xev) cudaEventDestroy(e);
     for (auto e : c->stage_ev)
       if (e) cudaEventDestroy(e);
     cudaStreamDestroy(c->st);

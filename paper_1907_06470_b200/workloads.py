@@ -89,39 +89,50 @@ def workload_dense_np(w: Workload, m: int | None = None, n: int | None = None) -
 
 
 def dense_lowrank_torch(m: int, n: int, kind: str, noise: float, seed: int,
-                        signal_rank: int | None = None, dtype=None, device="cuda"):
-    """Same construction on the GPU via torch (cfg2+ sizes). Returns a torch
-    tensor on `device`. Haar factors via torch.linalg.qr in f64."""
+                        signal_rank: int | None = None, dtype=None, device="cuda",
+                        rows: tuple | None = None, cols: tuple | None = None):
+    """Same construction on the GPU via torch (cfg2+ sizes): the block
+    A[rows[0]:rows[1], cols[0]:cols[1]] (default: all of A) as a torch tensor
+    on `device`. Haar factors via torch.linalg.qr in f64; the noise is drawn
+    per row chunk of fixed height from a generator keyed by the chunk index,
+    so any row or column block of A — one rank's shard — is bitwise the same
+    as the corresponding block of the whole matrix."""
     import torch
 
     dtype = dtype or torch.float64
+    r0, r1 = rows if rows is not None else (0, m)
+    c0, c1 = cols if cols is not None else (0, n)
     r = min(m, n) if signal_rank is None else signal_rank
     g = torch.Generator(device=device)
     g.manual_seed(1000 + seed)
     s = torch.from_numpy(spectrum(kind, r)).to(device)
 
-    def haar(rows, cols):
-        x = torch.randn(rows, cols, generator=g, device=device, dtype=torch.float64)
-        q, rr = torch.linalg.qr(x)
+    def haar(rr, cc):
+        x = torch.randn(rr, cc, generator=g, device=device, dtype=torch.float64)
+        q, R = torch.linalg.qr(x)
         del x
-        return q * torch.where(torch.diagonal(rr) < 0, -1.0, 1.0)
+        return q * torch.where(torch.diagonal(R) < 0, -1.0, 1.0)
 
-    u = haar(m, r)
+    u = haar(m, r)[r0:r1].clone()
+    torch.cuda.empty_cache()
     u.mul_(s)
-    v = haar(n, r)
-    # fill in row chunks of <= 2 GiB of f64 so wide/large A (cfg5: 16384 x 2^20)
-    # never materialises in f64
-    a = torch.empty((m, n), dtype=dtype, device=device)
-    chunk = max(1, min(m, (1 << 28) // max(n, 1)))
+    v = haar(n, r)[c0:c1].clone()
+    torch.cuda.empty_cache()
+    a = torch.empty((r1 - r0, c1 - c0), dtype=dtype, device=device)
+    # fixed chunk height (<= 2^28 elements of f64 per chunk): depends only on
+    # (m, n), never on the requested block
+    chunk = max(1, min(8192, (1 << 28) // max(n, 1)))
     gn = torch.Generator(device=device)
-    gn.manual_seed(2000 + seed)
-    for r0 in range(0, m, chunk):
-        r1 = min(m, r0 + chunk)
-        blk = u[r0:r1] @ v.T
+    for k0 in range((r0 // chunk) * chunk, r1, chunk):
+        k1 = min(m, k0 + chunk)
+        lo, hi = max(k0, r0), min(k1, r1)
+        blk = u[lo - r0:hi - r0] @ v.T
         if noise:
-            blk.add_(torch.randn(r1 - r0, n, generator=gn, device=device, dtype=torch.float64),
-                     alpha=noise)
-        a[r0:r1].copy_(blk)
+            gn.manual_seed((2000 + seed) * 1_000_003 + k0 // chunk)
+            z = torch.randn(k1 - k0, n, generator=gn, device=device, dtype=torch.float64)
+            blk.add_(z[lo - k0:hi - k0, c0:c1], alpha=noise)
+            del z
+        a[lo - r0:hi - r0].copy_(blk)
         del blk
     del u, v
     return a
