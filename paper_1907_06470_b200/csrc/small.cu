@@ -464,11 +464,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   int sweep = 0;
   for (; sweep < max_sweeps; ++sweep) {
     int rot = 0;
+    // circle method (position 0 fixed): this group's players move one seat
+    // per round, pp = 1 + (pa - 1 + round) mod (L2 - 1), kept incrementally
+    const int pa = grp, pb = L2 - 1 - grp;
+    int pp = pa, qq = pb;
     for (int round = 0; round < L2 - 1; ++round) {
+      if (round > 0) {
+        if (pa != 0 && ++pp == L2) pp = 1;
+        if (++qq == L2) qq = 1;
+      }
       if (grp < npairs) {
-        const int pa = grp, pb = L2 - 1 - grp;  // circle method: position 0 fixed
-        int p = pa == 0 ? 0 : 1 + (pa - 1 + round) % (L2 - 1);
-        int q = 1 + (pb - 1 + round) % (L2 - 1);
+        int p = pp, q = qq;
         if (p > q) {
           const int t = p;
           p = q;
@@ -509,13 +515,21 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             double* jp = J + (int64_t)p * l;
             double* jq = J + (int64_t)q * l;
+            // all loads of the two J columns before any store (no
+            // load-store-load serialisation on possible aliasing)
+            double ju[NR], jv[NR];
+#pragma unroll
+            for (int i = 0; i < NR; ++i) {
+              const int r = gl + kGroup * i;
+              ju[i] = r < l ? jp[r] : 0.0;
+              jv[i] = r < l ? jq[r] : 0.0;
+            }
 #pragma unroll
             for (int i = 0; i < NR; ++i) {
               const int r = gl + kGroup * i;
               if (r < l) {
-                const double ju = jp[r], jv = jq[r];
-                jp[r] = cs * ju - sn * jv;
-                jq[r] = sn * ju + cs * jv;
+                jp[r] = cs * ju[i] - sn * jv[i];
+                jq[r] = sn * ju[i] + cs * jv[i];
               }
             }
             rot = 1;
