@@ -231,12 +231,6 @@ void launch_csr_transpose(const Csr& a, int64_t* tptr, int32_t* trow, double* tv
 size_t chol_work_doubles(int l);
 void launch_chol_inv(const double* G, int64_t ldg, int l, double tau, double* R, double* Rinv,
                      int64_t ldr, int* flag, double* ws, cudaStream_t st);
-// Householder QR fallback (single CTA): if *flag != 0, recompute Q (rows x l,
-// ldq) and R (l x l, ldr) from X (rows x l, ldx) with the reference's
-// reflector convention; work needs rows * l doubles.
-void launch_householder_fallback(const double* X, int64_t ldx, int64_t rows, int l, int lpad, double* Q,
-                                 int64_t ldq, double* R, int64_t ldr, double* work,
-                                 const int* flag, cudaStream_t st);
 // TSQR (tsqr.cu): tree Householder QR of X (rows x l) -> Q (rows x lpad, zero
 // padding columns), R (l x l upper, diag >= 0); both passes return at once
 // when *flag == 0 (flag may be null: always run). Q may alias X.

@@ -348,22 +348,12 @@ void gemm(xb_ctx* c, bool ta, int64_t M, int64_t N, int64_t K, const double* A, 
   dgemm(g, splits, work, c->st);
 }
 
-// C = op(A) B for f64 device operands on the int8 tensor pipe (Ozaki
-// slices of both operands, ozgemm.cu): exponents, slicing and the GEMM.
-// Used for the n-side orthonormalisation products of float32 configs at
-// oz_qr_slices() (the 1e-4 / 1e-3 targets leave a large margin) and by the
-// XB_GEMM_OZ diagnostics at the f64 count, oz_slices().
-// Slice count of the float32 configs' f64 products on the int8 pipe (n-side
-// QR Grams, X R^-1, the V lift). 4 slices carry >= 28 bits, beyond the f32
-// data; measured at a cfg5-like 2048 x 65536 (tools/probe_qr_slices.py,
-// profiles/r01_qr_slices.md): sigma 3.9e-8 / angle 2.5e-5 at 4 slices vs
-// 3.6e-8 / 3.4e-5 at 6 (targets 1e-4 / 1e-3); 3 slices 1.2e-7 / 9.7e-5.
 // Jacobi rotation threshold for the small SVD of a float32 factorisation:
 // columns orthogonal to 1e-8 (relative) are far past the f32 targets and
 // save the last quadratic sweep (cfg5-like probe, l = 550: 11 -> 10 sweeps,
 // sigma 3.86e-8 and angles 2.5e-5 unchanged to 3 digits; cfg5 SVD0 stage
-// 38.6 -> 32.2 ms). XB_JACOBI_TOL_F32 overrides (<= 0: the f64 threshold).
-// float64 uses max(1e-15, l eps) unless XB_JACOBI_TOL_F64 (experiments).
+// 38.6 -> 32.2 ms). float64 uses max(1e-15, l eps). (Experiment builds:
+// XB_JACOBI_TOL_F32 / XB_JACOBI_TOL_F64 override.)
 static double jacobi_tol(bool f32) {
   static const double t = [] {
     const char* e = knob("XB_JACOBI_TOL_F32");
@@ -376,6 +366,12 @@ static double jacobi_tol(bool f32) {
   return f32 ? t : t64;
 }
 
+// Slice count of the float32 configs' f64 products on the int8 pipe (n-side
+// QR Grams, X R^-1, the V lift). 4 slices carry >= 28 bits, beyond the f32
+// data; measured at a cfg5-like 2048 x 65536 (tools/probe_qr_slices.py,
+// profiles/r01_qr_slices.md): sigma 3.9e-8 / angle 2.5e-5 at 4 slices vs
+// 3.6e-8 / 3.4e-5 at 6 (targets 1e-4 / 1e-3); 3 slices 1.2e-7 / 9.7e-5.
+// (Experiment builds: XB_OZ_QR_SLICES overrides.)
 static int oz_qr_slices() {
   static const int s = [] {
     const char* e = knob("XB_OZ_QR_SLICES");
@@ -384,6 +380,11 @@ static int oz_qr_slices() {
   return s;
 }
 
+// C = op(A) B for f64 device operands on the int8 tensor pipe (Ozaki
+// slices of both operands, ozgemm.cu): exponents, slicing and the GEMM.
+// Used for the n-side orthonormalisation products of float32 configs at
+// oz_qr_slices() (the 1e-4 / 1e-3 targets leave a large margin) and by the
+// XB_GEMM_OZ diagnostics at the f64 count, oz_slices().
 void oz_gemm64(xb_ctx* c, bool ta, int64_t m, int64_t n, int64_t kdim, const double* A,
                int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc, int tri, int S) {
   const int64_t kp = round_up(kdim, 32), np = round_up(n, 64), mp = round_up(m, 128);

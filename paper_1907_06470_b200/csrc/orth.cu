@@ -4,10 +4,8 @@
 //                core of CholQR2, which replaces the reference's streaming
 //                Householder thin_qr (kernels.py:297-351). Both give the
 //                unique Q with diag(R) > 0 for a full-rank input.
-//  householder   single-CTA Householder QR used when the Gram is not
-//                numerically positive definite (rank-deficient sketches);
-//                follows _house / _householder_qr / _apply_reflectors
-//                (kernels.py:247-294) so R keeps a non-negative diagonal.
+//  (the Householder fallback for Grams that are not numerically positive
+//   definite is the multi-CTA TSQR of tsqr.cu)
 //  deficient     |R_jj| <= eps * ||R||_F flags (kernels.py:327-331).
 //  jacobi_svd    one-sided (Hestenes) Jacobi SVD of M = R_B^T, replacing
 //                the Golub-Kahan svd_small (kernels.py:542-562) applied to
@@ -58,102 +56,6 @@ size_t max_dyn_smem() {
 }
 
 namespace {
-
-// ---------------------------------------------------------------------------
-// Householder QR fallback, single CTA, column-major workspaces.
-__global__ void __launch_bounds__(kSmallThreads, 1)
-    householder_kernel(const double* __restrict__ X, int64_t ldx, int64_t rows, int l, int lpad,
-                       double* __restrict__ Q, int64_t ldq, double* __restrict__ R, int64_t ldr,
-                       double* __restrict__ work, const int* __restrict__ flag) {
-  if (*flag == 0) return;
-  __shared__ double red[kSmallWarps];
-  __shared__ double betas[1024];
-  __shared__ double s_v0, s_beta, s_mu;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  double* Wc = work;                       // rows x l, column-major (reflectors + R)
-  double* E = work + (int64_t)rows * l;    // rows x l, column-major (Q build)
-  for (int64_t idx = tid; idx < rows * l; idx += blockDim.x) {
-    const int64_t i = idx / l;
-    const int c = (int)(idx - i * l);
-    Wc[(int64_t)c * rows + i] = X[i * ldx + c];
-  }
-  for (int64_t idx = tid; idx < (int64_t)l * l; idx += blockDim.x) {
-    const int i = (int)(idx / l), c = (int)(idx - (int64_t)i * l);
-    R[(int64_t)i * ldr + c] = 0.0;
-  }
-  __syncthreads();
-  const int steps = (int)((rows < l) ? rows : l);
-  for (int j = 0; j < steps; ++j) {
-    double* x = Wc + (int64_t)j * rows;
-    double part = 0.0;
-    for (int64_t i = j + 1 + tid; i < rows; i += blockDim.x) part += x[i] * x[i];
-    const double sigma = block_sum(part, red);
-    if (tid == 0) {
-      const double x0 = x[j];
-      double v0 = 1.0, beta, mu;
-      if (sigma == 0.0) {
-        beta = (x0 >= 0.0) ? 0.0 : 2.0;
-        mu = (x0 >= 0.0) ? x0 : -x0;
-      } else {
-        mu = sqrt(x0 * x0 + sigma);
-        v0 = (x0 <= 0.0) ? (x0 - mu) : (-sigma / (x0 + mu));
-        beta = 2.0 * v0 * v0 / (sigma + v0 * v0);
-      }
-      s_v0 = v0;
-      s_beta = beta;
-      s_mu = mu;
-      betas[j < 1024 ? j : 1023] = beta;
-    }
-    __syncthreads();
-    const double v0 = s_v0, beta = s_beta;
-    if (sigma != 0.0) {
-      const double iv = 1.0 / v0;
-      for (int64_t i = j + 1 + tid; i < rows; i += blockDim.x) x[i] *= iv;
-    }
-    __syncthreads();
-    // trailing columns: warp per column
-    for (int c = j + 1 + warp; c < l; c += kSmallWarps) {
-      double* y = Wc + (int64_t)c * rows;
-      double acc = (lane == 0) ? y[j] : 0.0;
-      if (sigma != 0.0)
-        for (int64_t i = j + 1 + lane; i < rows; i += 32) acc += x[i] * y[i];
-      acc = warp_sum(acc) * beta;
-      if (lane == 0) y[j] -= acc;
-      if (sigma != 0.0)
-        for (int64_t i = j + 1 + lane; i < rows; i += 32) y[i] -= acc * x[i];
-    }
-    __syncthreads();
-    if (tid == 0) R[(int64_t)j * ldr + j] = s_mu;
-    for (int c = j + 1 + tid; c < l; c += blockDim.x) R[(int64_t)j * ldr + c] = Wc[(int64_t)c * rows + j];
-    __syncthreads();
-  }
-  // Q = H_0 ... H_{l-1} [I; 0], reflectors applied right to left.
-  for (int64_t idx = tid; idx < rows * l; idx += blockDim.x) {
-    const int c = (int)(idx / rows);
-    const int64_t i = idx - (int64_t)c * rows;
-    E[idx] = (i == c) ? 1.0 : 0.0;
-  }
-  __syncthreads();
-  for (int j = steps - 1; j >= 0; --j) {
-    const double beta = betas[j < 1024 ? j : 1023];
-    if (beta == 0.0) continue;
-    const double* v = Wc + (int64_t)j * rows;  // v[j] = 1 implicit, v[i>j] stored
-    for (int c = j + warp; c < l; c += kSmallWarps) {
-      double* y = E + (int64_t)c * rows;
-      double acc = (lane == 0) ? y[j] : 0.0;
-      for (int64_t i = j + 1 + lane; i < rows; i += 32) acc += v[i] * y[i];
-      acc = warp_sum(acc) * beta;
-      if (lane == 0) y[j] -= acc;
-      for (int64_t i = j + 1 + lane; i < rows; i += 32) y[i] -= acc * v[i];
-    }
-    __syncthreads();
-  }
-  for (int64_t idx = tid; idx < rows * lpad; idx += blockDim.x) {
-    const int64_t i = idx / lpad;
-    const int c = (int)(idx - i * lpad);
-    Q[i * ldq + c] = (c < l) ? E[(int64_t)c * rows + i] : 0.0;
-  }
-}
 
 __global__ void deficient_kernel(const double* __restrict__ R, int64_t ldr, int l, double eps,
                                  int* __restrict__ count, int* __restrict__ cols) {
@@ -306,13 +208,6 @@ void launch_identity_if(double* M, int64_t ld, int l, const int* flag, cudaStrea
   identity_if_kernel<<<(unsigned)std::min<int64_t>(ceil_div((int64_t)l * l, 256), 1024), 256, 0, st>>>(
       M, ld, l, flag);
   check_launch("identity_if");
-}
-
-void launch_householder_fallback(const double* X, int64_t ldx, int64_t rows, int l, int lpad, double* Q,
-                                 int64_t ldq, double* R, int64_t ldr, double* work,
-                                 const int* flag, cudaStream_t st) {
-  householder_kernel<<<1, kSmallThreads, 0, st>>>(X, ldx, rows, l, lpad, Q, ldq, R, ldr, work, flag);
-  check_launch("householder");
 }
 
 void launch_deficient(const double* R, int64_t ldr, int l, double eps, int* count, int* cols,
