@@ -22,18 +22,12 @@ carried through the re-orthonormalised iteration as small triangular factors
 rank-wide probe. gram_path=True (526-580) projects the power matrix and
 factors its Gram on the device too.
 
-Durable plans (pipeline.py:163-253, 722-756, 838-934): with a BlockStore
-behind the pool (RsvdConfig.workdir, `run_command`, `resume`), PlanRunner
-writes a step record per step and flushes each step's outputs before
-marking it done, in the reference's on-disk formats (store.py). The device
-factorisation is ONE step ("rsvd-device", outputs U/S/V): it runs in
-milliseconds to seconds, so finer records would only add fsyncs. A resumed
-plan replays done steps from their records (U/S/V load from the store, the
-chosen q from the record's meta) and runs the rest; `_export_steps` writes
-U.blk/S.blk/V.blk/S.txt byte-compatible with the reference's exports.
-Step ids are our own sequence: a workdir the reference started does not
-resume here mid-plan (its op names differ, so its records never match and
-every step reruns).
+Durable plans (plan.py: PlanRunner, run_command, resume; the reference's
+pipeline.py:163-253, 719-770, 838-934): with a BlockStore behind the pool,
+each step is journalled in the reference's on-disk formats (store.py) and a
+resumed plan replays the finished ones. The device factorisation is ONE step
+("rsvd-device", outputs U/S/V); a direct call on a store-backed pool first
+runs an "ingest" step that makes A durable, as the reference does.
 """
 
 from __future__ import annotations
@@ -49,19 +43,10 @@ import numpy as np
 
 from . import _lib
 from .core import Precision, as_precision
-from .errors import ConfigMismatchError, PlanNotFoundError, ShapeError, XsvdError
+from .errors import ShapeError, XsvdError
 from .pool import (BlockPool, StoredMatrix, canonical_coo, is_sparse, register_dense,
                    stored_to_array)
-from .store import BlockStore, StepRecord, write_block_file
 
-ABORT_ENV = "XSVD_ABORT_AFTER_STEPS"
-ABORT_EXIT_CODE = 70
-
-
-def _abort_after():
-    """Test hook: exit between two steps after N of them (pipeline.py:54-60)."""
-    raw = os.environ.get(ABORT_ENV)
-    return int(raw) if raw else None
 
 STAGE_PARSE = "Text Parsing"
 STAGE_GAUSSIAN = "Preparation of O"
@@ -147,62 +132,6 @@ class RsvdResult:
     deficient_columns: tuple = ()
 
 
-class PlanRunner:
-    """Runs plan steps in order, skipping ones already durably done
-    (pipeline.py:163-253). Step ids follow call order, so a resumed process
-    lines each `step` call up with its prior record; a done step returns its
-    recorded meta instead of running."""
-
-    def __init__(self, store, pool, plan_id, clock, *, completed=None, abort_after=None):
-        self.store = store
-        self.pool = pool
-        self.plan_id = plan_id
-        self.clock = clock
-        self.completed = completed or {}
-        self.abort_after = abort_after
-        self.next_id = 0
-        self.ran = 0
-
-    def step(self, op, *, stage, fn, inputs=(), outputs=(), seed=None, self_clocked=False):
-        step_id = self.next_id
-        self.next_id += 1
-        prior = self.completed.get(step_id)
-        if (prior is not None and prior.status == "done" and prior.op == op
-                and prior.plan_id == self.plan_id):
-            return dict(prior.meta)
-        record = StepRecord(self.plan_id, step_id, op, list(inputs), list(outputs), "pending",
-                            seed)
-        if self.store is not None:
-            with self.clock.timing(stage):
-                self.store.write_step(record)
-        if self_clocked:
-            meta = fn() or {}
-        else:
-            with self.clock.timing(stage):
-                meta = fn() or {}
-        with self.clock.timing(stage):
-            if self.store is not None:
-                for matrix_id in outputs:
-                    self.pool.flush_matrix(matrix_id)
-                record.status = "done"
-                record.meta = meta
-                self.store.write_step(record)
-        self.ran += 1
-        if self.abort_after is not None and self.ran >= self.abort_after:
-            os._exit(ABORT_EXIT_CODE)  # simulated kill between two steps
-        return meta
-
-    def matrix(self, matrix_id):
-        """Handle on a step output, produced now or by a prior run."""
-        try:
-            return StoredMatrix(self.pool.descriptor(matrix_id), self.pool)
-        except KeyError:
-            if self.store is None:
-                raise
-            desc = self.pool.register(self.store.load_descriptor(matrix_id))
-            return StoredMatrix(desc, self.pool)
-
-
 def gaussian_matrix(pool, matrix_id, rows, cols, seed, *, precision=Precision.DOUBLE):
     """N(0,1) matrix keyed by (seed, row) (pipeline.py:259-284), generated on
     the device (rng.py restated in csrc/rng.cu)."""
@@ -236,10 +165,22 @@ def randomized_svd(pool, a, config: RsvdConfig, *, threads: int = 1, runner=None
     clock = clock or (runner.clock if runner is not None else StageClock())
     store = getattr(pool, "store", None)
     if runner is None and store is not None:
-        # a store-backed pool without a runner starts a plan (pipeline.py:466-479)
-        runner = PlanRunner(store, pool, config.digest(), clock, abort_after=_abort_after())
+        # a store-backed pool without a runner starts a plan of its own
+        # (pipeline.py:466-485): settings saved, then step 0 makes the input
+        # durable, so a killed run can resume from the workdir alone
+        from .plan import PlanRunner, abort_after_from_env
+
+        runner = PlanRunner(store, pool, config.digest(), clock,
+                            abort_after=abort_after_from_env())
         store.save_plan_config({"command": None, "input_matrix": a.matrix_id,
                                 "config": config.to_json(), "digest": config.digest()})
+        input_id = a.matrix_id
+
+        def ingest():
+            pool.flush_matrix(input_id)
+            return {}
+
+        runner.step("ingest", stage=STAGE_PARSE, outputs=[input_id], fn=ingest)
     if runner is None:
         u, s, v, deficient, chosen_q = _rsvd_device(a, config, precision, clock)
         register_dense(pool, "S", s.reshape(-1, 1), Precision.DOUBLE)
@@ -372,119 +313,6 @@ def full_svd(pool, a, config=None, *, threads: int = 1, runner=None, clock=None)
                       deficient_columns=tuple(meta.get("deficient", ())))
 
 
-# -- durable command drivers (pipeline.py:719-934) --------------------------
-
-
-def _export_steps(runner, outdir):
-    """U.blk / S.blk / V.blk and S.txt (%.17g per line), one step each
-    (pipeline.py:722-740)."""
-    os.makedirs(outdir, exist_ok=True)
-    for matrix_id, filename in (("U", "U.blk"), ("S", "S.blk"), ("V", "V.blk")):
-
-        def export(matrix_id=matrix_id, filename=filename):
-            mat = runner.matrix(matrix_id)
-            write_block_file(os.path.join(outdir, filename), mat)
-            if matrix_id == "S":
-                values = mat.to_array().astype(np.float64).ravel()
-                tmp = os.path.join(outdir, "S.txt.tmp")
-                with open(tmp, "w") as f:
-                    for value in values:
-                        f.write(f"{value:.17g}\n")
-                os.replace(tmp, os.path.join(outdir, "S.txt"))
-            return {}
-
-        runner.step(f"export-{matrix_id.lower()}", stage=STAGE_POST, inputs=[matrix_id], fn=export)
-
-
-def _parse_step(runner, pool, config, input_path):
-    from .formats import parse_matrix_market
-
-    runner.step("parse", stage=STAGE_PARSE, outputs=["A"],
-                fn=lambda: parse_matrix_market(input_path, pool, "A",
-                                               precision=config.precision) and {})
-
-
-def _drive_rsvd(runner, pool, config, threads, input_path, outdir):
-    """pipeline.py:743-756."""
-    _parse_step(runner, pool, config, input_path)
-    result = randomized_svd(pool, runner.matrix("A"), config, threads=threads, runner=runner)
-    _export_steps(runner, outdir)
-    return result
-
-
-def _drive_full_svd(runner, pool, config, threads, input_path, outdir):
-    """pipeline.py:759-770."""
-    _parse_step(runner, pool, config, input_path)
-    result = full_svd(pool, runner.matrix("A"), config, threads=threads, runner=runner)
-    _export_steps(runner, outdir)
-    return result
-
-
-_DRIVERS = {"rsvd": _drive_rsvd, "svd": _drive_full_svd}
-
-
-def run_command(command, input_path, output_path, config: RsvdConfig, *, threads: int = 1,
-                fresh: bool = True, profile_out=None):
-    """One factorisation command with a durable plan in config.workdir
-    (pipeline.py:838-877). `fresh` wipes any previous plan first."""
-    if config.workdir is None:
-        raise ValueError("run_command needs config.workdir for its plan state")
-    if command not in _DRIVERS:
-        raise XsvdError(f"command {command!r} is not built on the GPU path "
-                        f"(have: {', '.join(sorted(_DRIVERS))})")
-    clock = StageClock()
-    with clock.timing(STAGE_PARSE):
-        store = BlockStore(config.workdir)
-        if fresh:
-            store.clear_plan()
-        store.save_plan_config({
-            "command": command, "input": os.path.abspath(input_path),
-            "output": os.path.abspath(output_path), "threads": threads,
-            "profile_out": os.path.abspath(profile_out) if profile_out else None,
-            "config": config.to_json(), "digest": config.digest()})
-        pool = BlockPool(store, config.budget)
-    runner = PlanRunner(store, pool, config.digest(), clock, abort_after=_abort_after())
-    result = _DRIVERS[command](runner, pool, config, threads, input_path, output_path)
-    result.stage_seconds = dict(clock.seconds)
-    return result, pool, runner
-
-
-def resume(workdir: str, config: RsvdConfig | None = None, *, threads: int | None = None):
-    """Finish an interrupted plan; refuses to continue under changed settings
-    (pipeline.py:880-934)."""
-    if not os.path.exists(os.path.join(workdir, "plan", "config.json")):
-        raise PlanNotFoundError(f"no execution plan under {workdir}")
-    store = BlockStore(workdir)
-    saved = store.load_plan_config()
-    if saved is None or "config" not in saved or "digest" not in saved:
-        raise PlanNotFoundError(f"plan configuration under {workdir} is unreadable")
-    try:
-        saved_config = RsvdConfig.from_json(saved["config"], workdir=workdir)
-    except (KeyError, ValueError) as e:
-        raise PlanNotFoundError(f"plan configuration under {workdir} is unreadable: {e}")
-    if saved_config.digest() != saved["digest"]:
-        raise ConfigMismatchError(
-            "plan configuration does not match its recorded digest; refusing to resume")
-    if config is not None and config.digest() != saved["digest"]:
-        raise ConfigMismatchError(
-            "supplied configuration differs from the one this plan was started with")
-    pool = BlockPool(store, saved_config.budget)
-    clock = StageClock()
-    with clock.timing(STAGE_PARSE):
-        completed = {sid: rec for sid, rec in store.scan_plan().items()
-                     if rec.status == "done" and rec.plan_id == saved["digest"]}
-    runner = PlanRunner(store, pool, saved["digest"], clock, completed=completed,
-                        abort_after=_abort_after())
-    if threads is None:
-        threads = saved.get("threads", 1)
-    command = saved.get("command")
-    if command is None:
-        a = runner.matrix(saved.get("input_matrix", "A"))
-        result = randomized_svd(pool, a, saved_config, threads=threads, runner=runner)
-    else:
-        if command not in _DRIVERS:
-            raise XsvdError(f"command {command!r} is not built on the GPU path")
-        result = _DRIVERS[command](runner, pool, saved_config, threads, saved["input"],
-                                   saved["output"])
-    result.stage_seconds = dict(clock.seconds)
-    return result, pool, runner
+# The durable plan machinery (PlanRunner, run_command, resume) lives in
+# plan.py; re-exported here under the reference's module layout.
+from .plan import ABORT_ENV, ABORT_EXIT_CODE, PlanRunner, resume, run_command  # noqa: E402,F401

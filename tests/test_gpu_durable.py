@@ -122,3 +122,37 @@ def test_run_command_svd(lib, tmp_path):
         dense[int(i) - 1, int(j) - 1] = float(v)
     ref = np.linalg.svd(dense, compute_uv=False)
     assert np.max(np.abs(s - ref)) / ref[0] <= 1e-10
+
+
+def test_direct_call_on_store_pool_resumes_after_kill(lib, tmp_path):
+    """randomized_svd(pool-with-store, A, config) without a runner journals
+    its own plan: step 0 ("ingest") makes A durable, so a process killed
+    right after it resumes from the workdir alone (pipeline.py:466-485, 924)."""
+    import paper_1907_06470_b200 as X
+
+    work = str(tmp_path / "work")
+    script = (
+        "import sys; sys.path.insert(0, %r)\n"
+        "import numpy as np\n"
+        "import paper_1907_06470_b200 as X\n"
+        "cfg = X.RsvdConfig(rank=6, oversample=4, power=1, seed=5, workdir=%r)\n"
+        "pool = X.BlockPool(X.BlockStore(%r))\n"
+        "arr = np.random.default_rng(2).standard_normal((300, 120))\n"
+        "a = X.matrix_from_dense(pool, 'A', arr, precision=X.Precision.DOUBLE)\n"
+        "X.randomized_svd(pool, a, cfg)\n"
+    ) % (ROOT, work, work)
+    env = dict(os.environ, XSVD_ABORT_AFTER_STEPS="1")
+    proc = subprocess.run([sys.executable, "-c", script], env=env, cwd=ROOT, timeout=600)
+    assert proc.returncode == 70  # killed after the ingest step
+    recs = X.BlockStore(work).scan_plan()
+    assert [(r.op, r.status) for r in recs.values()] == [("ingest", "done")]
+    res, _, runner = X.resume(work)
+    assert runner.ran == 1  # only the device step reran
+    arr = np.random.default_rng(2).standard_normal((300, 120))
+    ref = np.linalg.svd(arr, compute_uv=False)[:6]
+    assert res.s.shape == (6,)
+    assert np.max(np.abs(res.s - ref) / ref) <= 0.2  # rSVD with q = 1 on a flat spectrum
+    from oracle import pipeline as OP
+
+    want = OP.rsvd_reorth(arr, 6, 4, 1, 5, "double", fast=True)
+    assert np.max(np.abs(res.s - want.s) / want.s) <= 1e-10
