@@ -1358,8 +1358,6 @@ void rsvd_stream(xb_ctx* c, const void* hostA, int64_t host_lda, bool f32, int64
                  int64_t tile_rows, uint64_t seed, int k, int p, int q, const RsvdOut& out,
                  int32_t* deficient, int* ndeficient, double* stage_seconds) {
   check_dims(m, n, k, p, q);
-  XB_REQUIRE(q >= 0, XB_EUNSUPPORTED, "power='auto' is not built for the out-of-core streamer");
-  XB_REQUIRE(!c->gram_path, XB_EUNSUPPORTED, "gram_path is not built for the out-of-core streamer");
   const int l = k + p;
   const int lp = (int)round_up(l, 8);
   const int kp = (int)round_up(k, 2);
@@ -1423,21 +1421,63 @@ void rsvd_stream(xb_ctx* c, const void* hostA, int64_t host_lda, bool f32, int64
     });
   };
 
+  // power = "auto" (pipeline.py:295-372): the same carried-R stopping rule
+  // as rsvd_impl; every fused pass yields the raw Y of the next power, so
+  // the rule costs no extra pass over A, and stopping after pass `it` finds
+  // B^T = W R^-1 already in hand
+  const bool autoq = q == XB_POWER_AUTO;
+  const int qlim = autoq ? c->auto_qmax : q;
+  AutoPower ap;
+  if (autoq) {
+    ap.on = true;
+    ap.lp = lp;
+    const size_t ll = (size_t)lp * lp;
+    ap.C = c->dbuf("ap_C", ll);
+    ap.M = c->dbuf("ap_M", ll);
+    ap.Rq = c->dbuf("ap_Rq", ll);
+    ap.Rz = c->dbuf("ap_Rz", ll);
+    ap.nrm = c->dbuf("ap_nrm", 1);
+    launch_identity(ap.C, lp, lp, st);
+    ap.scale = 1.0 / std::sqrt((double)m * (double)l);
+  }
   const double* X = Om;
-  for (int it = 0; it <= q; ++it) {
+  int chosen = 0;
+  double ln0 = 0.0, lnprev = 0.0;
+  for (int it = 0; it <= qlim; ++it) {
     clk.enter(kSketch);
     fused_pass(X);
     clk.enter(kOrtho);
-    if (it < q) {
-      cholqr1(c, s, Ym, m, Qm);  // R^-1 in s.R1i unless the fallback ran
+    bool last = it == qlim;
+    if (autoq) {
+      cholqr1(c, s, Ym, m, Qm, false, ap.Rq);  // R of the raw-product chain
+      const double ln = auto_nu(c, ap);
+      if (it == 0) {
+        ln0 = lnprev = ln;
+        if (!(ap.nus[0] > 0.0)) last = true;  // zero sketch: nothing to sharpen
+      } else {
+        // stopping rule of pipeline.py:361-370
+        if (ln < std::log(c->auto_tau) + ln0) {
+          last = true;
+        } else {
+          const double rho = std::exp(ln - lnprev);
+          if (std::fabs(rho - ap.prev_rho) <= 0.01 * rho) last = true;
+          ap.prev_rho = rho;
+        }
+        lnprev = ln;
+      }
+    }
+    if (!last) {
+      if (!autoq) cholqr1(c, s, Ym, m, Qm);  // R^-1 in s.R1i unless the fallback ran
       clk.enter(kSketch);
       if (host_flag(c, s.flag))
         tn_pass(Qm, Zn);
       else
         gemm(c, false, n, lp, lp, Wn, lp, s.R1i, lp, Zn, lp);  // Z = W R^-1 = A^T Q
       clk.enter(kOrtho);
-      cholqr1(c, s, Zn, n, Qn);
+      cholqr1(c, s, Zn, n, Qn, false, autoq ? ap.Rz : nullptr);
+      if (autoq) gemm(c, false, lp, lp, lp, ap.Rz, lp, ap.M, lp, ap.C, lp);  // C = R_z M
       X = Qn;
+      chosen = it + 1;
     } else {
       cholqr2(c, s, Ym, m, Tm, Qm, Rf);
       clk.enter(kProject);
@@ -1447,16 +1487,43 @@ void rsvd_stream(xb_ctx* c, const void* hostA, int64_t host_lda, bool f32, int64
         gemm(c, false, n, lp, lp, Wn, lp, s.R1i, lp, Tn, lp);  // B^T = W R1^-1 R2^-1
         gemm(c, false, n, lp, lp, Tn, lp, s.R2i, lp, Zn, lp);
       }
+      break;
     }
   }
+  c->last_q = autoq ? chosen : q;
+  c->last_nus = ap.nus;
   launch_deficient(Rf, lp, l, f32 ? (double)FLT_EPSILON : DBL_EPSILON, defc, defc + 1, st);
-  clk.enter(kSvdPrep);
-  cholqr2(c, s, Zn, n, Tn, Qn, Rf);
-  clk.enter(kSvd);
-  launch_jacobi_svd(Rf, lp, l, k, Ub, lp, sv, Wk, kp, jw, jstat, st, jacobi_tol(f32));
-  clk.enter(kPost);
-  gemm(c, false, m, k, lp, Qm, lp, Ub, lp, out.U, out.ldu);
-  gemm(c, false, n, k, lp, Qn, lp, Wk, kp, out.V, out.ldv);
+  if (c->gram_path) {
+    // gram_path (pipeline.py:526-580): B^T of the power matrix by 2q raw
+    // products — each a fused pass with X = B^T (Y' = A B^T, W = A^T Y') —
+    // then the l x l Gram, its eigen-decomposition by Jacobi, sigma =
+    // sqrt(eig)^(1/(2q+1)), U = Q U_B, V = B^T U_B with unit columns
+    const int qg = c->last_q;
+    for (int i = 0; i < qg; ++i) {
+      clk.enter(kProject);
+      fused_pass(Zn);
+      XB_CUDA(cudaMemcpyAsync(Zn, Wn, (size_t)n * lp * sizeof(double), cudaMemcpyDeviceToDevice,
+                              st));
+    }
+    clk.enter(kSvdPrep);
+    gemm(c, true, lp, lp, n, Zn, lp, Zn, lp, s.G, lp);  // full G (Jacobi reads all of it)
+    clk.enter(kSvd);
+    launch_jacobi_svd(s.G, lp, l, k, Ub, lp, sv, Wk, kp, jw, jstat, st);
+    launch_gram_sigma(sv, l, qg > 0 ? 1.0 / (2 * qg + 1) : 1.0, st);
+    clk.enter(kPost);
+    gemm(c, false, m, k, lp, Qm, lp, Ub, lp, out.U, out.ldu);  // U = Q U_B[:, :k]
+    gemm(c, false, n, k, lp, Zn, lp, Ub, lp, out.V, out.ldv);  // V = B^T U_B[:, :k]
+    gemm(c, true, k, k, n, out.V, out.ldv, out.V, out.ldv, s.Rs, k);  // column norms^2
+    launch_scale_cols_by_diag(out.V, out.ldv, n, k, s.Rs, k, st);
+  } else {
+    clk.enter(kSvdPrep);
+    cholqr2(c, s, Zn, n, Tn, Qn, Rf);
+    clk.enter(kSvd);
+    launch_jacobi_svd(Rf, lp, l, k, Ub, lp, sv, Wk, kp, jw, jstat, st, jacobi_tol(f32));
+    clk.enter(kPost);
+    gemm(c, false, m, k, lp, Qm, lp, Ub, lp, out.U, out.ldu);
+    gemm(c, false, n, k, lp, Qn, lp, Wk, kp, out.V, out.ldv);
+  }
   XB_CUDA(cudaMemcpyAsync(out.s, sv, k * sizeof(double), cudaMemcpyDeviceToDevice, st));
   int hstat = 0;
   std::vector<int> hdef(lp + 1, 0);

@@ -42,3 +42,42 @@ def test_streamed_rank_deficient_falls_back(lib):
     ref = np.linalg.svd(a, compute_uv=False)
     assert np.max(np.abs(s[:15] - ref[:15])) / ref[0] <= 1e-10
     assert M.sin_angle(u[:, :15], np.linalg.svd(a, full_matrices=False)[0][:, :15]) <= 1e-8
+
+
+def test_streamed_power_auto_matches_in_hbm(lib):
+    """power="auto" out of core (pipeline.py:295-372): the stopping rule is
+    evaluated on every fused pass's raw Y, so the chosen q and the nu
+    sequence equal the in-HBM engine's and the oracle loop's."""
+    from paper_1907_06470_b200 import _lib
+    from paper_1907_06470_b200.workloads import dense_lowrank_np
+
+    a = dense_lowrank_np(6000, 1200, "geom0.9", 1e-8, 45, 46)
+    lib.set_power_auto(5, 1e-6)
+    u0, s0, v0, _, _ = lib.rsvd_dense(a, 30, 10, _lib.POWER_AUTO, 4)
+    q0, nu0 = lib.last_power()
+    u1, s1, v1, _, _ = lib.rsvd_dense_streamed(a, 30, 10, _lib.POWER_AUTO, 4, tile_rows=1024)
+    q1, nu1 = lib.last_power()
+    qref, nuref = OP.sketch_power_auto(a, 30, 10, 4, "double", q_max=5, tau=1e-6, fast=True)
+    assert q1 == q0 == qref
+    np.testing.assert_allclose(nu1, nuref, rtol=1e-10)
+    ref = OP.rsvd_reorth(a, 30, 10, qref, 4, "double", fast=True)
+    assert M.sigma_rel(s1, ref.s) <= 1e-10
+    assert M.sin_angle(u1, ref.u) <= 1e-8 and M.sin_angle(v1, ref.v) <= 1e-8
+
+
+def test_streamed_gram_path_matches_oracle(lib):
+    """gram_path out of core (pipeline.py:526-580): the power-matrix
+    projection's 2q raw products are q more fused passes."""
+    from paper_1907_06470_b200.workloads import dense_lowrank_np
+
+    a = dense_lowrank_np(5000, 1000, "pow-1.5", 1e-8, 47, 48)
+    lib.set_gram_path(True)
+    try:
+        u, s, v, _, _ = lib.rsvd_dense_streamed(a, 40, 10, 2, 6, tile_rows=800)
+    finally:
+        lib.set_gram_path(False)
+    ref = OP.rsvd_reorth_gram(a, 40, 10, 2, 6, "double", fast=True)
+    # as tests/test_gpu_gram_path.py: the Gram squares the condition, so
+    # sigma is compared relative to sigma_1
+    assert np.max(np.abs(s - ref.s)) / ref.s[0] <= 1e-10
+    assert M.sin_angle(u, ref.u) <= 1e-8 and M.sin_angle(v, ref.v) <= 1e-8
