@@ -216,13 +216,22 @@ def _rsvd_device(a, config, precision, clock):
     ctx.set_gram_path(config.gram_path)
     try:
         if is_sparse(a):
-            if precision is not Precision.DOUBLE:
-                raise XsvdError("sparse A is built for float64 only")
             rows, cols, vals = canonical_coo(a)
             if a.desc.transposed:
                 rows, cols = cols, rows
-            u, s, v, deficient, stages = ctx.rsvd_coo(rows, cols, vals, tuple(a.shape), config.rank,
-                                                      config.oversample, q, config.seed)
+            omega = None
+            if precision is Precision.SINGLE:
+                # float32 storage (kernels.py:85-97 with cdt = f32): the values
+                # and Omega are float32 numbers (pipeline.py:281-282), carried
+                # exactly in the f64 sparse engine; U, V stored as float32
+                omega = ctx.gaussian(config.seed, 0, a.shape[1],
+                                     config.rank + config.oversample,
+                                     dtype=np.float32).astype(np.float64)
+            u, s, v, deficient, stages = ctx.rsvd_coo(
+                rows, cols, np.asarray(vals, dtype=np.float64), tuple(a.shape), config.rank,
+                config.oversample, q, config.seed, omega=omega)
+            u = u.astype(precision.storage_dtype, copy=False)
+            v = v.astype(precision.storage_dtype, copy=False)
         else:
             host = _dense_input(a).astype(precision.storage_dtype, copy=False)
             u, s, v, deficient, stages = ctx.rsvd_dense(host, config.rank, config.oversample, q,
@@ -253,12 +262,14 @@ def auto_select_q(pool, a, rank, *, q_max: int = 5, tau: float = 1e-6, seed: int
     ctx.set_power_auto(q_max, tau)
     ctx.set_gram_path(False)
     if is_sparse(a):
-        if precision is not Precision.DOUBLE:
-            raise XsvdError("sparse A is built for float64 only")
         rows, cols, vals = canonical_coo(a)
         if a.desc.transposed:
             rows, cols = cols, rows
-        ctx.rsvd_coo(rows, cols, vals, tuple(a.shape), rank, 0, _lib.POWER_AUTO, seed)
+        omega = None
+        if precision is Precision.SINGLE:
+            omega = ctx.gaussian(seed, 0, n, rank, dtype=np.float32).astype(np.float64)
+        ctx.rsvd_coo(rows, cols, np.asarray(vals, dtype=np.float64), tuple(a.shape), rank, 0,
+                     _lib.POWER_AUTO, seed, omega=omega)
     else:
         host = _dense_input(a).astype(precision.storage_dtype, copy=False)
         ctx.rsvd_dense(host, rank, 0, _lib.POWER_AUTO, seed)

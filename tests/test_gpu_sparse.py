@@ -150,3 +150,28 @@ def test_drop_in_sparse(lib):
     assert np.max(np.abs(out.to_array() - w.T @ a)) <= 1e-13
     out, _ = X.block_multiply(pool, ma.T, mw, "AtW")
     assert np.max(np.abs(out.to_array() - a.T @ w)) <= 1e-13
+
+
+def test_drop_in_sparse_single_precision(lib):
+    """Sparse A at Precision.SINGLE (kernels.py:85-97 with cdt = f32): float32
+    values and float32 Omega (pipeline.py:281-282); the device carries them
+    exactly in its f64 engine, U and V come back float32. Checked against
+    the oracle's float32 computation at the f32 tolerances."""
+    import paper_1907_06470_b200 as X
+    from paper_1907_06470_b200.workloads import sparse_uniform_np
+
+    m, n = 20000, 4000
+    rowptr, col, val = sparse_uniform_np(m, n, 20, 21)
+    rows = np.repeat(np.arange(m), np.diff(rowptr))
+    val32 = val.astype(np.float32)
+    pool = X.BlockPool()
+    ma = X.matrix_from_coo(pool, "A", m, n, rows, col.astype(np.int64), val32,
+                           precision=X.Precision.SINGLE)
+    res = X.randomized_svd(pool, ma, X.RsvdConfig(rank=40, oversample=10, power=2, seed=8,
+                                                  precision=X.Precision.SINGLE))
+    assert res.u.to_array().dtype == np.float32 and res.v.to_array().dtype == np.float32
+    ref = OP.rsvd_reorth(OP.Coo(rows, col.astype(np.int64), val32, (m, n)), 40, 10, 2, 8,
+                         "single", fast=True)
+    assert M.sigma_rel(res.s, ref.s) <= 1e-4
+    assert M.sin_angle(res.u.to_array(), ref.u) <= 1e-3
+    assert M.sin_angle(res.v.to_array(), ref.v) <= 1e-3
