@@ -146,6 +146,24 @@ int xb_last_power(xb_ctx* ctx, int* chosen_q, double* nus, int cap, int* count);
  * does not fit in device memory; this entry point forces it. Replaces the
  * reference's budgeted residency (BlockPool LRU + spill, pool.py:189-221)
  * for the A-larger-than-memory case (config 4). Omega is generated. */
+/* Dense A given as the reference's TILE GRID (a StoredMatrix of several
+ * tiles, possibly budgeted or backed by a BlockStore: pool.get /
+ * read_cell_dense, pool.py:397-418), never assembled in host memory. The
+ * library asks for each tile when it streams its row band:
+ *   fetch(user, ti, tj, &ld) -> host pointer to the tile (row-major, ld
+ *   elements per row), valid until release(user, ti, tj) (release may be
+ *   null); row_cuts[0..ntr], col_cuts[0..ntc] are the grid's cuts.
+ * A that fits HBM is ingested band by band (the first product computed as
+ * bands land); otherwise (or force_stream != 0) the out-of-core streamer
+ * runs q + 1 fused passes over the grid. Outputs as xb_rsvd_dense. */
+typedef const void* (*xb_tile_fetch_fn)(void* user, int64_t ti, int64_t tj, int64_t* ld);
+typedef void (*xb_tile_release_fn)(void* user, int64_t ti, int64_t tj);
+int xb_rsvd_dense_tiles(xb_ctx* ctx, int dtype, int64_t m, int64_t n, const int64_t* row_cuts,
+                        int ntr, const int64_t* col_cuts, int ntc, xb_tile_fetch_fn fetch,
+                        xb_tile_release_fn release, void* user, int force_stream, uint64_t seed,
+                        int k, int p, int q, void* U, int64_t ldu, double* s, void* V,
+                        int64_t ldv, int32_t* deficient, int* ndeficient,
+                        double* stage_seconds);
 int xb_rsvd_dense_streamed(xb_ctx* ctx, int dtype, int64_t m, int64_t n, const void* A,
                            int64_t lda, uint64_t seed, int k, int p, int q, int64_t tile_rows,
                            void* U, int64_t ldu, double* s, void* V, int64_t ldv,

@@ -23,6 +23,8 @@ NUM_STAGES = 8
 POWER_AUTO = -1  # XB_POWER_AUTO: q argument selecting power = "auto"
 COLL_ALLREDUCE_SUM, COLL_ALLGATHER = 0, 1  # xb_host_collective_fn ops
 HOST_COLLECTIVE = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_int64)
+TILE_FETCH = C.CFUNCTYPE(C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.POINTER(C.c_int64))
+TILE_RELEASE = C.CFUNCTYPE(None, C.c_void_p, C.c_int64, C.c_int64)
 
 _lock = threading.Lock()
 _lib = None
@@ -51,6 +53,9 @@ SIGNATURES = [
                              _vp, _i64, _vp, _vp, _i64, _vp, _intp, _vp]),
     ("xb_rsvd_dense_dev", _int, [_vp, _int, _i64, _i64, _vp, _i64, _vp, _u64, _int, _int, _int,
                                  _vp, _i64, _vp, _vp, _i64, _vp, _intp, _vp]),
+    ("xb_rsvd_dense_tiles", _int, [_vp, _int, _i64, _i64, _vp, _int, _vp, _int, _vp, _vp, _vp,
+                                   _int, _u64, _int, _int, _int, _vp, _i64, _vp, _vp, _i64, _vp,
+                                   _intp, _vp]),
     ("xb_rsvd_dense_streamed", _int, [_vp, _int, _i64, _i64, _vp, _i64, _u64, _int, _int, _int,
                                       _i64, _vp, _i64, _vp, _vp, _i64, _vp, _intp, _vp]),
     ("xb_comm_unique_id", _int, [_vp]),
@@ -245,6 +250,52 @@ class Context:
             self.h, dtype_code(dt), m, n, _ptr(a), lda, _ptr(om) if om is not None else None,
             int(seed) & (2**64 - 1), k, p, q, _ptr(u), k, _ptr(s), _ptr(v), k, _ptr(deficient),
             C.byref(ndef), _ptr(stages)))
+        return u, s, v, tuple(int(x) for x in deficient[: ndef.value]), stages
+
+    def rsvd_dense_tiles(self, shape, row_cuts, col_cuts, get_tile, dtype, k: int, p: int,
+                         q: int, seed: int, release=None, force_stream: bool = False):
+        """Dense A as a tile grid (xb_rsvd_dense_tiles): get_tile(ti, tj) ->
+        2-d array of the tile (any row stride, unit column stride), held
+        until the library releases it (then release(ti, tj), if given).
+        A is never assembled in host memory."""
+        m, n = shape
+        dt = np.dtype(dtype)
+        held = {}
+        errors = []
+
+        def fetch(user, ti, tj, ld_out):
+            try:
+                t = np.asarray(get_tile(int(ti), int(tj)))
+                if t.dtype != dt or t.strides[1] != dt.itemsize:
+                    t = np.ascontiguousarray(t, dtype=dt)
+                held[(int(ti), int(tj))] = t
+                ld_out[0] = t.strides[0] // dt.itemsize
+                return t.ctypes.data
+            except BaseException as e:  # noqa: BLE001 - reported as a null tile
+                errors.append(e)
+                return None
+
+        def rel(user, ti, tj):
+            held.pop((int(ti), int(tj)), None)
+            if release is not None:
+                release(int(ti), int(tj))
+
+        fetch_cb, rel_cb = TILE_FETCH(fetch), TILE_RELEASE(rel)
+        rc_ = np.ascontiguousarray(row_cuts, dtype=np.int64)
+        cc_ = np.ascontiguousarray(col_cuts, dtype=np.int64)
+        u = np.empty((m, k), dtype=dt)
+        v = np.empty((n, k), dtype=dt)
+        s = np.empty(k)
+        deficient = np.zeros(max(k + p, 1), dtype=np.int32)
+        ndef = C.c_int(0)
+        stages = np.zeros(NUM_STAGES)
+        status = self.lib.xb_rsvd_dense_tiles(
+            self.h, dtype_code(dt), m, n, _ptr(rc_), len(rc_) - 1, _ptr(cc_), len(cc_) - 1,
+            fetch_cb, rel_cb, None, int(bool(force_stream)), int(seed) & (2**64 - 1), k, p, q,
+            _ptr(u), k, _ptr(s), _ptr(v), k, _ptr(deficient), C.byref(ndef), _ptr(stages))
+        if errors:
+            raise errors[0]
+        _check(status)
         return u, s, v, tuple(int(x) for x in deficient[: ndef.value]), stages
 
     def rsvd_dense_streamed(self, a: np.ndarray, k: int, p: int, q: int, seed: int,

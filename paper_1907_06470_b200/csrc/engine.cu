@@ -628,10 +628,91 @@ void check_dims(int64_t m, int64_t n, int k, int p, int q) {
                  ")");
 }
 
+// Where a host-resident A comes from, band by band of rows. Either one
+// contiguous row-major array (the unbudgeted reference matrix is a single
+// tile) or the reference's tile grid itself, fetched tile by tile
+// through caller callbacks (a StoredMatrix of many tiles, possibly budgeted
+// or store-backed: pool.get / read_cell_dense, pool.py:397-418) — then A is
+// never assembled in host memory, and bands follow the grid's row cuts.
+struct HostSource {
+  virtual ~HostSource() {}
+  // rows of the band starting at row r0 (<= cap when possible)
+  virtual int64_t band_rows(int64_t r0, int64_t cap) const = 0;
+  // enqueue the H2D copy of rows [r0, r0 + rows) (one or more whole bands)
+  // into dst (ld elements per row) on stream s
+  virtual void copy_rows(void* dst, int64_t ld, int64_t r0, int64_t rows, cudaStream_t s) = 0;
+  // every copy enqueued so far has completed: host memory may be released
+  virtual void copies_done() {}
+  virtual bool pinned() const { return false; }
+};
+
+struct ContiguousSource final : HostSource {
+  const char* host;
+  int64_t host_ld, n;
+  size_t es;
+  ContiguousSource(const void* a, int64_t lda, int64_t cols, size_t esz)
+      : host(static_cast<const char*>(a)), host_ld(lda), n(cols), es(esz) {}
+  int64_t band_rows(int64_t, int64_t cap) const override { return cap; }
+  void copy_rows(void* dst, int64_t ld, int64_t r0, int64_t rows, cudaStream_t s) override {
+    const char* src = host + (size_t)r0 * host_ld * es;
+    if (host_ld == n && ld == n)  // contiguous rows: one linear DMA
+      XB_CUDA(cudaMemcpyAsync(dst, src, (size_t)rows * n * es, cudaMemcpyHostToDevice, s));
+    else
+      XB_CUDA(cudaMemcpy2DAsync(dst, ld * es, src, host_ld * es, n * es, rows,
+                                cudaMemcpyHostToDevice, s));
+  }
+  bool pinned() const override { return is_pinned(host); }
+};
+
+struct TileSource final : HostSource {
+  std::vector<int64_t> rcut, ccut;
+  xb_tile_fetch_fn fetch;
+  xb_tile_release_fn release;
+  void* user;
+  size_t es;
+  std::vector<std::pair<int64_t, int64_t>> held;  // fetched, not yet released
+  TileSource(const int64_t* row_cuts, int ntr, const int64_t* col_cuts, int ntc,
+             xb_tile_fetch_fn f, xb_tile_release_fn r, void* u, size_t esz)
+      : rcut(row_cuts, row_cuts + ntr + 1), ccut(col_cuts, col_cuts + ntc + 1), fetch(f),
+        release(r), user(u), es(esz) {}
+  ~TileSource() override { copies_done(); }
+  int64_t band_index(int64_t r0) const {
+    const auto it = std::upper_bound(rcut.begin(), rcut.end(), r0);
+    return (int64_t)(it - rcut.begin()) - 1;
+  }
+  int64_t band_rows(int64_t r0, int64_t) const override {
+    const int64_t ti = band_index(r0);
+    return rcut[ti + 1] - r0;
+  }
+  void copy_rows(void* dst, int64_t ld, int64_t r0, int64_t rows, cudaStream_t s) override {
+    for (int64_t r = r0; r < r0 + rows;) {
+      const int64_t ti = band_index(r);
+      XB_REQUIRE(rcut[ti] == r, XB_EVALUE, "tile source: copy not aligned to a row cut");
+      const int64_t h = rcut[ti + 1] - rcut[ti];
+      for (size_t tj = 0; tj + 1 < ccut.size(); ++tj) {
+        int64_t tld = 0;
+        const void* p = fetch(user, ti, (int64_t)tj, &tld);
+        XB_REQUIRE(p != nullptr, XB_EVALUE,
+                   "tile source: tile (" + std::to_string(ti) + ", " + std::to_string(tj) +
+                       ") unavailable");
+        held.push_back({ti, (int64_t)tj});
+        const int64_t w = ccut[tj + 1] - ccut[tj];
+        char* d = static_cast<char*>(dst) + ((size_t)(r - r0) * ld + ccut[tj]) * es;
+        XB_CUDA(cudaMemcpy2DAsync(d, ld * es, p, tld * es, w * es, h, cudaMemcpyHostToDevice, s));
+      }
+      r += h;
+    }
+  }
+  void copies_done() override {
+    if (release)
+      for (auto& t : held) release(user, t.first, t.second);
+    held.clear();
+  }
+};
+
 // Host-side description of how A reaches the device for the first product.
 struct IngestPlan {
-  const void* hostA = nullptr;  // non-null: stream row chunks H2D, overlapped
-  int64_t host_lda = 0;
+  HostSource* src = nullptr;  // non-null: stream row bands H2D, overlapped
   int64_t chunk_rows = 0;
 };
 
@@ -1020,7 +1101,7 @@ void rsvd_impl(xb_ctx* c, const AOp& op_in, int64_t m, int64_t n, const void* d_
     upd(false, n, lp, lp, false);
     upd(false, m, k, lp, false);
     upd(false, n, k, lp, false);
-    if (ing.hostA) upd(false, ing.chunk_rows, lp, n, a.f32);
+    if (ing.src) upd(false, ing.chunk_rows, lp, n, a.f32);
     if (need) c->dbuf("split", need);
     // the TSQR fallback's workspace, so no allocation lands mid-stream
     c->dbuf("tsqr_work", op_in.comm ? tsqr_sharded_work_doubles(std::max(m, n), l, op_in.comm->world)
@@ -1056,36 +1137,31 @@ void rsvd_impl(xb_ctx* c, const AOp& op_in, int64_t m, int64_t n, const void* d_
   // O*A^T: the sketch; with a host A, row chunks arrive on the copy stream and
   // each chunk's rows of Y are computed as soon as it lands.
   clk.enter(kSketch);
-  if (ing.hostA) {
+  if (ing.src) {
     cudaEvent_t t0 = nullptr, t1 = nullptr;
     XB_CUDA(cudaEventCreate(&t0));
     XB_CUDA(cudaEventCreate(&t1));
     XB_CUDA(cudaEventRecord(t0, c->cp));
     std::vector<cudaEvent_t> landed;
-    for (int64_t r0 = 0; r0 < m; r0 += ing.chunk_rows) {
-      const int64_t rows = std::min(ing.chunk_rows, m - r0);
-      const size_t es = a.esz();
-      const char* hsrc = static_cast<const char*>(ing.hostA) + (size_t)r0 * ing.host_lda * es;
-      if (ing.host_lda == n && a.ld == n)  // contiguous rows: one linear DMA
-        XB_CUDA(cudaMemcpyAsync(const_cast<void*>(a.rows_from(r0)), hsrc, (size_t)rows * n * es,
-                                cudaMemcpyHostToDevice, c->cp));
-      else
-        XB_CUDA(cudaMemcpy2DAsync(const_cast<void*>(a.rows_from(r0)), a.ld * es, hsrc,
-                                  ing.host_lda * es, n * es, rows, cudaMemcpyHostToDevice, c->cp));
+    for (int64_t r0 = 0; r0 < m;) {
+      const int64_t rows = std::min(ing.src->band_rows(r0, ing.chunk_rows), m - r0);
+      ing.src->copy_rows(const_cast<void*>(a.rows_from(r0)), a.ld, r0, rows, c->cp);
       cudaEvent_t e;
       XB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       XB_CUDA(cudaEventRecord(e, c->cp));
       XB_CUDA(cudaStreamWaitEvent(st, e, 0));
       landed.push_back(e);
       gemm_on_a(c, false, rows, lp, n, a, r0, Om, lp, Ym + r0 * lp, lp, l);
+      r0 += rows;
     }
     XB_CUDA(cudaEventRecord(t1, c->cp));
     XB_CUDA(cudaStreamSynchronize(c->cp));
+    ing.src->copies_done();
     float ms = 0.f;
     XB_CUDA(cudaEventElapsedTime(&ms, t0, t1));
     if (getenv("XB_TRACE"))
       fprintf(stderr, "[xb] ingest: %lld chunks, host pinned %d, %.1f ms (%.1f GB/s)\n",
-              (long long)landed.size(), (int)is_pinned(ing.hostA), ms,
+              (long long)landed.size(), (int)ing.src->pinned(), ms,
               (double)m * n * a.esz() / (ms * 1e-3) / 1e9);
     local_stage[kParse] += ms * 1e-3;  // ingest (H2D), overlapped with the sketch
     for (auto e : landed) cudaEventDestroy(e);
@@ -1271,20 +1347,18 @@ struct HostRegistration {
 // recomputed with one extra TN-only pass.
 struct Streamer {
   xb_ctx* c;
-  const char* host;
-  int64_t host_ld;  // elements
+  HostSource* src;
   bool f32;
-  int64_t m, n, tile_rows;
+  int64_t m, n, tile_rows;  // tile_rows: the largest band
   static constexpr int NB = 3;
   void* tiles[NB];
   cudaEvent_t landed[NB], freed[NB], t0, t1;
   double copy_seconds = 0.0;
   size_t es() const { return f32 ? 4 : 8; }
 
-  Streamer(xb_ctx* ctx, const void* a, int64_t lda, bool is_f32, int64_t rows, int64_t cols,
+  Streamer(xb_ctx* ctx, HostSource* source, bool is_f32, int64_t rows, int64_t cols,
            int64_t trows)
-      : c(ctx), host(static_cast<const char*>(a)), host_ld(lda), f32(is_f32), m(rows), n(cols),
-        tile_rows(trows) {
+      : c(ctx), src(source), f32(is_f32), m(rows), n(cols), tile_rows(trows) {
     for (int b = 0; b < NB; ++b) {
       tiles[b] = c->buf("stream_tile" + std::to_string(b), (size_t)tile_rows * n * es());
       XB_CUDA(cudaEventCreateWithFlags(&landed[b], cudaEventDisableTiming));
@@ -1302,25 +1376,27 @@ struct Streamer {
     cudaEventDestroy(t1);
   }
 
-  // Stream all row tiles; body(tile_view, r0, rows) enqueues the compute on
-  // c->st for one tile.
+  // Stream all row bands; body(tile_view, r0, rows) enqueues the compute on
+  // c->st for one band.
   template <typename F>
   void pass(F&& body) {
     XB_CUDA(cudaEventRecord(t0, c->cp));
-    const int64_t ntiles = ceil_div(m, tile_rows);
-    for (int64_t i = 0; i < ntiles; ++i) {
+    int64_t i = 0;
+    for (int64_t r0 = 0; r0 < m; ++i) {
       const int b = (int)(i % NB);
-      const int64_t r0 = i * tile_rows, rows = std::min(tile_rows, m - r0);
+      const int64_t rows = std::min(src->band_rows(r0, tile_rows), m - r0);
+      XB_REQUIRE(rows <= tile_rows, XB_EVALUE, "streamer: band taller than its buffers");
       if (i >= NB) XB_CUDA(cudaStreamWaitEvent(c->cp, freed[b], 0));
-      XB_CUDA(cudaMemcpy2DAsync(tiles[b], n * es(), host + (size_t)r0 * host_ld * es(),
-                                host_ld * es(), n * es(), rows, cudaMemcpyHostToDevice, c->cp));
+      src->copy_rows(tiles[b], n, r0, rows, c->cp);
       XB_CUDA(cudaEventRecord(landed[b], c->cp));
       XB_CUDA(cudaStreamWaitEvent(c->st, landed[b], 0));
       body(AView{tiles[b], n, f32}, r0, rows);
       XB_CUDA(cudaEventRecord(freed[b], c->st));
+      r0 += rows;
     }
     XB_CUDA(cudaEventRecord(t1, c->cp));
     XB_CUDA(cudaEventSynchronize(t1));
+    src->copies_done();
     float ms = 0.f;
     XB_CUDA(cudaEventElapsedTime(&ms, t0, t1));
     copy_seconds += ms * 1e-3;
@@ -1354,7 +1430,7 @@ int host_flag(xb_ctx* c, const int* dflag) {
   return h;
 }
 
-void rsvd_stream(xb_ctx* c, const void* hostA, int64_t host_lda, bool f32, int64_t m, int64_t n,
+void rsvd_stream(xb_ctx* c, HostSource* hsrc, bool f32, int64_t m, int64_t n,
                  int64_t tile_rows, uint64_t seed, int k, int p, int q, const RsvdOut& out,
                  int32_t* deficient, int* ndeficient, double* stage_seconds) {
   check_dims(m, n, k, p, q);
@@ -1396,7 +1472,7 @@ void rsvd_stream(xb_ctx* c, const void* hostA, int64_t host_lda, bool f32, int64
     upd(false, n, k, lp, false);
     if (need) c->dbuf("split", need);
   }
-  Streamer sm(c, hostA, host_lda, f32, m, n, tile_rows);
+  Streamer sm(c, hsrc, f32, m, n, tile_rows);
   Small s = small_bufs(c, l);
   XB_CUDA(cudaMemsetAsync(Ub, 0, (size_t)lp * lp * sizeof(double), st));
   XB_CUDA(cudaMemsetAsync(Wk, 0, (size_t)lp * kp * sizeof(double), st));
@@ -1775,6 +1851,81 @@ int xb_rsvd_dense_dev(xb_ctx* c, int dtype, int64_t m, int64_t n, const void* dA
   });
 }
 
+}  // extern "C"
+
+namespace {
+
+// One factorisation of a host-resident dense A (any HostSource) with host
+// outputs: in HBM when A fits next to the sketch buffers (bands ingested on
+// the copy stream, each band's rows of the first product computed as it
+// lands), else the out-of-core streamer (q + 1 fused passes over A).
+void rsvd_from_host(xb_ctx* c, bool f32, int64_t m, int64_t n, HostSource& src,
+                    int64_t max_band, bool force_stream, int64_t stream_rows, const void* omega,
+                    uint64_t seed, int k, int p, int q, void* U, int64_t ldu, double* s, void* V,
+                    int64_t ldv, int32_t* deficient, int* ndeficient, double* stage_seconds) {
+  const size_t es = f32 ? 4 : 8;
+  const int l = k + p;
+  const double t0 = now_s();
+  double* dU = c->dbuf("U", (size_t)m * k);
+  double* dV = c->dbuf("V", (size_t)n * k);
+  double* ds = c->dbuf("s", (size_t)k);
+  RsvdOut out{dU, k, ds, dV, k};
+  const int lp = (int)round_up(l, 8);
+  const bool stream = force_stream || !fits_in_hbm(c, m, n, es, lp);
+  double t1 = 0.0;
+  if (stream) {
+    XB_REQUIRE(omega == nullptr, XB_EUNSUPPORTED,
+               "an explicit Omega is not supported by the out-of-core streamer");
+    int64_t tr = max_band > 0 ? max_band
+                 : stream_rows > 0 ? std::min<int64_t>(stream_rows, m)
+                                   : auto_tile_rows(m, n, es);
+    t1 = now_s();
+    rsvd_stream(c, &src, f32, m, n, tr, seed, k, p, q, out, deficient, ndeficient, stage_seconds);
+  } else {
+    void* dA = c->buf("A", (size_t)m * n * es);
+    void* dO = nullptr;
+    if (omega) {
+      dO = c->buf("omega_in", (size_t)n * l * es);
+      XB_CUDA(cudaMemcpyAsync(dO, omega, (size_t)n * l * es, cudaMemcpyHostToDevice, c->st));
+    }
+    IngestPlan ing;
+    ing.src = &src;
+    if (max_band > 0) {
+      ing.chunk_rows = max_band;  // the tile grid's row bands
+    } else {
+      // ~1 GiB chunks, at least 8 of them when the matrix is large
+      int64_t rows =
+          std::max<int64_t>(256, ((int64_t)1 << 30) / std::max<int64_t>(n * (int64_t)es, 1));
+      rows = std::min(rows, std::max<int64_t>(256, round_up(ceil_div(m, 8), 128)));
+      ing.chunk_rows = std::min(rows, m);
+    }
+    t1 = now_s();
+    AOp op;
+    op.dense = AView{dA, n, f32};
+    rsvd_impl(c, op, m, n, dO, l, seed, k, p, q, out, deficient, ndeficient, stage_seconds, ing);
+  }
+  const double t2 = now_s();
+  void* oU = dU;
+  void* oV = dV;
+  if (f32) {
+    oU = c->buf("U32", (size_t)m * k * 4);
+    oV = c->buf("V32", (size_t)n * k * 4);
+    launch_copy2d_cast<double, float>(dU, m, k, k, static_cast<float*>(oU), k, c->st);
+    launch_copy2d_cast<double, float>(dV, n, k, k, static_cast<float*>(oV), k, c->st);
+  }
+  XB_CUDA(cudaMemcpyAsync(s, ds, k * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  d2h_rows(c, U, ldu * es, oU, k * es, k * es, m);
+  d2h_rows(c, V, ldv * es, oV, k * es, k * es, n);
+  XB_CUDA(cudaStreamSynchronize(c->st));
+  if (getenv("XB_TRACE"))
+    fprintf(stderr, "[xb] rsvd host A: setup %.1f ms, ingest+compute %.1f ms, d2h %.1f ms\n",
+            (t1 - t0) * 1e3, (t2 - t1) * 1e3, (now_s() - t2) * 1e3);
+}
+
+}  // namespace
+
+extern "C" {
+
 int xb_rsvd_dense(xb_ctx* c, int dtype, int64_t m, int64_t n, const void* A, int64_t lda,
                   const void* omega, uint64_t seed, int k, int p, int q, void* U, int64_t ldu,
                   double* s, void* V, int64_t ldv, int32_t* deficient, int* ndeficient,
@@ -1787,62 +1938,39 @@ int xb_rsvd_dense(xb_ctx* c, int dtype, int64_t m, int64_t n, const void* A, int
     check_dims(m, n, k, p, q);
     XB_REQUIRE(A && U && s && V, XB_EVALUE, "null buffer");
     XB_REQUIRE(lda >= n && ldu >= k && ldv >= k, XB_EVALUE, "leading dimension too small");
-    const int l = k + p;
-    const double t0 = now_s();
     HostRegistration reg(A, (size_t)((m - 1) * lda + n) * es);
-    double* dU = c->dbuf("U", (size_t)m * k);
-    double* dV = c->dbuf("V", (size_t)n * k);
-    double* ds = c->dbuf("s", (size_t)k);
-    RsvdOut out{dU, k, ds, dV, k};
-    // out of core when A does not fit in HBM next to the sketch buffers (or
-    // when streaming is forced): the tile streamer, q + 1 host passes
-    const int lp = (int)round_up(l, 8);
-    const bool stream = g_force_stream_rows >= 0 || !fits_in_hbm(c, m, n, es, lp);
-    double t1 = 0.0;
-    if (stream) {
-      XB_REQUIRE(omega == nullptr, XB_EUNSUPPORTED,
-                 "an explicit Omega is not supported by the out-of-core streamer");
-      const int64_t tr = g_force_stream_rows > 0 ? std::min<int64_t>(g_force_stream_rows, m)
-                                                 : auto_tile_rows(m, n, es);
-      t1 = now_s();
-      rsvd_stream(c, A, lda, f32, m, n, tr, seed, k, p, q, out, deficient, ndeficient,
-                  stage_seconds);
-    } else {
-      void* dA = c->buf("A", (size_t)m * n * es);
-      void* dO = nullptr;
-      if (omega) {
-        dO = c->buf("omega_in", (size_t)n * l * es);
-        XB_CUDA(cudaMemcpyAsync(dO, omega, (size_t)n * l * es, cudaMemcpyHostToDevice, c->st));
-      }
-      IngestPlan ing;
-      ing.hostA = A;
-      ing.host_lda = lda;
-      // ~1 GiB chunks, at least 8 of them when the matrix is large
-      int64_t rows =
-          std::max<int64_t>(256, ((int64_t)1 << 30) / std::max<int64_t>(n * (int64_t)es, 1));
-      rows = std::min(rows, std::max<int64_t>(256, round_up(ceil_div(m, 8), 128)));
-      ing.chunk_rows = std::min(rows, m);
-      t1 = now_s();
-      AOp op;
-      op.dense = AView{dA, n, f32};
-      rsvd_impl(c, op, m, n, dO, l, seed, k, p, q, out, deficient, ndeficient, stage_seconds, ing);
+    ContiguousSource src(A, lda, n, es);
+    rsvd_from_host(c, f32, m, n, src, 0, g_force_stream_rows >= 0, g_force_stream_rows, omega,
+                   seed, k, p, q, U, ldu, s, V, ldv, deficient, ndeficient, stage_seconds);
+  });
+}
+
+int xb_rsvd_dense_tiles(xb_ctx* c, int dtype, int64_t m, int64_t n, const int64_t* row_cuts,
+                        int ntr, const int64_t* col_cuts, int ntc, xb_tile_fetch_fn fetch,
+                        xb_tile_release_fn release, void* user, int force_stream, uint64_t seed,
+                        int k, int p, int q, void* U, int64_t ldu, double* s, void* V,
+                        int64_t ldv, int32_t* deficient, int* ndeficient,
+                        double* stage_seconds) {
+  return guarded([&] {
+    XB_REQUIRE(c, XB_EVALUE, "null context");
+    LaunchScope ls(c);
+    const bool f32 = check_dtype(dtype);
+    check_dims(m, n, k, p, q);
+    XB_REQUIRE(U && s && V && fetch && row_cuts && col_cuts && ntr >= 1 && ntc >= 1, XB_EVALUE,
+               "null argument");
+    XB_REQUIRE(ldu >= k && ldv >= k, XB_EVALUE, "leading dimension too small");
+    XB_REQUIRE(row_cuts[0] == 0 && row_cuts[ntr] == m && col_cuts[0] == 0 && col_cuts[ntc] == n,
+               XB_ESHAPE, "tile cuts must span the matrix");
+    int64_t band = 0;
+    for (int i = 0; i < ntr; ++i) {
+      XB_REQUIRE(row_cuts[i + 1] > row_cuts[i], XB_ESHAPE, "row cuts must increase");
+      band = std::max(band, row_cuts[i + 1] - row_cuts[i]);
     }
-    const double t2 = now_s();
-    void* oU = dU;
-    void* oV = dV;
-    if (f32) {
-      oU = c->buf("U32", (size_t)m * k * 4);
-      oV = c->buf("V32", (size_t)n * k * 4);
-      launch_copy2d_cast<double, float>(dU, m, k, k, static_cast<float*>(oU), k, c->st);
-      launch_copy2d_cast<double, float>(dV, n, k, k, static_cast<float*>(oV), k, c->st);
-    }
-    XB_CUDA(cudaMemcpyAsync(s, ds, k * sizeof(double), cudaMemcpyDeviceToHost, c->st));
-    d2h_rows(c, U, ldu * es, oU, k * es, k * es, m);
-    d2h_rows(c, V, ldv * es, oV, k * es, k * es, n);
-    XB_CUDA(cudaStreamSynchronize(c->st));
-    if (getenv("XB_TRACE"))
-      fprintf(stderr, "[xb] rsvd_dense host: setup %.1f ms, ingest+compute %.1f ms, d2h %.1f ms\n",
-              (t1 - t0) * 1e3, (t2 - t1) * 1e3, (now_s() - t2) * 1e3);
+    for (int j = 0; j < ntc; ++j)
+      XB_REQUIRE(col_cuts[j + 1] > col_cuts[j], XB_ESHAPE, "column cuts must increase");
+    TileSource src(row_cuts, ntr, col_cuts, ntc, fetch, release, user, f32 ? 4 : 8);
+    rsvd_from_host(c, f32, m, n, src, band, force_stream != 0, 0, nullptr, seed, k, p, q, U, ldu,
+                   s, V, ldv, deficient, ndeficient, stage_seconds);
   });
 }
 

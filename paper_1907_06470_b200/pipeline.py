@@ -152,6 +152,44 @@ def _dense_input(a) -> np.ndarray:
     return np.ascontiguousarray(stored_to_array(a))
 
 
+def _single_tile(a) -> bool:
+    d = a.desc
+    return not d.transposed and d.partition.n_row_tiles == 1 and d.partition.n_col_tiles == 1
+
+
+def _tile_grid(a):
+    """(row cuts, col cuts, get_tile, release) of A's tile grid as the
+    library streams it: tiles come from the caller's pool one at a time
+    (pinned while the library holds them, so a budgeted pool cannot evict
+    them mid-copy) and are never assembled into one host array. A transposed
+    view's tile (ti, tj) is the stored tile (tj, ti), transposed."""
+    d = a.desc
+    pool, mid = a.pool, d.matrix_id
+    part = d.partition
+    rows, cols = tuple(part.row_cuts), tuple(part.col_cuts)
+    if d.transposed:
+        rows, cols = cols, rows
+    unpin = getattr(pool, "unpin", None)
+
+    def key(ti, tj):
+        return (tj, ti) if d.transposed else (ti, tj)
+
+    def get_tile(ti, tj):
+        si, sj = key(ti, tj)
+        try:
+            block = pool.get(mid, si, sj, pin=True)
+        except TypeError:  # a pool without pinning
+            block = pool.get(mid, si, sj)
+        vals = np.asarray(block.values)
+        return np.ascontiguousarray(vals.T) if d.transposed else vals
+
+    def release(ti, tj):
+        if unpin is not None:
+            unpin(mid, *key(ti, tj))
+
+    return rows, cols, get_tile, release
+
+
 def randomized_svd(pool, a, config: RsvdConfig, *, threads: int = 1, runner=None, clock=None):
     """Rank-k randomized factorisation A ~ U diag(s) V^T on the GPU."""
     m, n = a.shape
@@ -232,10 +270,17 @@ def _rsvd_device(a, config, precision, clock):
                 config.oversample, q, config.seed, omega=omega)
             u = u.astype(precision.storage_dtype, copy=False)
             v = v.astype(precision.storage_dtype, copy=False)
-        else:
+        elif _single_tile(a):
             host = _dense_input(a).astype(precision.storage_dtype, copy=False)
             u, s, v, deficient, stages = ctx.rsvd_dense(host, config.rank, config.oversample, q,
                                                         config.seed)
+        else:
+            # a tile grid (budgeted / store-backed / partitioned A, or a
+            # transposed view): streamed tile by tile, never assembled
+            rows, cols, get_tile, release = _tile_grid(a)
+            u, s, v, deficient, stages = ctx.rsvd_dense_tiles(
+                tuple(a.shape), rows, cols, get_tile, precision.storage_dtype, config.rank,
+                config.oversample, q, config.seed, release=release)
     finally:
         ctx.set_gram_path(False)  # context state must not leak into other calls
     chosen_q = ctx.last_power()[0] if auto else int(config.power)
@@ -270,9 +315,13 @@ def auto_select_q(pool, a, rank, *, q_max: int = 5, tau: float = 1e-6, seed: int
             omega = ctx.gaussian(seed, 0, n, rank, dtype=np.float32).astype(np.float64)
         ctx.rsvd_coo(rows, cols, np.asarray(vals, dtype=np.float64), tuple(a.shape), rank, 0,
                      _lib.POWER_AUTO, seed, omega=omega)
-    else:
+    elif _single_tile(a):
         host = _dense_input(a).astype(precision.storage_dtype, copy=False)
         ctx.rsvd_dense(host, rank, 0, _lib.POWER_AUTO, seed)
+    else:
+        rows, cols, get_tile, release = _tile_grid(a)
+        ctx.rsvd_dense_tiles(tuple(a.shape), rows, cols, get_tile, precision.storage_dtype, rank,
+                             0, _lib.POWER_AUTO, seed, release=release)
     return ctx.last_power()[0]
 
 

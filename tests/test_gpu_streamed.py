@@ -81,3 +81,46 @@ def test_streamed_gram_path_matches_oracle(lib):
     # sigma is compared relative to sigma_1
     assert np.max(np.abs(s - ref.s)) / ref.s[0] <= 1e-10
     assert M.sin_angle(u, ref.u) <= 1e-8 and M.sin_angle(v, ref.v) <= 1e-8
+
+
+@pytest.mark.parametrize("grid,transposed,stream", [((5, 3), False, False), ((7, 2), False, True),
+                                                    ((3, 4), True, False), ((4, 4), True, True)])
+def test_tile_grid_source_matches_oracle(lib, grid, transposed, stream):
+    """A as the reference's tile grid (xb_rsvd_dense_tiles): tiles fetched one
+    at a time from the pool and never assembled into one host array — in HBM
+    (bands ingested as they land) or streamed (q + 1 fused passes over the
+    grid) — including a transposed view, whose tile (ti, tj) is the stored
+    (tj, ti) transposed (pool.py:390-418)."""
+    import paper_1907_06470_b200 as X
+    from paper_1907_06470_b200.pipeline import _tile_grid
+    from paper_1907_06470_b200.workloads import dense_lowrank_np
+
+    arr = dense_lowrank_np(3000, 1300, "pow-1.5", 1e-8, 51, 52)
+    pool = X.BlockPool()
+    base = arr.T.copy() if transposed else arr
+    ma = X.matrix_from_dense(pool, "A", base, precision=X.Precision.DOUBLE, grid=grid)
+    a = ma.T if transposed else ma
+    assert a.shape == arr.shape
+    rows, cols, get_tile, release = _tile_grid(a)
+    u, s, v, _, stages = lib.rsvd_dense_tiles(a.shape, rows, cols, get_tile, np.float64, 50, 10,
+                                              2, 7, release=release, force_stream=stream)
+    ref = OP.rsvd_reorth(arr, 50, 10, 2, 7, "double", fast=True)
+    assert M.sigma_rel(s, ref.s) <= 1e-10
+    assert M.sin_angle(u, ref.u) <= 1e-8 and M.sin_angle(v, ref.v) <= 1e-8
+    assert stages[0] > 0
+
+
+def test_budgeted_store_backed_tiles_through_drop_in(lib, tmp_path):
+    """A budgeted pool over a BlockStore (tiles spill to the workdir and come
+    back on demand, pool.py:189-221): randomized_svd streams the tile grid
+    from the pool — the path a matrix larger than host RAM takes."""
+    import paper_1907_06470_b200 as X
+    from paper_1907_06470_b200.workloads import dense_lowrank_np
+
+    arr = dense_lowrank_np(2400, 900, "geom0.9", 1e-8, 53, 54)
+    pool = X.BlockPool(X.BlockStore(str(tmp_path)))
+    ma = X.matrix_from_dense(pool, "A", arr, precision=X.Precision.DOUBLE, grid=(6, 3))
+    res = X.randomized_svd(pool, ma, X.RsvdConfig(rank=20, oversample=10, power=2, seed=3))
+    ref = OP.rsvd_reorth(arr, 20, 10, 2, 3, "double", fast=True)
+    assert M.sigma_rel(res.s, ref.s) <= 1e-10
+    assert M.sin_angle(res.u.to_array(), ref.u) <= 1e-8
