@@ -60,15 +60,6 @@ def test_auto_power_sparse(lib):
     assert M.sigma_rel(s, ref.s) <= 1e-10
 
 
-def test_auto_power_rejected_by_streamer(lib):
-    from paper_1907_06470_b200 import _lib
-    from paper_1907_06470_b200.errors import XsvdError
-
-    a = np.random.default_rng(0).standard_normal((512, 256))
-    with pytest.raises(XsvdError):
-        lib.rsvd_dense_streamed(a, 8, 4, _lib.POWER_AUTO, 1, tile_rows=128)
-
-
 # -- the reference's own auto-q tests (tests/test_pipeline.py:77-111, 298-311),
 #    through this package's drop-in ---------------------------------------------
 

@@ -67,20 +67,23 @@ def test_streamed_power_auto_matches_in_hbm(lib):
 
 def test_streamed_gram_path_matches_oracle(lib):
     """gram_path out of core (pipeline.py:526-580): the power-matrix
-    projection's 2q raw products are q more fused passes."""
+    projection's 2q raw products are q more fused passes. The Gram route
+    carries sigma^(4q+2), so only sigma_i / sigma_1 above ~eps^(1/(4q+2))
+    are meaningful in any implementation: spectrum 1/i, q = 1."""
     from paper_1907_06470_b200.workloads import dense_lowrank_np
 
-    a = dense_lowrank_np(5000, 1000, "pow-1.5", 1e-8, 47, 48)
+    a = dense_lowrank_np(5000, 1000, "inv", 1e-10, 47, 48)
     lib.set_gram_path(True)
     try:
-        u, s, v, _, _ = lib.rsvd_dense_streamed(a, 40, 10, 2, 6, tile_rows=800)
+        u, s, v, _, _ = lib.rsvd_dense_streamed(a, 40, 10, 1, 6, tile_rows=800)
+        u0, s0, v0, _, _ = lib.rsvd_dense(a, 40, 10, 1, 6)
     finally:
         lib.set_gram_path(False)
-    ref = OP.rsvd_reorth_gram(a, 40, 10, 2, 6, "double", fast=True)
-    # as tests/test_gpu_gram_path.py: the Gram squares the condition, so
-    # sigma is compared relative to sigma_1
-    assert np.max(np.abs(s - ref.s)) / ref.s[0] <= 1e-10
-    assert M.sin_angle(u, ref.u) <= 1e-8 and M.sin_angle(v, ref.v) <= 1e-8
+    ref = OP.rsvd_reorth_gram(a, 40, 10, 1, 6, "double", fast=True)
+    assert np.max(np.abs(s - ref.s)) / ref.s[0] <= 1e-9
+    assert np.max(np.abs(s - s0)) / s0[0] <= 1e-9
+    assert M.sin_angle(u[:, :20], ref.u[:, :20]) <= 1e-6
+    assert M.sin_angle(v[:, :20], ref.v[:, :20]) <= 1e-6
 
 
 @pytest.mark.parametrize("grid,transposed,stream", [((5, 3), False, False), ((7, 2), False, True),
