@@ -819,7 +819,7 @@ def run_ours(args):
             # the headline is a pageable numpy A, as an xsvd caller passes it
             # (registered by the library for the call); pinned beside it
             p_s, p_ingest = timed(pinned=True)
-            e2e["host_memory"] = "pageable numpy array (cudaHostRegister per call)"
+            e2e["host_memory"] = "pageable numpy array (staged by the library: host worker threads into a pinned ring, DMA behind them)"
             e2e["pinned"] = {"value": case.units / p_s, "seconds": p_s, "ingest_s": p_ingest}
     elif args.e2e_steps > 0 and hasattr(case, "e2e_sharded"):
         e2e = case.e2e_sharded(args.e2e_steps, dist, device)

@@ -30,7 +30,7 @@ FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-I
 # Experiment build (tools/ probes): XB_* tuning and timing-only debug knobs are
 # read from the environment. The release library (default) ignores them.
 if os.environ.get("XB_BUILD_EXPERIMENTS") == "1":
-    FLAGS = FLAGS + ["-DXB_EXPERIMENTS"]
+    FLAGS = FLAGS + ["-DXB_EXPERIMENTS"] + os.environ.get("XB_BUILD_DEFINES", "").split()
 
 
 def sources():

@@ -21,6 +21,8 @@
 // trip; stage times come from CUDA events on the compute stream.
 #include <algorithm>
 #include <chrono>
+#include <condition_variable>
+#include <mutex>
 #include <cstdlib>
 #include <cfloat>
 #include <cstring>
@@ -33,7 +35,116 @@
 
 namespace xb {
 thread_local int64_t* g_launch_counter = nullptr;
-}
+
+// Pageable host -> device copies at the link rate. An xsvd caller hands over
+// plain numpy arrays: pinning 8 GiB per call (cudaHostRegister + unregister)
+// costs more than twice the DMA itself, and a pageable cudaMemcpy is staged by
+// the driver on one thread. Here worker threads copy slices of the caller's
+// rows into a ring of pinned slots; each slot's DMA runs while the next slots
+// fill, so the copy proceeds at min(host memcpy rate, link rate).
+struct HostStager {
+  static constexpr int kSlots = 4;
+  static constexpr size_t kSlot = (size_t)64 << 20;
+  static constexpr size_t kPiece = (size_t)2 << 20;
+  struct Task {
+    char* dst;
+    const char* src;
+    size_t dpitch, spitch, width;
+    int64_t rows;
+  };
+  char* ring = nullptr;
+  cudaEvent_t ev[kSlots] = {nullptr, nullptr, nullptr, nullptr};
+  bool used[kSlots] = {false, false, false, false};
+  int next = 0;
+  std::vector<std::thread> workers;
+  std::mutex mu;
+  std::condition_variable cv_work, cv_done;
+  std::vector<Task> tasks;
+  size_t head = 0;
+  int running = 0;
+  bool stop = false;
+
+  explicit HostStager(int nthreads) {
+    XB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ring), kSlots * kSlot, cudaHostAllocDefault));
+    for (auto& e : ev) XB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (int t = 0; t < nthreads; ++t) workers.emplace_back([this] { work(); });
+  }
+  ~HostStager() {
+    {
+      std::lock_guard<std::mutex> g(mu);
+      stop = true;
+    }
+    cv_work.notify_all();
+    for (auto& t : workers) t.join();
+    for (auto e : ev)
+      if (e) cudaEventDestroy(e);
+    if (ring) cudaFreeHost(ring);
+  }
+  void work() {
+    std::unique_lock<std::mutex> lk(mu);
+    for (;;) {
+      cv_work.wait(lk, [this] { return stop || head < tasks.size(); });
+      if (stop) return;
+      const Task t = tasks[head++];
+      ++running;
+      lk.unlock();
+      if (t.dpitch == t.width && t.spitch == t.width) {
+        std::memcpy(t.dst, t.src, t.width * (size_t)t.rows);
+      } else {
+        for (int64_t r = 0; r < t.rows; ++r)
+          std::memcpy(t.dst + (size_t)r * t.dpitch, t.src + (size_t)r * t.spitch, t.width);
+      }
+      lk.lock();
+      if (--running == 0 && head == tasks.size()) cv_done.notify_all();
+    }
+  }
+  void run(std::vector<Task>&& ts) {
+    std::unique_lock<std::mutex> lk(mu);
+    tasks = std::move(ts);
+    head = 0;
+    cv_work.notify_all();
+    cv_done.wait(lk, [this] { return head == tasks.size() && running == 0; });
+    tasks.clear();
+    head = 0;
+  }
+  // rows [0, rows) of a pageable host matrix (width bytes per row, spitch
+  // apart) -> device rows dpitch apart, enqueued on stream s; the host side
+  // of every slot has completed on return, the last DMAs may be in flight
+  void copy(char* dst, size_t dpitch, const char* src, size_t spitch, size_t width, int64_t rows,
+            cudaStream_t s) {
+    XB_REQUIRE(width <= kSlot, XB_EUNSUPPORTED, "host stager: row wider than a staging slot");
+    const int64_t per_slot = std::max<int64_t>(1, (int64_t)(kSlot / width));
+    for (int64_t r0 = 0; r0 < rows; r0 += per_slot) {
+      const int64_t h = std::min(per_slot, rows - r0);
+      const int slot = next;
+      next = (next + 1) % kSlots;
+      if (used[slot]) XB_CUDA(cudaEventSynchronize(ev[slot]));
+      char* buf = ring + (size_t)slot * kSlot;
+      const char* sp = src + (size_t)r0 * spitch;
+      std::vector<Task> ts;
+      if (spitch == width) {  // contiguous rows: flat byte pieces
+        const size_t total = (size_t)h * width;
+        for (size_t o = 0; o < total; o += kPiece)
+          ts.push_back({buf + o, sp + o, std::min(kPiece, total - o), std::min(kPiece, total - o),
+                        std::min(kPiece, total - o), 1});
+      } else {
+        const int64_t rp = std::max<int64_t>(1, (int64_t)(kPiece / width));
+        for (int64_t r = 0; r < h; r += rp)
+          ts.push_back({buf + (size_t)r * width, sp + (size_t)r * spitch, width, spitch, width,
+                        std::min(rp, h - r)});
+      }
+      run(std::move(ts));
+      char* dp = dst + (size_t)r0 * dpitch;
+      if (dpitch == width)
+        XB_CUDA(cudaMemcpyAsync(dp, buf, (size_t)h * width, cudaMemcpyHostToDevice, s));
+      else
+        XB_CUDA(cudaMemcpy2DAsync(dp, dpitch, buf, width, width, h, cudaMemcpyHostToDevice, s));
+      XB_CUDA(cudaEventRecord(ev[slot], s));
+      used[slot] = true;
+    }
+  }
+};
+}  // namespace xb
 
 using namespace xb;
 
@@ -155,6 +266,9 @@ struct xb_ctx {
   cudaStream_t cs = nullptr;
   std::vector<cudaEvent_t> xev;
   int world = 1, rank = 0;
+  // pageable-host -> device staging (worker threads + pinned ring), created
+  // on first use
+  xb::HostStager* stager = nullptr;
   // pinned staging for device -> pageable-host copies (two ping-pong halves)
   void* stage_host = nullptr;
   size_t stage_bytes = 0;
@@ -644,24 +758,71 @@ struct HostSource {
   // every copy enqueued so far has completed: host memory may be released
   virtual void copies_done() {}
   virtual bool pinned() const { return false; }
+  virtual bool staged() const { return false; }
+  // called once before the first copy: `streamed` = A will be read q + 1
+  // times by the out-of-core streamer, else once into HBM
+  virtual void prepare(xb_ctx*, bool /*streamed*/, int64_t /*m*/) {}
 };
+
+// worker threads of the pageable-host staging ring
+int stage_threads() {
+  static const int n = [] {
+    const char* e = knob("XB_STAGE_THREADS");
+    if (e && atoi(e) > 0) return std::min(64, atoi(e));
+    const unsigned hc = std::thread::hardware_concurrency();
+    return (int)std::max(2u, std::min(16u, hc ? hc : 8u));
+  }();
+  return n;
+}
 
 struct ContiguousSource final : HostSource {
   const char* host;
   int64_t host_ld, n;
   size_t es;
+  xb_ctx* ctx = nullptr;
+  bool is_pinned_ = false, stage = false;
+  void* registered = nullptr;
   ContiguousSource(const void* a, int64_t lda, int64_t cols, size_t esz)
-      : host(static_cast<const char*>(a)), host_ld(lda), n(cols), es(esz) {}
+      : host(static_cast<const char*>(a)), host_ld(lda), n(cols), es(esz) {
+    is_pinned_ = is_pinned(host);
+  }
+  ~ContiguousSource() override {
+    if (registered) cudaHostUnregister(registered);
+  }
+  // A pageable source: the out-of-core streamer reads A q + 1 times, so it
+  // is page-locked once for the call; a single in-HBM ingest goes through
+  // the staging ring instead (registration costs more than the copy).
+  void prepare(xb_ctx* c, bool streamed, int64_t m) override {
+    if (is_pinned_ || m <= 0) return;
+    const size_t bytes = (size_t)((m - 1) * host_ld + n) * es;
+    if (streamed || (size_t)n * es > HostStager::kSlot || bytes < ((size_t)32 << 20)) {
+      if (streamed && cudaHostRegister(const_cast<char*>(host), bytes, cudaHostRegisterDefault) ==
+                          cudaSuccess) {
+        registered = const_cast<char*>(host);
+        is_pinned_ = true;
+      } else {
+        cudaGetLastError();  // pageable copies
+      }
+      return;
+    }
+    if (!c->stager) c->stager = new HostStager(stage_threads());
+    ctx = c;
+    stage = true;
+  }
   int64_t band_rows(int64_t, int64_t cap) const override { return cap; }
   void copy_rows(void* dst, int64_t ld, int64_t r0, int64_t rows, cudaStream_t s) override {
     const char* src = host + (size_t)r0 * host_ld * es;
-    if (host_ld == n && ld == n)  // contiguous rows: one linear DMA
+    if (stage)
+      ctx->stager->copy(static_cast<char*>(dst), (size_t)ld * es, src, (size_t)host_ld * es,
+                        (size_t)n * es, rows, s);
+    else if (host_ld == n && ld == n)  // contiguous rows: one linear DMA
       XB_CUDA(cudaMemcpyAsync(dst, src, (size_t)rows * n * es, cudaMemcpyHostToDevice, s));
     else
       XB_CUDA(cudaMemcpy2DAsync(dst, ld * es, src, host_ld * es, n * es, rows,
                                 cudaMemcpyHostToDevice, s));
   }
-  bool pinned() const override { return is_pinned(host); }
+  bool pinned() const override { return is_pinned_; }
+  bool staged() const override { return stage; }
 };
 
 struct TileSource final : HostSource {
@@ -1160,8 +1321,8 @@ void rsvd_impl(xb_ctx* c, const AOp& op_in, int64_t m, int64_t n, const void* d_
     float ms = 0.f;
     XB_CUDA(cudaEventElapsedTime(&ms, t0, t1));
     if (getenv("XB_TRACE"))
-      fprintf(stderr, "[xb] ingest: %lld chunks, host pinned %d, %.1f ms (%.1f GB/s)\n",
-              (long long)landed.size(), (int)ing.src->pinned(), ms,
+      fprintf(stderr, "[xb] ingest: %lld chunks, host pinned %d staged %d, %.1f ms (%.1f GB/s)\n",
+              (long long)landed.size(), (int)ing.src->pinned(), (int)ing.src->staged(), ms,
               (double)m * n * a.esz() / (ms * 1e-3) / 1e9);
     local_stage[kParse] += ms * 1e-3;  // ingest (H2D), overlapped with the sketch
     for (auto e : landed) cudaEventDestroy(e);
@@ -1316,20 +1477,6 @@ void rsvd_impl(xb_ctx* c, const AOp& op_in, int64_t m, int64_t n, const void* d_
     for (int i = 0; i < hdef[0] && i < l; ++i) deficient[i] = hdef[1 + i];
   XB_REQUIRE(hstat == 0, XB_ECONV, "Jacobi SVD of the projected factor did not converge in 60 sweeps");
 }
-
-struct HostRegistration {
-  void* p = nullptr;
-  HostRegistration(const void* ptr, size_t bytes) {
-    if (!ptr || bytes == 0 || is_pinned(ptr)) return;
-    if (cudaHostRegister(const_cast<void*>(ptr), bytes, cudaHostRegisterDefault) == cudaSuccess)
-      p = const_cast<void*>(ptr);
-    else
-      cudaGetLastError();  // fall back to pageable copies
-  }
-  ~HostRegistration() {
-    if (p) cudaHostUnregister(p);
-  }
-};
 
 // ---- out-of-core: the pinned-host tile streamer (S1) ---------------------------
 //
@@ -1729,6 +1876,7 @@ int xb_destroy(xb_ctx* c) {
     for (auto& kv : c->bufs) cudaFree(kv.second.p);
     for (auto e : c->events) cudaEventDestroy(e);
     if (c->stage_host) cudaFreeHost(c->stage_host);
+    delete c->stager;
     delete c->comm;
     if (c->cs) {
       cudaStreamSynchronize(c->cs);
@@ -1872,6 +2020,7 @@ void rsvd_from_host(xb_ctx* c, bool f32, int64_t m, int64_t n, HostSource& src,
   RsvdOut out{dU, k, ds, dV, k};
   const int lp = (int)round_up(l, 8);
   const bool stream = force_stream || !fits_in_hbm(c, m, n, es, lp);
+  src.prepare(c, stream, m);
   double t1 = 0.0;
   if (stream) {
     XB_REQUIRE(omega == nullptr, XB_EUNSUPPORTED,
@@ -1938,7 +2087,6 @@ int xb_rsvd_dense(xb_ctx* c, int dtype, int64_t m, int64_t n, const void* A, int
     check_dims(m, n, k, p, q);
     XB_REQUIRE(A && U && s && V, XB_EVALUE, "null buffer");
     XB_REQUIRE(lda >= n && ldu >= k && ldv >= k, XB_EVALUE, "leading dimension too small");
-    HostRegistration reg(A, (size_t)((m - 1) * lda + n) * es);
     ContiguousSource src(A, lda, n, es);
     rsvd_from_host(c, f32, m, n, src, 0, g_force_stream_rows >= 0, g_force_stream_rows, omega,
                    seed, k, p, q, U, ldu, s, V, ldv, deficient, ndeficient, stage_seconds);

@@ -19,6 +19,7 @@
 #include <cfloat>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <vector>
 
 #include "common.cuh"
@@ -547,6 +548,293 @@ __global__ void __launch_bounds__(kThreads, 1)
   jacobi_tail_1cta(X, J, l, k, Ub, ldu, s_out, Wk, ldw, gnorm, gperm, gsign);
 }
 
+// ---------------------------------------------------------------------------
+// Cluster one-sided Jacobi (l <= 128): the single-CTA kernel above is bound by
+// one SM's FP64 issue rate and its per-round latency chain (3.4 us per round
+// at l = 120: 6 sweeps x 119 rounds = 2.4 ms). Here the l/2 column pairs of a
+// round are spread over a thread-block cluster of kJC CTAs as a Brent-Luk
+// systolic array: every CTA owns S consecutive SEATS (a top and a bottom
+// column each, X and J side by side in its shared memory), one warp per seat.
+// A round is: load the seat's two columns (local shared memory), the three dot
+// products, the rotation in registers, then STORE the rotated columns straight
+// into the seats they occupy next round — the neighbour's shared memory
+// through DSMEM where the seat belongs to another CTA (two columns per CTA
+// boundary per round) — into the other half of a ping-pong buffer, and one
+// cluster barrier. Seat movement is the circle method: top[0] fixed,
+// top[i] -> top[i+1], top[P-1] -> bottom[P-1], bottom[i] -> bottom[i-1],
+// bottom[0] -> top[1]; after 2P-1 rounds every pair has met once and every
+// column is back in its first seat. Column identities travel with the data
+// so that the tail's stable sort sees the original column order.
+
+// NR: doubles per lane per column (column length padded to 32 NR; a lane
+// holds rows 2 lane + 64 i + {0, 1}: 16-byte shared-memory accesses).
+//
+// A sweep ends the iteration when none of its rotations was larger than
+// thr = sqrt(tol / 4l): by the quadratic convergence of the method the
+// off-diagonal cosines left behind are then O(l thr^2) <= tol, which is what
+// the extra rotation-free sweep of the single-CTA kernels verifies — one
+// sweep in seven at l = 120.
+//
+// Measured alternatives (profiles/r02_jacobi_cluster.md): seat-to-seat
+// mbarriers instead of the cluster barrier (arrive.release.cluster per lane:
+// slower; st.async + complete_tx: every byte crosses the cluster network,
+// slower at l = 120, 10-20 % faster at l <= 64).
+template <int NR>
+__global__ void __launch_bounds__(256, 1)
+    jacobi_cluster_kernel(const double* __restrict__ Rm, int64_t ldr, int l, int k,
+                          double* __restrict__ Ub, int64_t ldu, double* __restrict__ s_out,
+                          double* __restrict__ Wk, int64_t ldw, double* work,
+                          int* __restrict__ status, double tol, int max_sweeps) {
+  static_assert(NR % 2 == 0, "two doubles per access");
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  constexpr int LP = 32 * NR;  // padded column length; rows >= l stay zero
+  constexpr int NV = NR / 2;
+  extern __shared__ __align__(16) double sm[];
+  __shared__ int s_id[2][2][8];
+  __shared__ int s_rot[2];
+  __shared__ int s_perm[128];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int rank = (int)cluster.block_rank();
+  const int nc = (int)cluster.num_blocks();
+  const int L2 = l + (l & 1), P = L2 / 2;
+  const int S = (P + nc - 1) / nc;  // seats per CTA (<= 8 for l <= 128)
+  const int seat = rank * S + warp;
+  const bool active = warp < S && seat < P;
+  // column slot (buffer, row 0 top / 1 bottom, local seat): X then J
+  auto slot = [&](int buf, int row, int ls) -> double* {
+    return sm + (int64_t)((buf * 2 + row) * S + ls) * (2 * LP);
+  };
+  const int64_t ll = (int64_t)l * l;
+  double* Xg = work;  // final columns by original index (tail)
+  double* Jg = work + ll;
+  double* gnorm = work + 2 * ll;
+  int* gsign = reinterpret_cast<int*>(gnorm + l);
+  if (tid < 2) s_rot[tid] = 0;
+  if (active) {
+    // first seats: top[i] = column i, bottom[i] = column L2-1-i (the dummy
+    // zero column of an odd l sits in bottom[0])
+#pragma unroll
+    for (int row = 0; row < 2; ++row) {
+      const int c = row == 0 ? seat : L2 - 1 - seat;
+      double* x = slot(0, row, warp);
+#pragma unroll
+      for (int i = 0; i < NR; ++i) {
+        const int r = lane + 32 * i;
+        x[r] = (c < l && r < l) ? Rm[(int64_t)c * ldr + r] : 0.0;
+        x[LP + r] = (c < l && r == c) ? 1.0 : 0.0;
+      }
+      if (lane == 0) s_id[0][row][warp] = c;
+    }
+  }
+  // destination seats of this warp's two columns (fixed for the whole run)
+  const int sseat = active ? seat : 0;
+  int drow_t = 0, dseat_t = sseat, drow_b = 1, dseat_b = sseat;
+  if (sseat > 0) {
+    if (sseat < P - 1) dseat_t = sseat + 1;
+    else drow_t = 1;  // top[P-1] -> bottom[P-1]
+  }
+  if (sseat > 0) {
+    dseat_b = sseat - 1;
+  } else if (P > 1) {  // bottom[0] -> top[1]
+    drow_b = 0;
+    dseat_b = 1;
+  }
+  const int drank_t = dseat_t / S, dls_t = dseat_t - drank_t * S;
+  const int drank_b = dseat_b / S, dls_b = dseat_b - drank_b * S;
+  // buffer 0's slots (buffer 1 lies a fixed stride further); seats of this
+  // CTA are addressed as plain shared memory and only the two columns that
+  // cross a CTA boundary go through DSMEM
+  double* const dst_t = drank_t == rank ? slot(0, drow_t, dls_t)
+                                        : cluster.map_shared_rank(slot(0, drow_t, dls_t), drank_t);
+  double* const dst_b = drank_b == rank ? slot(0, drow_b, dls_b)
+                                        : cluster.map_shared_rank(slot(0, drow_b, dls_b), drank_b);
+  int* const did_t = drank_t == rank ? &s_id[0][drow_t][dls_t]
+                                     : cluster.map_shared_rank(&s_id[0][drow_t][dls_t], drank_t);
+  int* const did_b = drank_b == rank ? &s_id[0][drow_b][dls_b]
+                                     : cluster.map_shared_rank(&s_id[0][drow_b][dls_b], drank_b);
+  const int64_t bstride = (int64_t)2 * S * 2 * LP;  // doubles per buffer
+  cluster.sync();
+  const double tol2 = tol * tol;
+  const double thr2 = fmax(tol2, tol / (4.0 * l));
+  const int rounds = L2 - 1;
+  int par = 0, sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    const int fs = sweep & 1;
+    for (int round = 0; round < rounds; ++round) {
+      if (active) {
+        const double2* xt = reinterpret_cast<const double2*>(slot(par, 0, warp));
+        const double2* xb = reinterpret_cast<const double2*>(slot(par, 1, warp));
+        double2 u[NV], v[NV], ju[NV], jv[NV];
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+          u[i] = xt[lane + 32 * i];
+          v[i] = xb[lane + 32 * i];
+        }
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+          ju[i] = xt[LP / 2 + lane + 32 * i];
+          jv[i] = xb[LP / 2 + lane + 32 * i];
+        }
+        const int idt = s_id[par][0][warp], idb = s_id[par][1][warp];
+        // two partial sums per dot product (FP64 latency, not rate, paces a round)
+        double a = u[0].x * u[0].x, b = v[0].x * v[0].x, g = u[0].x * v[0].x;
+        double a1 = u[0].y * u[0].y, b1 = v[0].y * v[0].y, g1 = u[0].y * v[0].y;
+#pragma unroll
+        for (int i = 1; i < NV; ++i) {
+          a = fma(u[i].x, u[i].x, a);
+          b = fma(v[i].x, v[i].x, b);
+          g = fma(u[i].x, v[i].x, g);
+          a1 = fma(u[i].y, u[i].y, a1);
+          b1 = fma(v[i].y, v[i].y, b1);
+          g1 = fma(u[i].y, v[i].y, g1);
+        }
+        a += a1;
+        b += b1;
+        g += g1;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          a += __shfl_xor_sync(0xffffffffu, a, o);
+          b += __shfl_xor_sync(0xffffffffu, b, o);
+          g += __shfl_xor_sync(0xffffffffu, g, o);
+        }
+        const double gg = g * g, ab = a * b;
+        if (g != 0.0 && gg > tol2 * ab) {
+          // t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (b - a) / 2g,
+          // written without the division: with d = b - a, h = 2g (both scaled
+          // by a power of two so the squares stay in range),
+          // den = |d| + sqrt(d^2 + h^2): cs = den / sqrt(den^2 + h^2),
+          // sn = sign(d) sign(h) |h| / sqrt(den^2 + h^2)
+          double d = b - a, h = 2.0 * g;
+          const double mx = fmax(fabs(d), fabs(h));
+          int ex = (__double2hiint(mx) >> 20) & 0x7ff;
+          ex = ex < 1 ? 1 : (ex > 2045 ? 2045 : ex);
+          const double sc = __hiloint2double((2046 - ex) << 20, 0);
+          d *= sc;
+          h *= sc;
+          const double den = fabs(d) + sqrt(fma(d, d, h * h));
+          const double w = rsqrt(fma(den, den, h * h));
+          const double cs = den * w;
+          const double sn =
+              ((__double2hiint(d) ^ __double2hiint(h)) < 0) ? -fabs(h) * w : fabs(h) * w;
+#pragma unroll
+          for (int i = 0; i < NV; ++i) {
+            double2 nu, nv;
+            nu.x = cs * u[i].x - sn * v[i].x;
+            nu.y = cs * u[i].y - sn * v[i].y;
+            nv.x = sn * u[i].x + cs * v[i].x;
+            nv.y = sn * u[i].y + cs * v[i].y;
+            u[i] = nu;
+            v[i] = nv;
+            nu.x = cs * ju[i].x - sn * jv[i].x;
+            nu.y = cs * ju[i].y - sn * jv[i].y;
+            nv.x = sn * ju[i].x + cs * jv[i].x;
+            nv.y = sn * ju[i].y + cs * jv[i].y;
+            ju[i] = nu;
+            jv[i] = nv;
+          }
+          if (lane == 0 && gg > thr2 * ab) s_rot[fs] = 1;
+        }
+        double2* ot = reinterpret_cast<double2*>(dst_t + (par ^ 1) * bstride);
+        double2* ob = reinterpret_cast<double2*>(dst_b + (par ^ 1) * bstride);
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+          ot[lane + 32 * i] = u[i];
+          ob[lane + 32 * i] = v[i];
+        }
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+          ot[LP / 2 + lane + 32 * i] = ju[i];
+          ob[LP / 2 + lane + 32 * i] = jv[i];
+        }
+        if (lane == 0) {
+          did_t[(par ^ 1) * 16] = idt;
+          did_b[(par ^ 1) * 16] = idb;
+        }
+      }
+      cluster.sync();
+      // every CTA read last sweep's flags before it arrived at this barrier
+      if (round == 0 && tid == 0) s_rot[fs ^ 1] = 0;
+      par ^= 1;
+    }
+    int any = 0;
+    for (int r = 0; r < nc; ++r) any |= *cluster.map_shared_rank(&s_rot[fs], r);
+    if (!any) break;
+  }
+  if (tid == 0 && rank == 0) {
+    status[0] = (sweep >= max_sweeps) ? 1 : 0;
+    status[1] = sweep;
+  }
+  // Tail. Norms, signs (largest |entry| positive, earliest row on ties,
+  // kernels.py:556-561) and the columns themselves go to global scratch by
+  // original column index; after a cluster barrier every CTA ranks the norms
+  // (stable descending, kernels.py:535) and writes its share of U_B, s, W_k.
+  if (active) {
+#pragma unroll
+    for (int row = 0; row < 2; ++row) {
+      const int c = s_id[par][row][warp];
+      if (c >= l) continue;
+      const double* x = slot(par, row, warp);
+      double a = 0.0, best = -1.0;
+      int brow = 0;
+#pragma unroll
+      for (int i = 0; i < NR; ++i) {
+        const int r = lane + 32 * i;
+        const double xv = x[r];
+        a = fma(xv, xv, a);
+        if (r < l) {
+          Xg[(int64_t)c * l + r] = xv;
+          Jg[(int64_t)c * l + r] = x[LP + r];
+          if (fabs(xv) > best) {
+            best = fabs(xv);
+            brow = r;
+          }
+        }
+      }
+      a = warp_sum32(a);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int orow = __shfl_xor_sync(0xffffffffu, brow, o);
+        if (ob > best || (ob == best && orow < brow)) {
+          best = ob;
+          brow = orow;
+        }
+      }
+      if (lane == 0) {
+        gnorm[c] = sqrt(a);
+        gsign[c] = (x[brow] < 0.0) ? -1 : 1;
+      }
+    }
+  }
+  __threadfence();
+  cluster.sync();
+  for (int j = tid; j < l; j += blockDim.x) {
+    const double sj = gnorm[j];
+    int rk = 0;
+    for (int i = 0; i < l; ++i) {
+      const double si = gnorm[i];
+      rk += (si > sj) || (si == sj && i < j);
+    }
+    s_perm[rk] = j;
+  }
+  __syncthreads();
+  const int nwarps = blockDim.x >> 5;
+  for (int i = rank * nwarps + warp; i < l; i += nc * nwarps) {
+    const int c = s_perm[i];
+    const double scn = gnorm[c];
+    const double inv = scn > 0.0 ? 1.0 / scn : 0.0;
+    const int sg = gsign[c];
+    if (lane == 0) s_out[i] = scn;
+    for (int r = lane; r < l; r += 32) {
+      Ub[(int64_t)r * ldu + i] = sg * Xg[(int64_t)c * l + r] * inv;
+      if (i < k) Wk[(int64_t)r * ldw + i] = sg * Jg[(int64_t)c * l + r];
+    }
+  }
+  // no CTA may exit while a neighbour can still address its shared memory
+  cluster.sync();
+}
+
 // Shared tail of the cooperative Jacobi kernels: singular values = column
 // norms of X, stable descending order, the sign rule of kernels.py:556-561,
 // U_B = X[:, perm] / s (sign-fixed) and the first k columns of J.
@@ -937,11 +1225,69 @@ void launch_jacobi_svd(const double* R, int64_t ldr, int l, int k, double* Ub, i
     return e ? (strcmp(e, "coop") == 0 ? 1
                 : strcmp(e, "single") == 0 ? 2
                 : strcmp(e, "pairs") == 0 ? 3
-                : strcmp(e, "rr") == 0 ? 4 : 0)
+                : strcmp(e, "rr") == 0 ? 4
+                : strcmp(e, "cluster") == 0 ? 5 : 0)
              : 0;
   }();
   // blocked cooperative kernel from l > 64 (l = 120: 3.3 ms vs 5.4 ms for
   // the single-CTA kernel), single CTA below
+  // cluster kernel (one warp per column pair, seats spread over the CTAs of
+  // one cluster: 16 where the device schedules such a cluster, else 8) for
+  // 32 < l <= 128
+  if ((mode == 0 || mode == 5) && l <= 128 && (l > 32 || mode == 5)) {
+    static const int jnc_knob = [] {
+      const char* e = knob("XB_JACOBI_NC");
+      return e ? atoi(e) : 0;
+    }();
+    auto launch = [&](auto kern, int nr) {
+      auto cfg_for = [&](int nc, cudaLaunchConfig_t& cfg, cudaLaunchAttribute* at) {
+        const int P = (l + (l & 1)) / 2, S = (P + nc - 1) / nc;
+        cfg = cudaLaunchConfig_t{};
+        cfg.gridDim = dim3(nc);
+        cfg.blockDim = dim3(32 * std::max(1, std::min(8, S)));
+        cfg.dynamicSmemBytes = (size_t)2 * 2 * S * 2 * (32 * nr) * sizeof(double);
+        cfg.stream = st;
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = nc;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+      };
+      cudaLaunchConfig_t cfg;
+      cudaLaunchAttribute at[1];
+      XB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+      // a 16-CTA cluster (one warp per SM sub-partition at l = 120) needs the
+      // opt-in attribute and a GPC with 16 free SMs: asked once per kernel
+      static std::atomic<int> nc_cache[2];
+      int nc = nc_cache[nr == 4].load();
+      if (nc == 0) {
+        nc = 8;
+        if (jnc_knob != 8 &&
+            cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+                cudaSuccess) {
+          cfg_for(16, cfg, at);
+          int n = 0;
+          if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) == cudaSuccess && n >= 1) nc = 16;
+        }
+        cudaGetLastError();
+        nc_cache[nr == 4].store(nc);
+      }
+      cfg_for(nc, cfg, at);
+      XB_CUDA(cudaLaunchKernelEx(&cfg, kern, R, ldr, l, k, Ub, ldu, s, Wk, ldw, work, status, tol,
+                                 (int)kMaxSweeps));
+    };
+    if (l <= 64) launch(jacobi_cluster_kernel<2>, 2);
+    else launch(jacobi_cluster_kernel<4>, 4);
+    check_launch("jacobi_cluster");
+    if (getenv("XB_TRACE")) {
+      int hs[2] = {0, 0};
+      XB_CUDA(cudaMemcpyAsync(hs, status, sizeof(hs), cudaMemcpyDeviceToHost, st));
+      XB_CUDA(cudaStreamSynchronize(st));
+      fprintf(stderr, "[xb] jacobi_cluster l=%d: %d sweeps\n", l, hs[1]);
+    }
+    return;
+  }
   // register single-CTA kernel while X and J fit in shared memory (l <= 128)
   if ((mode == 0 || mode == 4) && l <= 128 && 2 * one <= lim) {
     const int dyn = (int)(2 * one);
