@@ -43,9 +43,10 @@ thread_local int64_t* g_launch_counter = nullptr;
 // rows into a ring of pinned slots; each slot's DMA runs while the next slots
 // fill, so the copy proceeds at min(host memcpy rate, link rate).
 struct HostStager {
-  static constexpr int kSlots = 4;
-  static constexpr size_t kSlot = (size_t)64 << 20;
-  static constexpr size_t kPiece = (size_t)2 << 20;
+  static constexpr int kMaxSlots = 16;
+  static constexpr size_t kMaxRow = (size_t)64 << 20;  // widest row staged
+  int kSlots;
+  size_t kSlot, kPiece;
   struct Task {
     char* dst;
     const char* src;
@@ -53,8 +54,8 @@ struct HostStager {
     int64_t rows;
   };
   char* ring = nullptr;
-  cudaEvent_t ev[kSlots] = {nullptr, nullptr, nullptr, nullptr};
-  bool used[kSlots] = {false, false, false, false};
+  cudaEvent_t ev[kMaxSlots] = {};
+  bool used[kMaxSlots] = {};
   int next = 0;
   std::vector<std::thread> workers;
   std::mutex mu;
@@ -64,9 +65,11 @@ struct HostStager {
   int running = 0;
   bool stop = false;
 
-  explicit HostStager(int nthreads) {
+  HostStager(int nthreads, int slots, size_t slot_bytes, size_t piece_bytes)
+      : kSlots(std::max(2, std::min(slots, kMaxSlots))), kSlot(slot_bytes), kPiece(piece_bytes) {
     XB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ring), kSlots * kSlot, cudaHostAllocDefault));
-    for (auto& e : ev) XB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (int i = 0; i < kSlots; ++i)
+      XB_CUDA(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
     for (int t = 0; t < nthreads; ++t) workers.emplace_back([this] { work(); });
   }
   ~HostStager() {
@@ -764,13 +767,34 @@ struct HostSource {
   virtual void prepare(xb_ctx*, bool /*streamed*/, int64_t /*m*/) {}
 };
 
+// geometry of the pageable-host staging ring: 6 x 8 MiB slots (the ring stays
+// in the host's last-level cache, so the DMA reads it from there) filled in
+// 256 KiB pieces (profiles/r02_stage_probe.md: 8.6 GB in 0.165-0.175 s against
+// 0.155 s from pinned memory and 0.52 s with cudaHostRegister per call)
+int knob_int(const char* name, int dflt) {
+  const char* e = knob(name);
+  return e && atoi(e) > 0 ? atoi(e) : dflt;
+}
+size_t stage_slot_bytes() {
+  static const size_t v = (size_t)knob_int("XB_STAGE_SLOT_MB", 8) << 20;
+  return v;
+}
+int stage_slots() {
+  static const int v = knob_int("XB_STAGE_SLOTS", 6);
+  return v;
+}
+size_t stage_piece_bytes() {
+  static const size_t v = (size_t)knob_int("XB_STAGE_PIECE_KB", 256) << 10;
+  return v;
+}
 // worker threads of the pageable-host staging ring
 int stage_threads() {
   static const int n = [] {
     const char* e = knob("XB_STAGE_THREADS");
     if (e && atoi(e) > 0) return std::min(64, atoi(e));
     const unsigned hc = std::thread::hardware_concurrency();
-    return (int)std::max(2u, std::min(16u, hc ? hc : 8u));
+    // one core left to the thread that feeds the DMA queue
+    return (int)std::max(2u, std::min(16u, hc ? hc : 8u) - 1u);
   }();
   return n;
 }
@@ -795,7 +819,8 @@ struct ContiguousSource final : HostSource {
   void prepare(xb_ctx* c, bool streamed, int64_t m) override {
     if (is_pinned_ || m <= 0) return;
     const size_t bytes = (size_t)((m - 1) * host_ld + n) * es;
-    if (streamed || (size_t)n * es > HostStager::kSlot || bytes < ((size_t)32 << 20)) {
+    const size_t slot_bytes = std::max<size_t>(stage_slot_bytes(), (size_t)round_up((int64_t)((size_t)n * es), 4096));
+    if (streamed || (size_t)n * es > HostStager::kMaxRow || bytes < ((size_t)32 << 20)) {
       if (streamed && cudaHostRegister(const_cast<char*>(host), bytes, cudaHostRegisterDefault) ==
                           cudaSuccess) {
         registered = const_cast<char*>(host);
@@ -805,7 +830,12 @@ struct ContiguousSource final : HostSource {
       }
       return;
     }
-    if (!c->stager) c->stager = new HostStager(stage_threads());
+    if (c->stager && c->stager->kSlot < slot_bytes) {
+      delete c->stager;
+      c->stager = nullptr;
+    }
+    if (!c->stager)
+      c->stager = new HostStager(stage_threads(), stage_slots(), slot_bytes, stage_piece_bytes());
     ctx = c;
     stage = true;
   }

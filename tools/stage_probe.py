@@ -35,7 +35,9 @@ def one():
         t0 = time.perf_counter()
         st = ctx.rsvd_dense(a, w.k, w.p, w.q, w.cfg)[4]
         times.append(time.perf_counter() - t0)
-    print(f"threads={os.environ.get('XB_STAGE_THREADS', 'default')} pageable: "
+    print(f"threads={os.environ.get('XB_STAGE_THREADS', 'default')} "
+          f"slot={os.environ.get('XB_STAGE_SLOT_MB', '64')}MB x{os.environ.get('XB_STAGE_SLOTS', '4')} "
+          f"piece={os.environ.get('XB_STAGE_PIECE_KB', '2048')}KB pageable: "
           f"{[round(t, 3) for t in times]} s, ingest stage {st[0]:.3f} s", flush=True)
     if os.environ.get("PROBE_PINNED"):
         hp = torch.empty((w.m, w.n), dtype=torch.float64 if dt == np.float64 else torch.float32,
@@ -55,8 +57,12 @@ if __name__ == "__main__":
         one()
     else:
         print("host cpus:", os.cpu_count(), flush=True)
-        for i, t in enumerate(sys.argv[1:] or ["4", "8", "12", "16", "24", "32"]):
-            env = dict(os.environ, PROBE_CHILD="1", XB_STAGE_THREADS=t)
+        # threads:slotMB:slots:pieceKB
+        for i, spec in enumerate(sys.argv[1:] or ["16:64:4:2048", "16:8:6:1024", "16:4:8:512",
+                                                  "16:16:4:1024", "12:8:6:1024", "15:8:6:512"]):
+            t, mb, ns, kb = spec.split(":")
+            env = dict(os.environ, PROBE_CHILD="1", XB_STAGE_THREADS=t, XB_STAGE_SLOT_MB=mb,
+                       XB_STAGE_SLOTS=ns, XB_STAGE_PIECE_KB=kb)
             if i == 0:
                 env["PROBE_PINNED"] = "1"
             subprocess.run([sys.executable, __file__], env=env, check=False)
