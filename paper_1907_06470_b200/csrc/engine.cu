@@ -1053,14 +1053,38 @@ void oz_prepare(xb_ctx* c, AOp& op, int64_t m, int64_t n) {
   // small matrices stay on DMMA: slicing A costs ~1.5 passes over it and the
   // products are launch-bound (cfg1, 4096 x 2048: 1.2 ms DMMA vs 1.8 ms)
   if ((double)m * (double)n < (double)(1 << 24) || std::min(m, n) < 1024) return;
-  const int S = oz_slices();
   const int64_t kpn = round_up(n, 32), kpm = round_up(m, 32);
-  const double need = (double)S * ((double)round_up(m, 128) * kpn + (double)round_up(n, 128) * kpm);
   static const bool trace = getenv("XB_TRACE") != nullptr;
+  OzA z;
+  z.kpn = kpn;
+  z.kpm = kpm;
+  z.mp = round_up(m, 128);
+  z.np = round_up(n, 128);
+  z.erow = c->ibuf("oz_erow", m);
+  z.ecol = c->ibuf("oz_ecol", n);
+  int* wide = c->ibuf("oz_wide", 1);
+  void* scr = c->buf("oz_scr", oz_both_exp_scratch_bytes(m, n));
+  const double* A = static_cast<const double*>(a.p);
+  // exponents + dynamic-range vote first (one small read-back per call):
+  // 0 = every row/column within 64x its RMS (S digit slices), 1 = within
+  // 16384x (one slice more keeps the same accuracy against the RMS scale),
+  // 2 = wider: DMMA keeps f64 accuracy
+  XB_CUDA(cudaMemsetAsync(wide, 0, sizeof(int), c->st));
+  oz_both_exp(A, m, n, a.ld, z.erow, z.ecol, scr, wide, c->st);
+  int hwide = 0;
+  XB_CUDA(cudaMemcpyAsync(&hwide, wide, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+  XB_CUDA(cudaStreamSynchronize(c->st));
+  if (hwide >= 2) {
+    if (trace) fprintf(stderr, "[xb] ozaki off: dynamic-range guard\n");
+    return;
+  }
+  const int S = hwide == 1 ? std::max(7, oz_slices()) : oz_slices();
+  z.S = S;
+  const double need = (double)S * ((double)z.mp * kpn + (double)z.np * kpm);
   // slice buffers already cached at this size (a repeat call): no memory
   // query (a driver round trip on the hot path)
-  const bool cached = c->buf_bytes("oz_rows") >= (size_t)S * round_up(m, 128) * kpn &&
-                      c->buf_bytes("oz_colsT") >= (size_t)S * round_up(n, 128) * kpm;
+  const bool cached = c->buf_bytes("oz_rows") >= (size_t)S * z.mp * kpn &&
+                      c->buf_bytes("oz_colsT") >= (size_t)S * z.np * kpm;
   size_t free_b = 0, total_b = 0;
   if (!cached && cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
     cudaGetLastError();
@@ -1071,28 +1095,7 @@ void oz_prepare(xb_ctx* c, AOp& op, int64_t m, int64_t n) {
     if (trace) fprintf(stderr, "[xb] ozaki off: slices %.2f GB, free+cached %.2f GB\n", need / 1e9, have / 1e9);
     return;
   }
-  OzA z;
-  z.S = S;
-  z.kpn = kpn;
-  z.kpm = kpm;
-  z.mp = round_up(m, 128);
-  z.np = round_up(n, 128);
-  z.erow = c->ibuf("oz_erow", m);
-  z.ecol = c->ibuf("oz_ecol", n);
-  int* wide = c->ibuf("oz_wide", 1);
-  void* scr = c->buf("oz_scr", oz_both_exp_scratch_bytes(m, n));
-  const double* A = static_cast<const double*>(a.p);
-  // exponents + dynamic-range guard first (one small read-back per call)
-  XB_CUDA(cudaMemsetAsync(wide, 0, sizeof(int), c->st));
-  oz_both_exp(A, m, n, a.ld, z.erow, z.ecol, scr, wide, c->st);
-  int hwide = 0;
-  XB_CUDA(cudaMemcpyAsync(&hwide, wide, sizeof(int), cudaMemcpyDeviceToHost, c->st));
-  XB_CUDA(cudaStreamSynchronize(c->st));
-  if (hwide) {  // some row/column of A spans > 64x its RMS: DMMA keeps f64 accuracy
-    if (trace) fprintf(stderr, "[xb] ozaki off: dynamic-range guard\n");
-    return;
-  }
-  if (trace) fprintf(stderr, "[xb] ozaki on: S=%d\n", S);
+  if (trace) fprintf(stderr, "[xb] ozaki on: S=%d%s\n", S, hwide ? " (wide rows/columns)" : "");
   z.rows = static_cast<int8_t*>(c->buf("oz_rows", (size_t)S * z.mp * kpn));
   z.colsT = static_cast<int8_t*>(c->buf("oz_colsT", (size_t)S * z.np * kpm));
   oz_slice_both(A, m, n, a.ld, z.erow, z.ecol, z.rows, z.mp, kpn, z.colsT, z.np, kpm, S, c->st);

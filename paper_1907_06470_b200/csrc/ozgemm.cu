@@ -67,7 +67,8 @@ struct OCfg {
   static constexpr int SMEM = BAR_OFF + 512 + 1024;  // barriers (3 NS + 1) + TMEM slot, align slack
   static constexpr int ACC_COLS = S * OBN;           // level accumulators
   static constexpr int ASLOT = S * (OBK / 4);        // TMEM columns per A slot
-  static constexpr int USED = ACC_COLS + 2 * ASLOT;
+  // (the two TMEM A slots exist only for the tcgen05.cp variants, S <= 6)
+  static constexpr int USED = ACC_COLS + (S <= 6 ? 2 * ASLOT : 0);
   static constexpr int TMEM_COLS = USED <= 256 ? 256 : 512;
   static_assert(USED <= 512, "TMEM budget");
 };
@@ -214,6 +215,7 @@ __global__ void __launch_bounds__(OTHREADS, 1)
                   int64_t split_stride,
                   int64_t k_per_split, int accumulate, int tiles_n, int dbg, int cl) {
   using Cfg = OCfg<S>;
+  static_assert(TC == 0 || S <= 6, "no TMEM A slots at S = 7");
   constexpr int NS = Cfg::NS;
   extern __shared__ unsigned char smem_raw_o[];
   unsigned char* smem = smem_raw_o + ((1024u - (su32(smem_raw_o) & 1023u)) & 1023u);
@@ -437,7 +439,7 @@ __device__ __forceinline__ void slice_digits(double x, int e, int (&a)[S]) {
   // balanced base-256 digits without a carry chain: adding 128 at every lower
   // digit position makes them plain bytes u_t (a_t = u_t - 128, i.e. the
   // byte with its top bit flipped); the top digit is what remains above
-  constexpr unsigned long long kBias = 0x8080808080ULL >> (8 * (6 - S));
+  constexpr unsigned long long kBias = 0x80808080808080ULL >> (8 * (8 - S));  // S - 1 digits
   const unsigned long long u = (unsigned long long)v + kBias;
   a[0] = (int)((long long)u >> (8 * (S - 1)));
 #pragma unroll
@@ -449,7 +451,15 @@ __device__ __forceinline__ void slice_digits(double x, int e, int (&a)[S]) {
 // carry a fixed number of bits relative to the row maximum, so a row whose
 // maximum towers over its RMS (max^2 > kOzRange^2 * mean square) loses
 // relative accuracy; such matrices raise *wide and stay on DMMA.
+// A range up to 256x wider (kOzRange7) takes one more digit slice (S = 7: 55
+// bits, 28 slice pairs instead of 21) instead of the 3.7x slower DMMA path:
+// *wide = 1. Beyond that *wide = 2 (DMMA).
 constexpr double kOzRange = 64.0;
+constexpr double kOzRange7 = 64.0 * 256.0;
+__device__ __forceinline__ void range_vote(int* wide, double m, double mean_sq) {
+  if (!(mean_sq <= DBL_MAX) || m * m > kOzRange7 * kOzRange7 * mean_sq) atomicMax(wide, 2);
+  else if (m * m > kOzRange * kOzRange * mean_sq) atomicMax(wide, 1);
+}
 
 __global__ void row_exp_kernel(const double* __restrict__ X, int64_t rows, int64_t cols,
                                int64_t ldx, int32_t* __restrict__ e, int* __restrict__ wide) {
@@ -470,7 +480,7 @@ __global__ void row_exp_kernel(const double* __restrict__ X, int64_t rows, int64
   }
   if (lane == 0) {
     e[w] = slice_exp(m);
-    if (wide && m * m > kOzRange * kOzRange * (ss / (double)cols)) atomicOr(wide, 1);
+    if (wide) range_vote(wide, m, ss / (double)cols);
   }
 }
 
@@ -500,7 +510,7 @@ __global__ void col_exp_kernel(const unsigned long long* __restrict__ cmax,
   if (c >= cols) return;
   const double m = __longlong_as_double((long long)cmax[c]);
   e[c] = slice_exp(m);
-  if (wide && css && m * m > kOzRange * kOzRange * (css[c] / (double)rows)) atomicOr(wide, 1);
+  if (wide && css) range_vote(wide, m, css[c] / (double)rows);
 }
 
 // Row AND column max |x| / sum of squares of A in ONE pass (the slicing
@@ -746,8 +756,7 @@ __global__ void rc_finish_kernel(const double2* __restrict__ part, int64_t count
   e[i] = slice_exp(m);
   // (a non-finite sum of squares — float partials that overflowed — counts
   // as wide)
-  if (wide && (!(ss <= DBL_MAX) || m * m > kOzRange * kOzRange * (ss / (double)len)))
-    atomicOr(wide, 1);
+  if (wide) range_vote(wide, m, ss / (double)len);
 }
 
 template <int S>
@@ -889,7 +898,10 @@ void launch_oz(const int8_t* L, const int8_t* R, int64_t rows_p, int64_t np, con
     const char* e = knob("XB_OZ_TC");
     return e && atoi(e) == S;
   }();
-  auto kern = staged ? ozgemm_kernel<S, S> : ozgemm_kernel<S, 0>;
+  auto kern = ozgemm_kernel<S, 0>;
+  if constexpr (S <= 6) {
+    if (staged) kern = ozgemm_kernel<S, S>;
+  }
   XB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
   const int64_t tn = ceil_div(N, OBN), tm = ceil_div(M, OBM);
   XB_REQUIRE(tn * tm < ((int64_t)1 << 31) && splits < 65536, XB_EUNSUPPORTED,
@@ -1302,7 +1314,7 @@ void launch_ozf(const CUtensorMap& ta, const int8_t* R, int64_t np, const int32_
 int oz_slices() {
   static const int s = [] {
     const char* e = knob("XB_OZ_SLICES");
-    return e ? std::max(3, std::min(6, atoi(e))) : 6;
+    return e ? std::max(3, std::min(7, atoi(e))) : 6;
   }();
   return s;
 }
@@ -1382,6 +1394,7 @@ void oz_both_exp_f32(const float* X, int64_t rows, int64_t cols, int64_t ldx, in
     case 3: CALL(3); break;  \
     case 4: CALL(4); break;  \
     case 5: CALL(5); break;  \
+    case 7: CALL(7); break;  \
     default: CALL(6); break; \
   }
 

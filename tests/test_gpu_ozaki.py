@@ -55,10 +55,40 @@ def test_ozaki_gemm_accuracy():
     assert worst <= 1e-13, worst
 
 
-def test_wide_dynamic_range_rows_stay_on_dmma(lib):
-    """Rows whose max towers over their RMS would lose relative accuracy in
-    fixed-point slices: the engine's range guard keeps such an A on DMMA, and
-    the factorisation still meets the f64 targets."""
+def test_wide_dynamic_range_rows_take_a_seventh_slice(lib):
+    """Rows whose max towers over their RMS (here ~128x: one entry per row
+    scaled by 1e4, n = 16384) would lose accuracy against the RMS scale in
+    47-bit fixed-point slices. The engine's range vote gives such an A one
+    more digit slice (28 slice pairs instead of 21) instead of leaving the
+    int8 pipe, and the factorisation still meets the f64 targets."""
+    import numpy as np
+
+    from oracle import metrics as M
+    from oracle import pipeline as OP
+
+    rng = np.random.default_rng(11)
+    m, n = 2048, 16384
+    a = rng.standard_normal((m, 40)) @ rng.standard_normal((40, n))
+    a[np.arange(m), rng.integers(0, n, m)] *= 1e4  # one dominant entry per row
+    lib.profile(True)
+    lib.profile_read()
+    u, s, v, _, _ = lib.rsvd_dense(a, 30, 10, 1, 5)
+    prof = lib.profile_read()
+    lib.profile(False)
+    assert prof["kind"] == "ozaki_i8", prof
+    # 3 of the 4 products over A run on the slices (the first one overlaps the
+    # ingest on DMMA, ops = flops): S (S + 1) / 2 = 28 slice pairs at S = 7,
+    # sketch width 40 padded to the 64-column tile
+    assert abs(prof["pipe_ops"] / prof["flops"] - (3 * 28 * 64 / 40 + 1) / 4) < 0.5, prof
+    ref = OP.rsvd_reorth(a, 30, 10, 1, 5, "double", fast=True)
+    assert M.sigma_rel(s, ref.s) <= 1e-10
+    assert M.sin_angle(u, ref.u) <= 1e-8
+    assert M.sin_angle(v, ref.v) <= 1e-8
+
+
+def test_moderate_dynamic_range_keeps_six_slices(lib):
+    """The same construction at n = 4096: max / RMS <= sqrt(n) = 64, inside
+    the 6-slice range (21 slice pairs)."""
     import numpy as np
 
     from oracle import metrics as M
@@ -67,8 +97,14 @@ def test_wide_dynamic_range_rows_stay_on_dmma(lib):
     rng = np.random.default_rng(11)
     m = n = 4096  # m n = 2^24: the int8 path's size threshold
     a = rng.standard_normal((m, 40)) @ rng.standard_normal((40, n))
-    a[np.arange(m), rng.integers(0, n, m)] *= 1e4  # one dominant entry per row
+    a[np.arange(m), rng.integers(0, n, m)] *= 1e4
+    lib.profile(True)
+    lib.profile_read()
     u, s, v, _, _ = lib.rsvd_dense(a, 30, 10, 1, 5)
+    prof = lib.profile_read()
+    lib.profile(False)
+    assert prof["kind"] == "ozaki_i8", prof
+    assert abs(prof["pipe_ops"] / prof["flops"] - (3 * 21 * 64 / 40 + 1) / 4) < 0.5, prof
     ref = OP.rsvd_reorth(a, 30, 10, 1, 5, "double", fast=True)
     assert M.sigma_rel(s, ref.s) <= 1e-10
     assert M.sin_angle(u, ref.u) <= 1e-8
