@@ -9,6 +9,7 @@
 #include <functional>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "xsvd_b200.h"
 
@@ -67,11 +68,30 @@ extern thread_local int64_t* g_launch_counter;
 inline void count_launch() {
   if (g_launch_counter) ++*g_launch_counter;
 }
+#ifdef XB_TIMELINE
+// Experiment build only (-DXB_TIMELINE, XB_TIMELINE=1): an event after every
+// launch on the compute stream; LaunchScope prints the gaps at the end of the
+// API call (tools: where a step's time goes beyond the kernels themselves).
+struct TimelineEntry {
+  const char* what;
+  cudaEvent_t ev;
+};
+extern thread_local std::vector<TimelineEntry>* g_timeline;
+extern thread_local cudaStream_t g_timeline_stream;
+#endif
 inline void check_launch(const char* what) {
   count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess)
     throw Error(XB_ECUDA, std::string("launch ") + what + ": " + cudaGetErrorString(e));
+#ifdef XB_TIMELINE
+  if (g_timeline) {
+    cudaEvent_t ev;
+    cudaEventCreate(&ev);
+    cudaEventRecord(ev, g_timeline_stream);
+    g_timeline->push_back({what, ev});
+  }
+#endif
 }
 
 // Experiment knobs (tile shapes, thresholds, timing-only debug modes used by

@@ -35,6 +35,10 @@
 
 namespace xb {
 thread_local int64_t* g_launch_counter = nullptr;
+#ifdef XB_TIMELINE
+thread_local std::vector<TimelineEntry>* g_timeline = nullptr;
+thread_local cudaStream_t g_timeline_stream = nullptr;
+#endif
 
 // Pageable host -> device copies at the link rate. An xsvd caller hands over
 // plain numpy arrays: pinning 8 GiB per call (cudaHostRegister + unregister)
@@ -384,8 +388,42 @@ struct LaunchScope {
     g_launch_counter = &c->launches;
     ++c->gen;
     cudaSetDevice(c->device);
+#ifdef XB_TIMELINE
+    if (getenv("XB_TIMELINE") && !g_timeline) {
+      g_timeline = new std::vector<TimelineEntry>();
+      g_timeline_stream = c->st;
+      cudaEvent_t ev;
+      cudaEventCreate(&ev);
+      cudaEventRecord(ev, c->st);
+      g_timeline->push_back({"(start)", ev});
+      own_timeline = true;
+    }
+#endif
   }
-  ~LaunchScope() { g_launch_counter = prev; }
+  ~LaunchScope() {
+    g_launch_counter = prev;
+#ifdef XB_TIMELINE
+    if (own_timeline) {
+      cudaStreamSynchronize(g_timeline_stream);
+      auto& v = *g_timeline;
+      float total = 0.f;
+      if (v.size() > 1) cudaEventElapsedTime(&total, v.front().ev, v.back().ev);
+      fprintf(stderr, "[xb timeline] %zu launches, %.3f ms first to last event\n", v.size() - 1,
+              total);
+      for (size_t i = 1; i < v.size(); ++i) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, v[i - 1].ev, v[i].ev);
+        fprintf(stderr, "[xb timeline] %3zu %-22s %9.1f us\n", i, v[i].what, ms * 1e3f);
+      }
+      for (auto& e : v) cudaEventDestroy(e.ev);
+      delete g_timeline;
+      g_timeline = nullptr;
+    }
+#endif
+  }
+#ifdef XB_TIMELINE
+  bool own_timeline = false;
+#endif
 };
 
 template <typename F>
@@ -813,16 +851,20 @@ struct ContiguousSource final : HostSource {
   ~ContiguousSource() override {
     if (registered) cudaHostUnregister(registered);
   }
-  // A pageable source: the out-of-core streamer reads A q + 1 times, so it
-  // is page-locked once for the call; a single in-HBM ingest goes through
-  // the staging ring instead (registration costs more than the copy).
-  void prepare(xb_ctx* c, bool streamed, int64_t m) override {
+  // A pageable source goes through the staging ring, for the single in-HBM
+  // ingest and for every pass of the out-of-core streamer alike: page-locking
+  // runs at ~23 GB/s and has to be undone, the ring at ~50 GB/s per pass, so
+  // registering would only pay beyond ~20 passes over A. Rows wider than a
+  // slot are page-locked for the call instead; small inputs use pageable
+  // copies.
+  void prepare(xb_ctx* c, bool /*streamed*/, int64_t m) override {
     if (is_pinned_ || m <= 0) return;
     const size_t bytes = (size_t)((m - 1) * host_ld + n) * es;
+    if (bytes < ((size_t)32 << 20)) return;
     const size_t slot_bytes = std::max<size_t>(stage_slot_bytes(), (size_t)round_up((int64_t)((size_t)n * es), 4096));
-    if (streamed || (size_t)n * es > HostStager::kMaxRow || bytes < ((size_t)32 << 20)) {
-      if (streamed && cudaHostRegister(const_cast<char*>(host), bytes, cudaHostRegisterDefault) ==
-                          cudaSuccess) {
+    if ((size_t)n * es > HostStager::kMaxRow) {
+      if (cudaHostRegister(const_cast<char*>(host), bytes, cudaHostRegisterDefault) ==
+          cudaSuccess) {
         registered = const_cast<char*>(host);
         is_pinned_ = true;
       } else {

@@ -35,9 +35,15 @@ def main():
     v = torch.empty((w.n, w.k), dtype=dt, device="cuda")
     s = torch.empty((w.k,), dtype=torch.float64, device="cuda")
     torch.cuda.synchronize()
+    import time
+    walls = []
     for i in range(args.warmup + args.steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
         _, stages = ctx.rsvd_dense_dev(np.float64 if w.precision == "double" else np.float32, w.m, w.n, a.data_ptr(), w.n, w.k, w.p, w.q,
                                        w.cfg, u.data_ptr(), s.data_ptr(), v.data_ptr())
+        walls.append(round((time.perf_counter() - t0) * 1e3, 3))
+    print("wall ms per call", walls)
     print("stage seconds", np.round(stages, 5).tolist(), "launches", ctx.launches)
 
 
