@@ -207,6 +207,97 @@ __device__ __forceinline__ void commit_elect(uint64_t* bar) {
 }
 
 
+
+// All slice-pair MMAs of one k-tile (grouped: up to 4 right slices per MMA,
+// see the kernel) and the stage's commits, from the one lane a single
+// elect.sync picks. tm: TMEM base of the level accumulators (64 columns per
+// level); ad / rd: shared-memory descriptors of left slice 0 / right slice 0
+// of this stage (slice t is t * 4096 / 16 = 256 t descriptor units further,
+// right slice u 128 u); idN: instruction descriptors for N = 64 N; acc0: 0 on
+// the first k-tile (levels overwritten by the t = 0 MMAs); ebar / cbar /
+// fbar: shared::cluster addresses of the stage's empty barrier, the cluster
+// leader's (0: none) and tmem_full (0: not the last k-tile).
+#define XB_MMA "@pe tcgen05.mma.cta_group::1.kind::i8 "
+#define XB_COMMIT_TAIL                                                                        \
+  "@pe tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%8];\n"          \
+  "setp.ne.and.b32 pc, %9, 0, pe;\n"                                                          \
+  "@pc tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%9];\n"          \
+  "setp.ne.and.b32 pf, %10, 0, pe;\n"                                                         \
+  "@pf tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%10];\n"         \
+  "}\n"
+#define XB_ISSUE_ARGS                                                                         \
+  ::"r"(tm), "l"(ad), "l"(rd), "r"(id1), "r"(id2), "r"(id3), "r"(id4), "r"(acc0), "r"(ebar),  \
+      "r"(cbar), "r"(fbar)                                                                    \
+      : "memory"
+#define XB_ISSUE_HEAD                                                                         \
+  "{\n"                                                                                       \
+  ".reg .pred pe, p0, pt, pc, pf;\n"                                                          \
+  ".reg .b64 a1, a2, a3, a4, a5, a6, b4;\n"                                                   \
+  ".reg .b32 d1, d2, d3, d4, d5, d6;\n"                                                       \
+  "elect.sync _|pe, 0xffffffff;\n"                                                            \
+  "setp.ne.b32 p0, %7, 0;\n"                                                                  \
+  "setp.eq.b32 pt, %7, %7;\n"                                                                 \
+  "add.u64 a1, %1, 256;\n"                                                                    \
+  "add.u64 a2, %1, 512;\n"                                                                    \
+  "add.u64 a3, %1, 768;\n"                                                                    \
+  "add.u64 a4, %1, 1024;\n"                                                                   \
+  "add.u64 a5, %1, 1280;\n"                                                                   \
+  "add.u64 a6, %1, 1536;\n"                                                                   \
+  "add.u64 b4, %2, 512;\n"                                                                    \
+  "add.u32 d1, %0, 64;\n"                                                                     \
+  "add.u32 d2, %0, 128;\n"                                                                    \
+  "add.u32 d3, %0, 192;\n"                                                                    \
+  "add.u32 d4, %0, 256;\n"                                                                    \
+  "add.u32 d5, %0, 320;\n"                                                                    \
+  "add.u32 d6, %0, 384;\n"
+
+template <int S>
+__device__ __forceinline__ void issue_tile(uint32_t tm, uint64_t ad, uint64_t rd, uint32_t id1,
+                                           uint32_t id2, uint32_t id3, uint32_t id4,
+                                           uint32_t acc0, uint32_t ebar, uint32_t cbar,
+                                           uint32_t fbar) {
+  static_assert(S == 4 || S == 6 || S == 7, "grouped issue lists exist for S = 4, 6, 7");
+  if constexpr (S == 6) {
+    // (t, u0, slices): (0,0,4) (0,4,2) (1,0,4) (1,4,1) (2,0,4) (3,0,3) (4,0,2) (5,0,1)
+    asm volatile(XB_ISSUE_HEAD
+                 XB_MMA "[%0], %1, %2, %6, p0;\n"
+                 XB_MMA "[d4], %1, b4, %4, p0;\n"
+                 XB_MMA "[d1], a1, %2, %6, pt;\n"
+                 XB_MMA "[d5], a1, b4, %3, pt;\n"
+                 XB_MMA "[d2], a2, %2, %6, pt;\n"
+                 XB_MMA "[d3], a3, %2, %5, pt;\n"
+                 XB_MMA "[d4], a4, %2, %4, pt;\n"
+                 XB_MMA "[d5], a5, %2, %3, pt;\n"
+                 XB_COMMIT_TAIL XB_ISSUE_ARGS);
+  } else if constexpr (S == 7) {
+    // (0,0,4) (0,4,3) (1,0,4) (1,4,2) (2,0,4) (2,4,1) (3,0,4) (4,0,3) (5,0,2) (6,0,1)
+    asm volatile(XB_ISSUE_HEAD
+                 XB_MMA "[%0], %1, %2, %6, p0;\n"
+                 XB_MMA "[d4], %1, b4, %5, p0;\n"
+                 XB_MMA "[d1], a1, %2, %6, pt;\n"
+                 XB_MMA "[d5], a1, b4, %4, pt;\n"
+                 XB_MMA "[d2], a2, %2, %6, pt;\n"
+                 XB_MMA "[d6], a2, b4, %3, pt;\n"
+                 XB_MMA "[d3], a3, %2, %6, pt;\n"
+                 XB_MMA "[d4], a4, %2, %5, pt;\n"
+                 XB_MMA "[d5], a5, %2, %4, pt;\n"
+                 XB_MMA "[d6], a6, %2, %3, pt;\n"
+                 XB_COMMIT_TAIL XB_ISSUE_ARGS);
+  } else {
+    // S = 4: (0,0,4) (1,0,3) (2,0,2) (3,0,1)
+    asm volatile(XB_ISSUE_HEAD
+                 XB_MMA "[%0], %1, %2, %6, p0;\n"
+                 XB_MMA "[d1], a1, %2, %5, pt;\n"
+                 XB_MMA "[d2], a2, %2, %4, pt;\n"
+                 XB_MMA "[d3], a3, %2, %3, pt;\n"
+                 XB_COMMIT_TAIL XB_ISSUE_ARGS);
+  }
+}
+#undef XB_MMA
+#undef XB_COMMIT_TAIL
+#undef XB_ISSUE_ARGS
+#undef XB_ISSUE_HEAD
+
 template <int S, int TC>
 __global__ void __launch_bounds__(OTHREADS, 1)
     ozgemm_kernel(const int8_t* __restrict__ L, const int8_t* __restrict__ R, int64_t rows_p,
@@ -302,6 +393,38 @@ __global__ void __launch_bounds__(OTHREADS, 1)
     const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
     const uint32_t cempty0 = cl > 1 ? mapa_rank(cempty, 0) : 0u;  // leader's cempty[0]
     const uint32_t sbase = su32(smem);
+    constexpr bool kLean = TC == 0 && (S == 4 || S == 6 || S == 7);
+    if (kLean && (dbg & ~(64 | 128)) == 0) {
+      if constexpr (kLean) {
+      // Production path: ONE elect per k-tile for the grouped MMAs and the
+      // commits together (issue_tile), shared-memory descriptors advanced by
+      // adds, the stage index and phase kept incrementally. The generic loop
+      // below spends ~20 uniform-datapath instructions per MMA (elect, vote,
+      // descriptor assembly, experiment branches): its issue time per k-tile
+      // was ~60 % of the k-tile's tensor time and paced the kernel.
+      const uint64_t ad0 = smem_desc(sbase, 256, 0, 128);
+      const uint64_t rd0 = smem_desc(sbase + (uint32_t)(S * Cfg::ATILE), 256, 0, 128);
+      constexpr uint64_t kStep = (uint64_t)(Cfg::STAGE >> 4);
+      const uint32_t e0 = su32(&empty[0]), tf = su32(tmem_full);
+      uint64_t ad = ad0, rd = rd0;
+      uint32_t st = 0, ph = 0;
+      for (int kt = 0; kt < ktiles; ++kt) {
+        mbar_wait(&full[st], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        issue_tile<S>(tm, ad, rd, idesc_n[0], idesc_n[1], idesc_n[2], idesc_n[3],
+                      kt > 0 ? 1u : 0u, e0 + 8u * st, cl > 1 ? cempty0 + 8u * st : 0u,
+                      kt == ktiles - 1 ? tf : 0u);
+        ad += kStep;
+        rd += kStep;
+        if (++st == NS) {
+          st = 0;
+          ph ^= 1;
+          ad = ad0;
+          rd = rd0;
+        }
+      }
+      }
+    } else
     for (int kt = 0; kt < ktiles; ++kt) {
       const int s = kt % NS, a = kt & 1;
       mbar_wait(&full[s], (kt / NS) & 1);
