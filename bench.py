@@ -797,6 +797,28 @@ def run_ours(args):
     roofline = case.roofline(prof, dmma_peak, dfma_peak, hbm_peak, i8_peak)
     roofline["tc_microbench"] = {"i8_tops": i8_peak, "bf16_tflops": bf16_meas,
                                  "dmma_tflops": dmma_peak, "dfma_tflops": dfma_peak}
+    if roofline.get("unit") == "TOP/s (int8)":
+        # The tensor pipe's rate on this device is power-limited: ncu shows the
+        # int8-slice GEMM running at an SM clock of ~1.50 GHz (maximum 1.965),
+        # and MEASURED_PEAKS.json carries the same effect for cuBLAS bf16 (burst
+        # vs sustained). Beside the short microbenchmark (`peak`): the same
+        # microbenchmark with random operand bytes run back to back for ~0.5 s
+        # (the steady-state rate a kernel inside a long step can reach), and
+        # 2 x the sustained bf16 figure.
+        sustained = []
+        t_end = time.perf_counter() + 0.5
+        while time.perf_counter() < t_end or len(sustained) < 3:
+            sustained.append(ctx.tc_peaks_data(True)[0])
+        i8_sus = min(sustained[-3:])
+        bf16_sus = measured_peaks().get("bf16_tflops_sustained")
+        roofline["peak_sustained"] = {
+            "i8_tops_random_operands_0p5s": i8_sus,
+            "frac": roofline["achieved"] / i8_sus if i8_sus else None,
+            "two_x_measured_bf16_sustained": 2 * bf16_sus if bf16_sus else None,
+            "frac_vs_2x_bf16_sustained": (roofline["achieved"] / (2 * bf16_sus)
+                                          if bf16_sus else None),
+            "note": "power-limited steady state; `frac` above is against the short-burst "
+                    "microbenchmark"}
     roofline["launches_per_step"] = prof["launches"] / args.steps
     roofline["share_of_step"] = prof["seconds"] / (ms * 1e-3 * args.steps)
     traffic = None

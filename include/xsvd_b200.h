@@ -101,6 +101,12 @@ int xb_fp64_peaks(xb_ctx* ctx, double* dmma_tflops, double* dfma_tflops);
  * pipe the f64/f32 int8-slice GEMMs run on) and bf16 TFLOP/s (kind::f16) —
  * the measured roofline denominator of the int8-slice GEMMs. */
 int xb_tc_peaks(xb_ctx* ctx, double* i8_tops, double* bf16_tflops);
+/* The same with the operand tiles filled with uniformly random bytes
+ * (random_data != 0) instead of small constants: real digit slices toggle
+ * every input bit of the tensor core, its power draw rises and the SM clock
+ * it sustains falls (B200: ~1.5 GHz instead of ~1.9 GHz), so this is the
+ * tensor rate a kernel working on real data can reach on this device. */
+int xb_tc_peaks_data(xb_ctx* ctx, int random_data, double* i8_tops, double* bf16_tflops);
 
 /*
  * Full factorization — replaces randomized_svd (pipeline.py:442-625) with

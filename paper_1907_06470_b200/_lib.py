@@ -46,6 +46,7 @@ SIGNATURES = [
     ("xb_profile_read_ext", _int, [_vp, _vp]),
     ("xb_fp64_peaks", _int, [_vp, _dp, _dp]),
     ("xb_tc_peaks", _int, [_vp, _dp, _dp]),
+    ("xb_tc_peaks_data", _int, [_vp, _int, _dp, _dp]),
     ("xb_set_power_auto", _int, [_vp, _int, C.c_double]),
     ("xb_last_power", _int, [_vp, _intp, _vp, _int, _intp]),
     ("xb_set_gram_path", _int, [_vp, _int]),
@@ -205,6 +206,12 @@ class Context:
         """Measured dense tcgen05 rates: (int8 TOP/s, bf16 TFLOP/s)."""
         a, b = C.c_double(), C.c_double()
         _check(self.lib.xb_tc_peaks(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    def tc_peaks_data(self, random_data: bool = True):
+        """The same with random operand bytes (the power-limited rate on real data)."""
+        a, b = C.c_double(), C.c_double()
+        _check(self.lib.xb_tc_peaks_data(self.h, int(random_data), C.byref(a), C.byref(b)))
         return a.value, b.value
 
     # -- power selection ------------------------------------------------------

@@ -312,7 +312,7 @@ size_t jacobi_work_doubles(int l);
 // FP64 pipe peaks (TFLOP/s) from saturating microbenchmarks (peak.cu).
 void measure_fp64_peaks(cudaStream_t st, double* dmma_tflops, double* dfma_tflops);
 // tcgen05 dense tensor-pipe peaks: int8 TOP/s (kind::i8), bf16 TFLOP/s (kind::f16).
-void measure_tc_peaks(cudaStream_t st, double* i8_tops, double* bf16_tflops);
+void measure_tc_peaks(cudaStream_t st, double* i8_tops, double* bf16_tflops, int random_data);
 
 // Small helpers
 void launch_transpose(const double* in, int64_t rows, int64_t cols, int64_t ldin, double* out,

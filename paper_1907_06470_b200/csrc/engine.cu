@@ -2039,7 +2039,15 @@ int xb_tc_peaks(xb_ctx* c, double* i8_tops, double* bf16_tflops) {
   return guarded([&] {
     XB_REQUIRE(c && i8_tops && bf16_tflops, XB_EVALUE, "null argument");
     LaunchScope ls(c);
-    measure_tc_peaks(c->st, i8_tops, bf16_tflops);
+    measure_tc_peaks(c->st, i8_tops, bf16_tflops, 0);
+  });
+}
+
+int xb_tc_peaks_data(xb_ctx* c, int random_data, double* i8_tops, double* bf16_tflops) {
+  return guarded([&] {
+    XB_REQUIRE(c && i8_tops && bf16_tflops, XB_EVALUE, "null argument");
+    LaunchScope ls(c);
+    measure_tc_peaks(c->st, i8_tops, bf16_tflops, random_data != 0);
   });
 }
 

@@ -97,16 +97,31 @@ void measure_fp64_peaks(cudaStream_t st, double* dmma_tflops, double* dfma_tflop
 namespace {
 
 template <bool I8>
-__global__ void __launch_bounds__(128) tc_peak_kernel(int iters) {
+__global__ void __launch_bounds__(128) tc_peak_kernel(int iters, int random_data) {
   __shared__ __align__(1024) uint8_t a_s[128 * 32];
   __shared__ __align__(1024) uint8_t b_s[256 * 32];
   __shared__ __align__(8) uint64_t bar;
   __shared__ uint32_t tmem_slot;
   const int warp = threadIdx.x >> 5;
+  // operand bytes: small constants, or (random_data) uniformly random bytes —
+  // the digit slices of real data toggle every input bit of the tensor core,
+  // and its power draw, hence the SM clock it sustains, depends on that
+  auto mix = [](uint32_t x) {
+    x ^= x >> 16;
+    x *= 0x7feb352dU;
+    x ^= x >> 15;
+    x *= 0x846ca68bU;
+    x ^= x >> 16;
+    return x;
+  };
   for (int i = threadIdx.x; i < 128 * 32 / 4; i += blockDim.x)
-    reinterpret_cast<uint32_t*>(a_s)[i] = 0x01010101u * (i & 3);
+    reinterpret_cast<uint32_t*>(a_s)[i] =
+        random_data ? (I8 ? mix(i + 977u * blockIdx.x) : (mix(i) & 0x3fff3fffu) | 0x30003000u)
+                    : 0x01010101u * (i & 3);
   for (int i = threadIdx.x; i < 256 * 32 / 4; i += blockDim.x)
-    reinterpret_cast<uint32_t*>(b_s)[i] = 0x01010101u * (i & 7);
+    reinterpret_cast<uint32_t*>(b_s)[i] =
+        random_data ? (I8 ? mix(i + 7919u + 31u * blockIdx.x) : (mix(i + 99u) & 0x3fff3fffu) | 0x30003000u)
+                    : 0x01010101u * (i & 7);
   if (threadIdx.x == 0) {
     tc::mbar_init(&bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -163,7 +178,7 @@ __global__ void __launch_bounds__(128) tc_peak_kernel(int iters) {
 
 // Dense tensor-pipe rates of this device (best of 4): int8 TOP/s
 // (tcgen05.mma kind::i8) and bf16 TFLOP/s (kind::f16, f32 accumulate).
-void measure_tc_peaks(cudaStream_t st, double* i8_tops, double* bf16_tflops) {
+void measure_tc_peaks(cudaStream_t st, double* i8_tops, double* bf16_tflops, int random_data) {
   cudaEvent_t e0, e1;
   XB_CUDA(cudaEventCreate(&e0));
   XB_CUDA(cudaEventCreate(&e1));
@@ -173,9 +188,9 @@ void measure_tc_peaks(cudaStream_t st, double* i8_tops, double* bf16_tflops) {
     for (int rep = 0; rep < 4; ++rep) {
       XB_CUDA(cudaEventRecord(e0, st));
       if (i8)
-        tc_peak_kernel<true><<<blocks, 128, 0, st>>>(iters);
+        tc_peak_kernel<true><<<blocks, 128, 0, st>>>(iters, random_data);
       else
-        tc_peak_kernel<false><<<blocks, 128, 0, st>>>(iters);
+        tc_peak_kernel<false><<<blocks, 128, 0, st>>>(iters, random_data);
       check_launch("tc_peak");
       XB_CUDA(cudaEventRecord(e1, st));
       XB_CUDA(cudaEventSynchronize(e1));

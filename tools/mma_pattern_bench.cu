@@ -35,7 +35,7 @@ __host__ __device__ constexpr Pattern pattern(int id) {
     default: return {8, {0, 0, 64, 64, 128, 128, 192, 192}, {256, 256, 256, 256, 256, 256, 256, 256}};
   }
 }
-constexpr int kPatterns = 15;
+constexpr int kPatterns = 25;
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -49,12 +49,15 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t sbo, uint
   return d;
 }
 
-template <int ID, bool TS = false>
+template <int ID, bool TS = false, int NC = 0, int WR = 0, bool RING = false>
 __global__ void __launch_bounds__(128) pattern_kernel(int iters, long long* cycles) {
+  extern __shared__ __align__(16) uint8_t wr_ring[];  // WR > 0: 96 KB the other warps write into
+  __shared__ volatile int done;
   constexpr Pattern pat = pattern(ID);
   __shared__ __align__(1024) uint8_t a_s[128 * 32];
   __shared__ __align__(1024) uint8_t b_s[256 * 32];
   __shared__ __align__(8) uint64_t bar[2];
+  __shared__ __align__(8) uint64_t scratch[2];  // NC commits per pattern land here, never waited on
   __shared__ uint32_t tmem_slot;
   const int warp = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < 128 * 32 / 4; i += blockDim.x)
@@ -64,6 +67,8 @@ __global__ void __launch_bounds__(128) pattern_kernel(int iters, long long* cycl
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(su32(&bar[0])));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(su32(&bar[1])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(su32(&scratch[0])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(su32(&scratch[1])));
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -76,6 +81,25 @@ __global__ void __launch_bounds__(128) pattern_kernel(int iters, long long* cycl
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem = tmem_slot;
+  if (threadIdx.x == 0) done = 0;
+  __syncthreads();
+  if (WR > 0 && warp > 0) {
+    // 96 threads store WR KB per 700 cycles (16-byte stores), paced by the clock
+    const int t = threadIdx.x - 32;
+    const int per_tick = WR * 1024 / 16 / 96;  // stores per thread per tick
+    uint4 v = make_uint4(t, t, t, t);
+    uint32_t pos = 0;
+    long long next = clock64();
+    while (!done) {
+      for (int i = 0; i < per_tick; ++i) {
+        *reinterpret_cast<uint4*>(wr_ring + ((pos + (uint32_t)t) % 6144u) * 16u) = v;
+        pos += 96;
+      }
+      next += 700;
+      while (clock64() < next && !done) {
+      }
+    }
+  }
   if (threadIdx.x == 0) {
     const uint32_t idesc0 = (2u << 4) | (1u << 7) | (1u << 10) | ((128u >> 4) << 24);
     const uint64_t da = smem_desc(su32(a_s), 256, 128);
@@ -95,12 +119,37 @@ __global__ void __launch_bounds__(128) pattern_kernel(int iters, long long* cycl
     const long long t0 = clock64();
     for (int it = 0; it < iters; ++it) {
 #pragma unroll 1
-      for (int r = 0; r < kRep; ++r)
+      for (int r = 0; r < kRep; ++r) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+          asm volatile(
+              "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                  su32(&scratch[c & 1]))
+              : "memory");
 #pragma unroll
       for (int j = 0; j < pat.n; ++j) {
         const uint32_t d = tmem + (uint32_t)pat.doff[j];
         const uint32_t idesc = idesc0 | ((uint32_t)(pat.ncol[j] >> 3) << 17);
-        if (TS)  // A operand from TMEM (columns 448..: a 128 x 32-byte slot per slice)
+        if (RING) {
+          // operands where ozgemm_kernel keeps them: stage r % 5 of a ring in the
+          // dynamic shared memory, left slice t at t * 4096, right slices from
+          // 24576 + u0 * 2048 (pattern 6's (t, u0) list)
+          constexpr int tt[8] = {0, 0, 1, 1, 2, 3, 4, 5};
+          constexpr int uu[8] = {0, 4, 0, 4, 0, 0, 0, 0};
+          const uint32_t stg = su32(wr_ring) + (uint32_t)((r % 5) * 36864);
+          const uint64_t xa = smem_desc(stg + tt[j % 8] * 4096, 256, 128);
+          const uint64_t xb = smem_desc(stg + 24576 + uu[j % 8] * 2048, 256, 128);
+          if (TS)
+            asm volatile(
+                "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
+                "r"(tmem + 448u + 8u * (uint32_t)tt[j % 8]), "l"(xb), "r"(idesc), "r"(1));
+          else
+            asm volatile(
+                "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+                "l"(xa), "l"(xb), "r"(idesc), "r"(1));
+        } else if (TS)  // A operand from TMEM (columns 448..: a 128 x 32-byte slot per slice)
           asm volatile(
               "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
               "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
@@ -111,6 +160,7 @@ __global__ void __launch_bounds__(128) pattern_kernel(int iters, long long* cycl
               "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
               "l"(da), "l"(db), "r"(idesc), "r"(1));
       }
+      }
       asm volatile(
           "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
               su32(&bar[it & 1]))
@@ -119,6 +169,7 @@ __global__ void __launch_bounds__(128) pattern_kernel(int iters, long long* cycl
     }
     wait((iters - 1) & 1);
     if (blockIdx.x == 0) *cycles = clock64() - t0;
+    done = 1;
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
@@ -144,6 +195,16 @@ int main() {
       "8 x N=256: pairs on the same accumulator, shifted by 64 between pairs",
       "ozgemm S=6 k-tile with the A operand from TMEM (TS mode)",
       "2 x N=256 alternating, A operand from TMEM",
+      "ozgemm S=6 k-tile, SS, 1 tcgen05.commit per k-tile",
+      "ozgemm S=6 k-tile, SS, 2 commits per k-tile",
+      "ozgemm S=6 k-tile, TS, 1 commit per k-tile",
+      "ozgemm S=6 k-tile, TS, 2 commits per k-tile",
+      "ozgemm S=6 k-tile, SS, other warps store 36 KB per 700 cycles into shared memory",
+      "ozgemm S=6 k-tile, SS, other warps store 72 KB per 700 cycles",
+      "ozgemm S=6 k-tile, TS, other warps store 24 KB per 700 cycles",
+      "ozgemm S=6 k-tile, TS, other warps store 72 KB per 700 cycles",
+      "ozgemm S=6 k-tile, SS, operands at the kernel's addresses (5-stage ring, per-slice tiles)",
+      "ozgemm S=6 k-tile, TS, right slices at the kernel's addresses",
   };
   long long* dc;
   cudaMalloc(&dc, sizeof(long long));
@@ -158,10 +219,32 @@ int main() {
 #undef XB_CASE
       case 13: pattern_kernel<6, true><<<sms, 128>>>(iters, dc); break;
       case 14: pattern_kernel<0, true><<<sms, 128>>>(iters, dc); break;
+      case 15: pattern_kernel<6, false, 1><<<sms, 128>>>(iters, dc); break;
+      case 16: pattern_kernel<6, false, 2><<<sms, 128>>>(iters, dc); break;
+      case 17: pattern_kernel<6, true, 1><<<sms, 128>>>(iters, dc); break;
+      case 18: pattern_kernel<6, true, 2><<<sms, 128>>>(iters, dc); break;
+#define XB_WR(I, TSV, KB)                                                                      \
+  case I:                                                                                      \
+    cudaFuncSetAttribute(pattern_kernel<6, TSV, 1, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                         98304);                                                               \
+    pattern_kernel<6, TSV, 1, KB><<<sms, 128, 98304>>>(iters, dc);                             \
+    break;
+      XB_WR(19, false, 36) XB_WR(20, false, 72) XB_WR(21, true, 24) XB_WR(22, true, 72)
+#undef XB_WR
+      case 23:
+        cudaFuncSetAttribute(pattern_kernel<6, false, 1, 0, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, 5 * 36864);
+        pattern_kernel<6, false, 1, 0, true><<<sms, 128, 5 * 36864>>>(iters, dc);
+        break;
+      case 24:
+        cudaFuncSetAttribute(pattern_kernel<6, true, 1, 0, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, 5 * 36864);
+        pattern_kernel<6, true, 1, 0, true><<<sms, 128, 5 * 36864>>>(iters, dc);
+        break;
     }
   };
   for (int id = 0; id < kPatterns; ++id) {
-    const Pattern p = pattern(id == 13 ? 6 : id == 14 ? 0 : id);
+    const Pattern p = pattern(id == 14 ? 0 : id >= 13 ? 6 : id);
     double best = 1e30;
     for (int rep = 0; rep < 3; ++rep) {
       launch(id);
