@@ -1040,7 +1040,9 @@ __global__ void __launch_bounds__(kJT, 1)
   double* xs = smj;                    // [W2][l] column-major: X[:, S]
   double* js = xs + (int64_t)W2 * l;   // [W2][l]: J[:, S]
   __shared__ int scol[64];
-  __shared__ int s_rot;
+  __shared__ int s_rot, s_big;
+  const double tol2 = tol * tol;
+  const double thr2 = fmax(tol2, tol / (4.0 * l));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + tid;
   const int64_t gthreads = (int64_t)gridDim.x * blockDim.x;
@@ -1070,6 +1072,7 @@ __global__ void __launch_bounds__(kJT, 1)
             for (int c = bb * bs; c < min(l, (bb + 1) * bs); ++c) scol[w++] = c;
           }
           s_rot = 0;
+          s_big = 0;
           scol[63] = w;
         }
         __syncthreads();
@@ -1121,14 +1124,46 @@ __global__ void __launch_bounds__(kJT, 1)
             }
             double a = a0 + a1, b = b0 + b1, g = g0 + g1;
             lanes_sum3<LANES>(a, b, g);
-            if (g != 0.0 && fabs(g) > tol * sqrt(a * b)) {
-              const double zeta = (b - a) / (2.0 * g);
-              const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-              const double cs = 1.0 / sqrt(1.0 + t * t);
-              const double sn = cs * t;
+            const double gg = g * g, ab = a * b;
+            if (g != 0.0 && gg > tol2 * ab) {
+              // rotation without the FP64 divisions (as jacobi_cluster_kernel):
+              // d = b - a, h = 2g scaled by a power of two, den = |d| + sqrt(d^2 + h^2),
+              // cs = den / sqrt(den^2 + h^2), sn = sign(d) sign(h) |h| / sqrt(den^2 + h^2)
+              double d = b - a, h = 2.0 * g;
+              const double mx = fmax(fabs(d), fabs(h));
+              int ex = (__double2hiint(mx) >> 20) & 0x7ff;
+              ex = ex < 1 ? 1 : (ex > 2045 ? 2045 : ex);
+              const double sc = __hiloint2double((2046 - ex) << 20, 0);
+              d *= sc;
+              h *= sc;
+              const double den = fabs(d) + sqrt(fma(d, d, h * h));
+              const double wr = rsqrt(fma(den, den, h * h));
+              const double cs = den * wr;
+              const double sn =
+                  ((__double2hiint(d) ^ __double2hiint(h)) < 0) ? -fabs(h) * wr : fabs(h) * wr;
               double* jp = js + (int64_t)p * l;
               double* jq = js + (int64_t)q * l;
-              for (int rr = gl; rr < l; rr += LANES) {
+              // four rows per pass, every load before the first store (a
+              // load -> fma -> store loop is a chain of dependent latencies)
+              int rr = gl;
+              for (; rr + 3 * LANES < l; rr += 4 * LANES) {
+                double u[4], v[4], uj[4], vj[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  u[i] = xp[rr + i * LANES];
+                  v[i] = xq[rr + i * LANES];
+                  uj[i] = jp[rr + i * LANES];
+                  vj[i] = jq[rr + i * LANES];
+                }
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  xp[rr + i * LANES] = cs * u[i] - sn * v[i];
+                  xq[rr + i * LANES] = sn * u[i] + cs * v[i];
+                  jp[rr + i * LANES] = cs * uj[i] - sn * vj[i];
+                  jq[rr + i * LANES] = sn * uj[i] + cs * vj[i];
+                }
+              }
+              for (; rr < l; rr += LANES) {
                 const double u = xp[rr], v = xq[rr];
                 const double uj = jp[rr], vj = jq[rr];
                 xp[rr] = cs * u - sn * v;
@@ -1136,7 +1171,12 @@ __global__ void __launch_bounds__(kJT, 1)
                 jp[rr] = cs * uj - sn * vj;
                 jq[rr] = sn * uj + cs * vj;
               }
-              if (gl == 0) s_rot = 1;
+              // only rotations above thr keep the iteration going (a sweep of
+              // tiny rotations leaves <= tol behind: no rotation-free check sweep)
+              if (gl == 0) {
+                s_rot = 1;
+                if (gg > thr2 * ab) s_big = 1;
+              }
             }
           }
           __syncthreads();
@@ -1152,7 +1192,7 @@ __global__ void __launch_bounds__(kJT, 1)
               __stcg(jg + r, jd[r]);
             }
           }
-          if (tid == 0) rotflag[sweep] = 1;
+          if (tid == 0 && s_big) rotflag[sweep] = 1;
         }
         __syncthreads();
       }
