@@ -1077,16 +1077,22 @@ __global__ void __launch_bounds__(kJT, 1)
         }
         __syncthreads();
         const int w = scol[63];
+        // global (L2) -> shared memory with cp.async: every element of the
+        // <= 2 bs columns of X and J in flight at once (a load -> store loop
+        // per column paid one L2 latency per 32 rows)
         for (int c = warp; c < w; c += kJT / 32) {
           const double* xg = X + (int64_t)scol[c] * l;
           const double* jg = J + (int64_t)scol[c] * l;
-          double* xd = xs + (int64_t)c * l;
-          double* jd = js + (int64_t)c * l;
+          const uint32_t xd = (uint32_t)__cvta_generic_to_shared(xs + (int64_t)c * l);
+          const uint32_t jd = (uint32_t)__cvta_generic_to_shared(js + (int64_t)c * l);
           for (int r = lane; r < l; r += 32) {
-            xd[r] = __ldcg(xg + r);
-            jd[r] = __ldcg(jg + r);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(xd + 8u * r), "l"(xg + r)
+                         : "memory");
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(jd + 8u * r), "l"(jg + r)
+                         : "memory");
           }
         }
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
         __syncthreads();
         // one inner cyclic sweep over the w columns (circle ordering); the
         // rotations act on X[:, S] and J[:, S] in shared memory
