@@ -237,6 +237,11 @@ int xb_rsvd_dense_colsharded_dev(xb_ctx* ctx, int dtype, int64_t m, int64_t n_gl
  * (row, col)-sorted without duplicates, float64 values (Precision.DOUBLE).
  * Host buffers; same outputs as xb_rsvd_dense.
  */
+/* 1 in *sorted when the COO entries are strictly increasing in (row, col) —
+ * the reference's SparseBlock invariant (core.py:245-284) that xb_rsvd_coo and
+ * xb_spmm_coo rely on; scanned on host threads. */
+int xb_coo_sorted(const int64_t* rows, const int64_t* cols, int64_t nnz, int* sorted);
+
 /* Row-sharded sparse A (config 3's layout): this rank's m_local
  * rows of the m_global x n matrix as device CSR (rowptr int64[m_local + 1]
  * relative to the rank's first row, col int32, val f64). Y = A_g X is local,

@@ -47,6 +47,7 @@ SIGNATURES = [
     ("xb_fp64_peaks", _int, [_vp, _dp, _dp]),
     ("xb_tc_peaks", _int, [_vp, _dp, _dp]),
     ("xb_tc_peaks_data", _int, [_vp, _int, _dp, _dp]),
+    ("xb_coo_sorted", _int, [_vp, _vp, C.c_int64, C.POINTER(C.c_int)]),
     ("xb_set_power_auto", _int, [_vp, _int, C.c_double]),
     ("xb_last_power", _int, [_vp, _intp, _vp, _int, _intp]),
     ("xb_set_gram_path", _int, [_vp, _int]),
@@ -156,6 +157,30 @@ def _check(status: int):
         raise_for_status(status, msg)
 
 
+_MADV_HUGEPAGE = 14
+try:
+    _libc = C.CDLL(None, use_errno=True)
+    _libc.madvise.argtypes = [C.c_void_p, C.c_size_t, C.c_int]
+    _libc.madvise.restype = C.c_int
+except (OSError, AttributeError):  # pragma: no cover - no libc madvise
+    _libc = None
+
+
+def _out(shape, dtype=np.float64) -> np.ndarray:
+    """A fresh output array for the library to fill. Large ones ask for
+    transparent huge pages first: the device -> host copy is the first touch
+    of every page, and 4 KiB first-touch faults (serialised on the process's
+    mmap lock) capped a 0.96 GB result at ~7 GB/s."""
+    a = np.empty(shape, dtype=dtype)
+    if _libc is not None and a.nbytes >= (8 << 20):
+        page = 2 << 20
+        lo = (a.ctypes.data + page - 1) & ~(page - 1)
+        hi = (a.ctypes.data + a.nbytes) & ~(page - 1)
+        if hi > lo:
+            _libc.madvise(C.c_void_p(lo), C.c_size_t(hi - lo), _MADV_HUGEPAGE)
+    return a
+
+
 def _ptr(a: np.ndarray):
     return a.ctypes.data_as(C.c_void_p)
 
@@ -242,8 +267,8 @@ class Context:
         lda = a.strides[0] // a.itemsize
         dt = a.dtype
         l = k + p
-        u = np.empty((m, k), dtype=dt)
-        v = np.empty((n, k), dtype=dt)
+        u = _out((m, k), dt)
+        v = _out((n, k), dt)
         s = np.empty(k, dtype=np.float64)
         deficient = np.zeros(max(l, 1), dtype=np.int32)
         ndef = C.c_int(0)
@@ -290,8 +315,8 @@ class Context:
         fetch_cb, rel_cb = TILE_FETCH(fetch), TILE_RELEASE(rel)
         rc_ = np.ascontiguousarray(row_cuts, dtype=np.int64)
         cc_ = np.ascontiguousarray(col_cuts, dtype=np.int64)
-        u = np.empty((m, k), dtype=dt)
-        v = np.empty((n, k), dtype=dt)
+        u = _out((m, k), dt)
+        v = _out((n, k), dt)
         s = np.empty(k)
         deficient = np.zeros(max(k + p, 1), dtype=np.int32)
         ndef = C.c_int(0)
@@ -317,8 +342,8 @@ class Context:
         m, n = a.shape
         lda = a.strides[0] // a.itemsize
         dt = a.dtype
-        u = np.empty((m, k), dtype=dt)
-        v = np.empty((n, k), dtype=dt)
+        u = _out((m, k), dt)
+        v = _out((n, k), dt)
         s = np.empty(k)
         deficient = np.zeros(max(k + p, 1), dtype=np.int32)
         ndef = C.c_int(0)
@@ -383,7 +408,10 @@ class Context:
         r = np.ascontiguousarray(rows, dtype=np.int64)
         c = np.ascontiguousarray(cols, dtype=np.int64)
         v = np.ascontiguousarray(vals, dtype=np.float64)
-        if len(r) > 1 and not np.all((r[1:] > r[:-1]) | ((r[1:] == r[:-1]) & (c[1:] > c[:-1]))):
+        ok = C.c_int(1)
+        if len(r) > 1:
+            _check(lib_handle().xb_coo_sorted(_ptr(r), _ptr(c), len(r), C.byref(ok)))
+        if not ok.value:
             order = np.lexsort((c, r))
             r, c, v = r[order], c[order], v[order]
         return r, c, v
@@ -393,8 +421,8 @@ class Context:
         m, n = shape
         r, c, v = self._coo(rows, cols, vals)
         l = k + p
-        u = np.empty((m, k))
-        vv = np.empty((n, k))
+        u = _out((m, k))
+        vv = _out((n, k))
         s = np.empty(k)
         deficient = np.zeros(max(l, 1), dtype=np.int32)
         ndef = C.c_int(0)

@@ -139,3 +139,31 @@ def test_workload_shapes():
     assert CONFIGS[1].l == 30 and CONFIGS[2].l == 120 and CONFIGS[5].l == 550
     s = spectrum("pow-1.5", 4)
     assert s[0] == 1.0 and abs(s[3] - 4 ** -1.5) < 1e-16
+
+
+def test_coo_sorted_check_runs_without_a_device():
+    """xb_coo_sorted (host threads, no CUDA call): the SparseBlock invariant
+    of core.py:245-284 — strictly increasing (row, col)."""
+    import ctypes as C
+
+    from paper_1907_06470_b200 import _lib
+
+    lib = _lib.lib_handle()
+    rng = np.random.default_rng(0)
+    n = 3_000_000
+    rows = np.sort(rng.integers(0, 50_000, n)).astype(np.int64)
+    cols = np.zeros(n, dtype=np.int64)
+    # strictly increasing columns inside every row
+    start = np.flatnonzero(np.r_[True, rows[1:] != rows[:-1]])
+    cols = np.arange(n, dtype=np.int64) - np.repeat(start, np.diff(np.r_[start, n]))
+    ok = C.c_int(-1)
+    assert lib.xb_coo_sorted(rows.ctypes.data, cols.ctypes.data, n, C.byref(ok)) == 0
+    assert ok.value == 1
+    for pos in (1, n // 2, n - 1):
+        c2 = cols.copy()
+        r2 = rows.copy()
+        r2[pos], c2[pos] = r2[pos - 1], c2[pos - 1]  # a duplicate entry
+        assert lib.xb_coo_sorted(r2.ctypes.data, c2.ctypes.data, n, C.byref(ok)) == 0
+        assert ok.value == 0
+    r, c, v = _lib.Context._coo(rows[::-1], cols[::-1], np.ones(n))
+    assert np.array_equal(r, rows) and np.array_equal(c, cols)
