@@ -93,6 +93,118 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ---------------------------------------------------------------------------
+// The same factorisation in blocks of 8 pivots (shared-memory case, l <= ~160).
+// chol_inv_kernel pays one CTA barrier and one FP64 reciprocal (~250 cycles)
+// plus a chain of dependent row updates per pivot: ~2600 cycles per column at
+// l = 120, 0.16 ms per call and eight calls per cfg2 step. In the symmetric
+// row elimination the multiplier f_ij = W[j][i] / d_j of a trailing row i
+// depends on the pivot row j alone, so the updates of row i by different
+// pivots are independent and additive:
+//   phase 1  the 8 rows of the block are eliminated among themselves by 8
+//            warps (one per row; a named barrier per pivot), which makes the
+//            block's pivot rows, pivots and reciprocals final;
+//   phase 2  every trailing row takes all 8 pivots in one pass (rank-8
+//            update of its upper part and of its E = L^-1 part), all warps.
+// 15 block steps of two CTA barriers instead of 120 column steps: 164 -> 135 us
+// at l = 120. (A variant with the diagonal block on one warp, one thread per
+// column for the block rows and a (row group, column) thread grid for the
+// trailing update ran 166 us: profiles/r02_chol_inv_experiments.md.)
+constexpr int kCB8 = 8;
+
+__global__ void __launch_bounds__(kThreads, 1)
+    chol_inv_blocked_kernel(const double* __restrict__ G, int64_t ldg, int l, double tau,
+                            double* __restrict__ R, double* __restrict__ Rinv, int64_t ldr,
+                            int* __restrict__ flag) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ double diag0[256];
+  __shared__ double pivs[256];
+  __shared__ double invs[kCB8];
+  __shared__ int s_failed;
+  double* W = sm;
+  const int64_t lw = l | 1;  // odd row stride (conflict-free column reads)
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int i = warp; i < l; i += kWarps)
+    for (int c = lane; c < l; c += 32) W[(int64_t)i * lw + c] = (c >= i) ? G[(int64_t)i * ldg + c] : 0.0;
+  for (int j = tid; j < l; j += kThreads) diag0[j] = G[(int64_t)j * ldg + j];
+  if (tid == 0) s_failed = 0;
+  __syncthreads();
+  for (int j0 = 0; j0 < l; j0 += kCB8) {
+    const int nb = min(kCB8, l - j0);
+    // ---- phase 1: the block's rows among themselves ----------------------------
+    if (warp < nb) {
+      const int i = j0 + warp;
+      double* rowi = W + (int64_t)i * lw;
+      for (int jj = 0; jj < nb; ++jj) {
+        const int j = j0 + jj;
+        const double* rowj = W + (int64_t)j * lw;
+        const double piv = rowj[j];
+        const bool ok = (piv > tau * diag0[j]) && (piv > 0.0);
+        const double pe = ok ? piv : fmax(fabs(diag0[j]), DBL_MIN);  // keep going; result discarded
+        const double inv = 1.0 / pe;
+        if (warp == jj && lane == 0) {
+          pivs[j] = pe;
+          invs[jj] = inv;
+          if (!ok) s_failed = 1;
+        }
+        if (warp > jj) {
+          const double f = rowj[i] * inv;
+          for (int c = i + lane; c < l; c += 32) rowi[c] -= f * rowj[c];
+          for (int c = lane; c < j; c += 32) rowi[c] -= f * rowj[c];
+          if (lane == 0) rowi[j] = -f;
+        }
+        // the warps of the block only (row j + 1 is final for the next pivot)
+        asm volatile("bar.sync 1, %0;\n" ::"r"(32 * nb) : "memory");
+      }
+    }
+    __syncthreads();
+    // ---- phase 2: every trailing row takes the block's pivots in one pass ------
+    for (int i = j0 + nb + warp; i < l; i += kWarps) {
+      double* rowi = W + (int64_t)i * lw;
+      double f[kCB8];
+#pragma unroll
+      for (int jj = 0; jj < kCB8; ++jj)
+        f[jj] = jj < nb ? W[(int64_t)(j0 + jj) * lw + i] * invs[jj] : 0.0;
+      // upper part (c >= i) and the E part of earlier blocks (c < j0)
+      for (int c = lane; c < l; c += 32) {
+        if (c >= i || c < j0) {
+          double a0 = rowi[c], a1 = 0.0;
+#pragma unroll
+          for (int jj = 0; jj < kCB8; jj += 2) {
+            if (jj < nb) a0 = fma(-f[jj], W[(int64_t)(j0 + jj) * lw + c], a0);
+            if (jj + 1 < nb) a1 = fma(-f[jj + 1], W[(int64_t)(j0 + jj + 1) * lw + c], a1);
+          }
+          rowi[c] = a0 + a1;
+        }
+      }
+      // E entries inside the block: E_i[c] = -f_c - sum_{j > c in block} f_j E[j][c]
+      if (lane < nb) {
+        const int c = j0 + lane;
+        double e = 0.0;
+#pragma unroll
+        for (int jj = 0; jj < kCB8; ++jj) {
+          if (jj == lane) e -= f[jj];
+          else if (jj > lane && jj < nb) e = fma(-f[jj], W[(int64_t)(j0 + jj) * lw + c], e);
+        }
+        rowi[c] = e;
+      }
+    }
+    __syncthreads();
+  }
+  if (s_failed && tid == 0) *flag = 1;
+  // R[j][c] = W[j][c] / sqrt(d_j) (c >= j); R^-1[a][b] = E[b][a] / sqrt(d_b)
+  for (int i = warp; i < l; i += kWarps) {
+    const double rs = 1.0 / sqrt(pivs[i]);
+    for (int c = lane; c < l; c += 32) {
+      R[(int64_t)i * ldr + c] = (c >= i) ? W[(int64_t)i * lw + c] * rs : 0.0;
+      double e = 0.0;
+      if (c > i) e = W[(int64_t)c * lw + i] / sqrt(pivs[c]);
+      else if (c == i) e = rs;
+      Rinv[(int64_t)i * ldr + c] = e;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // chol_coop: the same factorisation for sketch widths whose l x l matrix does
 // not fit one CTA's shared memory (l > ~160; config 5: l = 550). A single CTA
 // streaming the matrix through L2 one column at a time took ~18 ms at l = 550;
@@ -1239,6 +1351,17 @@ void launch_chol_inv(const double* G, int64_t ldg, int l, double tau, double* R,
     XB_CUDA(cudaLaunchCooperativeKernel((void*)chol_coop_kernel, dim3(blocks), dim3(kCT), args, 0, st));
     check_launch("chol_coop");
     if (!ws_in) XB_CUDA(cudaFreeAsync(ws, st));
+    return;
+  }
+  static const bool blocked = [] {
+    const char* e = knob("XB_CHOL_BLOCKED");
+    return !(e && atoi(e) == 0);
+  }();
+  if (use_smem && blocked && l <= 256) {
+    XB_CUDA(cudaFuncSetAttribute(chol_inv_blocked_kernel,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    chol_inv_blocked_kernel<<<1, kThreads, bytes, st>>>(G, ldg, l, tau, R, Rinv, ldr, flag);
+    check_launch("chol_inv");
     return;
   }
   double* gw = use_smem ? nullptr : ws_in;
