@@ -105,8 +105,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 //            block's pivot rows, pivots and reciprocals final;
 //   phase 2  every trailing row takes all 8 pivots in one pass (rank-8
 //            update of its upper part and of its E = L^-1 part), all warps.
-// 15 block steps of two CTA barriers instead of 120 column steps: 164 -> 135 us
-// at l = 120. (A variant with the diagonal block on one warp, one thread per
+// 15 block steps of one CTA barrier instead of 120 column steps, and phase 1
+// of the next block overlapped with phase 2 of this one: 164 -> 135 us at
+// l = 120 without the overlap. (A variant with the diagonal block on one warp, one thread per
 // column for the block rows and a (row group, column) thread grid for the
 // trailing update ran 166 us: profiles/r02_chol_inv_experiments.md.)
 constexpr int kCB8 = 8;
@@ -118,7 +119,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(16) double sm[];
   __shared__ double diag0[256];
   __shared__ double pivs[256];
-  __shared__ double invs[kCB8];
+  __shared__ double invs[2][kCB8];
   __shared__ int s_failed;
   double* W = sm;
   const int64_t lw = l | 1;  // odd row stride (conflict-free column reads)
@@ -128,65 +129,84 @@ __global__ void __launch_bounds__(kThreads, 1)
   for (int j = tid; j < l; j += kThreads) diag0[j] = G[(int64_t)j * ldg + j];
   if (tid == 0) s_failed = 0;
   __syncthreads();
-  for (int j0 = 0; j0 < l; j0 += kCB8) {
-    const int nb = min(kCB8, l - j0);
-    // ---- phase 1: the block's rows among themselves ----------------------------
-    if (warp < nb) {
-      const int i = j0 + warp;
-      double* rowi = W + (int64_t)i * lw;
-      for (int jj = 0; jj < nb; ++jj) {
-        const int j = j0 + jj;
-        const double* rowj = W + (int64_t)j * lw;
-        const double piv = rowj[j];
-        const bool ok = (piv > tau * diag0[j]) && (piv > 0.0);
-        const double pe = ok ? piv : fmax(fabs(diag0[j]), DBL_MIN);  // keep going; result discarded
-        const double inv = 1.0 / pe;
-        if (warp == jj && lane == 0) {
-          pivs[j] = pe;
-          invs[jj] = inv;
-          if (!ok) s_failed = 1;
+  // phase 1 of the block at j0 (warps 0 .. nb-1, one per row; reciprocals into
+  // invs[buf])
+  auto phase1 = [&](int j0, int nb, int buf) {
+    const int i = j0 + warp;
+    double* rowi = W + (int64_t)i * lw;
+    for (int jj = 0; jj < nb; ++jj) {
+      const int j = j0 + jj;
+      const double* rowj = W + (int64_t)j * lw;
+      const double piv = rowj[j];
+      const bool ok = (piv > tau * diag0[j]) && (piv > 0.0);
+      const double pe = ok ? piv : fmax(fabs(diag0[j]), DBL_MIN);  // keep going; result discarded
+      const double inv = 1.0 / pe;
+      if (warp == jj && lane == 0) {
+        pivs[j] = pe;
+        invs[buf][jj] = inv;
+        if (!ok) s_failed = 1;
+      }
+      if (warp > jj) {
+        const double f = rowj[i] * inv;
+        for (int c = i + lane; c < l; c += 32) rowi[c] -= f * rowj[c];
+        for (int c = lane; c < j; c += 32) rowi[c] -= f * rowj[c];
+        if (lane == 0) rowi[j] = -f;
+      }
+      // the warps of the block only (row j + 1 is final for the next pivot)
+      asm volatile("bar.sync 1, %0;\n" ::"r"(32 * nb) : "memory");
+    }
+  };
+  // phase 2 of trailing row i for the block at j0
+  auto phase2_row = [&](int i, int j0, int nb, int buf) {
+    double* rowi = W + (int64_t)i * lw;
+    double f[kCB8];
+#pragma unroll
+    for (int jj = 0; jj < kCB8; ++jj)
+      f[jj] = jj < nb ? W[(int64_t)(j0 + jj) * lw + i] * invs[buf][jj] : 0.0;
+    // upper part (c >= i) and the E part of earlier blocks (c < j0)
+    for (int c = lane; c < l; c += 32) {
+      if (c >= i || c < j0) {
+        double a0 = rowi[c], a1 = 0.0;
+#pragma unroll
+        for (int jj = 0; jj < kCB8; jj += 2) {
+          if (jj < nb) a0 = fma(-f[jj], W[(int64_t)(j0 + jj) * lw + c], a0);
+          if (jj + 1 < nb) a1 = fma(-f[jj + 1], W[(int64_t)(j0 + jj + 1) * lw + c], a1);
         }
-        if (warp > jj) {
-          const double f = rowj[i] * inv;
-          for (int c = i + lane; c < l; c += 32) rowi[c] -= f * rowj[c];
-          for (int c = lane; c < j; c += 32) rowi[c] -= f * rowj[c];
-          if (lane == 0) rowi[j] = -f;
-        }
-        // the warps of the block only (row j + 1 is final for the next pivot)
-        asm volatile("bar.sync 1, %0;\n" ::"r"(32 * nb) : "memory");
+        rowi[c] = a0 + a1;
       }
     }
-    __syncthreads();
-    // ---- phase 2: every trailing row takes the block's pivots in one pass ------
-    for (int i = j0 + nb + warp; i < l; i += kWarps) {
-      double* rowi = W + (int64_t)i * lw;
-      double f[kCB8];
+    // E entries inside the block: E_i[c] = -f_c - sum_{j > c in block} f_j E[j][c]
+    if (lane < nb) {
+      const int c = j0 + lane;
+      double e = 0.0;
 #pragma unroll
-      for (int jj = 0; jj < kCB8; ++jj)
-        f[jj] = jj < nb ? W[(int64_t)(j0 + jj) * lw + i] * invs[jj] : 0.0;
-      // upper part (c >= i) and the E part of earlier blocks (c < j0)
-      for (int c = lane; c < l; c += 32) {
-        if (c >= i || c < j0) {
-          double a0 = rowi[c], a1 = 0.0;
-#pragma unroll
-          for (int jj = 0; jj < kCB8; jj += 2) {
-            if (jj < nb) a0 = fma(-f[jj], W[(int64_t)(j0 + jj) * lw + c], a0);
-            if (jj + 1 < nb) a1 = fma(-f[jj + 1], W[(int64_t)(j0 + jj + 1) * lw + c], a1);
-          }
-          rowi[c] = a0 + a1;
-        }
+      for (int jj = 0; jj < kCB8; ++jj) {
+        if (jj == lane) e -= f[jj];
+        else if (jj > lane && jj < nb) e = fma(-f[jj], W[(int64_t)(j0 + jj) * lw + c], e);
       }
-      // E entries inside the block: E_i[c] = -f_c - sum_{j > c in block} f_j E[j][c]
-      if (lane < nb) {
-        const int c = j0 + lane;
-        double e = 0.0;
-#pragma unroll
-        for (int jj = 0; jj < kCB8; ++jj) {
-          if (jj == lane) e -= f[jj];
-          else if (jj > lane && jj < nb) e = fma(-f[jj], W[(int64_t)(j0 + jj) * lw + c], e);
-        }
-        rowi[c] = e;
+      rowi[c] = e;
+    }
+  };
+  // Look-ahead: in block step J the first 8 warps update the NEXT block's rows
+  // first and go straight on to that block's phase 1 while warps 8-31 update
+  // the remaining trailing rows — phase 1 (a chain of 8 reciprocals) hides
+  // behind phase 2.
+  if (warp < min(kCB8, l)) phase1(0, min(kCB8, l), 0);
+  __syncthreads();
+  int buf = 0;
+  for (int j0 = 0; j0 < l; j0 += kCB8, buf ^= 1) {
+    const int nb = min(kCB8, l - j0);
+    const int n1 = j0 + nb;              // first trailing row = the next block's first row
+    const int nb1 = min(kCB8, l - n1);   // rows of the next block (<= 0: none)
+    if (warp < kCB8) {
+      if (warp < nb1) {
+        phase2_row(n1 + warp, j0, nb, buf);
+        asm volatile("bar.sync 1, %0;\n" ::"r"(32 * nb1) : "memory");
+        phase1(n1, nb1, buf ^ 1);
       }
+    } else {
+      for (int i = n1 + kCB8 + (warp - kCB8); i < l; i += kWarps - kCB8)
+        phase2_row(i, j0, nb, buf);
     }
     __syncthreads();
   }
