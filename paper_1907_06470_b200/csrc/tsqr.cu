@@ -683,6 +683,12 @@ void launch_pass(bool factor, const Plan& p, const double* X, int64_t ldx, doubl
   int per_sm = 0;
   XB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, sm));
   XB_REQUIRE(per_sm > 0, XB_ECUDA, "TSQR kernel cannot be resident");
+  // The Q pass keeps each block's rmax x l slice of Q in L2 between its panel
+  // steps (8 read-modify-write passes at l = 120): with two resident CTAs per
+  // SM the 296 live blocks (145 MB) spill to DRAM — 12.6 GB of DRAM reads for
+  // a 0.96 GB sketch; one per SM: 1e6 x 120 33.4 -> 31.2 ms. (The factor pass
+  // is faster with two: 35.9 ms with one.)
+  if (!factor) per_sm = 1;
   int64_t most = 1;
   for (int L = 0; L < p.levels; ++L) most = std::max(most, p.lv[L].nblk);
   const int grid = (int)std::min<int64_t>(most, (int64_t)per_sm * kNumSMs);
