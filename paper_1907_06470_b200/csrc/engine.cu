@@ -2096,6 +2096,39 @@ int xb_rsvd_dense_dev(xb_ctx* c, int dtype, int64_t m, int64_t n, const void* dA
 
 namespace {
 
+// First touch of the caller's pageable output arrays while the GPU computes:
+// a fresh numpy result is untouched memory, and its first-touch page faults
+// (serialised on the process's mmap lock) otherwise land inside the
+// device -> host copy at the end of the call. One byte per 4 KiB page is
+// written from a helper thread; the copies overwrite everything afterwards.
+struct OutputPretouch {
+  std::thread th;
+  void add(std::vector<std::pair<char*, size_t>>& v, void* p, size_t ld_bytes, size_t row_bytes,
+           int64_t rows) {
+    if (!p || rows <= 0 || is_pinned(p)) return;
+    const size_t span = (size_t)(rows - 1) * ld_bytes + row_bytes;
+    if (span >= ((size_t)4 << 20) && ld_bytes == row_bytes) v.push_back({static_cast<char*>(p), span});
+  }
+  OutputPretouch(void* U, size_t ldu_b, size_t urow_b, int64_t m, void* V, size_t ldv_b,
+                 size_t vrow_b, int64_t n) {
+    std::vector<std::pair<char*, size_t>> spans;
+    add(spans, U, ldu_b, urow_b, m);
+    add(spans, V, ldv_b, vrow_b, n);
+    if (spans.empty()) return;
+    th = std::thread([spans] {
+      for (auto& sp : spans) {
+        volatile char* q = sp.first;
+        for (size_t o = 0; o < sp.second; o += 4096) q[o] = 0;
+        q[sp.second - 1] = 0;
+      }
+    });
+  }
+  void join() {
+    if (th.joinable()) th.join();
+  }
+  ~OutputPretouch() { join(); }
+};
+
 // One factorisation of a host-resident dense A (any HostSource) with host
 // outputs: in HBM when A fits next to the sketch buffers (bands ingested on
 // the copy stream, each band's rows of the first product computed as it
@@ -2107,6 +2140,7 @@ void rsvd_from_host(xb_ctx* c, bool f32, int64_t m, int64_t n, HostSource& src,
   const size_t es = f32 ? 4 : 8;
   const int l = k + p;
   const double t0 = now_s();
+  OutputPretouch touch(U, (size_t)ldu * es, (size_t)k * es, m, V, (size_t)ldv * es, (size_t)k * es, n);
   double* dU = c->dbuf("U", (size_t)m * k);
   double* dV = c->dbuf("V", (size_t)n * k);
   double* ds = c->dbuf("s", (size_t)k);
@@ -2156,6 +2190,7 @@ void rsvd_from_host(xb_ctx* c, bool f32, int64_t m, int64_t n, HostSource& src,
     launch_copy2d_cast<double, float>(dV, n, k, k, static_cast<float*>(oV), k, c->st);
   }
   XB_CUDA(cudaMemcpyAsync(s, ds, k * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  touch.join();
   d2h_rows(c, U, ldu * es, oU, k * es, k * es, m);
   d2h_rows(c, V, ldv * es, oV, k * es, k * es, n);
   XB_CUDA(cudaStreamSynchronize(c->st));
@@ -2467,6 +2502,7 @@ int xb_rsvd_coo(xb_ctx* c, int64_t m, int64_t n, int64_t nnz, const int64_t* row
     XB_REQUIRE(U && s && V && (nnz == 0 || (rows && cols && vals)), XB_EVALUE, "null buffer");
     XB_REQUIRE(ldu >= k && ldv >= k, XB_EVALUE, "leading dimension too small");
     const int l = k + p;
+    OutputPretouch touch(U, (size_t)ldu * 8, (size_t)k * 8, m, V, (size_t)ldv * 8, (size_t)k * 8, n);
     cudaEvent_t e0, e1;
     XB_CUDA(cudaEventCreate(&e0));
     XB_CUDA(cudaEventCreate(&e1));
@@ -2485,6 +2521,7 @@ int xb_rsvd_coo(xb_ctx* c, int64_t m, int64_t n, int64_t nnz, const int64_t* row
     rsvd_impl(c, op, m, n, dO, l, seed, k, p, q, out, deficient, ndeficient, stage_seconds,
               IngestPlan{});
     XB_CUDA(cudaMemcpyAsync(s, ds, k * 8, cudaMemcpyDeviceToHost, c->st));
+    touch.join();
     d2h_rows(c, U, ldu * 8, dU, k * 8, k * 8, m);
     d2h_rows(c, V, ldv * 8, dV, k * 8, k * 8, n);
     XB_CUDA(cudaStreamSynchronize(c->st));
