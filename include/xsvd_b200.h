@@ -112,10 +112,13 @@ int xb_tc_peaks_data(xb_ctx* ctx, int random_data, double* i8_tops, double* bf16
  * Full factorization — replaces randomized_svd (pipeline.py:442-625) with
  * re-orthonormalisation after every product (north star).
  *   A      m x n, leading dim lda, dtype `dtype` (HOST memory; pinned memory
- *          is used in place, pageable memory is registered for the call)
+ *          is used in place, pageable memory is staged through a ring of
+ *          pinned slots filled by host worker threads)
  *   omega  optional n x (k+p) row-major host buffer of `dtype`; NULL means
  *          generate gaussian_band(seed, 0, n, k+p) on the device (rng.py:65)
- *   U      m x k (ldu >= k) `dtype`;  s  k doubles;  V  n x k (ldv >= k)
+ *   U      m x k (ldu >= k) `dtype`;  s  k doubles;  V  n x k (ldv >= k).
+ *          U and V must not overlap A or omega: the library may write to
+ *          them (first touch of their pages) before the factors are ready
  *   deficient  optional int32[k+p]; *ndeficient receives the count of
  *          columns flagged like thin_qr (kernels.py:327-331)
  *   stage_seconds optional double[XB_NUM_STAGES], device-timed
