@@ -1463,8 +1463,17 @@ void launch_jacobi_svd(const double* R, int64_t ldr, int l, int k, double* Ub, i
         nc_cache[nr == 4].store(nc);
       }
       cfg_for(nc, cfg, at);
-      XB_CUDA(cudaLaunchKernelEx(&cfg, kern, R, ldr, l, k, Ub, ldu, s, Wk, ldw, work, status, tol,
-                                 (int)kMaxSweeps));
+      cudaError_t le = cudaLaunchKernelEx(&cfg, kern, R, ldr, l, k, Ub, ldu, s, Wk, ldw, work,
+                                          status, tol, (int)kMaxSweeps);
+      if (le != cudaSuccess && nc == 16) {
+        // the 16-CTA cluster could not be placed after all: the portable size
+        cudaGetLastError();
+        nc_cache[nr == 4].store(8);
+        cfg_for(8, cfg, at);
+        le = cudaLaunchKernelEx(&cfg, kern, R, ldr, l, k, Ub, ldu, s, Wk, ldw, work, status, tol,
+                                (int)kMaxSweeps);
+      }
+      XB_CUDA(le);
     };
     if (l <= 64) launch(jacobi_cluster_kernel<2>, 2);
     else launch(jacobi_cluster_kernel<4>, 4);
